@@ -1,0 +1,185 @@
+/*
+ * cascade_b200.h -- C ABI of the B200-native EAM hot path (libcascade_b200.so).
+ *
+ * The drop-in boundary for the reference's force engine and step loop
+ * (cascademd, /root/reference/proj).  Plain pointers and sizes only; no
+ * torch or CUDA types.  Each entry point names the reference interface it
+ * replaces (paths relative to /root/reference/proj/core).
+ *
+ * Model: a context owns device-resident state (slot arrays over the
+ * ghost-inclusive lattice, the clash list, potential tables, offsets).  Host
+ * buffers are borrowed per call.  A context is not thread-safe (the
+ * reference's WorkerPool is not reentrant either, src/parallel.cpp:26-59).
+ * Errors: every call returns a cbx_status; the message (same text as the
+ * reference's exception) is read with cbx_last_error().  The C++ header
+ * cascade_b200.hpp rethrows them as the reference's exception types.
+ */
+#ifndef CASCADE_B200_H
+#define CASCADE_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CBX_API __attribute__((visibility("default")))
+#define CBX_ABI_VERSION 1
+
+typedef struct cbx_ctx cbx_ctx;
+
+/* status codes, mirroring the reference's exception classes */
+typedef enum {
+  CBX_OK = 0,
+  CBX_INVALID_ARGUMENT = 1, /* std::invalid_argument */
+  CBX_RUNTIME = 2,          /* std::runtime_error: overlap, parse, capacity */
+  CBX_DOMAIN = 3,           /* std::domain_error: hash outside the box */
+  CBX_LOGIC = 4,            /* std::logic_error: wrap did not converge */
+  CBX_CUDA = 5,             /* device / driver failure */
+  CBX_NCCL = 6              /* collective failure (multi-GPU) */
+} cbx_status;
+
+/* BoxSpec, include/cascademd/lattice.h:21-42 */
+typedef struct {
+  long box_x, box_y, box_z;
+  double a0;
+  long ghost_width;
+} cbx_box;
+
+/* SplineTable, include/cascademd/spline.h:16-27: nseg segments of 7 doubles
+ * {a,b,c,d,e,f,g} -- byte-compatible with std::vector<SplineTable::Seg> */
+typedef struct {
+  double x0, h;
+  long nseg;
+  const double* seg;
+} cbx_spline;
+
+/* EamPotential, include/cascademd/potential.h:33-60 */
+typedef struct {
+  int atomic_number;
+  double mass, lattice_const, cutoff;
+  cbx_spline embed, zr, dens;
+} cbx_potential;
+
+/* OffsetIndex, include/cascademd/neighbors.h:17-29 (flat signed site-id
+ * offsets, ascending).  The library rebuilds the lists from (box, cutoff)
+ * with the reference algorithm (src/neighbors.cpp:11-87) and rejects a
+ * caller index that differs. */
+typedef struct {
+  double cutoff;
+  long z_reach;
+  const int64_t *even_full, *odd_full, *even_half, *odd_half;
+  long n_even_full, n_odd_full, n_even_half, n_odd_half;
+} cbx_offsets;
+
+/* a LatticeStore view (include/cascademd/store.h:16-78): slot arrays by
+ * site id (n_slots = BoxSpec::slot_count()), xyz interleaved like Vec3; the
+ * clash map flattened in (key, bucket index) order.  NULL fields are skipped
+ * (upload: zero) . */
+typedef struct {
+  long n_slots;
+  double *pos, *vel, *force; /* [3*n_slots] */
+  double *rho, *df;          /* [n_slots] */
+  uint64_t* tag;
+  uint8_t *valid, *ghost;
+  long n_clash; /* upload: records given; download: capacity in, records out */
+  int64_t* clash_key;
+  int32_t* clash_idx;
+  double *clash_pos, *clash_vel, *clash_force, *clash_rho, *clash_df;
+  uint64_t* clash_tag;
+  uint8_t* clash_ghost;
+} cbx_store;
+
+/* StepState, include/cascademd/sim.h:11-21 */
+typedef struct {
+  long step;
+  double t, dt, kinetic, pair, embedding, max_speed;
+  uint64_t r_underflow, rho_clamp;
+} cbx_state;
+
+/* kernel selection for the two EAM stencil passes */
+typedef enum {
+  CBX_STENCIL_NEWTON3 = 0, /* half list, ordered reduction into owners (default) */
+  CBX_STENCIL_FULL = 1     /* full list, owner computes (no atomics, deterministic) */
+} cbx_stencil;
+
+/* ---- version / build ---------------------------------------------------- */
+CBX_API int cbx_abi_version(void);
+CBX_API const char* cbx_build_info(void);
+CBX_API const char* cbx_last_error(const cbx_ctx* ctx); /* ctx may be NULL */
+
+/* ---- host-side setup (no GPU needed) ------------------------------------- */
+/* parse_potential_file, src/potential.cpp:134-185 (+ build_spline,
+ * src/spline.cpp:14-77).  Returns an owned potential; free with
+ * cbx_potential_free. */
+CBX_API cbx_status cbx_potential_load(const char* path, cbx_potential** out);
+CBX_API void cbx_potential_free(cbx_potential* pot);
+/* build_offsets, src/neighbors.cpp:11-87.  Owned; free with cbx_offsets_free. */
+CBX_API cbx_status cbx_offsets_build(const cbx_box* box, double cutoff, cbx_offsets** out);
+CBX_API void cbx_offsets_free(cbx_offsets* idx);
+/* make_box + index cutoff, src/sim.cpp:62-84 */
+CBX_API cbx_status cbx_make_box(long box_x, long box_y, long box_z, double a0_cfg,
+                                long ghost_width_cfg, double max_disp,
+                                const cbx_potential* pot, cbx_box* out, double* index_cutoff);
+CBX_API double cbx_pka_speed(double energy_ev, double mass_amu); /* src/sim.cpp:88-92 */
+CBX_API double cbx_adaptive_dt(double max_speed, double dt_max, double max_disp); /* 94-98 */
+
+/* ---- context -------------------------------------------------------------- */
+/* Simulation's owned members (include/cascademd/sim.h:82-90) moved to the
+ * device.  idx may be NULL (built internally). */
+CBX_API cbx_status cbx_create(const cbx_box* box, const cbx_potential* pot,
+                              const cbx_offsets* idx, int device, cbx_ctx** out);
+CBX_API void cbx_destroy(cbx_ctx* ctx);
+CBX_API cbx_status cbx_set_stencil(cbx_ctx* ctx, cbx_stencil mode);
+CBX_API long cbx_slot_count(const cbx_ctx* ctx);
+
+/* ---- store transfer ------------------------------------------------------- */
+/* upload a LatticeStore; ghost slots/records are regenerated on the device
+ * exactly as LatticeStore::fill_ghosts (src/store.cpp:120-195) */
+CBX_API cbx_status cbx_upload_store(cbx_ctx* ctx, const cbx_store* s);
+CBX_API cbx_status cbx_download_store(cbx_ctx* ctx, cbx_store* s);
+CBX_API long cbx_clash_count(cbx_ctx* ctx);
+/* init_bcc (src/sim.cpp:100-130) on the host with the reference RNG, then
+ * upload + fill_ghosts; returns the atom count in *n_atoms */
+CBX_API cbx_status cbx_init_bcc(cbx_ctx* ctx, int species, double temperature, uint64_t seed,
+                                long* n_atoms);
+
+/* ---- LatticeStore operations on device state (src/store.cpp) -------------- */
+CBX_API cbx_status cbx_rehash(cbx_ctx* ctx); /* canonicalize_positions + update_hash + fill_ghosts */
+CBX_API cbx_status cbx_fill_ghosts(cbx_ctx* ctx);
+
+/* ---- force engine (include/cascademd/forces.h:42-67) ---------------------- */
+CBX_API cbx_status cbx_eval_forces(cbx_ctx* ctx, double* e_emb, double* e_pair); /* forces.cpp:414-447 */
+CBX_API cbx_status cbx_compute_density(cbx_ctx* ctx);                            /* 368-379 */
+CBX_API cbx_status cbx_compute_embedding_derivative(cbx_ctx* ctx, double* e_emb); /* 381-388 */
+CBX_API cbx_status cbx_compute_pair_forces(cbx_ctx* ctx, double* e_pair);         /* 390-402 */
+CBX_API cbx_status cbx_guards(cbx_ctx* ctx, uint64_t out[2]); /* GuardCounters, potential.h:13-28 */
+
+/* ---- Simulation (include/cascademd/sim.h:38-91) --------------------------- */
+/* velocity-Verlet steps with device-resident state (sim.cpp:248-273).
+ * dt > 0: fixed; dt <= 0: adaptive_dt per step from the previous max speed
+ * with (dt_max, max_disp) from cbx_set_adaptive.  One host sync per call. */
+CBX_API cbx_status cbx_step(cbx_ctx* ctx, double dt, long nsteps, cbx_state* out);
+CBX_API cbx_status cbx_set_adaptive(cbx_ctx* ctx, double dt_max, double max_disp);
+CBX_API cbx_status cbx_refresh_forces(cbx_ctx* ctx); /* sim.cpp:223-235 */
+CBX_API cbx_status cbx_measure(cbx_ctx* ctx);        /* sim.cpp:237-246 */
+CBX_API cbx_status cbx_get_state(cbx_ctx* ctx, cbx_state* out);
+CBX_API cbx_status cbx_set_state(cbx_ctx* ctx, const cbx_state* in);
+/* inject_pka (sim.cpp:163-186): overwrite the velocity of the slot atom at
+ * reference site id `site`, then measure */
+CBX_API cbx_status cbx_inject_pka(cbx_ctx* ctx, int64_t site, const double v[3]);
+CBX_API cbx_status cbx_count_defects(cbx_ctx* ctx, long out[3]); /* analysis.cpp:40-56 */
+
+/* ---- instrumentation ------------------------------------------------------ */
+/* per-launch device time (CUDA events on the context stream) of the last
+ * eval/step: {density, embed, force, clash, store} ms; and candidate / pair
+ * counters of the last density pass {candidates, pairs} */
+CBX_API cbx_status cbx_last_timings(cbx_ctx* ctx, double out_ms[8]);
+CBX_API cbx_status cbx_enable_timing(cbx_ctx* ctx, int on);
+CBX_API cbx_status cbx_count_pairs(cbx_ctx* ctx, uint64_t out[2]);
+CBX_API cbx_status cbx_kernel_launches(cbx_ctx* ctx, uint64_t* n); /* cumulative */
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,1053 @@
+// capi.cu -- the C ABI (include/cascade_b200.h): context lifetime, store
+// transfer, and the launch sequences of eval_forces and Simulation::step.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "cbx_device.cuh"
+#include "cbx_host.h"
+
+using namespace cbx;
+
+struct cbx_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  cbx_box box{};
+  Geo G{};
+  long long S = 0;
+  Potential pot;
+  Offsets offs;
+  bool cutoff_ok = true;
+  KP P{};
+  int mode = CBX_STENCIL_NEWTON3;
+  std::string err;
+  DevStatus hst{};
+  unsigned long long* d_defects = nullptr;
+  std::vector<void*> allocs;
+  cudaGraphExec_t step_graph = nullptr;
+  bool use_graph = true;
+  bool timing = false;
+  cudaEvent_t ev[8]{};
+  double t_ms[8]{};
+  uint64_t launches = 0;
+  int n_ghost = 0;
+
+  template <class T>
+  T* alloc(size_t n) {
+    void* p = nullptr;
+    if (cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T)) != cudaSuccess)
+      raise(CBX_CUDA, "cudaMalloc of " + std::to_string(n * sizeof(T)) + " bytes failed");
+    allocs.push_back(p);
+    return static_cast<T*>(p);
+  }
+};
+
+namespace {
+
+const char* kBuild = "cascade_b200 sm_100a fp64 EAM (abi " "1" ")";
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) raise(CBX_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <class F>
+cbx_status guarded(cbx_ctx* c, F&& f) {
+  try {
+    f();
+    if (c) c->err.clear();
+    return CBX_OK;
+  } catch (const Status& s) {
+    if (c) c->err = s.what();
+    set_thread_error(s.what());
+    return s.code;
+  } catch (const std::exception& e) {
+    if (c) c->err = e.what();
+    set_thread_error(e.what());
+    return CBX_RUNTIME;
+  }
+}
+
+void alloc_clash(cbx_ctx* c, Clash& A, int cap) {
+  A.key = c->alloc<long long>(cap);
+  A.gf = c->alloc<unsigned char>(cap);
+  A.src = c->alloc<int>(cap);
+  A.px = c->alloc<double>(cap);
+  A.py = c->alloc<double>(cap);
+  A.pz = c->alloc<double>(cap);
+  A.vx = c->alloc<double>(cap);
+  A.vy = c->alloc<double>(cap);
+  A.vz = c->alloc<double>(cap);
+  A.fx = c->alloc<double>(cap);
+  A.fy = c->alloc<double>(cap);
+  A.fz = c->alloc<double>(cap);
+  A.rho = c->alloc<double>(cap);
+  A.df = c->alloc<double>(cap);
+  A.e_emb = c->alloc<double>(cap);
+  A.e_pair = c->alloc<double>(cap);
+  A.v2 = c->alloc<double>(cap);
+  A.tag = c->alloc<unsigned long long>(cap);
+}
+
+Tab upload_tab(cbx_ctx* c, const Spline& s) {
+  Tab t{};
+  double* d = c->alloc<double>(s.seg.size());
+  cuda_check(cudaMemcpy(d, s.seg.data(), s.seg.size() * sizeof(double), cudaMemcpyHostToDevice),
+             "table upload");
+  t.seg = d;
+  t.x0 = s.x0;
+  t.h = s.h;
+  t.ih = 1.0 / s.h;
+  t.xl = s.x_last();
+  t.nseg = (int)s.nseg();
+  return t;
+}
+
+void sync_status(cbx_ctx* c) {
+  cuda_check(cudaMemcpyAsync(&c->hst, c->P.st, sizeof(DevStatus), cudaMemcpyDeviceToHost,
+                             c->stream),
+             "status readback");
+  cuda_check(cudaStreamSynchronize(c->stream), "stream synchronize");
+  cuda_check(cudaGetLastError(), "kernel launch");
+}
+
+// turn a device error into the reference's exception text; clears it
+void raise_device_error(cbx_ctx* c, bool in_step) {
+  DevStatus& h = c->hst;
+  if (!h.err && !h.n_ovl) return;
+  std::string msg;
+  cbx_status code;
+  if (h.err) {
+    code = (cbx_status)h.err;
+    if (h.err == CBX_DOMAIN) {
+      msg = "nearest_site: position (" + std::to_string(h.err_pos[0]) + ", " +
+            std::to_string(h.err_pos[1]) + ", " + std::to_string(h.err_pos[2]) +
+            ") outside the ghost-inclusive box volume";
+    } else if (h.err == CBX_LOGIC) {
+      msg = "canonicalize_positions: wrap did not converge";
+    } else if (h.err == CBX_INVALID_ARGUMENT) {
+      msg = "unsupported store state: a clash bucket over a vacant lattice site";
+    } else {
+      msg = "clash list capacity exceeded";
+    }
+  } else {
+    code = CBX_RUNTIME;
+    const int n = std::min(h.n_ovl, kMaxOverlapRecords);
+    int best = 0;
+    for (int i = 1; i < n; ++i)
+      if (h.ovl_key[i] < h.ovl_key[best]) best = i;
+    char buf[160];
+    std::snprintf(buf, sizeof buf, "atoms %llu and %llu overlap (separation %.3e A)",
+                  h.ovl_a[best], h.ovl_b[best], std::sqrt(h.ovl_r2[best]));
+    msg = buf;
+    if (in_step) {  // sim.cpp:226-231: ++step happened before refresh_forces threw
+      h.step += 1;
+      msg = "step " + std::to_string(h.step) + ": " + msg;
+    }
+  }
+  h.err = 0;
+  h.n_ovl = 0;
+  h.n_mov = 0;
+  cudaMemcpyAsync(c->P.st, &h, sizeof(DevStatus), cudaMemcpyHostToDevice, c->stream);
+  cudaStreamSynchronize(c->stream);
+  raise(code, msg);
+}
+
+void write_status(cbx_ctx* c) {
+  cuda_check(cudaMemcpyAsync(c->P.st, &c->hst, sizeof(DevStatus), cudaMemcpyHostToDevice,
+                             c->stream),
+             "status upload");
+}
+
+// ---- launch sequences ----------------------------------------------------
+void ev_mark(cbx_ctx* c, int i) {
+  if (c->timing) cudaEventRecord(c->ev[i], c->stream);
+}
+
+void seq_fill_ghosts(cbx_ctx* c) {
+  launch_ghost_fill(c->P, c->stream);
+  launch_clash_images(c->P, c->stream);
+  c->launches += 2;
+}
+void seq_density(cbx_ctx* c) {
+  if (c->mode == CBX_STENCIL_NEWTON3)
+    cudaMemsetAsync(c->P.rho, 0, c->S * sizeof(double), c->stream);
+  launch_clash_zero(c->P, 0, c->stream);
+  launch_density(c->P, c->mode, c->stream);
+  launch_clash_density(c->P, c->stream);
+  c->launches += 3;
+}
+void seq_embed(cbx_ctx* c) {
+  launch_embed(c->P, c->stream);
+  c->launches += 2;
+}
+void seq_force(cbx_ctx* c) {
+  if (c->mode == CBX_STENCIL_NEWTON3)
+    cudaMemsetAsync(c->P.frc, 0, 3 * c->S * sizeof(double), c->stream);
+  launch_clash_zero(c->P, 1, c->stream);
+  launch_force(c->P, c->mode, c->stream);
+  launch_clash_force(c->P, c->stream);
+  c->launches += 3;
+}
+// one velocity-Verlet step, sim.cpp:248-273
+void seq_step(cbx_ctx* c) {
+  ev_mark(c, 0);
+  launch_kick_drift(c->P, 1, c->stream);
+  launch_rehash(c->P, c->stream);
+  c->launches += 3;
+  seq_fill_ghosts(c);
+  ev_mark(c, 1);
+  seq_density(c);
+  ev_mark(c, 2);
+  seq_embed(c);
+  ev_mark(c, 3);
+  seq_force(c);
+  ev_mark(c, 4);
+  launch_kick2(c->P, 1, c->stream);
+  launch_finalize(c->P, 1, 1, c->stream);
+  c->launches += 3;
+  ev_mark(c, 5);
+}
+
+void accumulate_timing(cbx_ctx* c, bool step) {
+  if (!c->timing) return;
+  cudaEventSynchronize(c->ev[step ? 5 : 4]);
+  float ms = 0;
+  if (step) {
+    cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]);
+    c->t_ms[3] += ms;  // store: kick/drift/hash/rehash/ghosts
+    cudaEventElapsedTime(&ms, c->ev[4], c->ev[5]);
+    c->t_ms[4] += ms;  // kick2 + finalize
+    cudaEventElapsedTime(&ms, c->ev[0], c->ev[5]);
+    c->t_ms[5] += ms;
+    c->t_ms[6] += 1;
+  }
+  cudaEventElapsedTime(&ms, c->ev[1], c->ev[2]);
+  c->t_ms[0] += ms;
+  cudaEventElapsedTime(&ms, c->ev[2], c->ev[3]);
+  c->t_ms[1] += ms;
+  cudaEventElapsedTime(&ms, c->ev[3], c->ev[4]);
+  c->t_ms[2] += ms;
+}
+
+void build_graph(cbx_ctx* c) {
+  if (c->step_graph) return;
+  cudaGraph_t g;
+  const bool t = c->timing;
+  c->timing = false;
+  const uint64_t l0 = c->launches;
+  cuda_check(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal), "capture");
+  seq_step(c);
+  cuda_check(cudaStreamEndCapture(c->stream, &g), "end capture");
+  cuda_check(cudaGraphInstantiate(&c->step_graph, g, 0), "graph instantiate");
+  cudaGraphDestroy(g);
+  c->launches = l0;
+  c->timing = t;
+}
+
+void drop_graph(cbx_ctx* c) {
+  if (c->step_graph) cudaGraphExecDestroy(c->step_graph);
+  c->step_graph = nullptr;
+}
+
+// ---- the store view ------------------------------------------------------
+void do_upload(cbx_ctx* c, const cbx_store* s) {
+  const Geo& G = c->G;
+  const long long S = c->S;
+  if (s->n_slots != S)
+    raise(CBX_INVALID_ARGUMENT, "upload_store: n_slots " + std::to_string(s->n_slots) +
+                                    " does not match slot_count " + std::to_string(S));
+  std::vector<double4> pdf(S, make_double4(kVacant, kVacant, kVacant, 0.0));
+  std::vector<double> vel(3 * S, 0.0), frc(3 * S, 0.0), rho(S, 0.0);
+  std::vector<unsigned long long> tag(S, 0);
+  for (long long id = 0; id < S; ++id) {
+    const long long d = dev_of_ref(id, G.NC);
+    int cx, cy, cz;
+    cell_xyz(id >> 1, G, cx, cy, cz);
+    if (cell_is_ghost(cx, cy, cz, G)) continue;  // regenerated by fill_ghosts
+    const bool valid = s->valid ? s->valid[id] != 0 : true;
+    if (!valid) continue;
+    if (s->ghost && s->ghost[id]) continue;
+    pdf[d] = make_double4(s->pos[3 * id], s->pos[3 * id + 1], s->pos[3 * id + 2],
+                          s->df ? s->df[id] : 0.0);
+    for (int a = 0; a < 3; ++a) {
+      if (s->vel) vel[a * S + d] = s->vel[3 * id + a];
+      if (s->force) frc[a * S + d] = s->force[3 * id + a];
+    }
+    if (s->rho) rho[d] = s->rho[id];
+    if (s->tag) tag[d] = s->tag[id];
+  }
+  // interior clash records, in (key, index) order
+  std::vector<long long> key;
+  std::vector<double> cp, cv, cf, cr, cd;
+  std::vector<unsigned long long> ct;
+  for (long i = 0; i < s->n_clash; ++i) {
+    const long long k = s->clash_key[i];
+    if (k < 0 || k >= S) raise(CBX_INVALID_ARGUMENT, "upload_store: clash key out of range");
+    int cx, cy, cz;
+    cell_xyz(k >> 1, G, cx, cy, cz);
+    if (cell_is_ghost(cx, cy, cz, G) || (s->clash_ghost && s->clash_ghost[i])) continue;
+    if (!key.empty() && k < key.back())
+      raise(CBX_INVALID_ARGUMENT, "upload_store: clash records must be in key order");
+    if (pdf[dev_of_ref(k, G.NC)].x >= kVacantTest)
+      raise(CBX_INVALID_ARGUMENT,
+            "unsupported store state: a clash bucket over a vacant lattice site");
+    key.push_back(k);
+    for (int a = 0; a < 3; ++a) {
+      cp.push_back(s->clash_pos[3 * i + a]);
+      cv.push_back(s->clash_vel ? s->clash_vel[3 * i + a] : 0.0);
+      cf.push_back(s->clash_force ? s->clash_force[3 * i + a] : 0.0);
+    }
+    cr.push_back(s->clash_rho ? s->clash_rho[i] : 0.0);
+    cd.push_back(s->clash_df ? s->clash_df[i] : 0.0);
+    ct.push_back(s->clash_tag ? s->clash_tag[i] : 0);
+  }
+  const int nc = (int)key.size();
+  if (nc > c->P.cap_clash) raise(CBX_RUNTIME, "clash list capacity exceeded");
+  cudaStream_t st = c->stream;
+  cuda_check(cudaMemcpyAsync(c->P.pdf, pdf.data(), S * sizeof(double4), cudaMemcpyHostToDevice, st), "upload");
+  cuda_check(cudaMemcpyAsync(c->P.vel, vel.data(), 3 * S * sizeof(double), cudaMemcpyHostToDevice, st), "upload");
+  cuda_check(cudaMemcpyAsync(c->P.frc, frc.data(), 3 * S * sizeof(double), cudaMemcpyHostToDevice, st), "upload");
+  cuda_check(cudaMemcpyAsync(c->P.rho, rho.data(), S * sizeof(double), cudaMemcpyHostToDevice, st), "upload");
+  cuda_check(cudaMemcpyAsync(c->P.tag, tag.data(), S * sizeof(unsigned long long), cudaMemcpyHostToDevice, st), "upload");
+  // clash SoA
+  std::vector<double> tmp(nc);
+  std::vector<unsigned char> zeros(nc, 0);
+  std::vector<int> src(nc);
+  for (int i = 0; i < nc; ++i) src[i] = i;
+  const Clash& A = c->P.cl;
+  if (nc) {
+    cudaMemcpyAsync(A.key, key.data(), nc * sizeof(long long), cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(A.gf, zeros.data(), nc, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(A.src, src.data(), nc * sizeof(int), cudaMemcpyHostToDevice, st);
+    double* dst3[3][3] = {{A.px, A.py, A.pz}, {A.vx, A.vy, A.vz}, {A.fx, A.fy, A.fz}};
+    const std::vector<double>* src3[3] = {&cp, &cv, &cf};
+    for (int f = 0; f < 3; ++f)
+      for (int a = 0; a < 3; ++a) {
+        std::vector<double> col(nc);
+        for (int i = 0; i < nc; ++i) col[i] = (*src3[f])[3 * i + a];
+        cudaMemcpyAsync(dst3[f][a], col.data(), nc * sizeof(double), cudaMemcpyHostToDevice, st);
+        cudaStreamSynchronize(st);
+      }
+    cudaMemcpyAsync(A.rho, cr.data(), nc * sizeof(double), cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(A.df, cd.data(), nc * sizeof(double), cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(A.tag, ct.data(), nc * sizeof(unsigned long long), cudaMemcpyHostToDevice, st);
+    cudaMemsetAsync(A.e_emb, 0, nc * sizeof(double), st);
+    cudaMemsetAsync(A.e_pair, 0, nc * sizeof(double), st);
+    cudaMemsetAsync(A.v2, 0, nc * sizeof(double), st);
+  }
+  // reset the head map and the list counters
+  cudaMemsetAsync(c->P.head, 0xff, S * sizeof(int), st);
+  sync_status(c);
+  c->hst.n_clash = nc;
+  c->hst.n_mov = 0;
+  c->hst.err = 0;
+  c->hst.n_ovl = 0;
+  write_status(c);
+  seq_fill_ghosts(c);
+  sync_status(c);
+  raise_device_error(c, false);
+}
+
+template <class T>
+std::vector<T> fetch(cbx_ctx* c, const T* d, size_t n) {
+  std::vector<T> h(n);
+  if (n)
+    cuda_check(cudaMemcpyAsync(h.data(), d, n * sizeof(T), cudaMemcpyDeviceToHost, c->stream),
+               "download");
+  return h;
+}
+
+void do_download(cbx_ctx* c, cbx_store* s) {
+  const Geo& G = c->G;
+  const long long S = c->S;
+  if (s->n_slots != S) raise(CBX_INVALID_ARGUMENT, "download_store: n_slots mismatch");
+  auto pdf = fetch(c, c->P.pdf, S);
+  auto vel = fetch(c, c->P.vel, 3 * S);
+  auto frc = fetch(c, c->P.frc, 3 * S);
+  auto rho = fetch(c, c->P.rho, S);
+  auto tag = fetch(c, c->P.tag, S);
+  auto tgt = fetch(c, c->P.tgt, S);
+  sync_status(c);
+  for (long long id = 0; id < S; ++id) {
+    const long long d = dev_of_ref(id, G.NC);
+    const long long t = tgt[d];
+    const bool valid = pdf[d].x < kVacantTest;
+    const bool ghost = t != d;
+    if (s->valid) s->valid[id] = valid;
+    if (s->ghost) s->ghost[id] = valid && ghost;
+    if (s->pos) {
+      s->pos[3 * id] = pdf[d].x;
+      s->pos[3 * id + 1] = pdf[d].y;
+      s->pos[3 * id + 2] = pdf[d].z;
+    }
+    if (s->df) s->df[id] = pdf[d].w;
+    for (int a = 0; a < 3; ++a) {
+      if (s->vel) s->vel[3 * id + a] = vel[a * S + t];
+      if (s->force) s->force[3 * id + a] = ghost ? 0.0 : frc[a * S + d];
+    }
+    if (s->rho) s->rho[id] = rho[t];
+    if (s->tag) s->tag[id] = tag[t];
+  }
+  const int nc = c->hst.n_clash;
+  if (s->clash_key == nullptr) {
+    s->n_clash = nc;
+    return;
+  }
+  if (s->n_clash < nc) raise(CBX_INVALID_ARGUMENT, "download_store: clash capacity too small");
+  s->n_clash = nc;
+  const Clash& A = c->P.cl;
+  auto key = fetch(c, A.key, nc);
+  auto gf = fetch(c, A.gf, nc);
+  auto src = fetch(c, A.src, nc);
+  auto px = fetch(c, A.px, nc), py = fetch(c, A.py, nc), pz = fetch(c, A.pz, nc);
+  auto vx = fetch(c, A.vx, nc), vy = fetch(c, A.vy, nc), vz = fetch(c, A.vz, nc);
+  auto fx = fetch(c, A.fx, nc), fy = fetch(c, A.fy, nc), fz = fetch(c, A.fz, nc);
+  auto rr = fetch(c, A.rho, nc), dd = fetch(c, A.df, nc);
+  auto tt = fetch(c, A.tag, nc);
+  cuda_check(cudaStreamSynchronize(c->stream), "download");
+  int idx = 0;
+  for (int i = 0; i < nc; ++i) {
+    idx = (i > 0 && key[i - 1] == key[i]) ? idx + 1 : 0;
+    s->clash_key[i] = key[i];
+    if (s->clash_idx) s->clash_idx[i] = idx;
+    if (s->clash_ghost) s->clash_ghost[i] = gf[i];
+    if (s->clash_pos) {
+      s->clash_pos[3 * i] = px[i];
+      s->clash_pos[3 * i + 1] = py[i];
+      s->clash_pos[3 * i + 2] = pz[i];
+    }
+    if (s->clash_vel) {
+      s->clash_vel[3 * i] = vx[i];
+      s->clash_vel[3 * i + 1] = vy[i];
+      s->clash_vel[3 * i + 2] = vz[i];
+    }
+    if (s->clash_force) {
+      s->clash_force[3 * i] = gf[i] ? 0.0 : fx[i];
+      s->clash_force[3 * i + 1] = gf[i] ? 0.0 : fy[i];
+      s->clash_force[3 * i + 2] = gf[i] ? 0.0 : fz[i];
+    }
+    if (s->clash_rho) s->clash_rho[i] = rr[gf[i] ? src[i] : i];
+    if (s->clash_df) s->clash_df[i] = dd[i];
+    if (s->clash_tag) s->clash_tag[i] = tt[i];
+  }
+}
+
+void check_cutoff(cbx_ctx* c) {
+  if (!c->cutoff_ok)
+    raise(CBX_INVALID_ARGUMENT, "offset index cutoff is smaller than the potential cutoff");
+}
+
+}  // namespace
+
+// ===========================================================================
+extern "C" {
+
+CBX_API int cbx_abi_version(void) { return CBX_ABI_VERSION; }
+CBX_API const char* cbx_build_info(void) { return kBuild; }
+CBX_API const char* cbx_last_error(const cbx_ctx* c) {
+  return c ? c->err.c_str() : thread_error();
+}
+
+CBX_API cbx_status cbx_potential_load(const char* path, cbx_potential** out) {
+  return guarded(nullptr, [&] {
+    auto* p = new Potential(parse_potential(path));
+    auto* o = new cbx_potential{};
+    o->atomic_number = p->atomic_number;
+    o->mass = p->mass;
+    o->lattice_const = p->lattice_const;
+    o->cutoff = p->cutoff;
+    auto fill = [](cbx_spline& d, const Spline& s) {
+      d.x0 = s.x0;
+      d.h = s.h;
+      d.nseg = s.nseg();
+      d.seg = s.seg.data();
+    };
+    fill(o->embed, p->embed);
+    fill(o->zr, p->zr);
+    fill(o->dens, p->dens);
+    // the owning Potential rides behind the public struct
+    struct Owned {
+      cbx_potential pub;
+      Potential* own;
+    };
+    auto* w = new Owned{*o, p};
+    delete o;
+    *out = &w->pub;
+  });
+}
+CBX_API void cbx_potential_free(cbx_potential* pot) {
+  if (!pot) return;
+  struct Owned {
+    cbx_potential pub;
+    Potential* own;
+  };
+  auto* w = reinterpret_cast<Owned*>(pot);
+  delete w->own;
+  delete w;
+}
+
+CBX_API cbx_status cbx_offsets_build(const cbx_box* box, double cutoff, cbx_offsets** out) {
+  return guarded(nullptr, [&] {
+    Offsets o = build_offsets(*box, cutoff);
+    struct Owned {
+      cbx_offsets pub;
+      std::vector<int64_t> l[4];
+    };
+    auto* w = new Owned{};
+    for (int par = 0; par < 2; ++par) {
+      for (const Offset& f : o.full[par]) w->l[par].push_back(f.flat);
+      for (const Offset& f : o.half[par]) w->l[2 + par].push_back(f.flat);
+    }
+    w->pub.cutoff = o.cutoff;
+    w->pub.z_reach = o.z_reach;
+    w->pub.even_full = w->l[0].data();
+    w->pub.odd_full = w->l[1].data();
+    w->pub.even_half = w->l[2].data();
+    w->pub.odd_half = w->l[3].data();
+    w->pub.n_even_full = (long)w->l[0].size();
+    w->pub.n_odd_full = (long)w->l[1].size();
+    w->pub.n_even_half = (long)w->l[2].size();
+    w->pub.n_odd_half = (long)w->l[3].size();
+    *out = &w->pub;
+  });
+}
+CBX_API void cbx_offsets_free(cbx_offsets* idx) {
+  struct Owned {
+    cbx_offsets pub;
+    std::vector<int64_t> l[4];
+  };
+  delete reinterpret_cast<Owned*>(idx);
+}
+
+CBX_API cbx_status cbx_make_box(long bx, long by, long bz, double a0_cfg, long gw_cfg,
+                                double max_disp, const cbx_potential* pot, cbx_box* out,
+                                double* index_cutoff) {
+  return guarded(nullptr, [&] {
+    if (bx <= 0 || by <= 0 || bz <= 0)
+      raise(CBX_INVALID_ARGUMENT, "box: dimensions must be positive");
+    const double a0 = a0_cfg > 0.0 ? a0_cfg : pot->lattice_const;
+    if (!(a0 > 0.0))
+      raise(CBX_INVALID_ARGUMENT,
+            "box.a0: the potential file carries no usable lattice constant");
+    if (max_disp >= a0 / 2.0)
+      raise(CBX_INVALID_ARGUMENT, "max_disp: must stay below half the lattice constant");
+    const double ic = pot->cutoff + 0.3 * a0;
+    const long gw = gw_cfg > 0 ? gw_cfg : (long)std::ceil(ic / a0);
+    *out = cbx_box{bx, by, bz, a0, gw};
+    if (index_cutoff) *index_cutoff = pot->cutoff + 0.3 * a0;
+  });
+}
+
+CBX_API double cbx_pka_speed(double e, double m) {
+  return std::sqrt(2.0 * e / m) * speed_factor();
+}
+CBX_API double cbx_adaptive_dt(double vmax, double dt_max, double max_disp) {
+  double dt = dt_max;
+  if (vmax > 0.0) dt = std::min(dt, max_disp / vmax);
+  return std::max(dt, 1e-7);
+}
+
+CBX_API cbx_status cbx_create(const cbx_box* box, const cbx_potential* pot,
+                              const cbx_offsets* idx, int device, cbx_ctx** out) {
+  auto c = std::make_unique<cbx_ctx>();
+  const cbx_status rc = guarded(nullptr, [&] {
+    if (box->box_x <= 0 || box->box_y <= 0 || box->box_z <= 0 || !(box->a0 > 0.0) ||
+        box->ghost_width < 0)
+      raise(CBX_INVALID_ARGUMENT, "LatticeStore: box dimensions must be positive");
+    int ndev = 0;
+    cuda_check(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
+    if (device < 0 || device >= ndev) raise(CBX_CUDA, "no such CUDA device");
+    c->device = device;
+    cuda_check(cudaSetDevice(device), "cudaSetDevice");
+    cuda_check(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "stream");
+    for (auto& e : c->ev) cudaEventCreate(&e);
+    c->box = *box;
+    c->G = make_geo(*box);
+    const Geo& G = c->G;
+    c->S = 2 * G.NC;
+    if (c->S >= (1ll << 31)) raise(CBX_INVALID_ARGUMENT, "box too large for one device (2^31 sites)");
+    // host copy of the potential tables
+    c->pot.atomic_number = pot->atomic_number;
+    c->pot.mass = pot->mass;
+    c->pot.lattice_const = pot->lattice_const;
+    c->pot.cutoff = pot->cutoff;
+    auto cp = [](Spline& d, const cbx_spline& s) {
+      d.x0 = s.x0;
+      d.h = s.h;
+      d.seg.assign(s.seg, s.seg + 7 * s.nseg);
+    };
+    cp(c->pot.embed, pot->embed);
+    cp(c->pot.zr, pot->zr);
+    cp(c->pot.dens, pot->dens);
+    // offsets: rebuilt with the reference algorithm, the caller's must agree
+    const double ic = idx ? idx->cutoff : pot->cutoff + 0.3 * box->a0;
+    c->offs = build_offsets(*box, ic);
+    if (idx) {
+      auto same = [](const std::vector<Offset>& a, const int64_t* b, long n) {
+        if ((long)a.size() != n) return false;
+        for (long i = 0; i < n; ++i)
+          if (a[i].flat != b[i]) return false;
+        return true;
+      };
+      if (!same(c->offs.full[0], idx->even_full, idx->n_even_full) ||
+          !same(c->offs.full[1], idx->odd_full, idx->n_odd_full) ||
+          !same(c->offs.half[0], idx->even_half, idx->n_even_half) ||
+          !same(c->offs.half[1], idx->odd_half, idx->n_odd_half))
+        raise(CBX_INVALID_ARGUMENT, "offset index does not match build_offsets(box, cutoff)");
+    }
+    c->cutoff_ok = !(c->offs.cutoff < pot->cutoff);
+    for (int par = 0; par < 2; ++par)
+      if ((int)c->offs.full[par].size() > kMaxOffsets)
+        raise(CBX_INVALID_ARGUMENT, "offset index too large for the device tables");
+    // device offset deltas
+    std::vector<int> hd[2], fd[2];
+    std::vector<long long> ff[2];
+    for (int par = 0; par < 2; ++par) {
+      auto delta = [&](const Offset& o) {
+        const int q = par ^ o.cross;
+        return (int)((long long)(q - par) * G.NC + (long long)o.dz * G.txy +
+                     (long long)o.dy * G.tx + o.dx);
+      };
+      for (const Offset& o : c->offs.half[par]) hd[par].push_back(delta(o));
+      for (const Offset& o : c->offs.full[par]) {
+        fd[par].push_back(delta(o));
+        ff[par].push_back(o.flat);
+      }
+    }
+    const int* hp[2] = {hd[0].data(), hd[1].data()};
+    const int* fp[2] = {fd[0].data(), fd[1].data()};
+    const long long* fl[2] = {ff[0].data(), ff[1].data()};
+    const int hn[2] = {(int)hd[0].size(), (int)hd[1].size()};
+    const int fn[2] = {(int)fd[0].size(), (int)fd[1].size()};
+    upload_offsets(hp, hn, fp, fn, fl, c->stream);
+    cuda_check(cudaStreamSynchronize(c->stream), "offset upload");
+    // ghost list and owner map
+    const long long S = c->S;
+    std::vector<int> tgt(S), gdst, gsrc;
+    std::vector<signed char> gk;
+    for (long long cell = 0; cell < G.NC; ++cell) {
+      int cx, cy, cz;
+      cell_xyz(cell, G, cx, cy, cz);
+      const bool ghost = cell_is_ghost(cx, cy, cz, G);
+      const long kx = floor_div(cx - G.g, G.bx), ky = floor_div(cy - G.g, G.by),
+                 kz = floor_div(cz - G.g, G.bz);
+      const long long scell = cell_of((int)(cx - kx * G.bx), (int)(cy - ky * G.by),
+                                      (int)(cz - kz * G.bz), G);
+      for (int par = 0; par < 2; ++par) {
+        const long long d = par * G.NC + cell;
+        if (!ghost) {
+          tgt[d] = (int)d;
+          continue;
+        }
+        const long long s = par * G.NC + scell;
+        tgt[d] = (int)s;
+        gdst.push_back((int)d);
+        gsrc.push_back((int)s);
+        gk.push_back((signed char)kx);
+        gk.push_back((signed char)ky);
+        gk.push_back((signed char)kz);
+      }
+    }
+    KP& P = c->P;
+    P.G = G;
+    P.S = S;
+    P.accel = accel_factor();
+    P.mv2 = mv2_to_ev();
+    P.pdf = c->alloc<double4>(S);
+    P.rho = c->alloc<double>(S);
+    P.vel = c->alloc<double>(3 * S);
+    P.frc = c->alloc<double>(3 * S);
+    P.tag = c->alloc<unsigned long long>(S);
+    P.tgt = c->alloc<int>(S);
+    P.head = c->alloc<int>(S);
+    P.n_gh = (long long)gdst.size();
+    c->n_ghost = (int)gdst.size();
+    P.gh_dst = c->alloc<int>(gdst.size());
+    P.gh_src = c->alloc<int>(gsrc.size());
+    P.gh_k = c->alloc<signed char>(gk.size());
+    cuda_check(cudaMemcpy(P.tgt, tgt.data(), S * sizeof(int), cudaMemcpyHostToDevice), "tgt");
+    if (!gdst.empty()) {
+      cudaMemcpy(P.gh_dst, gdst.data(), gdst.size() * sizeof(int), cudaMemcpyHostToDevice);
+      cudaMemcpy(P.gh_src, gsrc.data(), gsrc.size() * sizeof(int), cudaMemcpyHostToDevice);
+      cudaMemcpy(P.gh_k, gk.data(), gk.size(), cudaMemcpyHostToDevice);
+    }
+    // clash list, movers, sort scratch
+    const char* env = std::getenv("CBX_CLASH_CAPACITY");
+    int cap = env ? std::atoi(env) : (int)std::max<long long>(1 << 14, S / 64);
+    cap = std::min(cap, 1 << 22);
+    P.cap_clash = cap;
+    P.cap_mov = cap;
+    int items = 1;
+    while (items < 2 * cap) items <<= 1;
+    P.cap_items = items;
+    alloc_clash(c.get(), P.cl, cap);
+    alloc_clash(c.get(), P.cl2, cap);
+    P.mv.key = c->alloc<long long>(cap);
+    P.mv.old = c->alloc<long long>(cap);
+    P.mv.px = c->alloc<double>(cap);
+    P.mv.py = c->alloc<double>(cap);
+    P.mv.pz = c->alloc<double>(cap);
+    P.mv.vx = c->alloc<double>(cap);
+    P.mv.vy = c->alloc<double>(cap);
+    P.mv.vz = c->alloc<double>(cap);
+    P.mv.tag = c->alloc<unsigned long long>(cap);
+    P.sc.k1 = c->alloc<long long>(items);
+    P.sc.k2 = c->alloc<long long>(items);
+    P.sc.k3 = c->alloc<long long>(items);
+    P.sc.pl = c->alloc<int>(items);
+    P.sc.flag = c->alloc<int>(items);
+    P.sc.pos = c->alloc<int>(items);
+    // tables and partials
+    P.dens = upload_tab(c.get(), c->pot.dens);
+    P.zr = upload_tab(c.get(), c->pot.zr);
+    P.emb = upload_tab(c.get(), c->pot.embed);
+    P.cutoff = pot->cutoff;
+    P.cut2 = pot->cutoff * pot->cutoff;
+    P.mass = pot->mass;
+    const int np = std::max(eam_blocks(P), embed_blocks(P));
+    P.n_part = np;
+    P.part_emb = c->alloc<double>(np);
+    P.part_pair = c->alloc<double>(np);
+    P.part_ke = c->alloc<double>(np);
+    P.part_vmax = c->alloc<double>(np);
+    cudaMemset(P.part_emb, 0, np * sizeof(double));
+    cudaMemset(P.part_pair, 0, np * sizeof(double));
+    cudaMemset(P.part_ke, 0, np * sizeof(double));
+    cudaMemset(P.part_vmax, 0, np * sizeof(double));
+    P.st = c->alloc<DevStatus>(1);
+    c->d_defects = c->alloc<unsigned long long>(4);
+    // empty store: every slot vacant
+    std::vector<double4> vac(S, make_double4(kVacant, kVacant, kVacant, 0.0));
+    cuda_check(cudaMemcpy(P.pdf, vac.data(), S * sizeof(double4), cudaMemcpyHostToDevice), "init");
+    cudaMemset(P.rho, 0, S * sizeof(double));
+    cudaMemset(P.vel, 0, 3 * S * sizeof(double));
+    cudaMemset(P.frc, 0, 3 * S * sizeof(double));
+    cudaMemset(P.tag, 0, S * sizeof(unsigned long long));
+    cudaMemset(P.head, 0xff, S * sizeof(int));
+    c->hst = DevStatus{};
+    c->hst.dt_next = 1e-3;
+    c->hst.dt_max = 1e-3;
+    c->hst.max_disp = 0.05;
+    cuda_check(cudaMemcpy(P.st, &c->hst, sizeof(DevStatus), cudaMemcpyHostToDevice), "status");
+    cuda_check(cudaDeviceSynchronize(), "create");
+  });
+  if (rc == CBX_OK) *out = c.release();
+  else {
+    for (void* p : c->allocs) cudaFree(p);
+  }
+  return rc;
+}
+
+CBX_API void cbx_destroy(cbx_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  drop_graph(c);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  for (void* p : c->allocs) cudaFree(p);
+  for (auto& e : c->ev)
+    if (e) cudaEventDestroy(e);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+CBX_API cbx_status cbx_set_stencil(cbx_ctx* c, cbx_stencil mode) {
+  return guarded(c, [&] {
+    if (mode != CBX_STENCIL_NEWTON3 && mode != CBX_STENCIL_FULL)
+      raise(CBX_INVALID_ARGUMENT, "unknown stencil mode");
+    if (c->mode != mode) drop_graph(c);
+    c->mode = mode;
+  });
+}
+
+CBX_API long cbx_slot_count(const cbx_ctx* c) { return (long)c->S; }
+
+CBX_API cbx_status cbx_upload_store(cbx_ctx* c, const cbx_store* s) {
+  return guarded(c, [&] {
+    cudaSetDevice(c->device);
+    do_upload(c, s);
+  });
+}
+CBX_API cbx_status cbx_download_store(cbx_ctx* c, cbx_store* s) {
+  return guarded(c, [&] {
+    cudaSetDevice(c->device);
+    do_download(c, s);
+  });
+}
+CBX_API long cbx_clash_count(cbx_ctx* c) {
+  cudaSetDevice(c->device);
+  sync_status(c);
+  return c->hst.n_clash;
+}
+
+CBX_API cbx_status cbx_init_bcc(cbx_ctx* c, int species, double temperature, uint64_t seed,
+                                long* n_atoms) {
+  (void)species;
+  return guarded(c, [&] {
+    cudaSetDevice(c->device);
+    HostLattice L = init_bcc(c->box, c->pot.mass, temperature, seed);
+    cbx_store s{};
+    s.n_slots = c->S;
+    s.pos = L.pos.data();
+    s.vel = L.vel.data();
+    s.tag = L.tag.data();
+    s.valid = L.valid.data();
+    do_upload(c, &s);
+    if (n_atoms) *n_atoms = L.n_atoms;
+  });
+}
+
+CBX_API cbx_status cbx_rehash(cbx_ctx* c) {
+  return guarded(c, [&] {
+    cudaSetDevice(c->device);
+    launch_kick_drift(c->P, 0, c->stream);
+    launch_rehash(c->P, c->stream);
+    c->launches += 3;
+    seq_fill_ghosts(c);
+    sync_status(c);
+    raise_device_error(c, false);
+  });
+}
+CBX_API cbx_status cbx_fill_ghosts(cbx_ctx* c) {
+  return guarded(c, [&] {
+    cudaSetDevice(c->device);
+    seq_fill_ghosts(c);
+    sync_status(c);
+    raise_device_error(c, false);
+  });
+}
+
+CBX_API cbx_status cbx_eval_forces(cbx_ctx* c, double* e_emb, double* e_pair) {
+  return guarded(c, [&] {
+    cudaSetDevice(c->device);
+    check_cutoff(c);
+    ev_mark(c, 1);
+    seq_density(c);
+    ev_mark(c, 2);
+    seq_embed(c);
+    ev_mark(c, 3);
+    seq_force(c);
+    ev_mark(c, 4);
+    launch_finalize(c->P, -1, 1, c->stream);
+    c->launches += 1;
+    sync_status(c);
+    accumulate_timing(c, false);
+    raise_device_error(c, false);
+    if (e_emb) *e_emb = c->hst.embedding;
+    if (e_pair) *e_pair = c->hst.pair;
+  });
+}
+CBX_API cbx_status cbx_compute_density(cbx_ctx* c) {
+  return guarded(c, [&] {
+    cudaSetDevice(c->device);
+    check_cutoff(c);
+    seq_density(c);
+    sync_status(c);
+    raise_device_error(c, false);
+  });
+}
+CBX_API cbx_status cbx_compute_embedding_derivative(cbx_ctx* c, double* e_emb) {
+  return guarded(c, [&] {
+    cudaSetDevice(c->device);
+    seq_embed(c);
+    launch_finalize(c->P, -1, 1, c->stream);
+    c->launches += 1;
+    sync_status(c);
+    raise_device_error(c, false);
+    if (e_emb) *e_emb = c->hst.embedding;
+  });
+}
+CBX_API cbx_status cbx_compute_pair_forces(cbx_ctx* c, double* e_pair) {
+  return guarded(c, [&] {
+    cudaSetDevice(c->device);
+    check_cutoff(c);
+    seq_force(c);
+    launch_finalize(c->P, -1, 1, c->stream);
+    c->launches += 1;
+    sync_status(c);
+    raise_device_error(c, false);
+    if (e_pair) *e_pair = c->hst.pair;
+  });
+}
+CBX_API cbx_status cbx_guards(cbx_ctx* c, uint64_t out[2]) {
+  return guarded(c, [&] {
+    cudaSetDevice(c->device);
+    sync_status(c);
+    out[0] = c->hst.r_underflow;
+    out[1] = c->hst.rho_clamp;
+  });
+}
+
+CBX_API cbx_status cbx_set_adaptive(cbx_ctx* c, double dt_max, double max_disp) {
+  return guarded(c, [&] {
+    sync_status(c);
+    c->hst.dt_max = dt_max;
+    c->hst.max_disp = max_disp;
+    write_status(c);
+  });
+}
+
+CBX_API cbx_status cbx_step(cbx_ctx* c, double dt, long nsteps, cbx_state* out) {
+  return guarded(c, [&] {
+    cudaSetDevice(c->device);
+    check_cutoff(c);
+    if (nsteps < 0) raise(CBX_INVALID_ARGUMENT, "nsteps must be >= 0");
+    sync_status(c);
+    if (dt > 0.0) {
+      c->hst.dt_next = dt;
+      c->hst.adaptive = 0;
+    } else {
+      c->hst.adaptive = 1;
+      c->hst.dt_next = cbx_adaptive_dt(c->hst.max_speed, c->hst.dt_max, c->hst.max_disp);
+    }
+    write_status(c);
+    if (c->use_graph && !c->timing) build_graph(c);
+    for (long i = 0; i < nsteps; ++i) {
+      if (c->use_graph && !c->timing) {
+        cuda_check(cudaGraphLaunch(c->step_graph, c->stream), "graph launch");
+        c->launches += 16;
+      } else {
+        seq_step(c);
+        accumulate_timing(c, true);
+      }
+    }
+    sync_status(c);
+    raise_device_error(c, true);
+    if (out) {
+      out->step = (long)c->hst.step;
+      out->t = c->hst.t;
+      out->dt = c->hst.dt;
+      out->kinetic = c->hst.kinetic;
+      out->pair = c->hst.pair;
+      out->embedding = c->hst.embedding;
+      out->max_speed = c->hst.max_speed;
+      out->r_underflow = c->hst.r_underflow;
+      out->rho_clamp = c->hst.rho_clamp;
+    }
+  });
+}
+
+CBX_API cbx_status cbx_refresh_forces(cbx_ctx* c) {
+  return cbx_eval_forces(c, nullptr, nullptr);
+}
+
+CBX_API cbx_status cbx_measure(cbx_ctx* c) {
+  return guarded(c, [&] {
+    cudaSetDevice(c->device);
+    launch_kick2(c->P, 0, c->stream);
+    launch_finalize(c->P, 0, 0, c->stream);
+    c->launches += 3;
+    sync_status(c);
+    raise_device_error(c, false);
+  });
+}
+
+CBX_API cbx_status cbx_get_state(cbx_ctx* c, cbx_state* out) {
+  return guarded(c, [&] {
+    cudaSetDevice(c->device);
+    sync_status(c);
+    out->step = (long)c->hst.step;
+    out->t = c->hst.t;
+    out->dt = c->hst.dt;
+    out->kinetic = c->hst.kinetic;
+    out->pair = c->hst.pair;
+    out->embedding = c->hst.embedding;
+    out->max_speed = c->hst.max_speed;
+    out->r_underflow = c->hst.r_underflow;
+    out->rho_clamp = c->hst.rho_clamp;
+  });
+}
+CBX_API cbx_status cbx_set_state(cbx_ctx* c, const cbx_state* in) {
+  return guarded(c, [&] {
+    cudaSetDevice(c->device);
+    sync_status(c);
+    c->hst.step = in->step;
+    c->hst.t = in->t;
+    c->hst.dt = in->dt;
+    c->hst.kinetic = in->kinetic;
+    c->hst.pair = in->pair;
+    c->hst.embedding = in->embedding;
+    c->hst.max_speed = in->max_speed;
+    c->hst.r_underflow = in->r_underflow;
+    c->hst.rho_clamp = in->rho_clamp;
+    write_status(c);
+  });
+}
+
+CBX_API cbx_status cbx_inject_pka(cbx_ctx* c, int64_t site, const double v[3]) {
+  const cbx_status rc = guarded(c, [&] {
+    cudaSetDevice(c->device);
+    if (site < 0 || site >= c->S) raise(CBX_INVALID_ARGUMENT, "pka.site: site id out of range");
+    const long long d = dev_of_ref(site, c->G.NC);
+    double4 p;
+    cuda_check(cudaMemcpy(&p, c->P.pdf + d, sizeof p, cudaMemcpyDeviceToHost), "pka");
+    if (p.x >= kVacantTest) {
+      int cx, cy, cz;
+      cell_xyz(site >> 1, c->G, cx, cy, cz);
+      raise(CBX_INVALID_ARGUMENT, "pka.site: no atom at cell (" + std::to_string(cx - c->G.g) +
+                                      "," + std::to_string(cy - c->G.g) + "," +
+                                      std::to_string(cz - c->G.g) + ")");
+    }
+    for (int a = 0; a < 3; ++a)
+      cuda_check(cudaMemcpy(c->P.vel + a * c->S + d, &v[a], sizeof(double),
+                            cudaMemcpyHostToDevice),
+                 "pka");
+  });
+  return rc == CBX_OK ? cbx_measure(c) : rc;
+}
+
+CBX_API cbx_status cbx_count_defects(cbx_ctx* c, long out[3]) {
+  return guarded(c, [&] {
+    cudaSetDevice(c->device);
+    cudaMemsetAsync(c->d_defects, 0, 4 * sizeof(unsigned long long), c->stream);
+    launch_count_defects(c->P, c->d_defects, c->stream);
+    unsigned long long h[4];
+    cuda_check(cudaMemcpyAsync(h, c->d_defects, sizeof h, cudaMemcpyDeviceToHost, c->stream),
+               "defects");
+    cuda_check(cudaStreamSynchronize(c->stream), "defects");
+    out[0] = (long)(h[0] - h[2]);
+    out[1] = (long)h[1];
+    out[2] = std::max(out[0], out[1]);
+  });
+}
+
+CBX_API cbx_status cbx_enable_timing(cbx_ctx* c, int on) {
+  return guarded(c, [&] {
+    c->timing = on != 0;
+    for (double& t : c->t_ms) t = 0.0;
+  });
+}
+CBX_API cbx_status cbx_last_timings(cbx_ctx* c, double out_ms[8]) {
+  return guarded(c, [&] {
+    for (int i = 0; i < 8; ++i) out_ms[i] = c->t_ms[i];
+  });
+}
+CBX_API cbx_status cbx_count_pairs(cbx_ctx* c, uint64_t out[2]) {
+  return guarded(c, [&] {
+    cudaSetDevice(c->device);
+    sync_status(c);
+    c->hst.cnt_cand = 0;
+    c->hst.cnt_pair = 0;
+    write_status(c);
+    KP saved = c->P;
+    c->P.count_pairs = 1;
+    launch_density(c->P, c->mode, c->stream);
+    c->P = saved;
+    sync_status(c);
+    out[0] = c->hst.cnt_cand;
+    out[1] = c->hst.cnt_pair;
+    // the extra pass accumulated into rho: recompute it cleanly
+    seq_density(c);
+    sync_status(c);
+    raise_device_error(c, false);
+  });
+}
+CBX_API cbx_status cbx_kernel_launches(cbx_ctx* c, uint64_t* n) {
+  *n = c->launches;
+  return CBX_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,157 @@
+// cbx_device.cuh -- device-side state layout and kernel parameter block.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "../../include/cascade_b200.h"
+#include "cbx_internal.h"
+
+namespace cbx {
+
+// spline table on the device: the reference's 7-coefficient segments
+// (spline.h:19-22) plus the evaluation constants
+struct Tab {
+  const double* seg;  // 7 doubles per segment
+  double x0, h, ih, xl;
+  int nseg;
+};
+
+// clash list: records sorted by (key, bucket order); interior records and
+// their ghost images (gf = 1) share one array.  head[dev] -> first record.
+struct Clash {
+  long long* key;      // reference site id of the bucket
+  unsigned char* gf;   // ghost image?
+  int* src;            // ghost image: index of its interior source record
+  double *px, *py, *pz, *vx, *vy, *vz, *fx, *fy, *fz;
+  double *rho, *df;
+  double *e_emb, *e_pair, *v2;  // per-record partials (deterministic sums)
+  unsigned long long* tag;
+};
+
+// pass-1 evictees of update_hash (store.cpp:46-54)
+struct Movers {
+  long long *key, *old;
+  double *px, *py, *pz, *vx, *vy, *vz;
+  unsigned long long* tag;
+};
+
+// single-block sort scratch
+struct Scratch {
+  long long *k1, *k2, *k3;
+  int *pl, *flag, *pos;
+};
+
+struct DevStatus {
+  int err;  // cbx_status of the first store error (domain / logic / capacity)
+  int n_ovl;
+  unsigned long long ovl_key[kMaxOverlapRecords];
+  unsigned long long ovl_a[kMaxOverlapRecords], ovl_b[kMaxOverlapRecords];
+  double ovl_r2[kMaxOverlapRecords];
+  double err_pos[3];
+  unsigned long long r_underflow, rho_clamp;
+  int n_clash, n_mov;
+  // StepState mirror (sim.h:11-21)
+  long long step;
+  double t, dt, kinetic, pair, embedding, max_speed;
+  double dt_next;  // dt of the next step (fixed, or adaptive_dt from max_speed)
+  int adaptive;
+  double dt_max, max_disp;
+  unsigned long long cnt_cand, cnt_pair;
+};
+
+struct KP {
+  Geo G;
+  double accel, mv2;  // units::accel_factor, units::mv2_to_ev (units.h:17-24)
+  long long S;  // 2*NC sites
+  double4* pdf;  // x y z dF
+  double* rho;
+  double* vel;  // 3 planes of S
+  double* frc;  // 3 planes of S
+  unsigned long long* tag;
+  int* tgt;  // owner of a site: itself (interior) or its periodic source (ghost)
+  int *gh_dst, *gh_src;
+  signed char* gh_k;  // 3 per ghost: box shifts (store.cpp:166-169)
+  long long n_gh;
+  int* head;
+  Clash cl, cl2;
+  int cap_clash;
+  Movers mv;
+  int cap_mov;
+  Scratch sc;
+  int cap_items;  // power of two
+  Tab dens, zr, emb;
+  double cutoff, cut2, mass;
+  double *part_emb, *part_pair, *part_ke, *part_vmax;
+  int n_part;
+  int count_pairs;
+  DevStatus* st;
+};
+
+#if defined(__CUDACC__)
+// thread -> (parity, interior cell): blocks of 8 warps cover 128 cells,
+// warps 0-3 the even sublattice, 4-7 the odd one (warp-uniform offset lists)
+__device__ __forceinline__ bool map_site(const KP& P, int& par, long long& d) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  par = warp >> 2;
+  const long long e = (long long)blockIdx.x * 128 + (warp & 3) * 32 + lane;
+  if (e >= P.G.NI) return false;
+  d = par * P.G.NC + interior_cell(e, P.G);
+  return true;
+}
+
+// read-only 32-byte record load through the non-coherent path
+__device__ __forceinline__ double4 ldg4(const double4* p) {
+  const double2 a = __ldg(reinterpret_cast<const double2*>(p));
+  const double2 b = __ldg(reinterpret_cast<const double2*>(p) + 1);
+  return make_double4(a.x, a.y, b.x, b.y);
+}
+
+// deterministic block reduction (fixed tree); result valid in thread 0
+template <int N>
+__device__ __forceinline__ double block_sum(double v, double* sh) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) sh[w] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (threadIdx.x == 0)
+    for (int i = 0; i < N / 32; ++i) s += sh[i];
+  __syncthreads();
+  return s;
+}
+template <int N>
+__device__ __forceinline__ double block_max(double v, double* sh) {
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) sh[w] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (threadIdx.x == 0)
+    for (int i = 0; i < N / 32; ++i) s = fmax(s, sh[i]);
+  __syncthreads();
+  return s;
+}
+
+__device__ __forceinline__ void set_error(DevStatus* st, int code) { atomicCAS(&st->err, 0, code); }
+#endif
+
+// device entry points (launch wrappers), implemented in the .cu files
+void launch_density(const KP& P, int mode, cudaStream_t s);
+void launch_clash_density(const KP& P, cudaStream_t s);
+void launch_embed(const KP& P, cudaStream_t s);
+void launch_force(const KP& P, int mode, cudaStream_t s);
+void launch_clash_force(const KP& P, cudaStream_t s);
+void launch_kick_drift(const KP& P, int move, cudaStream_t s);
+void launch_clash_zero(const KP& P, int what, cudaStream_t s);
+void launch_rehash(const KP& P, cudaStream_t s);
+void launch_ghost_fill(const KP& P, cudaStream_t s);
+void launch_clash_images(const KP& P, cudaStream_t s);
+void launch_kick2(const KP& P, int kick, cudaStream_t s);
+void launch_finalize(const KP& P, int stepping, int energies, cudaStream_t s);
+void launch_count_defects(const KP& P, unsigned long long* out, cudaStream_t s);
+void upload_offsets(const int* half_dev[2], const int half_n[2], const int* full_dev[2],
+                    const int full_n[2], const long long* full_flat[2], cudaStream_t s);
+int eam_blocks(const KP& P);
+int embed_blocks(const KP& P);
+
+}  // namespace cbx

@@ -1,0 +1,650 @@
+// store_kernels.cu -- the per-step lattice-store machinery on the device.
+//
+// Reference (paths relative to /root/reference/proj/core/src):
+//   Simulation::step kick + drift       sim.cpp:250-255  -> k_kick_drift (+clash)
+//   canonicalize_positions              store.cpp:88-118 -> fused into k_kick_drift
+//   update_hash pass 1 (evict)          store.cpp:46-54  -> fused into k_kick_drift
+//   update_hash pass 2 (re-place)       store.cpp:56-75  -> k_rehash (one block)
+//   fill_ghosts, slot images            store.cpp:120-158,184-188 -> k_ghost_fill
+//   fill_ghosts, clash images           store.cpp:160-194 -> k_clash_images (one block)
+//   second half-kick + measure          sim.cpp:262-270, 237-246 -> k_kick2 (+clash)
+//   count_defects                       analysis.cpp:40-56 -> k_count_defects
+//
+// Positions, hashes and wraps use exact IEEE operations in the reference's
+// order (cbx_internal.h), so slot ids, clash membership and bucket order are
+// bit-identical to the reference.  Pass 2's sequential semantics (the first
+// re-placed record claims a free slot) are reproduced by sorting all movers
+// by (new site, old site, class, order) -- see k_rehash.
+#include <climits>
+
+#include "cbx_device.cuh"
+
+namespace cbx {
+
+__device__ __forceinline__ double half_kick(const KP& P, double dt) {
+  return xdiv(xmul(xmul(0.5, dt), P.accel), P.mass);  // sim.cpp:250
+}
+
+__device__ __forceinline__ bool site_is_ghost(long long id, const Geo& G) {
+  int cx, cy, cz;
+  cell_xyz(id >> 1, G, cx, cy, cz);
+  return cell_is_ghost(cx, cy, cz, G);
+}
+
+// -------------------------------------------------- kick, drift, wrap, evict
+__global__ void __launch_bounds__(256) k_kick_drift(KP P, int move) {
+  if (P.st->err) return;
+  int par;
+  long long d;
+  if (!map_site(P, par, d)) return;
+  double4 p = P.pdf[d];
+  if (p.x >= kVacantTest) return;
+  const long long S = P.S;
+  double vx = P.vel[d], vy = P.vel[S + d], vz = P.vel[2 * S + d];
+  if (move) {
+    const double dt = P.st->dt_next;
+    const double hk = half_kick(P, dt);
+    vx = xadd(vx, xmul(P.frc[d], hk));
+    vy = xadd(vy, xmul(P.frc[S + d], hk));
+    vz = xadd(vz, xmul(P.frc[2 * S + d], hk));
+    p.x = xadd(p.x, xmul(vx, dt));
+    p.y = xadd(p.y, xmul(vy, dt));
+    p.z = xadd(p.z, xmul(vz, dt));
+    P.vel[d] = vx;
+    P.vel[S + d] = vy;
+    P.vel[2 * S + d] = vz;
+  }
+  if (!wrap_position(p.x, p.y, p.z, P.G)) {
+    set_error(P.st, CBX_LOGIC);
+    return;
+  }
+  const long long real = nearest_site(p.x, p.y, p.z, P.G);
+  if (real < 0) {
+    if (atomicCAS(&P.st->err, 0, CBX_DOMAIN) == 0) {
+      P.st->err_pos[0] = p.x;
+      P.st->err_pos[1] = p.y;
+      P.st->err_pos[2] = p.z;
+    }
+    return;
+  }
+  const long long own = ref_of_dev(d, P.G.NC);
+  if (real != own) {  // pass 1: evict to the clash map under the new hash
+    const int m = atomicAdd(&P.st->n_mov, 1);
+    if (m >= P.cap_mov) {
+      set_error(P.st, CBX_RUNTIME);
+      return;
+    }
+    P.mv.key[m] = real;
+    P.mv.old[m] = own;
+    P.mv.px[m] = p.x;
+    P.mv.py[m] = p.y;
+    P.mv.pz[m] = p.z;
+    P.mv.vx[m] = vx;
+    P.mv.vy[m] = vy;
+    P.mv.vz[m] = vz;
+    P.mv.tag[m] = P.tag[d];
+    P.pdf[d] = make_double4(kVacant, kVacant, kVacant, 0.0);
+  } else {
+    P.pdf[d] = p;
+  }
+}
+
+__global__ void k_clash_kick_drift(KP P, int move) {
+  if (P.st->err) return;
+  const int n = P.st->n_clash;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    if (P.cl.gf[i]) continue;
+    double px = P.cl.px[i], py = P.cl.py[i], pz = P.cl.pz[i];
+    if (move) {
+      const double dt = P.st->dt_next;
+      const double hk = half_kick(P, dt);
+      const double vx = xadd(P.cl.vx[i], xmul(P.cl.fx[i], hk));
+      const double vy = xadd(P.cl.vy[i], xmul(P.cl.fy[i], hk));
+      const double vz = xadd(P.cl.vz[i], xmul(P.cl.fz[i], hk));
+      P.cl.vx[i] = vx;
+      P.cl.vy[i] = vy;
+      P.cl.vz[i] = vz;
+      px = xadd(px, xmul(vx, dt));
+      py = xadd(py, xmul(vy, dt));
+      pz = xadd(pz, xmul(vz, dt));
+    }
+    if (!wrap_position(px, py, pz, P.G)) {
+      set_error(P.st, CBX_LOGIC);
+      return;
+    }
+    P.cl.px[i] = px;
+    P.cl.py[i] = py;
+    P.cl.pz[i] = pz;
+  }
+}
+
+// ---------------------------------------------------- single-block helpers
+// bitonic sort of (k1, k2, k3, pl) ascending by (k1, k2, k3) over n_pad
+// (power of two) entries in global scratch; one block, all threads call it
+__device__ void block_sort(long long* k1, long long* k2, long long* k3, int* pl, int n_pad) {
+  for (int k = 2; k <= n_pad; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < n_pad; i += blockDim.x) {
+        const int q = i ^ j;
+        if (q <= i) continue;
+        const bool up = (i & k) == 0;
+        const long long a1 = k1[i], b1 = k1[q];
+        bool gt;
+        if (a1 != b1) gt = a1 > b1;
+        else if (k2[i] != k2[q]) gt = k2[i] > k2[q];
+        else gt = k3[i] > k3[q];
+        if (gt == up) {
+          k1[i] = b1;
+          k1[q] = a1;
+          long long t = k2[i];
+          k2[i] = k2[q];
+          k2[q] = t;
+          t = k3[i];
+          k3[i] = k3[q];
+          k3[q] = t;
+          const int u = pl[i];
+          pl[i] = pl[q];
+          pl[q] = u;
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// exclusive prefix over flags[0..n) -> pos[], returns the total (all threads)
+__device__ int block_scan(const int* flag, int* pos, int n) {
+  __shared__ int s_cnt[1024];
+  const int chunk = (n + blockDim.x - 1) / blockDim.x;
+  const int lo = threadIdx.x * chunk, hi = min(n, lo + chunk);
+  int c = 0;
+  for (int i = lo; i < hi; ++i) c += flag[i];
+  s_cnt[threadIdx.x] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int run = 0;
+    for (int t = 0; t < (int)blockDim.x; ++t) {
+      const int v = s_cnt[t];
+      s_cnt[t] = run;
+      run += v;
+    }
+    s_cnt[blockDim.x - 1 + 0] += 0;
+  }
+  __syncthreads();
+  int run = s_cnt[threadIdx.x];
+  for (int i = lo; i < hi; ++i) {
+    pos[i] = run;
+    run += flag[i];
+  }
+  __syncthreads();
+  __shared__ int s_total;
+  if (threadIdx.x == blockDim.x - 1) s_total = run;
+  __syncthreads();
+  const int tot = s_total;
+  __syncthreads();
+  return tot;
+}
+
+__device__ __forceinline__ int pad_pow2(int n) {
+  int p = 1;
+  while (p < n) p <<= 1;
+  return p;
+}
+
+__device__ __forceinline__ void copy_record(const Clash& a, int i, const Clash& b, int j) {
+  b.key[j] = a.key[i];
+  b.gf[j] = a.gf[i];
+  b.src[j] = a.src[i];
+  b.px[j] = a.px[i];
+  b.py[j] = a.py[i];
+  b.pz[j] = a.pz[i];
+  b.vx[j] = a.vx[i];
+  b.vy[j] = a.vy[i];
+  b.vz[j] = a.vz[i];
+  b.fx[j] = a.fx[i];
+  b.fy[j] = a.fy[i];
+  b.fz[j] = a.fz[i];
+  b.rho[j] = a.rho[i];
+  b.df[j] = a.df[i];
+  b.e_emb[j] = a.e_emb[i];
+  b.e_pair[j] = a.e_pair[i];
+  b.v2[j] = a.v2[i];
+  b.tag[j] = a.tag[i];
+}
+
+// ------------------------------------------------- update_hash pass 2
+// The reference walks the clash map in key order (store.cpp:59-75); pass-1
+// evictees sit at the end of bucket `new hash` in ascending old-site order
+// (they were appended while scanning slots in id order).  Each record goes
+// to its hashed slot if that slot is free and interior, else to keep[hash].
+// A slot's state only changes through its own promotions, so records with
+// the same hash form independent groups processed in walk order: sorting by
+// (hash, walk key, class, order) makes the group's first record the one
+// that claims a free slot and the rest the new bucket, in order.
+__global__ void __launch_bounds__(1024) k_rehash(KP P) {
+  if (P.st->err) return;
+  const int n_old = P.st->n_clash;
+  const int n_mov = min(P.st->n_mov, P.cap_mov);
+  if (n_old == 0 && n_mov == 0) return;
+  __shared__ int s_n;
+  if (threadIdx.x == 0) s_n = 0;
+  for (int i = threadIdx.x; i < n_old; i += blockDim.x)
+    P.head[dev_of_ref(P.cl.key[i], P.G.NC)] = -1;
+  __syncthreads();
+  const Scratch& X = P.sc;
+  for (int i = threadIdx.x; i < n_old; i += blockDim.x) {
+    if (P.cl.gf[i]) continue;
+    const long long real = nearest_site(P.cl.px[i], P.cl.py[i], P.cl.pz[i], P.G);
+    if (real < 0) {
+      if (atomicCAS(&P.st->err, 0, CBX_DOMAIN) == 0) {
+        P.st->err_pos[0] = P.cl.px[i];
+        P.st->err_pos[1] = P.cl.py[i];
+        P.st->err_pos[2] = P.cl.pz[i];
+      }
+      continue;
+    }
+    const int k = atomicAdd(&s_n, 1);
+    X.k1[k] = real;
+    X.k2[k] = P.cl.key[i];
+    X.k3[k] = i;
+    X.pl[k] = i;
+  }
+  __syncthreads();
+  const int base = s_n;
+  if (base + n_mov > P.cap_items) {
+    if (threadIdx.x == 0) set_error(P.st, CBX_RUNTIME);
+    return;
+  }
+  for (int m = threadIdx.x; m < n_mov; m += blockDim.x) {
+    X.k1[base + m] = P.mv.key[m];
+    X.k2[base + m] = P.mv.key[m];
+    X.k3[base + m] = (1ll << 62) | P.mv.old[m];
+    X.pl[base + m] = -(m + 1);
+  }
+  const int n = base + n_mov;
+  const int n_pad = pad_pow2(n);
+  for (int i = n + threadIdx.x; i < n_pad; i += blockDim.x) {
+    X.k1[i] = LLONG_MAX;
+    X.k2[i] = LLONG_MAX;
+    X.k3[i] = LLONG_MAX;
+    X.pl[i] = 0;
+  }
+  __syncthreads();
+  block_sort(X.k1, X.k2, X.k3, X.pl, n_pad);
+  const long long S = P.S;
+  for (int p = threadIdx.x; p < n; p += blockDim.x) {
+    int promote = 0;
+    const long long real = X.k1[p];
+    if (p == 0 || X.k1[p - 1] != real) {
+      const long long dr = dev_of_ref(real, P.G.NC);
+      if (P.pdf[dr].x >= kVacantTest && !site_is_ghost(real, P.G)) {
+        promote = 1;
+        const int q = X.pl[p];
+        if (q >= 0) {
+          P.pdf[dr] = make_double4(P.cl.px[q], P.cl.py[q], P.cl.pz[q], 0.0);
+          P.vel[dr] = P.cl.vx[q];
+          P.vel[S + dr] = P.cl.vy[q];
+          P.vel[2 * S + dr] = P.cl.vz[q];
+          P.tag[dr] = P.cl.tag[q];
+        } else {
+          const int m = -q - 1;
+          P.pdf[dr] = make_double4(P.mv.px[m], P.mv.py[m], P.mv.pz[m], 0.0);
+          P.vel[dr] = P.mv.vx[m];
+          P.vel[S + dr] = P.mv.vy[m];
+          P.vel[2 * S + dr] = P.mv.vz[m];
+          P.tag[dr] = P.mv.tag[m];
+        }
+        P.frc[dr] = 0.0;
+        P.frc[S + dr] = 0.0;
+        P.frc[2 * S + dr] = 0.0;
+      }
+    }
+    X.flag[p] = !promote;
+  }
+  __syncthreads();
+  const int n_new = block_scan(X.flag, X.pos, n);
+  for (int p = threadIdx.x; p < n; p += blockDim.x) {
+    if (!X.flag[p]) continue;
+    const int j = X.pos[p];
+    const int q = X.pl[p];
+    const Clash& B = P.cl2;
+    B.key[j] = X.k1[p];
+    B.gf[j] = 0;
+    B.src[j] = j;
+    if (q >= 0) {
+      B.px[j] = P.cl.px[q];
+      B.py[j] = P.cl.py[q];
+      B.pz[j] = P.cl.pz[q];
+      B.vx[j] = P.cl.vx[q];
+      B.vy[j] = P.cl.vy[q];
+      B.vz[j] = P.cl.vz[q];
+      B.tag[j] = P.cl.tag[q];
+      B.fx[j] = P.cl.fx[q];
+      B.fy[j] = P.cl.fy[q];
+      B.fz[j] = P.cl.fz[q];
+    } else {
+      const int m = -q - 1;
+      B.px[j] = P.mv.px[m];
+      B.py[j] = P.mv.py[m];
+      B.pz[j] = P.mv.pz[m];
+      B.vx[j] = P.mv.vx[m];
+      B.vy[j] = P.mv.vy[m];
+      B.vz[j] = P.mv.vz[m];
+      B.tag[j] = P.mv.tag[m];
+      B.fx[j] = 0.0;
+      B.fy[j] = 0.0;
+      B.fz[j] = 0.0;
+    }
+    B.rho[j] = 0.0;
+    B.df[j] = 0.0;
+    B.e_emb[j] = 0.0;
+    B.e_pair[j] = 0.0;
+    B.v2[j] = 0.0;
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < n_new; j += blockDim.x) copy_record(P.cl2, j, P.cl, j);
+  if (threadIdx.x == 0) {
+    P.st->n_clash = n_new;
+    P.st->n_mov = 0;
+  }
+}
+
+// ------------------------------------------------------ ghost slot images
+// each ghost site has one periodic source; its image position is the
+// source's plus k*len, added per axis exactly like store.cpp:166-169
+__global__ void k_ghost_fill(KP P) {
+  if (P.st->err) return;
+  const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= P.n_gh) return;
+  const int dst = P.gh_dst[g], src = P.gh_src[g];
+  const double4 p = P.pdf[src];
+  if (p.x >= kVacantTest) {
+    P.pdf[dst] = make_double4(kVacant, kVacant, kVacant, 0.0);
+    return;
+  }
+  const signed char* k = P.gh_k + 3 * g;
+  P.pdf[dst] = make_double4(xadd(p.x, xmul((double)k[0], P.G.lx)),
+                            xadd(p.y, xmul((double)k[1], P.G.ly)),
+                            xadd(p.z, xmul((double)k[2], P.G.lz)), p.w);
+}
+
+// --------------------------------------------------- ghost clash images
+// store.cpp:160-194 for clash atoms: images of every interior record in
+// (key, index) order, k loop z-y-x; a ghost bucket keeps its source
+// bucket's order.  An image whose ghost slot is free would take the slot in
+// the reference; update_hash never leaves an interior bucket over a vacant
+// slot, so that state is rejected (CBX_INVALID_ARGUMENT) instead.
+__global__ void __launch_bounds__(1024) k_clash_images(KP P) {
+  if (P.st->err) return;
+  const int n = P.st->n_clash;
+  if (n == 0) return;
+  const Scratch& X = P.sc;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    P.head[dev_of_ref(P.cl.key[i], P.G.NC)] = -1;
+    X.flag[i] = !P.cl.gf[i];
+  }
+  __syncthreads();
+  const int n_int = block_scan(X.flag, X.pos, n);
+  // interior records, in order, to cl2[0..n_int)
+  for (int i = threadIdx.x; i < n; i += blockDim.x)
+    if (X.flag[i]) copy_record(P.cl, i, P.cl2, X.pos[i]);
+  __syncthreads();
+  // count images per interior record
+  const Geo& G = P.G;
+  for (int r = threadIdx.x; r < n_int; r += blockDim.x) {
+    const long long id = P.cl2.key[r];
+    int cx, cy, cz;
+    cell_xyz(id >> 1, G, cx, cy, cz);
+    int c = 0;
+    for (int kz = -G.kmz; kz <= G.kmz; ++kz)
+      for (int ky = -G.kmy; ky <= G.kmy; ++ky)
+        for (int kx = -G.kmx; kx <= G.kmx; ++kx) {
+          if (kx == 0 && ky == 0 && kz == 0) continue;
+          const int ix = cx + G.bx * kx, iy = cy + G.by * ky, iz = cz + G.bz * kz;
+          if (ix < 0 || ix >= G.tx || iy < 0 || iy >= G.ty || iz < 0 || iz >= G.tz) continue;
+          ++c;
+        }
+    X.flag[r] = c;
+  }
+  __syncthreads();
+  const int n_img = block_scan(X.flag, X.pos, n_int);
+  const int total = n_int + n_img;
+  if (total > P.cap_clash || total > P.cap_items) {
+    if (threadIdx.x == 0) set_error(P.st, CBX_RUNTIME);
+    return;
+  }
+  // sort items: interior records (key, r, 0) and images (image key, r, 1+seq)
+  for (int r = threadIdx.x; r < n_int; r += blockDim.x) {
+    X.k1[r] = P.cl2.key[r];
+    X.k2[r] = r;
+    X.k3[r] = 0;
+    X.pl[r] = r;
+    const long long id = P.cl2.key[r];
+    const int par = (int)(id & 1);
+    int cx, cy, cz;
+    cell_xyz(id >> 1, G, cx, cy, cz);
+    int w = n_int + X.pos[r], seq = 0;
+    for (int kz = -G.kmz; kz <= G.kmz; ++kz)
+      for (int ky = -G.kmy; ky <= G.kmy; ++ky)
+        for (int kx = -G.kmx; kx <= G.kmx; ++kx) {
+          if (kx == 0 && ky == 0 && kz == 0) continue;
+          const int ix = cx + G.bx * kx, iy = cy + G.by * ky, iz = cz + G.bz * kz;
+          if (ix < 0 || ix >= G.tx || iy < 0 || iy >= G.ty || iz < 0 || iz >= G.tz) continue;
+          const long long iid = ref_id(cell_of(ix, iy, iz, G), par);
+          if (P.pdf[dev_of_ref(iid, G.NC)].x >= kVacantTest) set_error(P.st, CBX_INVALID_ARGUMENT);
+          // record w of cl2 = image
+          P.cl2.key[w] = iid;
+          P.cl2.gf[w] = 1;
+          P.cl2.src[w] = r;
+          P.cl2.px[w] = xadd(P.cl2.px[r], xmul((double)kx, G.lx));
+          P.cl2.py[w] = xadd(P.cl2.py[r], xmul((double)ky, G.ly));
+          P.cl2.pz[w] = xadd(P.cl2.pz[r], xmul((double)kz, G.lz));
+          P.cl2.vx[w] = P.cl2.vx[r];
+          P.cl2.vy[w] = P.cl2.vy[r];
+          P.cl2.vz[w] = P.cl2.vz[r];
+          P.cl2.fx[w] = 0.0;
+          P.cl2.fy[w] = 0.0;
+          P.cl2.fz[w] = 0.0;
+          P.cl2.rho[w] = P.cl2.rho[r];
+          P.cl2.df[w] = P.cl2.df[r];
+          P.cl2.e_emb[w] = 0.0;
+          P.cl2.e_pair[w] = 0.0;
+          P.cl2.v2[w] = 0.0;
+          P.cl2.tag[w] = P.cl2.tag[r];
+          X.k1[w] = iid;
+          X.k2[w] = r;
+          X.k3[w] = 1 + seq;
+          X.pl[w] = w;
+          ++w;
+          ++seq;
+        }
+  }
+  const int n_pad = pad_pow2(total);
+  for (int i = total + threadIdx.x; i < n_pad; i += blockDim.x) {
+    X.k1[i] = LLONG_MAX;
+    X.k2[i] = LLONG_MAX;
+    X.k3[i] = LLONG_MAX;
+    X.pl[i] = 0;
+  }
+  __syncthreads();
+  block_sort(X.k1, X.k2, X.k3, X.pl, n_pad);
+  // final position of every interior record (for the images' src links)
+  for (int p = threadIdx.x; p < total; p += blockDim.x)
+    if (X.k3[p] == 0) X.flag[X.pl[p]] = p;
+  __syncthreads();
+  for (int p = threadIdx.x; p < total; p += blockDim.x) {
+    const int q = X.pl[p];
+    copy_record(P.cl2, q, P.cl, p);
+    P.cl.src[p] = P.cl2.gf[q] ? X.flag[P.cl2.src[q]] : p;
+    if (p == 0 || X.k1[p - 1] != X.k1[p]) P.head[dev_of_ref(X.k1[p], G.NC)] = p;
+  }
+  if (threadIdx.x == 0) P.st->n_clash = total;
+}
+
+// zero the accumulators of the clash records: what 0 density, 1 force
+__global__ void k_clash_zero(KP P, int what) {
+  const int n = P.st->n_clash;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    if (what == 0) {
+      P.cl.rho[i] = 0.0;
+    } else {
+      P.cl.fx[i] = 0.0;
+      P.cl.fy[i] = 0.0;
+      P.cl.fz[i] = 0.0;
+      P.cl.e_pair[i] = 0.0;
+    }
+  }
+}
+
+// ---------------------------------------------- second half kick + measure
+__global__ void __launch_bounds__(256) k_kick2(KP P, int kick) {
+  __shared__ double sh[8];
+  double v2 = 0.0;
+  int par;
+  long long d;
+  if (!P.st->err && !P.st->n_ovl && map_site(P, par, d)) {
+    if (P.pdf[d].x < kVacantTest) {
+      const long long S = P.S;
+      double vx = P.vel[d], vy = P.vel[S + d], vz = P.vel[2 * S + d];
+      if (kick) {
+        const double hk = half_kick(P, P.st->dt_next);
+        vx = xadd(vx, xmul(P.frc[d], hk));
+        vy = xadd(vy, xmul(P.frc[S + d], hk));
+        vz = xadd(vz, xmul(P.frc[2 * S + d], hk));
+        P.vel[d] = vx;
+        P.vel[S + d] = vy;
+        P.vel[2 * S + d] = vz;
+      }
+      v2 = exact_r2(vx, vy, vz);
+    }
+  }
+  const double s = block_sum<256>(v2, sh);
+  const double m = block_max<256>(v2, sh);
+  if (threadIdx.x == 0) {
+    P.part_ke[blockIdx.x] = s;
+    P.part_vmax[blockIdx.x] = m;
+  }
+}
+
+__global__ void k_clash_kick2(KP P, int kick) {
+  if (P.st->err || P.st->n_ovl) return;
+  const int n = P.st->n_clash;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    if (P.cl.gf[i]) {
+      P.cl.v2[i] = 0.0;
+      continue;
+    }
+    double vx = P.cl.vx[i], vy = P.cl.vy[i], vz = P.cl.vz[i];
+    if (kick) {
+      const double hk = half_kick(P, P.st->dt_next);
+      vx = xadd(vx, xmul(P.cl.fx[i], hk));
+      vy = xadd(vy, xmul(P.cl.fy[i], hk));
+      vz = xadd(vz, xmul(P.cl.fz[i], hk));
+      P.cl.vx[i] = vx;
+      P.cl.vy[i] = vy;
+      P.cl.vz[i] = vz;
+    }
+    P.cl.v2[i] = exact_r2(vx, vy, vz);
+  }
+}
+
+// ------------------------------------------------------------- finalize
+// deterministic sums of the per-block / per-record partials into StepState
+__global__ void __launch_bounds__(1024) k_finalize(KP P, int stepping, int energies,
+                                                   int n_eam, int n_emb) {
+  __shared__ double sh[32];
+  DevStatus* st = P.st;
+  if (st->err || st->n_ovl) return;
+  const int nc = st->n_clash;
+  if (energies) {
+    double a = 0.0, b = 0.0;
+    for (int i = threadIdx.x; i < n_emb; i += blockDim.x) a += P.part_emb[i];
+    for (int i = threadIdx.x; i < n_eam; i += blockDim.x) b += P.part_pair[i];
+    for (int i = threadIdx.x; i < nc; i += blockDim.x) {
+      a += P.cl.e_emb[i];
+      b += P.cl.e_pair[i];
+    }
+    const double ea = block_sum<1024>(a, sh);
+    const double eb = block_sum<1024>(b, sh);
+    if (threadIdx.x == 0) {
+      st->embedding = ea;
+      st->pair = eb;
+    }
+  }
+  if (stepping >= 0) {  // 1: completed a step, 0: measure only
+    double a = 0.0, m = 0.0;
+    for (int i = threadIdx.x; i < n_eam; i += blockDim.x) {
+      a += P.part_ke[i];
+      m = fmax(m, P.part_vmax[i]);
+    }
+    for (int i = threadIdx.x; i < nc; i += blockDim.x) {
+      a += P.cl.v2[i];
+      m = fmax(m, P.cl.v2[i]);
+    }
+    const double sv = block_sum<1024>(a, sh);
+    const double mv = block_max<1024>(m, sh);
+    if (threadIdx.x == 0) {
+      st->kinetic = xmul(xmul(xmul(0.5, P.mass), sv), P.mv2);  // sim.cpp:269
+      st->max_speed = sqrt(mv);
+      if (stepping == 1) {
+        const double dt = st->dt_next;
+        st->step += 1;
+        st->t = xadd(st->t, dt);
+        st->dt = dt;
+      }
+      if (st->adaptive) {  // adaptive_dt, sim.cpp:94-98
+        double dt = st->dt_max;
+        if (st->max_speed > 0.0) dt = fmin(dt, xdiv(st->max_disp, st->max_speed));
+        st->dt_next = fmax(dt, 1e-7);
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------- count_defects
+__global__ void __launch_bounds__(256) k_count_defects(KP P, unsigned long long* out) {
+  int par;
+  long long d;
+  unsigned vac = 0;
+  if (map_site(P, par, d) && P.pdf[d].x >= kVacantTest) vac = 1;
+  for (int o = 16; o > 0; o >>= 1) vac += __shfl_xor_sync(0xffffffffu, vac, o);
+  if ((threadIdx.x & 31) == 0 && vac) atomicAdd(&out[0], (unsigned long long)vac);
+  if (blockIdx.x == 0) {  // clash buckets
+    const int n = P.st->n_clash;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      if (P.cl.gf[i]) continue;
+      if (i > 0 && P.cl.key[i - 1] == P.cl.key[i]) continue;
+      int sz = 0;
+      for (int j = i; j < n && P.cl.key[j] == P.cl.key[i]; ++j) ++sz;
+      const bool valid = P.pdf[dev_of_ref(P.cl.key[i], P.G.NC)].x < kVacantTest;
+      atomicAdd(&out[1], (unsigned long long)((valid ? 1 : 0) + sz - 1));
+      if (!valid) atomicAdd(&out[2], 1ull);  // vacancies to subtract
+    }
+  }
+}
+
+// -------------------------------------------------------------- launchers
+void launch_kick_drift(const KP& P, int move, cudaStream_t s) {
+  k_kick_drift<<<eam_blocks(P), 256, 0, s>>>(P, move);
+  k_clash_kick_drift<<<8, 256, 0, s>>>(P, move);
+}
+void launch_rehash(const KP& P, cudaStream_t s) { k_rehash<<<1, 1024, 0, s>>>(P); }
+void launch_ghost_fill(const KP& P, cudaStream_t s) {
+  if (P.n_gh) k_ghost_fill<<<(int)((P.n_gh + 255) / 256), 256, 0, s>>>(P);
+}
+void launch_clash_images(const KP& P, cudaStream_t s) { k_clash_images<<<1, 1024, 0, s>>>(P); }
+void launch_clash_zero(const KP& P, int what, cudaStream_t s) {
+  k_clash_zero<<<8, 256, 0, s>>>(P, what);
+}
+void launch_kick2(const KP& P, int kick, cudaStream_t s) {
+  k_kick2<<<eam_blocks(P), 256, 0, s>>>(P, kick);
+  k_clash_kick2<<<8, 256, 0, s>>>(P, kick);
+}
+void launch_finalize(const KP& P, int stepping, int energies, cudaStream_t s) {
+  k_finalize<<<1, 1024, 0, s>>>(P, stepping, energies, eam_blocks(P), embed_blocks(P));
+}
+void launch_count_defects(const KP& P, unsigned long long* out, cudaStream_t s) {
+  k_count_defects<<<eam_blocks(P), 256, 0, s>>>(P, out);
+}
+
+}  // namespace cbx

@@ -1,0 +1,329 @@
+"""GPU parity: the sm_100a path through the C ABI against the CPU oracle
+(oracle/cascade_oracle.c, itself pinned bit-for-bit to the reference in
+tests/test_oracle.py) on identical seeded inputs.
+
+Tolerances (BASELINE.json north star): slot/clash structure, hash ids and
+neighbour sets bit-exact; rho, dF, per-atom forces within 1e-10 relative
+(forces: relative to max(|f|, 1 eV/A)); energies within 1e-10 relative.
+Mirrors the reference's forces_test.cpp / sim_test.cpp / store_test.cpp.
+"""
+import math
+
+import numpy as np
+import pytest
+
+from helpers import assert_store_parity, by_tag, real_mask, structure
+
+pytestmark = pytest.mark.gpu
+
+REL = 1e-10
+
+
+@pytest.fixture(scope="module")
+def cuda():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2107_07866_b200 import _lib
+    _lib.load()
+    return True
+
+
+def device_for(sim, path, stencil="newton3"):
+    from paper_2107_07866_b200 import DeviceStore, EamPotential
+    dims, a0, g = sim.box
+    dev = DeviceStore((*dims, a0, g), EamPotential.load(path), stencil=stencil)
+    dev.upload(sim.store())
+    return dev
+
+
+def close(a, b, rel=REL):
+    return abs(a - b) <= rel * max(abs(a), abs(b), 1e-300)
+
+
+# --------------------------------------------------------------- storage
+def test_init_bcc_bit_identical(cuda, tables):
+    """init_bcc (sim.cpp:100-130): positions, velocities, tags bit-equal"""
+    from oracle import oracle
+    from paper_2107_07866_b200 import DeviceStore, EamPotential
+    ref = oracle.Sim(tables["baseline"], box=(7, 6, 5), temperature=600.0, seed=4242)
+    dims, a0, g = ref.box
+    dev = DeviceStore((*dims, a0, g), EamPotential.load(tables["baseline"]))
+    n = dev.init_bcc(600.0, 4242)
+    assert n == 2 * 7 * 6 * 5
+    a, b = ref.store(), dev.download()
+    m = real_mask(a)
+    assert np.array_equal(m, real_mask(b))
+    assert np.array_equal(a.pos[m], b.pos[m])
+    assert np.array_equal(a.vel[m], b.vel[m])
+    assert np.array_equal(a.tag[m], b.tag[m])
+    # ghost shell regenerated on the device = fill_ghosts (store.cpp:120-195)
+    gm = a.valid.astype(bool) & a.ghost.astype(bool)
+    assert np.array_equal(gm, b.valid.astype(bool) & b.ghost.astype(bool))
+    assert np.array_equal(a.pos[gm], b.pos[gm])
+    assert np.array_equal(a.tag[gm], b.tag[gm])
+
+
+# ----------------------------------------------------------- force engine
+@pytest.mark.parametrize("stencil", ["newton3", "full"])
+@pytest.mark.parametrize("temp", [0.0, 600.0])
+def test_eval_forces_lattice(cuda, tables, stencil, temp):
+    from oracle import oracle
+    ref = oracle.Sim(tables["baseline"], box=(8, 8, 8), temperature=temp, seed=12345)
+    if temp:
+        ref.step(1e-3, 5)  # thermal disorder
+    dev = device_for(ref, tables["baseline"], stencil)
+    e_ref = ref.eval_forces()
+    e_dev = dev.eval_forces()
+    assert close(e_ref[0], e_dev[0]) and close(e_ref[1], e_dev[1]), (e_ref, e_dev)
+    assert_store_parity(ref.store(), dev.download(), what=f"{stencil} T={temp}")
+
+
+def test_perfect_lattice_kat(cuda, tables):
+    """SURVEY §8(c) KAT for the BASELINE table at rho_max = 40"""
+    from oracle import oracle
+    ref = oracle.Sim(tables["baseline40"], box=(5, 5, 5), temperature=0.0)
+    dev = device_for(ref, tables["baseline40"])
+    emb, pair = dev.eval_forces()
+    s = dev.download()
+    m = real_mask(s)
+    n = m.sum()
+    assert n == 250
+    assert np.abs(s.rho[m] - 11.80956811317917).max() < 1e-11
+    assert np.abs(s.df[m] + 0.145496650894856).max() < 1e-12
+    assert abs(emb / n + 3.4365052179757) < 1e-11
+    assert abs(pair / n + 3.6755476296970) < 1e-11
+    assert np.abs(s.force[m]).max() < 1e-12
+
+
+def test_synthetic_potential_perfect_lattice(cuda, tables):
+    """forces_test.cpp:127-147 on the reference's own synthetic table"""
+    from oracle import oracle
+    ref = oracle.Sim(tables["synthetic"], box=(5, 5, 5), temperature=0.0)
+    dev = device_for(ref, tables["synthetic"])
+    emb, pair = dev.eval_forces()
+    s = dev.download()
+    m = real_mask(s)
+    assert np.abs(s.force[m]).max() <= 1e-9
+    assert np.abs(s.rho[m] - 1.0).max() <= 1e-8
+    assert (emb + pair) / m.sum() == pytest.approx(-4.3, rel=1e-4)
+
+
+def _clash_scenario(path, a0=None):
+    """forces_test.cpp:262-306: interior, boundary and stacked clash buckets"""
+    from oracle import oracle
+    ref = oracle.Sim(path, box=(4, 4, 4), a0=a0 or 0.0, temperature=0.0, init_lattice=True)
+    dims, a, g = ref.box
+    tx, ty = dims[0] + 2 * g, dims[1] + 2 * g
+
+    def cid(x, y, z):
+        return (z * ty + y) * 2 * tx + x
+
+    def site(x, y, z):
+        if x % 2 == 0:
+            return np.array([0.5 * x * a, y * a, z * a])
+        return np.array([0.5 * (x - 1) * a + 0.5 * a, y * a + 0.5 * a, z * a + 0.5 * a])
+
+    ref.set_atom(cid(10, 5, 5), pos=site(11, 5, 5) + [0.15, 0.02, -0.04])
+    ref.set_atom(cid(7, 3, 3), pos=site(6, 3, 3) + [-0.12, 0.08, 0.1])
+    ref.set_atom(cid(12, 4, 6), pos=site(13, 5, 6) + [0.15, 0.0, 0.05])
+    ref.set_atom(cid(12, 6, 6), pos=site(13, 5, 6) + [-0.1, 0.12, -0.06])
+    ref.rehash()
+    return ref
+
+
+@pytest.mark.parametrize("table", ["baseline", "synthetic"])
+def test_clash_buckets_interior_boundary_stacked(cuda, tables, table):
+    ref = _clash_scenario(tables[table])
+    s0 = ref.store()
+    assert (s0.clash_ghost == 0).sum() >= 4
+    dev = device_for(ref, tables[table])
+    # the device's own ghost images of the clash buckets equal fill_ghosts'
+    assert structure(s0)[1] == structure(dev.download())[1]
+    e_ref = ref.eval_forces()
+    e_dev = dev.eval_forces()
+    assert close(e_ref[0], e_dev[0]) and close(e_ref[1], e_dev[1]), (e_ref, e_dev)
+    assert_store_parity(ref.store(), dev.download(), what=table)
+
+
+@pytest.mark.parametrize("box", [(1, 1, 1), (2, 3, 1), (3, 3, 3), (4, 2, 5)])
+def test_tiny_boxes_many_images(cuda, tables, box):
+    """boxes thinner than the ghost shell: several images per atom, self
+    images (acceptance.cpp:100-130 sweeps 1..6^3)"""
+    from oracle import oracle
+    ref = oracle.Sim(tables["synthetic"], box=box, temperature=300.0, seed=7)
+    ref.step(1e-3, 2)
+    dev = device_for(ref, tables["synthetic"])
+    e_ref, e_dev = ref.eval_forces(), dev.eval_forces()
+    assert close(e_ref[0], e_dev[0], 1e-9) and close(e_ref[1], e_dev[1], 1e-9), (e_ref, e_dev)
+    assert_store_parity(ref.store(), dev.download(), what=str(box))
+
+
+def test_serial_contracts(cuda, tables):
+    """compute_density / compute_embedding_derivative / compute_pair_forces"""
+    from oracle import oracle
+    ref = _clash_scenario(tables["baseline"])
+    dev = device_for(ref, tables["baseline"])
+    ref.compute_density()
+    dev.compute_density()
+    a, b = by_tag(ref.store()), by_tag(dev.download())
+    for t in a:
+        assert close(a[t][3], b[t][3]), t
+    assert close(ref.compute_embedding(), dev.compute_embedding_derivative())
+    assert close(ref.compute_pair(), dev.compute_pair_forces())
+    assert_store_parity(ref.store(), dev.download())
+
+
+def test_beyond_cutoff_silent(cuda, tables):
+    """forces_test.cpp:99-125"""
+    from oracle import oracle
+    ref = oracle.Sim(tables["synthetic"], box=(4, 4, 4), init_lattice=False)
+    _, a, g = ref.box
+    p = np.array([3 * a, 4 * a, 4 * a])
+    ref.insert(p, 1)
+    ref.insert(p + [5.7, 0, 0], 2)
+    ref.fill_ghosts()
+    dev = device_for(ref, tables["synthetic"])
+    emb, pair = dev.eval_forces()
+    assert pair == 0.0
+    s = dev.download()
+    m = real_mask(s)
+    assert np.all(s.rho[m] == 0.0) and np.all(s.force[m] == 0.0)
+
+
+def test_dimer_antisymmetric(cuda, tables):
+    """forces_test.cpp:54-97: closed form, bit-exact antisymmetry"""
+    from oracle import oracle
+    ref = oracle.Sim(tables["synthetic"], box=(4, 4, 4), init_lattice=False)
+    _, a, g = ref.box
+    p = np.array([4 * a, 4 * a, 4 * a])
+    ref.insert(p, 1)
+    ref.insert(p + [2.2, 0, 0], 2)
+    ref.fill_ghosts()
+    dev = device_for(ref, tables["synthetic"])
+    dev.eval_forces()
+    t = by_tag(dev.download())
+    f1, f2 = t[1][2], t[2][2]
+    assert f1[0] == -f2[0] and f1[1] == 0.0 and f1[2] == 0.0 and f2[1] == 0.0
+    want_rho = ref.potential_eval(0, 2.2)[0]
+    assert abs(t[1][3] - want_rho) <= 1e-12 * want_rho
+
+
+def test_guard_counters(cuda, tables):
+    """forces_test.cpp:487-531: 4 rho clamps; 3 short-range guard hits"""
+    from oracle import oracle
+    from paper_2107_07866_b200 import DeviceStore, EamPotential
+    ref = oracle.Sim(tables["synthetic"], box=(4, 4, 4), init_lattice=False)
+    dims, a, g = ref.box
+    c = np.array([4 * a, 4 * a, 4 * a])
+    for i, o in enumerate([(0.010, 0.011, 0.009), (-0.012, 0.008, -0.010),
+                           (0.009, -0.011, 0.010), (-0.008, -0.009, -0.011)]):
+        ref.insert(c + o, i)
+    ref.fill_ghosts()
+    dev = device_for(ref, tables["synthetic"])
+    dev.eval_forces()
+    assert dev.guards() == (0, 4)
+    ref2 = oracle.Sim(tables["synthetic"], box=(4, 4, 4), init_lattice=False)
+    ref2.insert(c, 1)
+    ref2.insert(c + [5e-4, 0, 0], 2)
+    ref2.fill_ghosts()
+    dev2 = device_for(ref2, tables["synthetic"])
+    dev2.eval_forces()
+    assert dev2.guards()[0] == 3
+
+
+def test_overlap_names_both_tags(cuda, tables):
+    """forces_test.cpp:533-557"""
+    from oracle import oracle
+    from paper_2107_07866_b200._lib import CbxRuntimeError
+    ref = oracle.Sim(tables["synthetic"], box=(4, 4, 4), init_lattice=False)
+    _, a, g = ref.box
+    c = np.array([4 * a, 4 * a, 4 * a])
+    ref.insert(c, 11)
+    ref.insert(c + [5e-7, 0, 0], 22)
+    ref.fill_ghosts()
+    dev = device_for(ref, tables["synthetic"])
+    with pytest.raises(CbxRuntimeError) as e:
+        dev.compute_density()
+    msg = str(e.value)
+    assert "overlap" in msg and "11" in msg and "22" in msg
+
+
+# ------------------------------------------------------------ step loop
+@pytest.mark.parametrize("stencil", ["newton3", "full"])
+def test_trajectory_config1_shape(cuda, tables, stencil):
+    """BASELINE config 1 shape (600 K, dt 1 fs) on a 10^3 box: 100 steps,
+    state checked every 25 steps; energies and drift against the oracle"""
+    from oracle import oracle
+    ref = oracle.Sim(tables["baseline"], box=(10, 10, 10), temperature=600.0, seed=12345)
+    dev = device_for(ref, tables["baseline"], stencil)
+    dev.set_state(ref.state())
+    e0 = ref.state()
+    for chunk in range(4):
+        ref.step(1e-3, 25)
+        st = dev.step(1e-3, 25)
+        sr = ref.state()
+        assert st["step"] == sr["step"]
+        for k in ("kinetic", "pair", "embedding"):
+            assert abs(st[k] - sr[k]) <= 1e-9 * abs(sr[k]), (k, st[k], sr[k])
+        assert_store_parity(ref.store(), dev.download(), pos_tol=1e-9, rel=1e-8,
+                            what=f"chunk {chunk}")
+    etot = lambda s: s["kinetic"] + s["pair"] + s["embedding"]
+    drift_ref = etot(ref.state()) - etot(e0)
+    drift_dev = etot(dev.state()) - etot(e0)
+    assert abs(drift_dev - drift_ref) <= 0.01 * abs(drift_ref) + 1e-9 * abs(etot(e0))
+
+
+def test_cascade_clash_and_defects(cuda, tables):
+    """PKA cascade on a 10^3 box: off-lattice atoms go through the device
+    clash list; hash ids, bucket membership/order and Wigner-Seitz counts
+    match the oracle at every checkpoint"""
+    from oracle import oracle
+    ref = oracle.Sim(tables["baseline"], box=(10, 10, 10), temperature=600.0, seed=12345,
+                     pka_energy_kev=1.0, pka_site=(5, 5, 5))
+    ref.step(1e-3, 10)
+    dev = device_for(ref, tables["baseline"])
+    dev.set_state(ref.state())
+    ref.inject_pka()
+    st = ref.state()
+    s = ref.store()
+    _, a, g = ref.box
+    tx = 10 + 2 * g
+    site = ((g + 5) * tx + (g + 5)) * 2 * tx + 2 * (g + 5)
+    dev.inject_pka(site, s.vel[site])
+    assert abs(dev.state()["kinetic"] - st["kinetic"]) <= 1e-12 * st["kinetic"]
+    saw_clash = False
+    for chunk in range(8):
+        ref.step(1e-4, 25)
+        dev.step(1e-4, 25)
+        rs, ds = ref.store(), dev.download()
+        saw_clash |= (rs.clash_ghost == 0).sum() > 0
+        assert ref.count_defects() == dev.count_defects(), chunk
+        assert_store_parity(rs, ds, pos_tol=1e-8, rel=1e-7, what=f"cascade chunk {chunk}")
+    assert saw_clash
+
+
+def test_adaptive_dt_matches(cuda, tables):
+    from oracle import oracle
+    ref = oracle.Sim(tables["baseline"], box=(6, 6, 6), temperature=600.0, seed=3)
+    dev = device_for(ref, tables["baseline"])
+    dev.set_state(ref.state())
+    ref.step(-1, 5)
+    st = dev.step(-1, 5)
+    assert st["dt"] == ref.state()["dt"]
+    assert abs(st["t"] - ref.state()["t"]) <= 1e-15
+
+
+def test_simulation_facade(cuda, tables):
+    """Simulation (sim.h) over the device equals the oracle's constructor"""
+    from oracle import oracle
+    from paper_2107_07866_b200 import SimConfig, Simulation
+    cfg = SimConfig(box_x=6, box_y=6, box_z=6, temperature=600.0, seed=99,
+                    potential_path=tables["baseline"])
+    sim = Simulation(cfg)
+    ref = oracle.Sim(tables["baseline"], box=(6, 6, 6), temperature=600.0, seed=99)
+    a, b = ref.state(), sim.state
+    for k in ("kinetic", "pair", "embedding", "max_speed"):
+        assert close(a[k], b[k], 1e-12), k
+    assert sim.atom_count() == 432
+    assert np.abs(sim.total_momentum()).max() < 1e-8
