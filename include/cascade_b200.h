@@ -178,6 +178,15 @@ CBX_API cbx_status cbx_last_timings(cbx_ctx* ctx, double out_ms[8]);
 CBX_API cbx_status cbx_enable_timing(cbx_ctx* ctx, int on);
 CBX_API cbx_status cbx_count_pairs(cbx_ctx* ctx, uint64_t out[2]);
 CBX_API cbx_status cbx_kernel_launches(cbx_ctx* ctx, uint64_t* n); /* cumulative */
+/* benchmark loop: nsteps fixed-dt steps, each preceded (outside the timed
+ * region) by a write of flush_mb MB to evict L2; per-step CUDA events on the
+ * context stream.  out_ms = {density, embed, force, store, integrate, step,
+ * steps, 0} summed over the steps. */
+CBX_API cbx_status cbx_bench_steps(cbx_ctx* ctx, double dt, long nsteps, double flush_mb,
+                                   double out_ms[8]);
+/* measured fp64 peak of this device: a dependent-free DFMA stream over all
+ * SMs, timed with CUDA events (TFLOP/s, DFMA = 2 flops) */
+CBX_API cbx_status cbx_fp64_peak(int device, double* tflops, double* sm_mhz);
 
 #ifdef __cplusplus
 }

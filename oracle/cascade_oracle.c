@@ -1304,6 +1304,16 @@ int orc_set_atom(orc_ctx* c, long long site, int idx, const double p[3], const d
   if (v) { r->vel.x = v[0]; r->vel.y = v[1]; r->vel.z = v[2]; }
   return ORC_OK;
 }
+long orc_displace_interior(orc_ctx* c, const double* disp, long n) {
+  long i = 0;
+  FOR_INTERIOR(&c->box, id) {
+    rec_t* r = &c->slots[id];
+    if (!r->valid || i >= n) continue;
+    r->pos.x += disp[3 * i]; r->pos.y += disp[3 * i + 1]; r->pos.z += disp[3 * i + 2];
+    ++i;
+  }
+  return i;
+}
 int orc_canonicalize(orc_ctx* c) { return store_canonicalize(c); }
 int orc_update_hash(orc_ctx* c) { return store_update_hash(c); }
 int orc_fill_ghosts(orc_ctx* c) { return store_fill_ghosts(c); }

@@ -68,6 +68,9 @@ double orc_mass(const orc_ctx* c);
 
 /* LatticeStore ops (store.h:52-77) */
 int orc_insert(orc_ctx* c, const double pos[3], const double vel[3], unsigned long long tag);
+/* add disp[3i..3i+2] to the i-th valid interior slot atom (interior-id order);
+ * returns the number of atoms displaced (a harness feature: BASELINE config 2) */
+long orc_displace_interior(orc_ctx* c, const double* disp, long n);
 int orc_set_atom(orc_ctx* c, long long site, int clash_idx, const double pos[3], const double vel[3]);
 int orc_canonicalize(orc_ctx* c);
 int orc_update_hash(orc_ctx* c);

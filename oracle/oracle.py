@@ -82,6 +82,8 @@ def _load(kind: str):
         getattr(lib, name).argtypes = [P]
         getattr(lib, name).restype = D
     lib.orc_insert.argtypes = [P, dp, dp, C.c_ulonglong]
+    lib.orc_displace_interior.argtypes = [P, P, C.c_long]
+    lib.orc_displace_interior.restype = C.c_long
     lib.orc_set_atom.argtypes = [P, C.c_longlong, C.c_int, dp, dp]
     lib.orc_atom_count.argtypes = [P]
     lib.orc_atom_count.restype = C.c_long
@@ -227,6 +229,10 @@ class Sim:
         p = _dp(pos) if pos is not None else (None, None)
         v = _dp(vel) if vel is not None else (None, None)
         self._check(self.lib.orc_set_atom(self.h, site, clash_idx, p[0], v[0]))
+
+    def displace_interior(self, disp: np.ndarray) -> int:
+        d = np.ascontiguousarray(disp, dtype=np.float64)
+        return self.lib.orc_displace_interior(self.h, _ptr(d), len(d))
 
     def rehash(self):
         self._check(self.lib.orc_rehash(self.h))

@@ -168,6 +168,17 @@ int orc_set_atom(orc_ctx* c, long long site, int idx, const double p[3], const d
   });
 }
 
+long orc_displace_interior(orc_ctx* c, const double* disp, long n) {
+  long i = 0;
+  LatticeStore& s = c->store();
+  for_each_interior_id(s.box, [&](LatticeId id) {
+    AtomRecord& r = s.slots[static_cast<std::size_t>(id)];
+    if (!r.valid || i >= n) return;
+    r.position += Vec3{disp[3 * i], disp[3 * i + 1], disp[3 * i + 2]};
+    ++i;
+  });
+  return i;
+}
 int orc_canonicalize(orc_ctx* c) { return guard(c, [&] { c->store().canonicalize_positions(); }); }
 int orc_update_hash(orc_ctx* c) { return guard(c, [&] { c->store().update_hash(); }); }
 int orc_fill_ghosts(orc_ctx* c) { return guard(c, [&] { c->store().fill_ghosts(); }); }

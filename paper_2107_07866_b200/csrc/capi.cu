@@ -29,6 +29,9 @@ struct cbx_ctx {
   unsigned long long* d_defects = nullptr;
   std::vector<void*> allocs;
   cudaGraphExec_t step_graph = nullptr;
+  cudaGraphExec_t timed_graph = nullptr;
+  void* flush_buf = nullptr;
+  size_t flush_bytes = 0;
   bool use_graph = true;
   bool timing = false;
   cudaEvent_t ev[8]{};
@@ -233,24 +236,31 @@ void accumulate_timing(cbx_ctx* c, bool step) {
   c->t_ms[2] += ms;
 }
 
-void build_graph(cbx_ctx* c) {
-  if (c->step_graph) return;
+cudaGraphExec_t capture_step(cbx_ctx* c, bool with_events) {
   cudaGraph_t g;
+  cudaGraphExec_t exec = nullptr;
   const bool t = c->timing;
-  c->timing = false;
+  c->timing = with_events;
   const uint64_t l0 = c->launches;
   cuda_check(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal), "capture");
   seq_step(c);
   cuda_check(cudaStreamEndCapture(c->stream, &g), "end capture");
-  cuda_check(cudaGraphInstantiate(&c->step_graph, g, 0), "graph instantiate");
+  cuda_check(cudaGraphInstantiate(&exec, g, 0), "graph instantiate");
   cudaGraphDestroy(g);
   c->launches = l0;
   c->timing = t;
+  return exec;
+}
+
+void build_graph(cbx_ctx* c) {
+  if (!c->step_graph) c->step_graph = capture_step(c, false);
 }
 
 void drop_graph(cbx_ctx* c) {
   if (c->step_graph) cudaGraphExecDestroy(c->step_graph);
+  if (c->timed_graph) cudaGraphExecDestroy(c->timed_graph);
   c->step_graph = nullptr;
+  c->timed_graph = nullptr;
 }
 
 // ---- the store view ------------------------------------------------------
@@ -748,6 +758,7 @@ CBX_API void cbx_destroy(cbx_ctx* c) {
   drop_graph(c);
   if (c->stream) cudaStreamSynchronize(c->stream);
   for (void* p : c->allocs) cudaFree(p);
+  if (c->flush_buf) cudaFree(c->flush_buf);
   for (auto& e : c->ev)
     if (e) cudaEventDestroy(e);
   if (c->stream) cudaStreamDestroy(c->stream);
@@ -1045,6 +1056,42 @@ CBX_API cbx_status cbx_count_pairs(cbx_ctx* c, uint64_t out[2]) {
     raise_device_error(c, false);
   });
 }
+CBX_API cbx_status cbx_bench_steps(cbx_ctx* c, double dt, long nsteps, double flush_mb,
+                                   double out_ms[8]) {
+  return guarded(c, [&] {
+    cudaSetDevice(c->device);
+    check_cutoff(c);
+    sync_status(c);
+    c->hst.dt_next = dt;
+    c->hst.adaptive = 0;
+    write_status(c);
+    if (!c->timed_graph) c->timed_graph = capture_step(c, true);
+    const size_t fb = (size_t)(flush_mb * 1048576.0);
+    if (fb > c->flush_bytes) {
+      if (c->flush_buf) cudaFree(c->flush_buf);
+      cuda_check(cudaMalloc(&c->flush_buf, fb), "flush buffer");
+      c->flush_bytes = fb;
+    }
+    double acc[8] = {0};
+    for (long i = 0; i < nsteps; ++i) {
+      if (fb) cudaMemsetAsync(c->flush_buf, (int)(i & 0xff), fb, c->stream);  // evict L2
+      cuda_check(cudaGraphLaunch(c->timed_graph, c->stream), "graph launch");
+      c->launches += 16;
+      cuda_check(cudaEventSynchronize(c->ev[5]), "event sync");
+      float ms;
+      const int seg[6][2] = {{1, 2}, {2, 3}, {3, 4}, {0, 1}, {4, 5}, {0, 5}};
+      for (int k = 0; k < 6; ++k) {
+        cudaEventElapsedTime(&ms, c->ev[seg[k][0]], c->ev[seg[k][1]]);
+        acc[k] += ms;
+      }
+    }
+    acc[6] = (double)nsteps;
+    sync_status(c);
+    raise_device_error(c, true);
+    for (int k = 0; k < 8; ++k) out_ms[k] = acc[k];
+  });
+}
+
 CBX_API cbx_status cbx_kernel_launches(cbx_ctx* c, uint64_t* n) {
   *n = c->launches;
   return CBX_OK;

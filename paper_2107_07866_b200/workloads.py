@@ -1,0 +1,82 @@
+"""The BASELINE.json configurations as seeded synthetic workloads.
+
+BASELINE.json quotes five configurations (restated in SURVEY.md §8(d)).  No
+public dataset is involved: every initial state is generated on the host by
+the reference-compatible lattice/RNG code (init_bcc, sim.cpp:100-130) from a
+seed, plus -- for config 2 -- per-component uniform +-0.05 A displacements
+drawn with numpy's PCG64 (seed 12345) in interior-site order.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+
+@dataclass
+class Workload:
+    name: str
+    cells: tuple
+    temperature: float
+    dt: float
+    steps: int
+    displacement: float = 0.0
+    pka_kev: float = 0.0
+    pka_dir: tuple = (1, 3, 5)
+    seed: int = 12345
+    note: str = ""
+
+    @property
+    def atoms(self) -> int:
+        return 2 * self.cells[0] * self.cells[1] * self.cells[2]
+
+
+CONFIGS = {
+    "c1": Workload("c1", (20, 20, 20), 600.0, 1e-3, 100,
+                   note="BCC Fe 20^3 cells (16,000 atoms), 600 K, 100 x 1 fs"),
+    "c2": Workload("c2", (50, 50, 50), 600.0, 1e-3, 200, displacement=0.05,
+                   note="BCC Fe 50^3 cells (250,000 atoms), 600 K + U(-0.05,0.05) A, 200 x 1 fs"),
+    "c3": Workload("c3", (100, 100, 100), 600.0, 1e-4, 1000, pka_kev=10.0,
+                   note="BCC Fe 100^3 (2,000,000 atoms), 600 K, 10 keV PKA (1,3,5), 1000 x 0.1 fs"),
+    "c4": Workload("c4", (200, 200, 200), 600.0, 2e-4, 500, pka_kev=5.0,
+                   note="BCC Fe 200^3 (16,000,000 atoms), 600 K, 5 keV PKA, 500 x 0.2 fs"),
+    "c5": Workload("c5", (256, 256, 256), 600.0, 1e-3, 100, pka_kev=20.0,
+                   note="BCC Fe 256^3 per GPU (33,554,432 atoms), 600 K, 20 keV PKA, 100 x 1 fs"),
+}
+
+
+def displacements(w: Workload, n_atoms: int) -> np.ndarray:
+    """config 2's random displacements, one row per atom in interior-id order"""
+    if w.displacement <= 0.0:
+        return np.zeros((n_atoms, 3))
+    rng = np.random.Generator(np.random.PCG64(w.seed))
+    return rng.uniform(-w.displacement, w.displacement, size=(n_atoms, 3))
+
+
+def pka_site_id(w: Workload, ghost_width: int) -> int:
+    """corner site of the centre cell (sim.cpp:165-170)"""
+    bx, by, bz = w.cells
+    g = ghost_width
+    tx, ty = bx + 2 * g, by + 2 * g
+    cx, cy, cz = bx // 2, by // 2, bz // 2
+    return ((g + cz) * ty + (g + cy)) * 2 * tx + 2 * (g + cx)
+
+
+def build_device_state(w: Workload, potential, device: int = 0, stencil: str = "newton3"):
+    """A DeviceStore in the workload's initial state: lattice + MB velocities,
+    displacements, rehash, forces, measure (the Simulation constructor path)."""
+    from .engine import DeviceStore, SimConfig, make_box
+    cfg = SimConfig(box_x=w.cells[0], box_y=w.cells[1], box_z=w.cells[2],
+                    temperature=w.temperature, seed=w.seed)
+    box, _ = make_box(cfg, potential)
+    dev = DeviceStore(box, potential, device=device, stencil=stencil)
+    n = dev.init_bcc(w.temperature, w.seed, potential.atomic_number)
+    if w.displacement > 0.0:
+        s = dev.download()
+        m = s.valid.astype(bool) & ~s.ghost.astype(bool)
+        s.pos[m] += displacements(w, n)
+        dev.upload(s)
+        dev.rehash()
+    dev.eval_forces()
+    dev.measure()
+    return dev, n
