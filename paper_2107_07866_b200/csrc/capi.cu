@@ -166,8 +166,11 @@ void write_status(cbx_ctx* c) {
 }
 
 // ---- launch sequences ----------------------------------------------------
+bool g_capturing = false;
 void ev_mark(cbx_ctx* c, int i) {
-  if (c->timing) cudaEventRecord(c->ev[i], c->stream);
+  // inside a capture the record must become an external event-record node
+  if (c->timing)
+    cudaEventRecordWithFlags(c->ev[i], c->stream, g_capturing ? cudaEventRecordExternal : 0);
 }
 
 void seq_fill_ghosts(cbx_ctx* c) {
@@ -243,7 +246,9 @@ cudaGraphExec_t capture_step(cbx_ctx* c, bool with_events) {
   c->timing = with_events;
   const uint64_t l0 = c->launches;
   cuda_check(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal), "capture");
+  g_capturing = true;
   seq_step(c);
+  g_capturing = false;
   cuda_check(cudaStreamEndCapture(c->stream, &g), "end capture");
   cuda_check(cudaGraphInstantiate(&exec, g, 0), "graph instantiate");
   cudaGraphDestroy(g);
