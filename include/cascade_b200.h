@@ -100,7 +100,8 @@ typedef struct {
 /* kernel selection for the two EAM stencil passes */
 typedef enum {
   CBX_STENCIL_NEWTON3 = 0, /* half list, ordered reduction into owners (default) */
-  CBX_STENCIL_FULL = 1     /* full list, owner computes (no atomics, deterministic) */
+  CBX_STENCIL_FULL = 1,     /* full list, owner computes (no atomics, deterministic) */
+  CBX_STENCIL_REFERENCE = 2 /* half list with the reference's literal arithmetic (checker) */
 } cbx_stencil;
 
 /* ---- version / build ---------------------------------------------------- */

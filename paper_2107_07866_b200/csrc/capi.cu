@@ -38,6 +38,8 @@ struct cbx_ctx {
   double t_ms[8]{};
   uint64_t launches = 0;
   int n_ghost = 0;
+  bool fast_ok = true;
+  double band = 0.0;
 
   template <class T>
   T* alloc(size_t n) {
@@ -179,7 +181,8 @@ void seq_fill_ghosts(cbx_ctx* c) {
   c->launches += 2;
 }
 void seq_density(cbx_ctx* c) {
-  if (c->mode == CBX_STENCIL_NEWTON3)
+  cudaMemsetAsync(c->P.work, 0, sizeof(int), c->stream);
+  if (c->mode != CBX_STENCIL_FULL)
     cudaMemsetAsync(c->P.rho, 0, c->S * sizeof(double), c->stream);
   launch_clash_zero(c->P, 0, c->stream);
   launch_density(c->P, c->mode, c->stream);
@@ -191,7 +194,8 @@ void seq_embed(cbx_ctx* c) {
   c->launches += 2;
 }
 void seq_force(cbx_ctx* c) {
-  if (c->mode == CBX_STENCIL_NEWTON3)
+  cudaMemsetAsync(c->P.work + 1, 0, sizeof(int), c->stream);
+  if (c->mode != CBX_STENCIL_FULL)
     cudaMemsetAsync(c->P.frc, 0, 3 * c->S * sizeof(double), c->stream);
   launch_clash_zero(c->P, 1, c->stream);
   launch_force(c->P, c->mode, c->stream);
@@ -363,6 +367,7 @@ void do_upload(cbx_ctx* c, const cbx_store* s) {
   c->hst.n_ovl = 0;
   write_status(c);
   seq_fill_ghosts(c);
+  launch_uf_refresh(c->P, c->stream);
   sync_status(c);
   raise_device_error(c, false);
 }
@@ -449,6 +454,59 @@ void do_download(cbx_ctx* c, cbx_store* s) {
     if (s->clash_df) s->clash_df[i] = dd[i];
     if (s->clash_tag) s->clash_tag[i] = tt[i];
   }
+}
+
+// fast-path tables and the fp32 filter band (stencil_fast.cuh)
+void setup_fast(cbx_ctx* c) {
+  KP& P = c->P;
+  const Spline& zr = c->pot.zr;
+  const Spline& de = c->pot.dens;
+  c->fast_ok = zr.x0 == de.x0 && zr.h == de.h && zr.nseg() == de.nseg();
+  const int n = (int)de.nseg();
+  auto norm = [](const double* g, double h, double out[4]) {  // t = s h
+    out[0] = g[0] * h * h * h;
+    out[1] = g[1] * h * h;
+    out[2] = g[2] * h;
+    out[3] = g[3];
+  };
+  auto pad = [](const double in[4], double out[4]) {  // p(s + 1)
+    out[0] = in[0];
+    out[1] = 3.0 * in[0] + in[1];
+    out[2] = 3.0 * in[0] + 2.0 * in[1] + in[2];
+    out[3] = in[0] + in[1] + in[2] + in[3];
+  };
+  std::vector<double> fd(4 * (n + 1)), ff(8 * (n + 1));
+  for (int i = 0; i < n; ++i) {
+    norm(&de.seg[7 * i], de.h, &fd[4 * i]);
+    norm(&de.seg[7 * i], de.h, &ff[8 * i + 4]);
+    if (c->fast_ok) norm(&zr.seg[7 * i], zr.h, &ff[8 * i]);
+  }
+  pad(&fd[4 * (n - 1)], &fd[4 * n]);
+  pad(&ff[8 * (n - 1)], &ff[8 * n]);
+  pad(&ff[8 * (n - 1) + 4], &ff[8 * n + 4]);
+  double* dfd = c->alloc<double>(fd.size());
+  double* dff = c->alloc<double>(ff.size());
+  cuda_check(cudaMemcpy(dfd, fd.data(), fd.size() * 8, cudaMemcpyHostToDevice), "fast table");
+  cuda_check(cudaMemcpy(dff, ff.data(), ff.size() * 8, cudaMemcpyHostToDevice), "fast table");
+  P.fd.rec = dfd;
+  P.fd.ih = 1.0 / de.h;
+  P.fd.c0 = -de.x0 / de.h;
+  P.fd.nseg = n;
+  P.ff = P.fd;
+  P.ff.rec = dff;
+  // fp32 filter band: |r2_f32 - r2_exact| <= err for coordinates below
+  // maxc (two roundings to fp32, exact fp32 difference, three fp32 ops)
+  const double maxc = (std::max(std::max(c->G.tx, c->G.ty), c->G.tz) + 4) * c->G.a0;
+  const double ulp = std::ldexp(1.0, std::ilogb(maxc) - 23);
+  const double cut2 = P.cut2, dmax = std::sqrt(cut2) + 1.0;
+  const double err = 2.0 * dmax * std::sqrt(3.0) * ulp + 3.0 * ulp * ulp +
+                     4.0 * std::ldexp(1.0, -23) * (cut2 + 1.0);
+  const double band = 8.0 * err + 1e-9;
+  P.band_hi = std::nextafter((float)(cut2 + band), 1e30f);
+  P.band_lo = std::nextafter((float)(cut2 - band), -1e30f);
+  const double x0 = std::max(zr.x0, de.x0);
+  P.guard_r2 = x0 * x0 * 1.000001;
+  c->band = band;
 }
 
 void check_cutoff(cbx_ctx* c) {
@@ -723,7 +781,7 @@ CBX_API cbx_status cbx_create(const cbx_box* box, const cbx_potential* pot,
     P.cutoff = pot->cutoff;
     P.cut2 = pot->cutoff * pot->cutoff;
     P.mass = pot->mass;
-    const int np = std::max(eam_blocks(P), embed_blocks(P));
+    const int np = std::max(std::max(eam_blocks(P), embed_blocks(P)), 4 * 148 * 16);
     P.n_part = np;
     P.part_emb = c->alloc<double>(np);
     P.part_pair = c->alloc<double>(np);
@@ -733,6 +791,10 @@ CBX_API cbx_status cbx_create(const cbx_box* box, const cbx_potential* pot,
     cudaMemset(P.part_pair, 0, np * sizeof(double));
     cudaMemset(P.part_ke, 0, np * sizeof(double));
     cudaMemset(P.part_vmax, 0, np * sizeof(double));
+    P.uf = c->alloc<float4>(S);
+    P.work = c->alloc<int>(4);
+    cudaMemset(P.work, 0, 4 * sizeof(int));
+    setup_fast(c.get());
     P.st = c->alloc<DevStatus>(1);
     c->d_defects = c->alloc<unsigned long long>(4);
     // empty store: every slot vacant
@@ -743,6 +805,8 @@ CBX_API cbx_status cbx_create(const cbx_box* box, const cbx_potential* pot,
     cudaMemset(P.frc, 0, 3 * S * sizeof(double));
     cudaMemset(P.tag, 0, S * sizeof(unsigned long long));
     cudaMemset(P.head, 0xff, S * sizeof(int));
+    launch_uf_refresh(P, c->stream);
+    P.n_pair_part = pair_partials(P, c->mode);
     c->hst = DevStatus{};
     c->hst.dt_next = 1e-3;
     c->hst.dt_max = 1e-3;
@@ -772,10 +836,14 @@ CBX_API void cbx_destroy(cbx_ctx* c) {
 
 CBX_API cbx_status cbx_set_stencil(cbx_ctx* c, cbx_stencil mode) {
   return guarded(c, [&] {
-    if (mode != CBX_STENCIL_NEWTON3 && mode != CBX_STENCIL_FULL)
+    if (mode != CBX_STENCIL_NEWTON3 && mode != CBX_STENCIL_FULL &&
+        mode != CBX_STENCIL_REFERENCE)
       raise(CBX_INVALID_ARGUMENT, "unknown stencil mode");
+    if (mode != CBX_STENCIL_REFERENCE && !c->fast_ok)
+      raise(CBX_INVALID_ARGUMENT, "fast stencils need z(r) and rho(r) on one grid");
     if (c->mode != mode) drop_graph(c);
     c->mode = mode;
+    c->P.n_pair_part = pair_partials(c->P, mode);
   });
 }
 

@@ -10,6 +10,14 @@ namespace cbx {
 
 // spline table on the device: the reference's 7-coefficient segments
 // (spline.h:19-22) plus the evaluation constants
+// fast-path spline records: 32-byte aligned, normalised s = (r - x0)/h - i,
+// segment nseg padded with the last segment re-expanded at s + 1
+struct FastTab {
+  const double* rec;  // density: 4 doubles/segment (A B C D); force: 8 (z A-D, rho A-D)
+  double ih, c0;      // u = r*ih + c0
+  int nseg;
+};
+
 struct Tab {
   const double* seg;  // 7 doubles per segment
   double x0, h, ih, xl;
@@ -61,6 +69,12 @@ struct DevStatus {
 
 struct KP {
   Geo G;
+  float4* uf;      // fp32 shadow (x, y, z, owner-or--1) for the candidate filter
+  int* work;       // persistent-kernel work counters (zeroed per launch)
+  FastTab fd, ff;  // density / force fast tables
+  float band_hi, band_lo;  // fp32 r^2 filter: reject above hi, exact test in [lo, hi]
+  double guard_r2;         // below: overlap / short-range guard path
+  int n_pair_part;         // partials written by the force pass
   double accel, mv2;  // units::accel_factor, units::mv2_to_ev (units.h:17-24)
   long long S;  // 2*NC sites
   double4* pdf;  // x y z dF
@@ -152,6 +166,8 @@ void launch_count_defects(const KP& P, unsigned long long* out, cudaStream_t s);
 void upload_offsets(const int* half_dev[2], const int half_n[2], const int* full_dev[2],
                     const int full_n[2], const long long* full_flat[2], cudaStream_t s);
 int eam_blocks(const KP& P);
+int pair_partials(const KP& P, int mode);
+void launch_uf_refresh(const KP& P, cudaStream_t s);
 int embed_blocks(const KP& P);
 
 }  // namespace cbx

@@ -25,6 +25,7 @@ namespace cbx {
 // exceeds every cutoff: no separate validity load in the stencil loops.
 constexpr double kVacant = 1.0e30;
 constexpr double kVacantTest = 1.0e29;
+constexpr float kVacantF = 1.0e18f;  // fp32 shadow of a vacant site
 constexpr double kOverlapR2 = 1e-12;  // forces.cpp:14
 constexpr int kMaxOffsets = 1024;     // per list, constant memory
 constexpr int kMaxOverlapRecords = 64;

@@ -423,14 +423,20 @@ __global__ void __launch_bounds__(256) k_clash(KP P) {
   }
 }
 
+#include "stencil_fast.cuh"
+
 // ------------------------------------------------------------- launchers
+// mode: 0 fast half list (Newton-3), 1 fast full list, 2 reference-literal half list
 void launch_density(const KP& P, int mode, cudaStream_t s) {
-  if (mode) k_density<true><<<eam_blocks(P), 256, 0, s>>>(P);
-  else k_density<false><<<eam_blocks(P), 256, 0, s>>>(P);
+  if (mode == 2) k_density<false><<<eam_blocks(P), 256, 0, s>>>(P);
+  else launch_density_fast(P, mode, fast_grid(P, false, mode), s);
 }
 void launch_force(const KP& P, int mode, cudaStream_t s) {
-  if (mode) k_force<true><<<eam_blocks(P), 256, 0, s>>>(P);
-  else k_force<false><<<eam_blocks(P), 256, 0, s>>>(P);
+  if (mode == 2) k_force<false><<<eam_blocks(P), 256, 0, s>>>(P);
+  else launch_force_fast(P, mode, fast_grid(P, true, mode), s);
+}
+int pair_partials(const KP& P, int mode) {
+  return mode == 2 ? eam_blocks(P) : 4 * fast_grid(P, true, mode);
 }
 void launch_embed(const KP& P, cudaStream_t s) {
   k_embed<<<embed_blocks(P), 256, 0, s>>>(P);

@@ -21,6 +21,8 @@
 
 namespace cbx {
 
+__device__ __forceinline__ int eam_blocks_dev(const KP& P) { return (int)((P.G.NI + 127) / 128); }
+
 __device__ __forceinline__ double half_kick(const KP& P, double dt) {
   return xdiv(xmul(xmul(0.5, dt), P.accel), P.mass);  // sim.cpp:250
 }
@@ -84,8 +86,10 @@ __global__ void __launch_bounds__(256) k_kick_drift(KP P, int move) {
     P.mv.vz[m] = vz;
     P.mv.tag[m] = P.tag[d];
     P.pdf[d] = make_double4(kVacant, kVacant, kVacant, 0.0);
+    P.uf[d] = make_float4(kVacantF, kVacantF, kVacantF, __int_as_float(-1));
   } else {
     P.pdf[d] = p;
+    P.uf[d] = make_float4((float)p.x, (float)p.y, (float)p.z, __int_as_float(-1));
   }
 }
 
@@ -281,6 +285,8 @@ __global__ void __launch_bounds__(1024) k_rehash(KP P) {
         promote = 1;
         const int q = X.pl[p];
         if (q >= 0) {
+          P.uf[dr] = make_float4((float)P.cl.px[q], (float)P.cl.py[q], (float)P.cl.pz[q],
+                                 __int_as_float(-1));
           P.pdf[dr] = make_double4(P.cl.px[q], P.cl.py[q], P.cl.pz[q], 0.0);
           P.vel[dr] = P.cl.vx[q];
           P.vel[S + dr] = P.cl.vy[q];
@@ -288,6 +294,8 @@ __global__ void __launch_bounds__(1024) k_rehash(KP P) {
           P.tag[dr] = P.cl.tag[q];
         } else {
           const int m = -q - 1;
+          P.uf[dr] = make_float4((float)P.mv.px[m], (float)P.mv.py[m], (float)P.mv.pz[m],
+                                 __int_as_float(-1));
           P.pdf[dr] = make_double4(P.mv.px[m], P.mv.py[m], P.mv.pz[m], 0.0);
           P.vel[dr] = P.mv.vx[m];
           P.vel[S + dr] = P.mv.vy[m];
@@ -360,12 +368,15 @@ __global__ void k_ghost_fill(KP P) {
   const double4 p = P.pdf[src];
   if (p.x >= kVacantTest) {
     P.pdf[dst] = make_double4(kVacant, kVacant, kVacant, 0.0);
+    P.uf[dst] = make_float4(kVacantF, kVacantF, kVacantF, __int_as_float(src));
     return;
   }
   const signed char* k = P.gh_k + 3 * g;
-  P.pdf[dst] = make_double4(xadd(p.x, xmul((double)k[0], P.G.lx)),
-                            xadd(p.y, xmul((double)k[1], P.G.ly)),
-                            xadd(p.z, xmul((double)k[2], P.G.lz)), p.w);
+  const double4 q = make_double4(xadd(p.x, xmul((double)k[0], P.G.lx)),
+                                 xadd(p.y, xmul((double)k[1], P.G.ly)),
+                                 xadd(p.z, xmul((double)k[2], P.G.lz)), p.w);
+  P.pdf[dst] = q;
+  P.uf[dst] = make_float4((float)q.x, (float)q.y, (float)q.z, __int_as_float(src));
 }
 
 // --------------------------------------------------- ghost clash images
@@ -481,6 +492,20 @@ __global__ void __launch_bounds__(1024) k_clash_images(KP P) {
   if (threadIdx.x == 0) P.st->n_clash = total;
 }
 
+// fp32 shadow of every site from pdf (after a host upload)
+__global__ void k_uf_refresh(KP P) {
+  const long long d = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (d >= P.S) return;
+  const double4 p = P.pdf[d];
+  const int t = P.tgt[d];
+  const float w = __int_as_float(t == d ? -1 : t);
+  P.uf[d] = p.x >= kVacantTest ? make_float4(kVacantF, kVacantF, kVacantF, w)
+                               : make_float4((float)p.x, (float)p.y, (float)p.z, w);
+}
+void launch_uf_refresh(const KP& P, cudaStream_t s) {
+  k_uf_refresh<<<(int)((P.S + 255) / 256), 256, 0, s>>>(P);
+}
+
 // zero the accumulators of the clash records: what 0 density, 1 force
 __global__ void k_clash_zero(KP P, int what) {
   const int n = P.st->n_clash;
@@ -551,7 +576,8 @@ __global__ void k_clash_kick2(KP P, int kick) {
 // ------------------------------------------------------------- finalize
 // deterministic sums of the per-block / per-record partials into StepState
 __global__ void __launch_bounds__(1024) k_finalize(KP P, int stepping, int energies,
-                                                   int n_eam, int n_emb) {
+                                                   int n_pairp, int n_emb) {
+  const int n_eam = eam_blocks_dev(P);
   __shared__ double sh[32];
   DevStatus* st = P.st;
   if (st->err || st->n_ovl) return;
@@ -559,7 +585,7 @@ __global__ void __launch_bounds__(1024) k_finalize(KP P, int stepping, int energ
   if (energies) {
     double a = 0.0, b = 0.0;
     for (int i = threadIdx.x; i < n_emb; i += blockDim.x) a += P.part_emb[i];
-    for (int i = threadIdx.x; i < n_eam; i += blockDim.x) b += P.part_pair[i];
+    for (int i = threadIdx.x; i < n_pairp; i += blockDim.x) b += P.part_pair[i];
     for (int i = threadIdx.x; i < nc; i += blockDim.x) {
       a += P.cl.e_emb[i];
       b += P.cl.e_pair[i];
@@ -641,7 +667,7 @@ void launch_kick2(const KP& P, int kick, cudaStream_t s) {
   k_clash_kick2<<<8, 256, 0, s>>>(P, kick);
 }
 void launch_finalize(const KP& P, int stepping, int energies, cudaStream_t s) {
-  k_finalize<<<1, 1024, 0, s>>>(P, stepping, energies, eam_blocks(P), embed_blocks(P));
+  k_finalize<<<1, 1024, 0, s>>>(P, stepping, energies, P.n_pair_part, embed_blocks(P));
 }
 void launch_count_defects(const KP& P, unsigned long long* out, cudaStream_t s) {
   k_count_defects<<<eam_blocks(P), 256, 0, s>>>(P, out);

@@ -200,7 +200,7 @@ class DeviceStore:
         check(rc, self.h)
 
     def set_stencil(self, mode: str):
-        self._check(self.lib.cbx_set_stencil(self.h, {"newton3": 0, "full": 1}[mode]))
+        self._check(self.lib.cbx_set_stencil(self.h, {"newton3": 0, "full": 1, "reference": 2}[mode]))
 
     # --- store transfer ----------------------------------------------------
     def upload(self, s) -> None:

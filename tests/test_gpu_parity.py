@@ -65,7 +65,7 @@ def test_init_bcc_bit_identical(cuda, tables):
 
 
 # ----------------------------------------------------------- force engine
-@pytest.mark.parametrize("stencil", ["newton3", "full"])
+@pytest.mark.parametrize("stencil", ["newton3", "full", "reference"])
 @pytest.mark.parametrize("temp", [0.0, 600.0])
 def test_eval_forces_lattice(cuda, tables, stencil, temp):
     from oracle import oracle
@@ -132,12 +132,13 @@ def _clash_scenario(path, a0=None):
     return ref
 
 
+@pytest.mark.parametrize("stencil", ["newton3", "full", "reference"])
 @pytest.mark.parametrize("table", ["baseline", "synthetic"])
-def test_clash_buckets_interior_boundary_stacked(cuda, tables, table):
+def test_clash_buckets_interior_boundary_stacked(cuda, tables, table, stencil):
     ref = _clash_scenario(tables[table])
     s0 = ref.store()
     assert (s0.clash_ghost == 0).sum() >= 4
-    dev = device_for(ref, tables[table])
+    dev = device_for(ref, tables[table], stencil)
     # the device's own ghost images of the clash buckets equal fill_ghosts'
     assert structure(s0)[1] == structure(dev.download())[1]
     e_ref = ref.eval_forces()
@@ -146,14 +147,15 @@ def test_clash_buckets_interior_boundary_stacked(cuda, tables, table):
     assert_store_parity(ref.store(), dev.download(), what=table)
 
 
+@pytest.mark.parametrize("stencil", ["newton3", "full"])
 @pytest.mark.parametrize("box", [(1, 1, 1), (2, 3, 1), (3, 3, 3), (4, 2, 5)])
-def test_tiny_boxes_many_images(cuda, tables, box):
+def test_tiny_boxes_many_images(cuda, tables, box, stencil):
     """boxes thinner than the ghost shell: several images per atom, self
     images (acceptance.cpp:100-130 sweeps 1..6^3)"""
     from oracle import oracle
     ref = oracle.Sim(tables["synthetic"], box=box, temperature=300.0, seed=7)
     ref.step(1e-3, 2)
-    dev = device_for(ref, tables["synthetic"])
+    dev = device_for(ref, tables["synthetic"], stencil)
     e_ref, e_dev = ref.eval_forces(), dev.eval_forces()
     assert close(e_ref[0], e_dev[0], 1e-9) and close(e_ref[1], e_dev[1], 1e-9), (e_ref, e_dev)
     assert_store_parity(ref.store(), dev.download(), what=str(box))
@@ -250,7 +252,7 @@ def test_overlap_names_both_tags(cuda, tables):
 
 
 # ------------------------------------------------------------ step loop
-@pytest.mark.parametrize("stencil", ["newton3", "full"])
+@pytest.mark.parametrize("stencil", ["newton3", "full", "reference"])
 def test_trajectory_config1_shape(cuda, tables, stencil):
     """BASELINE config 1 shape (600 K, dt 1 fs) on a 10^3 box: 100 steps,
     state checked every 25 steps; energies and drift against the oracle"""
@@ -274,7 +276,8 @@ def test_trajectory_config1_shape(cuda, tables, stencil):
     assert abs(drift_dev - drift_ref) <= 0.01 * abs(drift_ref) + 1e-9 * abs(etot(e0))
 
 
-def test_cascade_clash_and_defects(cuda, tables):
+@pytest.mark.parametrize("stencil", ["newton3", "full"])
+def test_cascade_clash_and_defects(cuda, tables, stencil):
     """PKA cascade on a 10^3 box: off-lattice atoms go through the device
     clash list; hash ids, bucket membership/order and Wigner-Seitz counts
     match the oracle at every checkpoint"""
@@ -282,7 +285,7 @@ def test_cascade_clash_and_defects(cuda, tables):
     ref = oracle.Sim(tables["baseline"], box=(10, 10, 10), temperature=600.0, seed=12345,
                      pka_energy_kev=1.0, pka_site=(5, 5, 5))
     ref.step(1e-3, 10)
-    dev = device_for(ref, tables["baseline"])
+    dev = device_for(ref, tables["baseline"], stencil)
     dev.set_state(ref.state())
     ref.inject_pka()
     st = ref.state()
@@ -327,3 +330,48 @@ def test_simulation_facade(cuda, tables):
         assert close(a[k], b[k], 1e-12), k
     assert sim.atom_count() == 432
     assert np.abs(sim.total_momentum()).max() < 1e-8
+
+
+def test_near_cutoff_pairs_exact(cuda, tables):
+    """pairs placed within 1e-12 A of the cutoff on both sides: the fp32
+    filter must hand them to the exact test (in-cutoff set bit-identical)"""
+    from oracle import oracle
+    ref = oracle.Sim(tables["baseline"], box=(5, 5, 5), init_lattice=False)
+    _, a, g = ref.box
+    base = np.array([4.0 * a, 4.0 * a, 4.0 * a])
+    rc = 5.6
+    tag = 0
+    for k, dr in enumerate([-1e-12, -1e-14, 0.0, 1e-14, 1e-12, 1e-9]):
+        p0 = base + np.array([0.0, 0.37 * a * (k % 3), 0.41 * a * (k // 3)])
+        ref.insert(p0, tag)
+        ref.insert(p0 + np.array([rc + dr, 0.0, 0.0]), tag + 1)
+        tag += 2
+    ref.fill_ghosts()
+    for stencil in ("newton3", "full", "reference"):
+        r2 = oracle.Sim(tables["baseline"], box=(5, 5, 5), init_lattice=False)
+        s = ref.store()
+        dev = device_for(ref, tables["baseline"], stencil)
+        e_ref = ref.eval_forces()
+        e_dev = dev.eval_forces()
+        assert close(e_ref[1], e_dev[1], 1e-12), (stencil, e_ref, e_dev)
+        a_, b_ = by_tag(ref.store()), by_tag(dev.download())
+        for t in a_:
+            assert (a_[t][3] == 0.0) == (b_[t][3] == 0.0), (stencil, t)
+            assert close(a_[t][3], b_[t][3]), (stencil, t)
+
+
+def test_bench_steps_timed_graph(cuda, tables):
+    """the benchmark loop (timed graph with event nodes, L2 flush) advances
+    the same trajectory as plain steps"""
+    import ctypes as C
+    from oracle import oracle
+    from paper_2107_07866_b200 import _lib
+    ref = oracle.Sim(tables["baseline"], box=(8, 8, 8), temperature=600.0, seed=5)
+    dev = device_for(ref, tables["baseline"])
+    dev.set_state(ref.state())
+    out = (C.c_double * 8)()
+    _lib.check(dev.lib.cbx_bench_steps(dev.h, 1e-3, 10, 64.0, out), dev.h)
+    ref.step(1e-3, 10)
+    assert out[6] == 10 and out[5] > 0 and out[2] > 0 and out[0] > 0
+    assert dev.state()["step"] == ref.state()["step"]
+    assert_store_parity(ref.store(), dev.download(), pos_tol=1e-9, rel=1e-8)
