@@ -1116,19 +1116,22 @@ CBX_API cbx_status cbx_count_pairs(cbx_ctx* c, uint64_t out[2]) {
     c->hst.cnt_cand = 0;
     c->hst.cnt_pair = 0;
     write_status(c);
+    // one counting pass of the reference-literal half-list kernel (same
+    // candidate / in-cutoff pair sets as every stencil), then a clean density
     KP saved = c->P;
     c->P.count_pairs = 1;
-    launch_density(c->P, c->mode, c->stream);
+    cudaMemsetAsync(c->P.rho, 0, c->S * sizeof(double), c->stream);
+    launch_density(c->P, CBX_STENCIL_REFERENCE, c->stream);
     c->P = saved;
     sync_status(c);
     out[0] = c->hst.cnt_cand;
     out[1] = c->hst.cnt_pair;
-    // the extra pass accumulated into rho: recompute it cleanly
     seq_density(c);
     sync_status(c);
     raise_device_error(c, false);
   });
 }
+
 CBX_API cbx_status cbx_bench_steps(cbx_ctx* c, double dt, long nsteps, double flush_mb,
                                    double out_ms[8]) {
   return guarded(c, [&] {
