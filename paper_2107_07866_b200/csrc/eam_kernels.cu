@@ -20,6 +20,7 @@
 // decisions are bit-identical; the pair arithmetic after the cutoff test is
 // ordinary fp64 (within 1e-10 of the reference, tests/test_gpu_parity.py).
 #include <cstdio>
+#include <cstdlib>
 
 #include "cbx_device.cuh"
 
