@@ -456,6 +456,11 @@ void do_download(cbx_ctx* c, cbx_store* s) {
   }
 }
 
+// the parameter block's device copy (guard paths take it by pointer)
+void sync_kp(cbx_ctx* c) {
+  cuda_check(cudaMemcpy(c->P.dself, &c->P, sizeof(KP), cudaMemcpyHostToDevice), "kp upload");
+}
+
 // fast-path tables and the fp32 filter band (stencil_fast.cuh)
 void setup_fast(cbx_ctx* c) {
   KP& P = c->P;
@@ -506,6 +511,9 @@ void setup_fast(cbx_ctx* c) {
   P.band_lo = std::nextafter((float)(cut2 - band), -1e30f);
   const double x0 = std::max(zr.x0, de.x0);
   P.guard_r2 = x0 * x0 * 1.000001;
+  // fp64 r^2 by FMA vs the reference's r^2: a few ulp of r^2 apart
+  P.cut2_lo = cut2 * (1.0 - 1e-12);
+  P.cut2_hi = cut2 * (1.0 + 1e-12);
   c->band = band;
 }
 
@@ -676,17 +684,32 @@ CBX_API cbx_status cbx_create(const cbx_box* box, const cbx_potential* pot,
     for (int par = 0; par < 2; ++par)
       if ((int)c->offs.full[par].size() > kMaxOffsets)
         raise(CBX_INVALID_ARGUMENT, "offset index too large for the device tables");
-    // device offset deltas
+    // device offset deltas, ordered by lattice distance: sites within the
+    // potential cutoff first ("inner"), index-skin sites after (stencil_fast.cuh)
     std::vector<int> hd[2], fd[2];
     std::vector<long long> ff[2];
+    int hin[2] = {0, 0}, fin[2] = {0, 0};
     for (int par = 0; par < 2; ++par) {
       auto delta = [&](const Offset& o) {
         const int q = par ^ o.cross;
         return (int)((long long)(q - par) * G.NC + (long long)o.dz * G.txy +
                      (long long)o.dy * G.tx + o.dx);
       };
-      for (const Offset& o : c->offs.half[par]) hd[par].push_back(delta(o));
-      for (const Offset& o : c->offs.full[par]) {
+      auto dist2 = [&](const Offset& o) {
+        const double h = o.cross ? (par ? -0.5 : 0.5) : 0.0;
+        const double x = o.dx + h, y = o.dy + h, z = o.dz + h;
+        return (x * x + y * y + z * z) * box->a0 * box->a0;
+      };
+      auto order = [&](std::vector<Offset> v, int& nin) {
+        std::stable_sort(v.begin(), v.end(),
+                         [&](const Offset& a, const Offset& b) { return dist2(a) < dist2(b); });
+        nin = 0;
+        for (const Offset& o : v)
+          if (dist2(o) <= pot->cutoff * pot->cutoff) ++nin;
+        return v;
+      };
+      for (const Offset& o : order(c->offs.half[par], hin[par])) hd[par].push_back(delta(o));
+      for (const Offset& o : order(c->offs.full[par], fin[par])) {
         fd[par].push_back(delta(o));
         ff[par].push_back(o.flat);
       }
@@ -696,7 +719,7 @@ CBX_API cbx_status cbx_create(const cbx_box* box, const cbx_potential* pot,
     const long long* fl[2] = {ff[0].data(), ff[1].data()};
     const int hn[2] = {(int)hd[0].size(), (int)hd[1].size()};
     const int fn[2] = {(int)fd[0].size(), (int)fd[1].size()};
-    upload_offsets(hp, hn, fp, fn, fl, c->stream);
+    upload_offsets(hp, hn, fp, fn, fl, hin, fin, c->stream);
     cuda_check(cudaStreamSynchronize(c->stream), "offset upload");
     // ghost list and owner map
     const long long S = c->S;
@@ -796,6 +819,7 @@ CBX_API cbx_status cbx_create(const cbx_box* box, const cbx_potential* pot,
     cudaMemset(P.work, 0, 4 * sizeof(int));
     setup_fast(c.get());
     P.st = c->alloc<DevStatus>(1);
+    P.dself = c->alloc<KP>(1);
     c->d_defects = c->alloc<unsigned long long>(4);
     // empty store: every slot vacant
     std::vector<double4> vac(S, make_double4(kVacant, kVacant, kVacant, 0.0));
@@ -807,6 +831,7 @@ CBX_API cbx_status cbx_create(const cbx_box* box, const cbx_potential* pot,
     cudaMemset(P.head, 0xff, S * sizeof(int));
     launch_uf_refresh(P, c->stream);
     P.n_pair_part = pair_partials(P, c->mode);
+    sync_kp(c.get());
     c->hst = DevStatus{};
     c->hst.dt_next = 1e-3;
     c->hst.dt_max = 1e-3;
@@ -844,6 +869,7 @@ CBX_API cbx_status cbx_set_stencil(cbx_ctx* c, cbx_stencil mode) {
     if (c->mode != mode) drop_graph(c);
     c->mode = mode;
     c->P.n_pair_part = pair_partials(c->P, mode);
+    sync_kp(c);
   });
 }
 

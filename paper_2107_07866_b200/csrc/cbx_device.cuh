@@ -74,6 +74,8 @@ struct KP {
   FastTab fd, ff;  // density / force fast tables
   float band_hi, band_lo;  // fp32 r^2 filter: reject above hi, exact test in [lo, hi]
   double guard_r2;         // below: overlap / short-range guard path
+  double cut2_lo, cut2_hi; // fp64 (FMA) r^2 decides outside [lo, hi]; exact r^2 inside
+  struct KP* dself;        // this parameter block in device memory (guard paths)
   int n_pair_part;         // partials written by the force pass
   double accel, mv2;  // units::accel_factor, units::mv2_to_ev (units.h:17-24)
   long long S;  // 2*NC sites
@@ -164,7 +166,8 @@ void launch_kick2(const KP& P, int kick, cudaStream_t s);
 void launch_finalize(const KP& P, int stepping, int energies, cudaStream_t s);
 void launch_count_defects(const KP& P, unsigned long long* out, cudaStream_t s);
 void upload_offsets(const int* half_dev[2], const int half_n[2], const int* full_dev[2],
-                    const int full_n[2], const long long* full_flat[2], cudaStream_t s);
+                    const int full_n[2], const long long* full_flat[2], const int half_nin[2],
+                    const int full_nin[2], cudaStream_t s);
 int eam_blocks(const KP& P);
 int pair_partials(const KP& P, int mode);
 void launch_uf_refresh(const KP& P, cudaStream_t s);

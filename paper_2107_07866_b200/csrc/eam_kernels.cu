@@ -28,12 +28,17 @@ namespace cbx {
 
 __constant__ int c_half_n[2];
 __constant__ int c_full_n[2];
+__constant__ int c_half_nin[2];  // leading offsets with lattice distance <= cutoff
+__constant__ int c_full_nin[2];
 __constant__ int c_half[2][kMaxOffsets];
 __constant__ int c_full[2][kMaxOffsets];
 __constant__ long long c_full_flat[2][kMaxOffsets];
 
 void upload_offsets(const int* half_dev[2], const int half_n[2], const int* full_dev[2],
-                    const int full_n[2], const long long* full_flat[2], cudaStream_t s) {
+                    const int full_n[2], const long long* full_flat[2], const int half_nin[2],
+                    const int full_nin[2], cudaStream_t s) {
+  cudaMemcpyToSymbolAsync(c_half_nin, half_nin, 2 * sizeof(int), 0, cudaMemcpyHostToDevice, s);
+  cudaMemcpyToSymbolAsync(c_full_nin, full_nin, 2 * sizeof(int), 0, cudaMemcpyHostToDevice, s);
   cudaMemcpyToSymbolAsync(c_half_n, half_n, 2 * sizeof(int), 0, cudaMemcpyHostToDevice, s);
   cudaMemcpyToSymbolAsync(c_full_n, full_n, 2 * sizeof(int), 0, cudaMemcpyHostToDevice, s);
   for (int p = 0; p < 2; ++p) {

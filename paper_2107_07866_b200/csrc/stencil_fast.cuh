@@ -4,30 +4,29 @@
 //
 // Same candidate set, orientation and exact in-cutoff decisions as
 // eam_kernels.cu (which mirrors the reference's arithmetic literally and
-// serves as CBX_STENCIL_REFERENCE); this variant is organised for sm_100a:
+// serves as CBX_STENCIL_REFERENCE).  Organised for sm_100a:
 //
-// * candidate filter in fp32 on a 16-byte shadow record uf[] = (x, y, z,
-//   owner) -- one LDG.128 per candidate instead of a 32-byte fp64 gather, and
-//   the fp32 pipe instead of the fp64 pipe.  The float distance is only a
-//   filter: candidates within `band` of the cutoff (a bound on the float
-//   error derived from the box extent, host side) get the exact fp64 r^2 of
-//   the reference (operation order of forces.cpp:123-125), so every
-//   in-cutoff decision is bit-identical to the reference.
-// * fp64 work only for in-cutoff pairs: one 256-bit load of the partner's
-//   (x, y, z, dF) and one or two 256-bit loads of a 32-byte-aligned spline
-//   record in the normalised variable s in [0, 1) (coefficients A=a h^3,
-//   B=b h^2, C=c h, D=d of the reference segment, spline.h:19-22).
-// * 1/r from the fp64 reciprocal square root, the segment index from a
-//   round-down add of 2^52 (no fp64<->int conversions).
+// * offset lists are ordered by lattice distance and split (host side) into
+//   "inner" sites (lattice distance <= cutoff: shells 1-5, 29 of the 56
+//   half-list candidates) and "skin" sites (shells 6-8, index skin of
+//   sim.cpp:73).  Inner candidates go straight to a 256-bit load of the
+//   partner's (x, y, z, dF) and the fp64 r^2; skin candidates are first
+//   filtered in fp32 on the 16-byte shadow uf[] = (x, y, z, owner).
+// * every in-cutoff decision is exact: an fp64/fp32 distance only decides
+//   when it is farther from the cutoff than its rounding bound (host side);
+//   otherwise the reference's r^2 (operation order of forces.cpp:123-125,
+//   no FMA) decides, so the pair set is bit-identical to the reference.
+// * spline records are 32-byte aligned in the normalised variable
+//   s = (r - x0)/h - i (A = a h^3, B = b h^2, C = c h, D = d of the
+//   reference segment, spline.h:19-22); 1/r from the fp64 rsqrt; the segment
+//   index from a round-down add of 2^52 (no fp64<->int conversions).
+// * candidates are processed in batches whose loads are issued back to back
+//   (memory-level parallelism), partner contributions are RED.ADD.F64 to the
+//   partner's owner -- fold_rho / fold_force of forces.cpp:290-309 at
+//   scatter time.
 // * persistent CTAs pull 8x4x4-cell bricks from an atomic work counter; the
-//   4 warps of a CTA take one z-plane each and sweep both sublattices, so
-//   the brick's neighbourhood (~55 KB) stays in L1 across all its
-//   candidates, and the launch tail is one brick.
-// * candidates are processed in batches (4 for density, 2 for force): the
-//   batch's filter loads, then its partner loads, then its table loads are
-//   issued back to back, so each warp keeps several L1/L2 requests in flight.
-// * fold_rho / fold_force (forces.cpp:290-309): partner contributions are
-//   RED-added to the partner's owner (interior site or periodic source).
+//   4 warps of a CTA take one z-plane each and sweep both sublattices, so the
+//   brick's neighbourhood stays in L1 and the launch tail is one brick.
 #pragma once
 // (no namespace: included inside namespace cbx)
 
@@ -37,9 +36,12 @@ __device__ __forceinline__ void ld256(const void* p, double& a, double& b, doubl
                : "=d"(a), "=d"(b), "=d"(c), "=d"(d)
                : "l"(p));
 }
-__device__ __forceinline__ float4 ld128f(const float4* p) { return __ldg(p); }
+__device__ __forceinline__ void red_add(double* p, double v) {
+  asm volatile("red.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
 
 constexpr double kTwo52 = 4503599627370496.0;
+constexpr int kBrickX = 8, kBrickY = 4, kBrickZ = 4;
 
 // segment index and normalised offset: u = (r - x0)/h, i = floor(u), s = u - i
 __device__ __forceinline__ int seg_index(const FastTab& T, double r, double& s) {
@@ -49,192 +51,180 @@ __device__ __forceinline__ int seg_index(const FastTab& T, double r, double& s) 
   return min(__double2loint(t), T.nseg);  // segment nseg is the padded one
 }
 
-// 1/r and r from r^2 (rsqrt + Newton steps, ~1 ulp)
-__device__ __forceinline__ double rinv_of(double r2) { return rsqrt(r2); }
-
-
-constexpr int kBrickX = 8, kBrickY = 4, kBrickZ = 4;
-
-// guard pass (r below the first knot, overlaps): revisit the site's list
-// and treat only the pairs the hot loop skipped (fp64 r^2 < guard_r2) with
-// the reference-literal evaluation of eam_kernels.cu.  Never taken in
-// thermal runs; kept out of the hot loop's register budget.
-__device__ __forceinline__ bool guard_pair(const KP& P, int par, int d, int k, bool full,
-                                           double ax, double ay, double az, const float4& af,
-                                           int& j, int& tgt, double& dx, double& dy, double& dz,
-                                           double& pw) {
-  j = d + (full ? c_full[par][k] : c_half[par][k]);
-  const float4 pf = P.uf[j];
-  const float fx = af.x - pf.x, fy = af.y - pf.y, fz = af.z - pf.z;
-  if (fmaf(fz, fz, fmaf(fy, fy, fx * fx)) > P.band_hi) return false;
-  const double4 p = P.pdf[j];
-  dx = xsub(ax, p.x);
-  dy = xsub(ay, p.y);
-  dz = xsub(az, p.z);
-  pw = p.w;
-  if (fma(dz, dz, fma(dy, dy, dx * dx)) >= P.guard_r2) return false;
-  const int tw = __float_as_int(pf.w);
-  tgt = tw < 0 ? j : tw;
-  return true;
+__device__ __forceinline__ unsigned long long pair_key(const KP& P, long long d, long long j,
+                                                       unsigned long long phase) {
+  const long long a = ref_of_dev(d, P.G.NC), b = ref_of_dev(j, P.G.NC);
+  const long long lo = min(a, b), hi = max(a, b);
+  return phase | ((unsigned long long)lo << 24) | (unsigned long long)((hi - lo) & 0xffffff);
 }
 
-template <bool FULL, bool UNUSED>
-__device__ __noinline__ double guard_pass(const KP& P, int par, int d, double ax, double ay,
-                                          double az, double aw, float4 af) {
-  const int n = FULL ? c_full_n[par] : c_half_n[par];
-  double acc = 0.0;
-  for (int k = 0; k < n; ++k) {
-    int j, tgt;
-    double dx, dy, dz, pw;
-    if (!guard_pair(P, par, d, k, FULL, ax, ay, az, af, j, tgt, dx, dy, dz, pw)) continue;
-    const double r2x = exact_r2(dx, dy, dz);
-    if (r2x < kOverlapR2) {
-      const long long rd = ref_of_dev(d, P.G.NC), rj = ref_of_dev(j, P.G.NC);
-      report_overlap(P, ((unsigned long long)min(rd, rj) << 12) | (unsigned)k, P.tag[d],
-                     P.tag[tgt], r2x);
-      continue;
-    }
-    const double rho = pair_rho(P, r2x);
-    acc += rho;
-    if (!FULL) atomicAdd(&P.rho[tgt], rho);
-  }
-  return acc;
-}
-
+// the decision for one candidate once its fp64 displacement is known:
+// 0 out, 1 in (fast path), 2 guard (r below the first knot or overlap)
 template <bool FULL>
-__device__ __noinline__ void guard_force(const KP& P, int par, int d, double ax, double ay,
-                                         double az, double adf, float4 af, double* out) {
-  const int n = FULL ? c_full_n[par] : c_half_n[par];
-  const long long S = P.S;
-  double fx = 0.0, fy = 0.0, fz = 0.0, e = 0.0;
-  for (int k = 0; k < n; ++k) {
-    int j, tgt;
-    double dx, dy, dz, pw;
-    if (!guard_pair(P, par, d, k, FULL, ax, ay, az, af, j, tgt, dx, dy, dz, pw)) continue;
-    const double r2x = exact_r2(dx, dy, dz);
-    if (r2x < kOverlapR2) {
-      const long long rd = ref_of_dev(d, P.G.NC), rj = ref_of_dev(j, P.G.NC);
-      report_overlap(P, (1ull << 61) | ((unsigned long long)min(rd, rj) << 12) | (unsigned)k,
-                     P.tag[d], P.tag[tgt], r2x);
-      continue;
-    }
-    double fp, phi;
-    pair_force(P, r2x, adf + pw, fp, phi);
-    const double qx = -fp * dx, qy = -fp * dy, qz = -fp * dz;
-    fx -= qx;
-    fy -= qy;
-    fz -= qz;
-    if (FULL) {
-      e = fma(0.5, phi, e);
-    } else {
-      e += phi;
-      atomicAdd(&P.frc[tgt], qx);
-      atomicAdd(&P.frc[S + tgt], qy);
-      atomicAdd(&P.frc[2 * S + tgt], qz);
-    }
+__device__ __forceinline__ int decide(const KP& P, int par, int k, int j, double ax, double ay,
+                                      double az, double px, double py, double pz, double dx,
+                                      double dy, double dz, double r2) {
+  if (r2 > P.cut2_lo) {  // within rounding of the cutoff: exact reference r^2
+    if (r2 > P.cut2_hi) return 0;
+    double ex = dx, ey = dy, ez = dz;
+    if (FULL && c_full_flat[par][k] < 0)
+      full_orient(P, make_double4(ax, ay, az, 0.0), j, make_double4(px, py, pz, 0.0), ex, ey, ez);
+    if (exact_r2(ex, ey, ez) > P.cut2) return 0;
   }
-  out[0] = fx;
-  out[1] = fy;
-  out[2] = fz;
-  out[3] = e;
+  return r2 < P.guard_r2 ? 2 : 1;
+}
+
+// guard pairs (r below the first knot, overlaps): the reference-literal
+// evaluation of eam_kernels.cu, out of the hot loop
+__device__ __noinline__ double guard_rho(KP* P, long long d, int j, int tgt, double dx, double dy,
+                                         double dz, int full) {
+  const double r2x = exact_r2(dx, dy, dz);
+  if (r2x < kOverlapR2) {
+    report_overlap(*P, pair_key(*P, d, j, 0), P->tag[d], P->tag[tgt], r2x);
+    return 0.0;
+  }
+  const double rho = pair_rho(*P, r2x);
+  if (!full) red_add(&P->rho[tgt], rho);
+  return rho;
+}
+__device__ __noinline__ bool guard_force(KP* P, long long d, int j, int tgt, double dx,
+                                         double dy, double dz, double dfsum, int full,
+                                         double* q) {
+  const double r2x = exact_r2(dx, dy, dz);
+  if (r2x < kOverlapR2) {
+    report_overlap(*P, pair_key(*P, d, j, 1ull << 61), P->tag[d], P->tag[tgt], r2x);
+    return false;
+  }
+  double fp, phi;
+  pair_force(*P, r2x, dfsum, fp, phi);
+  q[0] = -fp * dx;
+  q[1] = -fp * dy;
+  q[2] = -fp * dz;
+  q[3] = phi;
+  if (!full) {
+    red_add(&P->frc[tgt], q[0]);
+    red_add(&P->frc[P->S + tgt], q[1]);
+    red_add(&P->frc[2 * P->S + tgt], q[2]);
+  }
+  return true;
 }
 
 // ------------------------------------------------------------------ density
 template <bool FULL, int B>
-__device__ __forceinline__ void density_site(const KP& P, int par, int d, bool live) {
+__device__ __forceinline__ void density_site(const KP& P, KP* Pp, int par, int d, bool live) {
   const double4* __restrict__ pdf = P.pdf;
-  const float4* __restrict__ uf = P.uf;
-  float4 af = make_float4(kVacantF, kVacantF, kVacantF, 0.f);
-  if (live) af = uf[d];
-  if (af.x >= kVacantF) {
+  const int* __restrict__ tgt = P.tgt;
+  double ax = kVacant, ay = 0, az = 0, aw = 0;
+  if (live) ld256(pdf + d, ax, ay, az, aw);
+  if (ax >= kVacantTest) {
     if (FULL && live) P.rho[d] = 0.0;
     return;
   }
-  double ax, ay, az, aw;
-  ld256(pdf + d, ax, ay, az, aw);
   const int n = FULL ? c_full_n[par] : c_half_n[par];
+  const int nin = FULL ? c_full_nin[par] : c_half_nin[par];
   const int* offs = FULL ? c_full[par] : c_half[par];
-  const float hi = P.band_hi, lo = P.band_lo;
   double acc = 0.0;
-  bool slow = false;
-  for (int k0 = 0; k0 < n; k0 += B) {
-    int j[B];
-    float4 pf[B];
+  // inner shells: direct fp64 gather, batched
+  for (int k0 = 0; k0 < nin; k0 += B) {
+    int j[B], t[B], st[B], seg[B];
+    double px[B], py[B], pz[B], s[B];
 #pragma unroll
     for (int b = 0; b < B; ++b) {
-      j[b] = d + offs[min(k0 + b, n - 1)];
-      pf[b] = ld128f(uf + j[b]);
+      j[b] = d + offs[min(k0 + b, nin - 1)];
+      double w;
+      ld256(pdf + j[b], px[b], py[b], pz[b], w);
+      t[b] = __ldg(tgt + j[b]);
     }
-    bool go[B], band[B];
 #pragma unroll
     for (int b = 0; b < B; ++b) {
-      const float fx = af.x - pf[b].x, fy = af.y - pf[b].y, fz = af.z - pf[b].z;
-      const float r2f = fmaf(fz, fz, fmaf(fy, fy, fx * fx));
-      go[b] = (k0 + b < n) && r2f <= hi;
-      band[b] = r2f >= lo;
-    }
-    double px[B], py[B], pz[B];
-#pragma unroll
-    for (int b = 0; b < B; ++b) {
-      if (go[b]) {
-        double w;
-        ld256(pdf + j[b], px[b], py[b], pz[b], w);
-      }
-    }
-    double s[B];
-    int seg[B];
-#pragma unroll
-    for (int b = 0; b < B; ++b) {
-      if (!go[b]) continue;
       const double dx = xsub(ax, px[b]), dy = xsub(ay, py[b]), dz = xsub(az, pz[b]);
-      if (band[b]) {  // near the cutoff: the reference's exact r^2 decides
-        double ex = dx, ey = dy, ez = dz;
-        if (FULL && c_full_flat[par][k0 + b] < 0)
-          full_orient(P, make_double4(ax, ay, az, aw), j[b], make_double4(px[b], py[b], pz[b], 0.0),
-                      ex, ey, ez);
-        if (exact_r2(ex, ey, ez) > P.cut2) {
-          go[b] = false;
-          continue;
-        }
-      }
       const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
-      if (r2 < P.guard_r2) {  // overlap / sub-table separation: second pass below
-        go[b] = false;
-        slow = true;
-        continue;
+      st[b] = k0 + b < nin ? decide<FULL>(P, par, k0 + b, j[b], ax, ay, az, px[b], py[b], pz[b],
+                                          dx, dy, dz, r2)
+                           : 0;
+      if (st[b] == 2) {
+        acc += guard_rho(Pp, d, j[b], t[b], dx, dy, dz, FULL);
+        st[b] = 0;
       }
-      const double r = r2 * rsqrt(r2);
-      seg[b] = seg_index(P.fd, r, s[b]);
+      seg[b] = seg_index(P.fd, r2 * rsqrt(r2), s[b]);
     }
     double tA[B], tB[B], tC[B], tD[B];
 #pragma unroll
     for (int b = 0; b < B; ++b)
-      if (go[b]) ld256(P.fd.rec + 4 * (size_t)seg[b], tA[b], tB[b], tC[b], tD[b]);
+      if (st[b]) ld256(P.fd.rec + 4 * (size_t)seg[b], tA[b], tB[b], tC[b], tD[b]);
 #pragma unroll
     for (int b = 0; b < B; ++b) {
-      if (!go[b]) continue;
+      if (!st[b]) continue;
       const double rho = fma(fma(fma(tA[b], s[b], tB[b]), s[b], tC[b]), s[b], tD[b]);
       acc += rho;
-      if (!FULL) {
-        const int tw = __float_as_int(pf[b].w);
-        atomicAdd(&P.rho[tw < 0 ? j[b] : tw], rho);
-      }
+      if (!FULL) red_add(&P.rho[t[b]], rho);
     }
   }
-  if (slow) acc += guard_pass<FULL, false>(P, par, d, ax, ay, az, aw, af);
+  // skin shells: fp32 filter first (almost all rejected)
+  const float4 af = make_float4((float)ax, (float)ay, (float)az, 0.f);
+  for (int k = nin; k < n; ++k) {
+    const int jj = d + offs[k];
+    const float4 pf = __ldg(P.uf + jj);
+    const float fx = af.x - pf.x, fy = af.y - pf.y, fz = af.z - pf.z;
+    if (fmaf(fz, fz, fmaf(fy, fy, fx * fx)) > P.band_hi) continue;
+    double px, py, pz, w;
+    ld256(pdf + jj, px, py, pz, w);
+    const double dx = xsub(ax, px), dy = xsub(ay, py), dz = xsub(az, pz);
+    const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+    const int stt = decide<FULL>(P, par, k, jj, ax, ay, az, px, py, pz, dx, dy, dz, r2);
+    if (!stt) continue;
+    const int tw = __float_as_int(pf.w);
+    const int to = tw < 0 ? jj : tw;
+    if (stt == 2) {
+      acc += guard_rho(Pp, d, jj, to, dx, dy, dz, FULL);
+      continue;
+    }
+    double s;
+    const int sg = seg_index(P.fd, r2 * rsqrt(r2), s);
+    double A, Bc, Cc, D;
+    ld256(P.fd.rec + 4 * (size_t)sg, A, Bc, Cc, D);
+    const double rho = fma(fma(fma(A, s, Bc), s, Cc), s, D);
+    acc += rho;
+    if (!FULL) red_add(&P.rho[to], rho);
+  }
   if (FULL) P.rho[d] = acc;
-  else atomicAdd(&P.rho[d], acc);
+  else red_add(&P.rho[d], acc);
 }
 
 // -------------------------------------------------------------------- force
+struct PairOut {
+  double qx, qy, qz, phi;
+};
+
+// -fp of forces.cpp:164 times d, and phi, from one 64-byte force record
+__device__ __forceinline__ PairOut pair_eval(const double* rec, double s, double ri, double ih,
+                                             double dfsum, double dx, double dy, double dz) {
+  double zA, zB, zC, zD, qA, qB, qC, qD;
+  ld256(rec, zA, zB, zC, zD);
+  ld256(rec + 4, qA, qB, qC, qD);
+  const double s15 = 1.5 * s, s2 = s + s;
+  const double z = fma(fma(fma(zA, s, zB), s, zC), s, zD);
+  const double zs = fma(fma(zA, s15, zB), s2, zC);  // dz/ds
+  const double ps = fma(fma(qA, s15, qB), s2, qC);  // drho/ds
+  PairOut o;
+  o.phi = z * ri;
+  // phi' = (z' - phi)/r;  -fp = ((dFa + dFp) rho' + phi')/r;  d/dr = ih d/ds
+  const double dphi = fma(zs, ih, -o.phi) * ri;
+  const double mfp = fma(dfsum * ps, ih, dphi) * ri;
+  o.qx = mfp * dx;
+  o.qy = mfp * dy;
+  o.qz = mfp * dz;
+  return o;
+}
+
 template <bool FULL, int B>
-__device__ __forceinline__ double force_site(const KP& P, int par, int d, bool live) {
+__device__ __forceinline__ double force_site(const KP& P, KP* Pp, int par, int d, bool live) {
   const double4* __restrict__ pdf = P.pdf;
-  const float4* __restrict__ uf = P.uf;
+  const int* __restrict__ tgt = P.tgt;
   const long long S = P.S;
-  float4 af = make_float4(kVacantF, kVacantF, kVacantF, 0.f);
-  if (live) af = uf[d];
-  if (af.x >= kVacantF) {
+  double ax = kVacant, ay = 0, az = 0, adf = 0;
+  if (live) ld256(pdf + d, ax, ay, az, adf);
+  if (ax >= kVacantTest) {
     if (FULL && live) {
       P.frc[d] = 0.0;
       P.frc[S + d] = 0.0;
@@ -242,113 +232,100 @@ __device__ __forceinline__ double force_site(const KP& P, int par, int d, bool l
     }
     return 0.0;
   }
-  double ax, ay, az, adf;
-  ld256(pdf + d, ax, ay, az, adf);
   const int n = FULL ? c_full_n[par] : c_half_n[par];
+  const int nin = FULL ? c_full_nin[par] : c_half_nin[par];
   const int* offs = FULL ? c_full[par] : c_half[par];
-  const float hi = P.band_hi, lo = P.band_lo;
   const double ih = P.ff.ih;
   double fx = 0.0, fy = 0.0, fz = 0.0, e = 0.0;
-  bool slow = false;
-  for (int k0 = 0; k0 < n; k0 += B) {
-    int j[B];
-    float4 pf[B];
-#pragma unroll
-    for (int b = 0; b < B; ++b) {
-      j[b] = d + offs[min(k0 + b, n - 1)];
-      pf[b] = ld128f(uf + j[b]);
+  auto accumulate = [&](const PairOut& o, int to) {
+    fx -= o.qx;
+    fy -= o.qy;
+    fz -= o.qz;
+    if (FULL) {
+      e = fma(0.5, o.phi, e);
+    } else {
+      e += o.phi;
+      red_add(&P.frc[to], o.qx);
+      red_add(&P.frc[S + to], o.qy);
+      red_add(&P.frc[2 * S + to], o.qz);
     }
-    bool go[B], band[B];
+  };
+  for (int k0 = 0; k0 < nin; k0 += B) {
+    int j[B], t[B], st[B], seg[B];
+    double px[B], py[B], pz[B], pw[B], dx[B], dy[B], dz[B], s[B], ri[B];
 #pragma unroll
     for (int b = 0; b < B; ++b) {
-      const float gx = af.x - pf[b].x, gy = af.y - pf[b].y, gz = af.z - pf[b].z;
-      const float r2f = fmaf(gz, gz, fmaf(gy, gy, gx * gx));
-      go[b] = (k0 + b < n) && r2f <= hi;
-      band[b] = r2f >= lo;
+      j[b] = d + offs[min(k0 + b, nin - 1)];
+      ld256(pdf + j[b], px[b], py[b], pz[b], pw[b]);
+      t[b] = __ldg(tgt + j[b]);
     }
-    double px[B], py[B], pz[B], pw[B];
-#pragma unroll
-    for (int b = 0; b < B; ++b)
-      if (go[b]) ld256(pdf + j[b], px[b], py[b], pz[b], pw[b]);
-    double dxs[B], dys[B], dzs[B], s[B], ri[B];
-    int seg[B];
 #pragma unroll
     for (int b = 0; b < B; ++b) {
-      if (!go[b]) continue;
-      const double dx = xsub(ax, px[b]), dy = xsub(ay, py[b]), dz = xsub(az, pz[b]);
-      dxs[b] = dx;
-      dys[b] = dy;
-      dzs[b] = dz;
-      if (band[b]) {
-        double ex = dx, ey = dy, ez = dz;
-        if (FULL && c_full_flat[par][k0 + b] < 0)
-          full_orient(P, make_double4(ax, ay, az, adf), j[b],
-                      make_double4(px[b], py[b], pz[b], pw[b]), ex, ey, ez);
-        if (exact_r2(ex, ey, ez) > P.cut2) {
-          go[b] = false;
-          continue;
+      dx[b] = xsub(ax, px[b]);
+      dy[b] = xsub(ay, py[b]);
+      dz[b] = xsub(az, pz[b]);
+      const double r2 = fma(dz[b], dz[b], fma(dy[b], dy[b], dx[b] * dx[b]));
+      st[b] = k0 + b < nin ? decide<FULL>(P, par, k0 + b, j[b], ax, ay, az, px[b], py[b], pz[b],
+                                          dx[b], dy[b], dz[b], r2)
+                           : 0;
+      if (st[b] == 2) {
+        double q[4];
+        if (guard_force(Pp, d, j[b], t[b], dx[b], dy[b], dz[b], adf + pw[b], FULL, q)) {
+          fx -= q[0];
+          fy -= q[1];
+          fz -= q[2];
+          e = FULL ? fma(0.5, q[3], e) : e + q[3];
         }
-      }
-      const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
-      if (r2 < P.guard_r2) {
-        go[b] = false;
-        slow = true;
-        continue;
+        st[b] = 0;
       }
       ri[b] = rsqrt(r2);
       seg[b] = seg_index(P.ff, r2 * ri[b], s[b]);
     }
-    double zA[B], zB[B], zC[B], zD[B], qA[B], qB[B], qC[B], qD[B];
 #pragma unroll
     for (int b = 0; b < B; ++b) {
-      if (!go[b]) continue;
-      const double* rec = P.ff.rec + 8 * (size_t)seg[b];
-      ld256(rec, zA[b], zB[b], zC[b], zD[b]);
-      ld256(rec + 4, qA[b], qB[b], qC[b], qD[b]);
-    }
-#pragma unroll
-    for (int b = 0; b < B; ++b) {
-      if (!go[b]) continue;
-      const double sb = s[b], s15 = 1.5 * sb, s2 = sb + sb;
-      const double z = fma(fma(fma(zA[b], sb, zB[b]), sb, zC[b]), sb, zD[b]);
-      const double zs = fma(fma(zA[b], s15, zB[b]), s2, zC[b]);  // dz/ds
-      const double ps = fma(fma(qA[b], s15, qB[b]), s2, qC[b]);  // drho/ds
-      const double phi = z * ri[b];
-      // phi' = (z' - phi)/r;  -fp = ((dFa + dFp) rho' + phi')/r;  d/dr = ih d/ds
-      const double dphi = fma(zs, ih, -phi) * ri[b];
-      const double mfp = fma((adf + pw[b]) * ps, ih, dphi) * ri[b];
-      const double qx = mfp * dxs[b], qy = mfp * dys[b], qz = mfp * dzs[b];
-      fx -= qx;
-      fy -= qy;
-      fz -= qz;
-      if (FULL) {
-        e = fma(0.5, phi, e);
-      } else {
-        e += phi;
-        const int tw = __float_as_int(pf[b].w);
-        const int tgt = tw < 0 ? j[b] : tw;
-        atomicAdd(&P.frc[tgt], qx);
-        atomicAdd(&P.frc[S + tgt], qy);
-        atomicAdd(&P.frc[2 * S + tgt], qz);
-      }
+      if (!st[b]) continue;
+      accumulate(pair_eval(P.ff.rec + 8 * (size_t)seg[b], s[b], ri[b], ih, adf + pw[b], dx[b],
+                           dy[b], dz[b]),
+                 t[b]);
     }
   }
-  if (slow) {
-    double g[4];
-    guard_force<FULL>(P, par, d, ax, ay, az, adf, af, g);
-    fx += g[0];
-    fy += g[1];
-    fz += g[2];
-    e += g[3];
+  const float4 af = make_float4((float)ax, (float)ay, (float)az, 0.f);
+  for (int k = nin; k < n; ++k) {
+    const int jj = d + offs[k];
+    const float4 pf = __ldg(P.uf + jj);
+    const float gx = af.x - pf.x, gy = af.y - pf.y, gz = af.z - pf.z;
+    if (fmaf(gz, gz, fmaf(gy, gy, gx * gx)) > P.band_hi) continue;
+    double px, py, pz, pw;
+    ld256(pdf + jj, px, py, pz, pw);
+    const double ddx = xsub(ax, px), ddy = xsub(ay, py), ddz = xsub(az, pz);
+    const double r2 = fma(ddz, ddz, fma(ddy, ddy, ddx * ddx));
+    const int stt = decide<FULL>(P, par, k, jj, ax, ay, az, px, py, pz, ddx, ddy, ddz, r2);
+    if (!stt) continue;
+    const int tw = __float_as_int(pf.w);
+    const int to = tw < 0 ? jj : tw;
+    if (stt == 2) {
+      double q[4];
+      if (guard_force(Pp, d, jj, to, ddx, ddy, ddz, adf + pw, FULL, q)) {
+        fx -= q[0];
+        fy -= q[1];
+        fz -= q[2];
+        e = FULL ? fma(0.5, q[3], e) : e + q[3];
+      }
+      continue;
+    }
+    const double ri = rsqrt(r2);
+    double s;
+    const int sg = seg_index(P.ff, r2 * ri, s);
+    accumulate(pair_eval(P.ff.rec + 8 * (size_t)sg, s, ri, ih, adf + pw, ddx, ddy, ddz), to);
   }
   if (FULL) {
     P.frc[d] = fx;
     P.frc[S + d] = fy;
     P.frc[2 * S + d] = fz;
   } else {
-    atomicAdd(&P.frc[d], fx);
-    atomicAdd(&P.frc[S + d], fy);
-    atomicAdd(&P.frc[2 * S + d], fz);
+    red_add(&P.frc[d], fx);
+    red_add(&P.frc[S + d], fy);
+    red_add(&P.frc[2 * S + d], fz);
   }
   return e;
 }
@@ -363,7 +340,7 @@ __device__ __forceinline__ int next_brick(int* ctr) {
   return s_brick;
 }
 
-__device__ __forceinline__ bool brick_site(const Geo& G, int brick, int par, long long& d) {
+__device__ __forceinline__ bool brick_site(const Geo& G, int brick, int par, int& d) {
   const int nbx = (G.bx + kBrickX - 1) / kBrickX, nby = (G.by + kBrickY - 1) / kBrickY;
   const int bxi = brick % nbx, r = brick / nbx;
   const int byi = r % nby, bzi = r / nby;
@@ -371,7 +348,7 @@ __device__ __forceinline__ bool brick_site(const Geo& G, int brick, int par, lon
   const int cx = bxi * kBrickX + (lane & 7), cy = byi * kBrickY + (lane >> 3),
             cz = bzi * kBrickZ + w;
   const bool live = cx < G.bx && cy < G.by && cz < G.bz;
-  d = live ? par * G.NC + cell_of(cx + G.g, cy + G.g, cz + G.g, G) : 0;
+  d = live ? (int)(par * G.NC + cell_of(cx + G.g, cy + G.g, cz + G.g, G)) : 0;
   return live;
 }
 
@@ -388,9 +365,9 @@ __global__ void __launch_bounds__(128, 4) k_density_fast(KP P) {
     const int b = next_brick(&P.work[0]);
     if (b >= nb) break;
     for (int par = 0; par < 2; ++par) {
-      long long d;
+      int d;
       const bool live = brick_site(P.G, b, par, d);
-      density_site<FULL, 4>(P, par, (int)d, live);
+      density_site<FULL, 4>(P, P.dself, par, d, live);
     }
   }
 }
@@ -404,9 +381,9 @@ __global__ void __launch_bounds__(128, 4) k_force_fast(KP P) {
     const int b = next_brick(&P.work[1]);
     if (b >= nb) break;
     for (int par = 0; par < 2; ++par) {
-      long long d;
+      int d;
       const bool live = brick_site(P.G, b, par, d);
-      e += force_site<FULL, B>(P, par, (int)d, live);
+      e += force_site<FULL, B>(P, P.dself, par, d, live);
     }
   }
   for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
