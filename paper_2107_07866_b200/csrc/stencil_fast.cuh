@@ -110,6 +110,27 @@ __device__ __noinline__ bool guard_force(KP* P, long long d, int j, int tgt, dou
 }
 
 // ------------------------------------------------------------------ density
+// one skin candidate that passed the fp32 filter (rare): full decision
+template <bool FULL>
+__device__ __forceinline__ double skin_density(const KP& P, KP* Pp, int par, int k, int d, int jj,
+                                               int tw, double ax, double ay, double az) {
+  double px, py, pz, w;
+  ld256(P.pdf + jj, px, py, pz, w);
+  const double dx = xsub(ax, px), dy = xsub(ay, py), dz = xsub(az, pz);
+  const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+  const int stt = decide<FULL>(P, par, k, jj, ax, ay, az, px, py, pz, dx, dy, dz, r2);
+  if (!stt) return 0.0;
+  const int to = tw < 0 ? jj : tw;
+  if (stt == 2) return guard_rho(Pp, d, jj, to, dx, dy, dz, FULL);
+  double s;
+  const int sg = seg_index(P.fd, r2 * rsqrt(r2), s);
+  double A, Bc, Cc, D;
+  ld256(P.fd.rec + 4 * (size_t)sg, A, Bc, Cc, D);
+  const double rho = fma(fma(fma(A, s, Bc), s, Cc), s, D);
+  if (!FULL) red_add(&P.rho[to], rho);
+  return rho;
+}
+
 template <bool FULL, int B>
 __device__ __forceinline__ void density_site(const KP& P, KP* Pp, int par, int d, bool live) {
   const double4* __restrict__ pdf = P.pdf;
@@ -123,11 +144,14 @@ __device__ __forceinline__ void density_site(const KP& P, KP* Pp, int par, int d
   const int n = FULL ? c_full_n[par] : c_half_n[par];
   const int nin = FULL ? c_full_nin[par] : c_half_nin[par];
   const int* offs = FULL ? c_full[par] : c_half[par];
+  const double lo = P.cut2_lo, g2 = P.guard_r2;
   double acc = 0.0;
-  // inner shells: direct fp64 gather, batched
+  // inner shells: direct fp64 gather, batched; the common case is decided
+  // by one compare, the near-cutoff / guard cases drop to decide()
   for (int k0 = 0; k0 < nin; k0 += B) {
-    int j[B], t[B], st[B], seg[B];
-    double px[B], py[B], pz[B], s[B];
+    int j[B], t[B], seg[B];
+    bool in[B];
+    double px[B], py[B], pz[B], s[B], r2[B];
 #pragma unroll
     for (int b = 0; b < B; ++b) {
       j[b] = d + offs[min(k0 + b, nin - 1)];
@@ -135,57 +159,66 @@ __device__ __forceinline__ void density_site(const KP& P, KP* Pp, int par, int d
       ld256(pdf + j[b], px[b], py[b], pz[b], w);
       t[b] = __ldg(tgt + j[b]);
     }
+    bool rare = false;
 #pragma unroll
     for (int b = 0; b < B; ++b) {
       const double dx = xsub(ax, px[b]), dy = xsub(ay, py[b]), dz = xsub(az, pz[b]);
-      const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
-      st[b] = k0 + b < nin ? decide<FULL>(P, par, k0 + b, j[b], ax, ay, az, px[b], py[b], pz[b],
-                                          dx, dy, dz, r2)
-                           : 0;
-      if (st[b] == 2) {
-        acc += guard_rho(Pp, d, j[b], t[b], dx, dy, dz, FULL);
-        st[b] = 0;
-      }
-      seg[b] = seg_index(P.fd, r2 * rsqrt(r2), s[b]);
+      r2[b] = fma(dz, dz, fma(dy, dy, dx * dx));
+      const bool live_k = k0 + b < nin;
+      in[b] = live_k && r2[b] <= lo && r2[b] >= g2;
+      rare |= live_k && !in[b] && (r2[b] <= P.cut2_hi);
     }
+    if (rare) {
+#pragma unroll
+      for (int b = 0; b < B; ++b) {
+        if (in[b] || k0 + b >= nin || r2[b] > P.cut2_hi) continue;
+        const double dx = xsub(ax, px[b]), dy = xsub(ay, py[b]), dz = xsub(az, pz[b]);
+        const int st = decide<FULL>(P, par, k0 + b, j[b], ax, ay, az, px[b], py[b], pz[b], dx, dy,
+                                    dz, r2[b]);
+        if (st == 1) in[b] = true;
+        else if (st == 2) acc += guard_rho(Pp, d, j[b], t[b], dx, dy, dz, FULL);
+      }
+    }
+#pragma unroll
+    for (int b = 0; b < B; ++b) seg[b] = seg_index(P.fd, r2[b] * rsqrt(r2[b]), s[b]);
     double tA[B], tB[B], tC[B], tD[B];
 #pragma unroll
     for (int b = 0; b < B; ++b)
-      if (st[b]) ld256(P.fd.rec + 4 * (size_t)seg[b], tA[b], tB[b], tC[b], tD[b]);
+      if (in[b]) ld256(P.fd.rec + 4 * (size_t)seg[b], tA[b], tB[b], tC[b], tD[b]);
 #pragma unroll
     for (int b = 0; b < B; ++b) {
-      if (!st[b]) continue;
-      const double rho = fma(fma(fma(tA[b], s[b], tB[b]), s[b], tC[b]), s[b], tD[b]);
-      acc += rho;
-      if (!FULL) red_add(&P.rho[t[b]], rho);
+      if (in[b]) {
+        const double rho = fma(fma(fma(tA[b], s[b], tB[b]), s[b], tC[b]), s[b], tD[b]);
+        acc += rho;
+        if (!FULL) red_add(&P.rho[t[b]], rho);
+      }
     }
   }
-  // skin shells: fp32 filter first (almost all rejected)
+  // skin shells: fp32 filter, batched; a pass is rare
   const float4 af = make_float4((float)ax, (float)ay, (float)az, 0.f);
-  for (int k = nin; k < n; ++k) {
-    const int jj = d + offs[k];
-    const float4 pf = __ldg(P.uf + jj);
-    const float fx = af.x - pf.x, fy = af.y - pf.y, fz = af.z - pf.z;
-    if (fmaf(fz, fz, fmaf(fy, fy, fx * fx)) > P.band_hi) continue;
-    double px, py, pz, w;
-    ld256(pdf + jj, px, py, pz, w);
-    const double dx = xsub(ax, px), dy = xsub(ay, py), dz = xsub(az, pz);
-    const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
-    const int stt = decide<FULL>(P, par, k, jj, ax, ay, az, px, py, pz, dx, dy, dz, r2);
-    if (!stt) continue;
-    const int tw = __float_as_int(pf.w);
-    const int to = tw < 0 ? jj : tw;
-    if (stt == 2) {
-      acc += guard_rho(Pp, d, jj, to, dx, dy, dz, FULL);
-      continue;
+  const float hi = P.band_hi;
+  for (int k0 = nin; k0 < n; k0 += 4) {
+    float4 pf[4];
+    int jj[4];
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      jj[b] = d + offs[min(k0 + b, n - 1)];
+      pf[b] = __ldg(P.uf + jj[b]);
     }
-    double s;
-    const int sg = seg_index(P.fd, r2 * rsqrt(r2), s);
-    double A, Bc, Cc, D;
-    ld256(P.fd.rec + 4 * (size_t)sg, A, Bc, Cc, D);
-    const double rho = fma(fma(fma(A, s, Bc), s, Cc), s, D);
-    acc += rho;
-    if (!FULL) red_add(&P.rho[to], rho);
+    bool any = false, pass[4];
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const float fx = af.x - pf[b].x, fy = af.y - pf[b].y, fz = af.z - pf[b].z;
+      pass[b] = k0 + b < n && fmaf(fz, fz, fmaf(fy, fy, fx * fx)) <= hi;
+      any |= pass[b];
+    }
+    if (any) {
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+        if (pass[b])
+          acc += skin_density<FULL>(P, Pp, par, k0 + b, d, jj[b], __float_as_int(pf[b].w), ax,
+                                    ay, az);
+    }
   }
   if (FULL) P.rho[d] = acc;
   else red_add(&P.rho[d], acc);
@@ -357,8 +390,8 @@ __host__ __device__ __forceinline__ int brick_count(const Geo& G) {
          ((G.bz + kBrickZ - 1) / kBrickZ);
 }
 
-template <bool FULL>
-__global__ void __launch_bounds__(128, 4) k_density_fast(KP P) {
+template <bool FULL, int B, int MINB>
+__global__ void __launch_bounds__(128, MINB) k_density_fast(KP P) {
   if (P.st->err) return;
   const int nb = brick_count(P.G);
   for (;;) {
@@ -367,7 +400,7 @@ __global__ void __launch_bounds__(128, 4) k_density_fast(KP P) {
     for (int par = 0; par < 2; ++par) {
       int d;
       const bool live = brick_site(P.G, b, par, d);
-      density_site<FULL, 4>(P, P.dself, par, d, live);
+      density_site<FULL, B>(P, P.dself, par, d, live);
     }
   }
 }
@@ -398,7 +431,7 @@ int fast_grid(const KP& P, bool force, int mode) {
         128, 0);
   else
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-        &per_sm, mode ? (const void*)k_density_fast<true> : (const void*)k_density_fast<false>,
+        &per_sm, mode ? (const void*)k_density_fast<true, 2, 6> : (const void*)k_density_fast<false, 2, 6>,
         128, 0);
   int sms = 148;
   int dev = 0;
@@ -409,8 +442,17 @@ int fast_grid(const KP& P, bool force, int mode) {
 }
 
 void launch_density_fast(const KP& P, int mode, int grid, cudaStream_t s) {
-  if (mode) k_density_fast<true><<<grid, 128, 0, s>>>(P);
-  else k_density_fast<false><<<grid, 128, 0, s>>>(P);
+  static const int batch = [] {
+    const char* e = getenv("CBX_DENSITY_BATCH");
+    return e ? atoi(e) : 2;
+  }();
+  if (batch == 4) {
+    if (mode) k_density_fast<true, 4, 4><<<grid, 128, 0, s>>>(P);
+    else k_density_fast<false, 4, 4><<<grid, 128, 0, s>>>(P);
+  } else {
+    if (mode) k_density_fast<true, 2, 6><<<grid, 128, 0, s>>>(P);
+    else k_density_fast<false, 2, 6><<<grid, 128, 0, s>>>(P);
+  }
 }
 void launch_force_fast(const KP& P, int mode, int grid, cudaStream_t s) {
   static const int batch = [] {
