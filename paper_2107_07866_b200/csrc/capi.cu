@@ -39,6 +39,7 @@ struct cbx_ctx {
   uint64_t launches = 0;
   int n_ghost = 0;
   bool fast_ok = true;
+  bool mask_valid = false;  // pmask matches the current positions (density ran last)
   double band = 0.0;
 
   template <class T>
@@ -176,6 +177,7 @@ void ev_mark(cbx_ctx* c, int i) {
 }
 
 void seq_fill_ghosts(cbx_ctx* c) {
+  c->mask_valid = false;
   launch_ghost_fill(c->P, c->stream);
   launch_clash_images(c->P, c->stream);
   c->launches += 2;
@@ -188,6 +190,7 @@ void seq_density(cbx_ctx* c) {
   launch_density(c->P, c->mode, c->stream);
   launch_clash_density(c->P, c->stream);
   c->launches += 3;
+  c->mask_valid = c->mode != CBX_STENCIL_REFERENCE && c->P.pmask != nullptr;
 }
 void seq_embed(cbx_ctx* c) {
   launch_embed(c->P, c->stream);
@@ -198,12 +201,15 @@ void seq_force(cbx_ctx* c) {
   if (c->mode != CBX_STENCIL_FULL)
     cudaMemsetAsync(c->P.frc, 0, 3 * c->S * sizeof(double), c->stream);
   launch_clash_zero(c->P, 1, c->stream);
-  launch_force(c->P, c->mode, c->stream);
+  KP q = c->P;
+  q.use_mask = c->mask_valid ? 1 : 0;
+  launch_force(q, c->mode, c->stream);
   launch_clash_force(c->P, c->stream);
   c->launches += 3;
 }
 // one velocity-Verlet step, sim.cpp:248-273
 void seq_step(cbx_ctx* c) {
+  c->mask_valid = false;
   ev_mark(c, 0);
   launch_kick_drift(c->P, 1, c->stream);
   launch_rehash(c->P, c->stream);
@@ -820,6 +826,10 @@ CBX_API cbx_status cbx_create(const cbx_box* box, const cbx_potential* pot,
     setup_fast(c.get());
     P.st = c->alloc<DevStatus>(1);
     P.dself = c->alloc<KP>(1);
+    {
+      const int maxn = std::max(std::max(fd[0].size(), fd[1].size()), std::max(hd[0].size(), hd[1].size()));
+      P.pmask = maxn <= 126 ? c->alloc<unsigned long long>(2 * S) : nullptr;
+    }
     c->d_defects = c->alloc<unsigned long long>(4);
     // empty store: every slot vacant
     std::vector<double4> vac(S, make_double4(kVacant, kVacant, kVacant, 0.0));
@@ -868,6 +878,7 @@ CBX_API cbx_status cbx_set_stencil(cbx_ctx* c, cbx_stencil mode) {
       raise(CBX_INVALID_ARGUMENT, "fast stencils need z(r) and rho(r) on one grid");
     if (c->mode != mode) drop_graph(c);
     c->mode = mode;
+    c->mask_valid = false;
     c->P.n_pair_part = pair_partials(c->P, mode);
     sync_kp(c);
   });

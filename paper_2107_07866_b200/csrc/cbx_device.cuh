@@ -76,6 +76,8 @@ struct KP {
   double guard_r2;         // below: overlap / short-range guard path
   double cut2_lo, cut2_hi; // fp64 (FMA) r^2 decides outside [lo, hi]; exact r^2 inside
   struct KP* dself;        // this parameter block in device memory (guard paths)
+  unsigned long long* pmask;  // [S][2] pair masks from the density pass (or null)
+  int use_mask;               // force pass replays pmask (set per launch by the host)
   int n_pair_part;         // partials written by the force pass
   double accel, mv2;  // units::accel_factor, units::mv2_to_ev (units.h:17-24)
   long long S;  // 2*NC sites

@@ -41,6 +41,15 @@ __device__ __forceinline__ void red_add(double* p, double v) {
 }
 
 constexpr double kTwo52 = 4503599627370496.0;
+// per-site pair mask written by the density pass (bit k: offset k in cutoff
+// on the fast path; top bit: the site has guard pairs) and replayed by the
+// force pass, so the force pass never re-filters candidates
+constexpr unsigned long long kGuardBit = 1ull << 63;
+constexpr int kMaskBits = 127;
+__device__ __forceinline__ void set_bit(unsigned long long& m0, unsigned long long& m1, int k) {
+  if (k < 64) m0 |= 1ull << k;
+  else m1 |= 1ull << (k - 64);
+}
 constexpr int kBrickX = 8, kBrickY = 4, kBrickZ = 4;
 
 // segment index and normalised offset: u = (r - x0)/h, i = floor(u), s = u - i
@@ -113,7 +122,8 @@ __device__ __noinline__ bool guard_force(KP* P, long long d, int j, int tgt, dou
 // one skin candidate that passed the fp32 filter (rare): full decision
 template <bool FULL>
 __device__ __forceinline__ double skin_density(const KP& P, KP* Pp, int par, int k, int d, int jj,
-                                               int tw, double ax, double ay, double az) {
+                                               int tw, double ax, double ay, double az,
+                                               unsigned long long& m0, unsigned long long& m1) {
   double px, py, pz, w;
   ld256(P.pdf + jj, px, py, pz, w);
   const double dx = xsub(ax, px), dy = xsub(ay, py), dz = xsub(az, pz);
@@ -121,7 +131,11 @@ __device__ __forceinline__ double skin_density(const KP& P, KP* Pp, int par, int
   const int stt = decide<FULL>(P, par, k, jj, ax, ay, az, px, py, pz, dx, dy, dz, r2);
   if (!stt) return 0.0;
   const int to = tw < 0 ? jj : tw;
-  if (stt == 2) return guard_rho(Pp, d, jj, to, dx, dy, dz, FULL);
+  if (stt == 2) {
+    m1 |= kGuardBit;
+    return guard_rho(Pp, d, jj, to, dx, dy, dz, FULL);
+  }
+  set_bit(m0, m1, k);
   double s;
   const int sg = seg_index(P.fd, r2 * rsqrt(r2), s);
   double A, Bc, Cc, D;
@@ -146,6 +160,7 @@ __device__ __forceinline__ void density_site(const KP& P, KP* Pp, int par, int d
   const int* offs = FULL ? c_full[par] : c_half[par];
   const double lo = P.cut2_lo, g2 = P.guard_r2;
   double acc = 0.0;
+  unsigned long long m0 = 0, m1 = 0;
   // inner shells: direct fp64 gather, batched; the common case is decided
   // by one compare, the near-cutoff / guard cases drop to decide()
   for (int k0 = 0; k0 < nin; k0 += B) {
@@ -175,8 +190,12 @@ __device__ __forceinline__ void density_site(const KP& P, KP* Pp, int par, int d
         const double dx = xsub(ax, px[b]), dy = xsub(ay, py[b]), dz = xsub(az, pz[b]);
         const int st = decide<FULL>(P, par, k0 + b, j[b], ax, ay, az, px[b], py[b], pz[b], dx, dy,
                                     dz, r2[b]);
-        if (st == 1) in[b] = true;
-        else if (st == 2) acc += guard_rho(Pp, d, j[b], t[b], dx, dy, dz, FULL);
+        if (st == 1) {
+          in[b] = true;
+        } else if (st == 2) {
+          m1 |= kGuardBit;
+          acc += guard_rho(Pp, d, j[b], t[b], dx, dy, dz, FULL);
+        }
       }
     }
 #pragma unroll
@@ -191,6 +210,7 @@ __device__ __forceinline__ void density_site(const KP& P, KP* Pp, int par, int d
         const double rho = fma(fma(fma(tA[b], s[b], tB[b]), s[b], tC[b]), s[b], tD[b]);
         acc += rho;
         if (!FULL) red_add(&P.rho[t[b]], rho);
+        set_bit(m0, m1, k0 + b);
       }
     }
   }
@@ -217,11 +237,15 @@ __device__ __forceinline__ void density_site(const KP& P, KP* Pp, int par, int d
       for (int b = 0; b < 4; ++b)
         if (pass[b])
           acc += skin_density<FULL>(P, Pp, par, k0 + b, d, jj[b], __float_as_int(pf[b].w), ax,
-                                    ay, az);
+                                    ay, az, m0, m1);
     }
   }
   if (FULL) P.rho[d] = acc;
   else red_add(&P.rho[d], acc);
+  if (P.pmask) {
+    P.pmask[2 * (size_t)d] = m0;
+    P.pmask[2 * (size_t)d + 1] = m1;
+  }
 }
 
 // -------------------------------------------------------------------- force
@@ -363,6 +387,111 @@ __device__ __forceinline__ double force_site(const KP& P, KP* Pp, int par, int d
   return e;
 }
 
+// the force pass replaying the density pass's pair mask: no candidate
+// filtering or cutoff decisions, only the in-cutoff pairs, two at a time
+template <bool FULL>
+__device__ __forceinline__ double force_site_mask(const KP& P, KP* Pp, int par, int d,
+                                                  bool live) {
+  const double4* __restrict__ pdf = P.pdf;
+  const int* __restrict__ tgt = P.tgt;
+  const long long S = P.S;
+  double ax = kVacant, ay = 0, az = 0, adf = 0;
+  if (live) ld256(pdf + d, ax, ay, az, adf);
+  if (ax >= kVacantTest) {
+    if (FULL && live) {
+      P.frc[d] = 0.0;
+      P.frc[S + d] = 0.0;
+      P.frc[2 * S + d] = 0.0;
+    }
+    return 0.0;
+  }
+  unsigned long long m0 = P.pmask[2 * (size_t)d], m1 = P.pmask[2 * (size_t)d + 1];
+  const bool guard = (m1 & kGuardBit) != 0;
+  m1 &= ~kGuardBit;
+  const int* offs = FULL ? c_full[par] : c_half[par];
+  const double ih = P.ff.ih;
+  double fx = 0.0, fy = 0.0, fz = 0.0, e = 0.0;
+  while (m0 | m1) {
+    int k[2];
+    bool v[2];
+#pragma unroll
+    for (int b = 0; b < 2; ++b) {
+      v[b] = (m0 | m1) != 0;
+      if (m0) {
+        k[b] = __ffsll(m0) - 1;
+        m0 &= m0 - 1;
+      } else if (m1) {
+        k[b] = 63 + __ffsll(m1);
+        m1 &= m1 - 1;
+      } else {
+        k[b] = 0;
+      }
+    }
+    int j[2], t[2], seg[2];
+    double px[2], py[2], pz[2], pw[2], dx[2], dy[2], dz[2], s[2], ri[2];
+#pragma unroll
+    for (int b = 0; b < 2; ++b) {
+      j[b] = d + offs[k[b]];
+      ld256(pdf + j[b], px[b], py[b], pz[b], pw[b]);
+      t[b] = __ldg(tgt + j[b]);
+    }
+#pragma unroll
+    for (int b = 0; b < 2; ++b) {
+      dx[b] = xsub(ax, px[b]);
+      dy[b] = xsub(ay, py[b]);
+      dz[b] = xsub(az, pz[b]);
+      const double r2 = fma(dz[b], dz[b], fma(dy[b], dy[b], dx[b] * dx[b]));
+      ri[b] = rsqrt(r2);
+      seg[b] = seg_index(P.ff, r2 * ri[b], s[b]);
+    }
+#pragma unroll
+    for (int b = 0; b < 2; ++b) {
+      if (!v[b]) continue;
+      const PairOut o = pair_eval(P.ff.rec + 8 * (size_t)seg[b], s[b], ri[b], ih, adf + pw[b],
+                                  dx[b], dy[b], dz[b]);
+      fx -= o.qx;
+      fy -= o.qy;
+      fz -= o.qz;
+      if (FULL) {
+        e = fma(0.5, o.phi, e);
+      } else {
+        e += o.phi;
+        red_add(&P.frc[t[b]], o.qx);
+        red_add(&P.frc[S + t[b]], o.qy);
+        red_add(&P.frc[2 * S + t[b]], o.qz);
+      }
+    }
+  }
+  if (guard) {  // the guard pairs skipped by the density pass's mask
+    const int n = FULL ? c_full_n[par] : c_half_n[par];
+    for (int kk = 0; kk < n; ++kk) {
+      const int jj = d + offs[kk];
+      double px, py, pz, pw;
+      ld256(pdf + jj, px, py, pz, pw);
+      const double ddx = xsub(ax, px), ddy = xsub(ay, py), ddz = xsub(az, pz);
+      const double r2 = fma(ddz, ddz, fma(ddy, ddy, ddx * ddx));
+      if (decide<FULL>(P, par, kk, jj, ax, ay, az, px, py, pz, ddx, ddy, ddz, r2) != 2) continue;
+      double q[4];
+      if (guard_force(Pp, d, jj, __ldg(tgt + jj), ddx, ddy, ddz, adf + pw, FULL, q)) {
+        fx -= q[0];
+        fy -= q[1];
+        fz -= q[2];
+        e = FULL ? fma(0.5, q[3], e) : e + q[3];
+      }
+    }
+  }
+  if (FULL) {
+    P.frc[d] = fx;
+    P.frc[S + d] = fy;
+    P.frc[2 * S + d] = fz;
+  } else {
+    red_add(&P.frc[d], fx);
+    red_add(&P.frc[S + d], fy);
+    red_add(&P.frc[2 * S + d], fz);
+  }
+  return e;
+}
+
 // persistent CTAs over bricks: warp w owns z-plane w of the brick and sweeps
 // both sublattices (even then odd: balanced half-list lengths 46 + 66)
 __device__ __forceinline__ int next_brick(int* ctr) {
@@ -423,13 +552,36 @@ __global__ void __launch_bounds__(128, 4) k_force_fast(KP P) {
   if ((threadIdx.x & 31) == 0) P.part_pair[(blockIdx.x * blockDim.x + threadIdx.x) >> 5] = e;
 }
 
+template <bool FULL>
+__global__ void __launch_bounds__(128, 5) k_force_mask(KP P) {
+  if (P.st->err || P.st->n_ovl) return;
+  const int nb = brick_count(P.G);
+  double e = 0.0;
+  for (;;) {
+    const int b = next_brick(&P.work[1]);
+    if (b >= nb) break;
+    for (int par = 0; par < 2; ++par) {
+      int d;
+      const bool live = brick_site(P.G, b, par, d);
+      e += force_site_mask<FULL>(P, P.dself, par, d, live);
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
+  if ((threadIdx.x & 31) == 0) P.part_pair[(blockIdx.x * blockDim.x + threadIdx.x) >> 5] = e;
+}
+
 int fast_grid(const KP& P, bool force, int mode) {
   int per_sm = 0;
-  if (force)
+  if (force) {  // one grid for both force variants: the partial-energy count must match
+    int a = 0, b = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-        &per_sm, mode ? (const void*)k_force_fast<true, 2> : (const void*)k_force_fast<false, 2>,
-        128, 0);
-  else
+        &a, mode ? (const void*)k_force_mask<true> : (const void*)k_force_mask<false>, 128, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &b, mode ? (const void*)k_force_fast<true, 2> : (const void*)k_force_fast<false, 2>, 128,
+        0);
+    per_sm = max(a, b);
+  }
+  if (!force)
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(
         &per_sm, mode ? (const void*)k_density_fast<true, 2, 6> : (const void*)k_density_fast<false, 2, 6>,
         128, 0);
@@ -444,7 +596,7 @@ int fast_grid(const KP& P, bool force, int mode) {
 void launch_density_fast(const KP& P, int mode, int grid, cudaStream_t s) {
   static const int batch = [] {
     const char* e = getenv("CBX_DENSITY_BATCH");
-    return e ? atoi(e) : 2;
+    return e ? atoi(e) : 4;
   }();
   if (batch == 4) {
     if (mode) k_density_fast<true, 4, 4><<<grid, 128, 0, s>>>(P);
@@ -455,6 +607,11 @@ void launch_density_fast(const KP& P, int mode, int grid, cudaStream_t s) {
   }
 }
 void launch_force_fast(const KP& P, int mode, int grid, cudaStream_t s) {
+  if (P.use_mask) {
+    if (mode) k_force_mask<true><<<grid, 128, 0, s>>>(P);
+    else k_force_mask<false><<<grid, 128, 0, s>>>(P);
+    return;
+  }
   static const int batch = [] {
     const char* e = getenv("CBX_FORCE_BATCH");
     return e ? atoi(e) : 2;
