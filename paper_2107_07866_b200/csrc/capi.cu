@@ -39,7 +39,8 @@ struct cbx_ctx {
   uint64_t launches = 0;
   int n_ghost = 0;
   bool fast_ok = true;
-  bool mask_valid = false;  // pmask matches the current positions (density ran last)
+  bool mask_valid = false;
+  bool tile_ok = false;  // every offset within the 2-cell tile halo  // pmask matches the current positions (density ran last)
   double band = 0.0;
 
   template <class T>
@@ -203,6 +204,7 @@ void seq_force(cbx_ctx* c) {
   launch_clash_zero(c->P, 1, c->stream);
   KP q = c->P;
   q.use_mask = c->mask_valid ? 1 : 0;
+  cudaMemsetAsync(c->P.part_pair, 0, c->P.n_part * sizeof(double), c->stream);
   launch_force(q, c->mode, c->stream);
   launch_clash_force(c->P, c->stream);
   c->launches += 3;
@@ -694,6 +696,7 @@ CBX_API cbx_status cbx_create(const cbx_box* box, const cbx_potential* pot,
     // potential cutoff first ("inner"), index-skin sites after (stencil_fast.cuh)
     std::vector<int> hd[2], fd[2];
     std::vector<long long> ff[2];
+    std::vector<int4> h4[2], f4[2];
     int hin[2] = {0, 0}, fin[2] = {0, 0};
     for (int par = 0; par < 2; ++par) {
       auto delta = [&](const Offset& o) {
@@ -714,10 +717,14 @@ CBX_API cbx_status cbx_create(const cbx_box* box, const cbx_potential* pot,
           if (dist2(o) <= pot->cutoff * pot->cutoff) ++nin;
         return v;
       };
-      for (const Offset& o : order(c->offs.half[par], hin[par])) hd[par].push_back(delta(o));
+      for (const Offset& o : order(c->offs.half[par], hin[par])) {
+        hd[par].push_back(delta(o));
+        h4[par].push_back(make_int4(o.dx, o.dy, o.dz, (par ^ o.cross) - par));
+      }
       for (const Offset& o : order(c->offs.full[par], fin[par])) {
         fd[par].push_back(delta(o));
         ff[par].push_back(o.flat);
+        f4[par].push_back(make_int4(o.dx, o.dy, o.dz, (par ^ o.cross) - par));
       }
     }
     const int* hp[2] = {hd[0].data(), hd[1].data()};
@@ -726,6 +733,11 @@ CBX_API cbx_status cbx_create(const cbx_box* box, const cbx_potential* pot,
     const int hn[2] = {(int)hd[0].size(), (int)hd[1].size()};
     const int fn[2] = {(int)fd[0].size(), (int)fd[1].size()};
     upload_offsets(hp, hn, fp, fn, fl, hin, fin, c->stream);
+    {
+      const int4* h4p[2] = {h4[0].data(), h4[1].data()};
+      const int4* f4p[2] = {f4[0].data(), f4[1].data()};
+      c->tile_ok = upload_tile_offsets(h4p, hn, f4p, fn, c->stream);
+    }
     cuda_check(cudaStreamSynchronize(c->stream), "offset upload");
     // ghost list and owner map
     const long long S = c->S;
@@ -826,6 +838,11 @@ CBX_API cbx_status cbx_create(const cbx_box* box, const cbx_potential* pot,
     setup_fast(c.get());
     P.st = c->alloc<DevStatus>(1);
     P.dself = c->alloc<KP>(1);
+    P.xp = std::getenv("CBX_XP") ? std::atoi(std::getenv("CBX_XP")) : 0;
+    {
+      const char* e = std::getenv("CBX_TILE");
+      P.use_tile = c->tile_ok && P.pmask != nullptr && (e ? std::atoi(e) != 0 : true);
+    }
     {
       const int maxn = std::max(std::max(fd[0].size(), fd[1].size()), std::max(hd[0].size(), hd[1].size()));
       P.pmask = maxn <= 126 ? c->alloc<unsigned long long>(2 * S) : nullptr;
@@ -840,7 +857,7 @@ CBX_API cbx_status cbx_create(const cbx_box* box, const cbx_potential* pot,
     cudaMemset(P.tag, 0, S * sizeof(unsigned long long));
     cudaMemset(P.head, 0xff, S * sizeof(int));
     launch_uf_refresh(P, c->stream);
-    P.n_pair_part = pair_partials(P, c->mode);
+    P.n_pair_part = P.n_part;
     sync_kp(c.get());
     c->hst = DevStatus{};
     c->hst.dt_next = 1e-3;
@@ -879,7 +896,6 @@ CBX_API cbx_status cbx_set_stencil(cbx_ctx* c, cbx_stencil mode) {
     if (c->mode != mode) drop_graph(c);
     c->mode = mode;
     c->mask_valid = false;
-    c->P.n_pair_part = pair_partials(c->P, mode);
     sync_kp(c);
   });
 }

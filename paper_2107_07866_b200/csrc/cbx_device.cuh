@@ -78,6 +78,8 @@ struct KP {
   struct KP* dself;        // this parameter block in device memory (guard paths)
   unsigned long long* pmask;  // [S][2] pair masks from the density pass (or null)
   int use_mask;               // force pass replays pmask (set per launch by the host)
+  int xp;                     // timing experiments only (CBX_XP): 1 fixed table row, 2 no RED
+  int use_tile;               // shared-memory tiled stencils (stencil_tile.cuh)
   int n_pair_part;         // partials written by the force pass
   double accel, mv2;  // units::accel_factor, units::mv2_to_ev (units.h:17-24)
   long long S;  // 2*NC sites
@@ -173,6 +175,8 @@ void upload_offsets(const int* half_dev[2], const int half_n[2], const int* full
 int eam_blocks(const KP& P);
 int pair_partials(const KP& P, int mode);
 void launch_uf_refresh(const KP& P, cudaStream_t s);
+bool upload_tile_offsets(const int4* half[2], const int half_n[2], const int4* full[2],
+                         const int full_n[2], cudaStream_t s);
 int embed_blocks(const KP& P);
 
 }  // namespace cbx

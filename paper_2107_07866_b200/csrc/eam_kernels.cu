@@ -21,6 +21,7 @@
 // ordinary fp64 (within 1e-10 of the reference, tests/test_gpu_parity.py).
 #include <cstdio>
 #include <cstdlib>
+#include <vector>
 
 #include "cbx_device.cuh"
 
@@ -430,15 +431,42 @@ __global__ void __launch_bounds__(256) k_clash(KP P) {
 }
 
 #include "stencil_fast.cuh"
+#include "stencil_tile.cuh"
+
+// tile-space deltas of the ordered offset lists: (dx, dy, dz, q - p) each
+bool upload_tile_offsets(const int4* half[2], const int half_n[2], const int4* full[2],
+                         const int full_n[2], cudaStream_t s) {
+  std::vector<int> h[2], f[2];
+  bool ok = true;
+  auto td = [&](const int4& o) {
+    ok &= abs(o.x) <= kTH && abs(o.y) <= kTH && abs(o.z) <= kTH;
+    return o.w * kTC + (o.z * kTY + o.y) * kTX + o.x;
+  };
+  for (int p = 0; p < 2; ++p) {
+    for (int i = 0; i < half_n[p]; ++i) h[p].push_back(td(half[p][i]));
+    for (int i = 0; i < full_n[p]; ++i) f[p].push_back(td(full[p][i]));
+  }
+  if (!ok) return false;
+  for (int p = 0; p < 2; ++p) {
+    cudaMemcpyToSymbolAsync(c_half_tile, h[p].data(), h[p].size() * sizeof(int),
+                            p * kMaxOffsets * sizeof(int), cudaMemcpyHostToDevice, s);
+    cudaMemcpyToSymbolAsync(c_full_tile, f[p].data(), f[p].size() * sizeof(int),
+                            p * kMaxOffsets * sizeof(int), cudaMemcpyHostToDevice, s);
+  }
+  cudaStreamSynchronize(s);
+  return true;
+}
 
 // ------------------------------------------------------------- launchers
 // mode: 0 fast half list (Newton-3), 1 fast full list, 2 reference-literal half list
 void launch_density(const KP& P, int mode, cudaStream_t s) {
   if (mode == 2) k_density<false><<<eam_blocks(P), 256, 0, s>>>(P);
+  else if (P.use_tile) launch_density_tile(P, mode, s);
   else launch_density_fast(P, mode, fast_grid(P, false, mode), s);
 }
 void launch_force(const KP& P, int mode, cudaStream_t s) {
   if (mode == 2) k_force<false><<<eam_blocks(P), 256, 0, s>>>(P);
+  else if (P.use_tile && P.use_mask) launch_force_tile(P, mode, tile_grid(P, true, mode), s);
   else launch_force_fast(P, mode, fast_grid(P, true, mode), s);
 }
 int pair_partials(const KP& P, int mode) {

@@ -447,8 +447,8 @@ __device__ __forceinline__ double force_site_mask(const KP& P, KP* Pp, int par, 
 #pragma unroll
     for (int b = 0; b < 2; ++b) {
       if (!v[b]) continue;
-      const PairOut o = pair_eval(P.ff.rec + 8 * (size_t)seg[b], s[b], ri[b], ih, adf + pw[b],
-                                  dx[b], dy[b], dz[b]);
+      const PairOut o = pair_eval(P.ff.rec + 8 * (size_t)((P.xp & 1) ? 2000 + (k[b] & 7) : seg[b]),
+                                  s[b], ri[b], ih, adf + pw[b], dx[b], dy[b], dz[b]);
       fx -= o.qx;
       fy -= o.qy;
       fz -= o.qz;
@@ -456,9 +456,11 @@ __device__ __forceinline__ double force_site_mask(const KP& P, KP* Pp, int par, 
         e = fma(0.5, o.phi, e);
       } else {
         e += o.phi;
-        red_add(&P.frc[t[b]], o.qx);
-        red_add(&P.frc[S + t[b]], o.qy);
-        red_add(&P.frc[2 * S + t[b]], o.qz);
+        if (!(P.xp & 2)) {
+          red_add(&P.frc[t[b]], o.qx);
+          red_add(&P.frc[S + t[b]], o.qy);
+          red_add(&P.frc[2 * S + t[b]], o.qz);
+        }
       }
     }
   }
