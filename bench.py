@@ -222,7 +222,8 @@ def run_ours(args, w, path, ws, rank, local):
            "roofline": roofline, "e2e": e2e, "gpu_launches": launches,
            "clocks": clocks.summary(),
            "kernels_ms_per_step": {k: v / K for k, v in t.items()},
-           "fp64_peak_probe": {"tflops": peak.value, "sm_mhz_est": mhz.value}}
+           "fp64_peak_probe": {"tflops": peak.value, "sm_mhz_est": mhz.value},
+           "engine": dev.describe()}
     return res
 
 

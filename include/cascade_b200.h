@@ -179,6 +179,8 @@ CBX_API cbx_status cbx_last_timings(cbx_ctx* ctx, double out_ms[8]);
 CBX_API cbx_status cbx_enable_timing(cbx_ctx* ctx, int on);
 CBX_API cbx_status cbx_count_pairs(cbx_ctx* ctx, uint64_t out[2]);
 CBX_API cbx_status cbx_kernel_launches(cbx_ctx* ctx, uint64_t* n); /* cumulative */
+/* JSON description of the context's kernel configuration */
+CBX_API cbx_status cbx_describe(cbx_ctx* ctx, char* buf, long n);
 /* benchmark loop: nsteps fixed-dt steps, each preceded (outside the timed
  * region) by a write of flush_mb MB to evict L2; per-step CUDA events on the
  * context stream.  out_ms = {density, embed, force, store, integrate, step,

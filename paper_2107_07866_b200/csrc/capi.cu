@@ -840,13 +840,14 @@ CBX_API cbx_status cbx_create(const cbx_box* box, const cbx_potential* pot,
     P.dself = c->alloc<KP>(1);
     P.xp = std::getenv("CBX_XP") ? std::atoi(std::getenv("CBX_XP")) : 0;
     {
-      const char* e = std::getenv("CBX_TILE");
-      P.use_tile = c->tile_ok && P.pmask != nullptr && (e ? std::atoi(e) != 0 : true);
-    }
-    {
       const int maxn = std::max(std::max(fd[0].size(), fd[1].size()), std::max(hd[0].size(), hd[1].size()));
       P.pmask = maxn <= 126 ? c->alloc<unsigned long long>(2 * S) : nullptr;
     }
+    {
+      const char* e = std::getenv("CBX_TILE");
+      P.use_tile = c->tile_ok && P.pmask != nullptr && (e ? std::atoi(e) != 0 : true);
+    }
+
     c->d_defects = c->alloc<unsigned long long>(4);
     // empty store: every slot vacant
     std::vector<double4> vac(S, make_double4(kVacant, kVacant, kVacant, 0.0));
@@ -1218,6 +1219,23 @@ CBX_API cbx_status cbx_bench_steps(cbx_ctx* c, double dt, long nsteps, double fl
     sync_status(c);
     raise_device_error(c, true);
     for (int k = 0; k < 8; ++k) out_ms[k] = acc[k];
+  });
+}
+
+CBX_API cbx_status cbx_describe(cbx_ctx* c, char* buf, long n) {
+  return guarded(c, [&] {
+    std::snprintf(buf, n,
+                  "{\"stencil\": %d, \"fast_ok\": %d, \"tile_ok\": %d, \"use_tile\": %d, "
+                  "\"pair_mask\": %d, \"slots\": %lld, \"ghost_sites\": %d, "
+                  "\"clash_capacity\": %d, \"band_A2\": %.3e, \"sm_count\": %d}",
+                  c->mode, (int)c->fast_ok, (int)c->tile_ok, c->P.use_tile,
+                  (int)(c->P.pmask != nullptr), c->S, c->n_ghost, c->P.cap_clash, c->band,
+                  [] {
+                    int d = 0, n = 0;
+                    cudaGetDevice(&d);
+                    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, d);
+                    return n;
+                  }());
   });
 }
 

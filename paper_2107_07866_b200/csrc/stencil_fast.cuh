@@ -572,6 +572,197 @@ __global__ void __launch_bounds__(128, 5) k_force_mask(KP P) {
   if ((threadIdx.x & 31) == 0) P.part_pair[(blockIdx.x * blockDim.x + threadIdx.x) >> 5] = e;
 }
 
+
+// force pass with the spline window in shared memory: 64-byte records of
+// segments [seg_lo, nseg] are staged once per CTA, chunk c of record i at
+// 16-byte slot 4 i + (c ^ (i & 3)) so random records spread over all banks;
+// pairs below seg_lo (r < ~1.6 A, cascade cores only) read the global table.
+constexpr int kSmemTabSegs = 3500;  // 3500 x 64 B = 224,000 B
+__device__ __forceinline__ double2 tab_chunk(const double2* T, int i, int c) {
+  return T[4 * i + (c ^ (i & 3))];
+}
+
+template <bool FULL>
+__device__ __forceinline__ double force_site_smtab(const KP& P, KP* Pp, const double2* T,
+                                                   int seg_lo, int par, int d, bool live) {
+  const double4* __restrict__ pdf = P.pdf;
+  const int* __restrict__ tgt = P.tgt;
+  const long long S = P.S;
+  double ax = kVacant, ay = 0, az = 0, adf = 0;
+  if (live) ld256(pdf + d, ax, ay, az, adf);
+  if (ax >= kVacantTest) {
+    if (FULL && live) {
+      P.frc[d] = 0.0;
+      P.frc[S + d] = 0.0;
+      P.frc[2 * S + d] = 0.0;
+    }
+    return 0.0;
+  }
+  unsigned long long m0 = P.pmask[2 * (size_t)d], m1 = P.pmask[2 * (size_t)d + 1];
+  const bool guard = (m1 & kGuardBit) != 0;
+  m1 &= ~kGuardBit;
+  const int* offs = FULL ? c_full[par] : c_half[par];
+  const double ih = P.ff.ih;
+  double fx = 0.0, fy = 0.0, fz = 0.0, e = 0.0;
+  while (m0 | m1) {
+    int k[2];
+    bool v[2];
+#pragma unroll
+    for (int b = 0; b < 2; ++b) {
+      v[b] = (m0 | m1) != 0;
+      if (m0) {
+        k[b] = __ffsll(m0) - 1;
+        m0 &= m0 - 1;
+      } else if (m1) {
+        k[b] = 63 + __ffsll(m1);
+        m1 &= m1 - 1;
+      } else {
+        k[b] = 0;
+      }
+    }
+    int j[2], t[2], seg[2];
+    double px[2], py[2], pz[2], pw[2], dx[2], dy[2], dz[2], s[2], ri[2];
+#pragma unroll
+    for (int b = 0; b < 2; ++b) {
+      j[b] = d + offs[k[b]];
+      ld256(pdf + j[b], px[b], py[b], pz[b], pw[b]);
+      t[b] = __ldg(tgt + j[b]);
+    }
+#pragma unroll
+    for (int b = 0; b < 2; ++b) {
+      dx[b] = xsub(ax, px[b]);
+      dy[b] = xsub(ay, py[b]);
+      dz[b] = xsub(az, pz[b]);
+      const double r2 = fma(dz[b], dz[b], fma(dy[b], dy[b], dx[b] * dx[b]));
+      ri[b] = rsqrt(r2);
+      seg[b] = seg_index(P.ff, r2 * ri[b], s[b]);
+    }
+#pragma unroll
+    for (int b = 0; b < 2; ++b) {
+      if (!v[b]) continue;
+      double zA, zB, zC, zD, qA, qB, qC, qD;
+      const int li = seg[b] - seg_lo;
+      if (li >= 0) {
+        const double2 c0 = tab_chunk(T, li, 0), c1 = tab_chunk(T, li, 1),
+                      c2 = tab_chunk(T, li, 2), c3 = tab_chunk(T, li, 3);
+        zA = c0.x; zB = c0.y; zC = c1.x; zD = c1.y; qA = c2.x; qB = c2.y; qC = c3.x; qD = c3.y;
+      } else {
+        const double* rec = P.ff.rec + 8 * (size_t)seg[b];
+        ld256(rec, zA, zB, zC, zD);
+        ld256(rec + 4, qA, qB, qC, qD);
+      }
+      (void)qD;
+      const double sb = s[b], s15 = 1.5 * sb, s2 = sb + sb;
+      const double z = fma(fma(fma(zA, sb, zB), sb, zC), sb, zD);
+      const double zs = fma(fma(zA, s15, zB), s2, zC);
+      const double ps = fma(fma(qA, s15, qB), s2, qC);
+      const double phi = z * ri[b];
+      const double dphi = fma(zs, ih, -phi) * ri[b];
+      const double mfp = fma((adf + pw[b]) * ps, ih, dphi) * ri[b];
+      const double qx = mfp * dx[b], qy = mfp * dy[b], qz = mfp * dz[b];
+      fx -= qx;
+      fy -= qy;
+      fz -= qz;
+      if (FULL) {
+        e = fma(0.5, phi, e);
+      } else {
+        e += phi;
+        red_add(&P.frc[t[b]], qx);
+        red_add(&P.frc[S + t[b]], qy);
+        red_add(&P.frc[2 * S + t[b]], qz);
+      }
+    }
+  }
+  if (guard) {
+    const int n = FULL ? c_full_n[par] : c_half_n[par];
+    for (int kk = 0; kk < n; ++kk) {
+      const int jj = d + offs[kk];
+      double px, py, pz, pw;
+      ld256(pdf + jj, px, py, pz, pw);
+      const double ddx = xsub(ax, px), ddy = xsub(ay, py), ddz = xsub(az, pz);
+      const double r2 = fma(ddz, ddz, fma(ddy, ddy, ddx * ddx));
+      if (decide<FULL>(P, par, kk, jj, ax, ay, az, px, py, pz, ddx, ddy, ddz, r2) != 2) continue;
+      double q[4];
+      if (guard_force(Pp, d, jj, __ldg(tgt + jj), ddx, ddy, ddz, adf + pw, FULL, q)) {
+        fx -= q[0];
+        fy -= q[1];
+        fz -= q[2];
+        e = FULL ? fma(0.5, q[3], e) : e + q[3];
+      }
+    }
+  }
+  if (FULL) {
+    P.frc[d] = fx;
+    P.frc[S + d] = fy;
+    P.frc[2 * S + d] = fz;
+  } else {
+    red_add(&P.frc[d], fx);
+    red_add(&P.frc[S + d], fy);
+    red_add(&P.frc[2 * S + d], fz);
+  }
+  return e;
+}
+
+// 512 threads = 4 groups of 4 warps, each group on its own brick
+__device__ __forceinline__ int next_brick_group(int* ctr, int group, volatile int* slot) {
+  asm volatile("bar.sync %0, 128;" ::"r"(group + 1));
+  if ((threadIdx.x & 127) == 0) slot[group] = atomicAdd(ctr, 1);
+  asm volatile("bar.sync %0, 128;" ::"r"(group + 1));
+  return slot[group];
+}
+
+template <bool FULL>
+__global__ void __launch_bounds__(512, 1) k_force_smtab(KP P) {
+  if (P.st->err || P.st->n_ovl) return;
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ int s_slot[4];
+  double2* T = reinterpret_cast<double2*>(smem);
+  const int nseg = P.ff.nseg;  // records 0..nseg (padded)
+  const int seg_lo = max(0, nseg + 1 - kSmemTabSegs);
+  const int nrec = nseg + 1 - seg_lo;
+  for (int q = threadIdx.x; q < 4 * nrec; q += blockDim.x) {
+    const int i = q >> 2, c = q & 3;
+    T[4 * i + (c ^ (i & 3))] = reinterpret_cast<const double2*>(P.ff.rec + 8 * (size_t)(seg_lo + i))[c];
+  }
+  __syncthreads();
+  const int group = threadIdx.x >> 7;
+  const int nb = brick_count(P.G);
+  double e = 0.0;
+  for (;;) {
+    const int b = next_brick_group(&P.work[1], group, s_slot);
+    if (b >= nb) break;
+    for (int par = 0; par < 2; ++par) {
+      const int lt = threadIdx.x & 127;
+      const int lane = lt & 31, w = lt >> 5;
+      const Geo& G = P.G;
+      const int nbx = (G.bx + kBrickX - 1) / kBrickX, nby = (G.by + kBrickY - 1) / kBrickY;
+      const int cx = (b % nbx) * kBrickX + (lane & 7), cy = ((b / nbx) % nby) * kBrickY + (lane >> 3),
+                cz = (b / (nbx * nby)) * kBrickZ + w;
+      const bool live = cx < G.bx && cy < G.by && cz < G.bz;
+      const int d = live ? (int)(par * G.NC + cell_of(cx + G.g, cy + G.g, cz + G.g, G)) : 0;
+      e += force_site_smtab<FULL>(P, P.dself, T, seg_lo, par, d, live);
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
+  if ((threadIdx.x & 31) == 0) P.part_pair[(blockIdx.x * blockDim.x + threadIdx.x) >> 5] = e;
+}
+
+void launch_force_smtab(const KP& P, int mode, cudaStream_t s) {
+  const size_t bytes = (size_t)kSmemTabSegs * 64;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_force_smtab<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    cudaFuncSetAttribute(k_force_smtab<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    attr = true;
+  }
+  int sms = 148, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int g = max(1, min(sms, (brick_count(P.G) + 3) / 4));
+  if (mode) k_force_smtab<true><<<g, 512, bytes, s>>>(P);
+  else k_force_smtab<false><<<g, 512, bytes, s>>>(P);
+}
+
 int fast_grid(const KP& P, bool force, int mode) {
   int per_sm = 0;
   if (force) {  // one grid for both force variants: the partial-energy count must match
@@ -609,6 +800,10 @@ void launch_density_fast(const KP& P, int mode, int grid, cudaStream_t s) {
   }
 }
 void launch_force_fast(const KP& P, int mode, int grid, cudaStream_t s) {
+  if (P.use_mask && (P.xp & 4)) {
+    launch_force_smtab(P, mode, s);
+    return;
+  }
   if (P.use_mask) {
     if (mode) k_force_mask<true><<<grid, 128, 0, s>>>(P);
     else k_force_mask<false><<<grid, 128, 0, s>>>(P);

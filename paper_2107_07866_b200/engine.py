@@ -325,6 +325,12 @@ class DeviceStore:
         self._check(self.lib.cbx_count_pairs(self.h, out))
         return int(out[0]), int(out[1])
 
+    def describe(self) -> dict:
+        import json
+        buf = C.create_string_buffer(1024)
+        self._check(self.lib.cbx_describe(self.h, buf, 1024))
+        return json.loads(buf.value.decode())
+
     def kernel_launches(self) -> int:
         n = C.c_uint64()
         self._check(self.lib.cbx_kernel_launches(self.h, C.byref(n)))
