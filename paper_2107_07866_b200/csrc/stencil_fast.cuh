@@ -32,12 +32,13 @@
 
 __device__ __forceinline__ void ld256(const void* p, double& a, double& b, double& c,
                                       double& d) {
-  asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
-               : "=d"(a), "=d"(b), "=d"(c), "=d"(d)
-               : "l"(p));
+  // not volatile: a pure read of data that is constant during the kernel,
+  // free to be scheduled early by the compiler
+  asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(p));
 }
 __device__ __forceinline__ void red_add(double* p, double v) {
-  asm volatile("red.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+  // no "memory" clobber: reductions need no ordering within the pass
+  asm volatile("red.global.add.f64 [%0], %1;" ::"l"(p), "d"(v));
 }
 
 constexpr double kTwo52 = 4503599627370496.0;
@@ -444,22 +445,35 @@ __device__ __forceinline__ double force_site_mask(const KP& P, KP* Pp, int par, 
       ri[b] = rsqrt(r2);
       seg[b] = seg_index(P.ff, r2 * ri[b], s[b]);
     }
+    double zA[2], zB[2], zC[2], zD[2], qA[2], qB[2], qC[2], qD[2];
 #pragma unroll
     for (int b = 0; b < 2; ++b) {
-      if (!v[b]) continue;
-      const PairOut o = pair_eval(P.ff.rec + 8 * (size_t)((P.xp & 1) ? 2000 + (k[b] & 7) : seg[b]),
-                                  s[b], ri[b], ih, adf + pw[b], dx[b], dy[b], dz[b]);
-      fx -= o.qx;
-      fy -= o.qy;
-      fz -= o.qz;
+      const double* rec = P.ff.rec + 8 * (size_t)((P.xp & 1) ? 2000 + (k[b] & 7) : seg[b]);
+      ld256(rec, zA[b], zB[b], zC[b], zD[b]);
+      ld256(rec + 4, qA[b], qB[b], qC[b], qD[b]);
+    }
+#pragma unroll
+    for (int b = 0; b < 2; ++b) {
+      const double sb = s[b], s15 = 1.5 * sb, s2 = sb + sb;
+      const double z = fma(fma(fma(zA[b], sb, zB[b]), sb, zC[b]), sb, zD[b]);
+      const double zs = fma(fma(zA[b], s15, zB[b]), s2, zC[b]);  // dz/ds
+      const double ps = fma(fma(qA[b], s15, qB[b]), s2, qC[b]);  // drho/ds
+      const double phi = z * ri[b];
+      // phi' = (z' - phi)/r;  -fp = ((dFa + dFp) rho' + phi')/r;  d/dr = ih d/ds
+      const double dphi = fma(zs, ih, -phi) * ri[b];
+      const double mfp = v[b] ? fma((adf + pw[b]) * ps, ih, dphi) * ri[b] : 0.0;
+      const double qx = mfp * dx[b], qy = mfp * dy[b], qz = mfp * dz[b];
+      fx -= qx;
+      fy -= qy;
+      fz -= qz;
       if (FULL) {
-        e = fma(0.5, o.phi, e);
-      } else {
-        e += o.phi;
+        e = fma(0.5, v[b] ? phi : 0.0, e);
+      } else if (v[b]) {
+        e += phi;
         if (!(P.xp & 2)) {
-          red_add(&P.frc[t[b]], o.qx);
-          red_add(&P.frc[S + t[b]], o.qy);
-          red_add(&P.frc[2 * S + t[b]], o.qz);
+          red_add(&P.frc[t[b]], qx);
+          red_add(&P.frc[S + t[b]], qy);
+          red_add(&P.frc[2 * S + t[b]], qz);
         }
       }
     }
