@@ -845,7 +845,7 @@ CBX_API cbx_status cbx_create(const cbx_box* box, const cbx_potential* pot,
     }
     {
       const char* e = std::getenv("CBX_TILE");
-      P.use_tile = c->tile_ok && P.pmask != nullptr && (e ? std::atoi(e) != 0 : true);
+      P.use_tile = c->tile_ok && P.pmask != nullptr && (e ? std::atoi(e) != 0 : false);
     }
 
     c->d_defects = c->alloc<unsigned long long>(4);
