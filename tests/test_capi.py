@@ -108,3 +108,18 @@ def test_create_without_gpu_fails_loudly(tables):
     from paper_2107_07866_b200._lib import CbxError
     with pytest.raises(CbxError):
         DeviceStore((4, 4, 4, 2.855, 3), EamPotential.load(tables["baseline"]))
+
+
+def test_cxx_host_header_compiles_and_runs(tmp_path, tables):
+    """include/cascade_b200.hpp: the C++ mirror compiles against the C ABI
+    and rethrows the reference's exception types (host-side calls only)"""
+    from paper_2107_07866_b200 import _lib
+    _lib.load()
+    exe = str(tmp_path / "cxx_host")
+    libdir = os.path.dirname(_lib.LIB_PATH)
+    subprocess.run(["g++", "-std=c++17", "-O1", "-I", os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "examples", "cxx_host.cpp"), "-L", libdir,
+                    "-l:libcascade_b200.so", f"-Wl,-rpath,{libdir}", "-o", exe], check=True)
+    out = subprocess.run([exe, tables["baseline"]], capture_output=True, text=True, check=True)
+    assert "offsets 112/112 half 46/66" in out.stdout
+    assert "runtime_error: cannot open potential file" in out.stdout

@@ -375,3 +375,19 @@ def test_bench_steps_timed_graph(cuda, tables):
     assert out[6] == 10 and out[5] > 0 and out[2] > 0 and out[0] > 0
     assert dev.state()["step"] == ref.state()["step"]
     assert_store_parity(ref.store(), dev.download(), pos_tol=1e-9, rel=1e-8)
+
+
+def test_cxx_host_on_device(cuda, tables, tmp_path):
+    """the C++ mirror drives a device run (Simulation ctor + 10 steps)"""
+    import os
+    import subprocess
+    from paper_2107_07866_b200 import _lib
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = str(tmp_path / "cxx_host")
+    libdir = os.path.dirname(_lib.LIB_PATH)
+    subprocess.run(["g++", "-std=c++17", "-O1", "-I", os.path.join(root, "include"),
+                    os.path.join(root, "examples", "cxx_host.cpp"), "-L", libdir,
+                    "-l:libcascade_b200.so", f"-Wl,-rpath,{libdir}", "-o", exe], check=True)
+    out = subprocess.run([exe, tables["baseline"], "gpu"], capture_output=True, text=True,
+                         check=True).stdout
+    assert "atoms 1024" in out and "-> step 10" in out
