@@ -1,0 +1,86 @@
+"""Summarise ncu captures into the committed profiles/ files.
+
+    python profiles/summarize.py <report.ncu-rep> <launches.csv> <tag>
+
+Writes profiles/<tag>_kernels.md (per-kernel key metrics of the --set full
+capture), profiles/<tag>_launches.csv (launch list: kernel, duration) and
+profiles/latest_traffic.json (dram bytes per launch of the dominant kernels,
+read by bench.py for roofline.traffic).
+"""
+import csv
+import io
+import json
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+KEYS = [
+    ("gpu__time_duration.sum", "duration"),
+    ("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "fp64 pipe % (active)"),
+    ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue active %"),
+    ("sm__warps_active.avg.pct_of_peak_sustained_active", "warps active %"),
+    ("l1tex__throughput.avg.pct_of_peak_sustained_active", "L1 throughput %"),
+    ("l1tex__t_sector_pipe_lsu_mem_global_op_ld_hit_rate.pct", "L1 ld hit %"),
+    ("lts__t_sector_hit_rate.pct", "L2 hit %"),
+    ("dram__bytes_read.sum", "dram read"),
+    ("dram__bytes_write.sum", "dram write"),
+    ("smsp__inst_executed.sum", "warp instructions"),
+    ("l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum", "L1 ld sectors"),
+    ("l1tex__t_sectors_pipe_lsu_mem_global_op_red.sum", "RED sectors"),
+    ("launch__registers_per_thread", "registers"),
+    ("launch__grid_size", "grid"),
+]
+
+
+def to_bytes(v, unit):
+    f = float(v.replace(",", ""))
+    return f * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
+
+
+def main():
+    rep, launches, tag = sys.argv[1:4]
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                         text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    hdr, units = rows[0], rows[1]
+    lines = [f"# ncu --set full summary ({tag})", "",
+             "| kernel | " + " | ".join(k[1] for k in KEYS) + " |",
+             "|---|" + "---|" * len(KEYS)]
+    traffic = {}
+    for r in rows[2:]:
+        name = r[hdr.index("Kernel Name")]
+        vals = []
+        for k, _ in KEYS:
+            if k in hdr:
+                i = hdr.index(k)
+                vals.append(f"{r[i]} {units[i]}".strip())
+            else:
+                vals.append("-")
+        lines.append(f"| `{name[:60]}` | " + " | ".join(vals) + " |")
+        i_r, i_w = hdr.index("dram__bytes_read.sum"), hdr.index("dram__bytes_write.sum")
+        tb = to_bytes(r[i_r], units[i_r]) + to_bytes(r[i_w], units[i_w])
+        key = "force_traffic" if "force" in name else ("density_traffic" if "density" in name
+                                                       else None)
+        if key and key not in traffic:
+            traffic[key] = tb
+    open(os.path.join(HERE, f"{tag}_kernels.md"), "w").write("\n".join(lines) + "\n")
+    traffic["source"] = f"profiles/{tag}_kernels.md (dram__bytes_read.sum + dram__bytes_write.sum)"
+    json.dump(traffic, open(os.path.join(HERE, "latest_traffic.json"), "w"), indent=1)
+    # launch list: kernel name, duration
+    out = []
+    with open(launches) as f:
+        text = f.read()
+    start = text.find('"ID"')
+    for r in csv.DictReader(io.StringIO(text[start:])):
+        if r.get("Metric Name") == "gpu__time_duration.sum":
+            out.append((r["Kernel Name"][:80], r["Metric Value"], r["Metric Unit"]))
+    with open(os.path.join(HERE, f"{tag}_launches.csv"), "w") as f:
+        w = csv.writer(f)
+        w.writerow(["kernel", "duration", "unit"])
+        w.writerows(out)
+    print("wrote", tag, len(out), "launches")
+
+
+if __name__ == "__main__":
+    main()
