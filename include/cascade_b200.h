@@ -191,6 +191,32 @@ CBX_API cbx_status cbx_bench_steps(cbx_ctx* ctx, double dt, long nsteps, double 
  * SMs, timed with CUDA events (TFLOP/s, DFMA = 2 flops) */
 CBX_API cbx_status cbx_fp64_peak(int device, double* tflops, double* sm_mhz);
 
+/* ---- z-slab domain decomposition (multi-GPU) ------------- */
+/* rank r of n owns global interior z planes [r*bz/n, (r+1)*bz/n) of the
+ * global box; positions, hashes and keys stay in the global frame.  A step
+ * is driven phase by phase by the host with the exchanges in between
+ * (paper_2107_07866_b200/slab.py):
+ *   phase 0 -> pack/unpack MIGRANTS(0) -> phase 1 -> POS(1) -> phase 2 ->
+ *   RHO(2) -> phase 3 -> DF(3) -> phase 4 -> FRC(4) -> phase 5 -> all-reduce
+ *   of cbx_slab_local_state -> cbx_slab_commit.
+ * pack: dir -1 toward the rank below, +1 above; unpack: from -1 / +1.
+ * Buffers are device memory of cbx_slab_buffer_bytes(kind) bytes. */
+CBX_API cbx_status cbx_create_slab(const cbx_box* global_box, const cbx_potential* pot,
+                                   const cbx_offsets* idx, int rank, int nranks, int device,
+                                   cbx_ctx** out);
+CBX_API cbx_status cbx_slab_info(cbx_ctx* ctx, long out[8]);
+CBX_API long cbx_slab_buffer_bytes(cbx_ctx* ctx, int kind);
+CBX_API cbx_status cbx_slab_phase(cbx_ctx* ctx, int phase, double dt);
+CBX_API cbx_status cbx_slab_pack(cbx_ctx* ctx, int kind, int dir, void* dev_buf, long cap,
+                                 long* bytes);
+CBX_API cbx_status cbx_slab_unpack(cbx_ctx* ctx, int kind, int from, const void* dev_buf,
+                                   long bytes);
+CBX_API cbx_status cbx_slab_local_state(cbx_ctx* ctx, double out[8]);
+CBX_API cbx_status cbx_slab_commit(cbx_ctx* ctx, const double in[4]);
+CBX_API cbx_status cbx_upload_store_global(cbx_ctx* ctx, const cbx_store* global_store);
+CBX_API cbx_status cbx_download_store_global(cbx_ctx* ctx, cbx_store* global_store,
+                                             long* n_clash_inout);
+
 #ifdef __cplusplus
 }
 #endif

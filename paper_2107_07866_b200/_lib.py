@@ -134,6 +134,17 @@ SIGNATURES = [
     ("cbx_describe", C.c_int, [_P, C.c_char_p, C.c_long]),
     ("cbx_bench_steps", C.c_int, [_P, _D, C.c_long, _D, C.POINTER(C.c_double)]),
     ("cbx_fp64_peak", C.c_int, [C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+    ("cbx_create_slab", C.c_int, [C.POINTER(Box), C.POINTER(Potential), C.POINTER(Offsets),
+                                  C.c_int, C.c_int, C.c_int, C.POINTER(_P)]),
+    ("cbx_slab_info", C.c_int, [_P, C.POINTER(C.c_long)]),
+    ("cbx_slab_buffer_bytes", C.c_long, [_P, C.c_int]),
+    ("cbx_slab_phase", C.c_int, [_P, C.c_int, _D]),
+    ("cbx_slab_pack", C.c_int, [_P, C.c_int, C.c_int, _P, C.c_long, C.POINTER(C.c_long)]),
+    ("cbx_slab_unpack", C.c_int, [_P, C.c_int, C.c_int, _P, C.c_long]),
+    ("cbx_slab_local_state", C.c_int, [_P, C.POINTER(C.c_double)]),
+    ("cbx_slab_commit", C.c_int, [_P, C.POINTER(C.c_double)]),
+    ("cbx_upload_store_global", C.c_int, [_P, C.POINTER(Store)]),
+    ("cbx_download_store_global", C.c_int, [_P, C.POINTER(Store), C.POINTER(C.c_long)]),
 ]
 
 _lib = None

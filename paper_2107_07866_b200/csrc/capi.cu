@@ -40,7 +40,12 @@ struct cbx_ctx {
   int n_ghost = 0;
   bool fast_ok = true;
   bool mask_valid = false;
-  bool tile_ok = false;  // every offset within the 2-cell tile halo  // pmask matches the current positions (density ran last)
+  bool tile_ok = false;  // every offset within the 2-cell tile halo
+  // z-slab decomposition
+  int rank = 0, nranks = 1;
+  cbx_box gbox{};       // the global box (slab ranks)
+  int rem_base[2] = {0, 0};
+  int* d_rem_base = nullptr;  // pmask matches the current positions (density ran last)
   double band = 0.0;
 
   template <class T>
@@ -80,6 +85,7 @@ cbx_status guarded(cbx_ctx* c, F&& f) {
 
 void alloc_clash(cbx_ctx* c, Clash& A, int cap) {
   A.key = c->alloc<long long>(cap);
+  A.hkey = c->alloc<long long>(cap);
   A.gf = c->alloc<unsigned char>(cap);
   A.src = c->alloc<int>(cap);
   A.px = c->alloc<double>(cap);
@@ -509,7 +515,7 @@ void setup_fast(cbx_ctx* c) {
   P.ff.rec = dff;
   // fp32 filter band: |r2_f32 - r2_exact| <= err for coordinates below
   // maxc (two roundings to fp32, exact fp32 difference, three fp32 ops)
-  const double maxc = (std::max(std::max(c->G.tx, c->G.ty), c->G.tz) + 4) * c->G.a0;
+  const double maxc = (std::max(std::max(c->G.tx, c->G.ty), c->G.gtz) + 4) * c->G.a0;
   const double ulp = std::ldexp(1.0, std::ilogb(maxc) - 23);
   const double cut2 = P.cut2, dmax = std::sqrt(cut2) + 1.0;
   const double err = 2.0 * dmax * std::sqrt(3.0) * ulp + 3.0 * ulp * ulp +
@@ -640,8 +646,13 @@ CBX_API double cbx_adaptive_dt(double vmax, double dt_max, double max_disp) {
   return std::max(dt, 1e-7);
 }
 
-CBX_API cbx_status cbx_create(const cbx_box* box, const cbx_potential* pot,
-                              const cbx_offsets* idx, int device, cbx_ctx** out) {
+struct SlabSpec {
+  int rank = 0, nranks = 1, zoff = 0, gbz = 0;
+};
+
+static cbx_status create_impl(const cbx_box* box, const cbx_potential* pot,
+                              const cbx_offsets* idx, int device, const SlabSpec* slab,
+                              cbx_ctx** out) {
   auto c = std::make_unique<cbx_ctx>();
   const cbx_status rc = guarded(nullptr, [&] {
     if (box->box_x <= 0 || box->box_y <= 0 || box->box_z <= 0 || !(box->a0 > 0.0) ||
@@ -656,6 +667,20 @@ CBX_API cbx_status cbx_create(const cbx_box* box, const cbx_potential* pot,
     for (auto& e : c->ev) cudaEventCreate(&e);
     c->box = *box;
     c->G = make_geo(*box);
+    if (slab && slab->nranks > 1) {
+      if (box->box_z < box->ghost_width)
+        raise(CBX_INVALID_ARGUMENT, "z slab thinner than the ghost width");
+      c->G.zoff = slab->zoff;
+      c->G.gbz = slab->gbz;
+      c->G.gtz = slab->gbz + 2 * c->G.g;
+      c->G.glz = slab->gbz * box->a0;
+      c->G.slab = 1;
+      c->G.kmz = 0;  // z images come from the neighbouring ranks
+      c->rank = slab->rank;
+      c->nranks = slab->nranks;
+      c->gbox = *box;
+      c->gbox.box_z = slab->gbz;
+    }
     const Geo& G = c->G;
     c->S = 2 * G.NC;
     if (c->S >= (1ll << 31)) raise(CBX_INVALID_ARGUMENT, "box too large for one device (2^31 sites)");
@@ -747,13 +772,16 @@ CBX_API cbx_status cbx_create(const cbx_box* box, const cbx_potential* pot,
       int cx, cy, cz;
       cell_xyz(cell, G, cx, cy, cz);
       const bool ghost = cell_is_ghost(cx, cy, cz, G);
+      // z-halo planes of a slab rank are remote: filled by the position halo,
+      // their partials returned by the reverse halos (tgt = the site itself)
+      const bool remote = G.slab && (cz < G.g || cz >= G.g + G.bz);
       const long kx = floor_div(cx - G.g, G.bx), ky = floor_div(cy - G.g, G.by),
                  kz = floor_div(cz - G.g, G.bz);
       const long long scell = cell_of((int)(cx - kx * G.bx), (int)(cy - ky * G.by),
                                       (int)(cz - kz * G.bz), G);
       for (int par = 0; par < 2; ++par) {
         const long long d = par * G.NC + cell;
-        if (!ghost) {
+        if (!ghost || remote) {
           tgt[d] = (int)d;
           continue;
         }
@@ -800,15 +828,22 @@ CBX_API cbx_status cbx_create(const cbx_box* box, const cbx_potential* pot,
     P.cap_items = items;
     alloc_clash(c.get(), P.cl, cap);
     alloc_clash(c.get(), P.cl2, cap);
-    P.mv.key = c->alloc<long long>(cap);
-    P.mv.old = c->alloc<long long>(cap);
-    P.mv.px = c->alloc<double>(cap);
-    P.mv.py = c->alloc<double>(cap);
-    P.mv.pz = c->alloc<double>(cap);
-    P.mv.vx = c->alloc<double>(cap);
-    P.mv.vy = c->alloc<double>(cap);
-    P.mv.vz = c->alloc<double>(cap);
-    P.mv.tag = c->alloc<unsigned long long>(cap);
+    for (Movers* M : {&P.mv, &P.out}) {
+      M->key = c->alloc<long long>(cap);
+      M->walk = c->alloc<long long>(cap);
+      M->sub = c->alloc<long long>(cap);
+      M->cls = c->alloc<int>(cap);
+      M->dir = c->alloc<int>(cap);
+      M->px = c->alloc<double>(cap);
+      M->py = c->alloc<double>(cap);
+      M->pz = c->alloc<double>(cap);
+      M->vx = c->alloc<double>(cap);
+      M->vy = c->alloc<double>(cap);
+      M->vz = c->alloc<double>(cap);
+      M->tag = c->alloc<unsigned long long>(cap);
+    }
+    P.cap_rem = std::max(4096, cap / 4);
+    alloc_clash(c.get(), P.rem, P.cap_rem);
     P.sc.k1 = c->alloc<long long>(items);
     P.sc.k2 = c->alloc<long long>(items);
     P.sc.k3 = c->alloc<long long>(items);
@@ -838,6 +873,7 @@ CBX_API cbx_status cbx_create(const cbx_box* box, const cbx_potential* pot,
     setup_fast(c.get());
     P.st = c->alloc<DevStatus>(1);
     P.dself = c->alloc<KP>(1);
+    c->d_rem_base = c->alloc<int>(2);
     P.xp = std::getenv("CBX_XP") ? std::atoi(std::getenv("CBX_XP")) : 0;
     {
       const int maxn = std::max(std::max(fd[0].size(), fd[1].size()), std::max(hd[0].size(), hd[1].size()));
@@ -872,6 +908,11 @@ CBX_API cbx_status cbx_create(const cbx_box* box, const cbx_potential* pot,
     for (void* p : c->allocs) cudaFree(p);
   }
   return rc;
+}
+
+CBX_API cbx_status cbx_create(const cbx_box* box, const cbx_potential* pot,
+                              const cbx_offsets* idx, int device, cbx_ctx** out) {
+  return create_impl(box, pot, idx, device, nullptr, out);
 }
 
 CBX_API void cbx_destroy(cbx_ctx* c) {
@@ -1242,6 +1283,329 @@ CBX_API cbx_status cbx_describe(cbx_ctx* c, char* buf, long n) {
 CBX_API cbx_status cbx_kernel_launches(cbx_ctx* c, uint64_t* n) {
   *n = c->launches;
   return CBX_OK;
+}
+
+// ===========================================================================
+// z-slab decomposition (multi-GPU), driven phase by phase by the host
+// (paper_2107_07866_b200/slab.py) with the exchanges in between.
+
+CBX_API cbx_status cbx_create_slab(const cbx_box* global_box, const cbx_potential* pot,
+                                   const cbx_offsets* idx, int rank, int nranks, int device,
+                                   cbx_ctx** out) {
+  if (nranks < 1 || rank < 0 || rank >= nranks) {
+    set_thread_error("cbx_create_slab: bad rank / nranks");
+    return CBX_INVALID_ARGUMENT;
+  }
+  if (nranks == 1) return create_impl(global_box, pot, idx, device, nullptr, out);
+  const long gbz = global_box->box_z;
+  const long z0 = rank * gbz / nranks, z1 = (rank + 1) * gbz / nranks;
+  cbx_box local = *global_box;
+  local.box_z = z1 - z0;
+  SlabSpec sp;
+  sp.rank = rank;
+  sp.nranks = nranks;
+  sp.zoff = (int)z0;
+  sp.gbz = (int)gbz;
+  return create_impl(&local, pot, idx, device, &sp, out);
+}
+
+CBX_API cbx_status cbx_slab_info(cbx_ctx* c, long out[8]) {
+  return guarded(c, [&] {
+    out[0] = c->rank;
+    out[1] = c->nranks;
+    out[2] = c->G.zoff;
+    out[3] = c->G.bz;
+    out[4] = c->G.g;
+    out[5] = c->G.tx;
+    out[6] = c->G.ty;
+    out[7] = c->G.gbz;
+  });
+}
+
+CBX_API long cbx_slab_buffer_bytes(cbx_ctx* c, int kind) {
+  return (long)slab_buffer_bytes(c->P, kind);
+}
+
+// phases: 0 begin step (kick, drift, wrap, hash, outbound migrants),
+// 1 rehash + x/y ghosts, 2 clash images + density, 3 embedding,
+// 4 force, 5 end step (second kick, local sums), 6 local energy sums only
+CBX_API cbx_status cbx_slab_phase(cbx_ctx* c, int phase, double dt) {
+  return guarded(c, [&] {
+    cudaSetDevice(c->device);
+    check_cutoff(c);
+    switch (phase) {
+      case 0:
+        sync_status(c);
+        if (dt > 0.0) {
+          c->hst.dt_next = dt;
+          c->hst.adaptive = 0;
+        } else {
+          c->hst.adaptive = 1;
+          c->hst.dt_next = cbx_adaptive_dt(c->hst.max_speed, c->hst.dt_max, c->hst.max_disp);
+        }
+        c->hst.n_out = 0;
+        write_status(c);
+        c->mask_valid = false;
+        launch_kick_drift(c->P, 1, c->stream);
+        c->launches += 2;
+        break;
+      case 1:
+        launch_rehash(c->P, c->stream);
+        launch_ghost_fill(c->P, c->stream);
+        c->launches += 2;
+        sync_status(c);
+        c->hst.n_remote = 0;
+        write_status(c);
+        break;
+      case 2:
+        launch_clash_images(c->P, c->stream);
+        c->launches += 1;
+        seq_density(c);
+        break;
+      case 3:
+        seq_embed(c);
+        break;
+      case 4:
+        launch_remote_df(c->P, c->stream);
+        c->launches += 1;
+        seq_force(c);
+        break;
+      case 5:
+        launch_kick2(c->P, 1, c->stream);
+        launch_finalize(c->P, 1, 1, c->stream);
+        c->launches += 3;
+        break;
+      case 6:
+        launch_finalize(c->P, -1, 1, c->stream);
+        c->launches += 1;
+        break;
+      case 7:  // measure only (kinetic energy, max speed)
+        launch_kick2(c->P, 0, c->stream);
+        launch_finalize(c->P, 0, 0, c->stream);
+        c->launches += 3;
+        break;
+      default:
+        raise(CBX_INVALID_ARGUMENT, "cbx_slab_phase: unknown phase");
+    }
+    sync_status(c);
+    raise_device_error(c, phase >= 2 && phase <= 5);
+  });
+}
+
+// dir -1: toward the rank below, +1: toward the rank above
+CBX_API cbx_status cbx_slab_pack(cbx_ctx* c, int kind, int dir, void* buf, long cap,
+                                 long* bytes) {
+  return guarded(c, [&] {
+    cudaSetDevice(c->device);
+    if (kind < 0 || kind > 4 || (dir != -1 && dir != 1))
+      raise(CBX_INVALID_ARGUMENT, "cbx_slab_pack: bad kind / direction");
+    launch_pack(c->P, kind, dir, static_cast<unsigned char*>(buf), cap, c->stream);
+    const long long pb = kind == 0 ? 0 : slab_buffer_bytes(c->P, kind) -
+                                             ((kind == 1 || kind == 3)
+                                                  ? 16 + (long long)c->P.cap_rem * 72
+                                                  : 0);
+    long long n = 0;
+    long long used = 0;
+    if (kind == 0 || kind == 1 || kind == 3) {
+      // record count sits at the start of the record section
+      const long long plane = kind == 0 ? 0 : 2ll * c->G.g * c->G.txy * (kind == 1 ? 40 : 8);
+      cuda_check(cudaMemcpyAsync(&n, static_cast<unsigned char*>(buf) + plane, 8,
+                                 cudaMemcpyDeviceToHost, c->stream),
+                 "pack count");
+      cuda_check(cudaStreamSynchronize(c->stream), "pack");
+      used = plane + 16 + n * (kind == 0 ? 88 : 72);
+    } else {
+      used = 2ll * c->G.g * c->G.txy * (kind == 2 ? 8 : 24);
+      cuda_check(cudaStreamSynchronize(c->stream), "pack");
+    }
+    (void)pb;
+    sync_status(c);
+    raise_device_error(c, false);
+    *bytes = (long)used;
+  });
+}
+
+// from -1: data sent by the rank below, +1: by the rank above
+CBX_API cbx_status cbx_slab_unpack(cbx_ctx* c, int kind, int from, const void* buf, long bytes) {
+  return guarded(c, [&] {
+    cudaSetDevice(c->device);
+    if (kind < 0 || kind > 4 || (from != -1 && from != 1))
+      raise(CBX_INVALID_ARGUMENT, "cbx_slab_unpack: bad kind / direction");
+    (void)bytes;
+    // position halos crossing the global z boundary are periodic images
+    long long gshift = 0;
+    if (kind == 1 && from < 0 && c->rank == 0) gshift = -1;
+    if (kind == 1 && from > 0 && c->rank == c->nranks - 1) gshift = 1;
+    launch_unpack(c->P, kind, from, static_cast<const unsigned char*>(buf), gshift,
+                  c->d_rem_base + (from < 0 ? 0 : 1), c->stream);
+    sync_status(c);
+    raise_device_error(c, false);
+  });
+}
+
+CBX_API cbx_status cbx_slab_local_state(cbx_ctx* c, double out[8]) {
+  return guarded(c, [&] {
+    cudaSetDevice(c->device);
+    sync_status(c);
+    out[0] = c->hst.kinetic;
+    out[1] = c->hst.pair;
+    out[2] = c->hst.embedding;
+    out[3] = c->hst.max_speed;
+    out[4] = (double)c->hst.r_underflow;
+    out[5] = (double)c->hst.rho_clamp;
+    out[6] = (double)c->hst.step;
+    out[7] = c->hst.t;
+  });
+}
+
+// the all-reduced sums / max become this rank's StepState
+CBX_API cbx_status cbx_slab_commit(cbx_ctx* c, const double in[4]) {
+  return guarded(c, [&] {
+    cudaSetDevice(c->device);
+    sync_status(c);
+    c->hst.kinetic = in[0];
+    c->hst.pair = in[1];
+    c->hst.embedding = in[2];
+    c->hst.max_speed = in[3];
+    if (c->hst.adaptive)
+      c->hst.dt_next = cbx_adaptive_dt(in[3], c->hst.dt_max, c->hst.max_disp);
+    write_status(c);
+  });
+}
+
+// global store <-> this slab (tests, setup)
+CBX_API cbx_status cbx_upload_store_global(cbx_ctx* c, const cbx_store* g) {
+  return guarded(c, [&] {
+    cudaSetDevice(c->device);
+    const Geo& G = c->G;
+    const long long pid = 2ll * G.tx * G.ty, S = c->S, off = (long long)G.zoff * pid;
+    std::vector<double> pos(3 * S, 0.0), vel(3 * S, 0.0), frc(3 * S, 0.0), rho(S, 0.0), df(S, 0.0);
+    std::vector<uint64_t> tag(S, 0);
+    std::vector<uint8_t> valid(S, 0);
+    // local interior planes cz in [g, g + bz) <- global ids + off
+    for (long long id = (long long)G.g * pid; id < (long long)(G.g + G.bz) * pid; ++id) {
+      const long long gid = id + off;
+      if (gid < 0 || gid >= g->n_slots) continue;
+      valid[id] = g->valid ? g->valid[gid] && !(g->ghost && g->ghost[gid]) : 1;
+      for (int a = 0; a < 3; ++a) {
+        pos[3 * id + a] = g->pos[3 * gid + a];
+        if (g->vel) vel[3 * id + a] = g->vel[3 * gid + a];
+        if (g->force) frc[3 * id + a] = g->force[3 * gid + a];
+      }
+      if (g->rho) rho[id] = g->rho[gid];
+      if (g->df) df[id] = g->df[gid];
+      if (g->tag) tag[id] = g->tag[gid];
+    }
+    std::vector<int64_t> ck;
+    std::vector<double> cp, cv, cf, cr, cd;
+    std::vector<uint64_t> ct;
+    for (long i = 0; i < g->n_clash; ++i) {
+      if (g->clash_ghost && g->clash_ghost[i]) continue;
+      const long long k = g->clash_key[i] - off;
+      const long cz = site_cz(k, G);
+      if (cz < G.g || cz >= G.g + G.bz) continue;
+      ck.push_back(k);
+      for (int a = 0; a < 3; ++a) {
+        cp.push_back(g->clash_pos[3 * i + a]);
+        cv.push_back(g->clash_vel ? g->clash_vel[3 * i + a] : 0.0);
+        cf.push_back(g->clash_force ? g->clash_force[3 * i + a] : 0.0);
+      }
+      cr.push_back(g->clash_rho ? g->clash_rho[i] : 0.0);
+      cd.push_back(g->clash_df ? g->clash_df[i] : 0.0);
+      ct.push_back(g->clash_tag ? g->clash_tag[i] : 0);
+    }
+    cbx_store l{};
+    l.n_slots = S;
+    l.pos = pos.data();
+    l.vel = vel.data();
+    l.force = frc.data();
+    l.rho = rho.data();
+    l.df = df.data();
+    l.tag = tag.data();
+    l.valid = valid.data();
+    l.n_clash = (long)ck.size();
+    l.clash_key = ck.data();
+    l.clash_pos = cp.data();
+    l.clash_vel = cv.data();
+    l.clash_force = cf.data();
+    l.clash_rho = cr.data();
+    l.clash_df = cd.data();
+    l.clash_tag = ct.data();
+    do_upload(c, &l);
+  });
+}
+
+// writes this slab's interior sites into the global arrays (by global id)
+// and appends its interior clash records (global keys) at g->clash_* from
+// index *n_clash_inout
+CBX_API cbx_status cbx_download_store_global(cbx_ctx* c, cbx_store* g, long* n_clash_inout) {
+  return guarded(c, [&] {
+    cudaSetDevice(c->device);
+    const Geo& G = c->G;
+    const long long pid = 2ll * G.tx * G.ty, S = c->S, off = (long long)G.zoff * pid;
+    std::vector<double> pos(3 * S), vel(3 * S), frc(3 * S), rho(S), df(S);
+    std::vector<uint64_t> tag(S);
+    std::vector<uint8_t> valid(S), ghost(S);
+    cbx_store l{};
+    l.n_slots = S;
+    l.pos = pos.data();
+    l.vel = vel.data();
+    l.force = frc.data();
+    l.rho = rho.data();
+    l.df = df.data();
+    l.tag = tag.data();
+    l.valid = valid.data();
+    l.ghost = ghost.data();
+    do_download(c, &l);  // counts only (clash_key null)
+    const long nc = l.n_clash;
+    std::vector<int64_t> ck(nc);
+    std::vector<int32_t> ci(nc);
+    std::vector<double> cp(3 * nc), cv(3 * nc), cf(3 * nc), cr(nc), cd(nc);
+    std::vector<uint64_t> ct(nc);
+    std::vector<uint8_t> cg(nc);
+    l.clash_key = ck.data();
+    l.clash_idx = ci.data();
+    l.clash_pos = cp.data();
+    l.clash_vel = cv.data();
+    l.clash_force = cf.data();
+    l.clash_rho = cr.data();
+    l.clash_df = cd.data();
+    l.clash_tag = ct.data();
+    l.clash_ghost = cg.data();
+    do_download(c, &l);
+    for (long long id = (long long)G.g * pid; id < (long long)(G.g + G.bz) * pid; ++id) {
+      const long long gid = id + off;
+      if (gid < 0 || gid >= g->n_slots) continue;
+      if (g->valid) g->valid[gid] = valid[id];
+      if (g->ghost) g->ghost[gid] = 0;
+      for (int a = 0; a < 3; ++a) {
+        if (g->pos) g->pos[3 * gid + a] = pos[3 * id + a];
+        if (g->vel) g->vel[3 * gid + a] = vel[3 * id + a];
+        if (g->force) g->force[3 * gid + a] = frc[3 * id + a];
+      }
+      if (g->rho) g->rho[gid] = rho[id];
+      if (g->df) g->df[gid] = df[id];
+      if (g->tag) g->tag[gid] = tag[id];
+    }
+    long k = *n_clash_inout;
+    for (long i = 0; i < nc; ++i) {
+      if (cg[i]) continue;
+      if (k >= g->n_clash) raise(CBX_INVALID_ARGUMENT, "download_store_global: clash capacity");
+      if (g->clash_key) g->clash_key[k] = ck[i] + off;
+      if (g->clash_idx) g->clash_idx[k] = ci[i];
+      for (int a = 0; a < 3; ++a) {
+        if (g->clash_pos) g->clash_pos[3 * k + a] = cp[3 * i + a];
+        if (g->clash_vel) g->clash_vel[3 * k + a] = cv[3 * i + a];
+        if (g->clash_force) g->clash_force[3 * k + a] = cf[3 * i + a];
+      }
+      if (g->clash_rho) g->clash_rho[k] = cr[i];
+      if (g->clash_df) g->clash_df[k] = cd[i];
+      if (g->clash_tag) g->clash_tag[k] = ct[i];
+      if (g->clash_ghost) g->clash_ghost[k] = 0;
+      ++k;
+    }
+    *n_clash_inout = k;
+  });
 }
 
 }  // extern "C"

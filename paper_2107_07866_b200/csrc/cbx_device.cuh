@@ -28,6 +28,7 @@ struct Tab {
 // their ghost images (gf = 1) share one array.  head[dev] -> first record.
 struct Clash {
   long long* key;      // reference site id of the bucket
+  long long* hkey;     // new hash computed by k_clash_kick_drift
   unsigned char* gf;   // ghost image?
   int* src;            // ghost image: index of its interior source record
   double *px, *py, *pz, *vx, *vy, *vz, *fx, *fy, *fz;
@@ -37,10 +38,16 @@ struct Clash {
 };
 
 // pass-1 evictees of update_hash (store.cpp:46-54)
+// rehash items: key = new hash (local id); (walk, cls, sub) = the record's
+// position in the reference's pass-2 walk (store.cpp:59-75): walk key of the
+// bucket it is visited in, class 0 = earlier bucket member / 1 = pass-1
+// evictee, sub = bucket order or old site id
 struct Movers {
-  long long *key, *old;
+  long long *key, *walk, *sub;
+  int* cls;
   double *px, *py, *pz, *vx, *vy, *vz;
   unsigned long long* tag;
+  int* dir;  // outbound list only: -1 / +1 neighbour rank
 };
 
 // single-block sort scratch
@@ -57,7 +64,7 @@ struct DevStatus {
   double ovl_r2[kMaxOverlapRecords];
   double err_pos[3];
   unsigned long long r_underflow, rho_clamp;
-  int n_clash, n_mov;
+  int n_clash, n_mov, n_out, n_remote;
   // StepState mirror (sim.h:11-21)
   long long step;
   double t, dt, kinetic, pair, embedding, max_speed;
@@ -96,7 +103,10 @@ struct KP {
   Clash cl, cl2;
   int cap_clash;
   Movers mv;
+  Movers out;      // outbound migrants (z-slab decomposition)
   int cap_mov;
+  Clash rem;       // remote clash sources received with the position halo
+  int cap_rem;
   Scratch sc;
   int cap_items;  // power of two
   Tab dens, zr, emb;
@@ -175,6 +185,12 @@ void upload_offsets(const int* half_dev[2], const int half_n[2], const int* full
 int eam_blocks(const KP& P);
 int pair_partials(const KP& P, int mode);
 void launch_uf_refresh(const KP& P, cudaStream_t s);
+long long slab_buffer_bytes(const KP& P, int kind);
+void launch_pack(const KP& P, int kind, int dir, unsigned char* buf, long long cap,
+                 cudaStream_t s);
+void launch_unpack(const KP& P, int kind, int from, const unsigned char* buf, long long gshift,
+                   int* rem_base, cudaStream_t s);
+void launch_remote_df(const KP& P, cudaStream_t s);
 bool upload_tile_offsets(const int4* half[2], const int half_n[2], const int4* full[2],
                          const int full_n[2], cudaStream_t s);
 int embed_blocks(const KP& P);

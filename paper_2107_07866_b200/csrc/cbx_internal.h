@@ -53,6 +53,14 @@ struct Geo {
   double a0;
   double lx, ly, lz;  // periodic lengths, BoxSpec::len_x = box_x * a0 (lattice.h:35-37)
   int kmx, kmy, kmz;  // fill_ghosts k_max per axis (store.cpp:139-141)
+  // z-slab decomposition (multi-GPU).  Positions and hashes stay in the
+  // global frame; this store covers global ghost-inclusive z cells
+  // [zoff, zoff + tz).  One rank: zoff = 0, gbz = bz.
+  int zoff;    // global ghost-inclusive z cell of local z cell 0
+  int gbz;     // global interior z cells
+  int gtz;     // global ghost-inclusive z cells (gbz + 2g)
+  double glz;  // global periodic z length (gbz * a0)
+  int slab;    // 1 when z ghosts come from neighbour ranks
 };
 
 CBX_HD long long ref_id(long long cell, int par) { return 2 * cell + par; }
@@ -120,20 +128,20 @@ CBX_HD void nearest_site_coord(double px, double py, double pz, double a0, long&
 CBX_HD long long nearest_site(double px, double py, double pz, const Geo& G) {
   const double a = G.a0;
   if (px < 0.0 || px >= xmul((double)G.tx, a) || py < 0.0 || py >= xmul((double)G.ty, a) ||
-      pz < 0.0 || pz >= xmul((double)G.tz, a))
+      pz < 0.0 || pz >= xmul((double)G.gtz, a))
     return -1;
   const double fx = xdiv(px, a), fy = xdiv(py, a), fz = xdiv(pz, a);
   const long ci = clampl(rhd(fx), 0, G.tx - 1);
   const long cj = clampl(rhd(fy), 0, G.ty - 1);
-  const long ck = clampl(rhd(fz), 0, G.tz - 1);
+  const long ck = clampl(rhd(fz), 0, G.gtz - 1) - G.zoff;
   const double dc = xadd(xadd(xsq(xsub(fx, (double)ci)), xsq(xsub(fy, (double)cj))),
-                         xsq(xsub(fz, (double)ck)));
+                         xsq(xsub(fz, (double)(ck + G.zoff))));
   const long bi = clampl(rhd(xsub(fx, 0.5)), 0, G.tx - 1);
   const long bj = clampl(rhd(xsub(fy, 0.5)), 0, G.ty - 1);
-  const long bk = clampl(rhd(xsub(fz, 0.5)), 0, G.tz - 1);
+  const long bk = clampl(rhd(xsub(fz, 0.5)), 0, G.gtz - 1) - G.zoff;
   const double db = xadd(xadd(xsq(xsub(xsub(fx, (double)bi), 0.5)),
                               xsq(xsub(xsub(fy, (double)bj), 0.5))),
-                         xsq(xsub(xsub(fz, (double)bk), 0.5)));
+                         xsq(xsub(xsub(fz, (double)(bk + G.zoff)), 0.5)));
   const long long idc = ref_id(cell_of((int)ci, (int)cj, (int)ck, G), 0);
   const long long idb = ref_id(cell_of((int)bi, (int)bj, (int)bk, G), 1);
   if (dc < db) return idc;
@@ -154,13 +162,34 @@ CBX_HD bool wrap_position(double& px, double& py, double& pz, const Geo& G) {
     nearest_site_coord(px, py, pz, G.a0, qx, qy, qz);
     const long kx = floor_div(qx - 2 * G.g, 2 * G.bx);
     const long ky = floor_div(qy - G.g, G.by);
-    const long kz = floor_div(qz - G.g, G.bz);
+    const long kz = floor_div(qz - G.g, G.gbz);
     if (kx == 0 && ky == 0 && kz == 0) return true;
     px = xsub(px, xmul((double)kx, G.lx));
     py = xsub(py, xmul((double)ky, G.ly));
-    pz = xsub(pz, xmul((double)kz, G.lz));
+    pz = xsub(pz, xmul((double)kz, G.glz));
   }
   return false;
+}
+
+// local z cell of a (local) reference site id; floor semantics for ids
+// outside the store (atoms hashed into another rank's slab)
+CBX_HD long site_cz(long long id, const Geo& G) {
+  const long long cell = id >= 0 ? (id >> 1) : -((-id + 1) >> 1);
+  const long long plane = (long long)G.tx * G.ty;
+  long long q = cell / plane;
+  if (cell % plane != 0 && cell < 0) --q;
+  return (long)q;
+}
+// 0: owned here; 1: owned by the rank above (z+); -1: by the rank below
+CBX_HD int owner_dir(long long id, const Geo& G) {
+  if (!G.slab) return 0;
+  const long cz = site_cz(id, G);
+  if (cz >= G.g && cz < G.g + G.bz) return 0;
+  // global interior z index of the site, and of this slab's first plane
+  const long gz = cz + G.zoff - G.g, lo = G.zoff, hi = G.zoff + G.bz;
+  // the neighbour that is nearer in the periodic sense
+  const long up = ((gz - hi) % G.gbz + G.gbz) % G.gbz, dn = ((lo - 1 - gz) % G.gbz + G.gbz) % G.gbz;
+  return up <= dn ? 1 : -1;
 }
 
 // exact squared distance in the reference's operation order (vec3.h:14)

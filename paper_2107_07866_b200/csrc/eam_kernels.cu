@@ -295,7 +295,14 @@ __global__ void __launch_bounds__(256) k_embed(KP P) {
       const double r = P.rho[t];
       double v, dv;
       seg_eval(P.emb, r, v, dv);
-      if (t == d) {
+      // owned here: interior site (a z-halo site of a slab rank also has
+      // t == d, but its rho is a partial and its dF comes from the owner)
+      bool owned = t == d;
+      if (owned && P.G.slab) {
+        const long cz = site_cz(ref_of_dev(d, P.G.NC), P.G);
+        owned = cz >= P.G.g && cz < P.G.g + P.G.bz;
+      }
+      if (owned) {
         if (r < P.emb.x0 || r > P.emb.xl) atomicAdd(&P.st->rho_clamp, 1ull);
         e = v;
       }
@@ -312,6 +319,7 @@ __global__ void k_clash_embed(KP P) {
   const int n = P.st->n_clash;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const int s = P.cl.gf[i] ? P.cl.src[i] : i;
+    if (s < 0) continue;  // remote source: dF arrives with the dF halo
     const double r = P.cl.rho[s];
     double v, dv;
     seg_eval(P.emb, r, v, dv);

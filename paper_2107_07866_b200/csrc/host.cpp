@@ -237,6 +237,11 @@ Geo make_geo(const cbx_box& b) {
   G.kmx = (int)((b.ghost_width + b.box_x - 1) / b.box_x);
   G.kmy = (int)((b.ghost_width + b.box_y - 1) / b.box_y);
   G.kmz = (int)((b.ghost_width + b.box_z - 1) / b.box_z);
+  G.zoff = 0;
+  G.gbz = G.bz;
+  G.gtz = G.tz;
+  G.glz = G.lz;
+  G.slab = 0;
   return G;
 }
 

@@ -71,20 +71,25 @@ __global__ void __launch_bounds__(256) k_kick_drift(KP P, int move) {
   }
   const long long own = ref_of_dev(d, P.G.NC);
   if (real != own) {  // pass 1: evict to the clash map under the new hash
-    const int m = atomicAdd(&P.st->n_mov, 1);
+    const int dir = owner_dir(real, P.G);
+    const Movers& M = dir ? P.out : P.mv;
+    const int m = atomicAdd(dir ? &P.st->n_out : &P.st->n_mov, 1);
     if (m >= P.cap_mov) {
       set_error(P.st, CBX_RUNTIME);
       return;
     }
-    P.mv.key[m] = real;
-    P.mv.old[m] = own;
-    P.mv.px[m] = p.x;
-    P.mv.py[m] = p.y;
-    P.mv.pz[m] = p.z;
-    P.mv.vx[m] = vx;
-    P.mv.vy[m] = vy;
-    P.mv.vz[m] = vz;
-    P.mv.tag[m] = P.tag[d];
+    if (dir) M.dir[m] = dir;
+    M.key[m] = real;
+    M.walk[m] = real;
+    M.cls[m] = 1;
+    M.sub[m] = own;
+    M.px[m] = p.x;
+    M.py[m] = p.y;
+    M.pz[m] = p.z;
+    M.vx[m] = vx;
+    M.vy[m] = vy;
+    M.vz[m] = vz;
+    M.tag[m] = P.tag[d];
     P.pdf[d] = make_double4(kVacant, kVacant, kVacant, 0.0);
     P.uf[d] = make_float4(kVacantF, kVacantF, kVacantF, __int_as_float(-1));
   } else {
@@ -119,6 +124,35 @@ __global__ void k_clash_kick_drift(KP P, int move) {
     P.cl.px[i] = px;
     P.cl.py[i] = py;
     P.cl.pz[i] = pz;
+    const long long real = nearest_site(px, py, pz, P.G);  // store.cpp:64
+    if (real < 0 && atomicCAS(&P.st->err, 0, CBX_DOMAIN) == 0) {
+      P.st->err_pos[0] = px;
+      P.st->err_pos[1] = py;
+      P.st->err_pos[2] = pz;
+    }
+    P.cl.hkey[i] = real;
+    const int dir = real < 0 ? 0 : owner_dir(real, P.G);
+    if (dir) {  // the record migrates with its walk position
+      const int m = atomicAdd(&P.st->n_out, 1);
+      if (m >= P.cap_mov) {
+        set_error(P.st, CBX_RUNTIME);
+        return;
+      }
+      const Movers& M = P.out;
+      M.dir[m] = dir;
+      M.key[m] = real;
+      M.walk[m] = P.cl.key[i];
+      M.cls[m] = 0;
+      M.sub[m] = i;
+      M.px[m] = px;
+      M.py[m] = py;
+      M.pz[m] = pz;
+      M.vx[m] = P.cl.vx[i];
+      M.vy[m] = P.cl.vy[i];
+      M.vz[m] = P.cl.vz[i];
+      M.tag[m] = P.cl.tag[i];
+      P.cl.gf[i] = 3;  // gone
+    }
   }
 }
 
@@ -197,6 +231,7 @@ __device__ __forceinline__ int pad_pow2(int n) {
 
 __device__ __forceinline__ void copy_record(const Clash& a, int i, const Clash& b, int j) {
   b.key[j] = a.key[i];
+  b.hkey[j] = a.hkey[i];
   b.gf[j] = a.gf[i];
   b.src[j] = a.src[i];
   b.px[j] = a.px[i];
@@ -237,20 +272,13 @@ __global__ void __launch_bounds__(1024) k_rehash(KP P) {
   __syncthreads();
   const Scratch& X = P.sc;
   for (int i = threadIdx.x; i < n_old; i += blockDim.x) {
-    if (P.cl.gf[i]) continue;
-    const long long real = nearest_site(P.cl.px[i], P.cl.py[i], P.cl.pz[i], P.G);
-    if (real < 0) {
-      if (atomicCAS(&P.st->err, 0, CBX_DOMAIN) == 0) {
-        P.st->err_pos[0] = P.cl.px[i];
-        P.st->err_pos[1] = P.cl.py[i];
-        P.st->err_pos[2] = P.cl.pz[i];
-      }
-      continue;
-    }
+    if (P.cl.gf[i]) continue;  // ghost images are rebuilt; gf 3 = migrated away
+    const long long real = P.cl.hkey[i];
+    if (real < 0) continue;
     const int k = atomicAdd(&s_n, 1);
     X.k1[k] = real;
     X.k2[k] = P.cl.key[i];
-    X.k3[k] = i;
+    X.k3[k] = (1ll << 60) + i;
     X.pl[k] = i;
   }
   __syncthreads();
@@ -261,8 +289,8 @@ __global__ void __launch_bounds__(1024) k_rehash(KP P) {
   }
   for (int m = threadIdx.x; m < n_mov; m += blockDim.x) {
     X.k1[base + m] = P.mv.key[m];
-    X.k2[base + m] = P.mv.key[m];
-    X.k3[base + m] = (1ll << 62) | P.mv.old[m];
+    X.k2[base + m] = P.mv.walk[m];
+    X.k3[base + m] = (long long)P.mv.cls[m] * (1ll << 61) + (1ll << 60) + P.mv.sub[m];
     X.pl[base + m] = -(m + 1);
   }
   const int n = base + n_mov;
@@ -385,14 +413,34 @@ __global__ void k_ghost_fill(KP P) {
 // bucket's order.  An image whose ghost slot is free would take the slot in
 // the reference; update_hash never leaves an interior bucket over a vacant
 // slot, so that state is rejected (CBX_INVALID_ARGUMENT) instead.
+// z-slab ranks (G.kmz = 0) also receive the interior clash records of the
+// neighbours' boundary planes (P.rem, position halo); each becomes a ghost
+// record here with its x/y images, src = -(remote index + 2).
+__device__ __forceinline__ int image_count(long long id, const Geo& G) {
+  int cx, cy, cz;
+  cell_xyz(id >> 1, G, cx, cy, cz);
+  int c = 0;
+  for (int kz = -G.kmz; kz <= G.kmz; ++kz)
+    for (int ky = -G.kmy; ky <= G.kmy; ++ky)
+      for (int kx = -G.kmx; kx <= G.kmx; ++kx) {
+        if (kx == 0 && ky == 0 && kz == 0) continue;
+        const int ix = cx + G.bx * kx, iy = cy + G.by * ky, iz = cz + G.bz * kz;
+        if (ix < 0 || ix >= G.tx || iy < 0 || iy >= G.ty || iz < 0 || iz >= G.tz) continue;
+        ++c;
+      }
+  return c;
+}
+
 __global__ void __launch_bounds__(1024) k_clash_images(KP P) {
   if (P.st->err) return;
   const int n = P.st->n_clash;
-  if (n == 0) return;
+  const int n_rem = P.st->n_remote;
+  if (n == 0 && n_rem == 0) return;
   const Scratch& X = P.sc;
+  const Geo& G = P.G;
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    P.head[dev_of_ref(P.cl.key[i], P.G.NC)] = -1;
-    X.flag[i] = !P.cl.gf[i];
+    P.head[dev_of_ref(P.cl.key[i], G.NC)] = -1;
+    X.flag[i] = P.cl.gf[i] == 0;
   }
   __syncthreads();
   const int n_int = block_scan(X.flag, X.pos, n);
@@ -400,37 +448,34 @@ __global__ void __launch_bounds__(1024) k_clash_images(KP P) {
   for (int i = threadIdx.x; i < n; i += blockDim.x)
     if (X.flag[i]) copy_record(P.cl, i, P.cl2, X.pos[i]);
   __syncthreads();
-  // count images per interior record
-  const Geo& G = P.G;
-  for (int r = threadIdx.x; r < n_int; r += blockDim.x) {
-    const long long id = P.cl2.key[r];
-    int cx, cy, cz;
-    cell_xyz(id >> 1, G, cx, cy, cz);
-    int c = 0;
-    for (int kz = -G.kmz; kz <= G.kmz; ++kz)
-      for (int ky = -G.kmy; ky <= G.kmy; ++ky)
-        for (int kx = -G.kmx; kx <= G.kmx; ++kx) {
-          if (kx == 0 && ky == 0 && kz == 0) continue;
-          const int ix = cx + G.bx * kx, iy = cy + G.by * ky, iz = cz + G.bz * kz;
-          if (ix < 0 || ix >= G.tx || iy < 0 || iy >= G.ty || iz < 0 || iz >= G.tz) continue;
-          ++c;
-        }
-    X.flag[r] = c;
+  // sources: interior records r < n_int emit images; remote records emit
+  // themselves plus images
+  const int n_src = n_int + n_rem;
+  for (int r = threadIdx.x; r < n_src; r += blockDim.x) {
+    const long long id = r < n_int ? P.cl2.key[r] : P.rem.key[r - n_int];
+    X.flag[r] = image_count(id, G) + (r < n_int ? 0 : 1);
   }
   __syncthreads();
-  const int n_img = block_scan(X.flag, X.pos, n_int);
+  const int n_img = block_scan(X.flag, X.pos, n_src);
   const int total = n_int + n_img;
   if (total > P.cap_clash || total > P.cap_items) {
     if (threadIdx.x == 0) set_error(P.st, CBX_RUNTIME);
     return;
   }
-  // sort items: interior records (key, r, 0) and images (image key, r, 1+seq)
-  for (int r = threadIdx.x; r < n_int; r += blockDim.x) {
-    X.k1[r] = P.cl2.key[r];
-    X.k2[r] = r;
-    X.k3[r] = 0;
-    X.pl[r] = r;
-    const long long id = P.cl2.key[r];
+  // sort items: interior records (key, r, 0); ghost records (key, r, 1 + seq)
+  for (int r = threadIdx.x; r < n_src; r += blockDim.x) {
+    const bool local = r < n_int;
+    const int rr = r - n_int;
+    const long long id = local ? P.cl2.key[r] : P.rem.key[rr];
+    if (local) {
+      X.k1[r] = id;
+      X.k2[r] = r;
+      X.k3[r] = 0;
+      X.pl[r] = r;
+    }
+    const double sx = local ? P.cl2.px[r] : P.rem.px[rr];
+    const double sy = local ? P.cl2.py[r] : P.rem.py[rr];
+    const double sz = local ? P.cl2.pz[r] : P.rem.pz[rr];
     const int par = (int)(id & 1);
     int cx, cy, cz;
     cell_xyz(id >> 1, G, cx, cy, cz);
@@ -438,32 +483,33 @@ __global__ void __launch_bounds__(1024) k_clash_images(KP P) {
     for (int kz = -G.kmz; kz <= G.kmz; ++kz)
       for (int ky = -G.kmy; ky <= G.kmy; ++ky)
         for (int kx = -G.kmx; kx <= G.kmx; ++kx) {
-          if (kx == 0 && ky == 0 && kz == 0) continue;
+          if (kx == 0 && ky == 0 && kz == 0 && local) continue;
           const int ix = cx + G.bx * kx, iy = cy + G.by * ky, iz = cz + G.bz * kz;
           if (ix < 0 || ix >= G.tx || iy < 0 || iy >= G.ty || iz < 0 || iz >= G.tz) continue;
           const long long iid = ref_id(cell_of(ix, iy, iz, G), par);
-          if (P.pdf[dev_of_ref(iid, G.NC)].x >= kVacantTest) set_error(P.st, CBX_INVALID_ARGUMENT);
-          // record w of cl2 = image
+          if (local && P.pdf[dev_of_ref(iid, G.NC)].x >= kVacantTest)
+            set_error(P.st, CBX_INVALID_ARGUMENT);
           P.cl2.key[w] = iid;
           P.cl2.gf[w] = 1;
-          P.cl2.src[w] = r;
-          P.cl2.px[w] = xadd(P.cl2.px[r], xmul((double)kx, G.lx));
-          P.cl2.py[w] = xadd(P.cl2.py[r], xmul((double)ky, G.ly));
-          P.cl2.pz[w] = xadd(P.cl2.pz[r], xmul((double)kz, G.lz));
-          P.cl2.vx[w] = P.cl2.vx[r];
-          P.cl2.vy[w] = P.cl2.vy[r];
-          P.cl2.vz[w] = P.cl2.vz[r];
+          P.cl2.src[w] = local ? r : -(rr + 2);
+          P.cl2.px[w] = xadd(sx, xmul((double)kx, G.lx));
+          P.cl2.py[w] = xadd(sy, xmul((double)ky, G.ly));
+          P.cl2.pz[w] = xadd(sz, xmul((double)kz, G.lz));
+          P.cl2.vx[w] = local ? P.cl2.vx[r] : P.rem.vx[rr];
+          P.cl2.vy[w] = local ? P.cl2.vy[r] : P.rem.vy[rr];
+          P.cl2.vz[w] = local ? P.cl2.vz[r] : P.rem.vz[rr];
           P.cl2.fx[w] = 0.0;
           P.cl2.fy[w] = 0.0;
           P.cl2.fz[w] = 0.0;
-          P.cl2.rho[w] = P.cl2.rho[r];
-          P.cl2.df[w] = P.cl2.df[r];
+          P.cl2.rho[w] = local ? P.cl2.rho[r] : 0.0;
+          P.cl2.df[w] = local ? P.cl2.df[r] : P.rem.df[rr];
           P.cl2.e_emb[w] = 0.0;
           P.cl2.e_pair[w] = 0.0;
           P.cl2.v2[w] = 0.0;
-          P.cl2.tag[w] = P.cl2.tag[r];
+          P.cl2.tag[w] = local ? P.cl2.tag[r] : P.rem.tag[rr];
+          // remote sources order after every local source of the same key
           X.k1[w] = iid;
-          X.k2[w] = r;
+          X.k2[w] = local ? r : (1ll << 40) + rr;
           X.k3[w] = 1 + seq;
           X.pl[w] = w;
           ++w;
@@ -486,7 +532,8 @@ __global__ void __launch_bounds__(1024) k_clash_images(KP P) {
   for (int p = threadIdx.x; p < total; p += blockDim.x) {
     const int q = X.pl[p];
     copy_record(P.cl2, q, P.cl, p);
-    P.cl.src[p] = P.cl2.gf[q] ? X.flag[P.cl2.src[q]] : p;
+    const int sq = P.cl2.src[q];
+    P.cl.src[p] = P.cl2.gf[q] ? (sq >= 0 ? X.flag[sq] : sq) : p;
     if (p == 0 || X.k1[p - 1] != X.k1[p]) P.head[dev_of_ref(X.k1[p], G.NC)] = p;
   }
   if (threadIdx.x == 0) P.st->n_clash = total;

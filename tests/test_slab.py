@@ -1,0 +1,243 @@
+"""z-slab decomposition.
+
+GPU: n virtual slab ranks on one device, exchanging through device buffers
+(LocalExchange), against the single-box oracle -- forces, densities,
+energies, trajectories and a cascade whose PKA crosses slab boundaries.
+CPU: the torch.distributed exchange (gloo, world_size 2 and 3) routes every
+buffer to the right neighbour and reduces the energies like the local one.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from helpers import assert_store_parity
+from paper_2107_07866_b200 import slab as S
+
+
+# ------------------------------------------------------------- host logic
+def test_slab_bounds_cover_box():
+    for bz in (5, 10, 17, 64):
+        for n in (1, 2, 3, 4):
+            b = [S.slab_bounds(bz, r, n) for r in range(n)]
+            assert b[0][0] == 0 and b[-1][1] == bz
+            assert all(b[i][1] == b[i + 1][0] for i in range(n - 1))
+
+
+def test_reduce_states():
+    a = np.array([1.0, 2.0, 3.0, 4.0, 1, 0, 7, 0.5])
+    b = np.array([10.0, 20.0, 30.0, 2.0, 2, 3, 7, 0.5])
+    r = S.reduce_states([a, b])
+    assert list(r[:3]) == [11.0, 22.0, 33.0]
+    assert r[3] == 4.0 and r[4] == 3 and r[5] == 3 and r[6] == 7 and r[7] == 0.5
+
+
+class MockRank:
+    """stands in for a SlabRank: packets encode (sender, kind, direction)"""
+
+    def __init__(self, rank, nranks):
+        import torch
+        self.torch = torch
+        self.rank, self.nranks = rank, nranks
+        self.got = {}
+        self.comm_device = "cpu"
+
+    def pack(self, kind, direction):
+        n = 16 + 8 * kind + (3 if direction > 0 else 0)  # distinct ragged sizes
+        t = self.torch.full((64,), 0, dtype=self.torch.uint8)
+        t[0], t[1], t[2] = self.rank, kind, 1 if direction > 0 else 0
+        t[3:n] = 200
+        return t, n
+
+    def unpack(self, kind, source, tensor, nbytes):
+        a = tensor[:nbytes].numpy().copy()
+        self.got[(kind, source)] = (int(a[0]), int(a[1]), int(a[2]), nbytes)
+
+    def local_state(self):
+        return np.array([1.0 + self.rank, 2.0, 3.0, 0.5 * self.rank, 1, 0, 4, 0.25])
+
+
+def _expect(rank, n):
+    lo, hi = S.neighbours(rank, n)
+    out = {}
+    for kind in range(5):
+        out[(kind, -1)] = (lo, kind, 1, 16 + 8 * kind + 3)   # the rank below's "up" packet
+        out[(kind, +1)] = (hi, kind, 0, 16 + 8 * kind)       # the rank above's "down" packet
+    return out
+
+
+def _gloo_worker(rank, n, port, q):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=n)
+    try:
+        r = MockRank(rank, n)
+        ex = S.DistExchange(r)
+        for kind in range(5):
+            ex.exchange(kind)
+        red = ex.allreduce([r.local_state()])
+        q.put((rank, r.got, list(red)))
+    finally:
+        dist.destroy_process_group()
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+@pytest.mark.parametrize("n", [2, 3])
+def test_dist_exchange_gloo(n):
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gloo_worker, args=(r, n, port, q)) for r in range(n)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(n):
+        rank, got, red = q.get(timeout=120)
+        res[rank] = (got, red)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    local = S.reduce_states([MockRank(r, n).local_state() for r in range(n)])
+    for r in range(n):
+        got, red = res[r]
+        assert got == _expect(r, n), r
+        assert np.allclose(red[:6], local[:6])
+
+
+def test_local_exchange_routing():
+    n = 3
+    ranks = [MockRank(r, n) for r in range(n)]
+    ex = S.LocalExchange(ranks)
+    for kind in range(5):
+        ex.exchange(kind)
+    for r in range(n):
+        assert ranks[r].got == _expect(r, n)
+
+
+# ------------------------------------------------------------- on the GPU
+@pytest.fixture(scope="module")
+def cuda():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2107_07866_b200 import _lib
+    _lib.load()
+    return True
+
+
+def _interior(s):
+    """drop ghost clash replicas so slab and single-box stores compare"""
+    import dataclasses
+    keep = s.clash_ghost == 0
+    d = {f.name: getattr(s, f.name) for f in dataclasses.fields(s)}
+    for k in list(d):
+        if k.startswith("clash_"):
+            d[k] = d[k][keep]
+    return type(s)(**d)
+
+
+def slab_domain(ref, path, n):
+    from paper_2107_07866_b200 import EamPotential
+    dims, a0, g = ref.box
+    pot = EamPotential.load(path)
+    ranks = [S.SlabRank((*dims, a0, g), pot, r, n) for r in range(n)]
+    st = ref.state()
+    for r in ranks:
+        r.upload_global(ref.store())
+        r.set_state(st)
+    dom = S.SlabDomain(ranks, S.LocalExchange(ranks))
+    dom._pot = pot
+    return dom
+
+
+def gather(dom, ref):
+    """the slabs' interiors assembled into one global store"""
+    s = _interior(ref.store())
+    Sg = len(s.tag)
+    g = dict(pos=np.zeros((Sg, 3)), vel=np.zeros((Sg, 3)), force=np.zeros((Sg, 3)),
+             rho=np.zeros(Sg), df=np.zeros(Sg), tag=np.zeros(Sg, np.uint64),
+             valid=np.zeros(Sg, np.uint8), ghost=np.zeros(Sg, np.uint8))
+    cap = 4096
+    g.update(clash_key=np.zeros(cap, np.int64), clash_idx=np.zeros(cap, np.int32),
+             clash_pos=np.zeros((cap, 3)), clash_vel=np.zeros((cap, 3)),
+             clash_force=np.zeros((cap, 3)), clash_rho=np.zeros(cap), clash_df=np.zeros(cap),
+             clash_tag=np.zeros(cap, np.uint64), clash_ghost=np.zeros(cap, np.uint8))
+    n = 0
+    for r in dom.ranks:
+        n = r.download_global(g, n)
+    for k in list(g):
+        if k.startswith("clash_"):
+            g[k] = g[k][:n]
+    return type(s)(**g)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n", [2, 3, 4])
+def test_slab_eval_matches_single_box(cuda, tables, n):
+    """forces / rho / dF / energies of the decomposed evaluation equal the
+    single-box reference (oracle) on a thermalised lattice"""
+    from oracle import oracle
+    ref = oracle.Sim(tables["baseline"], box=(8, 7, 10), temperature=600.0, seed=77)
+    dom = slab_domain(ref, tables["baseline"], n)
+    dom.prime()
+    sr, sd = ref.state(), dom.state()
+    for k in ("kinetic", "pair", "embedding"):
+        assert abs(sd[k] - sr[k]) <= 1e-10 * abs(sr[k]), (k, sd[k], sr[k])
+    assert_store_parity(_interior(ref.store()), gather(dom, ref), what=f"slab eval n={n}")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n", [2, 3])
+def test_slab_trajectory(cuda, tables, n):
+    """60 steps at 600 K: trajectories of the decomposed run follow the
+    single-box oracle (atoms migrate between slabs through the z faces)"""
+    from oracle import oracle
+    ref = oracle.Sim(tables["baseline"], box=(8, 8, 9), temperature=600.0, seed=12345)
+    dom = slab_domain(ref, tables["baseline"], n)
+    dom.prime()
+    for chunk in range(3):
+        ref.step(1e-3, 20)
+        dom.step(1e-3, 20)
+        sr, sd = ref.state(), dom.state()
+        assert sd["step"] == sr["step"]
+        for k in ("kinetic", "pair", "embedding"):
+            assert abs(sd[k] - sr[k]) <= 1e-9 * abs(sr[k]), (chunk, k, sd[k], sr[k])
+        assert_store_parity(_interior(ref.store()), gather(dom, ref), pos_tol=1e-9, rel=1e-8,
+                            what=f"slab n={n} chunk {chunk}")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n", [2, 3])
+def test_slab_cascade(cuda, tables, n):
+    """a PKA cascade whose recoils cross slab faces: off-lattice atoms move
+    between ranks as clash records; Wigner-Seitz counts, bucket structure and
+    forces match the single-box oracle; adaptive dt is agreed globally"""
+    from oracle import oracle
+    ref = oracle.Sim(tables["baseline"], box=(10, 10, 10), temperature=600.0, seed=12345,
+                     pka_energy_kev=1.0, pka_site=(5, 5, 3))
+    ref.step(1e-3, 5)
+    ref.inject_pka()
+    dom = slab_domain(ref, tables["baseline"], n)
+    dom.prime()
+    assert abs(dom.state()["kinetic"] - ref.state()["kinetic"]) <= 1e-12 * ref.state()["kinetic"]
+    saw_clash = False
+    for chunk in range(6):
+        ref.step(-1, 20)
+        dom.step(-1, 20)
+        rs = ref.store()
+        saw_clash |= (rs.clash_ghost == 0).sum() > 0
+        assert dom.state()["t"] == pytest.approx(ref.state()["t"], rel=1e-12, abs=0)
+        assert ref.count_defects() == dom.count_defects(), chunk
+        assert_store_parity(_interior(rs), gather(dom, ref), pos_tol=1e-8, rel=1e-7,
+                            what=f"slab cascade n={n} chunk {chunk}")
+    assert saw_clash
