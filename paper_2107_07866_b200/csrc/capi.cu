@@ -47,6 +47,13 @@ struct cbx_ctx {
   int rem_base[2] = {0, 0};
   int* d_rem_base = nullptr;  // pmask matches the current positions (density ran last)
   double band = 0.0;
+  // this context's stencil tables (device deltas depend on its box), kept
+  // to re-bind the device's __constant__ copy when contexts share a GPU
+  std::vector<int> c_hd[2], c_fd[2];
+  std::vector<long long> c_ff[2];
+  std::vector<int4> c_h4[2], c_f4[2];
+  int c_hin[2] = {0, 0}, c_fin[2] = {0, 0};
+  bool const_ready = false;
 
   template <class T>
   T* alloc(size_t n) {
@@ -66,9 +73,35 @@ void cuda_check(cudaError_t e, const char* what) {
   if (e != cudaSuccess) raise(CBX_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
+// The stencil deltas live in __constant__ memory, one copy per device; the
+// context whose tables are resident is recorded here and every entry point
+// re-binds before it launches (contexts sharing one GPU -- virtual slab
+// ranks, several boxes -- are used from one host thread at a time).
+cbx_ctx* g_const_owner[64] = {};
+
+void bind_constants(cbx_ctx* c) {
+  if (!c->const_ready || c->device < 0 || c->device >= 64) return;
+  if (g_const_owner[c->device] == c) return;
+  cudaSetDevice(c->device);
+  cudaDeviceSynchronize();  // other contexts' work finished with the old tables
+  const int* hp[2] = {c->c_hd[0].data(), c->c_hd[1].data()};
+  const int* fp[2] = {c->c_fd[0].data(), c->c_fd[1].data()};
+  const long long* fl[2] = {c->c_ff[0].data(), c->c_ff[1].data()};
+  const int hn[2] = {(int)c->c_hd[0].size(), (int)c->c_hd[1].size()};
+  const int fn[2] = {(int)c->c_fd[0].size(), (int)c->c_fd[1].size()};
+  upload_offsets(hp, hn, fp, fn, fl, c->c_hin, c->c_fin, c->stream);
+  const int4* h4p[2] = {c->c_h4[0].data(), c->c_h4[1].data()};
+  const int4* f4p[2] = {c->c_f4[0].data(), c->c_f4[1].data()};
+  c->tile_ok = upload_tile_offsets(h4p, hn, f4p, fn, c->stream);
+  if (cudaStreamSynchronize(c->stream) != cudaSuccess)
+    raise(CBX_CUDA, "offset table upload failed");
+  g_const_owner[c->device] = c;
+}
+
 template <class F>
 cbx_status guarded(cbx_ctx* c, F&& f) {
   try {
+    if (c) bind_constants(c);
     f();
     if (c) c->err.clear();
     return CBX_OK;
@@ -757,13 +790,19 @@ static cbx_status create_impl(const cbx_box* box, const cbx_potential* pot,
     const long long* fl[2] = {ff[0].data(), ff[1].data()};
     const int hn[2] = {(int)hd[0].size(), (int)hd[1].size()};
     const int fn[2] = {(int)fd[0].size(), (int)fd[1].size()};
-    upload_offsets(hp, hn, fp, fn, fl, hin, fin, c->stream);
-    {
-      const int4* h4p[2] = {h4[0].data(), h4[1].data()};
-      const int4* f4p[2] = {f4[0].data(), f4[1].data()};
-      c->tile_ok = upload_tile_offsets(h4p, hn, f4p, fn, c->stream);
+    (void)hp; (void)fp; (void)fl; (void)hn; (void)fn;
+    for (int par = 0; par < 2; ++par) {
+      c->c_hd[par] = hd[par];
+      c->c_fd[par] = fd[par];
+      c->c_ff[par] = ff[par];
+      c->c_h4[par] = h4[par];
+      c->c_f4[par] = f4[par];
+      c->c_hin[par] = hin[par];
+      c->c_fin[par] = fin[par];
     }
-    cuda_check(cudaStreamSynchronize(c->stream), "offset upload");
+    c->const_ready = true;
+    if (c->device < 64 && g_const_owner[c->device] == c.get()) g_const_owner[c->device] = nullptr;
+    bind_constants(c.get());
     // ghost list and owner map
     const long long S = c->S;
     std::vector<int> tgt(S), gdst, gsrc;
@@ -918,6 +957,8 @@ CBX_API cbx_status cbx_create(const cbx_box* box, const cbx_potential* pot,
 CBX_API void cbx_destroy(cbx_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
+  if (c->device >= 0 && c->device < 64 && g_const_owner[c->device] == c)
+    g_const_owner[c->device] = nullptr;
   drop_graph(c);
   if (c->stream) cudaStreamSynchronize(c->stream);
   for (void* p : c->allocs) cudaFree(p);
@@ -1577,7 +1618,7 @@ CBX_API cbx_status cbx_download_store_global(cbx_ctx* c, cbx_store* g, long* n_c
       const long long gid = id + off;
       if (gid < 0 || gid >= g->n_slots) continue;
       if (g->valid) g->valid[gid] = valid[id];
-      if (g->ghost) g->ghost[gid] = 0;
+      if (g->ghost) g->ghost[gid] = ghost[id];
       for (int a = 0; a < 3; ++a) {
         if (g->pos) g->pos[3 * gid + a] = pos[3 * id + a];
         if (g->vel) g->vel[3 * gid + a] = vel[3 * id + a];

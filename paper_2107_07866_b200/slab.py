@@ -294,7 +294,8 @@ class SlabDomain:
         return g
 
     def state(self) -> dict:
-        s = self.ex.allreduce([r.local_state() for r in self.ranks])
+        """the committed (already reduced) step state; every rank holds it"""
+        s = self.ranks[0].local_state()
         return {"kinetic": s[0], "pair": s[1], "embedding": s[2], "max_speed": s[3],
                 "r_underflow": int(s[4]), "rho_clamp": int(s[5]), "step": int(s[6]),
                 "t": s[7]}

@@ -391,3 +391,20 @@ def test_cxx_host_on_device(cuda, tables, tmp_path):
     out = subprocess.run([exe, tables["baseline"], "gpu"], capture_output=True, text=True,
                          check=True).stdout
     assert "atoms 1024" in out and "-> step 10" in out
+
+
+def test_two_contexts_interleaved(cuda, tables):
+    """two engines with different boxes on one GPU, used alternately: each
+    re-binds its own stencil tables (the __constant__ copy is per device)"""
+    from oracle import oracle
+    r1 = oracle.Sim(tables["baseline"], box=(6, 7, 8), temperature=600.0, seed=1)
+    r2 = oracle.Sim(tables["baseline"], box=(9, 6, 5), temperature=600.0, seed=2)
+    d1 = device_for(r1, tables["baseline"])
+    d2 = device_for(r2, tables["baseline"])
+    for ref, dev in ((r1, d1), (r2, d2), (r1, d1), (r2, d2)):
+        dev.set_state(ref.state())
+    for _ in range(2):
+        for ref, dev in ((r1, d1), (r2, d2)):
+            ref.step(1e-3, 5)
+            dev.step(1e-3, 5)
+            assert_store_parity(ref.store(), dev.download(), pos_tol=1e-10, rel=1e-9)

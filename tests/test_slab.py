@@ -187,7 +187,7 @@ def test_slab_eval_matches_single_box(cuda, tables, n):
     """forces / rho / dF / energies of the decomposed evaluation equal the
     single-box reference (oracle) on a thermalised lattice"""
     from oracle import oracle
-    ref = oracle.Sim(tables["baseline"], box=(8, 7, 10), temperature=600.0, seed=77)
+    ref = oracle.Sim(tables["baseline"], box=(8, 7, 13), temperature=600.0, seed=77)
     dom = slab_domain(ref, tables["baseline"], n)
     dom.prime()
     sr, sd = ref.state(), dom.state()
