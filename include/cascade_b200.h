@@ -213,6 +213,14 @@ CBX_API cbx_status cbx_slab_unpack(cbx_ctx* ctx, int kind, int from, const void*
                                    long bytes);
 CBX_API cbx_status cbx_slab_local_state(cbx_ctx* ctx, double out[8]);
 CBX_API cbx_status cbx_slab_commit(cbx_ctx* ctx, const double in[4]);
+/* In-graph exchange (one process per GPU): rank 0 makes an NCCL id, every
+ * rank passes it to cbx_slab_comm_init (collective).  cbx_step,
+ * cbx_eval_forces / cbx_refresh_forces, cbx_measure and cbx_bench_steps then
+ * run the whole decomposed step -- exchanges and the StepState all-reduce --
+ * as one CUDA graph per rank; with nranks == 1 the exchange is a self
+ * send/recv (the periodic z images of a one-slab box). */
+CBX_API cbx_status cbx_nccl_unique_id(void* out, long nbytes);
+CBX_API cbx_status cbx_slab_comm_init(cbx_ctx* ctx, const void* id, long nbytes);
 CBX_API cbx_status cbx_upload_store_global(cbx_ctx* ctx, const cbx_store* global_store);
 CBX_API cbx_status cbx_download_store_global(cbx_ctx* ctx, cbx_store* global_store,
                                              long* n_clash_inout);

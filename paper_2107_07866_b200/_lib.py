@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libcascade_b200.so")
+LIB_PATH = os.environ.get("CBX_LIB") or os.path.join(HERE, "libcascade_b200.so")
 
 STATUS = {0: "OK", 1: "INVALID_ARGUMENT", 2: "RUNTIME", 3: "DOMAIN", 4: "LOGIC", 5: "CUDA",
           6: "NCCL"}
@@ -143,6 +143,8 @@ SIGNATURES = [
     ("cbx_slab_unpack", C.c_int, [_P, C.c_int, C.c_int, _P, C.c_long]),
     ("cbx_slab_local_state", C.c_int, [_P, C.POINTER(C.c_double)]),
     ("cbx_slab_commit", C.c_int, [_P, C.POINTER(C.c_double)]),
+    ("cbx_nccl_unique_id", C.c_int, [_P, C.c_long]),
+    ("cbx_slab_comm_init", C.c_int, [_P, _P, C.c_long]),
     ("cbx_upload_store_global", C.c_int, [_P, C.POINTER(Store)]),
     ("cbx_download_store_global", C.c_int, [_P, C.POINTER(Store), C.POINTER(C.c_long)]),
 ]

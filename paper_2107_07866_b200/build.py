@@ -9,11 +9,11 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libcascade_b200.so")
-SOURCES = ["host.cpp", "eam_kernels.cu", "store_kernels.cu", "capi.cu", "peak.cu", "slab.cu"]
+SOURCES = ["host.cpp", "eam_kernels.cu", "store_kernels.cu", "capi.cu", "peak.cu", "slab.cu", "comm.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr",
          "-Xcompiler", "-fPIC,-fvisibility=hidden,-ffp-contract=off",
-         "-Xptxas", "-v", "-cudart", "static"]
+         "-Xptxas", "-v", "-cudart", "static", "-ldl"]
 
 
 def nvcc() -> str:

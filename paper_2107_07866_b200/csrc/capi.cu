@@ -8,6 +8,7 @@
 #include <string>
 #include <vector>
 
+#include "cbx_comm.h"
 #include "cbx_device.cuh"
 #include "cbx_host.h"
 
@@ -54,6 +55,12 @@ struct cbx_ctx {
   std::vector<int4> c_h4[2], c_f4[2];
   int c_hin[2] = {0, 0}, c_fin[2] = {0, 0};
   bool const_ready = false;
+  // in-graph NCCL exchange of a slab rank (cbx_slab_comm_init)
+  ncclComm_t comm = nullptr;
+  unsigned char* sbuf[2] = {nullptr, nullptr};
+  unsigned char* rbuf[2] = {nullptr, nullptr};
+  double* d_red = nullptr;
+  uint64_t graph_launches = 16;  // kernels per captured step
 
   template <class T>
   T* alloc(size_t n) {
@@ -248,8 +255,112 @@ void seq_force(cbx_ctx* c) {
   launch_clash_force(c->P, c->stream);
   c->launches += 3;
 }
+// ---- z-slab ranks: exchanges and reductions inside the step (NCCL) -------
+// Both halves of one exchange go out in one NCCL group: my "down" packet to
+// the rank below (it arrives there as "from above") and my "up" packet to the
+// rank above.  Messages have a fixed size (slab_msg_bytes), so the sequence
+// is capturable; with one rank both peers are this rank (self send/recv).
+void slab_exchange(cbx_ctx* c, int kind) {
+  const NcclApi& N = nccl();
+  const long long m = slab_msg_bytes(c->P, kind);
+  launch_pack(c->P, kind, -1, c->sbuf[0], m, c->stream);
+  launch_pack(c->P, kind, +1, c->sbuf[1], m, c->stream);
+  const int lo = (c->rank + c->nranks - 1) % c->nranks, hi = (c->rank + 1) % c->nranks;
+  nccl_check(N.group_start(), "ncclGroupStart");
+  nccl_check(N.send(c->sbuf[0], (size_t)m, ncclUint8, lo, c->comm, c->stream), "ncclSend");
+  nccl_check(N.recv(c->rbuf[1], (size_t)m, ncclUint8, hi, c->comm, c->stream), "ncclRecv");
+  nccl_check(N.send(c->sbuf[1], (size_t)m, ncclUint8, hi, c->comm, c->stream), "ncclSend");
+  nccl_check(N.recv(c->rbuf[0], (size_t)m, ncclUint8, lo, c->comm, c->stream), "ncclRecv");
+  nccl_check(N.group_end(), "ncclGroupEnd");
+  // position halos crossing the global z boundary are periodic images
+  const long long gs_lo = (kind == 1 && c->rank == 0) ? -1 : 0;
+  const long long gs_hi = (kind == 1 && c->rank == c->nranks - 1) ? 1 : 0;
+  launch_unpack(c->P, kind, -1, c->rbuf[0], gs_lo, c->d_rem_base + 0, c->stream);
+  launch_unpack(c->P, kind, +1, c->rbuf[1], gs_hi, c->d_rem_base + 1, c->stream);
+  c->launches += (kind == 1 || kind == 3) ? 8 : 4;
+}
+
+// StepState sums over ranks: energies (pair, embedding) and/or kinetic +
+// max speed (sum / max), then adaptive dt from the global max speed
+void slab_reduce(cbx_ctx* c, bool energies, bool kinetic) {
+  const NcclApi& N = nccl();
+  launch_slab_red_in(c->P, c->d_red, c->stream);
+  double* first = energies ? c->d_red : c->d_red + 2;
+  const size_t n = energies ? (kinetic ? 3 : 2) : 1;
+  nccl_check(N.all_reduce(first, first, n, ncclFloat64, ncclSum, c->comm, c->stream),
+             "ncclAllReduce");
+  if (kinetic)
+    nccl_check(N.all_reduce(c->d_red + 3, c->d_red + 3, 1, ncclFloat64, ncclMax, c->comm,
+                            c->stream),
+               "ncclAllReduce");
+  launch_slab_red_out(c->P, c->d_red, energies, kinetic, c->stream);
+  c->launches += 2;
+}
+
+void memset_field(cbx_ctx* c, int* field) { cudaMemsetAsync(field, 0, sizeof(int), c->stream); }
+
+// one step of a slab rank: the single-box sequence with the five exchanges
+void seq_slab_step(cbx_ctx* c) {
+  c->mask_valid = false;
+  ev_mark(c, 0);
+  memset_field(c, &c->P.st->n_out);
+  launch_kick_drift(c->P, 1, c->stream);
+  slab_exchange(c, 0);  // migrants
+  launch_rehash(c->P, c->stream);
+  launch_ghost_fill(c->P, c->stream);
+  c->launches += 4;
+  memset_field(c, &c->P.st->n_remote);
+  slab_exchange(c, 1);  // positions
+  ev_mark(c, 1);
+  launch_clash_images(c->P, c->stream);
+  c->launches += 1;
+  seq_density(c);
+  slab_exchange(c, 2);  // density partials (reverse)
+  ev_mark(c, 2);
+  seq_embed(c);
+  slab_exchange(c, 3);  // dF
+  ev_mark(c, 3);
+  launch_remote_df(c->P, c->stream);
+  c->launches += 1;
+  seq_force(c);
+  slab_exchange(c, 4);  // force partials (reverse)
+  ev_mark(c, 4);
+  launch_kick2(c->P, 1, c->stream);
+  launch_finalize(c->P, 1, 1, c->stream);
+  c->launches += 3;
+  slab_reduce(c, true, true);
+  ev_mark(c, 5);
+}
+
+// eval_forces of a slab rank (halos from the current positions)
+void seq_slab_eval(cbx_ctx* c) {
+  memset_field(c, &c->P.st->n_remote);
+  slab_exchange(c, 1);
+  ev_mark(c, 1);
+  launch_clash_images(c->P, c->stream);
+  c->launches += 1;
+  seq_density(c);
+  slab_exchange(c, 2);
+  ev_mark(c, 2);
+  seq_embed(c);
+  slab_exchange(c, 3);
+  ev_mark(c, 3);
+  launch_remote_df(c->P, c->stream);
+  c->launches += 1;
+  seq_force(c);
+  slab_exchange(c, 4);
+  ev_mark(c, 4);
+  launch_finalize(c->P, -1, 1, c->stream);
+  c->launches += 1;
+  slab_reduce(c, true, false);
+}
+
 // one velocity-Verlet step, sim.cpp:248-273
 void seq_step(cbx_ctx* c) {
+  if (c->comm) {
+    seq_slab_step(c);
+    return;
+  }
   c->mask_valid = false;
   ev_mark(c, 0);
   launch_kick_drift(c->P, 1, c->stream);
@@ -303,6 +414,7 @@ cudaGraphExec_t capture_step(cbx_ctx* c, bool with_events) {
   cuda_check(cudaStreamEndCapture(c->stream, &g), "end capture");
   cuda_check(cudaGraphInstantiate(&exec, g, 0), "graph instantiate");
   cudaGraphDestroy(g);
+  c->graph_launches = c->launches - l0;
   c->launches = l0;
   c->timing = t;
   return exec;
@@ -310,6 +422,17 @@ cudaGraphExec_t capture_step(cbx_ctx* c, bool with_events) {
 
 void build_graph(cbx_ctx* c) {
   if (!c->step_graph) c->step_graph = capture_step(c, false);
+}
+
+// single-box entry points that a slab rank can only run with its exchanges
+void require_box_or_comm(cbx_ctx* c, const char* what) {
+  if (c->G.slab && !c->comm)
+    raise(CBX_LOGIC, std::string(what) +
+                         ": slab rank without a communicator (cbx_slab_comm_init, or drive "
+                         "cbx_slab_phase with the exchanges)");
+}
+void require_box(cbx_ctx* c, const char* what) {
+  if (c->G.slab) raise(CBX_LOGIC, std::string(what) + ": not available on a slab rank");
 }
 
 void drop_graph(cbx_ctx* c) {
@@ -700,7 +823,7 @@ static cbx_status create_impl(const cbx_box* box, const cbx_potential* pot,
     for (auto& e : c->ev) cudaEventCreate(&e);
     c->box = *box;
     c->G = make_geo(*box);
-    if (slab && slab->nranks > 1) {
+    if (slab) {
       if (box->box_z < box->ghost_width)
         raise(CBX_INVALID_ARGUMENT, "z slab thinner than the ghost width");
       c->G.zoff = slab->zoff;
@@ -916,7 +1039,9 @@ static cbx_status create_impl(const cbx_box* box, const cbx_potential* pot,
     P.xp = std::getenv("CBX_XP") ? std::atoi(std::getenv("CBX_XP")) : 0;
     {
       const int maxn = std::max(std::max(fd[0].size(), fd[1].size()), std::max(hd[0].size(), hd[1].size()));
-      P.pmask = maxn <= 126 ? c->alloc<unsigned long long>(2 * S) : nullptr;
+      const char* nm = std::getenv("CBX_NOMASK");
+      P.pmask = maxn <= 126 && !(nm && std::atoi(nm)) ? c->alloc<unsigned long long>(2 * S)
+                                                       : nullptr;
     }
     {
       const char* e = std::getenv("CBX_TILE");
@@ -960,6 +1085,11 @@ CBX_API void cbx_destroy(cbx_ctx* c) {
   if (c->device >= 0 && c->device < 64 && g_const_owner[c->device] == c)
     g_const_owner[c->device] = nullptr;
   drop_graph(c);
+  if (c->comm) {
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    nccl().comm_destroy(c->comm);
+    c->comm = nullptr;
+  }
   if (c->stream) cudaStreamSynchronize(c->stream);
   for (void* p : c->allocs) cudaFree(p);
   if (c->flush_buf) cudaFree(c->flush_buf);
@@ -1008,7 +1138,10 @@ CBX_API cbx_status cbx_init_bcc(cbx_ctx* c, int species, double temperature, uin
   (void)species;
   return guarded(c, [&] {
     cudaSetDevice(c->device);
-    HostLattice L = init_bcc(c->box, c->pot.mass, temperature, seed);
+    // a slab rank keeps its planes of the global lattice (same RNG stream,
+    // so the decomposed initial state equals the single-box one)
+    HostLattice L = c->G.slab ? init_bcc_slab(c->gbox, c->G, c->pot.mass, temperature, seed)
+                              : init_bcc(c->box, c->pot.mass, temperature, seed);
     cbx_store s{};
     s.n_slots = c->S;
     s.pos = L.pos.data();
@@ -1023,6 +1156,7 @@ CBX_API cbx_status cbx_init_bcc(cbx_ctx* c, int species, double temperature, uin
 CBX_API cbx_status cbx_rehash(cbx_ctx* c) {
   return guarded(c, [&] {
     cudaSetDevice(c->device);
+    require_box(c, "cbx_rehash");
     launch_kick_drift(c->P, 0, c->stream);
     launch_rehash(c->P, c->stream);
     c->launches += 3;
@@ -1034,6 +1168,7 @@ CBX_API cbx_status cbx_rehash(cbx_ctx* c) {
 CBX_API cbx_status cbx_fill_ghosts(cbx_ctx* c) {
   return guarded(c, [&] {
     cudaSetDevice(c->device);
+    require_box(c, "cbx_fill_ghosts");
     seq_fill_ghosts(c);
     sync_status(c);
     raise_device_error(c, false);
@@ -1044,15 +1179,20 @@ CBX_API cbx_status cbx_eval_forces(cbx_ctx* c, double* e_emb, double* e_pair) {
   return guarded(c, [&] {
     cudaSetDevice(c->device);
     check_cutoff(c);
-    ev_mark(c, 1);
-    seq_density(c);
-    ev_mark(c, 2);
-    seq_embed(c);
-    ev_mark(c, 3);
-    seq_force(c);
-    ev_mark(c, 4);
-    launch_finalize(c->P, -1, 1, c->stream);
-    c->launches += 1;
+    require_box_or_comm(c, "cbx_eval_forces");
+    if (c->comm) {
+      seq_slab_eval(c);
+    } else {
+      ev_mark(c, 1);
+      seq_density(c);
+      ev_mark(c, 2);
+      seq_embed(c);
+      ev_mark(c, 3);
+      seq_force(c);
+      ev_mark(c, 4);
+      launch_finalize(c->P, -1, 1, c->stream);
+      c->launches += 1;
+    }
     sync_status(c);
     accumulate_timing(c, false);
     raise_device_error(c, false);
@@ -1063,6 +1203,7 @@ CBX_API cbx_status cbx_eval_forces(cbx_ctx* c, double* e_emb, double* e_pair) {
 CBX_API cbx_status cbx_compute_density(cbx_ctx* c) {
   return guarded(c, [&] {
     cudaSetDevice(c->device);
+    require_box(c, "cbx_compute_density");
     check_cutoff(c);
     seq_density(c);
     sync_status(c);
@@ -1072,6 +1213,7 @@ CBX_API cbx_status cbx_compute_density(cbx_ctx* c) {
 CBX_API cbx_status cbx_compute_embedding_derivative(cbx_ctx* c, double* e_emb) {
   return guarded(c, [&] {
     cudaSetDevice(c->device);
+    require_box(c, "cbx_compute_embedding_derivative");
     seq_embed(c);
     launch_finalize(c->P, -1, 1, c->stream);
     c->launches += 1;
@@ -1083,6 +1225,7 @@ CBX_API cbx_status cbx_compute_embedding_derivative(cbx_ctx* c, double* e_emb) {
 CBX_API cbx_status cbx_compute_pair_forces(cbx_ctx* c, double* e_pair) {
   return guarded(c, [&] {
     cudaSetDevice(c->device);
+    require_box(c, "cbx_compute_pair_forces");
     check_cutoff(c);
     seq_force(c);
     launch_finalize(c->P, -1, 1, c->stream);
@@ -1115,6 +1258,7 @@ CBX_API cbx_status cbx_step(cbx_ctx* c, double dt, long nsteps, cbx_state* out) 
     cudaSetDevice(c->device);
     check_cutoff(c);
     if (nsteps < 0) raise(CBX_INVALID_ARGUMENT, "nsteps must be >= 0");
+    require_box_or_comm(c, "cbx_step");
     sync_status(c);
     if (dt > 0.0) {
       c->hst.dt_next = dt;
@@ -1128,7 +1272,7 @@ CBX_API cbx_status cbx_step(cbx_ctx* c, double dt, long nsteps, cbx_state* out) 
     for (long i = 0; i < nsteps; ++i) {
       if (c->use_graph && !c->timing) {
         cuda_check(cudaGraphLaunch(c->step_graph, c->stream), "graph launch");
-        c->launches += 16;
+        c->launches += c->graph_launches;
       } else {
         seq_step(c);
         accumulate_timing(c, true);
@@ -1160,6 +1304,7 @@ CBX_API cbx_status cbx_measure(cbx_ctx* c) {
     launch_kick2(c->P, 0, c->stream);
     launch_finalize(c->P, 0, 0, c->stream);
     c->launches += 3;
+    if (c->comm) slab_reduce(c, false, true);
     sync_status(c);
     raise_device_error(c, false);
   });
@@ -1216,7 +1361,8 @@ CBX_API cbx_status cbx_inject_pka(cbx_ctx* c, int64_t site, const double v[3]) {
                             cudaMemcpyHostToDevice),
                  "pka");
   });
-  return rc == CBX_OK ? cbx_measure(c) : rc;
+  // a slab rank only sets the velocity: cbx_measure is collective there
+  return rc == CBX_OK && !c->G.slab ? cbx_measure(c) : rc;
 }
 
 CBX_API cbx_status cbx_count_defects(cbx_ctx* c, long out[3]) {
@@ -1274,6 +1420,7 @@ CBX_API cbx_status cbx_bench_steps(cbx_ctx* c, double dt, long nsteps, double fl
     cudaSetDevice(c->device);
     check_cutoff(c);
     sync_status(c);
+    require_box_or_comm(c, "cbx_bench_steps");
     c->hst.dt_next = dt;
     c->hst.adaptive = 0;
     write_status(c);
@@ -1288,7 +1435,7 @@ CBX_API cbx_status cbx_bench_steps(cbx_ctx* c, double dt, long nsteps, double fl
     for (long i = 0; i < nsteps; ++i) {
       if (fb) cudaMemsetAsync(c->flush_buf, (int)(i & 0xff), fb, c->stream);  // evict L2
       cuda_check(cudaGraphLaunch(c->timed_graph, c->stream), "graph launch");
-      c->launches += 16;
+      c->launches += c->graph_launches;
       cuda_check(cudaEventSynchronize(c->ev[5]), "event sync");
       float ms;
       const int seg[6][2] = {{1, 2}, {2, 3}, {3, 4}, {0, 1}, {4, 5}, {0, 5}};
@@ -1337,7 +1484,6 @@ CBX_API cbx_status cbx_create_slab(const cbx_box* global_box, const cbx_potentia
     set_thread_error("cbx_create_slab: bad rank / nranks");
     return CBX_INVALID_ARGUMENT;
   }
-  if (nranks == 1) return create_impl(global_box, pot, idx, device, nullptr, out);
   const long gbz = global_box->box_z;
   const long z0 = rank * gbz / nranks, z1 = (rank + 1) * gbz / nranks;
   cbx_box local = *global_box;
@@ -1511,6 +1657,41 @@ CBX_API cbx_status cbx_slab_commit(cbx_ctx* c, const double in[4]) {
     if (c->hst.adaptive)
       c->hst.dt_next = cbx_adaptive_dt(in[3], c->hst.dt_max, c->hst.max_disp);
     write_status(c);
+  });
+}
+
+CBX_API cbx_status cbx_nccl_unique_id(void* out, long nbytes) {
+  return guarded(nullptr, [&] {
+    if (nbytes < (long)sizeof(ncclUniqueId))
+      raise(CBX_INVALID_ARGUMENT, "cbx_nccl_unique_id: buffer smaller than 128 bytes");
+    ncclUniqueId id;
+    nccl_check(nccl().get_unique_id(&id), "ncclGetUniqueId");
+    std::memcpy(out, &id, sizeof id);
+  });
+}
+
+// collective over the slab ranks: every rank passes the same id
+CBX_API cbx_status cbx_slab_comm_init(cbx_ctx* c, const void* id, long nbytes) {
+  return guarded(c, [&] {
+    cudaSetDevice(c->device);
+    if (!c->G.slab) raise(CBX_LOGIC, "cbx_slab_comm_init: not a slab rank");
+    if (c->comm) raise(CBX_LOGIC, "cbx_slab_comm_init: communicator already set");
+    if (nbytes < (long)sizeof(ncclUniqueId))
+      raise(CBX_INVALID_ARGUMENT, "cbx_slab_comm_init: id smaller than 128 bytes");
+    ncclUniqueId u;
+    std::memcpy(&u, id, sizeof u);
+    long long mx = 0;
+    for (int k = 0; k < 5; ++k) mx = std::max(mx, slab_msg_bytes(c->P, k));
+    for (int i = 0; i < 2; ++i) {
+      c->sbuf[i] = c->alloc<unsigned char>(mx);
+      c->rbuf[i] = c->alloc<unsigned char>(mx);
+      cudaMemset(c->rbuf[i], 0, mx);
+    }
+    c->d_red = c->alloc<double>(8);
+    ncclComm_t comm = nullptr;
+    nccl_check(nccl().comm_init_rank(&comm, c->nranks, u, c->rank), "ncclCommInitRank");
+    c->comm = comm;
+    drop_graph(c);
   });
 }
 

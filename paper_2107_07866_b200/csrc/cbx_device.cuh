@@ -186,6 +186,10 @@ int eam_blocks(const KP& P);
 int pair_partials(const KP& P, int mode);
 void launch_uf_refresh(const KP& P, cudaStream_t s);
 long long slab_buffer_bytes(const KP& P, int kind);
+constexpr long long kMsgRecords = 8192;  // clash / migrant records per in-graph message
+long long slab_msg_bytes(const KP& P, int kind);
+void launch_slab_red_in(const KP& P, double* red, cudaStream_t s);
+void launch_slab_red_out(const KP& P, const double* red, int energies, int kinetic, cudaStream_t s);
 void launch_pack(const KP& P, int kind, int dir, unsigned char* buf, long long cap,
                  cudaStream_t s);
 void launch_unpack(const KP& P, int kind, int from, const unsigned char* buf, long long gshift,

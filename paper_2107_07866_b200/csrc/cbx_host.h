@@ -67,6 +67,8 @@ struct HostLattice {
   long n_atoms = 0;
 };
 HostLattice init_bcc(const cbx_box& b, double mass, double temperature, uint64_t seed);
+HostLattice init_bcc_slab(const cbx_box& global, const Geo& local, double mass,
+                          double temperature, uint64_t seed);
 
 Geo make_geo(const cbx_box& b);
 

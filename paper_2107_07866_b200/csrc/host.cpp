@@ -249,7 +249,13 @@ double accel_factor() { return accel_factor_c; }
 double mv2_to_ev() { return 1.0 / accel_factor_c; }
 double speed_factor() { return 98.22694750253277; }
 
-HostLattice init_bcc(const cbx_box& b, double mass, double temperature, uint64_t seed) {
+// init_bcc over the global box `b`; sites of global interior planes
+// [z_lo, z_hi) are stored in the layout of `out_geo` shifted down by z_lo -
+// out_geo.g planes (the whole box: z_lo = 0, out_geo = make_geo(b)).  The
+// RNG stream and the momentum removal run over every global site in id
+// order, so a slab gets exactly the single-box values of its planes.
+static HostLattice init_bcc_planes(const cbx_box& b, const Geo& out_geo, long z_lo, long z_hi,
+                                   double mass, double temperature, uint64_t seed) {
   const Geo G = make_geo(b);
   const double sigma =
       temperature > 0.0 ? std::sqrt(boltzmann_ev * temperature * accel_factor_c / mass) : 0.0;
@@ -268,7 +274,8 @@ HostLattice init_bcc(const cbx_box& b, double mass, double temperature, uint64_t
     have = true;
     return r * std::cos(a);
   };
-  const long long S = 2 * G.NC;
+  const Geo& O = out_geo;
+  const long long S = 2 * O.NC;
   HostLattice L;
   L.pos.assign(3 * S, 0.0);
   L.vel.assign(3 * S, 0.0);
@@ -276,10 +283,22 @@ HostLattice init_bcc(const cbx_box& b, double mass, double temperature, uint64_t
   L.valid.assign(S, 0);
   uint64_t tag = 0;
   const double a = b.a0;
-  for (long z = G.g; z < G.g + G.bz; ++z)
+  double mx = 0, my = 0, mz = 0;  // net momentum, summed in global site-id order
+  for (long z = G.g; z < G.g + G.bz; ++z) {
+    const bool mine = z - G.g >= z_lo && z - G.g < z_hi;
+    const long zl = z - z_lo;  // local plane (the halo offset g is shared)
     for (long y = G.g; y < G.g + G.by; ++y)
       for (long x = 2 * G.g; x < 2 * (G.g + G.bx); ++x) {
-        const long long id = ((long long)z * G.ty + y) * (2 * G.tx) + x;
+        double v[3];
+        v[0] = sigma * gauss();
+        v[1] = sigma * gauss();
+        v[2] = sigma * gauss();
+        mx += v[0];
+        my += v[1];
+        mz += v[2];
+        const uint64_t t = tag++;
+        if (!mine) continue;
+        const long long id = ((long long)zl * O.ty + y) * (2 * O.tx) + x;
         double* p = &L.pos[3 * id];
         if (x % 2 == 0) {  // site_position, lattice.cpp:45-52
           p[0] = 0.5 * x * a;
@@ -290,22 +309,13 @@ HostLattice init_bcc(const cbx_box& b, double mass, double temperature, uint64_t
           p[1] = y * a + 0.5 * a;
           p[2] = z * a + 0.5 * a;
         }
-        double* v = &L.vel[3 * id];
-        v[0] = sigma * gauss();
-        v[1] = sigma * gauss();
-        v[2] = sigma * gauss();
-        L.tag[id] = tag++;
+        for (int k = 0; k < 3; ++k) L.vel[3 * id + k] = v[k];
+        L.tag[id] = t;
         L.valid[id] = 1;
       }
+  }
   L.n_atoms = (long)tag;
-  // remove the net momentum in site-id order (sim.cpp:122-128)
-  double mx = 0, my = 0, mz = 0;
-  for (long long id = 0; id < S; ++id)
-    if (L.valid[id]) {
-      mx += L.vel[3 * id];
-      my += L.vel[3 * id + 1];
-      mz += L.vel[3 * id + 2];
-    }
+  // remove the net momentum (sim.cpp:122-128)
   const double inv = 1.0 / (double)L.n_atoms;
   mx *= inv;
   my *= inv;
@@ -316,6 +326,20 @@ HostLattice init_bcc(const cbx_box& b, double mass, double temperature, uint64_t
       L.vel[3 * id + 1] -= my;
       L.vel[3 * id + 2] -= mz;
     }
+  return L;
+}
+
+HostLattice init_bcc(const cbx_box& b, double mass, double temperature, uint64_t seed) {
+  return init_bcc_planes(b, make_geo(b), 0, b.box_z, mass, temperature, seed);
+}
+
+HostLattice init_bcc_slab(const cbx_box& global, const Geo& local, double mass,
+                          double temperature, uint64_t seed) {
+  HostLattice L = init_bcc_planes(global, local, local.zoff, local.zoff + local.bz, mass,
+                                  temperature, seed);
+  long n = 0;
+  for (uint8_t v : L.valid) n += v;
+  L.n_atoms = n;  // atoms of this slab
   return L;
 }
 

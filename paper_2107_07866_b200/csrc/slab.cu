@@ -62,7 +62,8 @@ __global__ void k_pack_migrants(KP P, int dir, unsigned char* buf, long long cap
     rec[k] = r;
   }
   __syncthreads();
-  if (threadIdx.x == 0) cnt[0] = s_n;
+  if (threadIdx.x == 0)
+    cnt[0] = min((long long)s_n, (cap - 16) / (long long)sizeof(MigRec));  // records written
 }
 
 __global__ void k_unpack_migrants(KP P, const unsigned char* buf, long long gshift) {
@@ -243,6 +244,22 @@ long long slab_plane_bytes(const KP& P, int kind) {
     default: return n * 24;
   }
 }
+// fixed message size of the in-graph NCCL exchange (sizes cannot depend on
+// device-side counts inside a captured step): the planes plus room for
+// kMsgRecords records; more sets CBX_RUNTIME on the sender
+long long slab_msg_bytes(const KP& P, int kind) {
+  const long long R = std::min<long long>(P.cap_rem, kMsgRecords);
+  const long long M = std::min<long long>(P.cap_mov, kMsgRecords);
+  long long b;
+  if (kind == 0) {
+    b = 16 + M * (long long)sizeof(MigRec);
+  } else {
+    b = slab_plane_bytes(P, kind);
+    if (kind == 1 || kind == 3) b += 16 + R * (long long)sizeof(RemRec);
+  }
+  return (b + 255) / 256 * 256;
+}
+
 long long slab_buffer_bytes(const KP& P, int kind) {
   if (kind == 0) return 16 + (long long)P.cap_mov * sizeof(MigRec);
   long long b = slab_plane_bytes(P, kind);
@@ -276,5 +293,41 @@ void launch_unpack(const KP& P, int kind, int from, const unsigned char* buf, lo
 }
 
 void launch_remote_df(const KP& P, cudaStream_t s) { k_remote_df<<<8, 256, 0, s>>>(P); }
+
+// ------------------------------------------------- step-state all-reduce
+// red = {pair, embedding, kinetic, max_speed}: the local sums go in, the
+// all-reduced values (sum, sum, sum, max) come back into the StepState
+__global__ void k_slab_red_in(KP P, double* red) {
+  if (threadIdx.x != 0) return;
+  const DevStatus* st = P.st;
+  red[0] = st->pair;
+  red[1] = st->embedding;
+  red[2] = st->kinetic;
+  red[3] = st->max_speed;
+}
+__global__ void k_slab_red_out(KP P, const double* red, int energies, int kinetic) {
+  if (threadIdx.x != 0) return;
+  DevStatus* st = P.st;
+  if (energies) {
+    st->pair = red[0];
+    st->embedding = red[1];
+  }
+  if (kinetic) {
+    st->kinetic = red[2];
+    st->max_speed = red[3];
+    if (st->adaptive) {  // adaptive_dt on the global max speed, sim.cpp:94-98
+      double dt = st->dt_max;
+      if (st->max_speed > 0.0) dt = fmin(dt, xdiv(st->max_disp, st->max_speed));
+      st->dt_next = fmax(dt, 1e-7);
+    }
+  }
+}
+void launch_slab_red_in(const KP& P, double* red, cudaStream_t s) {
+  k_slab_red_in<<<1, 32, 0, s>>>(P, red);
+}
+void launch_slab_red_out(const KP& P, const double* red, int energies, int kinetic,
+                         cudaStream_t s) {
+  k_slab_red_out<<<1, 32, 0, s>>>(P, red, energies, kinetic);
+}
 
 }  // namespace cbx

@@ -425,7 +425,7 @@ __device__ __forceinline__ double force_site_mask(const KP& P, KP* Pp, int par, 
         k[b] = 63 + __ffsll(m1);
         m1 &= m1 - 1;
       } else {
-        k[b] = 0;
+        k[b] = k[0];  // padding lane: a real in-cutoff partner, result discarded
       }
     }
     int j[2], t[2], seg[2];
@@ -444,6 +444,15 @@ __device__ __forceinline__ double force_site_mask(const KP& P, KP* Pp, int par, 
       const double r2 = fma(dz[b], dz[b], fma(dy[b], dy[b], dx[b] * dx[b]));
       ri[b] = rsqrt(r2);
       seg[b] = seg_index(P.ff, r2 * ri[b], s[b]);
+#ifdef CBX_DEBUG_BOUNDS
+      if (j[b] < 0 || j[b] >= S || seg[b] < 0 || seg[b] > P.ff.nseg) {
+        printf("force_mask oob: d=%d par=%d k=%d j=%d seg=%d r2=%g v=%d m=%llx %llx\n", d, par,
+               k[b], j[b], seg[b], r2, (int)v[b], P.pmask[2 * (size_t)d],
+               P.pmask[2 * (size_t)d + 1]);
+        seg[b] = 0;
+        j[b] = d;
+      }
+#endif
     }
     double zA[2], zB[2], zC[2], zD[2], qA[2], qB[2], qC[2], qD[2];
 #pragma unroll
@@ -631,7 +640,7 @@ __device__ __forceinline__ double force_site_smtab(const KP& P, KP* Pp, const do
         k[b] = 63 + __ffsll(m1);
         m1 &= m1 - 1;
       } else {
-        k[b] = 0;
+        k[b] = k[0];  // padding lane: a real in-cutoff partner, result discarded
       }
     }
     int j[2], t[2], seg[2];

@@ -171,7 +171,7 @@ __device__ __forceinline__ double force_site_tile(const KP& P, KP* Pp, TileRef t
         k[b] = 63 + __ffsll(m1);
         m1 &= m1 - 1;
       } else {
-        k[b] = 0;
+        k[b] = k[0];  // padding lane: a real in-cutoff partner, result discarded
       }
     }
     int t[2], seg[2];

@@ -30,6 +30,7 @@ import numpy as np
 
 from . import _lib
 from ._lib import check
+from .engine import DeviceStore
 
 MIGRANTS, POS, RHO, DF, FRC = 0, 1, 2, 3, 4
 KIND_NAMES = {MIGRANTS: "migrants", POS: "pos", RHO: "rho", DF: "df", FRC: "frc"}
@@ -45,16 +46,23 @@ def neighbours(rank: int, nranks: int):
     return (rank - 1) % nranks, (rank + 1) % nranks
 
 
-class SlabRank:
-    """One z slab resident on one GPU (a cbx_ctx created by cbx_create_slab)."""
+class SlabRank(DeviceStore):
+    """One z slab resident on one GPU (a cbx_ctx made by cbx_create_slab).
 
-    def __init__(self, gbox, potential, rank: int, nranks: int, device: int = 0):
-        import torch
+    Two ways to drive it: phase by phase with host-side exchanges
+    (`SlabDomain` + `LocalExchange` / `DistExchange`), or -- the production
+    path -- `init_comm` once, after which `step`, `eval_forces`, `measure` and
+    the bench run the decomposed step as one CUDA graph per rank with the
+    NCCL exchanges inside it."""
+
+    def __init__(self, gbox, potential, rank: int, nranks: int, device: int = 0,
+                 stencil: str = "newton3"):
         lib = _lib.load()
         self.lib = lib
         self.potential = potential
         self.rank, self.nranks, self.device = rank, nranks, device
         self.gbox = gbox if isinstance(gbox, _lib.Box) else _lib.Box(*gbox)
+        self.box = self.gbox
         h = C.c_void_p()
         check(lib.cbx_create_slab(C.byref(self.gbox), potential.handle, None, rank, nranks,
                                   device, C.byref(h)))
@@ -63,28 +71,45 @@ class SlabRank:
         info = (C.c_long * 8)()
         check(lib.cbx_slab_info(h, info), h)
         self.info = tuple(info)
-        dev = torch.device("cuda", device)
-        self.comm_device = dev
-        # two send buffers per kind (toward the rank below / above)
-        self.buf = {}
-        for k in KIND_NAMES:
-            nb = lib.cbx_slab_buffer_bytes(h, k)
-            self.buf[k] = (torch.empty(nb, dtype=torch.uint8, device=dev),
-                           torch.empty(nb, dtype=torch.uint8, device=dev))
+        self._buf = None
+        if stencil != "newton3":
+            self.set_stencil(stencil)
 
-    def close(self):
-        if getattr(self, "h", None):
-            self.lib.cbx_destroy(self.h)
-            self.h = None
+    @property
+    def comm_device(self):
+        import torch
+        return torch.device("cuda", self.device)
 
-    def __del__(self):
-        self.close()
+    @property
+    def buf(self):
+        """two device send buffers per exchange kind (toward below / above)"""
+        if self._buf is None:
+            import torch
+            self._buf = {}
+            for k in KIND_NAMES:
+                nb = self.lib.cbx_slab_buffer_bytes(self.h, k)
+                self._buf[k] = (torch.empty(nb, dtype=torch.uint8, device=self.comm_device),
+                                torch.empty(nb, dtype=torch.uint8, device=self.comm_device))
+        return self._buf
+
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        b = C.create_string_buffer(128)
+        check(_lib.load().cbx_nccl_unique_id(b, 128))
+        return b.raw
+
+    def init_comm(self, uid: bytes):
+        """collective: every rank of the decomposition passes rank 0's id"""
+        b = C.create_string_buffer(uid, 128)
+        self._check(self.lib.cbx_slab_comm_init(self.h, b, 128))
+
+    def bench_steps(self, dt: float, n: int, flush_mb: float = 0.0):
+        out = (C.c_double * 8)()
+        self._check(self.lib.cbx_bench_steps(self.h, dt, n, flush_mb, out))
+        return list(out)
 
     def _check(self, rc):
         check(rc, self.h)
-
-    def set_adaptive(self, dt_max, max_disp):
-        self._check(self.lib.cbx_set_adaptive(self.h, dt_max, max_disp))
 
     def phase(self, p: int, dt: float = 0.0):
         self._check(self.lib.cbx_slab_phase(self.h, p, dt))
@@ -108,15 +133,6 @@ class SlabRank:
     def commit(self, vals):
         v = (C.c_double * 4)(*[float(x) for x in vals[:4]])
         self._check(self.lib.cbx_slab_commit(self.h, v))
-
-    def set_state(self, d: dict):
-        st = _lib.State(*[d.get(k, 0) for k, _ in _lib.State._fields_])
-        self._check(self.lib.cbx_set_state(self.h, C.byref(st)))
-
-    def count_defects(self):
-        out = (C.c_long * 3)()
-        self._check(self.lib.cbx_count_defects(self.h, out))
-        return tuple(out)
 
     def upload_global(self, s):
         from .engine import _ptr

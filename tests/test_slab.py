@@ -241,3 +241,104 @@ def test_slab_cascade(cuda, tables, n):
         assert_store_parity(_interior(rs), gather(dom, ref), pos_tol=1e-8, rel=1e-7,
                             what=f"slab cascade n={n} chunk {chunk}")
     assert saw_clash
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n", [1, 3])
+def test_slab_init_bcc_matches_single_box(cuda, tables, n):
+    """init_bcc on slab ranks keeps each slab's planes of the global lattice:
+    the same RNG stream and momentum removal as the single box"""
+    from oracle import oracle
+    from paper_2107_07866_b200 import EamPotential
+    ref = oracle.Sim(tables["baseline"], box=(7, 6, 9), temperature=600.0, seed=4242)
+    dims, a0, g = ref.box
+    pot = EamPotential.load(tables["baseline"])
+    ranks = [S.SlabRank((*dims, a0, g), pot, r, n) for r in range(n)]
+    tot = sum(r.init_bcc(600.0, 4242) for r in ranks)
+    assert tot == 2 * 7 * 6 * 9
+    dom = S.SlabDomain(ranks, S.LocalExchange(ranks))
+    a, b = _interior(ref.store()), gather(dom, ref)
+    m = a.valid.astype(bool) & ~a.ghost.astype(bool)
+    mb = b.valid.astype(bool) & ~b.ghost.astype(bool)
+    assert np.array_equal(m, mb)
+    assert np.array_equal(a.pos[m], b.pos[m])
+    assert np.array_equal(a.vel[m], b.vel[m])
+    assert np.array_equal(a.tag[m], b.tag[m])
+
+
+def native_rank(ref, path):
+    """one slab rank that owns the whole box, exchanging with itself through
+    NCCL inside its step graph (the n == 1 case of the multi-GPU path)"""
+    from paper_2107_07866_b200 import EamPotential
+    dims, a0, g = ref.box
+    r = S.SlabRank((*dims, a0, g), EamPotential.load(path), 0, 1)
+    r.init_comm(S.SlabRank.nccl_unique_id())
+    r.upload_global(ref.store())
+    r.set_state(ref.state())
+    return r
+
+
+@pytest.mark.gpu
+def test_slab_local_exchange_single_rank(cuda, tables):
+    """the phase-driven path with one rank: halos are its own periodic images"""
+    from oracle import oracle
+    ref = oracle.Sim(tables["baseline"], box=(8, 8, 8), temperature=600.0, seed=5)
+    dom = slab_domain(ref, tables["baseline"], 1)
+    dom.prime()
+    ref.step(1e-3, 10)
+    dom.step(1e-3, 10)
+    assert_store_parity(_interior(ref.store()), gather(dom, ref), pos_tol=1e-10, rel=1e-9)
+
+
+@pytest.mark.gpu
+def test_slab_nccl_graph_eval_and_trajectory(cuda, tables):
+    """NCCL exchanges captured in the step graph (self send/recv): forces,
+    energies and a 60-step trajectory equal the single-box oracle"""
+    from oracle import oracle
+    ref = oracle.Sim(tables["baseline"], box=(8, 7, 9), temperature=600.0, seed=12345)
+    r = native_rank(ref, tables["baseline"])
+    e_emb, e_pair = r.eval_forces()
+    r.measure()
+    sr = ref.state()
+    assert abs(e_pair - sr["pair"]) <= 1e-10 * abs(sr["pair"])
+    assert abs(e_emb - sr["embedding"]) <= 1e-10 * abs(sr["embedding"])
+    assert abs(r.state()["kinetic"] - sr["kinetic"]) <= 1e-12 * sr["kinetic"]
+    dom = S.SlabDomain([r], None)
+    assert_store_parity(_interior(ref.store()), gather(dom, ref), what="nccl eval")
+    launches0 = r.kernel_launches()
+    for chunk in range(3):
+        ref.step(1e-3, 20)
+        st = r.step(1e-3, 20)
+        sr = ref.state()
+        assert st["step"] == sr["step"]
+        for k in ("kinetic", "pair", "embedding"):
+            assert abs(st[k] - sr[k]) <= 1e-9 * abs(sr[k]), (chunk, k, st[k], sr[k])
+        assert_store_parity(_interior(ref.store()), gather(dom, ref), pos_tol=1e-9, rel=1e-8,
+                            what=f"nccl chunk {chunk}")
+    assert r.kernel_launches() > launches0
+
+
+@pytest.mark.gpu
+def test_slab_nccl_graph_cascade(cuda, tables):
+    """cascade with adaptive dt through the NCCL step graph: clash records,
+    defect counts and the global-max-speed time step match the oracle"""
+    from oracle import oracle
+    ref = oracle.Sim(tables["baseline"], box=(10, 10, 10), temperature=600.0, seed=12345,
+                     pka_energy_kev=1.0, pka_site=(5, 5, 3))
+    ref.step(1e-3, 5)
+    ref.inject_pka()
+    r = native_rank(ref, tables["baseline"])
+    r.eval_forces()
+    r.measure()
+    dom = S.SlabDomain([r], None)
+    saw_clash = False
+    for chunk in range(6):
+        ref.step(-1, 20)
+        r.step(-1, 20)
+        rs = ref.store()
+        saw_clash |= (rs.clash_ghost == 0).sum() > 0
+        assert r.state()["t"] == pytest.approx(ref.state()["t"], rel=1e-12, abs=0)
+        assert ref.count_defects() == r.count_defects(), chunk
+        assert_store_parity(_interior(rs), gather(dom, ref), pos_tol=1e-8, rel=1e-7,
+                            what=f"nccl cascade chunk {chunk}")
+    assert saw_clash
