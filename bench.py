@@ -155,7 +155,16 @@ def run_ours(args, w, path, ws, rank, local):
 
     lib = _lib.load()
     pot = EamPotential.load(path)
-    dev, n = build_device_state(w, pot, device=local, stencil=args.stencil)
+    slab = ws > 1 or args.slab
+    if slab:
+        # z-slab decomposition: rank r owns cells[2] planes of a box stacked
+        # ws times along z; halos, migrants and the StepState reduction go
+        # through NCCL inside each rank's step graph
+        from paper_2107_07866_b200.workloads import build_slab_state
+        dev, n = build_slab_state(w, pot, rank, ws, device=local, stencil=args.stencil,
+                                  transport=args.transport)
+    else:
+        dev, n = build_device_state(w, pot, device=local, stencil=args.stencil)
     cand, pairs = dev.count_pairs()  # candidates / in-cutoff pairs of one half-list pass
     peak = C.c_double()
     mhz = C.c_double()
@@ -210,7 +219,7 @@ def run_ours(args, w, path, ws, rank, local):
         pass
 
     # e2e through the C ABI with host buffers
-    e2e = run_e2e(dev, w, args.e2e_steps)
+    e2e = run_e2e(dev, w, args.e2e_steps, ws, local)
     res = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
@@ -218,7 +227,10 @@ def run_ours(args, w, path, ws, rank, local):
            "config": {"workload": w.note, "atoms_per_gpu": n, "dt_ps": w.dt,
                       "stencil": args.stencil,
                       "l2": f"flushed ({args.flush_mb:.0f} MB write) before every timed step",
-                      "parallelism": "single-gpu" if ws == 1 else f"{ws} independent replicas"},
+                      "parallelism": (f"z-slab x{ws}, {args.transport} halo/migrant "
+                                      f"exchange + reduction inside the step graph") if slab
+                                     else "single-gpu",
+                      "global_cells": [w.cells[0], w.cells[1], w.cells[2] * ws]},
            "roofline": roofline, "e2e": e2e, "gpu_launches": launches,
            "clocks": clocks.summary(),
            "kernels_ms_per_step": {k: v / K for k, v in t.items()},
@@ -227,20 +239,30 @@ def run_ours(args, w, path, ws, rank, local):
     return res
 
 
-def run_e2e(dev, w, steps):
-    """host-resident store: upload -> one device step -> download, per step"""
+def run_e2e(dev, w, steps, ws=1, local=0):
+    """host-resident store: upload -> one device step -> download, per step
+    (every rank; the slowest rank's time counts)"""
     s = dev.download()
     nbytes_in = sum(getattr(s, k).nbytes for k in ("pos", "vel", "force", "rho", "df", "tag",
                                                    "valid", "ghost"))
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
     t0 = time.perf_counter()
     for _ in range(steps):
         dev.upload(s)
         dev.step(w.dt, 1)
         s = dev.download()
     el = time.perf_counter() - t0
+    if ws > 1:
+        import torch
+        import torch.distributed as dist
+        x = torch.tensor([el], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(x, op=dist.ReduceOp.MAX)
+        el = float(x.item())
     nbytes_out = sum(getattr(s, k).nbytes for k in ("pos", "vel", "force", "rho", "df", "tag",
                                                     "valid", "ghost", "clash_key", "clash_pos"))
-    n = int((s.valid.astype(bool) & ~s.ghost.astype(bool)).sum())
+    n = int((s.valid.astype(bool) & ~s.ghost.astype(bool)).sum()) * ws
     return {"value": n * steps / el, "unit": UNIT, "h2d_bytes_per_step": int(nbytes_in),
             "d2h_bytes_per_step": int(nbytes_out), "steps": steps,
             "path": "cbx_upload_store -> cbx_step(dt,1) -> cbx_download_store (host buffers)"}
@@ -266,6 +288,10 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--transport", default="p2p", choices=["p2p", "nccl"],
+                    help="slab exchange: peer-memory kernels or NCCL send/recv")
+    ap.add_argument("--slab", action="store_true",
+                    help="use the slab path (NCCL self-exchange) also at N=1")
     args = ap.parse_args()
     ws, rank, local = dist_env()
     from paper_2107_07866_b200.workloads import CONFIGS

@@ -221,6 +221,15 @@ CBX_API cbx_status cbx_slab_commit(cbx_ctx* ctx, const double in[4]);
  * send/recv (the periodic z images of a one-slab box). */
 CBX_API cbx_status cbx_nccl_unique_id(void* out, long nbytes);
 CBX_API cbx_status cbx_slab_comm_init(cbx_ctx* ctx, const void* id, long nbytes);
+/* Peer-memory exchange (ranks on one node, NVLink / NVSwitch): each rank
+ * exports its receive region (64-byte CUDA IPC handle), every rank passes the
+ * handles of all ranks (in rank order) to cbx_slab_p2p_init.  Each exchange
+ * is then two kernels -- the sender stores its boundary data straight into
+ * the neighbour's memory and raises a flag, the receiver waits on it and
+ * unpacks -- and the StepState reduction is one kernel.  Takes precedence
+ * over an NCCL communicator.  nranks == 1 maps the rank onto itself. */
+CBX_API cbx_status cbx_slab_p2p_handle(cbx_ctx* ctx, void* out, long nbytes);
+CBX_API cbx_status cbx_slab_p2p_init(cbx_ctx* ctx, const void* handles, long nbytes);
 CBX_API cbx_status cbx_upload_store_global(cbx_ctx* ctx, const cbx_store* global_store);
 CBX_API cbx_status cbx_download_store_global(cbx_ctx* ctx, cbx_store* global_store,
                                              long* n_clash_inout);

@@ -145,6 +145,8 @@ SIGNATURES = [
     ("cbx_slab_commit", C.c_int, [_P, C.POINTER(C.c_double)]),
     ("cbx_nccl_unique_id", C.c_int, [_P, C.c_long]),
     ("cbx_slab_comm_init", C.c_int, [_P, _P, C.c_long]),
+    ("cbx_slab_p2p_handle", C.c_int, [_P, _P, C.c_long]),
+    ("cbx_slab_p2p_init", C.c_int, [_P, _P, C.c_long]),
     ("cbx_upload_store_global", C.c_int, [_P, C.POINTER(Store)]),
     ("cbx_download_store_global", C.c_int, [_P, C.POINTER(Store), C.POINTER(C.c_long)]),
 ]

@@ -61,6 +61,13 @@ struct cbx_ctx {
   unsigned char* rbuf[2] = {nullptr, nullptr};
   double* d_red = nullptr;
   uint64_t graph_launches = 16;  // kernels per captured step
+  // peer-memory exchange (cbx_slab_p2p_init): this rank's receive region,
+  // the neighbours' regions mapped through CUDA IPC
+  unsigned char* p2p_region = nullptr;
+  size_t p2p_bytes = 0;
+  std::vector<void*> p2p_opened;
+  P2PLinks links{};
+  bool p2p = false;
 
   template <class T>
   T* alloc(size_t n) {
@@ -260,7 +267,16 @@ void seq_force(cbx_ctx* c) {
 // the rank below (it arrives there as "from above") and my "up" packet to the
 // rank above.  Messages have a fixed size (slab_msg_bytes), so the sequence
 // is capturable; with one rank both peers are this rank (self send/recv).
+bool has_transport(const cbx_ctx* c) { return c->comm != nullptr || c->p2p; }
+
 void slab_exchange(cbx_ctx* c, int kind) {
+  if (c->p2p) {  // fused: pack into the neighbours' memory, wait, unpack
+    const long long gs_lo = (kind == 1 && c->rank == 0) ? -1 : 0;
+    const long long gs_hi = (kind == 1 && c->rank == c->nranks - 1) ? 1 : 0;
+    launch_p2p_exchange(c->P, c->links, kind, gs_lo, gs_hi, c->d_rem_base, c->stream);
+    c->launches += 2;
+    return;
+  }
   const NcclApi& N = nccl();
   const long long m = slab_msg_bytes(c->P, kind);
   launch_pack(c->P, kind, -1, c->sbuf[0], m, c->stream);
@@ -283,6 +299,11 @@ void slab_exchange(cbx_ctx* c, int kind) {
 // StepState sums over ranks: energies (pair, embedding) and/or kinetic +
 // max speed (sum / max), then adaptive dt from the global max speed
 void slab_reduce(cbx_ctx* c, bool energies, bool kinetic) {
+  if (c->p2p) {
+    launch_p2p_reduce(c->P, c->links, energies, kinetic, c->stream);
+    c->launches += 1;
+    return;
+  }
   const NcclApi& N = nccl();
   launch_slab_red_in(c->P, c->d_red, c->stream);
   double* first = energies ? c->d_red : c->d_red + 2;
@@ -357,7 +378,7 @@ void seq_slab_eval(cbx_ctx* c) {
 
 // one velocity-Verlet step, sim.cpp:248-273
 void seq_step(cbx_ctx* c) {
-  if (c->comm) {
+  if (has_transport(c)) {
     seq_slab_step(c);
     return;
   }
@@ -426,7 +447,7 @@ void build_graph(cbx_ctx* c) {
 
 // single-box entry points that a slab rank can only run with its exchanges
 void require_box_or_comm(cbx_ctx* c, const char* what) {
-  if (c->G.slab && !c->comm)
+  if (c->G.slab && !has_transport(c))
     raise(CBX_LOGIC, std::string(what) +
                          ": slab rank without a communicator (cbx_slab_comm_init, or drive "
                          "cbx_slab_phase with the exchanges)");
@@ -1090,6 +1111,8 @@ CBX_API void cbx_destroy(cbx_ctx* c) {
     nccl().comm_destroy(c->comm);
     c->comm = nullptr;
   }
+  for (void* p : c->p2p_opened) cudaIpcCloseMemHandle(p);
+  if (c->p2p_region) cudaFree(c->p2p_region);
   if (c->stream) cudaStreamSynchronize(c->stream);
   for (void* p : c->allocs) cudaFree(p);
   if (c->flush_buf) cudaFree(c->flush_buf);
@@ -1180,7 +1203,7 @@ CBX_API cbx_status cbx_eval_forces(cbx_ctx* c, double* e_emb, double* e_pair) {
     cudaSetDevice(c->device);
     check_cutoff(c);
     require_box_or_comm(c, "cbx_eval_forces");
-    if (c->comm) {
+    if (has_transport(c)) {
       seq_slab_eval(c);
     } else {
       ev_mark(c, 1);
@@ -1304,7 +1327,7 @@ CBX_API cbx_status cbx_measure(cbx_ctx* c) {
     launch_kick2(c->P, 0, c->stream);
     launch_finalize(c->P, 0, 0, c->stream);
     c->launches += 3;
-    if (c->comm) slab_reduce(c, false, true);
+    if (has_transport(c)) slab_reduce(c, false, true);
     sync_status(c);
     raise_device_error(c, false);
   });
@@ -1691,6 +1714,101 @@ CBX_API cbx_status cbx_slab_comm_init(cbx_ctx* c, const void* id, long nbytes) {
     ncclComm_t comm = nullptr;
     nccl_check(nccl().comm_init_rank(&comm, c->nranks, u, c->rank), "ncclCommInitRank");
     c->comm = comm;
+    drop_graph(c);
+  });
+}
+
+// ---- P2P transport: receive regions exchanged as CUDA IPC handles --------
+// region layout (identical on every rank: message sizes depend only on the
+// shared x/y extent and ghost width): flags [5][2] u64 @0, reduction flags
+// [8] u64 @256, reduction slots [8][4] f64 @512, receive buffers from @1024
+namespace {
+constexpr size_t kFlagOff = 0, kRedFlagOff = 256, kRedOff = 512, kBufOff = 1024;
+size_t p2p_buf_off(const KP& P, int kind, int from) {
+  size_t o = kBufOff;
+  for (int k = 0; k < 5; ++k)
+    for (int f = 0; f < 2; ++f) {
+      if (k == kind && f == from) return o;
+      o += (size_t)slab_msg_bytes(P, k);
+    }
+  return o;
+}
+}  // namespace
+
+CBX_API cbx_status cbx_slab_p2p_handle(cbx_ctx* c, void* out, long nbytes) {
+  return guarded(c, [&] {
+    cudaSetDevice(c->device);
+    if (!c->G.slab) raise(CBX_LOGIC, "cbx_slab_p2p_handle: not a slab rank");
+    if (nbytes < (long)sizeof(cudaIpcMemHandle_t))
+      raise(CBX_INVALID_ARGUMENT, "cbx_slab_p2p_handle: buffer smaller than 64 bytes");
+    if (!c->p2p_region) {
+      c->p2p_bytes = p2p_buf_off(c->P, 5, 0);
+      cuda_check(cudaMalloc(&c->p2p_region, c->p2p_bytes), "p2p region");
+      cuda_check(cudaMemset(c->p2p_region, 0, c->p2p_bytes), "p2p region");
+    }
+    cudaIpcMemHandle_t h;
+    cuda_check(cudaIpcGetMemHandle(&h, c->p2p_region), "cudaIpcGetMemHandle");
+    std::memcpy(out, &h, sizeof h);
+  });
+}
+
+// collective in the sense that every rank must call it before any step;
+// handles[q] is rank q's cbx_slab_p2p_handle
+CBX_API cbx_status cbx_slab_p2p_init(cbx_ctx* c, const void* handles, long nbytes) {
+  return guarded(c, [&] {
+    cudaSetDevice(c->device);
+    if (!c->p2p_region) raise(CBX_LOGIC, "cbx_slab_p2p_init: call cbx_slab_p2p_handle first");
+    if (c->p2p) raise(CBX_LOGIC, "cbx_slab_p2p_init: already initialised");
+    const int n = c->nranks;
+    if (n > kMaxP2PRanks) raise(CBX_INVALID_ARGUMENT, "cbx_slab_p2p_init: more than 8 ranks");
+    if (nbytes < (long)(n * sizeof(cudaIpcMemHandle_t)))
+      raise(CBX_INVALID_ARGUMENT, "cbx_slab_p2p_init: need one 64-byte handle per rank");
+    std::vector<unsigned char*> base(n);
+    for (int q = 0; q < n; ++q) {
+      if (q == c->rank) {
+        base[q] = c->p2p_region;
+        continue;
+      }
+      cudaIpcMemHandle_t h;
+      std::memcpy(&h, static_cast<const unsigned char*>(handles) + q * sizeof h, sizeof h);
+      void* p = nullptr;
+      cuda_check(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess),
+                 "cudaIpcOpenMemHandle (ranks must share a node with peer access)");
+      c->p2p_opened.push_back(p);
+      base[q] = static_cast<unsigned char*>(p);
+    }
+    P2PLinks& L = c->links;
+    L = P2PLinks{};
+    const int lo = (c->rank + n - 1) % n, hi = (c->rank + 1) % n;
+    auto flag = [&](unsigned char* b, int kind, int from) {
+      return reinterpret_cast<unsigned long long*>(b + kFlagOff) + 2 * kind + from;
+    };
+    for (int k = 0; k < 5; ++k) {
+      L.msg[k] = slab_msg_bytes(c->P, k);
+      L.plane_bytes[k] = k == 0 ? 0 : slab_plane_bytes(c->P, k);
+      L.dst[k][0] = base[lo] + p2p_buf_off(c->P, k, 1);  // arrives "from above" below me
+      L.dst[k][1] = base[hi] + p2p_buf_off(c->P, k, 0);  // arrives "from below" above me
+      L.flag_dst[k][0] = flag(base[lo], k, 1);
+      L.flag_dst[k][1] = flag(base[hi], k, 0);
+      for (int f = 0; f < 2; ++f) {
+        L.src[k][f] = c->p2p_region + p2p_buf_off(c->P, k, f);
+        L.flag_src[k][f] = flag(c->p2p_region, k, f);
+      }
+    }
+    for (int q = 0; q < n; ++q) {
+      L.red_dst[q] = reinterpret_cast<double*>(base[q] + kRedOff);
+      L.red_flag_dst[q] = reinterpret_cast<unsigned long long*>(base[q] + kRedFlagOff);
+    }
+    L.red_src = reinterpret_cast<const double*>(c->p2p_region + kRedOff);
+    L.red_flag_src = reinterpret_cast<const unsigned long long*>(c->p2p_region + kRedFlagOff);
+    L.epoch = c->alloc<unsigned long long>(6);
+    L.done = c->alloc<unsigned>(6);
+    cudaMemset(L.epoch, 0, 6 * sizeof(unsigned long long));
+    cudaMemset(L.done, 0, 6 * sizeof(unsigned));
+    L.rank = c->rank;
+    L.nranks = n;
+    cuda_check(cudaDeviceSynchronize(), "p2p init");
+    c->p2p = true;
     drop_graph(c);
   });
 }

@@ -187,7 +187,31 @@ int pair_partials(const KP& P, int mode);
 void launch_uf_refresh(const KP& P, cudaStream_t s);
 long long slab_buffer_bytes(const KP& P, int kind);
 constexpr long long kMsgRecords = 8192;  // clash / migrant records per in-graph message
+
+// peer-memory links of one slab rank (P2P transport).  Exchange kinds 0-4;
+// index 5 of epoch/done is the StepState reduction.  [k][0] is the packet
+// toward / from the rank below, [k][1] toward / from the rank above.
+struct P2PLinks {
+  unsigned char* dst[5][2];               // neighbours' receive buffers for my packets
+  const unsigned char* src[5][2];         // my receive buffers
+  unsigned long long* flag_dst[5][2];     // neighbours' flags raised after my packets
+  const unsigned long long* flag_src[5][2];
+  unsigned long long* epoch;              // [6] exchanges completed (this rank)
+  unsigned* done;                         // [6] block arrival counters of k_p2p_send
+  long long msg[5], plane_bytes[5];
+  double* red_dst[8];                     // every rank's reduction slots [8][4]
+  unsigned long long* red_flag_dst[8];    // every rank's reduction flags [8]
+  const double* red_src;
+  const unsigned long long* red_flag_src;
+  int rank, nranks;
+};
+constexpr int kMaxP2PRanks = 8;
+void launch_p2p_exchange(const KP& P, const P2PLinks& L, int kind, long long gs_lo,
+                         long long gs_hi, int* rem_base, cudaStream_t s);
+void launch_p2p_reduce(const KP& P, const P2PLinks& L, int energies, int kinetic,
+                       cudaStream_t s);
 long long slab_msg_bytes(const KP& P, int kind);
+long long slab_plane_bytes(const KP& P, int kind);
 void launch_slab_red_in(const KP& P, double* red, cudaStream_t s);
 void launch_slab_red_out(const KP& P, const double* red, int energies, int kinetic, cudaStream_t s);
 void launch_pack(const KP& P, int kind, int dir, unsigned char* buf, long long cap,

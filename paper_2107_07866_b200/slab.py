@@ -103,6 +103,45 @@ class SlabRank(DeviceStore):
         b = C.create_string_buffer(uid, 128)
         self._check(self.lib.cbx_slab_comm_init(self.h, b, 128))
 
+    def p2p_handle(self) -> bytes:
+        """this rank's receive region as a 64-byte CUDA IPC handle"""
+        b = C.create_string_buffer(64)
+        self._check(self.lib.cbx_slab_p2p_handle(self.h, b, 64))
+        return b.raw
+
+    def init_p2p(self, handles):
+        """handles: every rank's p2p_handle, in rank order"""
+        blob = b"".join(handles)
+        b = C.create_string_buffer(blob, len(blob))
+        self._check(self.lib.cbx_slab_p2p_init(self.h, b, len(blob)))
+
+    def connect(self, transport: str = "p2p", group=None):
+        """set up the in-graph exchange with the other ranks of a
+        torch.distributed job (one rank per process and GPU); with one rank
+        the slab exchanges with itself"""
+        world = 1
+        if self.nranks > 1:
+            import torch.distributed as dist
+            world = dist.get_world_size(group)
+            if world != self.nranks:
+                raise ValueError("slab nranks does not match the process group")
+        if transport == "p2p":
+            h = [self.p2p_handle()]
+            if world > 1:
+                import torch.distributed as dist
+                allh = [None] * world
+                dist.all_gather_object(allh, h[0], group=group)
+                h = allh
+            self.init_p2p(h)
+        elif transport == "nccl":
+            uid = [SlabRank.nccl_unique_id() if self.rank == 0 else None]
+            if world > 1:
+                import torch.distributed as dist
+                dist.broadcast_object_list(uid, src=0, group=group)
+            self.init_comm(uid[0])
+        else:
+            raise ValueError(f"unknown transport {transport!r}")
+
     def bench_steps(self, dt: float, n: int, flush_mb: float = 0.0):
         out = (C.c_double * 8)()
         self._check(self.lib.cbx_bench_steps(self.h, dt, n, flush_mb, out))

@@ -80,3 +80,33 @@ def build_device_state(w: Workload, potential, device: int = 0, stencil: str = "
     dev.eval_forces()
     dev.measure()
     return dev, n
+
+
+def build_slab_state(w: Workload, potential, rank: int, nranks: int, device: int = 0,
+                     stencil: str = "newton3", transport: str = "p2p"):
+    """Rank `rank` of a weak-scaled z-slab run: the global box stacks `nranks`
+    copies of the workload's cells along z (cells[2] planes per rank).  The
+    slab holds exactly its planes of the single-box initial state of that
+    global box (same lattice RNG stream and displacement rows).  The ranks
+    connect through torch.distributed (P2P handles or the NCCL id); forces
+    and the kinetic energy are evaluated collectively."""
+    from .engine import SimConfig, make_box
+    from .slab import SlabRank
+    bx, by, bz = w.cells
+    cfg = SimConfig(box_x=bx, box_y=by, box_z=bz * nranks, temperature=w.temperature,
+                    seed=w.seed)
+    gbox, _ = make_box(cfg, potential)
+    r = SlabRank(gbox, potential, rank, nranks, device=device, stencil=stencil)
+    n = r.init_bcc(w.temperature, w.seed, potential.atomic_number)
+    if w.displacement > 0.0:
+        per_plane = 2 * bx * by
+        z0 = r.info[2]
+        d = displacements(w, per_plane * bz * nranks)[z0 * per_plane:(z0 + r.info[3]) * per_plane]
+        s = r.download()
+        m = s.valid.astype(bool) & ~s.ghost.astype(bool)
+        s.pos[m] += d
+        r.upload(s)
+    r.connect(transport)
+    r.eval_forces()
+    r.measure()
+    return r, n

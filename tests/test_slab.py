@@ -266,13 +266,14 @@ def test_slab_init_bcc_matches_single_box(cuda, tables, n):
     assert np.array_equal(a.tag[m], b.tag[m])
 
 
-def native_rank(ref, path):
-    """one slab rank that owns the whole box, exchanging with itself through
-    NCCL inside its step graph (the n == 1 case of the multi-GPU path)"""
+def native_rank(ref, path, transport):
+    """one slab rank that owns the whole box, exchanging with itself inside
+    its step graph (the n == 1 case of the multi-GPU path): NCCL self
+    send/recv, or the peer-memory kernels mapped onto the rank itself"""
     from paper_2107_07866_b200 import EamPotential
     dims, a0, g = ref.box
     r = S.SlabRank((*dims, a0, g), EamPotential.load(path), 0, 1)
-    r.init_comm(S.SlabRank.nccl_unique_id())
+    r.connect(transport)
     r.upload_global(ref.store())
     r.set_state(ref.state())
     return r
@@ -291,12 +292,14 @@ def test_slab_local_exchange_single_rank(cuda, tables):
 
 
 @pytest.mark.gpu
-def test_slab_nccl_graph_eval_and_trajectory(cuda, tables):
-    """NCCL exchanges captured in the step graph (self send/recv): forces,
-    energies and a 60-step trajectory equal the single-box oracle"""
+@pytest.mark.parametrize("transport", ["p2p", "nccl"])
+def test_slab_graph_eval_and_trajectory(cuda, tables, transport):
+    """exchanges captured in the step graph (NCCL self send/recv, or the
+    flag-synchronised peer-memory kernels): forces, energies and a 60-step
+    trajectory equal the single-box oracle"""
     from oracle import oracle
     ref = oracle.Sim(tables["baseline"], box=(8, 7, 9), temperature=600.0, seed=12345)
-    r = native_rank(ref, tables["baseline"])
+    r = native_rank(ref, tables["baseline"], transport)
     e_emb, e_pair = r.eval_forces()
     r.measure()
     sr = ref.state()
@@ -319,7 +322,8 @@ def test_slab_nccl_graph_eval_and_trajectory(cuda, tables):
 
 
 @pytest.mark.gpu
-def test_slab_nccl_graph_cascade(cuda, tables):
+@pytest.mark.parametrize("transport", ["p2p", "nccl"])
+def test_slab_graph_cascade(cuda, tables, transport):
     """cascade with adaptive dt through the NCCL step graph: clash records,
     defect counts and the global-max-speed time step match the oracle"""
     from oracle import oracle
@@ -327,7 +331,7 @@ def test_slab_nccl_graph_cascade(cuda, tables):
                      pka_energy_kev=1.0, pka_site=(5, 5, 3))
     ref.step(1e-3, 5)
     ref.inject_pka()
-    r = native_rank(ref, tables["baseline"])
+    r = native_rank(ref, tables["baseline"], transport)
     r.eval_forces()
     r.measure()
     dom = S.SlabDomain([r], None)
