@@ -241,9 +241,11 @@ void seq_density(cbx_ctx* c) {
   if (c->mode != CBX_STENCIL_FULL)
     cudaMemsetAsync(c->P.rho, 0, c->S * sizeof(double), c->stream);
   launch_clash_zero(c->P, 0, c->stream);
-  launch_density(c->P, c->mode, c->stream);
-  launch_clash_density(c->P, c->stream);
-  c->launches += 3;
+  if (!launch_density(c->P, c->mode, c->stream)) {
+    launch_clash_density(c->P, c->stream);
+    c->launches += 1;
+  }
+  c->launches += 2;
   c->mask_valid = c->mode != CBX_STENCIL_REFERENCE && c->P.pmask != nullptr;
 }
 void seq_embed(cbx_ctx* c) {
@@ -258,9 +260,11 @@ void seq_force(cbx_ctx* c) {
   KP q = c->P;
   q.use_mask = c->mask_valid ? 1 : 0;
   cudaMemsetAsync(c->P.part_pair, 0, c->P.n_part * sizeof(double), c->stream);
-  launch_force(q, c->mode, c->stream);
-  launch_clash_force(c->P, c->stream);
-  c->launches += 3;
+  if (!launch_force(q, c->mode, c->stream)) {
+    launch_clash_force(c->P, c->stream);
+    c->launches += 1;
+  }
+  c->launches += 2;
 }
 // ---- z-slab ranks: exchanges and reductions inside the step (NCCL) -------
 // Both halves of one exchange go out in one NCCL group: my "down" packet to
@@ -346,8 +350,7 @@ void seq_slab_step(cbx_ctx* c) {
   seq_force(c);
   slab_exchange(c, 4);  // force partials (reverse)
   ev_mark(c, 4);
-  launch_kick2(c->P, 1, c->stream);
-  launch_finalize(c->P, 1, 1, c->stream);
+  launch_kick2(c->P, 1, 1, 1, c->stream);
   c->launches += 3;
   slab_reduce(c, true, true);
   ev_mark(c, 5);
@@ -395,8 +398,7 @@ void seq_step(cbx_ctx* c) {
   ev_mark(c, 3);
   seq_force(c);
   ev_mark(c, 4);
-  launch_kick2(c->P, 1, c->stream);
-  launch_finalize(c->P, 1, 1, c->stream);
+  launch_kick2(c->P, 1, 1, 1, c->stream);
   c->launches += 3;
   ev_mark(c, 5);
 }
@@ -1079,7 +1081,7 @@ static cbx_status create_impl(const cbx_box* box, const cbx_potential* pot,
     cudaMemset(P.tag, 0, S * sizeof(unsigned long long));
     cudaMemset(P.head, 0xff, S * sizeof(int));
     launch_uf_refresh(P, c->stream);
-    P.n_pair_part = P.n_part;
+    P.n_pair_part = pair_partials(P, 0);
     sync_kp(c.get());
     c->hst = DevStatus{};
     c->hst.dt_next = 1e-3;
@@ -1324,8 +1326,7 @@ CBX_API cbx_status cbx_refresh_forces(cbx_ctx* c) {
 CBX_API cbx_status cbx_measure(cbx_ctx* c) {
   return guarded(c, [&] {
     cudaSetDevice(c->device);
-    launch_kick2(c->P, 0, c->stream);
-    launch_finalize(c->P, 0, 0, c->stream);
+    launch_kick2(c->P, 0, 0, 0, c->stream);
     c->launches += 3;
     if (has_transport(c)) slab_reduce(c, false, true);
     sync_status(c);
@@ -1581,8 +1582,7 @@ CBX_API cbx_status cbx_slab_phase(cbx_ctx* c, int phase, double dt) {
         seq_force(c);
         break;
       case 5:
-        launch_kick2(c->P, 1, c->stream);
-        launch_finalize(c->P, 1, 1, c->stream);
+        launch_kick2(c->P, 1, 1, 1, c->stream);
         c->launches += 3;
         break;
       case 6:
@@ -1590,8 +1590,7 @@ CBX_API cbx_status cbx_slab_phase(cbx_ctx* c, int phase, double dt) {
         c->launches += 1;
         break;
       case 7:  // measure only (kinetic energy, max speed)
-        launch_kick2(c->P, 0, c->stream);
-        launch_finalize(c->P, 0, 0, c->stream);
+        launch_kick2(c->P, 0, 0, 0, c->stream);
         c->launches += 3;
         break;
       default:

@@ -112,6 +112,7 @@ struct KP {
   Tab dens, zr, emb;
   double cutoff, cut2, mass;
   double *part_emb, *part_pair, *part_ke, *part_vmax;
+
   int n_part;
   int count_pairs;
   DevStatus* st;
@@ -166,17 +167,18 @@ __device__ __forceinline__ void set_error(DevStatus* st, int code) { atomicCAS(&
 #endif
 
 // device entry points (launch wrappers), implemented in the .cu files
-void launch_density(const KP& P, int mode, cudaStream_t s);
+bool launch_density(const KP& P, int mode, cudaStream_t s);  // true: clash pass fused
 void launch_clash_density(const KP& P, cudaStream_t s);
 void launch_embed(const KP& P, cudaStream_t s);
-void launch_force(const KP& P, int mode, cudaStream_t s);
+bool launch_force(const KP& P, int mode, cudaStream_t s);
 void launch_clash_force(const KP& P, cudaStream_t s);
 void launch_kick_drift(const KP& P, int move, cudaStream_t s);
 void launch_clash_zero(const KP& P, int what, cudaStream_t s);
 void launch_rehash(const KP& P, cudaStream_t s);
 void launch_ghost_fill(const KP& P, cudaStream_t s);
 void launch_clash_images(const KP& P, cudaStream_t s);
-void launch_kick2(const KP& P, int kick, cudaStream_t s);
+// second half kick; stepping > -2 also runs the finalize (last block)
+void launch_kick2(const KP& P, int kick, int stepping, int energies, cudaStream_t s);
 void launch_finalize(const KP& P, int stepping, int energies, cudaStream_t s);
 void launch_count_defects(const KP& P, unsigned long long* out, cudaStream_t s);
 void upload_offsets(const int* half_dev[2], const int half_n[2], const int* full_dev[2],
@@ -222,5 +224,7 @@ void launch_remote_df(const KP& P, cudaStream_t s);
 bool upload_tile_offsets(const int4* half[2], const int half_n[2], const int4* full[2],
                          const int full_n[2], cudaStream_t s);
 int embed_blocks(const KP& P);
+int embed_grid(const KP& P);  // energy partials of the embed pass
+int kick_grid(const KP& P);   // KE partials of the kick2 pass
 
 }  // namespace cbx

@@ -19,6 +19,7 @@
 // the reference's orientation and operation order (no FMA), so in-cutoff
 // decisions are bit-identical; the pair arithmetic after the cutoff test is
 // ordinary fp64 (within 1e-10 of the reference, tests/test_gpu_parity.py).
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
@@ -284,40 +285,10 @@ __global__ void __launch_bounds__(256) k_force(KP P) {
 // ---------------------------------------------------------- embedding pass
 // interior sites: dF = F'(rho), E += F(rho) (embed_slots); ghost sites take
 // F'(rho of their source) -- the refresh_ghosts copy, computed in place
-__global__ void __launch_bounds__(256) k_embed(KP P) {
-  __shared__ double sh[8];
-  double e = 0.0;
-  const long long d = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (!P.st->err && !P.st->n_ovl && d < P.S) {
-    const double4 p = P.pdf[d];
-    if (p.x < kVacantTest) {
-      const int t = P.tgt[d];
-      const double r = P.rho[t];
-      double v, dv;
-      seg_eval(P.emb, r, v, dv);
-      // owned here: interior site (a z-halo site of a slab rank also has
-      // t == d, but its rho is a partial and its dF comes from the owner)
-      bool owned = t == d;
-      if (owned && P.G.slab) {
-        const long cz = site_cz(ref_of_dev(d, P.G.NC), P.G);
-        owned = cz >= P.G.g && cz < P.G.g + P.G.bz;
-      }
-      if (owned) {
-        if (r < P.emb.x0 || r > P.emb.xl) atomicAdd(&P.st->rho_clamp, 1ull);
-        e = v;
-      }
-      P.pdf[d].w = dv;
-    }
-  }
-  const double s = block_sum<256>(e, sh);
-  if (threadIdx.x == 0) P.part_emb[blockIdx.x] = s;
-}
-int embed_blocks(const KP& P) { return (int)((P.S + 255) / 256); }
-
-__global__ void k_clash_embed(KP P) {
+__device__ void clash_embed_body(const KP& P, int blk, int nblk) {
   if (P.st->err || P.st->n_ovl) return;
   const int n = P.st->n_clash;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+  for (int i = blk * blockDim.x + threadIdx.x; i < n; i += nblk * blockDim.x) {
     const int s = P.cl.gf[i] ? P.cl.src[i] : i;
     if (s < 0) continue;  // remote source: dF arrives with the dF halo
     const double r = P.cl.rho[s];
@@ -333,20 +304,66 @@ __global__ void k_clash_embed(KP P) {
   }
 }
 
+// blocks [0, nsb): all slots, grid-stride, one energy partial per block;
+// blocks [nsb, grid): the clash records (fused k_clash_embed)
+__global__ void __launch_bounds__(256) k_embed(KP P, int nsb) {
+  if (blockIdx.x >= nsb) {
+    clash_embed_body(P, blockIdx.x - nsb, gridDim.x - nsb);
+    return;
+  }
+  __shared__ double sh[8];
+  double e = 0.0;
+  const bool ok = !P.st->err && !P.st->n_ovl;
+  for (long long d = (long long)blockIdx.x * blockDim.x + threadIdx.x; ok && d < P.S;
+       d += (long long)nsb * blockDim.x) {
+    const double4 p = P.pdf[d];
+    if (p.x >= kVacantTest) continue;
+    const int t = P.tgt[d];
+    const double r = P.rho[t];
+    double v, dv;
+    seg_eval(P.emb, r, v, dv);
+    // owned here: interior site (a z-halo site of a slab rank also has
+    // t == d, but its rho is a partial and its dF comes from the owner)
+    bool owned = t == d;
+    if (owned && P.G.slab) {
+      const long cz = site_cz(ref_of_dev(d, P.G.NC), P.G);
+      owned = cz >= P.G.g && cz < P.G.g + P.G.bz;
+    }
+    if (owned) {
+      if (r < P.emb.x0 || r > P.emb.xl) atomicAdd(&P.st->rho_clamp, 1ull);
+      e += v;
+    }
+    P.pdf[d].w = dv;
+  }
+  const double s = block_sum<256>(e, sh);
+  if (threadIdx.x == 0) P.part_emb[blockIdx.x] = s;
+}
+int embed_blocks(const KP& P) { return (int)((P.S + 255) / 256); }
+int embed_grid(const KP& P) {
+  int sms = 148, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return std::max(1, std::min(embed_blocks(P), 8 * sms));
+}
+
+__global__ void k_clash_embed(KP P) { clash_embed_body(P, blockIdx.x, gridDim.x); }
+
 // ------------------------------------------------------------ clash pairs
 // forces.cpp:185-225, one warp per interior clash record; partner classes:
 // own slot, later bucket mates, slot atoms at id + full offsets (incl.
 // ghosts -> owner), interior buckets with nid > id (symmetric), ghost
 // buckets (one-sided, half energy).  All partner updates are RED adds.
+// blk / nblk: this block's index among the blocks sweeping the records
+// (the standalone kernel, or the extra blocks of a fused pass)
 template <int MODE>  // 0 density, 1 force
-__global__ void __launch_bounds__(256) k_clash(KP P) {
+__device__ void clash_body(const KP& P, int blk, int nblk) {
   if (P.st->err) return;
   if (MODE == 1 && P.st->n_ovl) return;
   const int n = P.st->n_clash;
   if (n == 0) return;
   const int lane = threadIdx.x & 31;
-  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int nw = (gridDim.x * blockDim.x) >> 5;
+  const int gw = (blk * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (nblk * blockDim.x) >> 5;
   const long long S = P.S;
   for (int i = gw; i < n; i += nw) {
     if (P.cl.gf[i]) continue;
@@ -437,6 +454,12 @@ __global__ void __launch_bounds__(256) k_clash(KP P) {
     }
   }
 }
+template <int MODE>
+__global__ void __launch_bounds__(256) k_clash(KP P) {
+  clash_body<MODE>(P, blockIdx.x, gridDim.x);
+}
+template __device__ void clash_body<0>(const KP&, int, int);
+template __device__ void clash_body<1>(const KP&, int, int);
 
 #include "stencil_fast.cuh"
 #include "stencil_tile.cuh"
@@ -467,22 +490,33 @@ bool upload_tile_offsets(const int4* half[2], const int half_n[2], const int4* f
 
 // ------------------------------------------------------------- launchers
 // mode: 0 fast half list (Newton-3), 1 fast full list, 2 reference-literal half list
-void launch_density(const KP& P, int mode, cudaStream_t s) {
+// return true when the clash-record pass ran inside the same kernel
+bool launch_density(const KP& P, int mode, cudaStream_t s) {
   if (mode == 2) k_density<false><<<eam_blocks(P), 256, 0, s>>>(P);
   else if (P.use_tile) launch_density_tile(P, mode, s);
-  else launch_density_fast(P, mode, fast_grid(P, false, mode), s);
+  else return launch_density_fast(P, mode, fast_grid(P, false, mode), s);
+  return false;
 }
-void launch_force(const KP& P, int mode, cudaStream_t s) {
+bool launch_force(const KP& P, int mode, cudaStream_t s) {
   if (mode == 2) k_force<false><<<eam_blocks(P), 256, 0, s>>>(P);
   else if (P.use_tile && P.use_mask) launch_force_tile(P, mode, tile_grid(P, true, mode), s);
-  else launch_force_fast(P, mode, fast_grid(P, true, mode), s);
+  else return launch_force_fast(P, mode, fast_grid(P, true, mode), s);
+  return false;
 }
+// partials any force kernel may write (per warp / per block); the finalize
+// sums this many (the rest of part_pair is zeroed before every force pass)
 int pair_partials(const KP& P, int mode) {
-  return mode == 2 ? eam_blocks(P) : 4 * fast_grid(P, true, mode);
+  (void)mode;
+  int n = eam_blocks(P);
+  for (int m = 0; m < 2; ++m) {
+    n = std::max(n, 4 * fast_grid(P, true, m));
+    n = std::max(n, 8 * tile_grid(P, true, m));  // 256-thread blocks
+  }
+  return std::min(n, P.n_part);
 }
 void launch_embed(const KP& P, cudaStream_t s) {
-  k_embed<<<embed_blocks(P), 256, 0, s>>>(P);
-  k_clash_embed<<<16, 256, 0, s>>>(P);
+  const int nsb = embed_grid(P);
+  k_embed<<<nsb + 16, 256, 0, s>>>(P, nsb);
 }
 void launch_clash_density(const KP& P, cudaStream_t s) { k_clash<0><<<16, 256, 0, s>>>(P); }
 void launch_clash_force(const KP& P, cudaStream_t s) { k_clash<1><<<16, 256, 0, s>>>(P); }

@@ -15,7 +15,9 @@
 // bit-identical to the reference.  Pass 2's sequential semantics (the first
 // re-placed record claims a free slot) are reproduced by sorting all movers
 // by (new site, old site, class, order) -- see k_rehash.
+#include <algorithm>
 #include <climits>
+#include <cstdlib>
 
 #include "cbx_device.cuh"
 
@@ -34,8 +36,14 @@ __device__ __forceinline__ bool site_is_ghost(long long id, const Geo& G) {
 }
 
 // -------------------------------------------------- kick, drift, wrap, evict
-__global__ void __launch_bounds__(256) k_kick_drift(KP P, int move) {
+__device__ void clash_kick_drift_body(const KP& P, int move, int blk, int nblk);
+
+__global__ void __launch_bounds__(256) k_kick_drift(KP P, int move, int nsb) {
   if (P.st->err) return;
+  if (blockIdx.x >= nsb) {  // the clash records (fused k_clash_kick_drift)
+    clash_kick_drift_body(P, move, blockIdx.x - nsb, gridDim.x - nsb);
+    return;
+  }
   int par;
   long long d;
   if (!map_site(P, par, d)) return;
@@ -98,10 +106,10 @@ __global__ void __launch_bounds__(256) k_kick_drift(KP P, int move) {
   }
 }
 
-__global__ void k_clash_kick_drift(KP P, int move) {
+__device__ void clash_kick_drift_body(const KP& P, int move, int blk, int nblk) {
   if (P.st->err) return;
   const int n = P.st->n_clash;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+  for (int i = blk * blockDim.x + threadIdx.x; i < n; i += nblk * blockDim.x) {
     if (P.cl.gf[i]) continue;
     double px = P.cl.px[i], py = P.cl.py[i], pz = P.cl.pz[i];
     if (move) {
@@ -154,6 +162,9 @@ __global__ void k_clash_kick_drift(KP P, int move) {
       P.cl.gf[i] = 3;  // gone
     }
   }
+}
+__global__ void k_clash_kick_drift(KP P, int move) {
+  clash_kick_drift_body(P, move, blockIdx.x, gridDim.x);
 }
 
 // ---------------------------------------------------- single-block helpers
@@ -569,7 +580,37 @@ __global__ void k_clash_zero(KP P, int what) {
 }
 
 // ---------------------------------------------- second half kick + measure
-__global__ void __launch_bounds__(256) k_kick2(KP P, int kick) {
+// Blocks [0, nsb) sweep the interior sites (grid-stride, one KE / v_max
+// partial per block), blocks [nsb, grid) the clash records; the last block
+// to arrive sums every partial into StepState (finalize_body), so one
+// kernel ends the step.
+__device__ void clash_kick2_body(const KP& P, int kick, int blk, int nblk) {
+  if (P.st->err || P.st->n_ovl) return;
+  const int n = P.st->n_clash;
+  for (int i = blk * blockDim.x + threadIdx.x; i < n; i += nblk * blockDim.x) {
+    if (P.cl.gf[i]) {
+      P.cl.v2[i] = 0.0;
+      continue;
+    }
+    double vx = P.cl.vx[i], vy = P.cl.vy[i], vz = P.cl.vz[i];
+    if (kick) {
+      const double hk = half_kick(P, P.st->dt_next);
+      vx = xadd(vx, xmul(P.cl.fx[i], hk));
+      vy = xadd(vy, xmul(P.cl.fy[i], hk));
+      vz = xadd(vz, xmul(P.cl.fz[i], hk));
+      P.cl.vx[i] = vx;
+      P.cl.vy[i] = vy;
+      P.cl.vz[i] = vz;
+    }
+    P.cl.v2[i] = exact_r2(vx, vy, vz);
+  }
+}
+
+__global__ void __launch_bounds__(256) k_kick2(KP P, int kick, int nsb) {
+  if (blockIdx.x >= nsb) {  // the clash records (fused k_clash_kick2)
+    clash_kick2_body(P, kick, blockIdx.x - nsb, gridDim.x - nsb);
+    return;
+  }
   __shared__ double sh[8];
   double v2 = 0.0;
   int par;
@@ -599,79 +640,92 @@ __global__ void __launch_bounds__(256) k_kick2(KP P, int kick) {
 }
 
 __global__ void k_clash_kick2(KP P, int kick) {
-  if (P.st->err || P.st->n_ovl) return;
-  const int n = P.st->n_clash;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    if (P.cl.gf[i]) {
-      P.cl.v2[i] = 0.0;
-      continue;
-    }
-    double vx = P.cl.vx[i], vy = P.cl.vy[i], vz = P.cl.vz[i];
-    if (kick) {
-      const double hk = half_kick(P, P.st->dt_next);
-      vx = xadd(vx, xmul(P.cl.fx[i], hk));
-      vy = xadd(vy, xmul(P.cl.fy[i], hk));
-      vz = xadd(vz, xmul(P.cl.fz[i], hk));
-      P.cl.vx[i] = vx;
-      P.cl.vy[i] = vy;
-      P.cl.vz[i] = vz;
-    }
-    P.cl.v2[i] = exact_r2(vx, vy, vz);
-  }
+  clash_kick2_body(P, kick, blockIdx.x, gridDim.x);
 }
 
 // ------------------------------------------------------------- finalize
 // deterministic sums of the per-block / per-record partials into StepState
-__global__ void __launch_bounds__(1024) k_finalize(KP P, int stepping, int energies,
-                                                   int n_pairp, int n_emb) {
-  const int n_eam = eam_blocks_dev(P);
-  __shared__ double sh[32];
+// (fixed per-thread order, four independent accumulators for load
+// parallelism, then a fixed block tree)
+template <int NT>
+__device__ void finalize_body(const KP& P, int stepping, int energies, const double* pe, int n_emb,
+                              const double* pp, int n_pairp, int n_ke) {
+  __shared__ double sh[4][32];
   DevStatus* st = P.st;
   if (st->err || st->n_ovl) return;
   const int nc = st->n_clash;
+  // one pass over every partial array, all loads of a round independent
+  double ea[4] = {0, 0, 0, 0}, ep[4] = {0, 0, 0, 0}, ek[4] = {0, 0, 0, 0},
+         em[4] = {0, 0, 0, 0};
+  const int ne = energies ? n_emb : 0, np = energies ? n_pairp : 0;
+  const int nk = stepping >= 0 ? n_ke : 0;
+  const int n = max(max(ne, np), nk);
+  for (int i0 = threadIdx.x; i0 < n; i0 += 4 * NT) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = i0 + u * NT;
+      if (i < ne) ea[u] += pe[i];
+      if (i < np) ep[u] += pp[i];
+      if (i < nk) {
+        ek[u] += P.part_ke[i];
+        em[u] = fmax(em[u], P.part_vmax[i]);
+      }
+    }
+  }
+  for (int i = threadIdx.x; i < nc; i += NT) {
+    if (energies) {
+      ea[0] += P.cl.e_emb[i];
+      ep[0] += P.cl.e_pair[i];
+    }
+    if (stepping >= 0) {
+      ek[0] += P.cl.v2[i];
+      em[0] = fmax(em[0], P.cl.v2[i]);
+    }
+  }
+  double v[4] = {(ea[0] + ea[1]) + (ea[2] + ea[3]), (ep[0] + ep[1]) + (ep[2] + ep[3]),
+                 (ek[0] + ek[1]) + (ek[2] + ek[3]), fmax(fmax(em[0], em[1]), fmax(em[2], em[3]))};
+  for (int o = 16; o > 0; o >>= 1) {
+    v[0] += __shfl_xor_sync(0xffffffffu, v[0], o);
+    v[1] += __shfl_xor_sync(0xffffffffu, v[1], o);
+    v[2] += __shfl_xor_sync(0xffffffffu, v[2], o);
+    v[3] = fmax(v[3], __shfl_xor_sync(0xffffffffu, v[3], o));
+  }
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0)
+    for (int q = 0; q < 4; ++q) sh[q][w] = v[q];
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  double r[4] = {0, 0, 0, 0};
+  for (int i = 0; i < NT / 32; ++i) {
+    r[0] += sh[0][i];
+    r[1] += sh[1][i];
+    r[2] += sh[2][i];
+    r[3] = fmax(r[3], sh[3][i]);
+  }
   if (energies) {
-    double a = 0.0, b = 0.0;
-    for (int i = threadIdx.x; i < n_emb; i += blockDim.x) a += P.part_emb[i];
-    for (int i = threadIdx.x; i < n_pairp; i += blockDim.x) b += P.part_pair[i];
-    for (int i = threadIdx.x; i < nc; i += blockDim.x) {
-      a += P.cl.e_emb[i];
-      b += P.cl.e_pair[i];
-    }
-    const double ea = block_sum<1024>(a, sh);
-    const double eb = block_sum<1024>(b, sh);
-    if (threadIdx.x == 0) {
-      st->embedding = ea;
-      st->pair = eb;
-    }
+    st->embedding = r[0];
+    st->pair = r[1];
   }
   if (stepping >= 0) {  // 1: completed a step, 0: measure only
-    double a = 0.0, m = 0.0;
-    for (int i = threadIdx.x; i < n_eam; i += blockDim.x) {
-      a += P.part_ke[i];
-      m = fmax(m, P.part_vmax[i]);
+    st->kinetic = xmul(xmul(xmul(0.5, P.mass), r[2]), P.mv2);  // sim.cpp:269
+    st->max_speed = sqrt(r[3]);
+    if (stepping == 1) {
+      const double dt = st->dt_next;
+      st->step += 1;
+      st->t = xadd(st->t, dt);
+      st->dt = dt;
     }
-    for (int i = threadIdx.x; i < nc; i += blockDim.x) {
-      a += P.cl.v2[i];
-      m = fmax(m, P.cl.v2[i]);
-    }
-    const double sv = block_sum<1024>(a, sh);
-    const double mv = block_max<1024>(m, sh);
-    if (threadIdx.x == 0) {
-      st->kinetic = xmul(xmul(xmul(0.5, P.mass), sv), P.mv2);  // sim.cpp:269
-      st->max_speed = sqrt(mv);
-      if (stepping == 1) {
-        const double dt = st->dt_next;
-        st->step += 1;
-        st->t = xadd(st->t, dt);
-        st->dt = dt;
-      }
-      if (st->adaptive) {  // adaptive_dt, sim.cpp:94-98
-        double dt = st->dt_max;
-        if (st->max_speed > 0.0) dt = fmin(dt, xdiv(st->max_disp, st->max_speed));
-        st->dt_next = fmax(dt, 1e-7);
-      }
+    if (st->adaptive) {  // adaptive_dt, sim.cpp:94-98
+      double dt = st->dt_max;
+      if (st->max_speed > 0.0) dt = fmin(dt, xdiv(st->max_disp, st->max_speed));
+      st->dt_next = fmax(dt, 1e-7);
     }
   }
+}
+
+__global__ void __launch_bounds__(1024) k_finalize(KP P, int stepping, int energies,
+                                                   int n_pairp, int n_emb, int n_ke) {
+  finalize_body<1024>(P, stepping, energies, P.part_emb, n_emb, P.part_pair, n_pairp, n_ke);
 }
 
 // ---------------------------------------------------------- count_defects
@@ -697,9 +751,10 @@ __global__ void __launch_bounds__(256) k_count_defects(KP P, unsigned long long*
 }
 
 // -------------------------------------------------------------- launchers
+constexpr int kClashBlocks = 8;  // blocks of 256 threads for clash-record sweeps
 void launch_kick_drift(const KP& P, int move, cudaStream_t s) {
-  k_kick_drift<<<eam_blocks(P), 256, 0, s>>>(P, move);
-  k_clash_kick_drift<<<8, 256, 0, s>>>(P, move);
+  const int nsb = eam_blocks(P);
+  k_kick_drift<<<nsb + kClashBlocks, 256, 0, s>>>(P, move, nsb);
 }
 void launch_rehash(const KP& P, cudaStream_t s) { k_rehash<<<1, 1024, 0, s>>>(P); }
 void launch_ghost_fill(const KP& P, cudaStream_t s) {
@@ -709,12 +764,15 @@ void launch_clash_images(const KP& P, cudaStream_t s) { k_clash_images<<<1, 1024
 void launch_clash_zero(const KP& P, int what, cudaStream_t s) {
   k_clash_zero<<<8, 256, 0, s>>>(P, what);
 }
-void launch_kick2(const KP& P, int kick, cudaStream_t s) {
-  k_kick2<<<eam_blocks(P), 256, 0, s>>>(P, kick);
-  k_clash_kick2<<<8, 256, 0, s>>>(P, kick);
+int kick_grid(const KP& P) { return eam_blocks(P); }
+void launch_kick2(const KP& P, int kick, int stepping, int energies, cudaStream_t s) {
+  const int nsb = kick_grid(P);
+  k_kick2<<<nsb + kClashBlocks, 256, 0, s>>>(P, kick, nsb);
+  if (stepping > -2) launch_finalize(P, stepping, energies, s);
 }
 void launch_finalize(const KP& P, int stepping, int energies, cudaStream_t s) {
-  k_finalize<<<1, 1024, 0, s>>>(P, stepping, energies, P.n_pair_part, embed_blocks(P));
+  k_finalize<<<1, 1024, 0, s>>>(P, stepping, energies, P.n_pair_part, embed_grid(P),
+                                kick_grid(P));
 }
 void launch_count_defects(const KP& P, unsigned long long* out, cudaStream_t s) {
   k_count_defects<<<eam_blocks(P), 256, 0, s>>>(P, out);
