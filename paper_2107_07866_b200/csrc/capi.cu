@@ -41,6 +41,8 @@ struct cbx_ctx {
   int n_ghost = 0;
   bool fast_ok = true;
   bool mask_valid = false;
+  bool clash_rho_zero = false;  // the last clash-image pass zeroed the records' rho
+  bool clash_f_zero = false;    // the last embed pass zeroed the records' forces
   bool tile_ok = false;  // every offset within the 2-cell tile halo
   // z-slab decomposition
   int rank = 0, nranks = 1;
@@ -230,17 +232,19 @@ void ev_mark(cbx_ctx* c, int i) {
     cudaEventRecordWithFlags(c->ev[i], c->stream, g_capturing ? cudaEventRecordExternal : 0);
 }
 
-void seq_fill_ghosts(cbx_ctx* c) {
+void seq_fill_ghosts(cbx_ctx* c, bool zero_rho = false) {
   c->mask_valid = false;
   launch_ghost_fill(c->P, c->stream);
-  launch_clash_images(c->P, c->stream);
+  launch_clash_images(c->P, c->stream, zero_rho ? 1 : 0);
+  c->clash_rho_zero = zero_rho;
   c->launches += 2;
 }
 void seq_density(cbx_ctx* c) {
   cudaMemsetAsync(c->P.work, 0, sizeof(int), c->stream);
   if (c->mode != CBX_STENCIL_FULL)
     cudaMemsetAsync(c->P.rho, 0, c->S * sizeof(double), c->stream);
-  launch_clash_zero(c->P, 0, c->stream);
+  if (!c->clash_rho_zero) launch_clash_zero(c->P, 0, c->stream);
+  c->clash_rho_zero = false;
   if (!launch_density(c->P, c->mode, c->stream)) {
     launch_clash_density(c->P, c->stream);
     c->launches += 1;
@@ -250,13 +254,15 @@ void seq_density(cbx_ctx* c) {
 }
 void seq_embed(cbx_ctx* c) {
   launch_embed(c->P, c->stream);
+  c->clash_f_zero = true;
   c->launches += 2;
 }
 void seq_force(cbx_ctx* c) {
   cudaMemsetAsync(c->P.work + 1, 0, sizeof(int), c->stream);
   if (c->mode != CBX_STENCIL_FULL)
     cudaMemsetAsync(c->P.frc, 0, 3 * c->S * sizeof(double), c->stream);
-  launch_clash_zero(c->P, 1, c->stream);
+  if (!c->clash_f_zero) launch_clash_zero(c->P, 1, c->stream);
+  c->clash_f_zero = false;
   KP q = c->P;
   q.use_mask = c->mask_valid ? 1 : 0;
   cudaMemsetAsync(c->P.part_pair, 0, c->P.n_part * sizeof(double), c->stream);
@@ -337,7 +343,8 @@ void seq_slab_step(cbx_ctx* c) {
   memset_field(c, &c->P.st->n_remote);
   slab_exchange(c, 1);  // positions
   ev_mark(c, 1);
-  launch_clash_images(c->P, c->stream);
+  launch_clash_images(c->P, c->stream, 1);
+  c->clash_rho_zero = true;
   c->launches += 1;
   seq_density(c);
   slab_exchange(c, 2);  // density partials (reverse)
@@ -361,7 +368,8 @@ void seq_slab_eval(cbx_ctx* c) {
   memset_field(c, &c->P.st->n_remote);
   slab_exchange(c, 1);
   ev_mark(c, 1);
-  launch_clash_images(c->P, c->stream);
+  launch_clash_images(c->P, c->stream, 1);
+  c->clash_rho_zero = true;
   c->launches += 1;
   seq_density(c);
   slab_exchange(c, 2);
@@ -390,7 +398,7 @@ void seq_step(cbx_ctx* c) {
   launch_kick_drift(c->P, 1, c->stream);
   launch_rehash(c->P, c->stream);
   c->launches += 3;
-  seq_fill_ghosts(c);
+  seq_fill_ghosts(c, true);
   ev_mark(c, 1);
   seq_density(c);
   ev_mark(c, 2);
@@ -1569,7 +1577,8 @@ CBX_API cbx_status cbx_slab_phase(cbx_ctx* c, int phase, double dt) {
         write_status(c);
         break;
       case 2:
-        launch_clash_images(c->P, c->stream);
+        launch_clash_images(c->P, c->stream, 1);
+        c->clash_rho_zero = true;
         c->launches += 1;
         seq_density(c);
         break;

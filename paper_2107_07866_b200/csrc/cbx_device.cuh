@@ -176,7 +176,8 @@ void launch_kick_drift(const KP& P, int move, cudaStream_t s);
 void launch_clash_zero(const KP& P, int what, cudaStream_t s);
 void launch_rehash(const KP& P, cudaStream_t s);
 void launch_ghost_fill(const KP& P, cudaStream_t s);
-void launch_clash_images(const KP& P, cudaStream_t s);
+// zero_rho: also zero the records' density accumulators (density follows)
+void launch_clash_images(const KP& P, cudaStream_t s, int zero_rho = 0);
 // second half kick; stepping > -2 also runs the finalize (last block)
 void launch_kick2(const KP& P, int kick, int stepping, int energies, cudaStream_t s);
 void launch_finalize(const KP& P, int stepping, int energies, cudaStream_t s);

@@ -309,6 +309,15 @@ __device__ void clash_embed_body(const KP& P, int blk, int nblk) {
 __global__ void __launch_bounds__(256) k_embed(KP P, int nsb) {
   if (blockIdx.x >= nsb) {
     clash_embed_body(P, blockIdx.x - nsb, gridDim.x - nsb);
+    // the records' force accumulators for the force pass (clash_zero fused)
+    const int n = P.st->n_clash;
+    for (int i = (blockIdx.x - nsb) * blockDim.x + threadIdx.x; i < n;
+         i += (gridDim.x - nsb) * blockDim.x) {
+      P.cl.fx[i] = 0.0;
+      P.cl.fy[i] = 0.0;
+      P.cl.fz[i] = 0.0;
+      P.cl.e_pair[i] = 0.0;
+    }
     return;
   }
   __shared__ double sh[8];

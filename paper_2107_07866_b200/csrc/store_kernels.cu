@@ -442,7 +442,7 @@ __device__ __forceinline__ int image_count(long long id, const Geo& G) {
   return c;
 }
 
-__global__ void __launch_bounds__(1024) k_clash_images(KP P) {
+__global__ void __launch_bounds__(1024) k_clash_images(KP P, int zero_rho) {
   if (P.st->err) return;
   const int n = P.st->n_clash;
   const int n_rem = P.st->n_remote;
@@ -543,6 +543,7 @@ __global__ void __launch_bounds__(1024) k_clash_images(KP P) {
   for (int p = threadIdx.x; p < total; p += blockDim.x) {
     const int q = X.pl[p];
     copy_record(P.cl2, q, P.cl, p);
+    if (zero_rho) P.cl.rho[p] = 0.0;  // the density pass follows (clash_zero fused)
     const int sq = P.cl2.src[q];
     P.cl.src[p] = P.cl2.gf[q] ? (sq >= 0 ? X.flag[sq] : sq) : p;
     if (p == 0 || X.k1[p - 1] != X.k1[p]) P.head[dev_of_ref(X.k1[p], G.NC)] = p;
@@ -760,7 +761,9 @@ void launch_rehash(const KP& P, cudaStream_t s) { k_rehash<<<1, 1024, 0, s>>>(P)
 void launch_ghost_fill(const KP& P, cudaStream_t s) {
   if (P.n_gh) k_ghost_fill<<<(int)((P.n_gh + 255) / 256), 256, 0, s>>>(P);
 }
-void launch_clash_images(const KP& P, cudaStream_t s) { k_clash_images<<<1, 1024, 0, s>>>(P); }
+void launch_clash_images(const KP& P, cudaStream_t s, int zero_rho) {
+  k_clash_images<<<1, 1024, 0, s>>>(P, zero_rho);
+}
 void launch_clash_zero(const KP& P, int what, cudaStream_t s) {
   k_clash_zero<<<8, 256, 0, s>>>(P, what);
 }
