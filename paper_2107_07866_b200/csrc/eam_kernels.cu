@@ -516,7 +516,10 @@ bool launch_force(const KP& P, int mode, cudaStream_t s) {
 // sums this many (the rest of part_pair is zeroed before every force pass)
 int pair_partials(const KP& P, int mode) {
   (void)mode;
-  int n = eam_blocks(P);
+  int sms = 148, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int n = std::max(eam_blocks(P), 32 * sms);  // 1024-thread persistent variants
   for (int m = 0; m < 2; ++m) {
     n = std::max(n, 4 * fast_grid(P, true, m));
     n = std::max(n, 8 * tile_grid(P, true, m));  // 256-thread blocks

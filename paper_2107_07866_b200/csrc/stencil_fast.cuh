@@ -521,6 +521,15 @@ __device__ __forceinline__ double force_site_mask(const KP& P, KP* Pp, int par, 
 // indexed constant load); file scope so the address space is static
 __shared__ int g_soffs[2][kMaskBits + 1];
 
+// 64-byte spline records staged in shared memory: chunk c of record i at
+// 16-byte slot 4 i + (c ^ ((i >> 1) & 3)).  A 128-byte wavefront serves 8
+// distinct bank quads; record i lives in quad half (i & 1) and the XOR with
+// bits 1-2 of i spreads chunk c of random records over all 8 quads.
+__device__ __forceinline__ int smem_slot(int i, int c) { return 4 * i + (c ^ ((i >> 1) & 3)); }
+__device__ __forceinline__ double2 smem_chunk(const double2* T, int i, int c) {
+  return T[smem_slot(i, c)];
+}
+
 // 1/sqrt for r^2 in the normal range: the hardware approximation plus two
 // Newton steps (relative error a few ulp, no special-case branch)
 __device__ __forceinline__ double rsqrt_nr(double x) {
@@ -840,6 +849,134 @@ __device__ __forceinline__ double force_site_pipe(const KP& P, KP* Pp, int par, 
   return e;
 }
 
+// force pass, lean variant: one pair per iteration, no batching, so the
+// register footprint allows 6-8 resident CTAs per SM (latency hidden by
+// warps instead of by in-thread batching).  Warp-uniform union sweep.
+template <bool FULL, bool SMEM>
+__device__ __forceinline__ double force_site_lean(const KP& P, KP* Pp, int par, int d,
+                                                  bool live, const double2* T = nullptr,
+                                                  int seg_lo = 0) {
+  const double4* __restrict__ pdf = P.pdf;
+  const int* __restrict__ tgt = P.tgt;
+  const long long S = P.S;
+  double ax = kVacant, ay = 0, az = 0, adf = 0;
+  if (live) ld256(pdf + d, ax, ay, az, adf);
+  const bool occ = ax < kVacantTest;
+  if (!occ && FULL && live) {
+    P.frc[d] = 0.0;
+    P.frc[S + d] = 0.0;
+    P.frc[2 * S + d] = 0.0;
+  }
+  unsigned long long m0 = 0, m1 = 0;
+  if (occ) {
+    m0 = P.pmask[2 * (size_t)d];
+    m1 = P.pmask[2 * (size_t)d + 1];
+  }
+  const bool guard = (m1 & kGuardBit) != 0;
+  m1 &= ~kGuardBit;
+  const unsigned long long u0 = warp_or64(m0), u1 = warp_or64(m1);
+  unsigned cu = (unsigned)u0, co = (unsigned)m0;
+  unsigned pu1 = (unsigned)(u0 >> 32), po1 = (unsigned)(m0 >> 32);
+  unsigned pu2 = (unsigned)u1, po2 = (unsigned)m1;
+  unsigned pu3 = (unsigned)(u1 >> 32), po3 = (unsigned)(m1 >> 32);
+  int base = 0;
+  const int* s_offs = g_soffs[par];
+  const double ih = P.ff.ih;
+  const double r2_idle = P.cut2_lo;
+  double fx = 0.0, fy = 0.0, fz = 0.0, e = 0.0;
+  for (;;) {
+    while (cu == 0) {
+      if (base == 96) break;
+      cu = pu1;
+      co = po1;
+      pu1 = pu2;
+      po1 = po2;
+      pu2 = pu3;
+      po2 = po3;
+      pu3 = 0;
+      base += 32;
+    }
+    if (cu == 0) break;
+    const int bit = __ffs(cu) - 1;
+    cu &= cu - 1;
+    const bool v = (co >> bit) & 1;
+    const int j = v ? d + s_offs[base + bit] : d;
+    double px, py, pz, pw;
+    ld256(pdf + j, px, py, pz, pw);
+    const int t = __ldg(tgt + j);
+    const double dx = xsub(ax, px), dy = xsub(ay, py), dz = xsub(az, pz);
+    double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+    r2 = v ? r2 : r2_idle;
+    const double ri = rsqrt_nr(r2);
+    double sb;
+    const int seg = seg_index(P.ff, r2 * ri, sb);
+    double zA, zB, zC, zD, qA, qB, qC, qD;
+    const int li = seg - seg_lo;
+    if (SMEM && li >= 0) {
+      const double2 c0 = smem_chunk(T, li, 0), c1 = smem_chunk(T, li, 1);
+      const double2 c2 = smem_chunk(T, li, 2), c3 = smem_chunk(T, li, 3);
+      zA = c0.x; zB = c0.y; zC = c1.x; zD = c1.y;
+      qA = c2.x; qB = c2.y; qC = c3.x; qD = c3.y;
+    } else {
+      const double* rec = P.ff.rec + 8 * (size_t)seg;
+      ld256(rec, zA, zB, zC, zD);
+      ld256(rec + 4, qA, qB, qC, qD);
+    }
+    const double s15 = 1.5 * sb, s2 = sb + sb;
+    const double z = fma(fma(fma(zA, sb, zB), sb, zC), sb, zD);
+    const double zs = fma(fma(zA, s15, zB), s2, zC);  // dz/ds
+    const double ps = fma(fma(qA, s15, qB), s2, qC);  // drho/ds
+    const double phi = v ? z * ri : 0.0;
+    const double dphi = fma(zs, ih, -phi) * ri;
+    const double mfp = v ? fma((adf + pw) * ps, ih, dphi) * ri : 0.0;
+    const double qx = mfp * dx, qy = mfp * dy, qz = mfp * dz;
+    fx -= qx;
+    fy -= qy;
+    fz -= qz;
+    if (FULL) {
+      e = fma(0.5, phi, e);
+    } else {
+      e += phi;
+      if (v) {
+        red_add(&P.frc[t], qx);
+        red_add(&P.frc[S + t], qy);
+        red_add(&P.frc[2 * S + t], qz);
+      }
+    }
+  }
+  const int* offs = FULL ? c_full[par] : c_half[par];
+  if (guard) {  // the guard pairs skipped by the density pass's mask
+    const int n = FULL ? c_full_n[par] : c_half_n[par];
+    for (int kk = 0; kk < n; ++kk) {
+      const int jj = d + offs[kk];
+      double px, py, pz, pw;
+      ld256(pdf + jj, px, py, pz, pw);
+      const double ddx = xsub(ax, px), ddy = xsub(ay, py), ddz = xsub(az, pz);
+      const double r2 = fma(ddz, ddz, fma(ddy, ddy, ddx * ddx));
+      if (decide<FULL>(P, par, kk, jj, ax, ay, az, px, py, pz, ddx, ddy, ddz, r2) != 2) continue;
+      double q[4];
+      if (guard_force(Pp, d, jj, __ldg(tgt + jj), ddx, ddy, ddz, adf + pw, FULL, q)) {
+        fx -= q[0];
+        fy -= q[1];
+        fz -= q[2];
+        e = FULL ? fma(0.5, q[3], e) : e + q[3];
+      }
+    }
+  }
+  if (occ) {
+    if (FULL) {
+      P.frc[d] = fx;
+      P.frc[S + d] = fy;
+      P.frc[2 * S + d] = fz;
+    } else {
+      red_add(&P.frc[d], fx);
+      red_add(&P.frc[S + d], fy);
+      red_add(&P.frc[2 * S + d], fz);
+    }
+  }
+  return e;
+}
+
 // persistent CTAs over bricks: warp w owns z-plane w of the brick and sweeps
 // both sublattices (even then odd: balanced half-list lengths 46 + 66)
 __device__ __forceinline__ int next_brick(int* ctr) {
@@ -902,6 +1039,88 @@ __global__ void __launch_bounds__(128, 4) k_force_fast(KP P) {
       int d;
       const bool live = brick_site(P.G, b, par, d);
       e += force_site<FULL, B>(P, P.dself, par, d, live);
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
+  if ((threadIdx.x & 31) == 0) P.part_pair[(blockIdx.x * blockDim.x + threadIdx.x) >> 5] = e;
+}
+
+// lean force pass with the upper spline window (records [seg_lo, nseg])
+// in shared memory: 1024 threads, one CTA per SM, 8 groups of 4 warps each
+// on their own brick.  Pairs below the window (cascade cores) read global.
+constexpr int kLeanTabRecords = 3300;  // x 64 B = 211,200 B
+__device__ __forceinline__ int next_brick_group8(int* ctr, int group, volatile int* slot) {
+  asm volatile("bar.sync %0, 128;" ::"r"(group + 1));
+  if ((threadIdx.x & 127) == 0) slot[group] = atomicAdd(ctr, 1);
+  asm volatile("bar.sync %0, 128;" ::"r"(group + 1));
+  return slot[group];
+}
+
+template <bool FULL>
+__global__ void __launch_bounds__(1024, 1) k_force_lean_smem(KP P, int nsb) {
+  if (blockIdx.x >= nsb) {
+    clash_body<1>(P, blockIdx.x - nsb, gridDim.x - nsb);
+    return;
+  }
+  if (P.st->err || P.st->n_ovl) return;
+  extern __shared__ __align__(16) unsigned char smem_tab[];
+  __shared__ int s_slot[8];
+  double2* T = reinterpret_cast<double2*>(smem_tab);
+  const int nseg = P.ff.nseg;  // records 0..nseg (padded)
+  const int seg_lo = max(0, nseg + 1 - kLeanTabRecords);
+  const int nrec = nseg + 1 - seg_lo;
+  const double2* src = reinterpret_cast<const double2*>(P.ff.rec + 8 * (size_t)seg_lo);
+  for (int q = threadIdx.x; q < 4 * nrec; q += blockDim.x)
+    T[smem_slot(q >> 2, q & 3)] = __ldg(src + q);
+  for (int i = threadIdx.x; i < 2 * (kMaskBits + 1); i += blockDim.x) {
+    const int par = i / (kMaskBits + 1), k = i % (kMaskBits + 1);
+    const int n = FULL ? c_full_n[par] : c_half_n[par];
+    g_soffs[par][k] = k < n ? (FULL ? c_full[par][k] : c_half[par][k]) : 0;
+  }
+  __syncthreads();
+  const int group = threadIdx.x >> 7;
+  const int lt = threadIdx.x & 127, lane = lt & 31, w = lt >> 5;
+  const Geo& G = P.G;
+  const int nbx = (G.bx + kBrickX - 1) / kBrickX, nby = (G.by + kBrickY - 1) / kBrickY;
+  const int nb = brick_count(G);
+  double e = 0.0;
+  for (;;) {
+    const int b = next_brick_group8(&P.work[1], group, s_slot);
+    if (b >= nb) break;
+    const int cx = (b % nbx) * kBrickX + (lane & 7), cy = ((b / nbx) % nby) * kBrickY + (lane >> 3),
+              cz = (b / (nbx * nby)) * kBrickZ + w;
+    const bool live = cx < G.bx && cy < G.by && cz < G.bz;
+    const int c = live ? (int)cell_of(cx + G.g, cy + G.g, cz + G.g, G) : 0;
+    for (int par = 0; par < 2; ++par)
+      e += force_site_lean<FULL, true>(P, P.dself, par, live ? (int)(par * G.NC + c) : 0, live,
+                                       T, seg_lo);
+  }
+  for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
+  if ((threadIdx.x & 31) == 0) P.part_pair[(blockIdx.x * blockDim.x + threadIdx.x) >> 5] = e;
+}
+
+template <bool FULL, int MINB>
+__global__ void __launch_bounds__(128, MINB) k_force_lean(KP P, int nsb) {
+  if (blockIdx.x >= nsb) {
+    clash_body<1>(P, blockIdx.x - nsb, gridDim.x - nsb);
+    return;
+  }
+  if (P.st->err || P.st->n_ovl) return;
+  for (int i = threadIdx.x; i < 2 * (kMaskBits + 1); i += blockDim.x) {
+    const int par = i / (kMaskBits + 1), k = i % (kMaskBits + 1);
+    const int n = FULL ? c_full_n[par] : c_half_n[par];
+    g_soffs[par][k] = k < n ? (FULL ? c_full[par][k] : c_half[par][k]) : 0;
+  }
+  __syncthreads();
+  const int nb = brick_count(P.G);
+  double e = 0.0;
+  for (;;) {
+    const int b = next_brick(&P.work[1]);
+    if (b >= nb) break;
+    for (int par = 0; par < 2; ++par) {
+      int d;
+      const bool live = brick_site(P.G, b, par, d);
+      e += force_site_lean<FULL, false>(P, P.dself, par, d, live);
     }
   }
   for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
@@ -1191,7 +1410,12 @@ int fast_grid(const KP& P, bool force, int mode) {
     int c5 = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(
         &c5, mode ? (const void*)k_force_pipe<true> : (const void*)k_force_pipe<false>, 128, 0);
-    per_sm = max(max(max(a, b), max(c2, c4)), c5);
+    int c6 = 0, c8 = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &c6, mode ? (const void*)k_force_lean<true, 6> : (const void*)k_force_lean<false, 6>, 128, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &c8, mode ? (const void*)k_force_lean<true, 8> : (const void*)k_force_lean<false, 8>, 128, 0);
+    per_sm = max(max(max(a, b), max(c2, c4)), max(c5, max(c6, c8)));
   }
   if (!force)
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(
@@ -1234,6 +1458,39 @@ bool launch_force_fast(const KP& P, int mode, int grid, cudaStream_t s) {
     const char* e = getenv("CBX_FORCE_PIPE");
     return e ? atoi(e) : 1;
   }();
+  static const int lean = [] {
+    const char* e = getenv("CBX_FORCE_LEAN");
+    return e ? atoi(e) : 0;
+  }();
+  if (P.use_mask && lean == 1) {
+    const size_t bytes = (size_t)kLeanTabRecords * 64;
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_force_lean_smem<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)bytes);
+      cudaFuncSetAttribute(k_force_lean_smem<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)bytes);
+      attr = true;
+    }
+    int sms = 148, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int g = max(1, min(sms, (brick_count(P.G) + 7) / 8));
+    if (mode) k_force_lean_smem<true><<<g, 1024, bytes, s>>>(P, g);
+    else k_force_lean_smem<false><<<g + 4, 1024, bytes, s>>>(P, g);
+    return !mode;
+  }
+  if (P.use_mask && lean) {
+    const int ex = mode ? 0 : kClashBlocks128;
+    if (lean == 8) {
+      if (mode) k_force_lean<true, 8><<<grid, 128, 0, s>>>(P, grid);
+      else k_force_lean<false, 8><<<grid + ex, 128, 0, s>>>(P, grid);
+    } else {
+      if (mode) k_force_lean<true, 6><<<grid, 128, 0, s>>>(P, grid);
+      else k_force_lean<false, 6><<<grid + ex, 128, 0, s>>>(P, grid);
+    }
+    return !mode;
+  }
   if (P.use_mask && pipe) {
     if (mode) k_force_pipe<true><<<grid, 128, 0, s>>>(P, grid);
     else k_force_pipe<false><<<grid + kClashBlocks128, 128, 0, s>>>(P, grid);
