@@ -146,8 +146,13 @@ __device__ __forceinline__ double skin_density(const KP& P, KP* Pp, int par, int
   return rho;
 }
 
-template <bool FULL, int B>
-__device__ __forceinline__ void density_site(const KP& P, KP* Pp, int par, int d, bool live) {
+// 32-byte density records staged in shared memory: chunk c of record i at
+// 16-byte slot 2 i + (c ^ ((i >> 2) & 1)) (8 distinct bank quads for random i)
+__device__ __forceinline__ int smem_slot32(int i, int c) { return 2 * i + (c ^ ((i >> 2) & 1)); }
+
+template <bool FULL, int B, bool SMEM = false>
+__device__ __forceinline__ void density_site(const KP& P, KP* Pp, int par, int d, bool live,
+                                             const double2* T = nullptr, int seg_lo = 0) {
   const double4* __restrict__ pdf = P.pdf;
   const int* __restrict__ tgt = P.tgt;
   double ax = kVacant, ay = 0, az = 0, aw = 0;
@@ -204,7 +209,18 @@ __device__ __forceinline__ void density_site(const KP& P, KP* Pp, int par, int d
     double tA[B], tB[B], tC[B], tD[B];
 #pragma unroll
     for (int b = 0; b < B; ++b)
-      if (in[b]) ld256(P.fd.rec + 4 * (size_t)seg[b], tA[b], tB[b], tC[b], tD[b]);
+      if (in[b]) {
+        const int li = seg[b] - seg_lo;
+        if (SMEM && li >= 0) {
+          const double2 c0 = T[smem_slot32(li, 0)], c1 = T[smem_slot32(li, 1)];
+          tA[b] = c0.x;
+          tB[b] = c0.y;
+          tC[b] = c1.x;
+          tD[b] = c1.y;
+        } else {
+          ld256(P.fd.rec + 4 * (size_t)seg[b], tA[b], tB[b], tC[b], tD[b]);
+        }
+      }
 #pragma unroll
     for (int b = 0; b < B; ++b) {
       if (in[b]) {
@@ -1008,6 +1024,51 @@ __host__ __device__ __forceinline__ int brick_count(const Geo& G) {
 // only: every update is an atomic add, so it may overlap the slot sweep)
 constexpr int kClashBlocks128 = 32;
 
+// groups of 128 threads (4 warps) of a large CTA, each on its own brick
+__device__ __forceinline__ int next_brick_group8(int* ctr, int group, volatile int* slot) {
+  asm volatile("bar.sync %0, 128;" ::"r"(group + 1));
+  if ((threadIdx.x & 127) == 0) slot[group] = atomicAdd(ctr, 1);
+  asm volatile("bar.sync %0, 128;" ::"r"(group + 1));
+  return slot[group];
+}
+
+// density pass with the upper rho-spline window in shared memory (32-byte
+// records): 512 threads = 4 groups of 4 warps, one CTA per SM
+constexpr int kDensTabRecords = 3300;  // x 32 B = 105,600 B
+template <bool FULL, int B>
+__global__ void __launch_bounds__(512, 1) k_density_smem(KP P, int nsb) {
+  if (blockIdx.x >= nsb) {
+    clash_body<0>(P, blockIdx.x - nsb, gridDim.x - nsb);
+    return;
+  }
+  if (P.st->err) return;
+  extern __shared__ __align__(16) unsigned char smem_tab[];
+  __shared__ int s_slot[4];
+  double2* T = reinterpret_cast<double2*>(smem_tab);
+  const int nseg = P.fd.nseg;
+  const int seg_lo = max(0, nseg + 1 - kDensTabRecords);
+  const int nrec = nseg + 1 - seg_lo;
+  const double2* src = reinterpret_cast<const double2*>(P.fd.rec + 4 * (size_t)seg_lo);
+  for (int q = threadIdx.x; q < 2 * nrec; q += blockDim.x) T[smem_slot32(q >> 1, q & 1)] = __ldg(src + q);
+  __syncthreads();
+  const int group = threadIdx.x >> 7;
+  const int lt = threadIdx.x & 127, lane = lt & 31, w = lt >> 5;
+  const Geo& G = P.G;
+  const int nbx = (G.bx + kBrickX - 1) / kBrickX, nby = (G.by + kBrickY - 1) / kBrickY;
+  const int nb = brick_count(G);
+  for (;;) {
+    const int b = next_brick_group8(&P.work[0], group, s_slot);
+    if (b >= nb) break;
+    const int cx = (b % nbx) * kBrickX + (lane & 7), cy = ((b / nbx) % nby) * kBrickY + (lane >> 3),
+              cz = (b / (nbx * nby)) * kBrickZ + w;
+    const bool live = cx < G.bx && cy < G.by && cz < G.bz;
+    const int c = live ? (int)cell_of(cx + G.g, cy + G.g, cz + G.g, G) : 0;
+    for (int par = 0; par < 2; ++par)
+      density_site<FULL, B, true>(P, P.dself, par, live ? (int)(par * G.NC + c) : 0, live, T,
+                                  seg_lo);
+  }
+}
+
 template <bool FULL, int B, int MINB>
 __global__ void __launch_bounds__(128, MINB) k_density_fast(KP P, int nsb) {
   if (blockIdx.x >= nsb) {
@@ -1049,12 +1110,6 @@ __global__ void __launch_bounds__(128, 4) k_force_fast(KP P) {
 // in shared memory: 1024 threads, one CTA per SM, 8 groups of 4 warps each
 // on their own brick.  Pairs below the window (cascade cores) read global.
 constexpr int kLeanTabRecords = 3300;  // x 64 B = 211,200 B
-__device__ __forceinline__ int next_brick_group8(int* ctr, int group, volatile int* slot) {
-  asm volatile("bar.sync %0, 128;" ::"r"(group + 1));
-  if ((threadIdx.x & 127) == 0) slot[group] = atomicAdd(ctr, 1);
-  asm volatile("bar.sync %0, 128;" ::"r"(group + 1));
-  return slot[group];
-}
 
 template <bool FULL>
 __global__ void __launch_bounds__(1024, 1) k_force_lean_smem(KP P, int nsb) {
@@ -1430,6 +1485,28 @@ int fast_grid(const KP& P, bool force, int mode) {
 }
 
 bool launch_density_fast(const KP& P, int mode, int grid, cudaStream_t s) {
+  static const int dsm = [] {
+    const char* e = getenv("CBX_DENSITY_SMEM");
+    return e ? atoi(e) : 0;
+  }();
+  if (dsm) {
+    const size_t bytes = (size_t)kDensTabRecords * 32;
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_density_smem<false, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)bytes);
+      cudaFuncSetAttribute(k_density_smem<true, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)bytes);
+      attr = true;
+    }
+    int sms = 148, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int g = max(1, min(sms, (brick_count(P.G) + 3) / 4));
+    if (mode) k_density_smem<true, 4><<<g, 512, bytes, s>>>(P, g);
+    else k_density_smem<false, 4><<<g + 8, 512, bytes, s>>>(P, g);
+    return !mode;
+  }
   static const int batch = [] {
     const char* e = getenv("CBX_DENSITY_BATCH");
     return e ? atoi(e) : 4;
@@ -1458,9 +1535,9 @@ bool launch_force_fast(const KP& P, int mode, int grid, cudaStream_t s) {
     const char* e = getenv("CBX_FORCE_PIPE");
     return e ? atoi(e) : 1;
   }();
-  static const int lean = [] {
+  static const int lean = [] {  // 1: shared-memory spline window (default)
     const char* e = getenv("CBX_FORCE_LEAN");
-    return e ? atoi(e) : 0;
+    return e ? atoi(e) : 1;
   }();
   if (P.use_mask && lean == 1) {
     const size_t bytes = (size_t)kLeanTabRecords * 64;
