@@ -253,7 +253,7 @@ void seq_density(cbx_ctx* c) {
   c->mask_valid = c->mode != CBX_STENCIL_REFERENCE && c->P.pmask != nullptr;
 }
 void seq_embed(cbx_ctx* c) {
-  launch_embed(c->P, c->stream);
+  launch_embed(c->P, c->stream, c->mode == CBX_STENCIL_REFERENCE);
   c->clash_f_zero = true;
   c->launches += 2;
 }
@@ -700,6 +700,20 @@ void setup_fast(cbx_ctx* c) {
   P.fd.nseg = n;
   P.ff = P.fd;
   P.ff.rec = dff;
+  // embedding F(rho), same normalisation (its own grid)
+  {
+    const Spline& em = c->pot.embed;
+    const int ne = (int)em.nseg();
+    std::vector<double> fe(4 * (ne + 1));
+    for (int i = 0; i < ne; ++i) norm(&em.seg[7 * i], em.h, &fe[4 * i]);
+    pad(&fe[4 * (ne - 1)], &fe[4 * ne]);
+    double* dfe = c->alloc<double>(fe.size());
+    cuda_check(cudaMemcpy(dfe, fe.data(), fe.size() * 8, cudaMemcpyHostToDevice), "fast table");
+    P.fe.rec = dfe;
+    P.fe.ih = 1.0 / em.h;
+    P.fe.c0 = -em.x0 / em.h;
+    P.fe.nseg = ne;
+  }
   // fp32 filter band: |r2_f32 - r2_exact| <= err for coordinates below
   // maxc (two roundings to fp32, exact fp32 difference, three fp32 ops)
   const double maxc = (std::max(std::max(c->G.tx, c->G.ty), c->G.gtz) + 4) * c->G.a0;

@@ -79,6 +79,7 @@ struct KP {
   float4* uf;      // fp32 shadow (x, y, z, owner-or--1) for the candidate filter
   int* work;       // persistent-kernel work counters (zeroed per launch)
   FastTab fd, ff;  // density / force fast tables
+  FastTab fe;      // embedding F(rho): 4 doubles/segment (A B C D), padded
   float band_hi, band_lo;  // fp32 r^2 filter: reject above hi, exact test in [lo, hi]
   double guard_r2;         // below: overlap / short-range guard path
   double cut2_lo, cut2_hi; // fp64 (FMA) r^2 decides outside [lo, hi]; exact r^2 inside
@@ -169,7 +170,8 @@ __device__ __forceinline__ void set_error(DevStatus* st, int code) { atomicCAS(&
 // device entry points (launch wrappers), implemented in the .cu files
 bool launch_density(const KP& P, int mode, cudaStream_t s);  // true: clash pass fused
 void launch_clash_density(const KP& P, cudaStream_t s);
-void launch_embed(const KP& P, cudaStream_t s);
+// literal: the reference arithmetic of spline_eval (stencil mode 2)
+void launch_embed(const KP& P, cudaStream_t s, bool literal = false);
 bool launch_force(const KP& P, int mode, cudaStream_t s);
 void launch_clash_force(const KP& P, cudaStream_t s);
 void launch_kick_drift(const KP& P, int move, cudaStream_t s);

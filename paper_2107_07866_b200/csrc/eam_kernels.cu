@@ -74,6 +74,21 @@ __device__ __forceinline__ void seg_eval(const Tab& T, double x, double& v, doub
   v = ((__ldg(g) * t + __ldg(g + 1)) * t + __ldg(g + 2)) * t + __ldg(g + 3);
   dv = (__ldg(g + 4) * t + __ldg(g + 5)) * t + __ldg(g + 6);
 }
+// F(rho) and F'(rho) from the normalised records (clamped like spline_eval,
+// spline.cpp:79-93): u = (x - x0)/h by one FMA, segment by a round-down add
+__device__ __forceinline__ void emb_eval_fast(const KP& P, double x, double& v, double& dv) {
+  x = fmin(fmax(x, P.emb.x0), P.emb.xl);
+  const double u = fma(x, P.fe.ih, P.fe.c0);
+  const double t = __dadd_rd(u, 4503599627370496.0);
+  const double s = u - (t - 4503599627370496.0);
+  const int i = min(__double2loint(t), P.fe.nseg);
+  const double* r = P.fe.rec + 4 * (size_t)i;
+  const double2 ab = __ldg(reinterpret_cast<const double2*>(r));
+  const double2 cd = __ldg(reinterpret_cast<const double2*>(r) + 1);
+  v = fma(fma(fma(ab.x, s, ab.y), s, cd.x), s, cd.y);
+  dv = fma(fma(ab.x, 1.5 * s, ab.y), s + s, cd.x) * P.fe.ih;
+}
+
 __device__ __forceinline__ double seg_deriv(const Tab& T, double x) {
   if (x < T.x0) x = T.x0;
   if (x > T.xl) x = T.xl;
@@ -306,7 +321,7 @@ __device__ void clash_embed_body(const KP& P, int blk, int nblk) {
 
 // blocks [0, nsb): all slots, grid-stride, one energy partial per block;
 // blocks [nsb, grid): the clash records (fused k_clash_embed)
-__global__ void __launch_bounds__(256) k_embed(KP P, int nsb) {
+__global__ void __launch_bounds__(256) k_embed(KP P, int nsb, int literal) {
   if (blockIdx.x >= nsb) {
     clash_embed_body(P, blockIdx.x - nsb, gridDim.x - nsb);
     // the records' force accumulators for the force pass (clash_zero fused)
@@ -330,7 +345,8 @@ __global__ void __launch_bounds__(256) k_embed(KP P, int nsb) {
     const int t = P.tgt[d];
     const double r = P.rho[t];
     double v, dv;
-    seg_eval(P.emb, r, v, dv);
+    if (literal) seg_eval(P.emb, r, v, dv);
+    else emb_eval_fast(P, r, v, dv);
     // owned here: interior site (a z-halo site of a slab rank also has
     // t == d, but its rho is a partial and its dF comes from the owner)
     bool owned = t == d;
@@ -526,9 +542,9 @@ int pair_partials(const KP& P, int mode) {
   }
   return std::min(n, P.n_part);
 }
-void launch_embed(const KP& P, cudaStream_t s) {
+void launch_embed(const KP& P, cudaStream_t s, bool literal) {
   const int nsb = embed_grid(P);
-  k_embed<<<nsb + 16, 256, 0, s>>>(P, nsb);
+  k_embed<<<nsb + 16, 256, 0, s>>>(P, nsb, literal ? 1 : 0);
 }
 void launch_clash_density(const KP& P, cudaStream_t s) { k_clash<0><<<16, 256, 0, s>>>(P); }
 void launch_clash_force(const KP& P, cudaStream_t s) { k_clash<1><<<16, 256, 0, s>>>(P); }
