@@ -184,7 +184,8 @@ CBX_API cbx_status cbx_describe(cbx_ctx* ctx, char* buf, long n);
 /* benchmark loop: nsteps fixed-dt steps, each preceded (outside the timed
  * region) by a write of flush_mb MB to evict L2; per-step CUDA events on the
  * context stream.  out_ms = {density, embed, force, store, integrate, step,
- * steps, 0} summed over the steps. */
+ * steps, force kernel alone} summed over the steps (phases include their
+ * memsets; the last entry brackets only the force kernel launch). */
 CBX_API cbx_status cbx_bench_steps(cbx_ctx* ctx, double dt, long nsteps, double flush_mb,
                                    double out_ms[8]);
 /* measured fp64 peak of this device: a dependent-free DFMA stream over all

@@ -161,6 +161,25 @@ class StoreArrays:
     clash_ghost: np.ndarray
 
 
+def pinned_store(n_slots: int) -> StoreArrays:
+    """slot arrays in page-locked host memory (DMA at full PCIe / C2C rate);
+    clash arrays are small and stay pageable"""
+    import torch
+
+    def pin(shape, dtype):
+        return torch.empty(shape, dtype=dtype, pin_memory=True).numpy()
+    S = n_slots
+    return StoreArrays(pos=pin((S, 3), torch.float64), vel=pin((S, 3), torch.float64),
+                       force=pin((S, 3), torch.float64), rho=pin((S,), torch.float64),
+                       df=pin((S,), torch.float64), tag=pin((S,), torch.int64).view(np.uint64),
+                       valid=pin((S,), torch.uint8), ghost=pin((S,), torch.uint8),
+                       clash_key=np.zeros(0, np.int64), clash_idx=np.zeros(0, np.int32),
+                       clash_pos=np.zeros((0, 3)), clash_vel=np.zeros((0, 3)),
+                       clash_force=np.zeros((0, 3)), clash_rho=np.zeros(0),
+                       clash_df=np.zeros(0), clash_tag=np.zeros(0, np.uint64),
+                       clash_ghost=np.zeros(0, np.uint8))
+
+
 class DeviceStore:
     """A LatticeStore + force engine resident on one GPU (one cbx_ctx)."""
 
@@ -226,11 +245,17 @@ class DeviceStore:
                         _ptr(cf), _ptr(cr), _ptr(cd), _ptr(ct), _ptr(cg))
         self._check(self.lib.cbx_upload_store(self.h, C.byref(st)))
 
-    def download(self) -> StoreArrays:
+    def download(self, out: Optional["StoreArrays"] = None) -> StoreArrays:
+        """the store snapshot; `out` (e.g. from pinned_store()) is reused for
+        the slot arrays when given"""
         S = self.n_slots
-        a = dict(pos=np.zeros((S, 3)), vel=np.zeros((S, 3)), force=np.zeros((S, 3)),
-                 rho=np.zeros(S), df=np.zeros(S), tag=np.zeros(S, np.uint64),
-                 valid=np.zeros(S, np.uint8), ghost=np.zeros(S, np.uint8))
+        if out is not None and len(out.tag) == S:
+            a = {k: getattr(out, k) for k in ("pos", "vel", "force", "rho", "df", "tag", "valid",
+                                               "ghost")}
+        else:
+            a = dict(pos=np.zeros((S, 3)), vel=np.zeros((S, 3)), force=np.zeros((S, 3)),
+                     rho=np.zeros(S), df=np.zeros(S), tag=np.zeros(S, np.uint64),
+                     valid=np.zeros(S, np.uint8), ghost=np.zeros(S, np.uint8))
         n = self.lib.cbx_clash_count(self.h)
         c = dict(clash_key=np.zeros(n, np.int64), clash_idx=np.zeros(n, np.int32),
                  clash_pos=np.zeros((n, 3)), clash_vel=np.zeros((n, 3)),
