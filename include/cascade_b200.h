@@ -184,13 +184,17 @@ CBX_API cbx_status cbx_describe(cbx_ctx* ctx, char* buf, long n);
 /* benchmark loop: nsteps fixed-dt steps, each preceded (outside the timed
  * region) by a write of flush_mb MB to evict L2; per-step CUDA events on the
  * context stream.  out_ms = {density, embed, force, store, integrate, step,
- * steps, force kernel alone} summed over the steps (phases include their
- * memsets; the last entry brackets only the force kernel launch). */
+ * steps, force kernel alone} summed over the steps.  The step time comes
+ * from events around each graph launch and the force kernel from an event
+ * pair inside the graph; the per-phase entries (which include their
+ * memsets) are measured only after cbx_bench_phases(ctx, 1) -- their event
+ * nodes add latency to the step -- and are 0 otherwise. */
 CBX_API cbx_status cbx_bench_steps(cbx_ctx* ctx, double dt, long nsteps, double flush_mb,
                                    double out_ms[8]);
 /* measured fp64 peak of this device: a dependent-free DFMA stream over all
  * SMs, timed with CUDA events (TFLOP/s, DFMA = 2 flops) */
 CBX_API cbx_status cbx_fp64_peak(int device, double* tflops, double* sm_mhz);
+CBX_API cbx_status cbx_bench_phases(cbx_ctx* ctx, int on);
 
 /* ---- z-slab domain decomposition (multi-GPU) ------------- */
 /* rank r of n owns global interior z planes [r*bz/n, (r+1)*bz/n) of the

@@ -143,6 +143,7 @@ SIGNATURES = [
     ("cbx_slab_unpack", C.c_int, [_P, C.c_int, C.c_int, _P, C.c_long]),
     ("cbx_slab_local_state", C.c_int, [_P, C.POINTER(C.c_double)]),
     ("cbx_slab_commit", C.c_int, [_P, C.POINTER(C.c_double)]),
+    ("cbx_bench_phases", C.c_int, [_P, C.c_int]),
     ("cbx_nccl_unique_id", C.c_int, [_P, C.c_long]),
     ("cbx_slab_comm_init", C.c_int, [_P, _P, C.c_long]),
     ("cbx_slab_p2p_handle", C.c_int, [_P, _P, C.c_long]),

@@ -35,6 +35,10 @@ struct cbx_ctx {
   size_t flush_bytes = 0;
   bool use_graph = true;
   bool timing = false;
+  bool timing_lite = false;   // capture only the force-kernel events
+  bool bench_phases = false;  // cbx_bench_steps: per-phase events inside the graph
+  cudaGraphExec_t timed_lite = nullptr;
+  cudaEvent_t ev_outer[2]{};
   cudaEvent_t ev[8]{};
   double t_ms[8]{};
   uint64_t launches = 0;
@@ -232,8 +236,9 @@ void write_status(cbx_ctx* c) {
 // ---- launch sequences ----------------------------------------------------
 bool g_capturing = false;
 void ev_mark(cbx_ctx* c, int i) {
-  // inside a capture the record must become an external event-record node
-  if (c->timing)
+  // inside a capture the record must become an external event-record node;
+  // the lean timed graph keeps only the force-kernel bracket (6, 7)
+  if (c->timing && (!c->timing_lite || i >= 6))
     cudaEventRecordWithFlags(c->ev[i], c->stream, g_capturing ? cudaEventRecordExternal : 0);
 }
 
@@ -477,8 +482,10 @@ void require_box(cbx_ctx* c, const char* what) {
 void drop_graph(cbx_ctx* c) {
   if (c->step_graph) cudaGraphExecDestroy(c->step_graph);
   if (c->timed_graph) cudaGraphExecDestroy(c->timed_graph);
+  if (c->timed_lite) cudaGraphExecDestroy(c->timed_lite);
   c->step_graph = nullptr;
   c->timed_graph = nullptr;
+  c->timed_lite = nullptr;
 }
 
 // ---- the store view ------------------------------------------------------
@@ -1214,6 +1221,8 @@ CBX_API void cbx_destroy(cbx_ctx* c) {
   if (c->flush_buf) cudaFree(c->flush_buf);
   for (auto& e : c->ev)
     if (e) cudaEventDestroy(e);
+  for (auto& e : c->ev_outer)
+    if (e) cudaEventDestroy(e);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
 }
@@ -1542,7 +1551,15 @@ CBX_API cbx_status cbx_bench_steps(cbx_ctx* c, double dt, long nsteps, double fl
     c->hst.dt_next = dt;
     c->hst.adaptive = 0;
     write_status(c);
-    if (!c->timed_graph) c->timed_graph = capture_step(c, true);
+    const bool phases = c->bench_phases;
+    cudaGraphExec_t* gp = phases ? &c->timed_graph : &c->timed_lite;
+    if (!*gp) {
+      c->timing_lite = !phases;
+      *gp = capture_step(c, true);
+      c->timing_lite = false;
+    }
+    if (!c->ev_outer[0])
+      for (auto& e : c->ev_outer) cuda_check(cudaEventCreate(&e), "event");
     const size_t fb = (size_t)(flush_mb * 1048576.0);
     if (fb > c->flush_bytes) {
       if (c->flush_buf) cudaFree(c->flush_buf);
@@ -1552,14 +1569,23 @@ CBX_API cbx_status cbx_bench_steps(cbx_ctx* c, double dt, long nsteps, double fl
     double acc[8] = {0};
     for (long i = 0; i < nsteps; ++i) {
       if (fb) cudaMemsetAsync(c->flush_buf, (int)(i & 0xff), fb, c->stream);  // evict L2
-      cuda_check(cudaGraphLaunch(c->timed_graph, c->stream), "graph launch");
+      // the step: events on the stream around the graph launch
+      cudaEventRecord(c->ev_outer[0], c->stream);
+      cuda_check(cudaGraphLaunch(*gp, c->stream), "graph launch");
+      cudaEventRecord(c->ev_outer[1], c->stream);
       c->launches += c->graph_launches;
-      cuda_check(cudaEventSynchronize(c->ev[5]), "event sync");
+      cuda_check(cudaEventSynchronize(c->ev_outer[1]), "event sync");
       float ms;
-      const int seg[7][2] = {{1, 2}, {2, 3}, {3, 4}, {0, 1}, {4, 5}, {0, 5}, {6, 7}};
-      for (int k = 0; k < 7; ++k) {
-        cudaEventElapsedTime(&ms, c->ev[seg[k][0]], c->ev[seg[k][1]]);
-        acc[k == 6 ? 7 : k] += ms;
+      cudaEventElapsedTime(&ms, c->ev_outer[0], c->ev_outer[1]);
+      acc[5] += ms;
+      cudaEventElapsedTime(&ms, c->ev[6], c->ev[7]);
+      acc[7] += ms;
+      if (phases) {
+        const int seg[5][2] = {{1, 2}, {2, 3}, {3, 4}, {0, 1}, {4, 5}};
+        for (int k = 0; k < 5; ++k) {
+          cudaEventElapsedTime(&ms, c->ev[seg[k][0]], c->ev[seg[k][1]]);
+          acc[k] += ms;
+        }
       }
     }
     acc[6] = (double)nsteps;
@@ -1567,6 +1593,10 @@ CBX_API cbx_status cbx_bench_steps(cbx_ctx* c, double dt, long nsteps, double fl
     raise_device_error(c, true);
     for (int k = 0; k < 8; ++k) out_ms[k] = acc[k];
   });
+}
+
+CBX_API cbx_status cbx_bench_phases(cbx_ctx* c, int on) {
+  return guarded(c, [&] { c->bench_phases = on != 0; });
 }
 
 CBX_API cbx_status cbx_describe(cbx_ctx* c, char* buf, long n) {

@@ -1111,8 +1111,8 @@ __global__ void __launch_bounds__(128, 4) k_force_fast(KP P) {
 // on their own brick.  Pairs below the window (cascade cores) read global.
 constexpr int kLeanTabRecords = 3300;  // x 64 B = 211,200 B
 
-template <bool FULL>
-__global__ void __launch_bounds__(1024, 1) k_force_lean_smem(KP P, int nsb) {
+template <bool FULL, int NT>
+__global__ void __launch_bounds__(NT, 1) k_force_lean_smem(KP P, int nsb) {
   if (blockIdx.x >= nsb) {
     clash_body<1>(P, blockIdx.x - nsb, gridDim.x - nsb);
     return;
@@ -1543,18 +1543,32 @@ bool launch_force_fast(const KP& P, int mode, int grid, cudaStream_t s) {
     const size_t bytes = (size_t)kLeanTabRecords * 64;
     static bool attr = false;
     if (!attr) {
-      cudaFuncSetAttribute(k_force_lean_smem<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)bytes);
-      cudaFuncSetAttribute(k_force_lean_smem<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)bytes);
+      cudaFuncSetAttribute(k_force_lean_smem<false, 1024>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+      cudaFuncSetAttribute(k_force_lean_smem<true, 1024>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+      cudaFuncSetAttribute(k_force_lean_smem<false, 768>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+      cudaFuncSetAttribute(k_force_lean_smem<true, 768>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
       attr = true;
     }
     int sms = 148, dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int g = max(1, min(sms, (brick_count(P.G) + 7) / 8));
-    if (mode) k_force_lean_smem<true><<<g, 1024, bytes, s>>>(P, g);
-    else k_force_lean_smem<false><<<g + 4, 1024, bytes, s>>>(P, g);
+    static const int nt = [] {
+      const char* e = getenv("CBX_LEAN_THREADS");
+      return e ? atoi(e) : 1024;
+    }();
+    if (nt == 768) {
+      const int g6 = max(1, min(sms, (brick_count(P.G) + 5) / 6));
+      if (mode) k_force_lean_smem<true, 768><<<g6, 768, bytes, s>>>(P, g6);
+      else k_force_lean_smem<false, 768><<<g6 + 4, 768, bytes, s>>>(P, g6);
+    } else {
+      if (mode) k_force_lean_smem<true, 1024><<<g, 1024, bytes, s>>>(P, g);
+      else k_force_lean_smem<false, 1024><<<g + 4, 1024, bytes, s>>>(P, g);
+    }
     return !mode;
   }
   if (P.use_mask && lean) {

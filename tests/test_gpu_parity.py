@@ -370,9 +370,12 @@ def test_bench_steps_timed_graph(cuda, tables):
     dev = device_for(ref, tables["baseline"])
     dev.set_state(ref.state())
     out = (C.c_double * 8)()
-    _lib.check(dev.lib.cbx_bench_steps(dev.h, 1e-3, 10, 64.0, out), dev.h)
+    _lib.check(dev.lib.cbx_bench_steps(dev.h, 1e-3, 6, 64.0, out), dev.h)
+    assert out[6] == 6 and out[5] > 0 and out[7] > 0 and out[5] > out[7]
+    _lib.check(dev.lib.cbx_bench_phases(dev.h, 1), dev.h)
+    _lib.check(dev.lib.cbx_bench_steps(dev.h, 1e-3, 4, 64.0, out), dev.h)
     ref.step(1e-3, 10)
-    assert out[6] == 10 and out[5] > 0 and out[2] > 0 and out[0] > 0
+    assert out[6] == 4 and out[5] > 0 and out[2] > 0 and out[0] > 0
     assert dev.state()["step"] == ref.state()["step"]
     assert_store_parity(ref.store(), dev.download(), pos_tol=1e-9, rel=1e-8)
 
