@@ -47,6 +47,8 @@ struct cbx_ctx {
   bool mask_valid = false;
   bool clash_rho_zero = false;  // the last clash-image pass zeroed the records' rho
   bool clash_f_zero = false;    // the last embed pass zeroed the records' forces
+  bool acc_rho_zero = false;    // kick_drift of this step cleared rho (single box)
+  bool acc_frc_zero = false;    // ... and the forces
   bool tile_ok = false;  // every offset within the 2-cell tile halo
   // z-slab decomposition
   int rank = 0, nranks = 1;
@@ -250,9 +252,12 @@ void seq_fill_ghosts(cbx_ctx* c, bool zero_rho = false) {
   c->launches += 2;
 }
 void seq_density(cbx_ctx* c) {
-  cudaMemsetAsync(c->P.work, 0, sizeof(int), c->stream);
-  if (c->mode != CBX_STENCIL_FULL)
+  // on the step path the brick counter was reset by k_clash_images and rho
+  // by k_kick_drift; standalone calls clear them here
+  if (!c->clash_rho_zero) cudaMemsetAsync(c->P.work, 0, sizeof(int), c->stream);
+  if (c->mode != CBX_STENCIL_FULL && !c->acc_rho_zero)
     cudaMemsetAsync(c->P.rho, 0, c->S * sizeof(double), c->stream);
+  c->acc_rho_zero = false;
   if (!c->clash_rho_zero) launch_clash_zero(c->P, 0, c->stream);
   c->clash_rho_zero = false;
   if (!launch_density(c->P, c->mode, c->stream)) {
@@ -268,14 +273,16 @@ void seq_embed(cbx_ctx* c) {
   c->launches += 2;
 }
 void seq_force(cbx_ctx* c) {
-  cudaMemsetAsync(c->P.work + 1, 0, sizeof(int), c->stream);
-  if (c->mode != CBX_STENCIL_FULL)
+  // the embedding pass resets the brick counter and the clash records'
+  // forces; kick_drift of a step cleared the slot forces
+  if (!c->clash_f_zero) cudaMemsetAsync(c->P.work + 1, 0, sizeof(int), c->stream);
+  if (c->mode != CBX_STENCIL_FULL && !c->acc_frc_zero)
     cudaMemsetAsync(c->P.frc, 0, 3 * c->S * sizeof(double), c->stream);
+  c->acc_frc_zero = false;
   if (!c->clash_f_zero) launch_clash_zero(c->P, 1, c->stream);
   c->clash_f_zero = false;
   KP q = c->P;
   q.use_mask = c->mask_valid ? 1 : 0;
-  cudaMemsetAsync(c->P.part_pair, 0, c->P.n_part * sizeof(double), c->stream);
   ev_mark(c, 6);  // the force kernel alone (roofline of the dominant kernel)
   const bool fused = launch_force(q, c->mode, c->stream);
   ev_mark(c, 7);
@@ -408,7 +415,9 @@ void seq_step(cbx_ctx* c) {
   }
   c->mask_valid = false;
   ev_mark(c, 0);
-  launch_kick_drift(c->P, 1, c->stream);
+  const bool zacc = c->mode != CBX_STENCIL_FULL;  // single box: no remote halo sites
+  launch_kick_drift(c->P, 1, c->stream, zacc ? 1 : 0);
+  c->acc_rho_zero = c->acc_frc_zero = zacc;
   launch_rehash(c->P, c->stream);
   c->launches += 3;
   seq_fill_ghosts(c, true);

@@ -165,6 +165,14 @@ __device__ __forceinline__ double block_max(double v, double* sh) {
 }
 
 __device__ __forceinline__ void set_error(DevStatus* st, int code) { atomicCAS(&st->err, 0, code); }
+
+// zero the pair-energy partials no block of this launch writes (entries
+// [written, n_pair_part)), so the finalize sums a fixed range without a
+// memset before every force pass
+__device__ __forceinline__ void zero_pair_tail(const KP& P, int written) {
+  if (blockIdx.x == 0)
+    for (int i = written + threadIdx.x; i < P.n_pair_part; i += blockDim.x) P.part_pair[i] = 0.0;
+}
 #endif
 
 // device entry points (launch wrappers), implemented in the .cu files
@@ -174,7 +182,8 @@ void launch_clash_density(const KP& P, cudaStream_t s);
 void launch_embed(const KP& P, cudaStream_t s, bool literal = false);
 bool launch_force(const KP& P, int mode, cudaStream_t s);
 void launch_clash_force(const KP& P, cudaStream_t s);
-void launch_kick_drift(const KP& P, int move, cudaStream_t s);
+// zero_acc: clear the interior sites' rho / force accumulators as well
+void launch_kick_drift(const KP& P, int move, cudaStream_t s, int zero_acc = 0);
 void launch_clash_zero(const KP& P, int what, cudaStream_t s);
 void launch_rehash(const KP& P, cudaStream_t s);
 void launch_ghost_fill(const KP& P, cudaStream_t s);

@@ -231,6 +231,7 @@ __global__ void __launch_bounds__(256) k_density(KP P) {
 // -------------------------------------------------------------- force pass
 template <bool FULL>
 __global__ void __launch_bounds__(256) k_force(KP P) {
+  zero_pair_tail(P, gridDim.x);
   __shared__ double sh[8];
   double e = 0.0;
   int par;
@@ -335,6 +336,7 @@ __global__ void __launch_bounds__(256) k_embed(KP P, int nsb, int literal) {
     }
     return;
   }
+  if (blockIdx.x == 0 && threadIdx.x == 0) P.work[1] = 0;  // the force pass's brick queue
   __shared__ double sh[8];
   double e = 0.0;
   const bool ok = !P.st->err && !P.st->n_ovl;

@@ -1090,6 +1090,7 @@ __global__ void __launch_bounds__(128, MINB) k_density_fast(KP P, int nsb) {
 
 template <bool FULL, int B>
 __global__ void __launch_bounds__(128, 4) k_force_fast(KP P) {
+  zero_pair_tail(P, gridDim.x * blockDim.x / 32);
   if (P.st->err || P.st->n_ovl) return;
   const int nb = brick_count(P.G);
   double e = 0.0;
@@ -1113,6 +1114,7 @@ constexpr int kLeanTabRecords = 3300;  // x 64 B = 211,200 B
 
 template <bool FULL, int NT>
 __global__ void __launch_bounds__(NT, 1) k_force_lean_smem(KP P, int nsb) {
+  zero_pair_tail(P, nsb * blockDim.x / 32);
   if (blockIdx.x >= nsb) {
     clash_body<1>(P, blockIdx.x - nsb, gridDim.x - nsb);
     return;
@@ -1156,6 +1158,7 @@ __global__ void __launch_bounds__(NT, 1) k_force_lean_smem(KP P, int nsb) {
 
 template <bool FULL, int MINB>
 __global__ void __launch_bounds__(128, MINB) k_force_lean(KP P, int nsb) {
+  zero_pair_tail(P, nsb * blockDim.x / 32);
   if (blockIdx.x >= nsb) {
     clash_body<1>(P, blockIdx.x - nsb, gridDim.x - nsb);
     return;
@@ -1184,6 +1187,7 @@ __global__ void __launch_bounds__(128, MINB) k_force_lean(KP P, int nsb) {
 
 template <bool FULL>
 __global__ void __launch_bounds__(128, 4) k_force_pipe(KP P, int nsb) {
+  zero_pair_tail(P, nsb * blockDim.x / 32);
   if (blockIdx.x >= nsb) {
     clash_body<1>(P, blockIdx.x - nsb, gridDim.x - nsb);
     return;
@@ -1212,6 +1216,7 @@ __global__ void __launch_bounds__(128, 4) k_force_pipe(KP P, int nsb) {
 
 template <bool FULL, int B>
 __global__ void __launch_bounds__(128, 4) k_force_union(KP P) {
+  zero_pair_tail(P, gridDim.x * blockDim.x / 32);
   if (P.st->err || P.st->n_ovl) return;
   // the masked offsets (<= kMaskBits per parity) in shared memory: the
   // per-pair offset load is an LDS instead of an indexed constant load
@@ -1239,6 +1244,7 @@ __global__ void __launch_bounds__(128, 4) k_force_union(KP P) {
 
 template <bool FULL>
 __global__ void __launch_bounds__(128, 5) k_force_mask(KP P) {
+  zero_pair_tail(P, gridDim.x * blockDim.x / 32);
   if (P.st->err || P.st->n_ovl) return;
   const int nb = brick_count(P.G);
   double e = 0.0;
@@ -1396,6 +1402,7 @@ __device__ __forceinline__ int next_brick_group(int* ctr, int group, volatile in
 
 template <bool FULL>
 __global__ void __launch_bounds__(512, 1) k_force_smtab(KP P) {
+  zero_pair_tail(P, gridDim.x * blockDim.x / 32);
   if (P.st->err || P.st->n_ovl) return;
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ int s_slot[4];

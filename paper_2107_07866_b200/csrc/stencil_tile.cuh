@@ -271,6 +271,7 @@ __global__ void __launch_bounds__(256, 2) k_density_tile(KP P) {
 
 template <bool FULL>
 __global__ void __launch_bounds__(256, 2) k_force_tile(KP P) {
+  zero_pair_tail(P, gridDim.x * blockDim.x / 32);
   if (P.st->err || P.st->n_ovl) return;
   extern __shared__ __align__(16) unsigned char smem[];
   TileRef tl{reinterpret_cast<double4*>(smem),

@@ -38,7 +38,10 @@ __device__ __forceinline__ bool site_is_ghost(long long id, const Geo& G) {
 // -------------------------------------------------- kick, drift, wrap, evict
 __device__ void clash_kick_drift_body(const KP& P, int move, int blk, int nblk);
 
-__global__ void __launch_bounds__(256) k_kick_drift(KP P, int move, int nsb) {
+// zero_acc: also clear the site's rho / force accumulators once the half
+// kick has read the force (the density and force passes of this step add
+// into them; replaces two full-array memsets)
+__global__ void __launch_bounds__(256) k_kick_drift(KP P, int move, int nsb, int zero_acc) {
   if (P.st->err) return;
   if (blockIdx.x >= nsb) {  // the clash records (fused k_clash_kick_drift)
     clash_kick_drift_body(P, move, blockIdx.x - nsb, gridDim.x - nsb);
@@ -48,8 +51,16 @@ __global__ void __launch_bounds__(256) k_kick_drift(KP P, int move, int nsb) {
   long long d;
   if (!map_site(P, par, d)) return;
   double4 p = P.pdf[d];
-  if (p.x >= kVacantTest) return;
   const long long S = P.S;
+  if (p.x >= kVacantTest) {
+    if (zero_acc) {
+      P.rho[d] = 0.0;
+      P.frc[d] = 0.0;
+      P.frc[S + d] = 0.0;
+      P.frc[2 * S + d] = 0.0;
+    }
+    return;
+  }
   double vx = P.vel[d], vy = P.vel[S + d], vz = P.vel[2 * S + d];
   if (move) {
     const double dt = P.st->dt_next;
@@ -63,6 +74,12 @@ __global__ void __launch_bounds__(256) k_kick_drift(KP P, int move, int nsb) {
     P.vel[d] = vx;
     P.vel[S + d] = vy;
     P.vel[2 * S + d] = vz;
+  }
+  if (zero_acc) {
+    P.rho[d] = 0.0;
+    P.frc[d] = 0.0;
+    P.frc[S + d] = 0.0;
+    P.frc[2 * S + d] = 0.0;
   }
   if (!wrap_position(p.x, p.y, p.z, P.G)) {
     set_error(P.st, CBX_LOGIC);
@@ -443,6 +460,7 @@ __device__ __forceinline__ int image_count(long long id, const Geo& G) {
 }
 
 __global__ void __launch_bounds__(1024) k_clash_images(KP P, int zero_rho) {
+  if (zero_rho && threadIdx.x == 0) P.work[0] = 0;  // the density pass's brick queue
   if (P.st->err) return;
   const int n = P.st->n_clash;
   const int n_rem = P.st->n_remote;
@@ -753,9 +771,9 @@ __global__ void __launch_bounds__(256) k_count_defects(KP P, unsigned long long*
 
 // -------------------------------------------------------------- launchers
 constexpr int kClashBlocks = 8;  // blocks of 256 threads for clash-record sweeps
-void launch_kick_drift(const KP& P, int move, cudaStream_t s) {
+void launch_kick_drift(const KP& P, int move, cudaStream_t s, int zero_acc) {
   const int nsb = eam_blocks(P);
-  k_kick_drift<<<nsb + kClashBlocks, 256, 0, s>>>(P, move, nsb);
+  k_kick_drift<<<nsb + kClashBlocks, 256, 0, s>>>(P, move, nsb, zero_acc);
 }
 void launch_rehash(const KP& P, cudaStream_t s) { k_rehash<<<1, 1024, 0, s>>>(P); }
 void launch_ghost_fill(const KP& P, cudaStream_t s) {
