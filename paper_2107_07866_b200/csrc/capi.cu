@@ -80,6 +80,7 @@ struct cbx_ctx {
   size_t p2p_bytes = 0;
   std::vector<void*> p2p_opened;
   P2PLinks links{};
+  P2PLinks* d_links = nullptr;  // device copy (the finalize kernel's reduction)
   bool p2p = false;
 
   template <class T>
@@ -350,12 +351,36 @@ void slab_reduce(cbx_ctx* c, bool energies, bool kinetic) {
 
 void memset_field(cbx_ctx* c, int* field) { cudaMemsetAsync(field, 0, sizeof(int), c->stream); }
 
+// end of a slab phase: (kick2 when kick >= 0) + finalize + cross-rank
+// reduction -- on P2P the reduction is the tail of the finalize kernel
+void slab_finish(cbx_ctx* c, int kick, int stepping, int energies) {
+  if (c->p2p) {
+    if (kick >= 0) {
+      launch_kick2(c->P, kick, -2, 0, c->stream);
+      c->launches += 2;
+    }
+    launch_finalize(c->P, stepping, energies, c->stream, c->d_links);
+    c->launches += 1;
+    return;
+  }
+  if (kick >= 0) {
+    launch_kick2(c->P, kick, stepping, energies, c->stream);
+    c->launches += 3;
+  } else {
+    launch_finalize(c->P, stepping, energies, c->stream);
+    c->launches += 1;
+  }
+  slab_reduce(c, energies != 0, stepping >= 0);
+}
+
 // one step of a slab rank: the single-box sequence with the five exchanges
 void seq_slab_step(cbx_ctx* c) {
   c->mask_valid = false;
   ev_mark(c, 0);
   memset_field(c, &c->P.st->n_out);
-  launch_kick_drift(c->P, 1, c->stream);
+  // interior accumulators cleared here, the halo sites' by the POS unpack
+  const bool zacc = c->mode != CBX_STENCIL_FULL;
+  launch_kick_drift(c->P, 1, c->stream, zacc ? 1 : 0);
   slab_exchange(c, 0);  // migrants
   launch_rehash(c->P, c->stream);
   launch_ghost_fill(c->P, c->stream);
@@ -365,6 +390,7 @@ void seq_slab_step(cbx_ctx* c) {
   ev_mark(c, 1);
   launch_clash_images(c->P, c->stream, 1);
   c->clash_rho_zero = true;
+  c->acc_rho_zero = c->acc_frc_zero = zacc;
   c->launches += 1;
   seq_density(c);
   slab_exchange(c, 2);  // density partials (reverse)
@@ -377,9 +403,7 @@ void seq_slab_step(cbx_ctx* c) {
   seq_force(c);
   slab_exchange(c, 4);  // force partials (reverse)
   ev_mark(c, 4);
-  launch_kick2(c->P, 1, 1, 1, c->stream);
-  c->launches += 3;
-  slab_reduce(c, true, true);
+  slab_finish(c, 1, 1, 1);
   ev_mark(c, 5);
 }
 
@@ -402,9 +426,7 @@ void seq_slab_eval(cbx_ctx* c) {
   seq_force(c);
   slab_exchange(c, 4);
   ev_mark(c, 4);
-  launch_finalize(c->P, -1, 1, c->stream);
-  c->launches += 1;
-  slab_reduce(c, true, false);
+  slab_finish(c, -1, -1, 1);
 }
 
 // one velocity-Verlet step, sim.cpp:248-273
@@ -1438,9 +1460,12 @@ CBX_API cbx_status cbx_refresh_forces(cbx_ctx* c) {
 CBX_API cbx_status cbx_measure(cbx_ctx* c) {
   return guarded(c, [&] {
     cudaSetDevice(c->device);
-    launch_kick2(c->P, 0, 0, 0, c->stream);
-    c->launches += 3;
-    if (has_transport(c)) slab_reduce(c, false, true);
+    if (has_transport(c)) {
+      slab_finish(c, 0, 0, 0);
+    } else {
+      launch_kick2(c->P, 0, 0, 0, c->stream);
+      c->launches += 3;
+    }
     sync_status(c);
     raise_device_error(c, false);
   });
@@ -1940,6 +1965,8 @@ CBX_API cbx_status cbx_slab_p2p_init(cbx_ctx* c, const void* handles, long nbyte
     cudaMemset(L.done, 0, 6 * sizeof(unsigned));
     L.rank = c->rank;
     L.nranks = n;
+    c->d_links = c->alloc<P2PLinks>(1);
+    cuda_check(cudaMemcpy(c->d_links, &L, sizeof L, cudaMemcpyHostToDevice), "p2p links");
     cuda_check(cudaDeviceSynchronize(), "p2p init");
     c->p2p = true;
     drop_graph(c);

@@ -191,7 +191,7 @@ void launch_ghost_fill(const KP& P, cudaStream_t s);
 void launch_clash_images(const KP& P, cudaStream_t s, int zero_rho = 0);
 // second half kick; stepping > -2 also runs the finalize (last block)
 void launch_kick2(const KP& P, int kick, int stepping, int energies, cudaStream_t s);
-void launch_finalize(const KP& P, int stepping, int energies, cudaStream_t s);
+
 void launch_count_defects(const KP& P, unsigned long long* out, cudaStream_t s);
 void upload_offsets(const int* half_dev[2], const int half_n[2], const int* full_dev[2],
                     const int full_n[2], const long long* full_flat[2], const int half_nin[2],
@@ -220,6 +220,10 @@ struct P2PLinks {
   int rank, nranks;
 };
 constexpr int kMaxP2PRanks = 8;
+// links (device copy): slab rank on the P2P transport -- the cross-rank
+// reduction runs in the same kernel
+void launch_finalize(const KP& P, int stepping, int energies, cudaStream_t s,
+                     const P2PLinks* links = nullptr);
 void launch_p2p_exchange(const KP& P, const P2PLinks& L, int kind, long long gs_lo,
                          long long gs_hi, int* rem_base, cudaStream_t s);
 void launch_p2p_reduce(const KP& P, const P2PLinks& L, int energies, int kinetic,

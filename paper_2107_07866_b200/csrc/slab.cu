@@ -17,7 +17,11 @@
 //   RHO       halo density partials -> owner (reverse, added via tgt[])
 //   DF        boundary planes' dF -> neighbour's halo
 //   FRC       halo force partials -> owner (reverse)
+#include <algorithm>
+#include <cstdlib>
+
 #include "cbx_device.cuh"
+#include "p2p.cuh"
 
 namespace cbx {
 
@@ -175,6 +179,11 @@ __device__ __forceinline__ void unpack_plane_site(const KP& P, int kind, int fro
   const long long d =
       par * G.NC + (long long)plane_lo_recv(G, kind, from) * G.txy + (q - par * n);
   if (kind == 1) {
+    // a fresh halo site: its rho / force partials of this step start at 0
+    P.rho[d] = 0.0;
+    P.frc[d] = 0.0;
+    P.frc[P.S + d] = 0.0;
+    P.frc[2 * P.S + d] = 0.0;
     double4 p = ldcg(reinterpret_cast<const double4*>(buf) + q);
     if (p.x < kVacantTest) {
       p.z = xadd(p.z, dz);  // periodic image across the global z boundary
@@ -291,18 +300,6 @@ __global__ void k_remote_df(KP P) {
 }
 
 // ------------------------------------------------------ P2P (peer memory)
-__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ unsigned long long global_ns() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
-constexpr unsigned long long kWaitNs = 20ull * 1000000000ull;  // a dead peer, not a slow one
-
 // thread 0 of the block: wait until every flag reaches `epoch` (or time out)
 __device__ bool wait_flags(const KP& P, const unsigned long long* const* flags, int nflags,
                            unsigned long long epoch) {
@@ -330,9 +327,6 @@ __device__ bool wait_flags(const KP& P, const unsigned long long* const* flags, 
 // its stores at GPU scope (bar.sync + fence + arrival counter, the grid-sync
 // pattern); the last block's fence.sc.sys is cumulative over everything it
 // has observed, then the flags are plain system-scope stores.
-__device__ __forceinline__ void st_relaxed_sys(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
 __device__ void signal_peers(const P2PLinks& L, int kind) {
   __syncthreads();
   if (threadIdx.x != 0) return;
@@ -371,6 +365,74 @@ __global__ void __launch_bounds__(256) k_p2p_send(KP P, P2PLinks L, int kind) {
   signal_peers(L, kind);
 }
 
+// one exchange in one kernel: pack into the neighbours' memory, raise the
+// flags (last block), wait for the neighbours' packets, unpack.  The grid is
+// capped at the co-resident block count (the waiting blocks must not keep
+// blocks of the same launch from running their pack).
+__global__ void __launch_bounds__(256) k_p2p_xchg(KP P, P2PLinks L, int kind, long long gs_lo,
+                                                  long long gs_hi, int* rem_base) {
+  unsigned char* dn = L.dst[kind][0];
+  unsigned char* up = L.dst[kind][1];
+  if (kind == 0) {
+    if (blockIdx.x == 0) pack_migrants_block(P, -1, dn, L.msg[0]);
+    else if (blockIdx.x == 1) pack_migrants_block(P, +1, up, L.msg[0]);
+  } else {
+    const long long n2 = 2ll * P.G.g * P.G.txy;
+    for (long long q = blockIdx.x * blockDim.x + threadIdx.x; q < 2 * n2;
+         q += gridDim.x * blockDim.x) {
+      const bool hi = q >= n2;
+      pack_plane_site(P, kind, hi ? 1 : -1, hi ? up : dn, hi ? q - n2 : q);
+    }
+    if ((kind == 1 || kind == 3) && threadIdx.x == 0 && blockIdx.x < 2) {
+      const long long pb = L.plane_bytes[kind];
+      unsigned char* b = blockIdx.x == 0 ? dn : up;
+      pack_clash_thread(P, kind, blockIdx.x == 0 ? -1 : 1, b + pb, L.msg[kind] - pb);
+    }
+  }
+  // arrival + flags (signal_peers without the early return)
+  __shared__ unsigned long long s_epoch;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    // read the epoch before arriving: the last block bumps it only after
+    // every block's arrival, so all blocks see the same value
+    const unsigned long long e0 = *(volatile unsigned long long*)&L.epoch[kind];
+    __threadfence();
+    const unsigned t = atomicAdd(&L.done[kind], 1u);
+    if (t == gridDim.x - 1) {
+      __threadfence();
+      L.done[kind] = 0;
+      L.epoch[kind] = e0 + 1;
+      __threadfence_system();
+      st_relaxed_sys(L.flag_dst[kind][0], e0 + 1);
+      st_relaxed_sys(L.flag_dst[kind][1], e0 + 1);
+    }
+    s_epoch = e0 + 1;
+  }
+  __syncthreads();
+  const unsigned long long* fl[2] = {L.flag_src[kind][0], L.flag_src[kind][1]};
+  if (!wait_flags(P, fl, 2, s_epoch)) return;
+  const unsigned char* lo = L.src[kind][0];
+  const unsigned char* hi = L.src[kind][1];
+  if (kind == 0) {
+    const long long i0 = blockIdx.x * blockDim.x + threadIdx.x, st = gridDim.x * blockDim.x;
+    unpack_migrants(P, lo, i0, st);
+    unpack_migrants(P, hi, i0, st);
+    return;
+  }
+  const long long n2 = 2ll * P.G.g * P.G.txy;
+  const double dz_lo = xmul((double)gs_lo, P.G.glz), dz_hi = xmul((double)gs_hi, P.G.glz);
+  for (long long q = blockIdx.x * blockDim.x + threadIdx.x; q < 2 * n2;
+       q += gridDim.x * blockDim.x) {
+    const bool h = q >= n2;
+    unpack_plane_site(P, kind, h ? 1 : -1, h ? hi : lo, h ? dz_hi : dz_lo, h ? q - n2 : q);
+  }
+  if ((kind == 1 || kind == 3) && blockIdx.x == 0 && threadIdx.x == 0) {
+    const long long pb = L.plane_bytes[kind];
+    unpack_clash_thread(P, kind, lo + pb, gs_lo, rem_base + 0);
+    unpack_clash_thread(P, kind, hi + pb, gs_hi, rem_base + 1);
+  }
+}
+
 // wait for both neighbours' packets of this exchange, then unpack them
 __global__ void __launch_bounds__(256) k_p2p_recv(KP P, P2PLinks L, int kind, long long gs_lo,
                                                   long long gs_hi, int* rem_base) {
@@ -398,51 +460,8 @@ __global__ void __launch_bounds__(256) k_p2p_recv(KP P, P2PLinks L, int kind, lo
   }
 }
 
-// StepState sums over all ranks, deterministic: every rank stores its
-// {pair, embedding, kinetic, max_speed} into slot `rank` of every rank,
-// then sums the slots in rank order
 __global__ void k_p2p_reduce(KP P, P2PLinks L, int energies, int kinetic) {
-  if (threadIdx.x != 0) return;
-  DevStatus* st = P.st;
-  const unsigned long long e = L.epoch[5] + 1;
-  L.epoch[5] = e;
-  const double v[4] = {st->pair, st->embedding, st->kinetic, st->max_speed};
-  for (int q = 0; q < L.nranks; ++q) {
-    double* slot = L.red_dst[q] + 4 * L.rank;
-    for (int i = 0; i < 4; ++i) slot[i] = v[i];
-  }
-  __threadfence_system();
-  for (int q = 0; q < L.nranks; ++q) st_relaxed_sys(L.red_flag_dst[q] + L.rank, e);
-  const unsigned long long t0 = global_ns();
-  for (int q = 0; q < L.nranks; ++q)
-    while (ld_acquire_sys(L.red_flag_src + q) < e) {
-      if (global_ns() - t0 > kWaitNs) {
-        set_error(st, CBX_RUNTIME);
-        return;
-      }
-      __nanosleep(100);
-    }
-  double a = 0.0, b = 0.0, k = 0.0, m = 0.0;
-  for (int q = 0; q < L.nranks; ++q) {
-    const double* s = L.red_src + 4 * q;
-    a += __ldcg(s + 0);
-    b += __ldcg(s + 1);
-    k += __ldcg(s + 2);
-    m = fmax(m, __ldcg(s + 3));
-  }
-  if (energies) {
-    st->pair = a;
-    st->embedding = b;
-  }
-  if (kinetic) {
-    st->kinetic = k;
-    st->max_speed = m;
-    if (st->adaptive) {  // adaptive_dt on the global max speed, sim.cpp:94-98
-      double dt = st->dt_max;
-      if (m > 0.0) dt = fmin(dt, xdiv(st->max_disp, m));
-      st->dt_next = fmax(dt, 1e-7);
-    }
-  }
+  if (threadIdx.x == 0) p2p_reduce_thread(P, L, energies, kinetic);
 }
 
 // ---------------------------------------------------------------- launchers
@@ -507,6 +526,23 @@ void launch_remote_df(const KP& P, cudaStream_t s) { k_remote_df<<<8, 256, 0, s>
 
 void launch_p2p_exchange(const KP& P, const P2PLinks& L, int kind, long long gs_lo,
                          long long gs_hi, int* rem_base, cudaStream_t s) {
+  static const int fused = [] {
+    const char* e = getenv("CBX_P2P_SPLIT");
+    return e ? !atoi(e) : 1;
+  }();
+  if (fused) {
+    static int cap = 0;
+    if (!cap) {  // co-resident blocks of the fused kernel
+      int per_sm = 0, sms = 148, dev = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_p2p_xchg, 256, 0);
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      cap = std::max(2, std::min(per_sm, 2) * sms);
+    }
+    const int grid = kind == 0 ? 2 : std::min(plane_grid(P, 2), cap);
+    k_p2p_xchg<<<grid, 256, 0, s>>>(P, L, kind, gs_lo, gs_hi, rem_base);
+    return;
+  }
   const int grid = kind == 0 ? 2 : plane_grid(P, 2);
   k_p2p_send<<<grid, 256, 0, s>>>(P, L, kind);
   k_p2p_recv<<<kind == 0 ? 8 : plane_grid(P, 2), 256, 0, s>>>(P, L, kind, gs_lo, gs_hi,

@@ -1035,15 +1035,15 @@ __device__ __forceinline__ int next_brick_group8(int* ctr, int group, volatile i
 // density pass with the upper rho-spline window in shared memory (32-byte
 // records): 512 threads = 4 groups of 4 warps, one CTA per SM
 constexpr int kDensTabRecords = 3300;  // x 32 B = 105,600 B
-template <bool FULL, int B>
-__global__ void __launch_bounds__(512, 1) k_density_smem(KP P, int nsb) {
+template <bool FULL, int B, int NT>
+__global__ void __launch_bounds__(NT, 1) k_density_smem(KP P, int nsb) {
   if (blockIdx.x >= nsb) {
     clash_body<0>(P, blockIdx.x - nsb, gridDim.x - nsb);
     return;
   }
   if (P.st->err) return;
   extern __shared__ __align__(16) unsigned char smem_tab[];
-  __shared__ int s_slot[4];
+  __shared__ int s_slot[NT / 128];
   double2* T = reinterpret_cast<double2*>(smem_tab);
   const int nseg = P.fd.nseg;
   const int seg_lo = max(0, nseg + 1 - kDensTabRecords);
@@ -1492,26 +1492,36 @@ int fast_grid(const KP& P, bool force, int mode) {
 }
 
 bool launch_density_fast(const KP& P, int mode, int grid, cudaStream_t s) {
-  static const int dsm = [] {
+  static const int dsm = [] {  // 2: lean, spline window in shared memory (default)
     const char* e = getenv("CBX_DENSITY_SMEM");
-    return e ? atoi(e) : 0;
+    return e ? atoi(e) : 2;
   }();
   if (dsm) {
     const size_t bytes = (size_t)kDensTabRecords * 32;
     static bool attr = false;
     if (!attr) {
-      cudaFuncSetAttribute(k_density_smem<false, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)bytes);
-      cudaFuncSetAttribute(k_density_smem<true, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)bytes);
+      cudaFuncSetAttribute(k_density_smem<false, 4, 512>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+      cudaFuncSetAttribute(k_density_smem<true, 4, 512>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+      cudaFuncSetAttribute(k_density_smem<false, 1, 1024>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+      cudaFuncSetAttribute(k_density_smem<true, 1, 1024>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
       attr = true;
     }
     int sms = 148, dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int g = max(1, min(sms, (brick_count(P.G) + 3) / 4));
-    if (mode) k_density_smem<true, 4><<<g, 512, bytes, s>>>(P, g);
-    else k_density_smem<false, 4><<<g + 8, 512, bytes, s>>>(P, g);
+    if (dsm == 2) {  // lean: one candidate per iteration, 1024 threads
+      const int g8 = max(1, min(sms, (brick_count(P.G) + 7) / 8));
+      if (mode) k_density_smem<true, 1, 1024><<<g8, 1024, bytes, s>>>(P, g8);
+      else k_density_smem<false, 1, 1024><<<g8 + 4, 1024, bytes, s>>>(P, g8);
+    } else {
+      if (mode) k_density_smem<true, 4, 512><<<g, 512, bytes, s>>>(P, g);
+      else k_density_smem<false, 4, 512><<<g + 8, 512, bytes, s>>>(P, g);
+    }
     return !mode;
   }
   static const int batch = [] {

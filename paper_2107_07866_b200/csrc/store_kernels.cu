@@ -20,6 +20,7 @@
 #include <cstdlib>
 
 #include "cbx_device.cuh"
+#include "p2p.cuh"
 
 namespace cbx {
 
@@ -742,9 +743,18 @@ __device__ void finalize_body(const KP& P, int stepping, int energies, const dou
   }
 }
 
+// L (device copy, slab ranks on the P2P transport): the cross-rank
+// StepState reduction follows in the same kernel -- also after a device
+// error, so the ranks stay in step
 __global__ void __launch_bounds__(1024) k_finalize(KP P, int stepping, int energies,
-                                                   int n_pairp, int n_emb, int n_ke) {
+                                                   int n_pairp, int n_emb, int n_ke,
+                                                   const P2PLinks* L) {
   finalize_body<1024>(P, stepping, energies, P.part_emb, n_emb, P.part_pair, n_pairp, n_ke);
+  if (L) {
+    __syncthreads();
+    __threadfence();
+    if (threadIdx.x == 0) p2p_reduce_thread(P, *L, energies, stepping >= 0);
+  }
 }
 
 // ---------------------------------------------------------- count_defects
@@ -791,9 +801,10 @@ void launch_kick2(const KP& P, int kick, int stepping, int energies, cudaStream_
   k_kick2<<<nsb + kClashBlocks, 256, 0, s>>>(P, kick, nsb);
   if (stepping > -2) launch_finalize(P, stepping, energies, s);
 }
-void launch_finalize(const KP& P, int stepping, int energies, cudaStream_t s) {
+void launch_finalize(const KP& P, int stepping, int energies, cudaStream_t s,
+                     const P2PLinks* links) {
   k_finalize<<<1, 1024, 0, s>>>(P, stepping, energies, P.n_pair_part, embed_grid(P),
-                                kick_grid(P));
+                                kick_grid(P), links);
 }
 void launch_count_defects(const KP& P, unsigned long long* out, cudaStream_t s) {
   k_count_defects<<<eam_blocks(P), 256, 0, s>>>(P, out);

@@ -94,12 +94,16 @@ class SlabRank(DeviceStore):
 
     @staticmethod
     def nccl_unique_id() -> bytes:
+        # torch first: its libnccl.so.2 (newer) must be the one the process maps;
+        # the library dlopens by soname and then shares it
+        import torch  # noqa: F401
         b = C.create_string_buffer(128)
         check(_lib.load().cbx_nccl_unique_id(b, 128))
         return b.raw
 
     def init_comm(self, uid: bytes):
         """collective: every rank of the decomposition passes rank 0's id"""
+        import torch  # noqa: F401  (see nccl_unique_id)
         b = C.create_string_buffer(uid, 128)
         self._check(self.lib.cbx_slab_comm_init(self.h, b, 128))
 
