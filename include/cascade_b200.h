@@ -196,6 +196,44 @@ CBX_API cbx_status cbx_bench_steps(cbx_ctx* ctx, double dt, long nsteps, double 
 CBX_API cbx_status cbx_fp64_peak(int device, double* tflops, double* sm_mhz);
 CBX_API cbx_status cbx_bench_phases(cbx_ctx* ctx, int on);
 
+/* ---- the run loop and its outputs ------------------------
+ * Simulation::run (sim.cpp:289-360): equilibrate (with the thermostat), inject
+ * the PKA, step with the adaptive dt until the step or time cap, sampling
+ * Wigner-Seitz defects and writing snapshots at the configured intervals;
+ * then the defect time series and the final snapshot.  On a failed step the
+ * post-mortem snapshot and the series so far are written and the error is
+ * returned.  Files are byte-compatible with the reference's writers
+ * (analysis.cpp:66-116).  Single-box contexts. */
+typedef struct {
+  long steps;                      /* step cap, 0 = none */
+  double max_time;                 /* ps cap, 0 = none */
+  long equilibration_steps;        /* thermal steps before the PKA */
+  int thermostat_enabled;          /* ThermostatSpec (config.h:16-20) */
+  long thermostat_interval;
+  long thermostat_boundary_cells;  /* 0 = whole box */
+  double temperature;              /* thermostat target, K */
+  const char* timeseries;          /* defect CSV path; NULL / "" = skip */
+  const char* snapshot_prefix;     /* XYZ prefix; NULL / "" = skip */
+  long snapshot_interval;          /* 0 = only the final snapshot */
+  long defect_interval;            /* 0 = ends only */
+  long pka_site[3];                /* corner-sublattice cell, -1 = box centre */
+  double pka_energy_kev;           /* 0 = no PKA */
+  long pka_dir[3];
+} cbx_run_spec;
+
+/* log_path: NULL / "" = no log, "-" = stdout (sim.cpp:294-300 line format) */
+CBX_API cbx_status cbx_run(cbx_ctx* ctx, const cbx_run_spec* spec, const char* log_path);
+/* the defect series of the last run (sim.h:54): returns its length; t and
+ * defects (3 per sample: vacancies, interstitials, Frenkel pairs) may be NULL */
+CBX_API long cbx_run_series(cbx_ctx* ctx, double* t, long* defects);
+/* thermostat_rescale (sim.cpp:188-221) toward `temperature` in the band of
+ * `boundary_cells` cells at the faces (0 = whole box); then measure */
+CBX_API cbx_status cbx_thermostat_rescale(cbx_ctx* ctx, double temperature, long boundary_cells);
+/* write_snapshot / write_timeseries (analysis.cpp:77-116) */
+CBX_API cbx_status cbx_write_snapshot(cbx_ctx* ctx, const char* path, double t_ps);
+CBX_API cbx_status cbx_write_timeseries(const char* path, long n, const double* t,
+                                        const long* defects);
+
 /* ---- z-slab domain decomposition (multi-GPU) ------------- */
 /* rank r of n owns global interior z planes [r*bz/n, (r+1)*bz/n) of the
  * global box; positions, hashes and keys stay in the global frame.  A step

@@ -143,6 +143,29 @@ class Engine {
     inter = o[1];
     fp = o[2];
   }
+  // Simulation::run and its outputs (sim.cpp:188-360, analysis.cpp:66-116)
+  void thermostat_rescale(double temperature, long boundary_cells = 0) {
+    check(cbx_thermostat_rescale(c_, temperature, boundary_cells), c_);
+  }
+  void write_snapshot(const std::string& path, double t_ps) {
+    check(cbx_write_snapshot(c_, path.c_str(), t_ps), c_);
+  }
+  void run(const cbx_run_spec& spec, const std::string& log_path = "") {
+    check(cbx_run(c_, &spec, log_path.c_str()), c_);
+  }
+  struct DefectSample {
+    double t_ps;
+    long vacancies, interstitials, frenkel_pairs;
+  };
+  std::vector<DefectSample> series() const {
+    const long n = cbx_run_series(c_, nullptr, nullptr);
+    std::vector<double> t(n);
+    std::vector<long> d(3 * n);
+    cbx_run_series(c_, t.data(), d.data());
+    std::vector<DefectSample> out(n);
+    for (long i = 0; i < n; ++i) out[i] = {t[i], d[3 * i], d[3 * i + 1], d[3 * i + 2]};
+    return out;
+  }
   cbx_ctx* raw() { return c_; }
 
  private:

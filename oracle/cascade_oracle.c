@@ -90,6 +90,10 @@ struct orc_ctx {
   long nghost_ids;
   orc_state st;
   char err[512];
+  /* defect series of the last orc_run (sim.h:69, series_) */
+  double* ser_t;
+  long* ser_d;
+  long nser, capser;
 };
 
 static char g_create_err[512];
@@ -1262,6 +1266,7 @@ bad:
 }
 
 void orc_destroy(orc_ctx* c) {
+  if (c) { free(c->ser_t); free(c->ser_d); }
   if (!c) return;
   free(c->pot.embed.seg); free(c->pot.zr.seg); free(c->pot.dens.seg);
   free(c->idx.ef); free(c->idx.of); free(c->idx.eh); free(c->idx.oh);
@@ -1461,4 +1466,222 @@ int orc_write_synthetic_table(const char* path, long nrho, long nr) {
   write_block(f, v, nr);
   free(v);
   return fclose(f) == 0 ? ORC_OK : ORC_RUNTIME;
+}
+
+
+/* ------------------------------------------------------------- run loop */
+static int in_band(const orc_ctx* c, int64_t id, long band) { /* sim.cpp:190-197 */
+  if (band <= 0) return 1;
+  const box_t* b = &c->box;
+  const int64_t tx2 = 2 * total_x(b), ty = total_y(b);
+  const long cz = (long)(id / (tx2 * ty)), cy = (long)((id / tx2) % ty), x = (long)(id % tx2);
+  const long cx = x >> 1, g = b->g;
+  return cx - g < band || (g + b->bx - 1) - cx < band || cy - g < band ||
+         (g + b->by - 1) - cy < band || cz - g < band || (g + b->bz - 1) - cz < band;
+}
+
+int orc_thermostat_rescale(orc_ctx* c) { /* sim.cpp:188-221 */
+  const long band = c->cfg.thermostat_boundary_cells;
+  const box_t* b = &c->box;
+  double sum_v2 = 0.0;
+  long n = 0;
+  FOR_INTERIOR(b, id) {
+    const rec_t* a = &c->slots[id];
+    if (!a->valid || !in_band(c, id, band)) continue;
+    sum_v2 += norm2(a->vel);
+    ++n;
+  }
+  for (int i = 0; i < c->nbk; ++i) {
+    if (is_ghost_id(c->bk[i].key, b) || !in_band(c, c->bk[i].key, band)) continue;
+    for (int j = 0; j < c->bk[i].n; ++j) {
+      sum_v2 += norm2(c->bk[i].r[j].vel);
+      ++n;
+    }
+  }
+  const double measured =
+      n > 0 ? c->pot.mass * sum_v2 * MV2_TO_EV / (3.0 * (double)n * BOLTZMANN_EV) : 0.0;
+  if (!(measured > 0.0)) {
+    fprintf(stderr, "thermostat: measured temperature is zero, skipping\n");
+    return ORC_OK;
+  }
+  const double f = sqrt(c->cfg.temperature / measured);
+  FOR_INTERIOR(b, id) {
+    rec_t* a = &c->slots[id];
+    if (!a->valid || !in_band(c, id, band)) continue;
+    a->vel.x *= f; a->vel.y *= f; a->vel.z *= f;
+  }
+  for (int i = 0; i < c->nbk; ++i) {
+    if (is_ghost_id(c->bk[i].key, b) || !in_band(c, c->bk[i].key, band)) continue;
+    for (int j = 0; j < c->bk[i].n; ++j) {
+      rec_t* a = &c->bk[i].r[j];
+      a->vel.x *= f; a->vel.y *= f; a->vel.z *= f;
+    }
+  }
+  return orc_measure(c);
+}
+
+static const char* const k_symbols[] = { /* analysis.cpp:11-19 */
+    "X",  "H",  "He", "Li", "Be", "B",  "C",  "N",  "O",  "F",  "Ne", "Na", "Mg", "Al", "Si",
+    "P",  "S",  "Cl", "Ar", "K",  "Ca", "Sc", "Ti", "V",  "Cr", "Mn", "Fe", "Co", "Ni", "Cu",
+    "Zn", "Ga", "Ge", "As", "Se", "Br", "Kr", "Rb", "Sr", "Y",  "Zr", "Nb", "Mo", "Tc", "Ru",
+    "Rh", "Pd", "Ag", "Cd", "In", "Sn", "Sb", "Te", "I",  "Xe", "Cs", "Ba", "La", "Ce", "Pr",
+    "Nd", "Pm", "Sm", "Eu", "Gd", "Tb", "Dy", "Ho", "Er", "Tm", "Yb", "Lu", "Hf", "Ta", "W",
+    "Re", "Os", "Ir", "Pt", "Au", "Hg", "Tl", "Pb", "Bi", "Po", "At", "Rn", "Fr", "Ra", "Ac",
+    "Th", "Pa", "U"};
+
+static const char* symbol_for(unsigned z) {
+  return z < sizeof(k_symbols) / sizeof(k_symbols[0]) ? k_symbols[z] : "X";
+}
+
+static void csv_time(double t, char out[48]) { /* analysis.cpp:66-75 */
+  snprintf(out, 48, "%.9g", t);
+  if (!strpbrk(out, ".eE") && strspn(out, "-0123456789") == strlen(out)) strcat(out, ".0");
+}
+
+int orc_write_snapshot(const orc_ctx* c, const char* path) { /* analysis.cpp:90-116 */
+  const box_t* b = &c->box;
+  const double shift = b->g * b->a0;
+  FILE* f = fopen(path, "w");
+  if (!f) return fail((orc_ctx*)c, ORC_RUNTIME, "cannot open %s for writing", path);
+  char tb[48];
+  csv_time(c->st.t, tb);
+  fprintf(f, "%ld\n", store_atom_count(c));
+  fprintf(f,
+          "Lattice=\"%.10g 0 0 0 %.10g 0 0 0 %.10g\" "
+          "Properties=species:S:1:pos:R:3:tag:I:1 Time=%s\n",
+          b->bx * b->a0, b->by * b->a0, b->bz * b->a0, tb);
+#define EMIT(a)                                                                         \
+  fprintf(f, "%s %.10g %.10g %.10g %llu\n", symbol_for((a)->species), (a)->pos.x - shift, \
+          (a)->pos.y - shift, (a)->pos.z - shift, (unsigned long long)(a)->tag)
+  FOR_INTERIOR(b, id) {
+    if (c->slots[id].valid) EMIT(&c->slots[id]);
+  }
+  for (int i = 0; i < c->nbk; ++i) {
+    if (is_ghost_id(c->bk[i].key, b)) continue;
+    for (int j = 0; j < c->bk[i].n; ++j) EMIT(&c->bk[i].r[j]);
+  }
+#undef EMIT
+  const int bad = ferror(f);
+  fclose(f);
+  return bad ? fail((orc_ctx*)c, ORC_RUNTIME, "write failed: %s", path) : ORC_OK;
+}
+
+int orc_write_timeseries(const char* path, long n, const double* t, const long* d) {
+  FILE* f = fopen(path, "w"); /* analysis.cpp:77-88 */
+  if (!f) return ORC_RUNTIME;
+  fputs("t_ps,vacancies,interstitials,frenkel_pairs\n", f);
+  char tb[48];
+  for (long i = 0; i < n; ++i) {
+    csv_time(t[i], tb);
+    fprintf(f, "%s,%ld,%ld,%ld\n", tb, d[3 * i], d[3 * i + 1], d[3 * i + 2]);
+  }
+  const int bad = ferror(f);
+  fclose(f);
+  return bad ? ORC_RUNTIME : ORC_OK;
+}
+
+static void sample_defects(orc_ctx* c) { /* sim.cpp:275-277 */
+  if (c->nser == c->capser) {
+    c->capser = c->capser ? 2 * c->capser : 64;
+    c->ser_t = (double*)realloc(c->ser_t, c->capser * sizeof(double));
+    c->ser_d = (long*)realloc(c->ser_d, 3 * c->capser * sizeof(long));
+  }
+  c->ser_t[c->nser] = c->st.t;
+  orc_count_defects(c, c->ser_d + 3 * c->nser);
+  ++c->nser;
+}
+
+long orc_series(const orc_ctx* c, double* t, long* d) {
+  if (t) memcpy(t, c->ser_t, c->nser * sizeof(double));
+  if (d) memcpy(d, c->ser_d, 3 * c->nser * sizeof(long));
+  return c->nser;
+}
+
+static int nonempty(const char* s) { return s && s[0]; }
+
+static int snapshot_file(orc_ctx* c, const orc_run_spec* r, const char* suffix) {
+  if (!nonempty(r->snapshot_prefix)) return ORC_OK; /* sim.cpp:279-282 */
+  char path[1024];
+  snprintf(path, sizeof path, "%s%s", r->snapshot_prefix, suffix);
+  return orc_write_snapshot(c, path);
+}
+
+int orc_run(orc_ctx* c, const orc_run_spec* r, const char* log_path) { /* sim.cpp:289-360 */
+  c->cfg.thermostat_boundary_cells = r->thermostat_boundary_cells;
+  FILE* log = NULL;
+  if (nonempty(log_path)) log = strcmp(log_path, "-") == 0 ? stdout : fopen(log_path, "w");
+  c->nser = 0;
+  sample_defects(c);
+  int rc = ORC_OK;
+  if (r->snapshot_interval > 0 && (rc = snapshot_file(c, r, "_000000.xyz"))) goto out;
+#define LOG_LINE()                                                                       \
+  do {                                                                                   \
+    if (log) {                                                                           \
+      char tb_[48];                                                                      \
+      csv_time(c->st.t, tb_);                                                            \
+      const long n_ = store_atom_count(c);                                               \
+      const double T_ = n_ == 0 ? 0.0 : 2.0 * c->st.kinetic / (3.0 * (double)n_ * BOLTZMANN_EV); \
+      fprintf(log, "step %ld  t=%s ps  dt=%.4g  E=%.6f eV  T=%.1f K  FP=%ld\n", c->st.step, \
+              tb_, c->st.dt, c->st.kinetic + c->st.pair + c->st.embedding, T_,             \
+              c->ser_d[3 * (c->nser - 1) + 2]);                                         \
+    }                                                                                    \
+  } while (0)
+#define GUARDED_STEP()                                                                   \
+  do {                                                                                   \
+    rc = orc_step(c, -1.0, 1);                                                           \
+    if (rc) {                                                                            \
+      if (nonempty(r->snapshot_prefix)) {                                                \
+        char pm_[1024];                                                                  \
+        snprintf(pm_, sizeof pm_, "%s_postmortem.xyz", r->snapshot_prefix);              \
+        orc_write_snapshot(c, pm_);                                                      \
+      }                                                                                  \
+      if (nonempty(r->timeseries)) orc_write_timeseries(r->timeseries, c->nser, c->ser_t, c->ser_d); \
+      goto out;                                                                          \
+    }                                                                                    \
+  } while (0)
+  for (long i = 0; i < r->equilibration_steps; ++i) {
+    GUARDED_STEP();
+    if (r->thermostat_enabled && (i + 1) % r->thermostat_interval == 0)
+      orc_thermostat_rescale(c);
+  }
+  if (c->cfg.pka_energy_kev > 0.0 && (rc = orc_inject_pka(c))) goto out;
+  {
+    long done = 0;
+    int sampled_last = 1;
+    for (;;) {
+      const int step_cap = r->steps > 0 && done >= r->steps;
+      const int time_cap = r->max_time > 0.0 && c->st.t >= r->max_time;
+      const int no_budget = r->steps == 0 && r->max_time == 0.0;
+      if (step_cap || time_cap || no_budget) break;
+      GUARDED_STEP();
+      ++done;
+      if (r->thermostat_enabled && done % r->thermostat_interval == 0)
+        orc_thermostat_rescale(c);
+      sampled_last = 0;
+      if (r->defect_interval > 0 && done % r->defect_interval == 0) {
+        sample_defects(c);
+        sampled_last = 1;
+        LOG_LINE();
+      }
+      if (r->snapshot_interval > 0 && done % r->snapshot_interval == 0) {
+        char suffix[32];
+        snprintf(suffix, sizeof suffix, "_%06ld.xyz", done);
+        if ((rc = snapshot_file(c, r, suffix))) goto out;
+      }
+    }
+    if (!sampled_last) {
+      sample_defects(c);
+      LOG_LINE();
+    }
+  }
+  if (nonempty(r->timeseries) &&
+      orc_write_timeseries(r->timeseries, c->nser, c->ser_t, c->ser_d))
+    rc = fail(c, ORC_RUNTIME, "write failed: %s", r->timeseries);
+  if (!rc) rc = snapshot_file(c, r, "_final.xyz");
+#undef LOG_LINE
+#undef GUARDED_STEP
+out:
+  if (log && log != stdout) fclose(log);
+  if (log == stdout) fflush(stdout);
+  return rc;
 }

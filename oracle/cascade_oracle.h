@@ -39,6 +39,7 @@ typedef struct {
   double pka_energy_kev;
   long pka_dir[3];
   double dt_max, max_disp;
+  long thermostat_boundary_cells; /* ThermostatSpec::boundary_cells (config.h:16-20) */
 } orc_config;
 
 /* StepState (sim.h:11-21) */
@@ -114,6 +115,35 @@ int orc_potential_eval(orc_ctx* c, int which, double x, double out[2]);
 /* spline coefficient table dump (spline.h:16-27): which 0 embed, 1 zr, 2 dens.
  * seg may be NULL (query nseg); returns nseg, fills x0/h. */
 long orc_spline(const orc_ctx* c, int which, double* x0, double* h, double* seg);
+
+/* ---- the run loop and its outputs ---------------
+ * the SimConfig fields Simulation::run consumes (config.h:16-53); strings may
+ * be NULL or "" (skip) */
+typedef struct {
+  long steps;               /* step cap, 0 = none */
+  double max_time;          /* ps cap, 0 = none */
+  long equilibration_steps; /* thermal steps before the PKA */
+  int thermostat_enabled;
+  long thermostat_interval;
+  long thermostat_boundary_cells; /* 0 = whole box */
+  const char* timeseries;      /* defect CSV path */
+  const char* snapshot_prefix; /* XYZ prefix */
+  long snapshot_interval;      /* 0 = only the final snapshot */
+  long defect_interval;        /* 0 = ends only */
+} orc_run_spec;
+
+/* thermostat_rescale (sim.cpp:188-221): rescale toward cfg.temperature in
+ * the band cfg.thermostat_boundary_cells (0 = whole box) */
+int orc_thermostat_rescale(orc_ctx* c);
+/* write_snapshot (analysis.cpp:90-116) */
+int orc_write_snapshot(const orc_ctx* c, const char* path);
+/* write_timeseries (analysis.cpp:77-88): n samples, defects as 3n longs */
+int orc_write_timeseries(const char* path, long n, const double* t, const long* defects);
+/* Simulation::run (sim.cpp:289-360); log_path NULL/"" = no log, "-" = stdout.
+ * The ref harness runs a fresh Simulation built from the creation config. */
+int orc_run(orc_ctx* c, const orc_run_spec* spec, const char* log_path);
+/* the defect series of the last run: returns its length; t / defects (3n) may be NULL */
+long orc_series(const orc_ctx* c, double* t, long* defects);
 
 double orc_pka_speed(double energy_ev, double mass_amu);
 double orc_adaptive_dt(double max_speed, double dt_max, double max_disp);

@@ -33,7 +33,26 @@ class OrcConfig(C.Structure):
         ("seed", C.c_ulonglong), ("workers", C.c_int),
         ("pka_site", C.c_long * 3), ("pka_energy_kev", C.c_double), ("pka_dir", C.c_long * 3),
         ("dt_max", C.c_double), ("max_disp", C.c_double),
+        ("thermostat_boundary_cells", C.c_long),
     ]
+
+
+class OrcRunSpec(C.Structure):  # orc_run_spec
+    _fields_ = [
+        ("steps", C.c_long), ("max_time", C.c_double), ("equilibration_steps", C.c_long),
+        ("thermostat_enabled", C.c_int), ("thermostat_interval", C.c_long),
+        ("thermostat_boundary_cells", C.c_long), ("timeseries", C.c_char_p),
+        ("snapshot_prefix", C.c_char_p), ("snapshot_interval", C.c_long),
+        ("defect_interval", C.c_long),
+    ]
+
+
+def run_spec(steps=0, max_time=0.0, equilibration_steps=0, thermostat=False,
+             thermostat_interval=10, boundary_cells=0, timeseries="", snapshot_prefix="",
+             snapshot_interval=0, defect_interval=10) -> OrcRunSpec:
+    return OrcRunSpec(steps, max_time, equilibration_steps, 1 if thermostat else 0,
+                      thermostat_interval, boundary_cells, timeseries.encode(),
+                      snapshot_prefix.encode(), snapshot_interval, defect_interval)
 
 
 class OrcState(C.Structure):
@@ -111,6 +130,12 @@ def _load(kind: str):
     lib.orc_adaptive_dt.argtypes = [D, D, D]
     lib.orc_adaptive_dt.restype = D
     lib.orc_write_synthetic_table.argtypes = [C.c_char_p, C.c_long, C.c_long]
+    lib.orc_thermostat_rescale.argtypes = [P]
+    lib.orc_write_snapshot.argtypes = [P, C.c_char_p]
+    lib.orc_write_timeseries.argtypes = [C.c_char_p, C.c_long, dp, C.POINTER(C.c_long)]
+    lib.orc_run.argtypes = [P, C.POINTER(OrcRunSpec), C.c_char_p]
+    lib.orc_series.argtypes = [P, dp, C.POINTER(C.c_long)]
+    lib.orc_series.restype = C.c_long
     _LIBS[kind] = lib
     return lib
 
@@ -160,7 +185,7 @@ class Sim:
     def __init__(self, potential_path: str, box=(10, 10, 10), a0=0.0, ghost_width=0,
                  temperature=0.0, seed=12345, workers=1, init_lattice=True,
                  pka_site=(-1, -1, -1), pka_energy_kev=0.0, pka_dir=(1, 3, 5),
-                 dt_max=1e-3, max_disp=0.05, kind="oracle"):
+                 dt_max=1e-3, max_disp=0.05, kind="oracle", boundary_cells=0):
         self.kind = kind
         self.lib = _load(kind)
         cfg = OrcConfig()
@@ -171,6 +196,7 @@ class Sim:
         cfg.pka_energy_kev = pka_energy_kev
         cfg.pka_dir[:] = list(pka_dir)
         cfg.dt_max, cfg.max_disp = dt_max, max_disp
+        cfg.thermostat_boundary_cells = boundary_cells
         self.cfg = cfg
         h = self.lib.orc_create(potential_path.encode(), C.byref(cfg), 1 if init_lattice else 0)
         if not h:
@@ -298,6 +324,25 @@ class Sim:
         out = (C.c_long * 3)()
         self.lib.orc_count_defects(self.h, out)
         return tuple(out)
+
+    # run loop (sim.cpp:188-360, analysis.cpp:66-116) -------------------
+    def thermostat_rescale(self):
+        self._check(self.lib.orc_thermostat_rescale(self.h))
+
+    def write_snapshot(self, path: str):
+        self._check(self.lib.orc_write_snapshot(self.h, path.encode()))
+
+    def run(self, spec: OrcRunSpec, log_path: str = ""):
+        self._spec = spec  # keep the strings alive
+        self._check(self.lib.orc_run(self.h, C.byref(spec), log_path.encode()))
+
+    def series(self):
+        n = self.lib.orc_series(self.h, None, None)
+        t = np.zeros(n)
+        d = np.zeros(3 * n, dtype=np.int64)
+        self.lib.orc_series(self.h, t.ctypes.data_as(C.POINTER(C.c_double)),
+                            d.ctypes.data_as(C.POINTER(C.c_long)))
+        return t, d.reshape(n, 3)
 
     def store(self) -> Store:
         n = self.lib.orc_slot_count(self.h)

@@ -7,10 +7,12 @@
 // `--impl reference` / cpu_baseline arm (Simulation::step with a WorkerPool
 // of all host cores).  No product code links it.
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <memory>
 #include <stdexcept>
 #include <string>
+#include <vector>
 
 #include "cascade_oracle.h"
 #include "cascademd/analysis.h"
@@ -23,6 +25,7 @@ using namespace cascademd;
 
 struct orc_ctx {
   orc_config cfg{};
+  std::string pot_path;
   std::unique_ptr<Simulation> sim;  // init_lattice != 0
   // standalone store (init_lattice == 0)
   std::unique_ptr<EamPotential> pot_own;
@@ -83,6 +86,7 @@ SimConfig to_sim_config(const orc_config* cfg) {
   s.pka.dir_z = cfg->pka_dir[2];
   if (cfg->dt_max > 0.0) s.dt_max = cfg->dt_max;
   if (cfg->max_disp > 0.0) s.max_disp = cfg->max_disp;
+  s.thermostat.boundary_cells = cfg->thermostat_boundary_cells;
   return s;
 }
 
@@ -107,6 +111,7 @@ const char* orc_create_error(void) { return g_err.c_str(); }
 orc_ctx* orc_create(const char* path, const orc_config* cfg, int init_lattice) {
   auto c = std::make_unique<orc_ctx>();
   c->cfg = *cfg;
+  c->pot_path = path;
   try {
     EamPotential pot = parse_potential_file(path);
     const SimConfig sc = to_sim_config(cfg);
@@ -355,6 +360,86 @@ int orc_write_synthetic_table(const char* path, long nrho, long nr) {
     return ORC_RUNTIME;
   }
   return ORC_OK;
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------- run loop
+extern "C" {
+
+int orc_thermostat_rescale(orc_ctx* c) {
+  if (!c->sim) {
+    c->err = "thermostat: needs a Simulation-backed context";
+    return ORC_LOGIC;
+  }
+  return guard(c, [&] { c->sim->thermostat_rescale(); });
+}
+
+int orc_write_snapshot(const orc_ctx* c, const char* path) {
+  return guard(const_cast<orc_ctx*>(c), [&] {
+    write_snapshot(path, c->store(), c->sim ? c->sim->state().t : c->st_own.t);
+  });
+}
+
+int orc_write_timeseries(const char* path, long n, const double* t, const long* d) {
+  std::vector<DefectSample> v;
+  for (long i = 0; i < n; ++i) {
+    DefectReport r;
+    r.vacancies = d[3 * i];
+    r.interstitials = d[3 * i + 1];
+    r.frenkel_pairs = d[3 * i + 2];
+    v.push_back(DefectSample{t[i], r});
+  }
+  try {
+    write_timeseries(path, v);
+  } catch (const std::exception&) {
+    return ORC_RUNTIME;
+  }
+  return ORC_OK;
+}
+
+// a fresh Simulation from the creation config plus the run spec (the
+// reference fixes cfg_ at construction), which then replaces the context's
+int orc_run(orc_ctx* c, const orc_run_spec* r, const char* log_path) {
+  return guard(c, [&] {
+    SimConfig sc = to_sim_config(&c->cfg);
+    sc.steps = r->steps;
+    sc.max_time = r->max_time;
+    sc.equilibration_steps = r->equilibration_steps;
+    sc.thermostat.enabled = r->thermostat_enabled != 0;
+    sc.thermostat.interval = r->thermostat_interval;
+    sc.thermostat.boundary_cells = r->thermostat_boundary_cells;
+    sc.output.timeseries = r->timeseries ? r->timeseries : "";
+    sc.output.snapshot_prefix = r->snapshot_prefix ? r->snapshot_prefix : "";
+    sc.output.snapshot_interval = r->snapshot_interval;
+    sc.output.defect_interval = r->defect_interval;
+    c->cfg.thermostat_boundary_cells = r->thermostat_boundary_cells;
+    c->sim = std::make_unique<Simulation>(sc, parse_potential_file(c->pot_path));
+    std::FILE* log = nullptr;
+    if (log_path && log_path[0]) log = std::strcmp(log_path, "-") == 0 ? stdout : std::fopen(log_path, "w");
+    try {
+      c->sim->run(log);
+    } catch (...) {
+      if (log && log != stdout) std::fclose(log);
+      throw;
+    }
+    if (log && log != stdout) std::fclose(log);
+    if (log == stdout) std::fflush(stdout);
+  });
+}
+
+long orc_series(const orc_ctx* c, double* t, long* d) {
+  if (!c->sim) return 0;
+  const auto& s = c->sim->series();
+  for (size_t i = 0; i < s.size(); ++i) {
+    if (t) t[i] = s[i].t_ps;
+    if (d) {
+      d[3 * i] = s[i].defects.vacancies;
+      d[3 * i + 1] = s[i].defects.interstitials;
+      d[3 * i + 2] = s[i].defects.frenkel_pairs;
+    }
+  }
+  return static_cast<long>(s.size());
 }
 
 }  // extern "C"

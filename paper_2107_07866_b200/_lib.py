@@ -81,6 +81,16 @@ class Store(C.Structure):
                 ("clash_ghost", C.c_void_p)]
 
 
+class RunSpec(C.Structure):  # cbx_run_spec
+    _fields_ = [("steps", C.c_long), ("max_time", C.c_double),
+                ("equilibration_steps", C.c_long), ("thermostat_enabled", C.c_int),
+                ("thermostat_interval", C.c_long), ("thermostat_boundary_cells", C.c_long),
+                ("temperature", C.c_double), ("timeseries", C.c_char_p),
+                ("snapshot_prefix", C.c_char_p), ("snapshot_interval", C.c_long),
+                ("defect_interval", C.c_long), ("pka_site", C.c_long * 3),
+                ("pka_energy_kev", C.c_double), ("pka_dir", C.c_long * 3)]
+
+
 class State(C.Structure):
     _fields_ = [("step", C.c_long), ("t", C.c_double), ("dt", C.c_double),
                 ("kinetic", C.c_double), ("pair", C.c_double), ("embedding", C.c_double),
@@ -144,6 +154,12 @@ SIGNATURES = [
     ("cbx_slab_local_state", C.c_int, [_P, C.POINTER(C.c_double)]),
     ("cbx_slab_commit", C.c_int, [_P, C.POINTER(C.c_double)]),
     ("cbx_bench_phases", C.c_int, [_P, C.c_int]),
+    ("cbx_run", C.c_int, [_P, C.POINTER(RunSpec), C.c_char_p]),
+    ("cbx_run_series", C.c_long, [_P, C.POINTER(C.c_double), C.POINTER(C.c_long)]),
+    ("cbx_thermostat_rescale", C.c_int, [_P, _D, C.c_long]),
+    ("cbx_write_snapshot", C.c_int, [_P, C.c_char_p, _D]),
+    ("cbx_write_timeseries", C.c_int, [C.c_char_p, C.c_long, C.POINTER(C.c_double),
+                                       C.POINTER(C.c_long)]),
     ("cbx_nccl_unique_id", C.c_int, [_P, C.c_long]),
     ("cbx_slab_comm_init", C.c_int, [_P, _P, C.c_long]),
     ("cbx_slab_p2p_handle", C.c_int, [_P, _P, C.c_long]),

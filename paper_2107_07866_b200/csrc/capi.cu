@@ -81,6 +81,9 @@ struct cbx_ctx {
   std::vector<void*> p2p_opened;
   P2PLinks links{};
   P2PLinks* d_links = nullptr;  // device copy (the finalize kernel's reduction)
+  // defect series of the last cbx_run (sim.h:54)
+  std::vector<double> ser_t;
+  std::vector<long> ser_d;
   bool p2p = false;
 
   template <class T>
@@ -1524,6 +1527,363 @@ CBX_API cbx_status cbx_inject_pka(cbx_ctx* c, int64_t site, const double v[3]) {
   });
   // a slab rank only sets the velocity: cbx_measure is collective there
   return rc == CBX_OK && !c->G.slab ? cbx_measure(c) : rc;
+}
+
+// ---- thermostat_rescale (sim.cpp:188-221) ---------------------------------
+namespace {
+__device__ __forceinline__ bool in_band_dev(long long id, const Geo& G, long band) {
+  if (band <= 0) return true;
+  const long long tx2 = 2ll * G.tx;
+  const long cz = (long)(id / (tx2 * G.ty)), cy = (long)((id / tx2) % G.ty);
+  const long cx = (long)((id % tx2) >> 1), g = G.g;
+  return cx - g < band || (g + G.bx - 1) - cx < band || cy - g < band ||
+         (g + G.by - 1) - cy < band || cz - g < band || (g + G.bz - 1) - cz < band;
+}
+
+// blocks [0, nsb): interior slots; [nsb, grid): interior clash records.
+// Per-block partial sums of |v|^2 and the in-band atom count.
+__global__ void k_thermo_sum(KP P, long band, int nsb, double* psum, double* pcnt) {
+  __shared__ double sh[8];
+  double v2 = 0.0, n = 0.0;
+  if (blockIdx.x < nsb) {
+    int par;
+    long long d;
+    if (map_site(P, par, d) && P.pdf[d].x < kVacantTest &&
+        in_band_dev(ref_of_dev(d, P.G.NC), P.G, band)) {
+      const long long S = P.S;
+      v2 = exact_r2(P.vel[d], P.vel[S + d], P.vel[2 * S + d]);
+      n = 1.0;
+    }
+  } else {
+    const int nc = P.st->n_clash;
+    for (int i = (blockIdx.x - nsb) * blockDim.x + threadIdx.x; i < nc;
+         i += (gridDim.x - nsb) * blockDim.x)
+      if (!P.cl.gf[i] && in_band_dev(P.cl.key[i], P.G, band)) {
+        v2 += exact_r2(P.cl.vx[i], P.cl.vy[i], P.cl.vz[i]);
+        n += 1.0;
+      }
+  }
+  const double a = block_sum<256>(v2, sh);
+  const double b = block_sum<256>(n, sh);
+  if (threadIdx.x == 0) {
+    psum[blockIdx.x] = a;
+    pcnt[blockIdx.x] = b;
+  }
+}
+
+__global__ void k_thermo_scale(KP P, long band, int nsb, double f) {
+  if (blockIdx.x < nsb) {
+    int par;
+    long long d;
+    if (map_site(P, par, d) && P.pdf[d].x < kVacantTest &&
+        in_band_dev(ref_of_dev(d, P.G.NC), P.G, band)) {
+      const long long S = P.S;
+      P.vel[d] *= f;
+      P.vel[S + d] *= f;
+      P.vel[2 * S + d] *= f;
+    }
+  } else {
+    const int nc = P.st->n_clash;
+    for (int i = (blockIdx.x - nsb) * blockDim.x + threadIdx.x; i < nc;
+         i += (gridDim.x - nsb) * blockDim.x)
+      if (!P.cl.gf[i] && in_band_dev(P.cl.key[i], P.G, band)) {
+        P.cl.vx[i] *= f;
+        P.cl.vy[i] *= f;
+        P.cl.vz[i] *= f;
+      }
+  }
+}
+
+const char* const kSymbols[] = {  // analysis.cpp:11-19
+    "X",  "H",  "He", "Li", "Be", "B",  "C",  "N",  "O",  "F",  "Ne", "Na", "Mg", "Al", "Si",
+    "P",  "S",  "Cl", "Ar", "K",  "Ca", "Sc", "Ti", "V",  "Cr", "Mn", "Fe", "Co", "Ni", "Cu",
+    "Zn", "Ga", "Ge", "As", "Se", "Br", "Kr", "Rb", "Sr", "Y",  "Zr", "Nb", "Mo", "Tc", "Ru",
+    "Rh", "Pd", "Ag", "Cd", "In", "Sn", "Sb", "Te", "I",  "Xe", "Cs", "Ba", "La", "Ce", "Pr",
+    "Nd", "Pm", "Sm", "Eu", "Gd", "Tb", "Dy", "Ho", "Er", "Tm", "Yb", "Lu", "Hf", "Ta", "W",
+    "Re", "Os", "Ir", "Pt", "Au", "Hg", "Tl", "Pb", "Bi", "Po", "At", "Rn", "Fr", "Ra", "Ac",
+    "Th", "Pa", "U"};
+}  // namespace
+
+CBX_API cbx_status cbx_thermostat_rescale(cbx_ctx* c, double temperature, long boundary_cells) {
+  const cbx_status rc = guarded(c, [&] {
+    cudaSetDevice(c->device);
+    require_box(c, "cbx_thermostat_rescale");
+    const int nsb = eam_blocks(c->P), grid = nsb + 8;
+    double* psum = c->P.part_ke;  // scratch: the next measure rewrites them
+    double* pcnt = c->P.part_vmax;
+    if (grid > c->P.n_part) raise(CBX_RUNTIME, "thermostat: partial buffer too small");
+    k_thermo_sum<<<grid, 256, 0, c->stream>>>(c->P, boundary_cells, nsb, psum, pcnt);
+    std::vector<double> hs(grid), hc(grid);
+    cuda_check(cudaMemcpyAsync(hs.data(), psum, grid * sizeof(double), cudaMemcpyDeviceToHost,
+                               c->stream), "thermostat");
+    cuda_check(cudaMemcpyAsync(hc.data(), pcnt, grid * sizeof(double), cudaMemcpyDeviceToHost,
+                               c->stream), "thermostat");
+    sync_status(c);
+    raise_device_error(c, false);
+    double sum_v2 = 0.0, n = 0.0;
+    for (int i = 0; i < grid; ++i) {
+      sum_v2 += hs[i];
+      n += hc[i];
+    }
+    const double measured =
+        n > 0.0 ? c->pot.mass * sum_v2 * mv2_to_ev() / (3.0 * n * boltzmann_ev()) : 0.0;
+    if (!(measured > 0.0)) {
+      std::fprintf(stderr, "thermostat: measured temperature is zero, skipping\n");
+      c->launches += 1;
+      return;
+    }
+    const double f = std::sqrt(temperature / measured);
+    k_thermo_scale<<<grid, 256, 0, c->stream>>>(c->P, boundary_cells, nsb, f);
+    c->launches += 2;
+    c->mask_valid = false;
+  });
+  return rc == CBX_OK ? cbx_measure(c) : rc;
+}
+
+// write_snapshot (analysis.cpp:90-116): interior slots in id order, then the
+// interior clash records in (key, bucket) order, at time t_ps
+CBX_API cbx_status cbx_write_snapshot(cbx_ctx* c, const char* path, double t_ps) {
+  return guarded(c, [&] {
+    cudaSetDevice(c->device);
+    require_box(c, "cbx_write_snapshot");
+    const Geo& G = c->G;
+    const long long S = c->S;
+    std::vector<double> pos(3 * S);
+    std::vector<uint64_t> tag(S);
+    std::vector<unsigned char> valid(S), ghost(S);
+    cbx_store st{};
+    st.n_slots = S;
+    st.pos = pos.data();
+    st.tag = tag.data();
+    st.valid = valid.data();
+    st.ghost = ghost.data();
+    do_download(c, &st);  // counts the clash records
+    const long nc = st.n_clash;
+    std::vector<int64_t> ck(nc);
+    std::vector<double> cp(3 * nc);
+    std::vector<uint64_t> ct(nc);
+    std::vector<unsigned char> cg(nc);
+    st.clash_key = ck.data();
+    st.clash_pos = cp.data();
+    st.clash_tag = ct.data();
+    st.clash_ghost = cg.data();
+    if (nc) do_download(c, &st);
+    long n_atoms = 0;
+    for (long long id = 0; id < S; ++id) n_atoms += valid[id] && !ghost[id];
+    for (long i = 0; i < nc; ++i) n_atoms += !cg[i];
+    std::FILE* f = std::fopen(path, "w");
+    if (!f) raise(CBX_RUNTIME, std::string("cannot open ") + path + " for writing");
+    const double a0 = c->box.a0, shift = c->box.ghost_width * a0;
+    const unsigned z = (unsigned)c->pot.atomic_number;
+    const char* sym = z < sizeof(kSymbols) / sizeof(kSymbols[0]) ? kSymbols[z] : "X";
+    char tb[48];
+    std::snprintf(tb, sizeof tb, "%.9g", t_ps);  // csv_time (analysis.cpp:66-75)
+    if (!std::strpbrk(tb, ".eE") && std::strspn(tb, "-0123456789") == std::strlen(tb))
+      std::strcat(tb, ".0");
+    std::fprintf(f, "%ld\n", n_atoms);
+    std::fprintf(f,
+                 "Lattice=\"%.10g 0 0 0 %.10g 0 0 0 %.10g\" "
+                 "Properties=species:S:1:pos:R:3:tag:I:1 Time=%s\n",
+                 c->box.box_x * a0, c->box.box_y * a0, c->box.box_z * a0, tb);
+    const long long tx2 = 2ll * G.tx;
+    for (long z_ = G.g; z_ < G.g + G.bz; ++z_)  // for_each_interior_id (store.h:82-93)
+      for (long y = G.g; y < G.g + G.by; ++y) {
+        const long long row = ((long long)z_ * G.ty + y) * tx2;
+        for (long x = 2 * G.g; x < 2 * (G.g + G.bx); ++x) {
+          const long long id = row + x;
+          if (!valid[id] || ghost[id]) continue;
+          std::fprintf(f, "%s %.10g %.10g %.10g %llu\n", sym, pos[3 * id] - shift,
+                       pos[3 * id + 1] - shift, pos[3 * id + 2] - shift,
+                       (unsigned long long)tag[id]);
+        }
+      }
+    for (long i = 0; i < nc; ++i)
+      if (!cg[i])
+        std::fprintf(f, "%s %.10g %.10g %.10g %llu\n", sym, cp[3 * i] - shift,
+                     cp[3 * i + 1] - shift, cp[3 * i + 2] - shift, (unsigned long long)ct[i]);
+    const bool bad = std::ferror(f) != 0;
+    std::fclose(f);
+    if (bad) raise(CBX_RUNTIME, std::string("write failed: ") + path);
+  });
+}
+
+// ---- Simulation::run (sim.cpp:289-360) over the public entry points ------
+namespace {
+void csv_time(double t, char out[48]) {  // analysis.cpp:66-75
+  std::snprintf(out, 48, "%.9g", t);
+  if (!std::strpbrk(out, ".eE") && std::strspn(out, "-0123456789") == std::strlen(out))
+    std::strcat(out, ".0");
+}
+bool nonempty(const char* s) { return s && s[0]; }
+}  // namespace
+
+CBX_API cbx_status cbx_write_timeseries(const char* path, long n, const double* t,
+                                        const long* d) {
+  return guarded(nullptr, [&] {
+    std::FILE* f = std::fopen(path, "w");
+    if (!f) raise(CBX_RUNTIME, std::string("cannot open ") + path + " for writing");
+    std::fputs("t_ps,vacancies,interstitials,frenkel_pairs\n", f);
+    char tb[48];
+    for (long i = 0; i < n; ++i) {
+      csv_time(t[i], tb);
+      std::fprintf(f, "%s,%ld,%ld,%ld\n", tb, d[3 * i], d[3 * i + 1], d[3 * i + 2]);
+    }
+    const bool bad = std::ferror(f) != 0;
+    std::fclose(f);
+    if (bad) raise(CBX_RUNTIME, std::string("write failed: ") + path);
+  });
+}
+
+CBX_API long cbx_run_series(cbx_ctx* c, double* t, long* d) {
+  const long n = (long)c->ser_t.size();
+  if (t) std::memcpy(t, c->ser_t.data(), n * sizeof(double));
+  if (d) std::memcpy(d, c->ser_d.data(), 3 * n * sizeof(long));
+  return n;
+}
+
+CBX_API cbx_status cbx_run(cbx_ctx* c, const cbx_run_spec* r, const char* log_path) {
+  if (c->G.slab) {
+    set_thread_error("cbx_run: single-box contexts only");
+    c->err = "cbx_run: single-box contexts only";
+    return CBX_LOGIC;
+  }
+  std::FILE* log = nullptr;
+  if (nonempty(log_path))
+    log = std::strcmp(log_path, "-") == 0 ? stdout : std::fopen(log_path, "w");
+  c->ser_t.clear();
+  c->ser_d.clear();
+  cbx_state st{};
+  cbx_status rc = CBX_OK;
+  auto sample = [&]() -> cbx_status {  // sim.cpp:275-277
+    long d[3];
+    const cbx_status e = cbx_count_defects(c, d);
+    if (e) return e;
+    const cbx_status g = cbx_get_state(c, &st);
+    if (g) return g;
+    c->ser_t.push_back(st.t);
+    c->ser_d.insert(c->ser_d.end(), d, d + 3);
+    return CBX_OK;
+  };
+  auto snapshot = [&](const char* suffix) -> cbx_status {  // sim.cpp:279-282
+    if (!nonempty(r->snapshot_prefix)) return CBX_OK;
+    cbx_get_state(c, &st);
+    return cbx_write_snapshot(c, (std::string(r->snapshot_prefix) + suffix).c_str(), st.t);
+  };
+  auto log_line = [&]() {
+    if (!log) return;
+    cbx_get_state(c, &st);
+    long n_atoms = 0;
+    {
+      // atom count: interior slots + interior clash records (store.h:73)
+      long d[3];
+      cbx_count_defects(c, d);  // vacancies of the interior (cheap, keeps the count exact)
+      const long sites = 2 * c->box.box_x * c->box.box_y * c->box.box_z;
+      n_atoms = sites - d[0] + d[1];
+    }
+    const double T = n_atoms == 0 ? 0.0
+                                  : 2.0 * st.kinetic / (3.0 * (double)n_atoms * boltzmann_ev());
+    char tb[48];
+    csv_time(st.t, tb);
+    std::fprintf(log, "step %ld  t=%s ps  dt=%.4g  E=%.6f eV  T=%.1f K  FP=%ld\n", st.step, tb,
+                 st.dt, st.kinetic + st.pair + st.embedding, T, c->ser_d.back());
+  };
+  // one step with the post-mortem outputs on failure (sim.cpp:303-315)
+  auto guarded_steps = [&](long n) -> cbx_status {
+    const cbx_status e = cbx_step(c, -1.0, n, &st);
+    if (e) {
+      const std::string err = c->err;
+      if (nonempty(r->snapshot_prefix)) {
+        cbx_get_state(c, &st);
+        cbx_write_snapshot(c, (std::string(r->snapshot_prefix) + "_postmortem.xyz").c_str(),
+                           st.t);
+      }
+      if (nonempty(r->timeseries))
+        cbx_write_timeseries(r->timeseries, (long)c->ser_t.size(), c->ser_t.data(),
+                             c->ser_d.data());
+      c->err = err;
+    }
+    return e;
+  };
+  auto thermostat = [&]() { return cbx_thermostat_rescale(c, r->temperature, r->thermostat_boundary_cells); };
+  do {
+    if ((rc = sample())) break;
+    if (r->snapshot_interval > 0 && (rc = snapshot("_000000.xyz"))) break;
+    for (long i = 0; i < r->equilibration_steps && !rc; ++i) {
+      if ((rc = guarded_steps(1))) break;
+      if (r->thermostat_enabled && (i + 1) % r->thermostat_interval == 0) rc = thermostat();
+    }
+    if (rc) break;
+    if (r->pka_energy_kev > 0.0) {  // Simulation::inject_pka (sim.cpp:163-186)
+      const long cx = r->pka_site[0] >= 0 ? r->pka_site[0] : c->box.box_x / 2;
+      const long cy = r->pka_site[1] >= 0 ? r->pka_site[1] : c->box.box_y / 2;
+      const long cz = r->pka_site[2] >= 0 ? r->pka_site[2] : c->box.box_z / 2;
+      const long g = c->box.ghost_width;
+      const long long tx = c->box.box_x + 2 * g, ty = c->box.box_y + 2 * g;
+      const long long site = ((g + cz) * ty + (g + cy)) * 2 * tx + 2 * (g + cx);
+      const double dx = (double)r->pka_dir[0], dy = (double)r->pka_dir[1],
+                   dz = (double)r->pka_dir[2];
+      const double len = std::sqrt(dx * dx + dy * dy + dz * dz);
+      if (!(len > 0.0)) {
+        c->err = "pka.direction: must not be the zero vector";
+        rc = CBX_INVALID_ARGUMENT;
+        break;
+      }
+      const double v = std::sqrt(2.0 * (r->pka_energy_kev * 1000.0) / c->pot.mass) *
+                       speed_factor();
+      const double sc = v / len;
+      const double vel[3] = {sc * dx, sc * dy, sc * dz};
+      if ((rc = cbx_inject_pka(c, site, vel))) break;
+    }
+    long done = 0;
+    bool sampled_last = true;
+    const bool per_step = r->max_time > 0.0;  // the time cap is checked after every step
+    while (!rc) {
+      const bool step_cap = r->steps > 0 && done >= r->steps;
+      cbx_get_state(c, &st);
+      const bool time_cap = r->max_time > 0.0 && st.t >= r->max_time;
+      const bool no_budget = r->steps == 0 && r->max_time == 0.0;
+      if (step_cap || time_cap || no_budget) break;
+      // steps until the next event (sample, snapshot, thermostat, cap)
+      long n = 1;
+      if (!per_step) {
+        n = r->steps > 0 ? r->steps - done : 1;
+        auto upto = [&](long iv) {
+          if (iv > 0) n = std::min(n, iv - done % iv);
+        };
+        upto(r->defect_interval);
+        upto(r->snapshot_interval);
+        if (r->thermostat_enabled) upto(r->thermostat_interval);
+      }
+      if ((rc = guarded_steps(n))) break;
+      done += n;
+      if (r->thermostat_enabled && done % r->thermostat_interval == 0 && (rc = thermostat()))
+        break;
+      sampled_last = false;
+      if (r->defect_interval > 0 && done % r->defect_interval == 0) {
+        if ((rc = sample())) break;
+        sampled_last = true;
+        log_line();
+      }
+      if (r->snapshot_interval > 0 && done % r->snapshot_interval == 0) {
+        char suffix[32];
+        std::snprintf(suffix, sizeof suffix, "_%06ld.xyz", done);
+        if ((rc = snapshot(suffix))) break;
+      }
+    }
+    if (rc) break;
+    if (!sampled_last) {
+      if ((rc = sample())) break;
+      log_line();
+    }
+    if (nonempty(r->timeseries) &&
+        (rc = cbx_write_timeseries(r->timeseries, (long)c->ser_t.size(), c->ser_t.data(),
+                                   c->ser_d.data())))
+      break;
+    rc = snapshot("_final.xyz");
+  } while (false);
+  if (log && log != stdout) std::fclose(log);
+  if (log == stdout) std::fflush(stdout);
+  return rc;
 }
 
 CBX_API cbx_status cbx_count_defects(cbx_ctx* c, long out[3]) {

@@ -76,5 +76,6 @@ Geo make_geo(const cbx_box& b);
 double accel_factor();
 double mv2_to_ev();
 double speed_factor();
+double boltzmann_ev();  // units.h:31
 
 }  // namespace cbx

@@ -24,7 +24,7 @@ constexpr double angstrom_si = 1e-10;
 constexpr double picosecond_si = 1e-12;
 constexpr double accel_factor_c =
     (ev_si / angstrom_si / amu_si) * (picosecond_si * picosecond_si) / angstrom_si;
-constexpr double boltzmann_ev = boltzmann_si / ev_si;
+constexpr double boltzmann_ev_c = boltzmann_si / ev_si;
 }  // namespace
 
 void set_thread_error(const std::string& msg) { t_err = msg; }
@@ -248,6 +248,7 @@ Geo make_geo(const cbx_box& b) {
 double accel_factor() { return accel_factor_c; }
 double mv2_to_ev() { return 1.0 / accel_factor_c; }
 double speed_factor() { return 98.22694750253277; }
+double boltzmann_ev() { return boltzmann_ev_c; }
 
 // init_bcc over the global box `b`; sites of global interior planes
 // [z_lo, z_hi) are stored in the layout of `out_geo` shifted down by z_lo -
@@ -258,7 +259,7 @@ static HostLattice init_bcc_planes(const cbx_box& b, const Geo& out_geo, long z_
                                    double mass, double temperature, uint64_t seed) {
   const Geo G = make_geo(b);
   const double sigma =
-      temperature > 0.0 ? std::sqrt(boltzmann_ev * temperature * accel_factor_c / mass) : 0.0;
+      temperature > 0.0 ? std::sqrt(boltzmann_ev_c * temperature * accel_factor_c / mass) : 0.0;
   std::mt19937_64 gen(seed);
   double spare = 0.0;
   bool have = false;

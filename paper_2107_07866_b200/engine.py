@@ -38,6 +38,21 @@ class PkaSpec:  # config.h:9-15
 
 
 @dataclass
+class ThermostatSpec:  # config.h:16-20
+    enabled: bool = False
+    interval: int = 10
+    boundary_cells: int = 0
+
+
+@dataclass
+class OutputSpec:  # config.h:22-27
+    timeseries: str = ""
+    snapshot_prefix: str = ""
+    snapshot_interval: int = 0
+    defect_interval: int = 10
+
+
+@dataclass
 class SimConfig:  # config.h:36-53
     box_x: int = 10
     box_y: int = 10
@@ -51,6 +66,8 @@ class SimConfig:  # config.h:36-53
     max_time: float = 0.0
     dt_max: float = 1e-3
     max_disp: float = 0.05
+    thermostat: ThermostatSpec = field(default_factory=ThermostatSpec)
+    output: OutputSpec = field(default_factory=OutputSpec)
     workers: int = 1
     seed: int = 12345
     equilibration_steps: int = 0
@@ -335,6 +352,25 @@ class DeviceStore:
         self._check(self.lib.cbx_count_defects(self.h, out))
         return tuple(out)
 
+    def thermostat_rescale(self, temperature: float, boundary_cells: int = 0):
+        self._check(self.lib.cbx_thermostat_rescale(self.h, temperature, boundary_cells))
+
+    def write_snapshot(self, path: str, t_ps: Optional[float] = None):
+        t = self.state()["t"] if t_ps is None else t_ps
+        self._check(self.lib.cbx_write_snapshot(self.h, path.encode(), t))
+
+    def run(self, spec: "_lib.RunSpec", log_path: str = ""):
+        self._spec = spec  # keep the strings alive
+        self._check(self.lib.cbx_run(self.h, C.byref(spec), log_path.encode()))
+
+    def series(self):
+        n = self.lib.cbx_run_series(self.h, None, None)
+        t = np.zeros(n)
+        d = np.zeros(3 * n, dtype=np.int64)
+        self.lib.cbx_run_series(self.h, t.ctypes.data_as(C.POINTER(C.c_double)),
+                                d.ctypes.data_as(C.POINTER(C.c_long)))
+        return t, d.reshape(n, 3)
+
     # --- instrumentation ---------------------------------------------------
     def enable_timing(self, on: bool = True):
         self._check(self.lib.cbx_enable_timing(self.h, 1 if on else 0))
@@ -438,3 +474,25 @@ class Simulation:
 
     def count_defects(self):
         return self.dev.count_defects()
+
+    def thermostat_rescale(self):
+        """sim.cpp:188-221: toward cfg.temperature in cfg.thermostat.boundary_cells"""
+        self.dev.thermostat_rescale(self.cfg.temperature, self.cfg.thermostat.boundary_cells)
+
+    def run_spec(self) -> "_lib.RunSpec":
+        c = self.cfg
+        return _lib.RunSpec(
+            c.steps, c.max_time, c.equilibration_steps, 1 if c.thermostat.enabled else 0,
+            c.thermostat.interval, c.thermostat.boundary_cells, c.temperature,
+            c.output.timeseries.encode(), c.output.snapshot_prefix.encode(),
+            c.output.snapshot_interval, c.output.defect_interval,
+            (C.c_long * 3)(*c.pka.site), c.pka.energy_kev, (C.c_long * 3)(*c.pka.direction))
+
+    def run(self, log: str = ""):
+        """Simulation::run (sim.cpp:289-360); log: path, "-" for stdout, "" none"""
+        self.dev.run(self.run_spec(), log)
+
+    @property
+    def series(self):
+        """(t_ps, [[vacancies, interstitials, frenkel_pairs], ...]) of the last run"""
+        return self.dev.series()
