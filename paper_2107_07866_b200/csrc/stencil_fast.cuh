@@ -916,7 +916,7 @@ __device__ __forceinline__ double force_site_lean(const KP& P, KP* Pp, int par, 
     const int bit = __ffs(cu) - 1;
     cu &= cu - 1;
     const bool v = (co >> bit) & 1;
-    const int j = v ? d + s_offs[base + bit] : d;
+    const int j = v ? d + s_offs[(P.xp & 16) ? 0 : base + bit] : d;
     double px, py, pz, pw;
     ld256(pdf + j, px, py, pz, pw);
     const int t = __ldg(tgt + j);
@@ -953,7 +953,7 @@ __device__ __forceinline__ double force_site_lean(const KP& P, KP* Pp, int par, 
       e = fma(0.5, phi, e);
     } else {
       e += phi;
-      if (v) {
+      if (v && !(P.xp & 2)) {
         red_add(&P.frc[t], qx);
         red_add(&P.frc[S + t], qy);
         red_add(&P.frc[2 * S + t], qz);
