@@ -49,7 +49,6 @@ struct cbx_ctx {
   bool clash_f_zero = false;    // the last embed pass zeroed the records' forces
   bool acc_rho_zero = false;    // kick_drift of this step cleared rho (single box)
   bool acc_frc_zero = false;    // ... and the forces
-  bool tile_ok = false;  // every offset within the 2-cell tile halo
   // z-slab decomposition
   int rank = 0, nranks = 1;
   cbx_box gbox{};       // the global box (slab ranks)
@@ -60,7 +59,6 @@ struct cbx_ctx {
   // to re-bind the device's __constant__ copy when contexts share a GPU
   std::vector<int> c_hd[2], c_fd[2];
   std::vector<long long> c_ff[2];
-  std::vector<int4> c_h4[2], c_f4[2];
   int c_hin[2] = {0, 0}, c_fin[2] = {0, 0};
   bool const_ready = false;
   // in-graph NCCL exchange of a slab rank (cbx_slab_comm_init)
@@ -121,9 +119,6 @@ void bind_constants(cbx_ctx* c) {
   const int hn[2] = {(int)c->c_hd[0].size(), (int)c->c_hd[1].size()};
   const int fn[2] = {(int)c->c_fd[0].size(), (int)c->c_fd[1].size()};
   upload_offsets(hp, hn, fp, fn, fl, c->c_hin, c->c_fin, c->stream);
-  const int4* h4p[2] = {c->c_h4[0].data(), c->c_h4[1].data()};
-  const int4* f4p[2] = {c->c_f4[0].data(), c->c_f4[1].data()};
-  c->tile_ok = upload_tile_offsets(h4p, hn, f4p, fn, c->stream);
   if (cudaStreamSynchronize(c->stream) != cudaSuccess)
     raise(CBX_CUDA, "offset table upload failed");
   g_const_owner[c->device] = c;
@@ -1035,7 +1030,6 @@ static cbx_status create_impl(const cbx_box* box, const cbx_potential* pot,
     // potential cutoff first ("inner"), index-skin sites after (stencil_fast.cuh)
     std::vector<int> hd[2], fd[2];
     std::vector<long long> ff[2];
-    std::vector<int4> h4[2], f4[2];
     int hin[2] = {0, 0}, fin[2] = {0, 0};
     for (int par = 0; par < 2; ++par) {
       auto delta = [&](const Offset& o) {
@@ -1058,12 +1052,10 @@ static cbx_status create_impl(const cbx_box* box, const cbx_potential* pot,
       };
       for (const Offset& o : order(c->offs.half[par], hin[par])) {
         hd[par].push_back(delta(o));
-        h4[par].push_back(make_int4(o.dx, o.dy, o.dz, (par ^ o.cross) - par));
       }
       for (const Offset& o : order(c->offs.full[par], fin[par])) {
         fd[par].push_back(delta(o));
         ff[par].push_back(o.flat);
-        f4[par].push_back(make_int4(o.dx, o.dy, o.dz, (par ^ o.cross) - par));
       }
     }
     const int* hp[2] = {hd[0].data(), hd[1].data()};
@@ -1076,8 +1068,6 @@ static cbx_status create_impl(const cbx_box* box, const cbx_potential* pot,
       c->c_hd[par] = hd[par];
       c->c_fd[par] = fd[par];
       c->c_ff[par] = ff[par];
-      c->c_h4[par] = h4[par];
-      c->c_f4[par] = f4[par];
       c->c_hin[par] = hin[par];
       c->c_fin[par] = fin[par];
     }
@@ -1200,10 +1190,6 @@ static cbx_status create_impl(const cbx_box* box, const cbx_potential* pot,
       const char* nm = std::getenv("CBX_NOMASK");
       P.pmask = maxn <= 126 && !(nm && std::atoi(nm)) ? c->alloc<unsigned long long>(2 * S)
                                                        : nullptr;
-    }
-    {
-      const char* e = std::getenv("CBX_TILE");
-      P.use_tile = c->tile_ok && P.pmask != nullptr && (e ? std::atoi(e) != 0 : false);
     }
 
     c->d_defects = c->alloc<unsigned long long>(4);
@@ -1996,10 +1982,10 @@ CBX_API cbx_status cbx_bench_phases(cbx_ctx* c, int on) {
 CBX_API cbx_status cbx_describe(cbx_ctx* c, char* buf, long n) {
   return guarded(c, [&] {
     std::snprintf(buf, n,
-                  "{\"stencil\": %d, \"fast_ok\": %d, \"tile_ok\": %d, \"use_tile\": %d, "
+                  "{\"stencil\": %d, \"fast_ok\": %d, "
                   "\"pair_mask\": %d, \"slots\": %lld, \"ghost_sites\": %d, "
                   "\"clash_capacity\": %d, \"band_A2\": %.3e, \"sm_count\": %d}",
-                  c->mode, (int)c->fast_ok, (int)c->tile_ok, c->P.use_tile,
+                  c->mode, (int)c->fast_ok,
                   (int)(c->P.pmask != nullptr), c->S, c->n_ghost, c->P.cap_clash, c->band,
                   [] {
                     int d = 0, n = 0;

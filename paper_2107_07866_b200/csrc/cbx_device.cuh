@@ -87,7 +87,6 @@ struct KP {
   unsigned long long* pmask;  // [S][2] pair masks from the density pass (or null)
   int use_mask;               // force pass replays pmask (set per launch by the host)
   int xp;                     // timing experiments only (CBX_XP): 1 fixed table row, 2 no RED
-  int use_tile;               // shared-memory tiled stencils (stencil_tile.cuh)
   int n_pair_part;         // partials written by the force pass
   double accel, mv2;  // units::accel_factor, units::mv2_to_ev (units.h:17-24)
   long long S;  // 2*NC sites
@@ -237,8 +236,7 @@ void launch_pack(const KP& P, int kind, int dir, unsigned char* buf, long long c
 void launch_unpack(const KP& P, int kind, int from, const unsigned char* buf, long long gshift,
                    int* rem_base, cudaStream_t s);
 void launch_remote_df(const KP& P, cudaStream_t s);
-bool upload_tile_offsets(const int4* half[2], const int half_n[2], const int4* full[2],
-                         const int full_n[2], cudaStream_t s);
+
 int embed_blocks(const KP& P);
 int embed_grid(const KP& P);  // energy partials of the embed pass
 int kick_grid(const KP& P);   // KE partials of the kick2 pass

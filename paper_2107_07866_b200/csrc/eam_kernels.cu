@@ -489,44 +489,17 @@ template __device__ void clash_body<0>(const KP&, int, int);
 template __device__ void clash_body<1>(const KP&, int, int);
 
 #include "stencil_fast.cuh"
-#include "stencil_tile.cuh"
-
-// tile-space deltas of the ordered offset lists: (dx, dy, dz, q - p) each
-bool upload_tile_offsets(const int4* half[2], const int half_n[2], const int4* full[2],
-                         const int full_n[2], cudaStream_t s) {
-  std::vector<int> h[2], f[2];
-  bool ok = true;
-  auto td = [&](const int4& o) {
-    ok &= abs(o.x) <= kTH && abs(o.y) <= kTH && abs(o.z) <= kTH;
-    return o.w * kTC + (o.z * kTY + o.y) * kTX + o.x;
-  };
-  for (int p = 0; p < 2; ++p) {
-    for (int i = 0; i < half_n[p]; ++i) h[p].push_back(td(half[p][i]));
-    for (int i = 0; i < full_n[p]; ++i) f[p].push_back(td(full[p][i]));
-  }
-  if (!ok) return false;
-  for (int p = 0; p < 2; ++p) {
-    cudaMemcpyToSymbolAsync(c_half_tile, h[p].data(), h[p].size() * sizeof(int),
-                            p * kMaxOffsets * sizeof(int), cudaMemcpyHostToDevice, s);
-    cudaMemcpyToSymbolAsync(c_full_tile, f[p].data(), f[p].size() * sizeof(int),
-                            p * kMaxOffsets * sizeof(int), cudaMemcpyHostToDevice, s);
-  }
-  cudaStreamSynchronize(s);
-  return true;
-}
 
 // ------------------------------------------------------------- launchers
 // mode: 0 fast half list (Newton-3), 1 fast full list, 2 reference-literal half list
 // return true when the clash-record pass ran inside the same kernel
 bool launch_density(const KP& P, int mode, cudaStream_t s) {
   if (mode == 2) k_density<false><<<eam_blocks(P), 256, 0, s>>>(P);
-  else if (P.use_tile) launch_density_tile(P, mode, s);
   else return launch_density_fast(P, mode, fast_grid(P, false, mode), s);
   return false;
 }
 bool launch_force(const KP& P, int mode, cudaStream_t s) {
   if (mode == 2) k_force<false><<<eam_blocks(P), 256, 0, s>>>(P);
-  else if (P.use_tile && P.use_mask) launch_force_tile(P, mode, tile_grid(P, true, mode), s);
   else return launch_force_fast(P, mode, fast_grid(P, true, mode), s);
   return false;
 }
@@ -540,7 +513,6 @@ int pair_partials(const KP& P, int mode) {
   int n = std::max(eam_blocks(P), 32 * sms);  // 1024-thread persistent variants
   for (int m = 0; m < 2; ++m) {
     n = std::max(n, 4 * fast_grid(P, true, m));
-    n = std::max(n, 8 * tile_grid(P, true, m));  // 256-thread blocks
   }
   return std::min(n, P.n_part);
 }
