@@ -239,7 +239,7 @@ def run_ours(args, w, path, ws, rank, local):
            "config": {"workload": w.note, "atoms_per_gpu": n, "dt_ps": w.dt,
                       "stencil": args.stencil,
                       "l2": f"flushed ({args.flush_mb:.0f} MB write) before every timed step",
-                      "parallelism": (f"z-slab x{ws}, {args.transport} halo/migrant "
+                      "parallelism": (f"z-slab x{ws}, {getattr(dev, 'transport', args.transport)} halo/migrant "
                                       f"exchange + reduction inside the step graph") if slab
                                      else "single-gpu",
                       "global_cells": [w.cells[0], w.cells[1], w.cells[2] * ws]},

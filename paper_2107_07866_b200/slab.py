@@ -136,13 +136,30 @@ class SlabRank(DeviceStore):
                 allh = [None] * world
                 dist.all_gather_object(allh, h[0], group=group)
                 h = allh
-            self.init_p2p(h)
+            ok, err = True, ""
+            try:
+                self.init_p2p(h)
+            except _lib.CbxError as e:  # e.g. no peer access between these GPUs
+                ok, err = False, str(e)
+            if world > 1:  # every rank must agree, or the exchanges would hang
+                import torch.distributed as dist
+                flags = [None] * world
+                dist.all_gather_object(flags, ok, group=group)
+                ok = all(flags)
+            if not ok:
+                import sys
+                print(f"slab: peer-memory transport unavailable ({err or 'another rank'}); "
+                      "using NCCL", file=sys.stderr)
+                self.transport = "nccl"
+                return self.connect("nccl", group)
+            self.transport = "p2p"
         elif transport == "nccl":
             uid = [SlabRank.nccl_unique_id() if self.rank == 0 else None]
             if world > 1:
                 import torch.distributed as dist
                 dist.broadcast_object_list(uid, src=0, group=group)
             self.init_comm(uid[0])
+            self.transport = "nccl"
         else:
             raise ValueError(f"unknown transport {transport!r}")
 
