@@ -8,7 +8,7 @@
 
 int main(int argc, char** argv) {
   if (argc < 2) {
-    std::fprintf(stderr, "usage: %s potential.eam [gpu]\n", argv[0]);
+    std::fprintf(stderr, "usage: %s potential.eam [gpu [slab]]\n", argv[0]);
     return 2;
   }
   using namespace cascade_b200;
@@ -32,6 +32,15 @@ int main(int argc, char** argv) {
     const cbx_state s = eng.step(1e-3, 10);
     std::printf("atoms %ld E_emb %.10f E_pair %.10f -> step %ld KE %.10f\n", n, e.embedding,
                 e.pair, s.step, s.kinetic);
+  }
+  if (argc > 3) {  // one-rank z-slab over peer memory
+    SlabEngine slab(box, pot, 0, 1, 0);
+    slab.connect_p2p(slab.p2p_handle());
+    const long n = slab.init_bcc(600.0, 12345);
+    slab.eval_forces();
+    slab.measure();
+    const cbx_state s = slab.step(1e-3, 10);
+    std::printf("slab atoms %ld -> step %ld KE %.10f\n", n, s.step, s.kinetic);
   }
   return 0;
 }

@@ -123,6 +123,9 @@ CBX_API cbx_status cbx_make_box(long box_x, long box_y, long box_z, double a0_cf
                                 long ghost_width_cfg, double max_disp,
                                 const cbx_potential* pot, cbx_box* out, double* index_cutoff);
 CBX_API double cbx_pka_speed(double energy_ev, double mass_amu); /* src/sim.cpp:88-92 */
+/* synthetic::write_table, src/synthetic.cpp:49-98: the reference's own
+ * single-element test table (the CLI's gen-potential).  Same bytes. */
+CBX_API cbx_status cbx_write_synthetic_table(const char* path, long nrho, long nr);
 CBX_API double cbx_adaptive_dt(double max_speed, double dt_max, double max_disp); /* 94-98 */
 
 /* ---- context -------------------------------------------------------------- */
@@ -180,6 +183,21 @@ CBX_API cbx_status cbx_enable_timing(cbx_ctx* ctx, int on);
 CBX_API cbx_status cbx_count_pairs(cbx_ctx* ctx, uint64_t out[2]);
 CBX_API cbx_status cbx_kernel_launches(cbx_ctx* ctx, uint64_t* n); /* cumulative */
 /* JSON description of the context's kernel configuration */
+/* Device bytes by structure (the CLI's bench-mem, tools/src/main.cpp:72-115):
+ * out[k] for k < CBX_MEM_CATEGORIES, then slots, clash capacity, ghost
+ * links and the offset-list bytes. */
+enum {
+  CBX_MEM_SLOTS = 0,     /* per-slot SoA: pos+dF, shadow, vel, force, rho, tag, owner, mask */
+  CBX_MEM_CLASH = 1,     /* clash records (double-buffered) + the halo clash arena */
+  CBX_MEM_GHOSTS = 2,    /* ghost-image links */
+  CBX_MEM_REHASH = 3,    /* movers and sort scratch of update_hash */
+  CBX_MEM_TABLES = 4,    /* spline segments (reference and fast layouts) */
+  CBX_MEM_REDUCTION = 5, /* partial sums, status, counters */
+  CBX_MEM_STAGING = 6,   /* reference-layout upload/download staging */
+  CBX_MEM_EXCHANGE = 7,  /* slab exchange buffers (NCCL / peer memory) */
+  CBX_MEM_CATEGORIES = 8
+};
+CBX_API cbx_status cbx_memory_report(cbx_ctx* ctx, long long out[CBX_MEM_CATEGORIES + 4]);
 CBX_API cbx_status cbx_describe(cbx_ctx* ctx, char* buf, long n);
 /* benchmark loop: nsteps fixed-dt steps, each preceded (outside the timed
  * region) by a write of flush_mb MB to evict L2; per-step CUDA events on the

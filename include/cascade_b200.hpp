@@ -79,6 +79,7 @@ class Engine {
   Engine(const cbx_box& box, const Potential& pot, const Offsets* idx = nullptr, int device = 0) {
     check(cbx_create(&box, pot.get(), idx ? idx->get() : nullptr, device, &c_));
   }
+  explicit Engine(cbx_ctx* adopt) : c_(adopt) {}
   ~Engine() { cbx_destroy(c_); }
   Engine(const Engine&) = delete;
   Engine& operator=(const Engine&) = delete;
@@ -166,10 +167,55 @@ class Engine {
     for (long i = 0; i < n; ++i) out[i] = {t[i], d[3 * i], d[3 * i + 1], d[3 * i + 2]};
     return out;
   }
-  cbx_ctx* raw() { return c_; }
+  cbx_ctx* raw() const { return c_; }
 
  private:
   cbx_ctx* c_ = nullptr;
+};
+
+// One z slab of a box decomposed over `nranks` GPUs: the same
+// Engine operations (step, eval_forces, measure, count_defects) run the
+// decomposed step once the ranks are connected.  Peer memory (ranks of one
+// node): every rank exports p2p_handle(), every rank passes all handles in
+// rank order to connect_p2p().  NCCL: rank 0 makes nccl_unique_id(), every
+// rank passes it to connect_nccl().
+class SlabEngine : public Engine {
+ public:
+  SlabEngine(const cbx_box& global_box, const Potential& pot, int rank, int nranks,
+             int device = 0)
+      : Engine(create(global_box, pot, rank, nranks, device)) {}
+
+  std::vector<unsigned char> p2p_handle() {
+    std::vector<unsigned char> h(64);
+    check(cbx_slab_p2p_handle(raw(), h.data(), (long)h.size()), raw());
+    return h;
+  }
+  void connect_p2p(const std::vector<unsigned char>& all_handles) {
+    check(cbx_slab_p2p_init(raw(), all_handles.data(), (long)all_handles.size()), raw());
+  }
+  static std::vector<unsigned char> nccl_unique_id() {
+    std::vector<unsigned char> id(128);
+    check(cbx_nccl_unique_id(id.data(), (long)id.size()));
+    return id;
+  }
+  void connect_nccl(const std::vector<unsigned char>& id) {
+    check(cbx_slab_comm_init(raw(), id.data(), (long)id.size()), raw());
+  }
+  // global store <-> this slab (reference-layout arrays of the whole box)
+  void upload_global(const cbx_store& s) { check(cbx_upload_store_global(raw(), &s), raw()); }
+  long download_global(cbx_store& s, long n_clash_in = 0) {
+    long n = n_clash_in;
+    check(cbx_download_store_global(raw(), &s, &n), raw());
+    return n;
+  }
+
+ private:
+  static cbx_ctx* create(const cbx_box& b, const Potential& pot, int rank, int nranks,
+                         int device) {
+    cbx_ctx* c = nullptr;
+    check(cbx_create_slab(&b, pot.get(), nullptr, rank, nranks, device, &c));
+    return c;
+  }
 };
 
 }  // namespace cascade_b200

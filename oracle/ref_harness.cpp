@@ -443,3 +443,73 @@ long orc_series(const orc_ctx* c, double* t, long* d) {
 }
 
 }  // extern "C"
+
+// ------------------------------------------------------- config front end
+// config.cpp:162-188 through the real reference: the parsed SimConfig as
+// key=value lines (the layout of paper_2107_07866_b200.config.dump_config),
+// or the exception message.  Returns ORC_OK, ORC_INVALID (invalid_argument)
+// or ORC_RUNTIME (runtime_error).
+#include "cascademd/config.h"
+extern "C" {
+
+int ref_load_config(const char* path, const char* const* overrides, int n, char* out, long cap) {
+  std::string text;
+  int rc = ORC_OK;
+  try {
+    std::vector<std::string> ov(overrides, overrides + n);
+    const SimConfig c = load_config(path, ov);
+    char b[256];
+    auto add = [&](const char* k, const std::string& v) { text += std::string(k) + "=" + v + "\n"; };
+    auto L = [&](long x) { return std::to_string(x); };
+    auto D = [&](double x) {
+      std::snprintf(b, sizeof b, "%.17g", x);
+      return std::string(b);
+    };
+    auto T = [&](long x, long y, long z) { return L(x) + "," + L(y) + "," + L(z); };
+    add("box.x", L(c.box_x));
+    add("box.y", L(c.box_y));
+    add("box.z", L(c.box_z));
+    add("box.a0", D(c.a0));
+    add("box.ghost_width", L(c.ghost_width));
+    add("temperature", D(c.temperature));
+    add("potential", c.potential_path);
+    add("pka.site", T(c.pka.site_x, c.pka.site_y, c.pka.site_z));
+    add("pka.energy", D(c.pka.energy_kev));
+    add("pka.direction", T(c.pka.dir_x, c.pka.dir_y, c.pka.dir_z));
+    add("steps", L(c.steps));
+    add("max_time", D(c.max_time));
+    add("dt_max", D(c.dt_max));
+    add("max_disp", D(c.max_disp));
+    add("thermostat.enabled", L(c.thermostat.enabled ? 1 : 0));
+    add("thermostat.interval", L(c.thermostat.interval));
+    add("thermostat.boundary_cells", L(c.thermostat.boundary_cells));
+    add("output.timeseries", c.output.timeseries);
+    add("output.snapshot_prefix", c.output.snapshot_prefix);
+    add("output.snapshot_interval", L(c.output.snapshot_interval));
+    add("output.defect_interval", L(c.output.defect_interval));
+    add("workers", L(c.workers));
+    add("seed", std::to_string(c.seed));
+    add("equilibration_steps", L(c.equilibration_steps));
+    add("displacement_energy", D(c.displacement_energy));
+  } catch (const std::invalid_argument& e) {
+    text = e.what();
+    rc = ORC_INVALID;
+  } catch (const std::exception& e) {
+    text = e.what();
+    rc = ORC_RUNTIME;
+  }
+  std::snprintf(out, cap, "%s", text.c_str());
+  return rc;
+}
+
+int ref_nrt_displacements(double e, double ed, double* out) {
+  try {
+    *out = nrt_displacements(e, ed);
+  } catch (const std::invalid_argument& x) {
+    g_err = x.what();
+    return ORC_INVALID;
+  }
+  return ORC_OK;
+}
+
+}  // extern "C"

@@ -112,6 +112,7 @@ SIGNATURES = [
     ("cbx_make_box", C.c_int, [C.c_long, C.c_long, C.c_long, _D, C.c_long, _D,
                                C.POINTER(Potential), C.POINTER(Box), C.POINTER(C.c_double)]),
     ("cbx_pka_speed", _D, [_D, _D]),
+    ("cbx_write_synthetic_table", C.c_int, [C.c_char_p, C.c_long, C.c_long]),
     ("cbx_adaptive_dt", _D, [_D, _D, _D]),
     ("cbx_create", C.c_int, [C.POINTER(Box), C.POINTER(Potential), C.POINTER(Offsets), C.c_int,
                              C.POINTER(_P)]),
@@ -142,6 +143,7 @@ SIGNATURES = [
     ("cbx_count_pairs", C.c_int, [_P, C.POINTER(C.c_uint64)]),
     ("cbx_kernel_launches", C.c_int, [_P, C.POINTER(C.c_uint64)]),
     ("cbx_describe", C.c_int, [_P, C.c_char_p, C.c_long]),
+    ("cbx_memory_report", C.c_int, [_P, C.POINTER(C.c_longlong)]),
     ("cbx_bench_steps", C.c_int, [_P, _D, C.c_long, _D, C.POINTER(C.c_double)]),
     ("cbx_fp64_peak", C.c_int, [C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     ("cbx_create_slab", C.c_int, [C.POINTER(Box), C.POINTER(Potential), C.POINTER(Offsets),

@@ -84,11 +84,17 @@ struct cbx_ctx {
   std::vector<long> ser_d;
   bool p2p = false;
 
+  // device bytes by structure (cbx_memory_report): the category the next
+  // allocations are charged to
+  int mem_cat = 0;
+  size_t mem_bytes[CBX_MEM_CATEGORIES] = {};
+
   template <class T>
   T* alloc(size_t n) {
     void* p = nullptr;
     if (cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T)) != cudaSuccess)
       raise(CBX_CUDA, "cudaMalloc of " + std::to_string(n * sizeof(T)) + " bytes failed");
+    mem_bytes[mem_cat] += std::max<size_t>(n, 1) * sizeof(T);
     allocs.push_back(p);
     return static_cast<T*>(p);
   }
@@ -135,6 +141,10 @@ cbx_status guarded(cbx_ctx* c, F&& f) {
     if (c) c->err = s.what();
     set_thread_error(s.what());
     return s.code;
+  } catch (const std::invalid_argument& e) {
+    if (c) c->err = e.what();
+    set_thread_error(e.what());
+    return CBX_INVALID_ARGUMENT;
   } catch (const std::exception& e) {
     if (c) c->err = e.what();
     set_thread_error(e.what());
@@ -584,6 +594,7 @@ __global__ void k_export_store(KP P, StoreStage H) {
 StoreStage& stage(cbx_ctx* c) {
   if (!c->stage_pos) {
     const long long S = c->S;
+    c->mem_cat = CBX_MEM_STAGING;
     c->stage_pos = c->alloc<double>(3 * S);
     c->stage_vel = c->alloc<double>(3 * S);
     c->stage_frc = c->alloc<double>(3 * S);
@@ -856,6 +867,10 @@ CBX_API const char* cbx_last_error(const cbx_ctx* c) {
   return c ? c->err.c_str() : thread_error();
 }
 
+CBX_API cbx_status cbx_write_synthetic_table(const char* path, long nrho, long nr) {
+  return guarded(nullptr, [&] { write_synthetic_table(path ? path : "", nrho, nr); });
+}
+
 CBX_API cbx_status cbx_potential_load(const char* path, cbx_potential** out) {
   return guarded(nullptr, [&] {
     auto* p = new Potential(parse_potential(path));
@@ -1109,6 +1124,7 @@ static cbx_status create_impl(const cbx_box* box, const cbx_potential* pot,
     P.S = S;
     P.accel = accel_factor();
     P.mv2 = mv2_to_ev();
+    c->mem_cat = CBX_MEM_SLOTS;
     P.pdf = c->alloc<double4>(S);
     P.rho = c->alloc<double>(S);
     P.vel = c->alloc<double>(3 * S);
@@ -1118,6 +1134,7 @@ static cbx_status create_impl(const cbx_box* box, const cbx_potential* pot,
     P.head = c->alloc<int>(S);
     P.n_gh = (long long)gdst.size();
     c->n_ghost = (int)gdst.size();
+    c->mem_cat = CBX_MEM_GHOSTS;
     P.gh_dst = c->alloc<int>(gdst.size());
     P.gh_src = c->alloc<int>(gsrc.size());
     P.gh_k = c->alloc<signed char>(gk.size());
@@ -1136,8 +1153,10 @@ static cbx_status create_impl(const cbx_box* box, const cbx_potential* pot,
     int items = 1;
     while (items < 2 * cap) items <<= 1;
     P.cap_items = items;
+    c->mem_cat = CBX_MEM_CLASH;
     alloc_clash(c.get(), P.cl, cap);
     alloc_clash(c.get(), P.cl2, cap);
+    c->mem_cat = CBX_MEM_REHASH;
     for (Movers* M : {&P.mv, &P.out}) {
       M->key = c->alloc<long long>(cap);
       M->walk = c->alloc<long long>(cap);
@@ -1153,7 +1172,9 @@ static cbx_status create_impl(const cbx_box* box, const cbx_potential* pot,
       M->tag = c->alloc<unsigned long long>(cap);
     }
     P.cap_rem = std::max(4096, cap / 4);
+    c->mem_cat = CBX_MEM_CLASH;
     alloc_clash(c.get(), P.rem, P.cap_rem);
+    c->mem_cat = CBX_MEM_REHASH;
     P.sc.k1 = c->alloc<long long>(items);
     P.sc.k2 = c->alloc<long long>(items);
     P.sc.k3 = c->alloc<long long>(items);
@@ -1161,6 +1182,7 @@ static cbx_status create_impl(const cbx_box* box, const cbx_potential* pot,
     P.sc.flag = c->alloc<int>(items);
     P.sc.pos = c->alloc<int>(items);
     // tables and partials
+    c->mem_cat = CBX_MEM_TABLES;
     P.dens = upload_tab(c.get(), c->pot.dens);
     P.zr = upload_tab(c.get(), c->pot.zr);
     P.emb = upload_tab(c.get(), c->pot.embed);
@@ -1169,6 +1191,7 @@ static cbx_status create_impl(const cbx_box* box, const cbx_potential* pot,
     P.mass = pot->mass;
     const int np = std::max(std::max(eam_blocks(P), embed_blocks(P)), 4 * 148 * 16);
     P.n_part = np;
+    c->mem_cat = CBX_MEM_REDUCTION;
     P.part_emb = c->alloc<double>(np);
     P.part_pair = c->alloc<double>(np);
     P.part_ke = c->alloc<double>(np);
@@ -1177,10 +1200,14 @@ static cbx_status create_impl(const cbx_box* box, const cbx_potential* pot,
     cudaMemset(P.part_pair, 0, np * sizeof(double));
     cudaMemset(P.part_ke, 0, np * sizeof(double));
     cudaMemset(P.part_vmax, 0, np * sizeof(double));
+    c->mem_cat = CBX_MEM_SLOTS;
     P.uf = c->alloc<float4>(S);
+    c->mem_cat = CBX_MEM_REDUCTION;
     P.work = c->alloc<int>(4);
     cudaMemset(P.work, 0, 4 * sizeof(int));
+    c->mem_cat = CBX_MEM_TABLES;
     setup_fast(c.get());
+    c->mem_cat = CBX_MEM_REDUCTION;
     P.st = c->alloc<DevStatus>(1);
     P.dself = c->alloc<KP>(1);
     c->d_rem_base = c->alloc<int>(2);
@@ -1188,10 +1215,12 @@ static cbx_status create_impl(const cbx_box* box, const cbx_potential* pot,
     {
       const int maxn = std::max(std::max(fd[0].size(), fd[1].size()), std::max(hd[0].size(), hd[1].size()));
       const char* nm = std::getenv("CBX_NOMASK");
+      c->mem_cat = CBX_MEM_SLOTS;
       P.pmask = maxn <= 126 && !(nm && std::atoi(nm)) ? c->alloc<unsigned long long>(2 * S)
                                                        : nullptr;
     }
 
+    c->mem_cat = CBX_MEM_REDUCTION;
     c->d_defects = c->alloc<unsigned long long>(4);
     // empty store: every slot vacant
     std::vector<double4> vac(S, make_double4(kVacant, kVacant, kVacant, 0.0));
@@ -1996,6 +2025,18 @@ CBX_API cbx_status cbx_describe(cbx_ctx* c, char* buf, long n) {
   });
 }
 
+CBX_API cbx_status cbx_memory_report(cbx_ctx* c, long long out[CBX_MEM_CATEGORIES + 4]) {
+  return guarded(c, [&] {
+    for (int k = 0; k < CBX_MEM_CATEGORIES; ++k) out[k] = (long long)c->mem_bytes[k];
+    out[CBX_MEM_CATEGORIES] = c->S;                       // slots (ghost-inclusive)
+    out[CBX_MEM_CATEGORIES + 1] = c->P.cap_clash;         // clash capacity (records)
+    out[CBX_MEM_CATEGORIES + 2] = c->n_ghost;             // ghost links
+    out[CBX_MEM_CATEGORIES + 3] = (long long)(           // offset lists (__constant__)
+        sizeof(int) * (c->c_fd[0].size() + c->c_fd[1].size() + c->c_hd[0].size() +
+                       c->c_hd[1].size()));
+  });
+}
+
 CBX_API cbx_status cbx_kernel_launches(cbx_ctx* c, uint64_t* n) {
   *n = c->launches;
   return CBX_OK;
@@ -2209,6 +2250,7 @@ CBX_API cbx_status cbx_slab_comm_init(cbx_ctx* c, const void* id, long nbytes) {
     std::memcpy(&u, id, sizeof u);
     long long mx = 0;
     for (int k = 0; k < 5; ++k) mx = std::max(mx, slab_msg_bytes(c->P, k));
+    c->mem_cat = CBX_MEM_EXCHANGE;
     for (int i = 0; i < 2; ++i) {
       c->sbuf[i] = c->alloc<unsigned char>(mx);
       c->rbuf[i] = c->alloc<unsigned char>(mx);
@@ -2248,6 +2290,7 @@ CBX_API cbx_status cbx_slab_p2p_handle(cbx_ctx* c, void* out, long nbytes) {
     if (!c->p2p_region) {
       c->p2p_bytes = p2p_buf_off(c->P, 5, 0);
       cuda_check(cudaMalloc(&c->p2p_region, c->p2p_bytes), "p2p region");
+      c->mem_bytes[CBX_MEM_EXCHANGE] += c->p2p_bytes;
       cuda_check(cudaMemset(c->p2p_region, 0, c->p2p_bytes), "p2p region");
     }
     cudaIpcMemHandle_t h;
@@ -2305,6 +2348,7 @@ CBX_API cbx_status cbx_slab_p2p_init(cbx_ctx* c, const void* handles, long nbyte
     }
     L.red_src = reinterpret_cast<const double*>(c->p2p_region + kRedOff);
     L.red_flag_src = reinterpret_cast<const unsigned long long*>(c->p2p_region + kRedFlagOff);
+    c->mem_cat = CBX_MEM_EXCHANGE;
     L.epoch = c->alloc<unsigned long long>(6);
     L.done = c->alloc<unsigned>(6);
     cudaMemset(L.epoch, 0, 6 * sizeof(unsigned long long));

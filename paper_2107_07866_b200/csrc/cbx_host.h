@@ -42,6 +42,8 @@ struct Potential {
 };
 // src/potential.cpp:134-185
 Potential parse_potential(const std::string& path);
+// synthetic::write_table (synthetic.cpp:49-98): the reference's test table
+void write_synthetic_table(const std::string& path, long nrho, long nr);
 
 // one neighbour offset in cell units: partner cell = cell + (dx, dy, dz),
 // partner sublattice = par ^ cross

@@ -344,4 +344,65 @@ HostLattice init_bcc_slab(const cbx_box& global, const Geo& local, double mass,
   return L;
 }
 
+// ---- synthetic::write_table (synthetic.cpp:10-98, synthetic.h:19-32) ------
+// The reference's own single-element test table: rho = A (rc - r)^3,
+// phi = B exp(-s (r/rnn - 1)) ((rc - r)/(rc - rnn))^3, F = -C (sqrt(rho + e) -
+// sqrt(e)).  Same constants, same operation order, same %.17g layout.
+namespace {
+namespace syn {
+constexpr int atomic_number = 26;
+constexpr double mass = 55.845;
+constexpr double a0 = 2.8553;
+constexpr double cutoff = 5.6;
+constexpr double r_nn = 2.4727640449591856;
+constexpr double rho_rc = 4.1;
+constexpr double rho_amp = 0.02171868164588797;
+constexpr double pair_slope = 6.5;
+constexpr double pair_amp = 0.5123847826890735;
+constexpr double embed_amp = 9.053882773088201;
+constexpr double embed_reg = 0.09;
+constexpr double rho_table_max = 4.0;
+
+double density(double r) {
+  if (r >= rho_rc) return 0.0;
+  const double t = rho_rc - r;
+  return rho_amp * t * t * t;
+}
+double zfun(double r) {
+  if (r >= cutoff) return r * 0.0;
+  const double damp = (cutoff - r) / (cutoff - r_nn);
+  return r * (pair_amp * std::exp(-pair_slope * (r / r_nn - 1.0)) * damp * damp * damp);
+}
+double embedding(double rho) {
+  return -embed_amp * (std::sqrt(rho + embed_reg) - std::sqrt(embed_reg));
+}
+}  // namespace syn
+}  // namespace
+
+void write_synthetic_table(const std::string& path, long nrho, long nr) {
+  if (nrho < 4 || nr < 4)
+    throw std::invalid_argument("write_table: need at least 4 knots per table");
+  std::FILE* f = std::fopen(path.c_str(), "w");
+  if (!f) throw std::runtime_error("write_table: cannot open '" + path + "' for writing");
+  using namespace syn;
+  std::fprintf(f,
+               "synthetic Fe-like EAM: rho=%.17g*(%.17g-r)^3; "
+               "phi=%.17g*exp(-%.17g*(r/%.17g-1))*((%.17g-r)/(%.17g-%.17g))^3; "
+               "F=-%.17g*(sqrt(rho+%.17g)-sqrt(%.17g))\n",
+               rho_amp, rho_rc, pair_amp, pair_slope, r_nn, cutoff, cutoff, r_nn, embed_amp,
+               embed_reg, embed_reg);
+  std::fprintf(f, "%d %.17g %.17g bcc\n", atomic_number, mass, a0);
+  const double drho = rho_table_max / (double)(nrho - 1);
+  const double dr = cutoff / (double)nr;
+  std::fprintf(f, "%ld %.17g %ld %.17g %.17g\n", nrho, drho, nr, dr, cutoff);
+  auto block = [f](long n, auto value) {  // four values per line
+    for (long i = 0; i < n; ++i) std::fprintf(f, "%.17g%c", value(i), (i % 4 == 3) ? '\n' : ' ');
+    if (n % 4 != 0) std::fputc('\n', f);
+  };
+  block(nrho, [&](long k) { return embedding(drho * (double)k); });
+  block(nr, [&](long k) { return zfun(dr * (double)(k + 1)); });
+  block(nr, [&](long k) { return density(dr * (double)(k + 1)); });
+  if (std::fclose(f) != 0) throw std::runtime_error("write_table: write error on '" + path + "'");
+}
+
 }  // namespace cbx

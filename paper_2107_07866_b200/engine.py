@@ -71,6 +71,7 @@ class SimConfig:  # config.h:36-53
     workers: int = 1
     seed: int = 12345
     equilibration_steps: int = 0
+    displacement_energy: float = 40.0  # eV, NRT threshold (analysis.cpp:58-65)
     device: int = 0
     stencil: str = "newton3"
 
@@ -392,6 +393,20 @@ class DeviceStore:
         self._check(self.lib.cbx_describe(self.h, buf, 1024))
         return json.loads(buf.value.decode())
 
+    MEM_CATEGORIES = ("slots", "clash", "ghosts", "rehash", "tables", "reduction",
+                      "staging", "exchange")
+
+    def memory_report(self) -> dict:
+        """device bytes by structure (cbx_memory_report) plus the slot, clash
+        capacity, ghost-link and offset-list counts"""
+        n = len(self.MEM_CATEGORIES)
+        out = (C.c_longlong * (n + 4))()
+        self._check(self.lib.cbx_memory_report(self.h, out))
+        r = {k: int(out[i]) for i, k in enumerate(self.MEM_CATEGORIES)}
+        r.update(n_slots=int(out[n]), clash_capacity=int(out[n + 1]),
+                 ghost_links=int(out[n + 2]), offset_bytes=int(out[n + 3]))
+        return r
+
     def kernel_launches(self) -> int:
         n = C.c_uint64()
         self._check(self.lib.cbx_kernel_launches(self.h, C.byref(n)))
@@ -487,6 +502,11 @@ class Simulation:
             c.output.timeseries.encode(), c.output.snapshot_prefix.encode(),
             c.output.snapshot_interval, c.output.defect_interval,
             (C.c_long * 3)(*c.pka.site), c.pka.energy_kev, (C.c_long * 3)(*c.pka.direction))
+
+    def post_mortem_path(self) -> str:
+        """sim.cpp:284-287: the snapshot a failed step leaves behind"""
+        p = self.cfg.output.snapshot_prefix
+        return p + "_postmortem.xyz" if p else ""
 
     def run(self, log: str = ""):
         """Simulation::run (sim.cpp:289-360); log: path, "-" for stdout, "" none"""

@@ -123,3 +123,27 @@ def test_cxx_host_header_compiles_and_runs(tmp_path, tables):
     out = subprocess.run([exe, tables["baseline"]], capture_output=True, text=True, check=True)
     assert "offsets 112/112 half 46/66" in out.stdout
     assert "runtime_error: cannot open potential file" in out.stdout
+
+
+@pytest.mark.gpu
+def test_cxx_engine_and_slab_engine_on_device(tmp_path, tables):
+    """the C++ mirror drives the single-box Engine and a one-rank SlabEngine
+    (peer-memory transport to itself) to the same trajectory"""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2107_07866_b200 import _lib
+    _lib.load()
+    exe = str(tmp_path / "cxx_host")
+    libdir = os.path.dirname(_lib.LIB_PATH)
+    subprocess.run(["g++", "-std=c++17", "-O1", "-I", os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "examples", "cxx_host.cpp"), "-L", libdir,
+                    "-l:libcascade_b200.so", f"-Wl,-rpath,{libdir}", "-o", exe], check=True)
+    out = subprocess.run([exe, tables["baseline"], "gpu", "slab"], capture_output=True,
+                         text=True, check=True, timeout=300).stdout
+    box = [ln for ln in out.splitlines() if ln.startswith("atoms")][0]
+    slab = [ln for ln in out.splitlines() if ln.startswith("slab atoms")][0]
+    assert box.split()[1] == slab.split()[2] == "1024"
+    ke_box, ke_slab = float(box.split()[-1]), float(slab.split()[-1])
+    assert box.split()[-3] == slab.split()[-3] == "10"
+    assert abs(ke_box - ke_slab) <= 1e-9 * ke_box
