@@ -172,6 +172,35 @@ __device__ __forceinline__ void zero_pair_tail(const KP& P, int written) {
   if (blockIdx.x == 0)
     for (int i = written + threadIdx.x; i < P.n_pair_part; i += blockDim.x) P.part_pair[i] = 0.0;
 }
+
+// Programmatic dependent launch (PDL) on the step path: a kernel launched by
+// launch_pdl may start while its predecessor in the stream drains (its CTAs
+// take SMs as the predecessor's leave, its launch latency and constant-table
+// staging overlap the predecessor's tail).  Every such kernel executes
+// pdl_wait() -- which returns once the predecessor grid has completed and its
+// writes are visible -- before it reads or writes anything the stream's
+// earlier work touches, then pdl_trigger() to let its own successor launch.
+// Without the launch attribute both are no-ops.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+bool pdl_enabled();  // CBX_PDL (default on)
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                       Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, k, args...);
+}
 #endif
 
 // device entry points (launch wrappers), implemented in the .cu files

@@ -323,6 +323,8 @@ __device__ void clash_embed_body(const KP& P, int blk, int nblk) {
 // blocks [0, nsb): all slots, grid-stride, one energy partial per block;
 // blocks [nsb, grid): the clash records (fused k_clash_embed)
 __global__ void __launch_bounds__(256) k_embed(KP P, int nsb, int literal) {
+  pdl_wait();
+  pdl_trigger();
   if (blockIdx.x >= nsb) {
     clash_embed_body(P, blockIdx.x - nsb, gridDim.x - nsb);
     // the records' force accumulators for the force pass (clash_zero fused)
@@ -518,7 +520,7 @@ int pair_partials(const KP& P, int mode) {
 }
 void launch_embed(const KP& P, cudaStream_t s, bool literal) {
   const int nsb = embed_grid(P);
-  k_embed<<<nsb + 16, 256, 0, s>>>(P, nsb, literal ? 1 : 0);
+  launch_pdl(k_embed, nsb + 16, 256, 0, s, P, nsb, literal ? 1 : 0);
 }
 void launch_clash_density(const KP& P, cudaStream_t s) { k_clash<0><<<16, 256, 0, s>>>(P); }
 void launch_clash_force(const KP& P, cudaStream_t s) { k_clash<1><<<16, 256, 0, s>>>(P); }

@@ -610,10 +610,11 @@ constexpr int kDensTabRecords = 3300;  // x 32 B = 105,600 B
 template <bool FULL, int B, int NT>
 __global__ void __launch_bounds__(NT, 1) k_density_smem(KP P, int nsb) {
   if (blockIdx.x >= nsb) {
+    pdl_wait();
+    pdl_trigger();
     clash_body<0>(P, blockIdx.x - nsb, gridDim.x - nsb);
     return;
   }
-  if (P.st->err) return;
   extern __shared__ __align__(16) unsigned char smem_tab[];
   __shared__ int s_slot[NT / 128];
   double2* T = reinterpret_cast<double2*>(smem_tab);
@@ -621,8 +622,12 @@ __global__ void __launch_bounds__(NT, 1) k_density_smem(KP P, int nsb) {
   const int seg_lo = max(0, nseg + 1 - kDensTabRecords);
   const int nrec = nseg + 1 - seg_lo;
   const double2* src = reinterpret_cast<const double2*>(P.fd.rec + 4 * (size_t)seg_lo);
+  // the constant table is staged while the predecessor drains (PDL)
   for (int q = threadIdx.x; q < 2 * nrec; q += blockDim.x) T[smem_slot32(q >> 1, q & 1)] = __ldg(src + q);
   __syncthreads();
+  pdl_wait();
+  pdl_trigger();
+  if (P.st->err) return;
   const int group = threadIdx.x >> 7;
   const int lt = threadIdx.x & 127, lane = lt & 31, w = lt >> 5;
   const Geo& G = P.G;
@@ -686,12 +691,12 @@ constexpr int kLeanTabRecords = 3300;  // x 64 B = 211,200 B
 
 template <bool FULL, int NT>
 __global__ void __launch_bounds__(NT, 1) k_force_lean_smem(KP P, int nsb) {
-  zero_pair_tail(P, nsb * blockDim.x / 32);
   if (blockIdx.x >= nsb) {
+    pdl_wait();
+    pdl_trigger();
     clash_body<1>(P, blockIdx.x - nsb, gridDim.x - nsb);
     return;
   }
-  if (P.st->err || P.st->n_ovl) return;
   extern __shared__ __align__(16) unsigned char smem_tab[];
   __shared__ int s_slot[8];
   double2* T = reinterpret_cast<double2*>(smem_tab);
@@ -707,6 +712,10 @@ __global__ void __launch_bounds__(NT, 1) k_force_lean_smem(KP P, int nsb) {
     g_soffs[par][k] = k < n ? (FULL ? c_full[par][k] : c_half[par][k]) : 0;
   }
   __syncthreads();
+  pdl_wait();
+  pdl_trigger();
+  zero_pair_tail(P, nsb * blockDim.x / 32);
+  if (P.st->err || P.st->n_ovl) return;
   const int group = threadIdx.x >> 7;
   const int lt = threadIdx.x & 127, lane = lt & 31, w = lt >> 5;
   const Geo& G = P.G;
@@ -775,8 +784,8 @@ bool launch_density_fast(const KP& P, int mode, int grid, cudaStream_t s) {
       attr = true;
     }
     const int g = max(1, min(sm_count(), (brick_count(P.G) + 7) / 8));
-    if (mode) k_density_smem<true, 1, 1024><<<g, 1024, bytes, s>>>(P, g);
-    else k_density_smem<false, 1, 1024><<<g + 4, 1024, bytes, s>>>(P, g);
+    if (mode) launch_pdl(k_density_smem<true, 1, 1024>, g, 1024, bytes, s, P, g);
+    else launch_pdl(k_density_smem<false, 1, 1024>, g + 4, 1024, bytes, s, P, g);
     return !mode;
   }
   const int ex = mode ? 0 : kClashBlocks128;  // fused clash pass (Newton-3)
@@ -800,8 +809,8 @@ bool launch_force_fast(const KP& P, int mode, int grid, cudaStream_t s) {
       attr = true;
     }
     const int g = max(1, min(sm_count(), (brick_count(P.G) + 7) / 8));
-    if (mode) k_force_lean_smem<true, 1024><<<g, 1024, bytes, s>>>(P, g);
-    else k_force_lean_smem<false, 1024><<<g + 4, 1024, bytes, s>>>(P, g);
+    if (mode) launch_pdl(k_force_lean_smem<true, 1024>, g, 1024, bytes, s, P, g);
+    else launch_pdl(k_force_lean_smem<false, 1024>, g + 4, 1024, bytes, s, P, g);
     return !mode;
   }
   if (mode) k_force_fast<true, 2><<<grid, 128, 0, s>>>(P);

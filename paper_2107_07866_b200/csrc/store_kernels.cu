@@ -290,6 +290,8 @@ __device__ __forceinline__ void copy_record(const Clash& a, int i, const Clash& 
 // (hash, walk key, class, order) makes the group's first record the one
 // that claims a free slot and the rest the new bucket, in order.
 __global__ void __launch_bounds__(1024) k_rehash(KP P) {
+  pdl_wait();
+  pdl_trigger();
   if (P.st->err) return;
   const int n_old = P.st->n_clash;
   const int n_mov = min(P.st->n_mov, P.cap_mov);
@@ -418,6 +420,8 @@ __global__ void __launch_bounds__(1024) k_rehash(KP P) {
 // each ghost site has one periodic source; its image position is the
 // source's plus k*len, added per axis exactly like store.cpp:166-169
 __global__ void k_ghost_fill(KP P) {
+  pdl_wait();
+  pdl_trigger();
   if (P.st->err) return;
   const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= P.n_gh) return;
@@ -461,6 +465,8 @@ __device__ __forceinline__ int image_count(long long id, const Geo& G) {
 }
 
 __global__ void __launch_bounds__(1024) k_clash_images(KP P, int zero_rho) {
+  pdl_wait();
+  pdl_trigger();
   if (zero_rho && threadIdx.x == 0) P.work[0] = 0;  // the density pass's brick queue
   if (P.st->err) return;
   const int n = P.st->n_clash;
@@ -627,6 +633,8 @@ __device__ void clash_kick2_body(const KP& P, int kick, int blk, int nblk) {
 }
 
 __global__ void __launch_bounds__(256) k_kick2(KP P, int kick, int nsb) {
+  pdl_wait();
+  pdl_trigger();
   if (blockIdx.x >= nsb) {  // the clash records (fused k_clash_kick2)
     clash_kick2_body(P, kick, blockIdx.x - nsb, gridDim.x - nsb);
     return;
@@ -749,6 +757,8 @@ __device__ void finalize_body(const KP& P, int stepping, int energies, const dou
 __global__ void __launch_bounds__(1024) k_finalize(KP P, int stepping, int energies,
                                                    int n_pairp, int n_emb, int n_ke,
                                                    const P2PLinks* L) {
+  pdl_wait();
+  pdl_trigger();
   finalize_body<1024>(P, stepping, energies, P.part_emb, n_emb, P.part_pair, n_pairp, n_ke);
   if (L) {
     __syncthreads();
@@ -785,12 +795,12 @@ void launch_kick_drift(const KP& P, int move, cudaStream_t s, int zero_acc) {
   const int nsb = eam_blocks(P);
   k_kick_drift<<<nsb + kClashBlocks, 256, 0, s>>>(P, move, nsb, zero_acc);
 }
-void launch_rehash(const KP& P, cudaStream_t s) { k_rehash<<<1, 1024, 0, s>>>(P); }
+void launch_rehash(const KP& P, cudaStream_t s) { launch_pdl(k_rehash, 1, 1024, 0, s, P); }
 void launch_ghost_fill(const KP& P, cudaStream_t s) {
-  if (P.n_gh) k_ghost_fill<<<(int)((P.n_gh + 255) / 256), 256, 0, s>>>(P);
+  if (P.n_gh) launch_pdl(k_ghost_fill, (int)((P.n_gh + 255) / 256), 256, 0, s, P);
 }
 void launch_clash_images(const KP& P, cudaStream_t s, int zero_rho) {
-  k_clash_images<<<1, 1024, 0, s>>>(P, zero_rho);
+  launch_pdl(k_clash_images, 1, 1024, 0, s, P, zero_rho);
 }
 void launch_clash_zero(const KP& P, int what, cudaStream_t s) {
   k_clash_zero<<<8, 256, 0, s>>>(P, what);
@@ -798,16 +808,26 @@ void launch_clash_zero(const KP& P, int what, cudaStream_t s) {
 int kick_grid(const KP& P) { return eam_blocks(P); }
 void launch_kick2(const KP& P, int kick, int stepping, int energies, cudaStream_t s) {
   const int nsb = kick_grid(P);
-  k_kick2<<<nsb + kClashBlocks, 256, 0, s>>>(P, kick, nsb);
+  launch_pdl(k_kick2, nsb + kClashBlocks, 256, 0, s, P, kick, nsb);
   if (stepping > -2) launch_finalize(P, stepping, energies, s);
 }
 void launch_finalize(const KP& P, int stepping, int energies, cudaStream_t s,
                      const P2PLinks* links) {
-  k_finalize<<<1, 1024, 0, s>>>(P, stepping, energies, P.n_pair_part, embed_grid(P),
-                                kick_grid(P), links);
+  launch_pdl(k_finalize, 1, 1024, 0, s, P, stepping, energies, P.n_pair_part, embed_grid(P),
+             kick_grid(P), links);
 }
 void launch_count_defects(const KP& P, unsigned long long* out, cudaStream_t s) {
   k_count_defects<<<eam_blocks(P), 256, 0, s>>>(P, out);
 }
 
+}  // namespace cbx
+
+namespace cbx {
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("CBX_PDL");
+    return e ? atoi(e) != 0 : true;
+  }();
+  return on;
+}
 }  // namespace cbx
