@@ -267,19 +267,22 @@ void seq_density(cbx_ctx* c) {
   if (c->mode != CBX_STENCIL_FULL && !c->acc_rho_zero)
     cudaMemsetAsync(c->P.rho, 0, c->S * sizeof(double), c->stream);
   c->acc_rho_zero = false;
-  if (!c->clash_rho_zero) launch_clash_zero(c->P, 0, c->stream);
+  if (!c->clash_rho_zero) {
+    launch_clash_zero(c->P, 0, c->stream);
+    c->launches += 1;
+  }
   c->clash_rho_zero = false;
   if (!launch_density(c->P, c->mode, c->stream)) {
     launch_clash_density(c->P, c->stream);
     c->launches += 1;
   }
-  c->launches += 2;
+  c->launches += 1;
   c->mask_valid = c->mode != CBX_STENCIL_REFERENCE && c->P.pmask != nullptr;
 }
 void seq_embed(cbx_ctx* c) {
   launch_embed(c->P, c->stream, c->mode == CBX_STENCIL_REFERENCE);
   c->clash_f_zero = true;
-  c->launches += 2;
+  c->launches += 1;
 }
 void seq_force(cbx_ctx* c) {
   // the embedding pass resets the brick counter and the clash records'
@@ -288,7 +291,10 @@ void seq_force(cbx_ctx* c) {
   if (c->mode != CBX_STENCIL_FULL && !c->acc_frc_zero)
     cudaMemsetAsync(c->P.frc, 0, 3 * c->S * sizeof(double), c->stream);
   c->acc_frc_zero = false;
-  if (!c->clash_f_zero) launch_clash_zero(c->P, 1, c->stream);
+  if (!c->clash_f_zero) {
+    launch_clash_zero(c->P, 1, c->stream);
+    c->launches += 1;
+  }
   c->clash_f_zero = false;
   KP q = c->P;
   q.use_mask = c->mask_valid ? 1 : 0;
@@ -299,7 +305,7 @@ void seq_force(cbx_ctx* c) {
     launch_clash_force(c->P, c->stream);
     c->launches += 1;
   }
-  c->launches += 2;
+  c->launches += 1;
 }
 // ---- z-slab ranks: exchanges and reductions inside the step (NCCL) -------
 // Both halves of one exchange go out in one NCCL group: my "down" packet to
@@ -312,8 +318,8 @@ void slab_exchange(cbx_ctx* c, int kind) {
   if (c->p2p) {  // fused: pack into the neighbours' memory, wait, unpack
     const long long gs_lo = (kind == 1 && c->rank == 0) ? -1 : 0;
     const long long gs_hi = (kind == 1 && c->rank == c->nranks - 1) ? 1 : 0;
-    launch_p2p_exchange(c->P, c->links, kind, gs_lo, gs_hi, c->d_rem_base, c->stream);
-    c->launches += 2;
+    c->launches += launch_p2p_exchange(c->P, c->links, kind, gs_lo, gs_hi, c->d_rem_base,
+                                       c->stream);
     return;
   }
   const NcclApi& N = nccl();
@@ -365,7 +371,7 @@ void slab_finish(cbx_ctx* c, int kick, int stepping, int energies) {
   if (c->p2p) {
     if (kick >= 0) {
       launch_kick2(c->P, kick, -2, 0, c->stream);
-      c->launches += 2;
+      c->launches += 1;
     }
     launch_finalize(c->P, stepping, energies, c->stream, c->d_links);
     c->launches += 1;
@@ -373,7 +379,7 @@ void slab_finish(cbx_ctx* c, int kick, int stepping, int energies) {
   }
   if (kick >= 0) {
     launch_kick2(c->P, kick, stepping, energies, c->stream);
-    c->launches += 3;
+    c->launches += 2;
   } else {
     launch_finalize(c->P, stepping, energies, c->stream);
     c->launches += 1;
@@ -392,7 +398,7 @@ void seq_slab_step(cbx_ctx* c) {
   slab_exchange(c, 0);  // migrants
   launch_rehash(c->P, c->stream);
   launch_ghost_fill(c->P, c->stream);
-  c->launches += 4;
+  c->launches += 3;
   memset_field(c, &c->P.st->n_remote);
   slab_exchange(c, 1);  // positions
   ev_mark(c, 1);
@@ -446,11 +452,13 @@ void seq_step(cbx_ctx* c) {
   c->mask_valid = false;
   ev_mark(c, 0);
   const bool zacc = c->mode != CBX_STENCIL_FULL;  // single box: no remote halo sites
-  launch_kick_drift(c->P, 1, c->stream, zacc ? 1 : 0);
+  // kick, drift, hash pass 1 and the slot images in one launch; hash pass 2
+  // and the clash images in one single-block launch (no k_ghost_fill)
+  launch_kick_drift(c->P, 1, c->stream, zacc ? 1 : 0, 1);
   c->acc_rho_zero = c->acc_frc_zero = zacc;
-  launch_rehash(c->P, c->stream);
-  c->launches += 3;
-  seq_fill_ghosts(c, true);
+  launch_rehash_images(c->P, c->stream);
+  c->clash_rho_zero = true;
+  c->launches += 2;
   ev_mark(c, 1);
   seq_density(c);
   ev_mark(c, 2);
@@ -459,7 +467,7 @@ void seq_step(cbx_ctx* c) {
   seq_force(c);
   ev_mark(c, 4);
   launch_kick2(c->P, 1, 1, 1, c->stream);
-  c->launches += 3;
+  c->launches += 2;
   ev_mark(c, 5);
 }
 
@@ -1336,7 +1344,7 @@ CBX_API cbx_status cbx_rehash(cbx_ctx* c) {
     require_box(c, "cbx_rehash");
     launch_kick_drift(c->P, 0, c->stream);
     launch_rehash(c->P, c->stream);
-    c->launches += 3;
+    c->launches += 2;
     seq_fill_ghosts(c);
     sync_status(c);
     raise_device_error(c, false);
@@ -1482,7 +1490,7 @@ CBX_API cbx_status cbx_measure(cbx_ctx* c) {
       slab_finish(c, 0, 0, 0);
     } else {
       launch_kick2(c->P, 0, 0, 0, c->stream);
-      c->launches += 3;
+      c->launches += 2;
     }
     sync_status(c);
     raise_device_error(c, false);
@@ -2103,7 +2111,7 @@ CBX_API cbx_status cbx_slab_phase(cbx_ctx* c, int phase, double dt) {
         write_status(c);
         c->mask_valid = false;
         launch_kick_drift(c->P, 1, c->stream);
-        c->launches += 2;
+        c->launches += 1;
         break;
       case 1:
         launch_rehash(c->P, c->stream);
@@ -2129,7 +2137,7 @@ CBX_API cbx_status cbx_slab_phase(cbx_ctx* c, int phase, double dt) {
         break;
       case 5:
         launch_kick2(c->P, 1, 1, 1, c->stream);
-        c->launches += 3;
+        c->launches += 2;
         break;
       case 6:
         launch_finalize(c->P, -1, 1, c->stream);
@@ -2137,7 +2145,7 @@ CBX_API cbx_status cbx_slab_phase(cbx_ctx* c, int phase, double dt) {
         break;
       case 7:  // measure only (kinetic energy, max speed)
         launch_kick2(c->P, 0, 0, 0, c->stream);
-        c->launches += 3;
+        c->launches += 2;
         break;
       default:
         raise(CBX_INVALID_ARGUMENT, "cbx_slab_phase: unknown phase");

@@ -210,8 +210,11 @@ void launch_clash_density(const KP& P, cudaStream_t s);
 void launch_embed(const KP& P, cudaStream_t s, bool literal = false);
 bool launch_force(const KP& P, int mode, cudaStream_t s);
 void launch_clash_force(const KP& P, cudaStream_t s);
-// zero_acc: clear the interior sites' rho / force accumulators as well
-void launch_kick_drift(const KP& P, int move, cudaStream_t s, int zero_acc = 0);
+// zero_acc: clear the interior sites' rho / force accumulators as well;
+// images: write each site's ghost images too (the step path, no ghost fill)
+void launch_kick_drift(const KP& P, int move, cudaStream_t s, int zero_acc = 0, int images = 0);
+// update_hash pass 2 + ghost clash images in one single-block launch
+void launch_rehash_images(const KP& P, cudaStream_t s);
 void launch_clash_zero(const KP& P, int what, cudaStream_t s);
 void launch_rehash(const KP& P, cudaStream_t s);
 void launch_ghost_fill(const KP& P, cudaStream_t s);
@@ -252,7 +255,7 @@ constexpr int kMaxP2PRanks = 8;
 // reduction runs in the same kernel
 void launch_finalize(const KP& P, int stepping, int energies, cudaStream_t s,
                      const P2PLinks* links = nullptr);
-void launch_p2p_exchange(const KP& P, const P2PLinks& L, int kind, long long gs_lo,
+int launch_p2p_exchange(const KP& P, const P2PLinks& L, int kind, long long gs_lo,
                          long long gs_hi, int* rem_base, cudaStream_t s);
 void launch_p2p_reduce(const KP& P, const P2PLinks& L, int energies, int kinetic,
                        cudaStream_t s);

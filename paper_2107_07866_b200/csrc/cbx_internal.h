@@ -72,6 +72,13 @@ CBX_HD long long ref_of_dev(long long d, long long NC) {
 
 // cell coordinates (ghost-inclusive, cell units) of a cell index
 CBX_HD void cell_xyz(long long cell, const Geo& G, int& cx, int& cy, int& cz) {
+  if (cell < (1ll << 31)) {  // 32-bit division (every box that fits one GPU)
+    const unsigned c = (unsigned)cell, r = c / (unsigned)G.tx;
+    cx = (int)(c - r * (unsigned)G.tx);
+    cy = (int)(r % (unsigned)G.ty);
+    cz = (int)(r / (unsigned)G.ty);
+    return;
+  }
   cx = (int)(cell % G.tx);
   const long long r = cell / G.tx;
   cy = (int)(r % G.ty);
@@ -86,6 +93,13 @@ CBX_HD bool cell_is_ghost(int cx, int cy, int cz, const Geo& G) {
 }
 // interior enumeration e in [0, NI) -> cell, x fastest (matches for_each_interior_id order)
 CBX_HD long long interior_cell(long long e, const Geo& G) {
+  if (e < (1ll << 31)) {
+    const unsigned u = (unsigned)e, r = u / (unsigned)G.bx;
+    const int cx = (int)(u - r * (unsigned)G.bx);
+    const int cy = (int)(r % (unsigned)G.by);
+    const int cz = (int)(r / (unsigned)G.by);
+    return cell_of(cx + G.g, cy + G.g, cz + G.g, G);
+  }
   const int cx = (int)(e % G.bx);
   const long long r = e / G.bx;
   const int cy = (int)(r % G.by);

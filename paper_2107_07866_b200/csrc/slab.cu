@@ -524,8 +524,8 @@ void launch_unpack(const KP& P, int kind, int from, const unsigned char* buf, lo
 
 void launch_remote_df(const KP& P, cudaStream_t s) { k_remote_df<<<8, 256, 0, s>>>(P); }
 
-void launch_p2p_exchange(const KP& P, const P2PLinks& L, int kind, long long gs_lo,
-                         long long gs_hi, int* rem_base, cudaStream_t s) {
+int launch_p2p_exchange(const KP& P, const P2PLinks& L, int kind, long long gs_lo,
+                        long long gs_hi, int* rem_base, cudaStream_t s) {
   static const int fused = [] {
     const char* e = getenv("CBX_P2P_SPLIT");
     return e ? !atoi(e) : 1;
@@ -541,12 +541,13 @@ void launch_p2p_exchange(const KP& P, const P2PLinks& L, int kind, long long gs_
     }
     const int grid = kind == 0 ? 2 : std::min(plane_grid(P, 2), cap);
     k_p2p_xchg<<<grid, 256, 0, s>>>(P, L, kind, gs_lo, gs_hi, rem_base);
-    return;
+    return 1;
   }
   const int grid = kind == 0 ? 2 : plane_grid(P, 2);
   k_p2p_send<<<grid, 256, 0, s>>>(P, L, kind);
   k_p2p_recv<<<kind == 0 ? 8 : plane_grid(P, 2), 256, 0, s>>>(P, L, kind, gs_lo, gs_hi,
                                                                 rem_base);
+  return 2;
 }
 void launch_p2p_reduce(const KP& P, const P2PLinks& L, int energies, int kinetic,
                        cudaStream_t s) {

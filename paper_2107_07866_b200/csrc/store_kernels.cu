@@ -42,7 +42,10 @@ __device__ void clash_kick_drift_body(const KP& P, int move, int blk, int nblk);
 // zero_acc: also clear the site's rho / force accumulators once the half
 // kick has read the force (the density and force passes of this step add
 // into them; replaces two full-array memsets)
-__global__ void __launch_bounds__(256) k_kick_drift(KP P, int move, int nsb, int zero_acc) {
+// images: also write the site's ghost images (the step path's k_ghost_fill)
+__device__ void ghost_images(const KP& P, long long d, const double4& p);
+__global__ void __launch_bounds__(256) k_kick_drift(KP P, int move, int nsb, int zero_acc,
+                                                    int images) {
   if (P.st->err) return;
   if (blockIdx.x >= nsb) {  // the clash records (fused k_clash_kick_drift)
     clash_kick_drift_body(P, move, blockIdx.x - nsb, gridDim.x - nsb);
@@ -51,8 +54,12 @@ __global__ void __launch_bounds__(256) k_kick_drift(KP P, int move, int nsb, int
   int par;
   long long d;
   if (!map_site(P, par, d)) return;
-  double4 p = P.pdf[d];
+  // every load of the site issued before the first use (one round trip)
   const long long S = P.S;
+  double4 p = P.pdf[d];
+  double vx = P.vel[d], vy = P.vel[S + d], vz = P.vel[2 * S + d];
+  const double fx = P.frc[d], fy = P.frc[S + d], fz = P.frc[2 * S + d];
+  const double dt = P.st->dt_next;
   if (p.x >= kVacantTest) {
     if (zero_acc) {
       P.rho[d] = 0.0;
@@ -60,15 +67,14 @@ __global__ void __launch_bounds__(256) k_kick_drift(KP P, int move, int nsb, int
       P.frc[S + d] = 0.0;
       P.frc[2 * S + d] = 0.0;
     }
+    if (images) ghost_images(P, d, p);
     return;
   }
-  double vx = P.vel[d], vy = P.vel[S + d], vz = P.vel[2 * S + d];
   if (move) {
-    const double dt = P.st->dt_next;
     const double hk = half_kick(P, dt);
-    vx = xadd(vx, xmul(P.frc[d], hk));
-    vy = xadd(vy, xmul(P.frc[S + d], hk));
-    vz = xadd(vz, xmul(P.frc[2 * S + d], hk));
+    vx = xadd(vx, xmul(fx, hk));
+    vy = xadd(vy, xmul(fy, hk));
+    vz = xadd(vz, xmul(fz, hk));
     p.x = xadd(p.x, xmul(vx, dt));
     p.y = xadd(p.y, xmul(vy, dt));
     p.z = xadd(p.z, xmul(vz, dt));
@@ -118,9 +124,11 @@ __global__ void __launch_bounds__(256) k_kick_drift(KP P, int move, int nsb, int
     M.tag[m] = P.tag[d];
     P.pdf[d] = make_double4(kVacant, kVacant, kVacant, 0.0);
     P.uf[d] = make_float4(kVacantF, kVacantF, kVacantF, __int_as_float(-1));
+    if (images) ghost_images(P, d, make_double4(kVacant, kVacant, kVacant, 0.0));
   } else {
     P.pdf[d] = p;
     P.uf[d] = make_float4((float)p.x, (float)p.y, (float)p.z, __int_as_float(-1));
+    if (images) ghost_images(P, d, p);
   }
 }
 
@@ -289,9 +297,9 @@ __device__ __forceinline__ void copy_record(const Clash& a, int i, const Clash& 
 // the same hash form independent groups processed in walk order: sorting by
 // (hash, walk key, class, order) makes the group's first record the one
 // that claims a free slot and the rest the new bucket, in order.
-__global__ void __launch_bounds__(1024) k_rehash(KP P) {
-  pdl_wait();
-  pdl_trigger();
+__device__ void ghost_images(const KP& P, long long d, const double4& p);
+
+__device__ void rehash_body(const KP& P) {
   if (P.st->err) return;
   const int n_old = P.st->n_clash;
   const int n_mov = min(P.st->n_mov, P.cap_mov);
@@ -364,6 +372,7 @@ __global__ void __launch_bounds__(1024) k_rehash(KP P) {
         P.frc[dr] = 0.0;
         P.frc[S + dr] = 0.0;
         P.frc[2 * S + dr] = 0.0;
+        ghost_images(P, dr, P.pdf[dr]);  // the slot's periodic images follow it
       }
     }
     X.flag[p] = !promote;
@@ -415,8 +424,56 @@ __global__ void __launch_bounds__(1024) k_rehash(KP P) {
     P.st->n_mov = 0;
   }
 }
+__global__ void __launch_bounds__(1024) k_rehash(KP P) {
+  pdl_wait();
+  pdl_trigger();
+  rehash_body(P);
+}
 
 // ------------------------------------------------------ ghost slot images
+// the images of interior site d with content p, from the source side: what
+// k_ghost_fill writes for every ghost whose source is d (same arithmetic)
+__device__ void ghost_images(const KP& P, long long d, const double4& p) {
+  const Geo& G = P.G;
+  const int par = d >= G.NC;
+  const long long cell = d - par * G.NC;
+  int cx, cy, cz;
+  cell_xyz(cell, G, cx, cy, cz);
+  int xl = 0, xh = 0, yl = 0, yh = 0, zl = 0, zh = 0;  // valid image shifts per axis
+  for (int k = 1; k <= G.kmx; ++k) {
+    if (cx - k * G.bx >= 0) xl = -k;
+    if (cx + k * G.bx < G.tx) xh = k;
+  }
+  for (int k = 1; k <= G.kmy; ++k) {
+    if (cy - k * G.by >= 0) yl = -k;
+    if (cy + k * G.by < G.ty) yh = k;
+  }
+  for (int k = 1; k <= G.kmz; ++k) {
+    if (cz - k * G.bz >= 0) zl = -k;
+    if (cz + k * G.bz < G.tz) zh = k;
+  }
+  if (xl == 0 && xh == 0 && yl == 0 && yh == 0 && zl == 0 && zh == 0) return;
+  const bool vac = p.x >= kVacantTest;
+  const float w = __int_as_float((int)d);
+  for (int kz = zl; kz <= zh; ++kz)
+    for (int ky = yl; ky <= yh; ++ky)
+      for (int kx = xl; kx <= xh; ++kx) {
+        if (kx == 0 && ky == 0 && kz == 0) continue;
+        const long long di =
+            par * G.NC + cell_of(cx + G.bx * kx, cy + G.by * ky, cz + G.bz * kz, G);
+        if (vac) {
+          P.pdf[di] = make_double4(kVacant, kVacant, kVacant, 0.0);
+          P.uf[di] = make_float4(kVacantF, kVacantF, kVacantF, w);
+          continue;
+        }
+        const double4 q = make_double4(xadd(p.x, xmul((double)kx, G.lx)),
+                                       xadd(p.y, xmul((double)ky, G.ly)),
+                                       xadd(p.z, xmul((double)kz, G.lz)), p.w);
+        P.pdf[di] = q;
+        P.uf[di] = make_float4((float)q.x, (float)q.y, (float)q.z, w);
+      }
+}
+
 // each ghost site has one periodic source; its image position is the
 // source's plus k*len, added per axis exactly like store.cpp:166-169
 __global__ void k_ghost_fill(KP P) {
@@ -464,9 +521,7 @@ __device__ __forceinline__ int image_count(long long id, const Geo& G) {
   return c;
 }
 
-__global__ void __launch_bounds__(1024) k_clash_images(KP P, int zero_rho) {
-  pdl_wait();
-  pdl_trigger();
+__device__ void clash_images_body(const KP& P, int zero_rho) {
   if (zero_rho && threadIdx.x == 0) P.work[0] = 0;  // the density pass's brick queue
   if (P.st->err) return;
   const int n = P.st->n_clash;
@@ -575,6 +630,20 @@ __global__ void __launch_bounds__(1024) k_clash_images(KP P, int zero_rho) {
   }
   if (threadIdx.x == 0) P.st->n_clash = total;
 }
+__global__ void __launch_bounds__(1024) k_clash_images(KP P, int zero_rho) {
+  pdl_wait();
+  pdl_trigger();
+  clash_images_body(P, zero_rho);
+}
+// the store phase's two single-block passes in one launch (the step path,
+// whose slot images k_kick_drift and rehash_body already wrote)
+__global__ void __launch_bounds__(1024) k_rehash_images(KP P) {
+  pdl_wait();
+  pdl_trigger();
+  rehash_body(P);
+  __syncthreads();
+  clash_images_body(P, 1);
+}
 
 // fp32 shadow of every site from pdf (after a host upload)
 __global__ void k_uf_refresh(KP P) {
@@ -644,14 +713,19 @@ __global__ void __launch_bounds__(256) k_kick2(KP P, int kick, int nsb) {
   int par;
   long long d;
   if (!P.st->err && !P.st->n_ovl && map_site(P, par, d)) {
-    if (P.pdf[d].x < kVacantTest) {
-      const long long S = P.S;
-      double vx = P.vel[d], vy = P.vel[S + d], vz = P.vel[2 * S + d];
+    // every load of the site issued before the first use (one memory round
+    // trip per thread; a vacant slot's velocity/force reads are discarded)
+    const long long S = P.S;
+    const double px = P.pdf[d].x;
+    double vx = P.vel[d], vy = P.vel[S + d], vz = P.vel[2 * S + d];
+    const double fx = P.frc[d], fy = P.frc[S + d], fz = P.frc[2 * S + d];
+    const double dt = P.st->dt_next;
+    if (px < kVacantTest) {
       if (kick) {
-        const double hk = half_kick(P, P.st->dt_next);
-        vx = xadd(vx, xmul(P.frc[d], hk));
-        vy = xadd(vy, xmul(P.frc[S + d], hk));
-        vz = xadd(vz, xmul(P.frc[2 * S + d], hk));
+        const double hk = half_kick(P, dt);
+        vx = xadd(vx, xmul(fx, hk));
+        vy = xadd(vy, xmul(fy, hk));
+        vz = xadd(vz, xmul(fz, hk));
         P.vel[d] = vx;
         P.vel[S + d] = vy;
         P.vel[2 * S + d] = vz;
@@ -791,9 +865,12 @@ __global__ void __launch_bounds__(256) k_count_defects(KP P, unsigned long long*
 
 // -------------------------------------------------------------- launchers
 constexpr int kClashBlocks = 8;  // blocks of 256 threads for clash-record sweeps
-void launch_kick_drift(const KP& P, int move, cudaStream_t s, int zero_acc) {
+void launch_kick_drift(const KP& P, int move, cudaStream_t s, int zero_acc, int images) {
   const int nsb = eam_blocks(P);
-  k_kick_drift<<<nsb + kClashBlocks, 256, 0, s>>>(P, move, nsb, zero_acc);
+  k_kick_drift<<<nsb + kClashBlocks, 256, 0, s>>>(P, move, nsb, zero_acc, images);
+}
+void launch_rehash_images(const KP& P, cudaStream_t s) {
+  launch_pdl(k_rehash_images, 1, 1024, 0, s, P);
 }
 void launch_rehash(const KP& P, cudaStream_t s) { launch_pdl(k_rehash, 1, 1024, 0, s, P); }
 void launch_ghost_fill(const KP& P, cudaStream_t s) {
