@@ -130,9 +130,10 @@ def cmd_check(cfg_path: str, overrides) -> int:  # main.cpp:128-160
     print("offsets per site: even %d (half %d), odd %d (half %d)"
           % (len(idx["even_full"]), len(idx["even_half"]), len(idx["odd_full"]),
              len(idx["odd_half"])))
-    nb = -(-cfg.box_x // 8) * -(-cfg.box_y // 4) * -(-cfg.box_z // 4)
-    print("partition: device cuda:%d, %d bricks of 8x4x4 cells per sublattice pass "
-          "(CPU workers %d unused)" % (cfg.device, nb, cfg.workers))
+    strips = -(-cfg.box_x * cfg.box_y // 32)
+    units = strips * -(-cfg.box_z // 4)
+    print("partition: device cuda:%d, %d units of 32-cell strips x 4 z planes per pass "
+          "(CPU workers %d unused)" % (cfg.device, units, cfg.workers))
     return 0
 
 

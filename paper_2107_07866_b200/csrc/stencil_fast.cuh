@@ -595,13 +595,37 @@ __host__ __device__ __forceinline__ int brick_count(const Geo& G) {
 // only: every update is an atomic add, so it may overlap the slot sweep)
 constexpr int kClashBlocks128 = 32;
 
-// groups of 128 threads (4 warps) of a large CTA, each on its own brick
-__device__ __forceinline__ int next_brick_group8(int* ctr, int group, volatile int* slot) {
+// Work units of the shared-table passes: a strip of 32 consecutive interior
+// cells of one x-y plane (x fastest, rows wrapping, so no partly empty
+// bricks at the box faces) on 4 consecutive z planes, warp w on plane
+// 4 zb + w.  Config 2: 79 strips x 13 z blocks = 1027 units, 99 % of the
+// lanes live (8x4x4 bricks: 1183, 85 %).
+__host__ __device__ __forceinline__ int strip_count(const Geo& G) {
+  return (G.bx * G.by + 31) / 32;
+}
+__host__ __device__ __forceinline__ int unit_count(const Geo& G) {
+  return strip_count(G) * ((G.bz + 3) / 4);
+}
+__device__ __forceinline__ bool unit_cell(const Geo& G, int u, int lane, int w, int& c) {
+  const int ns = strip_count(G);
+  const int zb = u / ns, e = (u - zb * ns) * 32 + lane, cz = zb * 4 + w;
+  const bool live = e < G.bx * G.by && cz < G.bz;
+  const int cy = e / G.bx, cx = e - cy * G.bx;
+  c = live ? (int)cell_of(cx + G.g, cy + G.g, cz + G.g, G) : 0;
+  return live;
+}
+// A group's first unit is static, spread round-robin over the CTAs (one per
+// SM), so a pass with fewer units than groups loads every SM alike; later
+// units come from the counter *ctr (reset by the kernel before the pass).
+__device__ __forceinline__ int next_unit(int* ctr, int group, int nsb, volatile int* slot,
+                                         bool first) {
+  if (first) return blockIdx.x + nsb * group;
   asm volatile("bar.sync %0, 128;" ::"r"(group + 1));
-  if ((threadIdx.x & 127) == 0) slot[group] = atomicAdd(ctr, 1);
+  if ((threadIdx.x & 127) == 0) slot[group] = 8 * nsb + atomicAdd(ctr, 1);
   asm volatile("bar.sync %0, 128;" ::"r"(group + 1));
   return slot[group];
 }
+
 
 // density pass with the upper rho-spline window in shared memory (32-byte
 // records): NT threads = NT/128 groups of 4 warps, one CTA per SM; B = 1
@@ -631,15 +655,12 @@ __global__ void __launch_bounds__(NT, 1) k_density_smem(KP P, int nsb) {
   const int group = threadIdx.x >> 7;
   const int lt = threadIdx.x & 127, lane = lt & 31, w = lt >> 5;
   const Geo& G = P.G;
-  const int nbx = (G.bx + kBrickX - 1) / kBrickX, nby = (G.by + kBrickY - 1) / kBrickY;
-  const int nb = brick_count(G);
-  for (;;) {
-    const int b = next_brick_group8(&P.work[0], group, s_slot);
-    if (b >= nb) break;
-    const int cx = (b % nbx) * kBrickX + (lane & 7), cy = ((b / nbx) % nby) * kBrickY + (lane >> 3),
-              cz = (b / (nbx * nby)) * kBrickZ + w;
-    const bool live = cx < G.bx && cy < G.by && cz < G.bz;
-    const int c = live ? (int)cell_of(cx + G.g, cy + G.g, cz + G.g, G) : 0;
+  const int nu = unit_count(G);
+  for (bool first = true;; first = false) {
+    const int u = next_unit(&P.work[0], group, nsb, s_slot, first);
+    if (u >= nu) break;
+    int c;
+    const bool live = unit_cell(G, u, lane, w, c);
     for (int par = 0; par < 2; ++par)
       density_site<FULL, B, true>(P, P.dself, par, live ? (int)(par * G.NC + c) : 0, live, T,
                                   seg_lo);
@@ -719,16 +740,13 @@ __global__ void __launch_bounds__(NT, 1) k_force_lean_smem(KP P, int nsb) {
   const int group = threadIdx.x >> 7;
   const int lt = threadIdx.x & 127, lane = lt & 31, w = lt >> 5;
   const Geo& G = P.G;
-  const int nbx = (G.bx + kBrickX - 1) / kBrickX, nby = (G.by + kBrickY - 1) / kBrickY;
-  const int nb = brick_count(G);
+  const int nu = unit_count(G);
   double e = 0.0;
-  for (;;) {
-    const int b = next_brick_group8(&P.work[1], group, s_slot);
-    if (b >= nb) break;
-    const int cx = (b % nbx) * kBrickX + (lane & 7), cy = ((b / nbx) % nby) * kBrickY + (lane >> 3),
-              cz = (b / (nbx * nby)) * kBrickZ + w;
-    const bool live = cx < G.bx && cy < G.by && cz < G.bz;
-    const int c = live ? (int)cell_of(cx + G.g, cy + G.g, cz + G.g, G) : 0;
+  for (bool first = true;; first = false) {
+    const int u = next_unit(&P.work[1], group, nsb, s_slot, first);
+    if (u >= nu) break;
+    int c;
+    const bool live = unit_cell(G, u, lane, w, c);
     for (int par = 0; par < 2; ++par)
       e += force_site_lean<FULL, true>(P, P.dself, par, live ? (int)(par * G.NC + c) : 0, live,
                                        T, seg_lo);
@@ -783,7 +801,7 @@ bool launch_density_fast(const KP& P, int mode, int grid, cudaStream_t s) {
                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
       attr = true;
     }
-    const int g = max(1, min(sm_count(), (brick_count(P.G) + 7) / 8));
+    const int g = max(1, min(sm_count(), unit_count(P.G)));
     if (mode) launch_pdl(k_density_smem<true, 1, 1024>, g, 1024, bytes, s, P, g);
     else launch_pdl(k_density_smem<false, 1, 1024>, g + 4, 1024, bytes, s, P, g);
     return !mode;
@@ -808,7 +826,7 @@ bool launch_force_fast(const KP& P, int mode, int grid, cudaStream_t s) {
                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
       attr = true;
     }
-    const int g = max(1, min(sm_count(), (brick_count(P.G) + 7) / 8));
+    const int g = max(1, min(sm_count(), unit_count(P.G)));
     if (mode) launch_pdl(k_force_lean_smem<true, 1024>, g, 1024, bytes, s, P, g);
     else launch_pdl(k_force_lean_smem<false, 1024>, g + 4, 1024, bytes, s, P, g);
     return !mode;

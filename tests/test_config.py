@@ -236,7 +236,7 @@ def test_cli_gen_potential_and_check(tmp_path):
     assert lines[1] == "potential: Z=26, 55.84 amu, cutoff 5.6 A, a0 2.8553 A"
     assert lines[2] == "ghost width: 3 cells; index cutoff 6.457 A"
     assert lines[3] == "offsets per site: even 112 (half 46), odd 112 (half 66)"
-    assert lines[4].startswith("partition: device cuda:0, 75 bricks")
+    assert lines[4].startswith("partition: device cuda:0, 65 units")
     r = cli("check", "--config", str(cfg), "--set", "box.x=0")
     assert r.returncode == 1
     assert r.stderr == "error: box.x/box.y/box.z: box must be at least 1 cell per axis\n"
