@@ -79,6 +79,10 @@ struct KP {
   float4* uf;      // fp32 shadow (x, y, z, owner-or--1) for the candidate filter
   int* work;       // persistent-kernel work counters (zeroed per launch)
   FastTab fd, ff;  // density / force fast tables
+  // force table with the cubic coefficients in fp32, 48-byte records
+  // [zB zC zD qB qC (zA,qA as two floats)]; null when a table's cubic terms
+  // are too large for the fp32 bound (setup_fast)
+  const double* ffc;
   FastTab fe;      // embedding F(rho): 4 doubles/segment (A B C D), padded
   float band_hi, band_lo;  // fp32 r^2 filter: reject above hi, exact test in [lo, hi]
   double guard_r2;         // below: overlap / short-range guard path

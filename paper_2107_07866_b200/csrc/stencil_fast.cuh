@@ -439,7 +439,7 @@ __device__ __forceinline__ unsigned long long warp_or64(unsigned long long m) {
 // force pass, lean variant: one pair per iteration, no batching, so the
 // register footprint allows 6-8 resident CTAs per SM (latency hidden by
 // warps instead of by in-thread batching).  Warp-uniform union sweep.
-template <bool FULL, bool SMEM>
+template <bool FULL, bool SMEM, bool CMP = false>
 __device__ __forceinline__ double force_site_lean(const KP& P, KP* Pp, int par, int d,
                                                   bool live, const double2* T = nullptr,
                                                   int seg_lo = 0) {
@@ -499,7 +499,14 @@ __device__ __forceinline__ double force_site_lean(const KP& P, KP* Pp, int par, 
     const int seg = seg_index(P.ff, r2 * ri, sb);
     double zA, zB, zC, zD, qA, qB, qC, qD;
     const int li = seg - seg_lo;
-    if (SMEM && li >= 0) {
+    if (SMEM && CMP && li >= 0) {  // 48-byte record, cubic terms in fp32
+      const double2 c0 = T[3 * li], c1 = T[3 * li + 1], c2 = T[3 * li + 2];
+      zB = c0.x; zC = c0.y; zD = c1.x; qB = c1.y; qC = c2.x;
+      const unsigned long long ab = (unsigned long long)__double_as_longlong(c2.y);
+      zA = (double)__uint_as_float((unsigned)ab);
+      qA = (double)__uint_as_float((unsigned)(ab >> 32));
+      qD = 0.0;
+    } else if (SMEM && li >= 0) {
       const double2 c0 = smem_chunk(T, li, 0), c1 = smem_chunk(T, li, 1);
       const double2 c2 = smem_chunk(T, li, 2), c3 = smem_chunk(T, li, 3);
       zA = c0.x; zB = c0.y; zC = c1.x; zD = c1.y;
@@ -708,9 +715,9 @@ __global__ void __launch_bounds__(128, 4) k_force_fast(KP P) {
 // lean force pass with the upper spline window (records [seg_lo, nseg])
 // in shared memory: 1024 threads, one CTA per SM, 8 groups of 4 warps each
 // on their own brick.  Pairs below the window (cascade cores) read global.
-constexpr int kLeanTabRecords = 3300;  // x 64 B = 211,200 B
+constexpr int kLeanTabRecords = 3300;  // x 64 B = 211,200 B (x 48 B = 158,400 B compressed)
 
-template <bool FULL, int NT>
+template <bool FULL, int NT, bool CMP>
 __global__ void __launch_bounds__(NT, 1) k_force_lean_smem(KP P, int nsb) {
   if (blockIdx.x >= nsb) {
     pdl_wait();
@@ -724,9 +731,14 @@ __global__ void __launch_bounds__(NT, 1) k_force_lean_smem(KP P, int nsb) {
   const int nseg = P.ff.nseg;  // records 0..nseg (padded)
   const int seg_lo = max(0, nseg + 1 - kLeanTabRecords);
   const int nrec = nseg + 1 - seg_lo;
-  const double2* src = reinterpret_cast<const double2*>(P.ff.rec + 8 * (size_t)seg_lo);
-  for (int q = threadIdx.x; q < 4 * nrec; q += blockDim.x)
-    T[smem_slot(q >> 2, q & 3)] = __ldg(src + q);
+  if (CMP) {  // 48-byte records, three 16-byte chunks each, in order
+    const double2* src = reinterpret_cast<const double2*>(P.ffc + 6 * (size_t)seg_lo);
+    for (int q = threadIdx.x; q < 3 * nrec; q += blockDim.x) T[q] = __ldg(src + q);
+  } else {
+    const double2* src = reinterpret_cast<const double2*>(P.ff.rec + 8 * (size_t)seg_lo);
+    for (int q = threadIdx.x; q < 4 * nrec; q += blockDim.x)
+      T[smem_slot(q >> 2, q & 3)] = __ldg(src + q);
+  }
   for (int i = threadIdx.x; i < 2 * (kMaskBits + 1); i += blockDim.x) {
     const int par = i / (kMaskBits + 1), k = i % (kMaskBits + 1);
     const int n = FULL ? c_full_n[par] : c_half_n[par];
@@ -748,8 +760,8 @@ __global__ void __launch_bounds__(NT, 1) k_force_lean_smem(KP P, int nsb) {
     int c;
     const bool live = unit_cell(G, u, lane, w, c);
     for (int par = 0; par < 2; ++par)
-      e += force_site_lean<FULL, true>(P, P.dself, par, live ? (int)(par * G.NC + c) : 0, live,
-                                       T, seg_lo);
+      e += force_site_lean<FULL, true, CMP>(P, P.dself, par, live ? (int)(par * G.NC + c) : 0,
+                                            live, T, seg_lo);
   }
   for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
   if ((threadIdx.x & 31) == 0) P.part_pair[(blockIdx.x * blockDim.x + threadIdx.x) >> 5] = e;
@@ -815,20 +827,27 @@ bool launch_density_fast(const KP& P, int mode, int grid, cudaStream_t s) {
 // force pass: with a valid pair mask the lean mask-replay kernel with the
 // force spline window in shared memory; otherwise (positions changed since
 // the density pass) the decision path, which re-derives every pair
+template <bool CMP>
+void launch_force_lean(const KP& P, int mode, cudaStream_t s) {
+  const size_t bytes = (size_t)kLeanTabRecords * (CMP ? 48 : 64);
+  static bool attr = false;
+  if (!attr) {
+    // default carveout: the driver takes the smallest shared-memory split
+    // that fits the table and leaves the rest of the SM's 256 KB as L1 for
+    // the partner gathers (an explicit carveout hint measured 10 % slower)
+    for (const void* k : {(const void*)k_force_lean_smem<false, 1024, CMP>,
+                          (const void*)k_force_lean_smem<true, 1024, CMP>})
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    attr = true;
+  }
+  const int g = max(1, min(sm_count(), unit_count(P.G)));
+  if (mode) launch_pdl(k_force_lean_smem<true, 1024, CMP>, g, 1024, bytes, s, P, g);
+  else launch_pdl(k_force_lean_smem<false, 1024, CMP>, g + 4, 1024, bytes, s, P, g);
+}
 bool launch_force_fast(const KP& P, int mode, int grid, cudaStream_t s) {
   if (P.use_mask) {
-    const size_t bytes = (size_t)kLeanTabRecords * 64;
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(k_force_lean_smem<false, 1024>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-      cudaFuncSetAttribute(k_force_lean_smem<true, 1024>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-      attr = true;
-    }
-    const int g = max(1, min(sm_count(), unit_count(P.G)));
-    if (mode) launch_pdl(k_force_lean_smem<true, 1024>, g, 1024, bytes, s, P, g);
-    else launch_pdl(k_force_lean_smem<false, 1024>, g + 4, 1024, bytes, s, P, g);
+    if (P.ffc) launch_force_lean<true>(P, mode, s);
+    else launch_force_lean<false>(P, mode, s);
     return !mode;
   }
   if (mode) k_force_fast<true, 2><<<grid, 128, 0, s>>>(P);
