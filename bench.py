@@ -240,7 +240,10 @@ def run_ours(args, w, path, ws, rank, local):
                       "stencil": args.stencil,
                       "l2": f"flushed ({args.flush_mb:.0f} MB write) before every timed step",
                       "parallelism": (f"z-slab x{ws}, {getattr(dev, 'transport', args.transport)} halo/migrant "
-                                      f"exchange + reduction inside the step graph") if slab
+                                      f"exchange + reduction inside the step graph"
+                                      + (", density/force partials added into the neighbours' "
+                                         "memory by the passes" if getattr(dev, "fused", False)
+                                         else "")) if slab
                                      else "single-gpu",
                       "global_cells": [w.cells[0], w.cells[1], w.cells[2] * ws]},
            "roofline": roofline, "e2e": e2e, "gpu_launches": launches,

@@ -283,14 +283,31 @@ CBX_API cbx_status cbx_slab_commit(cbx_ctx* ctx, const double in[4]);
 CBX_API cbx_status cbx_nccl_unique_id(void* out, long nbytes);
 CBX_API cbx_status cbx_slab_comm_init(cbx_ctx* ctx, const void* id, long nbytes);
 /* Peer-memory exchange (ranks on one node, NVLink / NVSwitch): each rank
- * exports its receive region (64-byte CUDA IPC handle), every rank passes the
- * handles of all ranks (in rank order) to cbx_slab_p2p_init.  Each exchange
- * is then two kernels -- the sender stores its boundary data straight into
- * the neighbour's memory and raises a flag, the receiver waits on it and
- * unpacks -- and the StepState reduction is one kernel.  Takes precedence
- * over an NCCL communicator.  nranks == 1 maps the rank onto itself. */
+ * exports a CBX_P2P_HANDLE_BYTES handle (CUDA IPC handles of its receive
+ * region and of its rho / force accumulators, plus its slab geometry); every
+ * rank passes the handles of all ranks (in rank order) to cbx_slab_p2p_init.
+ * The forward exchanges (migrants, positions, dF) are one kernel each -- the
+ * sender stores its boundary data straight into the neighbour's memory and
+ * raises a flag, the receiver waits on it and unpacks.  The reverse ones
+ * (density and force partials of the halo planes) are fused into the passes:
+ * with the Newton-3 stencil a partial for a halo site is added straight into
+ * the neighbour's boundary site over NVLink, and the consumer (embedding,
+ * second half kick) waits on the neighbours' flags.  The StepState reduction
+ * is the tail of the finalize kernel.  Takes precedence over an NCCL
+ * communicator.  nranks == 1 maps the rank onto itself. */
+#define CBX_P2P_HANDLE_BYTES 256
 CBX_API cbx_status cbx_slab_p2p_handle(cbx_ctx* ctx, void* out, long nbytes);
 CBX_API cbx_status cbx_slab_p2p_init(cbx_ctx* ctx, const void* handles, long nbytes);
+/* 1 when this rank adds its halo partials straight into the neighbours'
+ * memory (needs native fp64 peer atomics between every pair of the ranks'
+ * GPUs), 0 for the staged reverse exchanges.  All ranks must agree: a caller
+ * that cannot guarantee identical device visibility on every rank sets the
+ * minimum over ranks with cbx_slab_p2p_set_fused. */
+CBX_API int cbx_slab_p2p_fused(cbx_ctx* ctx);
+CBX_API cbx_status cbx_slab_p2p_set_fused(cbx_ctx* ctx, int on);
+/* drop the peer-memory transport again (before any step), e.g. when another
+ * rank could not map its neighbours; connect NCCL afterwards */
+CBX_API cbx_status cbx_slab_p2p_close(cbx_ctx* ctx);
 CBX_API cbx_status cbx_upload_store_global(cbx_ctx* ctx, const cbx_store* global_store);
 CBX_API cbx_status cbx_download_store_global(cbx_ctx* ctx, cbx_store* global_store,
                                              long* n_clash_inout);

@@ -186,7 +186,7 @@ class SlabEngine : public Engine {
       : Engine(create(global_box, pot, rank, nranks, device)) {}
 
   std::vector<unsigned char> p2p_handle() {
-    std::vector<unsigned char> h(64);
+    std::vector<unsigned char> h(CBX_P2P_HANDLE_BYTES);
     check(cbx_slab_p2p_handle(raw(), h.data(), (long)h.size()), raw());
     return h;
   }

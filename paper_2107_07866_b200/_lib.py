@@ -143,6 +143,9 @@ SIGNATURES = [
     ("cbx_count_pairs", C.c_int, [_P, C.POINTER(C.c_uint64)]),
     ("cbx_kernel_launches", C.c_int, [_P, C.POINTER(C.c_uint64)]),
     ("cbx_describe", C.c_int, [_P, C.c_char_p, C.c_long]),
+    ("cbx_slab_p2p_fused", C.c_int, [_P]),
+    ("cbx_slab_p2p_set_fused", C.c_int, [_P, C.c_int]),
+    ("cbx_slab_p2p_close", C.c_int, [_P]),
     ("cbx_memory_report", C.c_int, [_P, C.POINTER(C.c_longlong)]),
     ("cbx_bench_steps", C.c_int, [_P, _D, C.c_long, _D, C.POINTER(C.c_double)]),
     ("cbx_fp64_peak", C.c_int, [C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double)]),

@@ -83,6 +83,8 @@ struct cbx_ctx {
   std::vector<double> ser_t;
   std::vector<long> ser_d;
   bool p2p = false;
+  bool rev_mapped = false;  // the neighbours' rho / force arrays are mapped (KP::rev)
+  bool fused_off = false;   // cbx_slab_p2p_set_fused(0)
 
   // device bytes by structure (cbx_memory_report): the category the next
   // allocations are charged to
@@ -279,8 +281,10 @@ void seq_density(cbx_ctx* c) {
   c->launches += 1;
   c->mask_valid = c->mode != CBX_STENCIL_REFERENCE && c->P.pmask != nullptr;
 }
-void seq_embed(cbx_ctx* c) {
-  launch_embed(c->P, c->stream, c->mode == CBX_STENCIL_REFERENCE);
+void seq_embed(cbx_ctx* c, int rev_wait = 0) {
+  KP q = c->P;
+  q.rev_wait = rev_wait;  // the neighbours' density partials arrive first
+  launch_embed(q, c->stream, c->mode == CBX_STENCIL_REFERENCE);
   c->clash_f_zero = true;
   c->launches += 1;
 }
@@ -313,6 +317,12 @@ void seq_force(cbx_ctx* c) {
 // rank above.  Messages have a fixed size (slab_msg_bytes), so the sequence
 // is capturable; with one rank both peers are this rank (self send/recv).
 bool has_transport(const cbx_ctx* c) { return c->comm != nullptr || c->p2p; }
+// the RHO / FRC exchanges fused into the passes (peer memory, Newton-3,
+// neighbours' accumulators mapped); CBX_P2P_FUSED=0 keeps the staged exchanges
+bool rev_fused(const cbx_ctx* c) {
+  static const bool on = !getenv("CBX_P2P_FUSED") || atoi(getenv("CBX_P2P_FUSED"));
+  return on && c->p2p && c->rev_mapped && !c->fused_off && c->mode == CBX_STENCIL_NEWTON3;
+}
 
 void slab_exchange(cbx_ctx* c, int kind) {
   if (c->p2p) {  // fused: pack into the neighbours' memory, wait, unpack
@@ -339,6 +349,17 @@ void slab_exchange(cbx_ctx* c, int kind) {
   launch_unpack(c->P, kind, -1, c->rbuf[0], gs_lo, c->d_rem_base + 0, c->stream);
   launch_unpack(c->P, kind, +1, c->rbuf[1], gs_hi, c->d_rem_base + 1, c->stream);
   c->launches += (kind == 1 || kind == 3) ? 8 : 4;
+}
+
+// a reverse halo (2 RHO, 4 FRC): with the fused path the pass already
+// added into the neighbours' memory -- only raise their flags
+void slab_reverse(cbx_ctx* c, int kind) {
+  if (c->P.rev.on) {
+    launch_rev_signal(c->P, kind, c->stream);
+    c->launches += 1;
+    return;
+  }
+  slab_exchange(c, kind);
 }
 
 // StepState sums over ranks: energies (pair, embedding) and/or kinetic +
@@ -370,7 +391,12 @@ void memset_field(cbx_ctx* c, int* field) { cudaMemsetAsync(field, 0, sizeof(int
 void slab_finish(cbx_ctx* c, int kick, int stepping, int energies) {
   if (c->p2p) {
     if (kick >= 0) {
-      launch_kick2(c->P, kick, -2, 0, c->stream);
+      KP q = c->P;
+      q.rev_wait = c->P.rev.on ? 4 : 0;  // the neighbours' force partials arrive first
+      launch_kick2(q, kick, -2, 0, c->stream);
+      c->launches += 1;
+    } else if (c->P.rev.on) {
+      launch_rev_wait(c->P, 4, c->stream);
       c->launches += 1;
     }
     launch_finalize(c->P, stepping, energies, c->stream, c->d_links);
@@ -407,15 +433,15 @@ void seq_slab_step(cbx_ctx* c) {
   c->acc_rho_zero = c->acc_frc_zero = zacc;
   c->launches += 1;
   seq_density(c);
-  slab_exchange(c, 2);  // density partials (reverse)
+  slab_reverse(c, 2);  // density partials (reverse)
   ev_mark(c, 2);
-  seq_embed(c);
+  seq_embed(c, c->P.rev.on ? 2 : 0);
   slab_exchange(c, 3);  // dF
   ev_mark(c, 3);
   launch_remote_df(c->P, c->stream);
   c->launches += 1;
   seq_force(c);
-  slab_exchange(c, 4);  // force partials (reverse)
+  slab_reverse(c, 4);  // force partials (reverse)
   ev_mark(c, 4);
   slab_finish(c, 1, 1, 1);
   ev_mark(c, 5);
@@ -430,15 +456,15 @@ void seq_slab_eval(cbx_ctx* c) {
   c->clash_rho_zero = true;
   c->launches += 1;
   seq_density(c);
-  slab_exchange(c, 2);
+  slab_reverse(c, 2);
   ev_mark(c, 2);
-  seq_embed(c);
+  seq_embed(c, c->P.rev.on ? 2 : 0);
   slab_exchange(c, 3);
   ev_mark(c, 3);
   launch_remote_df(c->P, c->stream);
   c->launches += 1;
   seq_force(c);
-  slab_exchange(c, 4);
+  slab_reverse(c, 4);
   ev_mark(c, 4);
   slab_finish(c, -1, -1, 1);
 }
@@ -1138,7 +1164,8 @@ static cbx_status create_impl(const cbx_box* box, const cbx_potential* pot,
       cell_xyz(cell, G, cx, cy, cz);
       const bool ghost = cell_is_ghost(cx, cy, cz, G);
       // z-halo planes of a slab rank are remote: filled by the position halo,
-      // their partials returned by the reverse halos (tgt = the site itself)
+      // their partials returned by the reverse halos (tgt = the x/y owner
+      // column in the same plane)
       const bool remote = G.slab && (cz < G.g || cz >= G.g + G.bz);
       const long kx = floor_div(cx - G.g, G.bx), ky = floor_div(cy - G.g, G.by),
                  kz = floor_div(cz - G.g, G.bz);
@@ -1146,8 +1173,12 @@ static cbx_status create_impl(const cbx_box* box, const cbx_potential* pot,
                                       (int)(cz - kz * G.bz), G);
       for (int par = 0; par < 2; ++par) {
         const long long d = par * G.NC + cell;
-        if (!ghost || remote) {
+        if (!ghost) {
           tgt[d] = (int)d;
+          continue;
+        }
+        if (remote) {  // in-plane owner column; the plane itself comes by exchange
+          tgt[d] = (int)(par * G.NC + cell_of((int)(cx - kx * G.bx), (int)(cy - ky * G.by), cz, G));
           continue;
         }
         const long long s = par * G.NC + scell;
@@ -1326,6 +1357,7 @@ CBX_API cbx_status cbx_set_stencil(cbx_ctx* c, cbx_stencil mode) {
     if (c->mode != mode) drop_graph(c);
     c->mode = mode;
     c->mask_valid = false;
+    c->P.rev.on = rev_fused(c);
     sync_kp(c);
   });
 }
@@ -2128,6 +2160,8 @@ CBX_API long cbx_slab_buffer_bytes(cbx_ctx* c, int kind) {
 CBX_API cbx_status cbx_slab_phase(cbx_ctx* c, int phase, double dt) {
   return guarded(c, [&] {
     cudaSetDevice(c->device);
+    if (c->p2p)
+      raise(CBX_LOGIC, "cbx_slab_phase: this rank exchanges on the device (peer memory)");
     check_cutoff(c);
     switch (phase) {
       case 0:
@@ -2325,17 +2359,31 @@ CBX_API cbx_status cbx_slab_p2p_handle(cbx_ctx* c, void* out, long nbytes) {
   return guarded(c, [&] {
     cudaSetDevice(c->device);
     if (!c->G.slab) raise(CBX_LOGIC, "cbx_slab_p2p_handle: not a slab rank");
-    if (nbytes < (long)sizeof(cudaIpcMemHandle_t))
-      raise(CBX_INVALID_ARGUMENT, "cbx_slab_p2p_handle: buffer smaller than 64 bytes");
+    if (nbytes < CBX_P2P_HANDLE_BYTES)
+      raise(CBX_INVALID_ARGUMENT, "cbx_slab_p2p_handle: buffer smaller than CBX_P2P_HANDLE_BYTES");
     if (!c->p2p_region) {
       c->p2p_bytes = p2p_buf_off(c->P, 5, 0);
       cuda_check(cudaMalloc(&c->p2p_region, c->p2p_bytes), "p2p region");
       c->mem_bytes[CBX_MEM_EXCHANGE] += c->p2p_bytes;
       cuda_check(cudaMemset(c->p2p_region, 0, c->p2p_bytes), "p2p region");
     }
-    cudaIpcMemHandle_t h;
-    cuda_check(cudaIpcGetMemHandle(&h, c->p2p_region), "cudaIpcGetMemHandle");
-    std::memcpy(out, &h, sizeof h);
+    // [receive region][rho][force] IPC handles, then NC, S, bz of this rank
+    unsigned char* o = static_cast<unsigned char*>(out);
+    std::memset(o, 0, CBX_P2P_HANDLE_BYTES);
+    const void* bases[3] = {c->p2p_region, c->P.rho, c->P.frc};
+    for (int k = 0; k < 3; ++k) {
+      cudaIpcMemHandle_t h;
+      cuda_check(cudaIpcGetMemHandle(&h, const_cast<void*>(bases[k])), "cudaIpcGetMemHandle");
+      std::memcpy(o + 64 * k, &h, sizeof h);
+    }
+    // PCI bus id of this rank's GPU: the neighbours check native peer atomics
+    int bus = 0, dev_id = 0, dom = 0;
+    cudaDeviceGetAttribute(&bus, cudaDevAttrPciBusId, c->device);
+    cudaDeviceGetAttribute(&dev_id, cudaDevAttrPciDeviceId, c->device);
+    cudaDeviceGetAttribute(&dom, cudaDevAttrPciDomainId, c->device);
+    const long long geo[4] = {c->G.NC, c->S, (long long)c->G.bz,
+                              ((long long)dom << 32) | ((long long)bus << 16) | dev_id};
+    std::memcpy(o + 192, geo, sizeof geo);
   });
 }
 
@@ -2348,25 +2396,89 @@ CBX_API cbx_status cbx_slab_p2p_init(cbx_ctx* c, const void* handles, long nbyte
     if (c->p2p) raise(CBX_LOGIC, "cbx_slab_p2p_init: already initialised");
     const int n = c->nranks;
     if (n > kMaxP2PRanks) raise(CBX_INVALID_ARGUMENT, "cbx_slab_p2p_init: more than 8 ranks");
-    if (nbytes < (long)(n * sizeof(cudaIpcMemHandle_t)))
-      raise(CBX_INVALID_ARGUMENT, "cbx_slab_p2p_init: need one 64-byte handle per rank");
-    std::vector<unsigned char*> base(n);
-    for (int q = 0; q < n; ++q) {
-      if (q == c->rank) {
-        base[q] = c->p2p_region;
-        continue;
-      }
+    if (nbytes < (long)n * CBX_P2P_HANDLE_BYTES)
+      raise(CBX_INVALID_ARGUMENT,
+            "cbx_slab_p2p_init: need one CBX_P2P_HANDLE_BYTES handle per rank");
+    const unsigned char* hb = static_cast<const unsigned char*>(handles);
+    auto open = [&](int q, int k) -> void* {  // rank q's k-th exported allocation
+      if (q == c->rank) return k == 0 ? (void*)c->p2p_region : k == 1 ? (void*)c->P.rho
+                                                                      : (void*)c->P.frc;
       cudaIpcMemHandle_t h;
-      std::memcpy(&h, static_cast<const unsigned char*>(handles) + q * sizeof h, sizeof h);
+      std::memcpy(&h, hb + (size_t)q * CBX_P2P_HANDLE_BYTES + 64 * k, sizeof h);
       void* p = nullptr;
       cuda_check(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess),
                  "cudaIpcOpenMemHandle (ranks must share a node with peer access)");
       c->p2p_opened.push_back(p);
-      base[q] = static_cast<unsigned char*>(p);
-    }
+      return p;
+    };
+    std::vector<unsigned char*> base(n);
+    for (int q = 0; q < n; ++q) base[q] = static_cast<unsigned char*>(open(q, 0));
     P2PLinks& L = c->links;
     L = P2PLinks{};
     const int lo = (c->rank + n - 1) % n, hi = (c->rank + 1) % n;
+    // fused reverse halo: the neighbours' accumulators (KP::rev)
+    {
+      RevHalo& R = c->P.rev;
+      R = RevHalo{};
+      const Geo& G = c->G;
+      long long plane0[2] = {0, 0};
+      const int nb[2] = {lo, hi};
+      void* rho_nb[2] = {nullptr, nullptr};
+      void* frc_nb[2] = {nullptr, nullptr};
+      // the fused reverse halo adds into the neighbours' memory with fp64
+      // atomics: only where the links support them natively (NVLink).  Every
+      // rank checks every pair, so all ranks take the same path.
+      bool atomics = true;
+      std::vector<int> devs(n, -1);
+      int ndev = 0;
+      cudaGetDeviceCount(&ndev);
+      for (int q = 0; q < n; ++q) {
+        long long pci = 0;
+        std::memcpy(&pci, hb + (size_t)q * CBX_P2P_HANDLE_BYTES + 216, sizeof pci);
+        for (int d = 0; d < ndev && devs[q] < 0; ++d) {
+          int b = 0, i = 0, m = 0;
+          cudaDeviceGetAttribute(&b, cudaDevAttrPciBusId, d);
+          cudaDeviceGetAttribute(&i, cudaDevAttrPciDeviceId, d);
+          cudaDeviceGetAttribute(&m, cudaDevAttrPciDomainId, d);
+          if ((((long long)m << 32) | ((long long)b << 16) | i) == pci) devs[q] = d;
+        }
+        if (devs[q] < 0) atomics = false;
+      }
+      for (int a = 0; a < n && atomics; ++a)
+        for (int b = 0; b < n && atomics; ++b) {
+          if (a == b) continue;
+          int v = 0;
+          if (devs[a] == devs[b] ||
+              cudaDeviceGetP2PAttribute(&v, cudaDevP2PAttrNativeAtomicSupported, devs[a],
+                                        devs[b]) != cudaSuccess || !v)
+            atomics = false;
+        }
+      cudaGetLastError();
+      for (int side = 0; side < 2 && atomics; ++side) {
+        const int q = nb[side];
+        if (side == 1 && hi == lo) {  // two ranks: one neighbour on both sides
+          rho_nb[1] = rho_nb[0];
+          frc_nb[1] = frc_nb[0];
+        } else {
+          rho_nb[side] = open(q, 1);
+          frc_nb[side] = open(q, 2);
+        }
+        long long geo[3];
+        std::memcpy(geo, hb + (size_t)q * CBX_P2P_HANDLE_BYTES + 192, sizeof geo);
+        R.rho[side] = static_cast<double*>(rho_nb[side]);
+        R.frc[side] = static_cast<double*>(frc_nb[side]);
+        R.NC[side] = geo[0];
+        R.S[side] = geo[1];
+        // my lower halo lands on the top boundary planes of the rank below,
+        // my upper halo on the bottom boundary planes of the rank above
+        plane0[side] = side == 0 ? geo[2] : G.g;
+      }
+      R.lo = (long long)G.g * G.txy;
+      R.hi = (long long)(G.g + G.bz) * G.txy;
+      R.delta[0] = plane0[0] * G.txy;  // c in [0, g txy) -> the planes [bz_lo, bz_lo + g)
+      R.delta[1] = (long long)G.g * G.txy - R.hi;  // [hi, hi + g txy) -> [g, 2 g)
+      c->rev_mapped = atomics;
+    }
     auto flag = [&](unsigned char* b, int kind, int from) {
       return reinterpret_cast<unsigned long long*>(b + kFlagOff) + 2 * kind + from;
     };
@@ -2397,8 +2509,36 @@ CBX_API cbx_status cbx_slab_p2p_init(cbx_ctx* c, const void* handles, long nbyte
     L.nranks = n;
     c->d_links = c->alloc<P2PLinks>(1);
     cuda_check(cudaMemcpy(c->d_links, &L, sizeof L, cudaMemcpyHostToDevice), "p2p links");
-    cuda_check(cudaDeviceSynchronize(), "p2p init");
     c->p2p = true;
+    c->P.lk = c->d_links;
+    c->P.rev.on = rev_fused(c);
+    sync_kp(c);
+    cuda_check(cudaDeviceSynchronize(), "p2p init");
+    drop_graph(c);
+  });
+}
+
+// the reverse halos fused into the passes (1) or staged exchanges (0); every
+// rank must use the same: the Python connect() agrees on it and sets it
+CBX_API int cbx_slab_p2p_fused(cbx_ctx* c) { return c->P.rev.on ? 1 : 0; }
+// back to no device transport (a rank whose peers could not all map peer
+// memory; the caller then connects NCCL)
+CBX_API cbx_status cbx_slab_p2p_close(cbx_ctx* c) {
+  return guarded(c, [&] {
+    c->p2p = false;
+    c->P.rev.on = 0;
+    sync_kp(c);
+    drop_graph(c);
+  });
+}
+CBX_API cbx_status cbx_slab_p2p_set_fused(cbx_ctx* c, int on) {
+  return guarded(c, [&] {
+    if (!c->p2p) raise(CBX_LOGIC, "cbx_slab_p2p_set_fused: no peer-memory transport");
+    if (on && !c->rev_mapped)
+      raise(CBX_INVALID_ARGUMENT, "cbx_slab_p2p_set_fused: no native peer atomics");
+    c->fused_off = !on;
+    c->P.rev.on = rev_fused(c);
+    sync_kp(c);
     drop_graph(c);
   });
 }

@@ -74,8 +74,30 @@ struct DevStatus {
   unsigned long long cnt_cand, cnt_pair;
 };
 
+struct P2PLinks;
+
+// Reverse halo fused into the passes (z-slab ranks on the peer-memory
+// transport, Newton-3 stencil): a density / force partial for a site of my
+// halo planes is added straight into the owning neighbour's boundary site
+// (peer memory over NVLink) instead of being staged and sent by the RHO / FRC
+// exchanges.  Index 0: the neighbour below, 1: above.
+struct RevHalo {
+  double* rho[2];
+  double* frc[2];    // 3 planes of S[q]
+  long long S[2], NC[2];
+  long long lo, hi;  // my halo cells: cell < lo (below) or cell >= hi (above)
+  // cell shift of my halo block into the neighbour's frame (the halo planes'
+  // x/y images are already folded by tgt, so a partial's target is an owner
+  // column of the plane)
+  long long delta[2];
+  int on;
+};
+
 struct KP {
   Geo G;
+  RevHalo rev;
+  P2PLinks* lk;  // device copy of the peer links (fused reverse halo signals)
+  int rev_wait;  // per launch: wait for the neighbours' flags of this exchange first
   float4* uf;      // fp32 shadow (x, y, z, owner-or--1) for the candidate filter
   int* work;       // persistent-kernel work counters (zeroed per launch)
   FastTab fd, ff;  // density / force fast tables
@@ -172,6 +194,37 @@ __device__ __forceinline__ void set_error(DevStatus* st, int code) { atomicCAS(&
 // zero the pair-energy partials no block of this launch writes (entries
 // [written, n_pair_part)), so the finalize sums a fixed range without a
 // memset before every force pass
+// where a partial for site t goes: locally, or (fused reverse halo, halo
+// plane) into the neighbour's boundary site
+template <int A>
+__device__ __forceinline__ double* acc_ptr(const KP& P, long long t) {
+  if (P.rev.on) {
+    const int par = t >= P.G.NC;
+    const long long c = par ? t - P.G.NC : t;
+    if (c < P.rev.lo || c >= P.rev.hi) {
+      const int up = c >= P.rev.hi;
+      const long long d = (up ? P.rev.NC[1] : P.rev.NC[0]) * par + c +
+                          (up ? P.rev.delta[1] : P.rev.delta[0]);
+      if (A < 0) return (up ? P.rev.rho[1] : P.rev.rho[0]) + d;
+      return (up ? P.rev.frc[1] : P.rev.frc[0]) + A * (up ? P.rev.S[1] : P.rev.S[0]) + d;
+    }
+  }
+  return A < 0 ? P.rho + t : P.frc + (long long)A * P.S + t;
+}
+
+// the hot-loop form for the Newton-3 slot passes, whose half-list partners
+// lie at dz >= 0: only the upper halo can be hit; 32-bit site arithmetic
+__device__ __forceinline__ double* acc_ptr_up(const KP& P, int t, int A) {
+  const int NC = (int)P.G.NC;
+  const int par = t >= NC;
+  const int c = t - (par ? NC : 0);
+  if (c >= (int)P.rev.hi) {
+    const long long d = par * P.rev.NC[1] + c + P.rev.delta[1];
+    return A < 0 ? P.rev.rho[1] + d : P.rev.frc[1] + d;
+  }
+  return A < 0 ? P.rho + t : P.frc + t;
+}
+
 __device__ __forceinline__ void zero_pair_tail(const KP& P, int written) {
   if (blockIdx.x == 0)
     for (int i = written + threadIdx.x; i < P.n_pair_part; i += blockDim.x) P.part_pair[i] = 0.0;
@@ -263,6 +316,12 @@ int launch_p2p_exchange(const KP& P, const P2PLinks& L, int kind, long long gs_l
                          long long gs_hi, int* rem_base, cudaStream_t s);
 void launch_p2p_reduce(const KP& P, const P2PLinks& L, int energies, int kinetic,
                        cudaStream_t s);
+// fused reverse halo: raise the neighbours' flags of exchange `kind` (2 RHO,
+// 4 FRC) once the pass that added into their memory has completed
+void launch_rev_signal(const KP& P, int kind, cudaStream_t s);
+// wait for both neighbours' flags of exchange `kind` (a consumer that is not
+// k_embed / k_kick2, e.g. the evaluation's finalize)
+void launch_rev_wait(const KP& P, int kind, cudaStream_t s);
 long long slab_msg_bytes(const KP& P, int kind);
 long long slab_plane_bytes(const KP& P, int kind);
 void launch_slab_red_in(const KP& P, double* red, cudaStream_t s);

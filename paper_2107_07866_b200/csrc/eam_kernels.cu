@@ -25,6 +25,7 @@
 #include <vector>
 
 #include "cbx_device.cuh"
+#include "p2p.cuh"
 
 namespace cbx {
 
@@ -325,6 +326,7 @@ __device__ void clash_embed_body(const KP& P, int blk, int nblk) {
 __global__ void __launch_bounds__(256) k_embed(KP P, int nsb, int literal) {
   pdl_wait();
   pdl_trigger();
+  if (P.rev_wait && !rev_wait(P, P.rev_wait)) return;  // the neighbours' density partials
   if (blockIdx.x >= nsb) {
     clash_embed_body(P, blockIdx.x - nsb, gridDim.x - nsb);
     // the records' force accumulators for the force pass (clash_zero fused)
@@ -417,7 +419,7 @@ __device__ void clash_body(const KP& P, int blk, int nblk) {
       if (MODE == 0) {
         const double rho = pair_rho(P, r2);
         acc += rho;
-        if (kind == 0) atomicAdd(&P.rho[tidx], rho);
+        if (kind == 0) atomicAdd(acc_ptr<-1>(P, tidx), rho);
         else if (kind == 1) atomicAdd(&P.cl.rho[tidx], rho);
       } else {
         double fp, phi;
@@ -427,9 +429,9 @@ __device__ void clash_body(const KP& P, int blk, int nblk) {
         fy += gy;
         fz += gz;
         if (kind == 0) {
-          atomicAdd(&P.frc[tidx], -gx);
-          atomicAdd(&P.frc[S + tidx], -gy);
-          atomicAdd(&P.frc[2 * S + tidx], -gz);
+          atomicAdd(acc_ptr<0>(P, tidx), -gx);
+          atomicAdd(acc_ptr<1>(P, tidx), -gy);
+          atomicAdd(acc_ptr<2>(P, tidx), -gz);
           e += phi;
         } else if (kind == 1) {
           atomicAdd(&P.cl.fx[tidx], -gx);

@@ -69,4 +69,55 @@ __device__ inline void p2p_reduce_thread(const KP& P, const P2PLinks& L, int ene
   }
 }
 
+// thread 0 of the block: wait until every flag reaches `epoch` (or time out)
+__device__ inline bool wait_flags(const KP& P, const unsigned long long* const* flags, int nflags,
+                           unsigned long long epoch) {
+  __shared__ int s_ok;
+  if (threadIdx.x == 0) {
+    int ok = 1;
+    const unsigned long long t0 = global_ns();
+    for (int f = 0; f < nflags && ok; ++f)
+      while (ld_acquire_sys(flags[f]) < epoch) {
+        if (global_ns() - t0 > kWaitNs) {
+          set_error(P.st, CBX_RUNTIME);
+          ok = 0;
+          break;
+        }
+        __nanosleep(200);
+      }
+    s_ok = ok;
+  }
+  __syncthreads();
+  return s_ok != 0;
+}
+
+// all blocks done writing -> the last one bumps the epoch and raises the
+// peers' flags.  One system-scope fence per exchange: each block publishes
+// its stores at GPU scope (bar.sync + fence + arrival counter, the grid-sync
+// pattern); the last block's fence.sc.sys is cumulative over everything it
+// has observed, then the flags are plain system-scope stores.
+__device__ inline void signal_peers(const P2PLinks& L, int kind) {
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  __threadfence();
+  const unsigned t = atomicAdd(&L.done[kind], 1u);
+  if (t != gridDim.x - 1) return;
+  __threadfence();
+  L.done[kind] = 0;
+  const unsigned long long e = L.epoch[kind] + 1;
+  L.epoch[kind] = e;
+  __threadfence_system();
+  st_relaxed_sys(L.flag_dst[kind][0], e);
+  st_relaxed_sys(L.flag_dst[kind][1], e);
+}
+
+// the consumer of those partials: every block waits for both neighbours'
+// flags of exchange `kind` to reach this rank's own epoch (bumped by its own
+// pass, earlier in the stream)
+__device__ __forceinline__ bool rev_wait(const KP& P, int kind) {
+  const P2PLinks& L = *P.lk;
+  const unsigned long long* fl[2] = {L.flag_src[kind][0], L.flag_src[kind][1]};
+  return wait_flags(P, fl, 2, *(volatile unsigned long long*)&L.epoch[kind]);
+}
+
 }  // namespace cbx

@@ -185,11 +185,13 @@ __device__ __forceinline__ void unpack_plane_site(const KP& P, int kind, int fro
     P.frc[P.S + d] = 0.0;
     P.frc[2 * P.S + d] = 0.0;
     double4 p = ldcg(reinterpret_cast<const double4*>(buf) + q);
+    const int t = P.tgt[d];
+    const float w = __int_as_float(t == d ? -1 : t);  // owner column (x/y image) or self
     if (p.x < kVacantTest) {
       p.z = xadd(p.z, dz);  // periodic image across the global z boundary
-      P.uf[d] = make_float4((float)p.x, (float)p.y, (float)p.z, __int_as_float(-1));
+      P.uf[d] = make_float4((float)p.x, (float)p.y, (float)p.z, w);
     } else {
-      P.uf[d] = make_float4(kVacantF, kVacantF, kVacantF, __int_as_float(-1));
+      P.uf[d] = make_float4(kVacantF, kVacantF, kVacantF, w);
     }
     P.pdf[d] = p;
     P.tag[d] = ldcg(reinterpret_cast<const unsigned long long*>(buf + 2 * n * sizeof(double4)) + q);
@@ -300,48 +302,6 @@ __global__ void k_remote_df(KP P) {
 }
 
 // ------------------------------------------------------ P2P (peer memory)
-// thread 0 of the block: wait until every flag reaches `epoch` (or time out)
-__device__ bool wait_flags(const KP& P, const unsigned long long* const* flags, int nflags,
-                           unsigned long long epoch) {
-  __shared__ int s_ok;
-  if (threadIdx.x == 0) {
-    int ok = 1;
-    const unsigned long long t0 = global_ns();
-    for (int f = 0; f < nflags && ok; ++f)
-      while (ld_acquire_sys(flags[f]) < epoch) {
-        if (global_ns() - t0 > kWaitNs) {
-          set_error(P.st, CBX_RUNTIME);
-          ok = 0;
-          break;
-        }
-        __nanosleep(200);
-      }
-    s_ok = ok;
-  }
-  __syncthreads();
-  return s_ok != 0;
-}
-
-// all blocks done writing -> the last one bumps the epoch and raises the
-// peers' flags.  One system-scope fence per exchange: each block publishes
-// its stores at GPU scope (bar.sync + fence + arrival counter, the grid-sync
-// pattern); the last block's fence.sc.sys is cumulative over everything it
-// has observed, then the flags are plain system-scope stores.
-__device__ void signal_peers(const P2PLinks& L, int kind) {
-  __syncthreads();
-  if (threadIdx.x != 0) return;
-  __threadfence();
-  const unsigned t = atomicAdd(&L.done[kind], 1u);
-  if (t != gridDim.x - 1) return;
-  __threadfence();
-  L.done[kind] = 0;
-  const unsigned long long e = L.epoch[kind] + 1;
-  L.epoch[kind] = e;
-  __threadfence_system();
-  st_relaxed_sys(L.flag_dst[kind][0], e);
-  st_relaxed_sys(L.flag_dst[kind][1], e);
-}
-
 // both directions of one exchange, stored into the neighbours' buffers
 __global__ void __launch_bounds__(256) k_p2p_send(KP P, P2PLinks L, int kind) {
   unsigned char* dn = L.dst[kind][0];  // my "down" packet: the rank below's from-above buffer
@@ -458,6 +418,32 @@ __global__ void __launch_bounds__(256) k_p2p_recv(KP P, P2PLinks L, int kind, lo
     unpack_clash_thread(P, kind, lo + pb, gs_lo, rem_base + 0);  // below first, as the
     unpack_clash_thread(P, kind, hi + pb, gs_hi, rem_base + 1);  // staged path does
   }
+}
+
+// end of a pass with the fused reverse halo: its partials are in the
+// neighbours' memory (the pass grid has completed), publish them
+__global__ void k_rev_signal(KP P, int kind) {
+  pdl_wait();
+  pdl_trigger();
+  if (threadIdx.x != 0) return;
+  const P2PLinks& L = *P.lk;
+  __threadfence_system();
+  const unsigned long long e = L.epoch[kind] + 1;
+  L.epoch[kind] = e;
+  __threadfence_system();
+  st_relaxed_sys(L.flag_dst[kind][0], e);
+  st_relaxed_sys(L.flag_dst[kind][1], e);
+}
+void launch_rev_signal(const KP& P, int kind, cudaStream_t s) {
+  launch_pdl(k_rev_signal, 1, 32, 0, s, P, kind);
+}
+__global__ void k_rev_wait(KP P, int kind) {
+  pdl_wait();
+  pdl_trigger();
+  rev_wait(P, kind);
+}
+void launch_rev_wait(const KP& P, int kind, cudaStream_t s) {
+  launch_pdl(k_rev_wait, 1, 32, 0, s, P, kind);
 }
 
 __global__ void k_p2p_reduce(KP P, P2PLinks L, int energies, int kinetic) {

@@ -94,7 +94,7 @@ __device__ __noinline__ double guard_rho(KP* P, long long d, int j, int tgt, dou
     return 0.0;
   }
   const double rho = pair_rho(*P, r2x);
-  if (!full) red_add(&P->rho[tgt], rho);
+  if (!full) red_add(acc_ptr<-1>(*P, tgt), rho);
   return rho;
 }
 __device__ __noinline__ bool guard_force(KP* P, long long d, int j, int tgt, double dx,
@@ -112,16 +112,16 @@ __device__ __noinline__ bool guard_force(KP* P, long long d, int j, int tgt, dou
   q[2] = -fp * dz;
   q[3] = phi;
   if (!full) {
-    red_add(&P->frc[tgt], q[0]);
-    red_add(&P->frc[P->S + tgt], q[1]);
-    red_add(&P->frc[2 * P->S + tgt], q[2]);
+    red_add(acc_ptr<0>(*P, tgt), q[0]);
+    red_add(acc_ptr<1>(*P, tgt), q[1]);
+    red_add(acc_ptr<2>(*P, tgt), q[2]);
   }
   return true;
 }
 
 // ------------------------------------------------------------------ density
 // one skin candidate that passed the fp32 filter (rare): full decision
-template <bool FULL>
+template <bool FULL, bool REV = true>
 __device__ __forceinline__ double skin_density(const KP& P, KP* Pp, int par, int k, int d, int jj,
                                                int tw, double ax, double ay, double az,
                                                unsigned long long& m0, unsigned long long& m1) {
@@ -142,7 +142,7 @@ __device__ __forceinline__ double skin_density(const KP& P, KP* Pp, int par, int
   double A, Bc, Cc, D;
   ld256(P.fd.rec + 4 * (size_t)sg, A, Bc, Cc, D);
   const double rho = fma(fma(fma(A, s, Bc), s, Cc), s, D);
-  if (!FULL) red_add(&P.rho[to], rho);
+  if (!FULL) red_add(REV ? acc_ptr<-1>(P, to) : P.rho + to, rho);
   return rho;
 }
 
@@ -150,9 +150,10 @@ __device__ __forceinline__ double skin_density(const KP& P, KP* Pp, int par, int
 // 16-byte slot 2 i + (c ^ ((i >> 2) & 1)) (8 distinct bank quads for random i)
 __device__ __forceinline__ int smem_slot32(int i, int c) { return 2 * i + (c ^ ((i >> 2) & 1)); }
 
-template <bool FULL, int B, bool SMEM = false>
+template <bool FULL, int B, bool SMEM = false, bool REV = false>
 __device__ __forceinline__ void density_site(const KP& P, KP* Pp, int par, int d, bool live,
-                                             const double2* T = nullptr, int seg_lo = 0) {
+                                             const double2* T = nullptr, int seg_lo = 0,
+                                             bool rev_here = true) {
   const double4* __restrict__ pdf = P.pdf;
   const int* __restrict__ tgt = P.tgt;
   double ax = kVacant, ay = 0, az = 0, aw = 0;
@@ -226,7 +227,7 @@ __device__ __forceinline__ void density_site(const KP& P, KP* Pp, int par, int d
       if (in[b]) {
         const double rho = fma(fma(fma(tA[b], s[b], tB[b]), s[b], tC[b]), s[b], tD[b]);
         acc += rho;
-        if (!FULL) red_add(&P.rho[t[b]], rho);
+        if (!FULL) red_add(REV && rev_here ? acc_ptr_up(P, t[b], -1) : P.rho + t[b], rho);
         set_bit(m0, m1, k0 + b);
       }
     }
@@ -254,7 +255,7 @@ __device__ __forceinline__ void density_site(const KP& P, KP* Pp, int par, int d
 #pragma unroll
       for (int b = 0; b < 4; ++b)
         if (pass[b])
-          acc += skin_density<FULL>(P, Pp, par, k0 + b, d, jj[b], __float_as_int(pf[b].w), ax,
+          acc += skin_density<FULL, REV>(P, Pp, par, k0 + b, d, jj[b], __float_as_int(pf[b].w), ax,
                                     ay, az, m0, m1);
     }
   }
@@ -320,9 +321,9 @@ __device__ __forceinline__ double force_site(const KP& P, KP* Pp, int par, int d
       e = fma(0.5, o.phi, e);
     } else {
       e += o.phi;
-      red_add(&P.frc[to], o.qx);
-      red_add(&P.frc[S + to], o.qy);
-      red_add(&P.frc[2 * S + to], o.qz);
+      red_add(acc_ptr<0>(P, to), o.qx);
+      red_add(acc_ptr<1>(P, to), o.qy);
+      red_add(acc_ptr<2>(P, to), o.qz);
     }
   };
   for (int k0 = 0; k0 < nin; k0 += B) {
@@ -439,10 +440,10 @@ __device__ __forceinline__ unsigned long long warp_or64(unsigned long long m) {
 // force pass, lean variant: one pair per iteration, no batching, so the
 // register footprint allows 6-8 resident CTAs per SM (latency hidden by
 // warps instead of by in-thread batching).  Warp-uniform union sweep.
-template <bool FULL, bool SMEM, bool CMP = false>
+template <bool FULL, bool SMEM, bool CMP = false, bool REV = false>
 __device__ __forceinline__ double force_site_lean(const KP& P, KP* Pp, int par, int d,
                                                   bool live, const double2* T = nullptr,
-                                                  int seg_lo = 0) {
+                                                  int seg_lo = 0, bool rev_here = false) {
   const double4* __restrict__ pdf = P.pdf;
   const int* __restrict__ tgt = P.tgt;
   const long long S = P.S;
@@ -532,9 +533,18 @@ __device__ __forceinline__ double force_site_lean(const KP& P, KP* Pp, int par, 
     } else {
       e += phi;
       if (v && !(P.xp & 2)) {
-        red_add(&P.frc[t], qx);
-        red_add(&P.frc[S + t], qy);
-        red_add(&P.frc[2 * S + t], qz);
+        if (REV && rev_here) {  // warp-uniform: a plane within reach of the halo
+          double* f = acc_ptr_up(P, t, 0);
+          const long long st = (int)t - ((int)t >= (int)P.G.NC ? (int)P.G.NC : 0) >= (int)P.rev.hi
+                                   ? P.rev.S[1] : S;
+          red_add(f, qx);
+          red_add(f + st, qy);
+          red_add(f + 2 * st, qz);
+        } else {
+          red_add(&P.frc[t], qx);
+          red_add(&P.frc[S + t], qy);
+          red_add(&P.frc[2 * S + t], qz);
+        }
       }
     }
   }
@@ -621,6 +631,11 @@ __device__ __forceinline__ bool unit_cell(const Geo& G, int u, int lane, int w, 
   c = live ? (int)cell_of(cx + G.g, cy + G.g, cz + G.g, G) : 0;
   return live;
 }
+// warp w of unit u sits on a z plane whose partners can lie in a halo plane
+// (Newton-3 half lists reach dz >= 0 only, at most the ghost width)
+__device__ __forceinline__ bool near_halo(const Geo& G, int u, int w) {
+  return (u / strip_count(G)) * 4 + w + G.g >= G.bz;
+}
 // A group's first unit is static, spread round-robin over the CTAs (one per
 // SM), so a pass with fewer units than groups loads every SM alike; later
 // units come from the counter *ctr (reset by the kernel before the pass).
@@ -638,7 +653,7 @@ __device__ __forceinline__ int next_unit(int* ctr, int group, int nsb, volatile 
 // records): NT threads = NT/128 groups of 4 warps, one CTA per SM; B = 1
 // (one candidate per iteration) keeps the thread at 64 registers
 constexpr int kDensTabRecords = 3300;  // x 32 B = 105,600 B
-template <bool FULL, int B, int NT>
+template <bool FULL, int B, int NT, bool REV = false>
 __global__ void __launch_bounds__(NT, 1) k_density_smem(KP P, int nsb) {
   if (blockIdx.x >= nsb) {
     pdl_wait();
@@ -669,8 +684,8 @@ __global__ void __launch_bounds__(NT, 1) k_density_smem(KP P, int nsb) {
     int c;
     const bool live = unit_cell(G, u, lane, w, c);
     for (int par = 0; par < 2; ++par)
-      density_site<FULL, B, true>(P, P.dself, par, live ? (int)(par * G.NC + c) : 0, live, T,
-                                  seg_lo);
+      density_site<FULL, B, true, REV>(P, P.dself, par, live ? (int)(par * G.NC + c) : 0, live, T,
+                                       seg_lo, near_halo(G, u, w));
   }
 }
 
@@ -688,7 +703,7 @@ __global__ void __launch_bounds__(128, MINB) k_density_fast(KP P, int nsb) {
     for (int par = 0; par < 2; ++par) {
       int d;
       const bool live = brick_site(P.G, b, par, d);
-      density_site<FULL, B>(P, P.dself, par, d, live);
+      density_site<FULL, B, false, true>(P, P.dself, par, d, live);  // runtime rev check
     }
   }
 }
@@ -717,7 +732,7 @@ __global__ void __launch_bounds__(128, 4) k_force_fast(KP P) {
 // on their own brick.  Pairs below the window (cascade cores) read global.
 constexpr int kLeanTabRecords = 3300;  // x 64 B = 211,200 B (x 48 B = 158,400 B compressed)
 
-template <bool FULL, int NT, bool CMP>
+template <bool FULL, int NT, bool CMP, bool REV = false>
 __global__ void __launch_bounds__(NT, 1) k_force_lean_smem(KP P, int nsb) {
   if (blockIdx.x >= nsb) {
     pdl_wait();
@@ -760,8 +775,8 @@ __global__ void __launch_bounds__(NT, 1) k_force_lean_smem(KP P, int nsb) {
     int c;
     const bool live = unit_cell(G, u, lane, w, c);
     for (int par = 0; par < 2; ++par)
-      e += force_site_lean<FULL, true, CMP>(P, P.dself, par, live ? (int)(par * G.NC + c) : 0,
-                                            live, T, seg_lo);
+      e += force_site_lean<FULL, true, CMP, REV>(P, P.dself, par, live ? (int)(par * G.NC + c) : 0,
+                                                 live, T, seg_lo, near_halo(G, u, w));
   }
   for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
   if ((threadIdx.x & 31) == 0) P.part_pair[(blockIdx.x * blockDim.x + threadIdx.x) >> 5] = e;
@@ -807,14 +822,15 @@ bool launch_density_fast(const KP& P, int mode, int grid, cudaStream_t s) {
     const size_t bytes = (size_t)kDensTabRecords * 32;
     static bool attr = false;
     if (!attr) {
-      cudaFuncSetAttribute(k_density_smem<false, 1, 1024>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-      cudaFuncSetAttribute(k_density_smem<true, 1, 1024>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+      for (const void* k : {(const void*)k_density_smem<false, 1, 1024>,
+                            (const void*)k_density_smem<true, 1, 1024>,
+                            (const void*)k_density_smem<false, 1, 1024, true>})
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
       attr = true;
     }
     const int g = max(1, min(sm_count(), unit_count(P.G)));
     if (mode) launch_pdl(k_density_smem<true, 1, 1024>, g, 1024, bytes, s, P, g);
+    else if (P.rev.on) launch_pdl(k_density_smem<false, 1, 1024, true>, g + 4, 1024, bytes, s, P, g);
     else launch_pdl(k_density_smem<false, 1, 1024>, g + 4, 1024, bytes, s, P, g);
     return !mode;
   }
@@ -836,12 +852,15 @@ void launch_force_lean(const KP& P, int mode, cudaStream_t s) {
     // that fits the table and leaves the rest of the SM's 256 KB as L1 for
     // the partner gathers (an explicit carveout hint measured 10 % slower)
     for (const void* k : {(const void*)k_force_lean_smem<false, 1024, CMP>,
-                          (const void*)k_force_lean_smem<true, 1024, CMP>})
+                          (const void*)k_force_lean_smem<true, 1024, CMP>,
+                          (const void*)k_force_lean_smem<false, 1024, CMP, true>})
       cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
     attr = true;
   }
   const int g = max(1, min(sm_count(), unit_count(P.G)));
   if (mode) launch_pdl(k_force_lean_smem<true, 1024, CMP>, g, 1024, bytes, s, P, g);
+  else if (P.rev.on)
+    launch_pdl(k_force_lean_smem<false, 1024, CMP, true>, g + 4, 1024, bytes, s, P, g);
   else launch_pdl(k_force_lean_smem<false, 1024, CMP>, g + 4, 1024, bytes, s, P, g);
 }
 bool launch_force_fast(const KP& P, int mode, int grid, cudaStream_t s) {

@@ -704,6 +704,7 @@ __device__ void clash_kick2_body(const KP& P, int kick, int blk, int nblk) {
 __global__ void __launch_bounds__(256) k_kick2(KP P, int kick, int nsb) {
   pdl_wait();
   pdl_trigger();
+  if (P.rev_wait && !rev_wait(P, P.rev_wait)) return;  // the neighbours' force partials
   if (blockIdx.x >= nsb) {  // the clash records (fused k_clash_kick2)
     clash_kick2_body(P, kick, blockIdx.x - nsb, gridDim.x - nsb);
     return;

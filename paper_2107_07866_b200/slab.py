@@ -107,10 +107,14 @@ class SlabRank(DeviceStore):
         b = C.create_string_buffer(uid, 128)
         self._check(self.lib.cbx_slab_comm_init(self.h, b, 128))
 
+    P2P_HANDLE_BYTES = 256  # CBX_P2P_HANDLE_BYTES
+
     def p2p_handle(self) -> bytes:
-        """this rank's receive region as a 64-byte CUDA IPC handle"""
-        b = C.create_string_buffer(64)
-        self._check(self.lib.cbx_slab_p2p_handle(self.h, b, 64))
+        """this rank's peer-memory handle: CUDA IPC handles of its receive
+        region and of its rho / force accumulators, plus its slab geometry"""
+        n = self.P2P_HANDLE_BYTES
+        b = C.create_string_buffer(n)
+        self._check(self.lib.cbx_slab_p2p_handle(self.h, b, n))
         return b.raw
 
     def init_p2p(self, handles):
@@ -150,8 +154,20 @@ class SlabRank(DeviceStore):
                 import sys
                 print(f"slab: peer-memory transport unavailable ({err or 'another rank'}); "
                       "using NCCL", file=sys.stderr)
+                if not err:  # this rank mapped its peers: undo
+                    self._check(self.lib.cbx_slab_p2p_close(self.h))
                 self.transport = "nccl"
                 return self.connect("nccl", group)
+            # the reverse halos fused into the passes only if every rank can
+            fused = bool(self.lib.cbx_slab_p2p_fused(self.h))
+            if world > 1:
+                import torch.distributed as dist
+                flags = [None] * world
+                dist.all_gather_object(flags, fused, group=group)
+                if not all(flags) and fused:
+                    self._check(self.lib.cbx_slab_p2p_set_fused(self.h, 0))
+                fused = all(flags)
+            self.fused = fused
             self.transport = "p2p"
         elif transport == "nccl":
             uid = [SlabRank.nccl_unique_id() if self.rank == 0 else None]
@@ -159,6 +175,7 @@ class SlabRank(DeviceStore):
                 import torch.distributed as dist
                 dist.broadcast_object_list(uid, src=0, group=group)
             self.init_comm(uid[0])
+            self.fused = False
             self.transport = "nccl"
         else:
             raise ValueError(f"unknown transport {transport!r}")

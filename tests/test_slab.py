@@ -13,6 +13,7 @@ import numpy as np
 import pytest
 
 from helpers import assert_store_parity
+from paper_2107_07866_b200 import _lib
 from paper_2107_07866_b200 import slab as S
 
 
@@ -273,7 +274,13 @@ def native_rank(ref, path, transport):
     from paper_2107_07866_b200 import EamPotential
     dims, a0, g = ref.box
     r = S.SlabRank((*dims, a0, g), EamPotential.load(path), 0, 1)
-    r.connect(transport)
+    r.connect("p2p" if transport.startswith("p2p") else transport)
+    if transport.startswith("p2p"):
+        # the reverse halos fused into the passes (default) or staged
+        assert r.fused
+        if transport == "p2p-staged":
+            _lib.check(r.lib.cbx_slab_p2p_set_fused(r.h, 0), r.h)
+            assert not r.lib.cbx_slab_p2p_fused(r.h)
     r.upload_global(ref.store())
     r.set_state(ref.state())
     return r
@@ -292,7 +299,7 @@ def test_slab_local_exchange_single_rank(cuda, tables):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("transport", ["p2p", "nccl"])
+@pytest.mark.parametrize("transport", ["p2p", "p2p-staged", "nccl"])
 def test_slab_graph_eval_and_trajectory(cuda, tables, transport):
     """exchanges captured in the step graph (NCCL self send/recv, or the
     flag-synchronised peer-memory kernels): forces, energies and a 60-step
@@ -322,7 +329,7 @@ def test_slab_graph_eval_and_trajectory(cuda, tables, transport):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("transport", ["p2p", "nccl"])
+@pytest.mark.parametrize("transport", ["p2p", "p2p-staged", "nccl"])
 def test_slab_graph_cascade(cuda, tables, transport):
     """cascade with adaptive dt through the NCCL step graph: clash records,
     defect counts and the global-max-speed time step match the oracle"""
