@@ -235,8 +235,7 @@ __device__ __forceinline__ void density_site(const KP& P, KP* Pp, int par, int d
   // skin shells: fp32 filter, batched; a pass is rare
   const float4 af = make_float4((float)ax, (float)ay, (float)az, 0.f);
   const float hi = P.band_hi;
-  const int n_skin = (P.xp & 64) ? nin : n;  // timing experiment: no skin shells
-  for (int k0 = nin; k0 < n_skin; k0 += 4) {
+  for (int k0 = nin; k0 < n; k0 += 4) {
     float4 pf[4];
     int jj[4];
 #pragma unroll
@@ -462,88 +461,79 @@ __device__ __forceinline__ double force_site_lean(const KP& P, KP* Pp, int par, 
   }
   const bool guard = (m1 & kGuardBit) != 0;
   m1 &= ~kGuardBit;
-  const unsigned long long u0 = warp_or64(m0), u1 = warp_or64(m1);
-  unsigned cu = (unsigned)u0, co = (unsigned)m0;
-  unsigned pu1 = (unsigned)(u0 >> 32), po1 = (unsigned)(m0 >> 32);
-  unsigned pu2 = (unsigned)u1, po2 = (unsigned)m1;
-  unsigned pu3 = (unsigned)(u1 >> 32), po3 = (unsigned)(m1 >> 32);
-  int base = 0;
   const int* s_offs = g_soffs[par];
   const double ih = P.ff.ih;
   const double r2_idle = P.cut2_lo;
   double fx = 0.0, fy = 0.0, fz = 0.0, e = 0.0;
-  for (;;) {
-    while (cu == 0) {
-      if (base == 96) break;
-      cu = pu1;
-      co = po1;
-      pu1 = pu2;
-      po1 = po2;
-      pu2 = pu3;
-      po2 = po3;
-      pu3 = 0;
-      base += 32;
-    }
-    if (cu == 0) break;
-    const int bit = __ffs(cu) - 1;
-    cu &= cu - 1;
-    const bool v = (co >> bit) & 1;
-    const int j = v ? d + s_offs[(P.xp & 16) ? 0 : base + bit] : d;
-    double px, py, pz, pw;
-    ld256(pdf + j, px, py, pz, pw);
-    const int t = __ldg(tgt + j);
-    const double dx = xsub(ax, px), dy = xsub(ay, py), dz = xsub(az, pz);
-    double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
-    r2 = v ? r2 : r2_idle;
-    const double ri = rsqrt_nr(r2);
-    double sb;
-    const int seg = seg_index(P.ff, r2 * ri, sb);
-    double zA, zB, zC, zD, qA, qB, qC, qD;
-    const int li = seg - seg_lo;
-    if (SMEM && CMP && li >= 0) {  // 48-byte record, cubic terms in fp32
-      const double2 c0 = T[3 * li], c1 = T[3 * li + 1], c2 = T[3 * li + 2];
-      zB = c0.x; zC = c0.y; zD = c1.x; qB = c1.y; qC = c2.x;
-      const unsigned long long ab = (unsigned long long)__double_as_longlong(c2.y);
-      zA = (double)__uint_as_float((unsigned)ab);
-      qA = (double)__uint_as_float((unsigned)(ab >> 32));
-      qD = 0.0;
-    } else if (SMEM && li >= 0) {
-      const double2 c0 = smem_chunk(T, li, 0), c1 = smem_chunk(T, li, 1);
-      const double2 c2 = smem_chunk(T, li, 2), c3 = smem_chunk(T, li, 3);
-      zA = c0.x; zB = c0.y; zC = c1.x; zD = c1.y;
-      qA = c2.x; qB = c2.y; qC = c3.x; qD = c3.y;
-    } else {
-      const double* rec = P.ff.rec + 8 * (size_t)seg;
-      ld256(rec, zA, zB, zC, zD);
-      ld256(rec + 4, qA, qB, qC, qD);
-    }
-    const double s15 = 1.5 * sb, s2 = sb + sb;
-    const double z = fma(fma(fma(zA, sb, zB), sb, zC), sb, zD);
-    const double zs = fma(fma(zA, s15, zB), s2, zC);  // dz/ds
-    const double ps = fma(fma(qA, s15, qB), s2, qC);  // drho/ds
-    const double phi = v ? z * ri : 0.0;
-    const double dphi = fma(zs, ih, -phi) * ri;
-    const double mfp = v ? fma((adf + pw) * ps, ih, dphi) * ri : 0.0;
-    const double qx = mfp * dx, qy = mfp * dy, qz = mfp * dz;
-    fx -= qx;
-    fy -= qy;
-    fz -= qz;
-    if (FULL) {
-      e = fma(0.5, phi, e);
-    } else {
-      e += phi;
-      if (v && !(P.xp & 2)) {
-        if (REV && rev_here) {  // warp-uniform: a plane within reach of the halo
-          double* f = acc_ptr_up(P, t, 0);
-          const long long st = (int)t - ((int)t >= (int)P.G.NC ? (int)P.G.NC : 0) >= (int)P.rev.hi
-                                   ? P.rev.S[1] : S;
-          red_add(f, qx);
-          red_add(f + st, qy);
-          red_add(f + 2 * st, qz);
-        } else {
-          red_add(&P.frc[t], qx);
-          red_add(&P.frc[S + t], qy);
-          red_add(&P.frc[2 * S + t], qz);
+  // one 32-bit word of the mask at a time: the warp walks the union of its
+  // lanes' words (warp-uniform offset), lanes without the bit idle
+#pragma unroll 1
+  for (int wd = 0; wd < 4; ++wd) {
+    const unsigned long long mw = wd < 2 ? m0 : m1;
+    const unsigned co = (wd & 1) ? (unsigned)(mw >> 32) : (unsigned)mw;
+    unsigned cu = __reduce_or_sync(0xffffffffu, co);
+    const int* so = s_offs + 32 * wd;
+    while (cu) {
+      const int bit = __ffs(cu) - 1;
+      cu &= cu - 1;
+      const bool v = (co >> bit) & 1;
+      const int j = v ? d + so[bit] : d;
+      double px, py, pz, pw;
+      ld256(pdf + j, px, py, pz, pw);
+      const int t = __ldg(tgt + j);
+      const double dx = xsub(ax, px), dy = xsub(ay, py), dz = xsub(az, pz);
+      double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+      r2 = v ? r2 : r2_idle;
+      const double ri = rsqrt_nr(r2);
+      double sb;
+      const int seg = seg_index(P.ff, r2 * ri, sb);
+      double zA, zB, zC, zD, qA, qB, qC, qD;
+      const int li = seg - seg_lo;
+      if (SMEM && CMP && li >= 0) {  // 48-byte record, cubic terms in fp32
+        const double2 c0 = T[3 * li], c1 = T[3 * li + 1], c2 = T[3 * li + 2];
+        zB = c0.x; zC = c0.y; zD = c1.x; qB = c1.y; qC = c2.x;
+        const unsigned long long ab = (unsigned long long)__double_as_longlong(c2.y);
+        zA = (double)__uint_as_float((unsigned)ab);
+        qA = (double)__uint_as_float((unsigned)(ab >> 32));
+        qD = 0.0;
+      } else if (SMEM && li >= 0) {
+        const double2 c0 = smem_chunk(T, li, 0), c1 = smem_chunk(T, li, 1);
+        const double2 c2 = smem_chunk(T, li, 2), c3 = smem_chunk(T, li, 3);
+        zA = c0.x; zB = c0.y; zC = c1.x; zD = c1.y;
+        qA = c2.x; qB = c2.y; qC = c3.x; qD = c3.y;
+      } else {
+        const double* rec = P.ff.rec + 8 * (size_t)seg;
+        ld256(rec, zA, zB, zC, zD);
+        ld256(rec + 4, qA, qB, qC, qD);
+      }
+      const double s15 = 1.5 * sb, s2 = sb + sb;
+      const double z = fma(fma(fma(zA, sb, zB), sb, zC), sb, zD);
+      const double zs = fma(fma(zA, s15, zB), s2, zC);  // dz/ds
+      const double ps = fma(fma(qA, s15, qB), s2, qC);  // drho/ds
+      const double phi = v ? z * ri : 0.0;
+      const double dphi = fma(zs, ih, -phi) * ri;
+      const double mfp = v ? fma((adf + pw) * ps, ih, dphi) * ri : 0.0;
+      const double qx = mfp * dx, qy = mfp * dy, qz = mfp * dz;
+      fx -= qx;
+      fy -= qy;
+      fz -= qz;
+      if (FULL) {
+        e = fma(0.5, phi, e);
+      } else {
+        e += phi;
+        if (v) {
+          if (REV && rev_here) {  // warp-uniform: a plane within reach of the halo
+            double* f = acc_ptr_up(P, t, 0);
+            const long long st = (int)t - ((int)t >= (int)P.G.NC ? (int)P.G.NC : 0) >= (int)P.rev.hi
+                                     ? P.rev.S[1] : S;
+            red_add(f, qx);
+            red_add(f + st, qy);
+            red_add(f + 2 * st, qz);
+          } else {
+            red_add(&P.frc[t], qx);
+            red_add(&P.frc[S + t], qy);
+            red_add(&P.frc[2 * S + t], qz);
+          }
         }
       }
     }
@@ -636,18 +626,22 @@ __device__ __forceinline__ bool unit_cell(const Geo& G, int u, int lane, int w, 
 __device__ __forceinline__ bool near_halo(const Geo& G, int u, int w) {
   return (u / strip_count(G)) * 4 + w + G.g >= G.bz;
 }
-// A group's first unit is static, spread round-robin over the CTAs (one per
-// SM), so a pass with fewer units than groups loads every SM alike; later
-// units come from the counter *ctr (reset by the kernel before the pass).
-__device__ __forceinline__ int next_unit(int* ctr, int group, int nsb, volatile int* slot,
-                                         bool first) {
-  if (first) return blockIdx.x + nsb * group;
-  asm volatile("bar.sync %0, 128;" ::"r"(group + 1));
-  if ((threadIdx.x & 127) == 0) slot[group] = 8 * nsb + atomicAdd(ctr, 1);
-  asm volatile("bar.sync %0, 128;" ::"r"(group + 1));
-  return slot[group];
+// CTA b owns the contiguous unit range [b nu / nsb, (b + 1) nu / nsb): its
+// concurrent groups sit on neighbouring strips of one z block and share most
+// of their partner rows in L1 (scattered units shared none).  Within the
+// range the groups take units in order from a shared-memory counter, so a
+// heavier unit (a cascade core) delays only its own group.
+__device__ __forceinline__ int unit_lo(int b, int nsb, int nu) {
+  return (int)(((long long)b * nu) / nsb);
 }
-
+__device__ __forceinline__ int next_unit(int* s_ctr, int group, int nsb, int nu,
+                                         volatile int* slot) {
+  asm volatile("bar.sync %0, 128;" ::"r"(group + 1));
+  if ((threadIdx.x & 127) == 0) slot[group] = unit_lo(blockIdx.x, nsb, nu) + atomicAdd(s_ctr, 1);
+  asm volatile("bar.sync %0, 128;" ::"r"(group + 1));
+  const int u = slot[group];
+  return u < unit_lo(blockIdx.x + 1, nsb, nu) ? u : nu;
+}
 
 // density pass with the upper rho-spline window in shared memory (32-byte
 // records): NT threads = NT/128 groups of 4 warps, one CTA per SM; B = 1
@@ -663,8 +657,10 @@ __global__ void __launch_bounds__(NT, 1) k_density_smem(KP P, int nsb) {
   }
   extern __shared__ __align__(16) unsigned char smem_tab[];
   __shared__ int s_slot[NT / 128];
+  __shared__ int s_ctr;
   double2* T = reinterpret_cast<double2*>(smem_tab);
   const int nseg = P.fd.nseg;
+  if (threadIdx.x == 0) s_ctr = 0;
   const int seg_lo = max(0, nseg + 1 - kDensTabRecords);
   const int nrec = nseg + 1 - seg_lo;
   const double2* src = reinterpret_cast<const double2*>(P.fd.rec + 4 * (size_t)seg_lo);
@@ -678,8 +674,8 @@ __global__ void __launch_bounds__(NT, 1) k_density_smem(KP P, int nsb) {
   const int lt = threadIdx.x & 127, lane = lt & 31, w = lt >> 5;
   const Geo& G = P.G;
   const int nu = unit_count(G);
-  for (bool first = true;; first = false) {
-    const int u = next_unit(&P.work[0], group, nsb, s_slot, first);
+  for (;;) {
+    const int u = next_unit(&s_ctr, group, nsb, nu, s_slot);
     if (u >= nu) break;
     int c;
     const bool live = unit_cell(G, u, lane, w, c);
@@ -742,8 +738,10 @@ __global__ void __launch_bounds__(NT, 1) k_force_lean_smem(KP P, int nsb) {
   }
   extern __shared__ __align__(16) unsigned char smem_tab[];
   __shared__ int s_slot[8];
+  __shared__ int s_ctr;
   double2* T = reinterpret_cast<double2*>(smem_tab);
   const int nseg = P.ff.nseg;  // records 0..nseg (padded)
+  if (threadIdx.x == 0) s_ctr = 0;
   const int seg_lo = max(0, nseg + 1 - kLeanTabRecords);
   const int nrec = nseg + 1 - seg_lo;
   if (CMP) {  // 48-byte records, three 16-byte chunks each, in order
@@ -769,8 +767,8 @@ __global__ void __launch_bounds__(NT, 1) k_force_lean_smem(KP P, int nsb) {
   const Geo& G = P.G;
   const int nu = unit_count(G);
   double e = 0.0;
-  for (bool first = true;; first = false) {
-    const int u = next_unit(&P.work[1], group, nsb, s_slot, first);
+  for (;;) {
+    const int u = next_unit(&s_ctr, group, nsb, nu, s_slot);
     if (u >= nu) break;
     int c;
     const bool live = unit_cell(G, u, lane, w, c);
