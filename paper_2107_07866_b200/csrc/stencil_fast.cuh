@@ -119,6 +119,33 @@ __device__ __noinline__ bool guard_force(KP* P, long long d, int j, int tgt, dou
   return true;
 }
 
+// 1/sqrt for r^2 in the normal range: the hardware approximation plus two
+// Newton steps (relative error a few ulp, no special-case branch)
+__device__ __forceinline__ double rsqrt_nr(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double h = 0.5 * x;
+  y = y * fma(-h * y, y, 1.5);
+  y = y * fma(-h * y, y, 1.5);
+  return y;
+}
+
+// shared-memory loads through a 32-bit shared address held in a register
+// (the generic-to-shared conversion is done once per kernel, not per load)
+__device__ __forceinline__ unsigned smem_addr(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ double2 lds2(unsigned a) {
+  double2 v;
+  asm("ld.shared.v2.f64 {%0,%1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ int lds_i(unsigned a) {
+  int v;
+  asm("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+
 // ------------------------------------------------------------------ density
 // one skin candidate that passed the fp32 filter (rare): full decision
 template <bool FULL, bool REV = true>
@@ -152,7 +179,7 @@ __device__ __forceinline__ int smem_slot32(int i, int c) { return 2 * i + (c ^ (
 
 template <bool FULL, int B, bool SMEM = false, bool REV = false>
 __device__ __forceinline__ void density_site(const KP& P, KP* Pp, int par, int d, bool live,
-                                             const double2* T = nullptr, int seg_lo = 0,
+                                             unsigned tb = 0, int seg_lo = 0,
                                              bool rev_here = true) {
   const double4* __restrict__ pdf = P.pdf;
   const int* __restrict__ tgt = P.tgt;
@@ -206,21 +233,21 @@ __device__ __forceinline__ void density_site(const KP& P, KP* Pp, int par, int d
       }
     }
 #pragma unroll
-    for (int b = 0; b < B; ++b) seg[b] = seg_index(P.fd, r2[b] * rsqrt(r2[b]), s[b]);
+    for (int b = 0; b < B; ++b) seg[b] = seg_index(P.fd, r2[b] * rsqrt_nr(r2[b]), s[b]);
     double tA[B], tB[B], tC[B], tD[B];
 #pragma unroll
     for (int b = 0; b < B; ++b)
       if (in[b]) {
         const int li = seg[b] - seg_lo;
-        if (SMEM && li >= 0) {
-          const double2 c0 = T[smem_slot32(li, 0)], c1 = T[smem_slot32(li, 1)];
+        if (SMEM) {
+          const int lc = max(li, 0);
+          const double2 c0 = lds2(tb + 16 * smem_slot32(lc, 0)), c1 = lds2(tb + 16 * smem_slot32(lc, 1));
           tA[b] = c0.x;
           tB[b] = c0.y;
           tC[b] = c1.x;
           tD[b] = c1.y;
-        } else {
-          ld256(P.fd.rec + 4 * (size_t)seg[b], tA[b], tB[b], tC[b], tD[b]);
         }
+        if (!SMEM || li < 0) ld256(P.fd.rec + 4 * (size_t)seg[b], tA[b], tB[b], tC[b], tD[b]);
       }
 #pragma unroll
     for (int b = 0; b < B; ++b) {
@@ -418,17 +445,6 @@ __device__ __forceinline__ double2 smem_chunk(const double2* T, int i, int c) {
   return T[smem_slot(i, c)];
 }
 
-// 1/sqrt for r^2 in the normal range: the hardware approximation plus two
-// Newton steps (relative error a few ulp, no special-case branch)
-__device__ __forceinline__ double rsqrt_nr(double x) {
-  double y;
-  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-  const double h = 0.5 * x;
-  y = y * fma(-h * y, y, 1.5);
-  y = y * fma(-h * y, y, 1.5);
-  return y;
-}
-
 // OR of a 64-bit value over the warp (the union of the lanes' pair masks)
 __device__ __forceinline__ unsigned long long warp_or64(unsigned long long m) {
   const unsigned lo = __reduce_or_sync(0xffffffffu, (unsigned)m);
@@ -441,7 +457,7 @@ __device__ __forceinline__ unsigned long long warp_or64(unsigned long long m) {
 // warps instead of by in-thread batching).  Warp-uniform union sweep.
 template <bool FULL, bool SMEM, bool CMP = false, bool REV = false>
 __device__ __forceinline__ double force_site_lean(const KP& P, KP* Pp, int par, int d,
-                                                  bool live, const double2* T = nullptr,
+                                                  bool live, unsigned tb = 0,
                                                   int seg_lo = 0, bool rev_here = false) {
   const double4* __restrict__ pdf = P.pdf;
   const int* __restrict__ tgt = P.tgt;
@@ -461,7 +477,7 @@ __device__ __forceinline__ double force_site_lean(const KP& P, KP* Pp, int par, 
   }
   const bool guard = (m1 & kGuardBit) != 0;
   m1 &= ~kGuardBit;
-  const int* s_offs = g_soffs[par];
+  const unsigned s_offs = smem_addr(g_soffs[par]);
   const double ih = P.ff.ih;
   const double r2_idle = P.cut2_lo;
   double fx = 0.0, fy = 0.0, fz = 0.0, e = 0.0;
@@ -472,12 +488,12 @@ __device__ __forceinline__ double force_site_lean(const KP& P, KP* Pp, int par, 
     const unsigned long long mw = wd < 2 ? m0 : m1;
     const unsigned co = (wd & 1) ? (unsigned)(mw >> 32) : (unsigned)mw;
     unsigned cu = __reduce_or_sync(0xffffffffu, co);
-    const int* so = s_offs + 32 * wd;
+    const unsigned so = s_offs + 128 * wd;
     while (cu) {
       const int bit = __ffs(cu) - 1;
       cu &= cu - 1;
       const bool v = (co >> bit) & 1;
-      const int j = v ? d + so[bit] : d;
+      const int j = v ? d + lds_i(so + 4 * bit) : d;
       double px, py, pz, pw;
       ld256(pdf + j, px, py, pz, pw);
       const int t = __ldg(tgt + j);
@@ -489,19 +505,22 @@ __device__ __forceinline__ double force_site_lean(const KP& P, KP* Pp, int par, 
       const int seg = seg_index(P.ff, r2 * ri, sb);
       double zA, zB, zC, zD, qA, qB, qC, qD;
       const int li = seg - seg_lo;
-      if (SMEM && CMP && li >= 0) {  // 48-byte record, cubic terms in fp32
-        const double2 c0 = T[3 * li], c1 = T[3 * li + 1], c2 = T[3 * li + 2];
+      const int lc = max(li, 0);
+      if (SMEM && CMP) {  // 48-byte record, cubic terms in fp32
+        const unsigned a = tb + 48 * lc;
+        const double2 c0 = lds2(a), c1 = lds2(a + 16), c2 = lds2(a + 32);
         zB = c0.x; zC = c0.y; zD = c1.x; qB = c1.y; qC = c2.x;
         const unsigned long long ab = (unsigned long long)__double_as_longlong(c2.y);
         zA = (double)__uint_as_float((unsigned)ab);
         qA = (double)__uint_as_float((unsigned)(ab >> 32));
         qD = 0.0;
-      } else if (SMEM && li >= 0) {
-        const double2 c0 = smem_chunk(T, li, 0), c1 = smem_chunk(T, li, 1);
-        const double2 c2 = smem_chunk(T, li, 2), c3 = smem_chunk(T, li, 3);
+      } else if (SMEM) {
+        const double2 c0 = lds2(tb + 16 * smem_slot(lc, 0)), c1 = lds2(tb + 16 * smem_slot(lc, 1));
+        const double2 c2 = lds2(tb + 16 * smem_slot(lc, 2)), c3 = lds2(tb + 16 * smem_slot(lc, 3));
         zA = c0.x; zB = c0.y; zC = c1.x; zD = c1.y;
         qA = c2.x; qB = c2.y; qC = c3.x; qD = c3.y;
-      } else {
+      }
+      if (!SMEM || li < 0) {  // below the window (cascade cores): global record
         const double* rec = P.ff.rec + 8 * (size_t)seg;
         ld256(rec, zA, zB, zC, zD);
         ld256(rec + 4, qA, qB, qC, qD);
@@ -680,8 +699,8 @@ __global__ void __launch_bounds__(NT, 1) k_density_smem(KP P, int nsb) {
     int c;
     const bool live = unit_cell(G, u, lane, w, c);
     for (int par = 0; par < 2; ++par)
-      density_site<FULL, B, true, REV>(P, P.dself, par, live ? (int)(par * G.NC + c) : 0, live, T,
-                                       seg_lo, near_halo(G, u, w));
+      density_site<FULL, B, true, REV>(P, P.dself, par, live ? (int)(par * G.NC + c) : 0, live,
+                                       smem_addr(T), seg_lo, near_halo(G, u, w));
   }
 }
 
@@ -774,7 +793,7 @@ __global__ void __launch_bounds__(NT, 1) k_force_lean_smem(KP P, int nsb) {
     const bool live = unit_cell(G, u, lane, w, c);
     for (int par = 0; par < 2; ++par)
       e += force_site_lean<FULL, true, CMP, REV>(P, P.dself, par, live ? (int)(par * G.NC + c) : 0,
-                                                 live, T, seg_lo, near_halo(G, u, w));
+                                                 live, smem_addr(T), seg_lo, near_halo(G, u, w));
   }
   for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
   if ((threadIdx.x & 31) == 0) P.part_pair[(blockIdx.x * blockDim.x + threadIdx.x) >> 5] = e;
