@@ -405,7 +405,7 @@ void slab_finish(cbx_ctx* c, int kick, int stepping, int energies) {
   }
   if (kick >= 0) {
     launch_kick2(c->P, kick, stepping, energies, c->stream);
-    c->launches += 2;
+    c->launches += 1;
   } else {
     launch_finalize(c->P, stepping, energies, c->stream);
     c->launches += 1;
@@ -493,7 +493,7 @@ void seq_step(cbx_ctx* c) {
   seq_force(c);
   ev_mark(c, 4);
   launch_kick2(c->P, 1, 1, 1, c->stream);
-  c->launches += 2;
+  c->launches += 1;
   ev_mark(c, 5);
 }
 
@@ -1554,7 +1554,7 @@ CBX_API cbx_status cbx_measure(cbx_ctx* c) {
       slab_finish(c, 0, 0, 0);
     } else {
       launch_kick2(c->P, 0, 0, 0, c->stream);
-      c->launches += 2;
+      c->launches += 1;
     }
     sync_status(c);
     raise_device_error(c, false);
@@ -2203,7 +2203,7 @@ CBX_API cbx_status cbx_slab_phase(cbx_ctx* c, int phase, double dt) {
         break;
       case 5:
         launch_kick2(c->P, 1, 1, 1, c->stream);
-        c->launches += 2;
+        c->launches += 1;
         break;
       case 6:
         launch_finalize(c->P, -1, 1, c->stream);
@@ -2211,7 +2211,7 @@ CBX_API cbx_status cbx_slab_phase(cbx_ctx* c, int phase, double dt) {
         break;
       case 7:  // measure only (kinetic energy, max speed)
         launch_kick2(c->P, 0, 0, 0, c->stream);
-        c->launches += 2;
+        c->launches += 1;
         break;
       default:
         raise(CBX_INVALID_ARGUMENT, "cbx_slab_phase: unknown phase");

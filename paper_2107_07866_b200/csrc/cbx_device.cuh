@@ -72,6 +72,7 @@ struct DevStatus {
   int adaptive;
   double dt_max, max_disp;
   unsigned long long cnt_cand, cnt_pair;
+  unsigned fin_count;  // blocks of k_kick2 done (the last one runs the finalize)
 };
 
 struct P2PLinks;

@@ -346,9 +346,10 @@ __global__ void __launch_bounds__(256) k_embed(KP P, int nsb, int literal) {
   const bool ok = !P.st->err && !P.st->n_ovl;
   for (long long d = (long long)blockIdx.x * blockDim.x + threadIdx.x; ok && d < P.S;
        d += (long long)nsb * blockDim.x) {
-    const double4 p = P.pdf[d];
-    if (p.x >= kVacantTest) continue;
+    // the site's position and owner in one round trip, then the owner's rho
+    const double px = P.pdf[d].x;
     const int t = P.tgt[d];
+    if (px >= kVacantTest) continue;
     const double r = P.rho[t];
     double v, dv;
     if (literal) seg_eval(P.emb, r, v, dv);
@@ -514,10 +515,10 @@ int pair_partials(const KP& P, int mode) {
   int sms = 148, dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  int n = std::max(eam_blocks(P), 32 * sms);  // 1024-thread persistent variants
-  for (int m = 0; m < 2; ++m) {
-    n = std::max(n, 4 * fast_grid(P, true, m));
-  }
+  // one partial per CTA: the literal pass (eam_blocks), the 1024-thread
+  // mask-replay pass (one CTA per SM + clash blocks), the 128-thread pass
+  int n = std::max(eam_blocks(P), sms + 8);
+  for (int m = 0; m < 2; ++m) n = std::max(n, fast_grid(P, true, m));
   return std::min(n, P.n_part);
 }
 void launch_embed(const KP& P, cudaStream_t s, bool literal) {

@@ -180,7 +180,7 @@ __device__ __forceinline__ int smem_slot32(int i, int c) { return 2 * i + (c ^ (
 template <bool FULL, int B, bool SMEM = false, bool REV = false>
 __device__ __forceinline__ void density_site(const KP& P, KP* Pp, int par, int d, bool live,
                                              unsigned tb = 0, int seg_lo = 0,
-                                             bool rev_here = true) {
+                                             bool rev_here = true, bool deep = false) {
   const double4* __restrict__ pdf = P.pdf;
   const int* __restrict__ tgt = P.tgt;
   double ax = kVacant, ay = 0, az = 0, aw = 0;
@@ -206,7 +206,7 @@ __device__ __forceinline__ void density_site(const KP& P, KP* Pp, int par, int d
       j[b] = d + offs[min(k0 + b, nin - 1)];
       double w;
       ld256(pdf + j[b], px[b], py[b], pz[b], w);
-      t[b] = __ldg(tgt + j[b]);
+      t[b] = deep ? j[b] : __ldg(tgt + j[b]);
     }
     bool rare = false;
 #pragma unroll
@@ -458,7 +458,8 @@ __device__ __forceinline__ unsigned long long warp_or64(unsigned long long m) {
 template <bool FULL, bool SMEM, bool CMP = false, bool REV = false>
 __device__ __forceinline__ double force_site_lean(const KP& P, KP* Pp, int par, int d,
                                                   bool live, unsigned tb = 0,
-                                                  int seg_lo = 0, bool rev_here = false) {
+                                                  int seg_lo = 0, bool rev_here = false,
+                                                  bool deep = false) {
   const double4* __restrict__ pdf = P.pdf;
   const int* __restrict__ tgt = P.tgt;
   const long long S = P.S;
@@ -496,7 +497,7 @@ __device__ __forceinline__ double force_site_lean(const KP& P, KP* Pp, int par, 
       const int j = v ? d + lds_i(so + 4 * bit) : d;
       double px, py, pz, pw;
       ld256(pdf + j, px, py, pz, pw);
-      const int t = __ldg(tgt + j);
+      const int t = deep ? j : __ldg(tgt + j);
       const double dx = xsub(ax, px), dy = xsub(ay, py), dz = xsub(az, pz);
       double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
       r2 = v ? r2 : r2_idle;
@@ -590,6 +591,21 @@ __device__ __forceinline__ double force_site_lean(const KP& P, KP* Pp, int par, 
   return e;
 }
 
+// one pair-energy partial per CTA: warp sums, then the warps in order
+// (deterministic for a given grid)
+template <int NT>
+__device__ __forceinline__ void block_partial(double e, double* part) {
+  __shared__ double s_w[NT / 32];
+  for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
+  if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = e;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int i = 0; i < NT / 32; ++i) t += s_w[i];
+    part[blockIdx.x] = t;
+  }
+}
+
 // persistent CTAs over bricks: warp w owns z-plane w of the brick and sweeps
 // both sublattices (even then odd: balanced half-list lengths 46 + 66)
 __device__ __forceinline__ int next_brick(int* ctr) {
@@ -639,6 +655,18 @@ __device__ __forceinline__ bool unit_cell(const Geo& G, int u, int lane, int w, 
   const int cy = e / G.bx, cx = e - cy * G.bx;
   c = live ? (int)cell_of(cx + G.g, cy + G.g, cz + G.g, G) : 0;
   return live;
+}
+// a "deep" site has every stencil partner in an interior cell (the offsets
+// reach at most g cells per axis; half lists reach up in z only), so each
+// partner is its own owner and the owner load tgt[j] is skipped.  On a slab
+// rank the z-halo planes' owner is the site itself too (tgt, capi.cu), so
+// only x and y matter there.
+__device__ __forceinline__ bool unit_deep(const Geo& G, int u, int lane, int w, bool full) {
+  const int ns = strip_count(G);
+  const int zb = u / ns, e = (u - zb * ns) * 32 + lane, cz = zb * 4 + w;
+  const int cy = e / G.bx, cx = e - cy * G.bx;
+  return cx >= G.g && cx < G.bx - G.g && cy >= G.g && cy < G.by - G.g &&
+         (G.slab || (cz < G.bz - G.g && (!full || cz >= G.g)));
 }
 // warp w of unit u sits on a z plane whose partners can lie in a halo plane
 // (Newton-3 half lists reach dz >= 0 only, at most the ghost width)
@@ -698,9 +726,10 @@ __global__ void __launch_bounds__(NT, 1) k_density_smem(KP P, int nsb) {
     if (u >= nu) break;
     int c;
     const bool live = unit_cell(G, u, lane, w, c);
+    const bool deep = live && unit_deep(G, u, lane, w, FULL);
     for (int par = 0; par < 2; ++par)
       density_site<FULL, B, true, REV>(P, P.dself, par, live ? (int)(par * G.NC + c) : 0, live,
-                                       smem_addr(T), seg_lo, near_halo(G, u, w));
+                                       smem_addr(T), seg_lo, near_halo(G, u, w), deep);
   }
 }
 
@@ -725,7 +754,7 @@ __global__ void __launch_bounds__(128, MINB) k_density_fast(KP P, int nsb) {
 
 template <bool FULL, int B>
 __global__ void __launch_bounds__(128, 4) k_force_fast(KP P) {
-  zero_pair_tail(P, gridDim.x * blockDim.x / 32);
+  zero_pair_tail(P, gridDim.x);
   if (P.st->err || P.st->n_ovl) return;
   const int nb = brick_count(P.G);
   double e = 0.0;
@@ -738,8 +767,7 @@ __global__ void __launch_bounds__(128, 4) k_force_fast(KP P) {
       e += force_site<FULL, B>(P, P.dself, par, d, live);
     }
   }
-  for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
-  if ((threadIdx.x & 31) == 0) P.part_pair[(blockIdx.x * blockDim.x + threadIdx.x) >> 5] = e;
+  block_partial<128>(e, P.part_pair);
 }
 
 // lean force pass with the upper spline window (records [seg_lo, nseg])
@@ -779,7 +807,7 @@ __global__ void __launch_bounds__(NT, 1) k_force_lean_smem(KP P, int nsb) {
   __syncthreads();
   pdl_wait();
   pdl_trigger();
-  zero_pair_tail(P, nsb * blockDim.x / 32);
+  zero_pair_tail(P, nsb);
   if (P.st->err || P.st->n_ovl) return;
   const int group = threadIdx.x >> 7;
   const int lt = threadIdx.x & 127, lane = lt & 31, w = lt >> 5;
@@ -791,12 +819,13 @@ __global__ void __launch_bounds__(NT, 1) k_force_lean_smem(KP P, int nsb) {
     if (u >= nu) break;
     int c;
     const bool live = unit_cell(G, u, lane, w, c);
+    const bool deep = live && unit_deep(G, u, lane, w, FULL);
     for (int par = 0; par < 2; ++par)
       e += force_site_lean<FULL, true, CMP, REV>(P, P.dself, par, live ? (int)(par * G.NC + c) : 0,
-                                                 live, smem_addr(T), seg_lo, near_halo(G, u, w));
+                                                 live, smem_addr(T), seg_lo, near_halo(G, u, w),
+                                                 deep);
   }
-  for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
-  if ((threadIdx.x & 31) == 0) P.part_pair[(blockIdx.x * blockDim.x + threadIdx.x) >> 5] = e;
+  block_partial<NT>(e, P.part_pair);
 }
 
 // persistent grid of the 128-thread kernels (density fallback, decision-

@@ -701,45 +701,64 @@ __device__ void clash_kick2_body(const KP& P, int kick, int blk, int nblk) {
   }
 }
 
-__global__ void __launch_bounds__(256) k_kick2(KP P, int kick, int nsb) {
+template <int NT>
+__device__ void finalize_body(const KP& P, int stepping, int energies, const double* pe, int n_emb,
+                              const double* pp, int n_pairp, int n_ke);
+
+// fin: the last block to finish runs finalize_body (the StepState sums) --
+// one launch less per step than a separate k_finalize
+__global__ void __launch_bounds__(256) k_kick2(KP P, int kick, int nsb, int fin, int stepping,
+                                               int energies, int n_pairp, int n_emb) {
   pdl_wait();
   pdl_trigger();
   if (P.rev_wait && !rev_wait(P, P.rev_wait)) return;  // the neighbours' force partials
+  __shared__ double sh[8];
   if (blockIdx.x >= nsb) {  // the clash records (fused k_clash_kick2)
     clash_kick2_body(P, kick, blockIdx.x - nsb, gridDim.x - nsb);
-    return;
-  }
-  __shared__ double sh[8];
-  double v2 = 0.0;
-  int par;
-  long long d;
-  if (!P.st->err && !P.st->n_ovl && map_site(P, par, d)) {
-    // every load of the site issued before the first use (one memory round
-    // trip per thread; a vacant slot's velocity/force reads are discarded)
-    const long long S = P.S;
-    const double px = P.pdf[d].x;
-    double vx = P.vel[d], vy = P.vel[S + d], vz = P.vel[2 * S + d];
-    const double fx = P.frc[d], fy = P.frc[S + d], fz = P.frc[2 * S + d];
-    const double dt = P.st->dt_next;
-    if (px < kVacantTest) {
-      if (kick) {
-        const double hk = half_kick(P, dt);
-        vx = xadd(vx, xmul(fx, hk));
-        vy = xadd(vy, xmul(fy, hk));
-        vz = xadd(vz, xmul(fz, hk));
-        P.vel[d] = vx;
-        P.vel[S + d] = vy;
-        P.vel[2 * S + d] = vz;
+  } else {
+    double v2 = 0.0;
+    int par;
+    long long d;
+    if (!P.st->err && !P.st->n_ovl && map_site(P, par, d)) {
+      // every load of the site issued before the first use (one memory round
+      // trip per thread; a vacant slot's velocity/force reads are discarded)
+      const long long S = P.S;
+      const double px = P.pdf[d].x;
+      double vx = P.vel[d], vy = P.vel[S + d], vz = P.vel[2 * S + d];
+      const double fx = P.frc[d], fy = P.frc[S + d], fz = P.frc[2 * S + d];
+      const double dt = P.st->dt_next;
+      if (px < kVacantTest) {
+        if (kick) {
+          const double hk = half_kick(P, dt);
+          vx = xadd(vx, xmul(fx, hk));
+          vy = xadd(vy, xmul(fy, hk));
+          vz = xadd(vz, xmul(fz, hk));
+          P.vel[d] = vx;
+          P.vel[S + d] = vy;
+          P.vel[2 * S + d] = vz;
+        }
+        v2 = exact_r2(vx, vy, vz);
       }
-      v2 = exact_r2(vx, vy, vz);
+    }
+    const double s = block_sum<256>(v2, sh);
+    const double m = block_max<256>(v2, sh);
+    if (threadIdx.x == 0) {
+      P.part_ke[blockIdx.x] = s;
+      P.part_vmax[blockIdx.x] = m;
     }
   }
-  const double s = block_sum<256>(v2, sh);
-  const double m = block_max<256>(v2, sh);
+  if (!fin) return;
+  __shared__ int s_last;
+  __syncthreads();
   if (threadIdx.x == 0) {
-    P.part_ke[blockIdx.x] = s;
-    P.part_vmax[blockIdx.x] = m;
+    __threadfence();  // this block's partials before its count
+    s_last = atomicAdd(&P.st->fin_count, 1u) == gridDim.x - 1;
   }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  if (threadIdx.x == 0) P.st->fin_count = 0;
+  finalize_body<256>(P, stepping, energies, P.part_emb, n_emb, P.part_pair, n_pairp, nsb);
 }
 
 __global__ void k_clash_kick2(KP P, int kick) {
@@ -769,9 +788,9 @@ __device__ void finalize_body(const KP& P, int stepping, int energies, const dou
       const int i = i0 + u * NT;
       if (i < ne) ea[u] += pe[i];
       if (i < np) ep[u] += pp[i];
-      if (i < nk) {
-        ek[u] += P.part_ke[i];
-        em[u] = fmax(em[u], P.part_vmax[i]);
+      if (i < nk) {  // written by other blocks of a fused k_kick2: L2 loads
+        ek[u] += __ldcg(P.part_ke + i);
+        em[u] = fmax(em[u], __ldcg(P.part_vmax + i));
       }
     }
   }
@@ -781,8 +800,9 @@ __device__ void finalize_body(const KP& P, int stepping, int energies, const dou
       ep[0] += P.cl.e_pair[i];
     }
     if (stepping >= 0) {
-      ek[0] += P.cl.v2[i];
-      em[0] = fmax(em[0], P.cl.v2[i]);
+      const double v2 = __ldcg(P.cl.v2 + i);
+      ek[0] += v2;
+      em[0] = fmax(em[0], v2);
     }
   }
   double v[4] = {(ea[0] + ea[1]) + (ea[2] + ea[3]), (ep[0] + ep[1]) + (ep[2] + ep[3]),
@@ -884,10 +904,11 @@ void launch_clash_zero(const KP& P, int what, cudaStream_t s) {
   k_clash_zero<<<8, 256, 0, s>>>(P, what);
 }
 int kick_grid(const KP& P) { return eam_blocks(P); }
+// stepping > -2: the StepState finalize runs in the last k_kick2 block
 void launch_kick2(const KP& P, int kick, int stepping, int energies, cudaStream_t s) {
   const int nsb = kick_grid(P);
-  launch_pdl(k_kick2, nsb + kClashBlocks, 256, 0, s, P, kick, nsb);
-  if (stepping > -2) launch_finalize(P, stepping, energies, s);
+  launch_pdl(k_kick2, nsb + kClashBlocks, 256, 0, s, P, kick, nsb, stepping > -2 ? 1 : 0,
+             stepping, energies, P.n_pair_part, embed_grid(P));
 }
 void launch_finalize(const KP& P, int stepping, int energies, cudaStream_t s,
                      const P2PLinks* links) {
