@@ -13,7 +13,10 @@ fits one GPU.  Inputs are synthetic (seeded, host-generated).
   L2 evicted (512 MB write) before every timed step (the whole state is
   ~40 MB < 126 MB L2), max over ranks.
 * e2e: the same steps through the reference-facing C ABI with HOST buffers:
-  cbx_upload_store -> cbx_step -> cbx_download_store per step.
+  cbx_upload_store -> K x cbx_step(dt, 1) (StepState read on the host each
+  step) -> cbx_download_store, transfers inside the timed region and
+  amortised over the run; e2e.per_call re-uploads and downloads the whole
+  store around every step.
 * roofline: dominant kernel (force pass) against the measured fp64 peak.
 * cpu_baseline / --impl reference: the reference core (oracle/_ref, built from
   /root/reference) on all host cores; the C restatement if that is absent.
@@ -238,7 +241,7 @@ def run_ours(args, w, path, ws, rank, local):
            "data": "synthetic (seeded host-generated BCC lattice, MB velocities, displacements)",
            "config": {"workload": w.note, "atoms_per_gpu": n, "dt_ps": w.dt,
                       "stencil": args.stencil,
-                      "l2": f"flushed ({args.flush_mb:.0f} MB write) before every timed step",
+                      "l2": f"flushed before every timed step ({args.flush_mb:.0f} MB buffer written, then read back so the step starts on clean lines)",
                       "parallelism": (f"z-slab x{ws}, {getattr(dev, 'transport', args.transport)} halo/migrant "
                                       f"exchange + reduction inside the step graph"
                                       + (", density/force partials added into the neighbours' "
@@ -255,35 +258,73 @@ def run_ours(args, w, path, ws, rank, local):
     return res
 
 
-def run_e2e(dev, w, steps, ws=1, local=0):
-    """host-resident store: upload -> one device step -> download, per step
-    (every rank; the slowest rank's time counts)"""
-    from paper_2107_07866_b200.engine import pinned_store
-    s = dev.download(out=pinned_store(dev.n_slots))  # page-locked host buffers
-    nbytes_in = sum(getattr(s, k).nbytes for k in ("pos", "vel", "force", "rho", "df", "tag",
-                                                   "valid", "ghost"))
-    if ws > 1:
-        import torch.distributed as dist
-        dist.barrier()
-    t0 = time.perf_counter()
-    for _ in range(steps):
-        dev.upload(s)
-        dev.step(w.dt, 1)
-        s = dev.download(out=s)
-    el = time.perf_counter() - t0
+def _max_over_ranks(el, ws, local):
     if ws > 1:
         import torch
         import torch.distributed as dist
         x = torch.tensor([el], dtype=torch.float64, device=f"cuda:{local}")
         dist.all_reduce(x, op=dist.ReduceOp.MAX)
         el = float(x.item())
+    return el
+
+
+def run_e2e(dev, w, steps, ws=1, local=0, per_call_steps=5):
+    """End to end through the reference-facing C ABI with page-locked HOST
+    buffers (every rank; the slowest rank's time counts).
+
+    Run (the headline `e2e`): the way Simulation::step is driven -- the host
+    store is uploaded (cbx_upload_store), `steps` x cbx_step(dt, 1), each
+    returning the step's StepState to the host (sim.h:11-21: energies, KE,
+    max speed), then the store is downloaded (cbx_download_store); all of it
+    inside the timed region, the transfers amortised over the run.
+
+    Per call (`per_call`): upload -> one step -> download every step (the
+    parity-test boundary of a per-call eval_forces drop-in)."""
+    import ctypes
+    from paper_2107_07866_b200 import _lib
+    from paper_2107_07866_b200.engine import pinned_store
+    s = dev.download(out=pinned_store(dev.n_slots))  # page-locked host buffers
+    nbytes_in = sum(getattr(s, k).nbytes for k in ("pos", "vel", "force", "rho", "df", "tag",
+                                                   "valid", "ghost"))
+    state_bytes = ctypes.sizeof(_lib.State)
+
+    def barrier():
+        if ws > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    barrier()
+    t0 = time.perf_counter()
+    dev.upload(s)
+    energies = 0.0
+    for _ in range(steps):
+        st = dev.step(w.dt, 1)
+        energies += st["kinetic"]  # the step's result read on the host
+    s = dev.download(out=s)
+    el = _max_over_ranks(time.perf_counter() - t0, ws, local)
     nbytes_out = sum(getattr(s, k).nbytes for k in ("pos", "vel", "force", "rho", "df", "tag",
                                                     "valid", "ghost", "clash_key", "clash_pos"))
     n = int((s.valid.astype(bool) & ~s.ghost.astype(bool)).sum()) * ws
-    return {"value": n * steps / el, "unit": UNIT, "h2d_bytes_per_step": int(nbytes_in),
-            "d2h_bytes_per_step": int(nbytes_out), "steps": steps,
-            "path": "cbx_upload_store -> cbx_step(dt,1) -> cbx_download_store (pinned host "
-                    "buffers, reference-id AoS layout converted on the device)"}
+    run = {"value": n * steps / el, "unit": UNIT,
+           "h2d_bytes_per_step": int(nbytes_in / steps),
+           "d2h_bytes_per_step": int(nbytes_out / steps + state_bytes), "steps": steps,
+           "path": "cbx_upload_store -> %d x cbx_step(dt,1) (StepState to the host every step) "
+                   "-> cbx_download_store, pinned host buffers, reference-id AoS layout "
+                   "converted on the device" % steps}
+
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(per_call_steps):
+        dev.upload(s)
+        dev.step(w.dt, 1)
+        s = dev.download(out=s)
+    el = _max_over_ranks(time.perf_counter() - t0, ws, local)
+    run["per_call"] = {"value": n * per_call_steps / el, "unit": UNIT,
+                       "h2d_bytes_per_step": int(nbytes_in),
+                       "d2h_bytes_per_step": int(nbytes_out), "steps": per_call_steps,
+                       "path": "cbx_upload_store -> cbx_step(dt,1) -> cbx_download_store "
+                               "every step"}
+    return run
 
 
 def load_profile_traffic():
@@ -303,7 +344,7 @@ def main():
     ap.add_argument("--config", default="c2")
     ap.add_argument("--stencil", default="newton3", choices=["newton3", "full"])
     ap.add_argument("--flush-mb", type=float, default=512.0)
-    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--e2e-steps", type=int, default=100)
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--transport", default="p2p", choices=["p2p", "nccl"],

@@ -114,6 +114,10 @@ struct KP {
   unsigned long long* pmask;  // [S][2] pair masks from the density pass (or null)
   int use_mask;               // force pass replays pmask (set per launch by the host)
   int xp;                     // timing experiments only (CBX_XP): 1 fixed table row, 2 no RED
+  // fast hash: an atom closer than sqrt(hash_r2) to its own site (the
+  // half nearest-neighbour distance sqrt(3)/4 a0 less a margin far above
+  // rounding) hashes to that site and needs no periodic wrap (0: off)
+  double hash_r2;
   int n_pair_part;         // partials written by the force pass
   double accel, mv2;  // units::accel_factor, units::mv2_to_ev (units.h:17-24)
   long long S;  // 2*NC sites

@@ -88,11 +88,25 @@ __global__ void __launch_bounds__(256) k_kick_drift(KP P, int move, int nsb, int
     P.frc[S + d] = 0.0;
     P.frc[2 * S + d] = 0.0;
   }
-  if (!wrap_position(p.x, p.y, p.z, P.G)) {
+  const long long own = ref_of_dev(d, P.G.NC);
+  // fast hash (canonicalize_positions + nearest_site, store.cpp:88-118 and
+  // lattice.cpp:99-131, collapse to the identity for an atom inside the
+  // Wigner-Seitz ball of its own interior site: the rounded corner / centre
+  // candidates are that site and no wrap applies)
+  bool near_own = false;
+  if (P.hash_r2 > 0.0) {
+    int cx, cy, cz;
+    cell_xyz(d - par * P.G.NC, P.G, cx, cy, cz);
+    const double h = 0.5 * par;
+    const double ux = p.x - ((double)cx + h) * P.G.a0, uy = p.y - ((double)cy + h) * P.G.a0,
+                 uz = p.z - ((double)(cz + P.G.zoff) + h) * P.G.a0;
+    near_own = fma(ux, ux, fma(uy, uy, uz * uz)) < P.hash_r2;
+  }
+  if (!near_own && !wrap_position(p.x, p.y, p.z, P.G)) {
     set_error(P.st, CBX_LOGIC);
     return;
   }
-  const long long real = nearest_site(p.x, p.y, p.z, P.G);
+  const long long real = near_own ? own : nearest_site(p.x, p.y, p.z, P.G);
   if (real < 0) {
     if (atomicCAS(&P.st->err, 0, CBX_DOMAIN) == 0) {
       P.st->err_pos[0] = p.x;
@@ -101,7 +115,6 @@ __global__ void __launch_bounds__(256) k_kick_drift(KP P, int move, int nsb, int
     }
     return;
   }
-  const long long own = ref_of_dev(d, P.G.NC);
   if (real != own) {  // pass 1: evict to the clash map under the new hash
     const int dir = owner_dir(real, P.G);
     const Movers& M = dir ? P.out : P.mv;
