@@ -476,23 +476,29 @@ void seq_step(cbx_ctx* c) {
     return;
   }
   c->mask_valid = false;
+  // timing experiment only (CBX_SKIP bit mask, results invalid): leave a
+  // phase out of the step to measure its marginal cost inside the graph
+  static const int skip = [] {
+    const char* e = std::getenv("CBX_SKIP");
+    return e ? std::atoi(e) : 0;
+  }();
   ev_mark(c, 0);
   const bool zacc = c->mode != CBX_STENCIL_FULL;  // single box: no remote halo sites
   // kick, drift, hash pass 1 and the slot images in one launch; hash pass 2
   // and the clash images in one single-block launch (no k_ghost_fill)
-  launch_kick_drift(c->P, 1, c->stream, zacc ? 1 : 0, 1);
+  if (!(skip & 1)) launch_kick_drift(c->P, 1, c->stream, zacc ? 1 : 0, 1);
   c->acc_rho_zero = c->acc_frc_zero = zacc;
-  launch_rehash_images(c->P, c->stream);
+  if (!(skip & 2)) launch_rehash_images(c->P, c->stream);
   c->clash_rho_zero = true;
   c->launches += 2;
   ev_mark(c, 1);
-  seq_density(c);
+  if (!(skip & 4)) seq_density(c);
   ev_mark(c, 2);
-  seq_embed(c);
+  if (!(skip & 8)) seq_embed(c);
   ev_mark(c, 3);
-  seq_force(c);
+  if (!(skip & 16)) seq_force(c);
   ev_mark(c, 4);
-  launch_kick2(c->P, 1, 1, 1, c->stream);
+  if (!(skip & 32)) launch_kick2(c->P, 1, (skip & 64) ? -2 : 1, 1, c->stream);
   c->launches += 1;
   ev_mark(c, 5);
 }

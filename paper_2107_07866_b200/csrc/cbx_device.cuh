@@ -152,12 +152,37 @@ struct KP {
 #if defined(__CUDACC__)
 // thread -> (parity, interior cell): blocks of 8 warps cover 128 cells,
 // warps 0-3 the even sublattice, 4-7 the odd one (warp-uniform offset lists)
-__device__ __forceinline__ bool map_site(const KP& P, int& par, long long& d) {
+__device__ __forceinline__ bool map_site(const KP& P, int& par, long long& d, int vb = -1) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   par = warp >> 2;
-  const long long e = (long long)blockIdx.x * 128 + (warp & 3) * 32 + lane;
+  const long long e = (long long)(vb < 0 ? (int)blockIdx.x : vb) * 128 + (warp & 3) * 32 + lane;
   if (e >= P.G.NI) return false;
   d = par * P.G.NC + interior_cell(e, P.G);
+  return true;
+}
+
+// map_site that also returns the ghost-inclusive cell coordinates of the
+// site (one magic-number division pair, reused by the caller)
+__device__ __forceinline__ bool map_site_xyz(const KP& P, int vb, int& par, long long& d,
+                                             int& cx, int& cy, int& cz) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  par = warp >> 2;
+  const long long e = (long long)vb * 128 + (warp & 3) * 32 + lane;
+  if (e >= P.G.NI) return false;
+  const Geo& G = P.G;
+  if (e < (1ll << 31)) {
+    const unsigned u = (unsigned)e, r = magic_div(u, G.mbx, G.sbx);
+    const unsigned q = magic_div(r, G.mby, G.sby);
+    cx = (int)(u - r * (unsigned)G.bx) + G.g;
+    cy = (int)(r - q * (unsigned)G.by) + G.g;
+    cz = (int)q + G.g;
+  } else {
+    const long long r = e / G.bx;
+    cx = (int)(e - r * G.bx) + G.g;
+    cy = (int)(r % G.by) + G.g;
+    cz = (int)(r / G.by) + G.g;
+  }
+  d = par * G.NC + cell_of(cx, cy, cz, G);
   return true;
 }
 

@@ -61,7 +61,16 @@ struct Geo {
   int gtz;     // global ghost-inclusive z cells (gbz + 2g)
   double glz;  // global periodic z length (gbz * a0)
   int slab;    // 1 when z ghosts come from neighbour ranks
+  // n / bx and n / by for n < 2^31 as (n * m) >> sh (Granlund-Montgomery:
+  // sh = 31 + ceil(log2 d), m = ceil(2^sh / d)); device site mapping
+  unsigned long long mbx, mby;
+  int sbx, sby;
 };
+
+// exact floor(n / d) for 0 <= n < 2^31 from the constants of make_magic
+CBX_HD unsigned magic_div(unsigned n, unsigned long long m, int sh) {
+  return (unsigned)(((unsigned long long)n * m) >> sh);
+}
 
 CBX_HD long long ref_id(long long cell, int par) { return 2 * cell + par; }
 CBX_HD long long dev_of_ref(long long id, long long NC) { return (id & 1) * NC + (id >> 1); }

@@ -323,7 +323,7 @@ __device__ void clash_embed_body(const KP& P, int blk, int nblk) {
 
 // blocks [0, nsb): all slots, grid-stride, one energy partial per block;
 // blocks [nsb, grid): the clash records (fused k_clash_embed)
-__global__ void __launch_bounds__(256) k_embed(KP P, int nsb, int literal) {
+__global__ void __launch_bounds__(256, 6) k_embed(KP P, int nsb, int literal) {
   pdl_wait();
   pdl_trigger();
   if (P.rev_wait && !rev_wait(P, P.rev_wait)) return;  // the neighbours' density partials

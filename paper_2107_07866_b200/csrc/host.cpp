@@ -242,6 +242,14 @@ Geo make_geo(const cbx_box& b) {
   G.gtz = G.tz;
   G.glz = G.lz;
   G.slab = 0;
+  auto magic = [](unsigned d, unsigned long long& m, int& sh) {
+    int l = 0;
+    while ((1ull << l) < d) ++l;
+    sh = 31 + l;
+    m = ((1ull << sh) + d - 1) / d;
+  };
+  magic((unsigned)G.bx, G.mbx, G.sbx);
+  magic((unsigned)G.by, G.mby, G.sby);
   return G;
 }
 

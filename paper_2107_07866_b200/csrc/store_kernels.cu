@@ -44,16 +44,13 @@ __device__ void clash_kick_drift_body(const KP& P, int move, int blk, int nblk);
 // into them; replaces two full-array memsets)
 // images: also write the site's ghost images (the step path's k_ghost_fill)
 __device__ void ghost_images(const KP& P, long long d, const double4& p);
-__global__ void __launch_bounds__(256) k_kick_drift(KP P, int move, int nsb, int zero_acc,
-                                                    int images) {
-  if (P.st->err) return;
-  if (blockIdx.x >= nsb) {  // the clash records (fused k_clash_kick_drift)
-    clash_kick_drift_body(P, move, blockIdx.x - nsb, gridDim.x - nsb);
-    return;
-  }
-  int par;
+__device__ void ghost_images_at(const KP& P, int par, int cx, int cy, int cz, const double4& p);
+// one site per thread of virtual block vb (128 cells x 2 sublattices)
+__device__ __forceinline__ void kick_drift_site(const KP& P, int move, int zero_acc, int images,
+                                                int vb) {
+  int par, cx, cy, cz;
   long long d;
-  if (!map_site(P, par, d)) return;
+  if (!map_site_xyz(P, vb, par, d, cx, cy, cz)) return;
   // every load of the site issued before the first use (one round trip)
   const long long S = P.S;
   double4 p = P.pdf[d];
@@ -67,7 +64,7 @@ __global__ void __launch_bounds__(256) k_kick_drift(KP P, int move, int nsb, int
       P.frc[S + d] = 0.0;
       P.frc[2 * S + d] = 0.0;
     }
-    if (images) ghost_images(P, d, p);
+    if (images) ghost_images_at(P, par, cx, cy, cz, p);
     return;
   }
   if (move) {
@@ -95,8 +92,6 @@ __global__ void __launch_bounds__(256) k_kick_drift(KP P, int move, int nsb, int
   // candidates are that site and no wrap applies)
   bool near_own = false;
   if (P.hash_r2 > 0.0) {
-    int cx, cy, cz;
-    cell_xyz(d - par * P.G.NC, P.G, cx, cy, cz);
     const double h = 0.5 * par;
     const double ux = p.x - ((double)cx + h) * P.G.a0, uy = p.y - ((double)cy + h) * P.G.a0,
                  uz = p.z - ((double)(cz + P.G.zoff) + h) * P.G.a0;
@@ -137,12 +132,23 @@ __global__ void __launch_bounds__(256) k_kick_drift(KP P, int move, int nsb, int
     M.tag[m] = P.tag[d];
     P.pdf[d] = make_double4(kVacant, kVacant, kVacant, 0.0);
     P.uf[d] = make_float4(kVacantF, kVacantF, kVacantF, __int_as_float(-1));
-    if (images) ghost_images(P, d, make_double4(kVacant, kVacant, kVacant, 0.0));
+    if (images) ghost_images_at(P, par, cx, cy, cz, make_double4(kVacant, kVacant, kVacant, 0.0));
   } else {
     P.pdf[d] = p;
     P.uf[d] = make_float4((float)p.x, (float)p.y, (float)p.z, __int_as_float(-1));
-    if (images) ghost_images(P, d, p);
+    if (images) ghost_images_at(P, par, cx, cy, cz, p);
   }
+}
+
+// a single wave of blocks (resident on every SM) walks the virtual blocks
+__global__ void __launch_bounds__(256, 4) k_kick_drift(KP P, int move, int nsb, int zero_acc,
+                                                    int images, int nvb) {
+  if (P.st->err) return;
+  if (blockIdx.x >= nsb) {  // the clash records (fused k_clash_kick_drift)
+    clash_kick_drift_body(P, move, blockIdx.x - nsb, gridDim.x - nsb);
+    return;
+  }
+  for (int vb = blockIdx.x; vb < nvb; vb += nsb) kick_drift_site(P, move, zero_acc, images, vb);
 }
 
 __device__ void clash_kick_drift_body(const KP& P, int move, int blk, int nblk) {
@@ -449,9 +455,13 @@ __global__ void __launch_bounds__(1024) k_rehash(KP P) {
 __device__ void ghost_images(const KP& P, long long d, const double4& p) {
   const Geo& G = P.G;
   const int par = d >= G.NC;
-  const long long cell = d - par * G.NC;
   int cx, cy, cz;
-  cell_xyz(cell, G, cx, cy, cz);
+  cell_xyz(d - par * G.NC, G, cx, cy, cz);
+  ghost_images_at(P, par, cx, cy, cz, p);
+}
+__device__ void ghost_images_at(const KP& P, int par, int cx, int cy, int cz, const double4& p) {
+  const Geo& G = P.G;
+  const long long d = par * G.NC + cell_of(cx, cy, cz, G);
   int xl = 0, xh = 0, yl = 0, yh = 0, zl = 0, zh = 0;  // valid image shifts per axis
   for (int k = 1; k <= G.kmx; ++k) {
     if (cx - k * G.bx >= 0) xl = -k;
@@ -715,13 +725,13 @@ __device__ void clash_kick2_body(const KP& P, int kick, int blk, int nblk) {
 }
 
 template <int NT>
-__device__ void finalize_body(const KP& P, int stepping, int energies, const double* pe, int n_emb,
+__device__ __noinline__ void finalize_body(const KP& P, int stepping, int energies, const double* pe, int n_emb,
                               const double* pp, int n_pairp, int n_ke);
 
 // fin: the last block to finish runs finalize_body (the StepState sums) --
 // one launch less per step than a separate k_finalize
-__global__ void __launch_bounds__(256) k_kick2(KP P, int kick, int nsb, int fin, int stepping,
-                                               int energies, int n_pairp, int n_emb) {
+__global__ void __launch_bounds__(256, 6) k_kick2(KP P, int kick, int nsb, int fin, int stepping,
+                                                  int energies, int n_pairp, int n_emb, int nvb) {
   pdl_wait();
   pdl_trigger();
   if (P.rev_wait && !rev_wait(P, P.rev_wait)) return;  // the neighbours' force partials
@@ -729,10 +739,12 @@ __global__ void __launch_bounds__(256) k_kick2(KP P, int kick, int nsb, int fin,
   if (blockIdx.x >= nsb) {  // the clash records (fused k_clash_kick2)
     clash_kick2_body(P, kick, blockIdx.x - nsb, gridDim.x - nsb);
   } else {
+    double v2s = 0.0, v2m = 0.0;
+    for (int vb = blockIdx.x; vb < nvb; vb += nsb) {
     double v2 = 0.0;
     int par;
     long long d;
-    if (!P.st->err && !P.st->n_ovl && map_site(P, par, d)) {
+    if (!P.st->err && !P.st->n_ovl && map_site(P, par, d, vb)) {
       // every load of the site issued before the first use (one memory round
       // trip per thread; a vacant slot's velocity/force reads are discarded)
       const long long S = P.S;
@@ -753,8 +765,11 @@ __global__ void __launch_bounds__(256) k_kick2(KP P, int kick, int nsb, int fin,
         v2 = exact_r2(vx, vy, vz);
       }
     }
-    const double s = block_sum<256>(v2, sh);
-    const double m = block_max<256>(v2, sh);
+    v2s += v2;
+    v2m = fmax(v2m, v2);
+    }
+    const double s = block_sum<256>(v2s, sh);
+    const double m = block_max<256>(v2m, sh);
     if (threadIdx.x == 0) {
       P.part_ke[blockIdx.x] = s;
       P.part_vmax[blockIdx.x] = m;
@@ -771,7 +786,9 @@ __global__ void __launch_bounds__(256) k_kick2(KP P, int kick, int nsb, int fin,
   if (!s_last) return;
   __threadfence();
   if (threadIdx.x == 0) P.st->fin_count = 0;
-  finalize_body<256>(P, stepping, energies, P.part_emb, n_emb, P.part_pair, n_pairp, nsb);
+  // through the device copy of P: a noinline callee taking the parameter
+  // struct by reference would copy it to the stack of every thread
+  finalize_body<256>(*P.dself, stepping, energies, P.part_emb, n_emb, P.part_pair, n_pairp, nsb);
 }
 
 __global__ void k_clash_kick2(KP P, int kick) {
@@ -783,7 +800,7 @@ __global__ void k_clash_kick2(KP P, int kick) {
 // (fixed per-thread order, four independent accumulators for load
 // parallelism, then a fixed block tree)
 template <int NT>
-__device__ void finalize_body(const KP& P, int stepping, int energies, const double* pe, int n_emb,
+__device__ __noinline__ void finalize_body(const KP& P, int stepping, int energies, const double* pe, int n_emb,
                               const double* pp, int n_pairp, int n_ke) {
   __shared__ double sh[4][32];
   DevStatus* st = P.st;
@@ -899,9 +916,24 @@ __global__ void __launch_bounds__(256) k_count_defects(KP P, unsigned long long*
 
 // -------------------------------------------------------------- launchers
 constexpr int kClashBlocks = 8;  // blocks of 256 threads for clash-record sweeps
+// per-site sweeps: one resident wave (blocks per SM x SMs) over eam_blocks
+// virtual blocks
+static int site_wave(const KP& P, int per_sm) {
+  static int sms = [] {
+    int n = 148, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n;
+  }();
+  static const int wave = [] {  // CBX_SITE_WAVE=0: one block per virtual block
+    const char* e = std::getenv("CBX_SITE_WAVE");
+    return e ? std::atoi(e) : 1;
+  }();
+  return wave ? std::max(1, std::min(eam_blocks(P), per_sm * sms)) : eam_blocks(P);
+}
 void launch_kick_drift(const KP& P, int move, cudaStream_t s, int zero_acc, int images) {
-  const int nsb = eam_blocks(P);
-  k_kick_drift<<<nsb + kClashBlocks, 256, 0, s>>>(P, move, nsb, zero_acc, images);
+  const int nsb = site_wave(P, 4);
+  k_kick_drift<<<nsb + kClashBlocks, 256, 0, s>>>(P, move, nsb, zero_acc, images, eam_blocks(P));
 }
 void launch_rehash_images(const KP& P, cudaStream_t s) {
   launch_pdl(k_rehash_images, 1, 1024, 0, s, P);
@@ -916,12 +948,12 @@ void launch_clash_images(const KP& P, cudaStream_t s, int zero_rho) {
 void launch_clash_zero(const KP& P, int what, cudaStream_t s) {
   k_clash_zero<<<8, 256, 0, s>>>(P, what);
 }
-int kick_grid(const KP& P) { return eam_blocks(P); }
+int kick_grid(const KP& P) { return site_wave(P, 6); }
 // stepping > -2: the StepState finalize runs in the last k_kick2 block
 void launch_kick2(const KP& P, int kick, int stepping, int energies, cudaStream_t s) {
   const int nsb = kick_grid(P);
   launch_pdl(k_kick2, nsb + kClashBlocks, 256, 0, s, P, kick, nsb, stepping > -2 ? 1 : 0,
-             stepping, energies, P.n_pair_part, embed_grid(P));
+             stepping, energies, P.n_pair_part, embed_grid(P), eam_blocks(P));
 }
 void launch_finalize(const KP& P, int stepping, int energies, cudaStream_t s,
                      const P2PLinks* links) {
