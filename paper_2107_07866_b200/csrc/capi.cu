@@ -32,6 +32,10 @@ struct cbx_ctx {
   cudaGraphExec_t step_graph = nullptr;
   cudaGraphExec_t timed_graph = nullptr;
   void* flush_buf = nullptr;
+  // deferred StepState finalize (fixed dt, single box): graphs captured with
+  // it; a pending finalize may exist on the device; its pair partial count
+  bool graph_defer = false, fin_maybe = false;
+  int fin_npp = 0;
   size_t flush_bytes = 0;
   bool use_graph = true;
   bool timing = false;
@@ -191,6 +195,11 @@ Tab upload_tab(cbx_ctx* c, const Spline& s) {
 }
 
 void sync_status(cbx_ctx* c) {
+  if (c->fin_maybe) {  // the last step's StepState sums before the host reads them
+    launch_finalize_pending(c->P, c->fin_npp, c->stream);
+    c->launches += 1;
+    c->fin_maybe = false;
+  }
   cuda_check(cudaMemcpyAsync(&c->hst, c->P.st, sizeof(DevStatus), cudaMemcpyDeviceToHost,
                              c->stream),
              "status readback");
@@ -470,6 +479,16 @@ void seq_slab_eval(cbx_ctx* c) {
 }
 
 // one velocity-Verlet step, sim.cpp:248-273
+// defer the StepState finalize of a step into the next step's first kernel
+// (fixed dt only: with adaptive dt the next kick needs the reduced max speed)
+bool want_defer(const cbx_ctx* c) {
+  static const bool on = [] {
+    const char* e = std::getenv("CBX_DEFER_FIN");
+    return e ? std::atoi(e) != 0 : true;
+  }();
+  return on && !has_transport(c) && !c->hst.adaptive;
+}
+
 void seq_step(cbx_ctx* c) {
   if (has_transport(c)) {
     seq_slab_step(c);
@@ -486,7 +505,13 @@ void seq_step(cbx_ctx* c) {
   const bool zacc = c->mode != CBX_STENCIL_FULL;  // single box: no remote halo sites
   // kick, drift, hash pass 1 and the slot images in one launch; hash pass 2
   // and the clash images in one single-block launch (no k_ghost_fill)
-  if (!(skip & 1)) launch_kick_drift(c->P, 1, c->stream, zacc ? 1 : 0, 1);
+  KP qf = c->P;
+  qf.use_mask = 1;  // the force pass below replays the density pass's mask
+  const int npp = force_partials(qf, c->mode);
+  const bool defer = want_defer(c);
+  c->graph_defer = defer;
+  c->fin_npp = npp;
+  if (!(skip & 1)) launch_kick_drift(c->P, 1, c->stream, zacc ? 1 : 0, 1, npp);
   c->acc_rho_zero = c->acc_frc_zero = zacc;
   if (!(skip & 2)) launch_rehash_images(c->P, c->stream);
   c->clash_rho_zero = true;
@@ -498,7 +523,8 @@ void seq_step(cbx_ctx* c) {
   ev_mark(c, 3);
   if (!(skip & 16)) seq_force(c);
   ev_mark(c, 4);
-  if (!(skip & 32)) launch_kick2(c->P, 1, (skip & 64) ? -2 : 1, 1, c->stream);
+  if (!(skip & 32)) launch_kick2(c->P, 1, (skip & 64) ? -2 : 1, 1, c->stream, defer ? 2 : 1, npp);
+  if (defer && !g_capturing) c->fin_maybe = true;
   c->launches += 1;
   ev_mark(c, 5);
 }
@@ -1528,11 +1554,13 @@ CBX_API cbx_status cbx_step(cbx_ctx* c, double dt, long nsteps, cbx_state* out) 
       c->hst.dt_next = cbx_adaptive_dt(c->hst.max_speed, c->hst.dt_max, c->hst.max_disp);
     }
     write_status(c);
+    if (c->step_graph && c->graph_defer != want_defer(c)) drop_graph(c);
     if (c->use_graph && !c->timing) build_graph(c);
     for (long i = 0; i < nsteps; ++i) {
       if (c->use_graph && !c->timing) {
         cuda_check(cudaGraphLaunch(c->step_graph, c->stream), "graph launch");
         c->launches += c->graph_launches;
+        if (c->graph_defer) c->fin_maybe = true;
       } else {
         seq_step(c);
         accumulate_timing(c, true);
@@ -2055,6 +2083,8 @@ CBX_API cbx_status cbx_bench_steps(cbx_ctx* c, double dt, long nsteps, double fl
     c->hst.adaptive = 0;
     write_status(c);
     const bool phases = c->bench_phases;
+    if ((c->step_graph || c->timed_graph || c->timed_lite) && c->graph_defer != want_defer(c))
+      drop_graph(c);
     cudaGraphExec_t* gp = phases ? &c->timed_graph : &c->timed_lite;
     if (!*gp) {
       c->timing_lite = !phases;
@@ -2082,6 +2112,7 @@ CBX_API cbx_status cbx_bench_steps(cbx_ctx* c, double dt, long nsteps, double fl
       cuda_check(cudaGraphLaunch(*gp, c->stream), "graph launch");
       cudaEventRecord(c->ev_outer[1], c->stream);
       c->launches += c->graph_launches;
+      if (c->graph_defer) c->fin_maybe = true;
       cuda_check(cudaEventSynchronize(c->ev_outer[1]), "event sync");
       float ms;
       cudaEventElapsedTime(&ms, c->ev_outer[0], c->ev_outer[1]);

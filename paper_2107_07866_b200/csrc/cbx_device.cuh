@@ -73,6 +73,10 @@ struct DevStatus {
   double dt_max, max_disp;
   unsigned long long cnt_cand, cnt_pair;
   unsigned fin_count;  // blocks of k_kick2 done (the last one runs the finalize)
+  // deferred finalize: the StepState sums of the last k_kick2 run later, in
+  // an otherwise idle block of the next step's k_kick_drift (fixed dt) or
+  // before the host reads the status (k_finalize_pending)
+  int fin_pending, fin_stepping, fin_energies;
 };
 
 struct P2PLinks;
@@ -299,7 +303,8 @@ bool launch_force(const KP& P, int mode, cudaStream_t s);
 void launch_clash_force(const KP& P, cudaStream_t s);
 // zero_acc: clear the interior sites' rho / force accumulators as well;
 // images: write each site's ghost images too (the step path, no ghost fill)
-void launch_kick_drift(const KP& P, int move, cudaStream_t s, int zero_acc = 0, int images = 0);
+void launch_kick_drift(const KP& P, int move, cudaStream_t s, int zero_acc = 0, int images = 0,
+                       int n_pairp = 0);
 // update_hash pass 2 + ghost clash images in one single-block launch
 void launch_rehash_images(const KP& P, cudaStream_t s);
 void launch_clash_zero(const KP& P, int what, cudaStream_t s);
@@ -308,7 +313,12 @@ void launch_ghost_fill(const KP& P, cudaStream_t s);
 // zero_rho: also zero the records' density accumulators (density follows)
 void launch_clash_images(const KP& P, cudaStream_t s, int zero_rho = 0);
 // second half kick; stepping > -2 also runs the finalize (last block)
-void launch_kick2(const KP& P, int kick, int stepping, int energies, cudaStream_t s);
+// fin: 1 the StepState finalize in the last block, 2 deferred (fin_pending);
+// n_pairp: pair-energy partials written by the preceding force pass
+void launch_kick2(const KP& P, int kick, int stepping, int energies, cudaStream_t s, int fin = 1,
+                  int n_pairp = -1);
+void launch_finalize_pending(const KP& P, int n_pairp, cudaStream_t s);
+int force_partials(const KP& P, int mode);  // partials the force launch writes
 
 void launch_count_defects(const KP& P, unsigned long long* out, cudaStream_t s);
 void upload_offsets(const int* half_dev[2], const int half_n[2], const int* full_dev[2],

@@ -521,6 +521,14 @@ int pair_partials(const KP& P, int mode) {
   for (int m = 0; m < 2; ++m) n = std::max(n, fast_grid(P, true, m));
   return std::min(n, P.n_part);
 }
+int force_partials(const KP& P, int mode) {
+  if (mode == 2) return eam_blocks(P);
+  if (!P.use_mask) return fast_grid(P, true, mode);
+  int sms = 148, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return std::max(1, std::min(sms, unit_count(P.G)));  // launch_force_lean
+}
 void launch_embed(const KP& P, cudaStream_t s, bool literal) {
   const int nsb = embed_grid(P);
   launch_pdl(k_embed, nsb + 16, 256, 0, s, P, nsb, literal ? 1 : 0);

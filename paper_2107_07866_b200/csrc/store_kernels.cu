@@ -141,8 +141,27 @@ __device__ __forceinline__ void kick_drift_site(const KP& P, int move, int zero_
 }
 
 // a single wave of blocks (resident on every SM) walks the virtual blocks
+template <int NT>
+__device__ void finalize_body(const KP& P, int stepping, int energies, const double* pe, int n_emb,
+                              const double* pp, int n_pairp, int n_ke);
+// the deferred StepState finalize of the previous k_kick2, if one is pending
+template <int NT>
+__device__ void finalize_pending(const KP& P, int n_emb, int n_pairp, int n_ke) {
+  DevStatus* st = P.st;
+  if (!st->fin_pending) return;
+  finalize_body<NT>(*P.dself, st->fin_stepping, st->fin_energies, P.part_emb, n_emb, P.part_pair,
+                    n_pairp, n_ke);
+  __syncthreads();
+  if (threadIdx.x == 0) st->fin_pending = 0;
+}
+
 __global__ void __launch_bounds__(256, 4) k_kick_drift(KP P, int move, int nsb, int zero_acc,
-                                                    int images, int nvb) {
+                                                    int images, int nvb, int n_pairp,
+                                                    int n_emb, int n_ke) {
+  if (blockIdx.x == nsb) {  // an idle clash block: the previous step's StepState
+    // sums (the step's dt is fixed when they are deferred)
+    finalize_pending<256>(P, n_emb, n_pairp, n_ke);
+  }
   if (P.st->err) return;
   if (blockIdx.x >= nsb) {  // the clash records (fused k_clash_kick_drift)
     clash_kick_drift_body(P, move, blockIdx.x - nsb, gridDim.x - nsb);
@@ -775,6 +794,14 @@ __global__ void __launch_bounds__(256, 6) k_kick2(KP P, int kick, int nsb, int f
       P.part_vmax[blockIdx.x] = m;
     }
   }
+  if (fin == 2) {  // deferred: the next step's k_kick_drift (or the host) sums
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      P.st->fin_stepping = stepping;
+      P.st->fin_energies = energies;
+      P.st->fin_pending = 1;
+    }
+    return;
+  }
   if (!fin) return;
   __shared__ int s_last;
   __syncthreads();
@@ -931,9 +958,12 @@ static int site_wave(const KP& P, int per_sm) {
   }();
   return wave ? std::max(1, std::min(eam_blocks(P), per_sm * sms)) : eam_blocks(P);
 }
-void launch_kick_drift(const KP& P, int move, cudaStream_t s, int zero_acc, int images) {
+void launch_kick_drift(const KP& P, int move, cudaStream_t s, int zero_acc, int images,
+                       int n_pairp) {
   const int nsb = site_wave(P, 4);
-  k_kick_drift<<<nsb + kClashBlocks, 256, 0, s>>>(P, move, nsb, zero_acc, images, eam_blocks(P));
+  k_kick_drift<<<nsb + kClashBlocks, 256, 0, s>>>(P, move, nsb, zero_acc, images, eam_blocks(P),
+                                                   n_pairp > 0 ? n_pairp : P.n_pair_part,
+                                                   embed_grid(P), kick_grid(P));
 }
 void launch_rehash_images(const KP& P, cudaStream_t s) {
   launch_pdl(k_rehash_images, 1, 1024, 0, s, P);
@@ -950,10 +980,19 @@ void launch_clash_zero(const KP& P, int what, cudaStream_t s) {
 }
 int kick_grid(const KP& P) { return site_wave(P, 6); }
 // stepping > -2: the StepState finalize runs in the last k_kick2 block
-void launch_kick2(const KP& P, int kick, int stepping, int energies, cudaStream_t s) {
+void launch_kick2(const KP& P, int kick, int stepping, int energies, cudaStream_t s, int fin,
+                  int n_pairp) {
   const int nsb = kick_grid(P);
-  launch_pdl(k_kick2, nsb + kClashBlocks, 256, 0, s, P, kick, nsb, stepping > -2 ? 1 : 0,
-             stepping, energies, P.n_pair_part, embed_grid(P), eam_blocks(P));
+  launch_pdl(k_kick2, nsb + kClashBlocks, 256, 0, s, P, kick, nsb, stepping > -2 ? fin : 0,
+             stepping, energies, n_pairp > 0 ? n_pairp : P.n_pair_part, embed_grid(P),
+             eam_blocks(P));
+}
+__global__ void __launch_bounds__(1024) k_finalize_pending(KP P, int n_emb, int n_pairp, int n_ke) {
+  finalize_pending<1024>(P, n_emb, n_pairp, n_ke);
+}
+void launch_finalize_pending(const KP& P, int n_pairp, cudaStream_t s) {
+  k_finalize_pending<<<1, 1024, 0, s>>>(P, embed_grid(P), n_pairp > 0 ? n_pairp : P.n_pair_part,
+                                        kick_grid(P));
 }
 void launch_finalize(const KP& P, int stepping, int energies, cudaStream_t s,
                      const P2PLinks* links) {
