@@ -480,6 +480,11 @@ __device__ void ghost_images(const KP& P, long long d, const double4& p) {
 }
 __device__ void ghost_images_at(const KP& P, int par, int cx, int cy, int cz, const double4& p) {
   const Geo& G = P.G;
+  // one image shift per axis at most (every box at least as wide as the
+  // ghost shell): a site has images only within 2g cells of a face
+  if (G.kmx == 1 && G.kmy == 1 && G.kmz <= 1 && cx < G.bx && cx >= G.tx - G.bx && cy < G.by &&
+      cy >= G.ty - G.by && (G.kmz == 0 || (cz < G.bz && cz >= G.tz - G.bz)))
+    return;
   const long long d = par * G.NC + cell_of(cx, cy, cz, G);
   int xl = 0, xh = 0, yl = 0, yh = 0, zl = 0, zh = 0;  // valid image shifts per axis
   for (int k = 1; k <= G.kmx; ++k) {

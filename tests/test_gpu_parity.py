@@ -317,6 +317,30 @@ def test_adaptive_dt_matches(cuda, tables):
     assert abs(st["t"] - ref.state()["t"]) <= 1e-15
 
 
+def test_deferred_finalize_state(cuda, tables):
+    """With a fixed dt the StepState sums of a step run inside the next
+    step's first kernel (or before the host reads the status): one call of
+    n steps and n calls of one step give identical StepStates, equal to the
+    oracle's, and a measure right after a multi-step call sees the final
+    state"""
+    from oracle import oracle
+    ref = oracle.Sim(tables["baseline"], box=(7, 6, 5), temperature=600.0, seed=17)
+    a = device_for(ref, tables["baseline"])
+    b = device_for(ref, tables["baseline"])
+    a.set_state(ref.state())
+    b.set_state(ref.state())
+    sa = a.step(1e-3, 6)
+    for _ in range(6):
+        sb = b.step(1e-3, 1)
+    ref.step(1e-3, 6)
+    r = ref.state()
+    # (partner contributions are atomic adds: sums agree to rounding, not bitwise)
+    assert sa["step"] == sb["step"] == r["step"] and sa["t"] == sb["t"] == r["t"]
+    for k in ("kinetic", "pair", "embedding", "max_speed"):
+        assert close(sa[k], sb[k], 1e-12) and close(sa[k], r[k]), k
+    assert a.state() == sa
+
+
 def test_simulation_facade(cuda, tables):
     """Simulation (sim.h) over the device equals the oracle's constructor"""
     from oracle import oracle
