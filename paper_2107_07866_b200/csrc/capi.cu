@@ -917,6 +917,33 @@ void setup_fast(cbx_ctx* c) {
       P.ffc = dfc;
     }
   }
+  // compressed density records for the density pass: the cubic and quadratic
+  // coefficients (~1e-9 and ~1e-6 of rho at the BASELINE spacing) in fp32
+  // move a pair's rho by < 1e-12 of the table's scale (a per-atom rho-bar by
+  // a few 1e-12 against the 1e-10 tolerance); used only when that holds
+  P.fdc = nullptr;
+  {
+    double md = 0, ea = 0;
+    for (int i = 0; i <= n; ++i) {
+      const double* r = &fd[4 * i];
+      md = std::max(md, std::max(std::fabs(r[2]), std::fabs(r[3])));
+      ea = std::max(ea, std::fabs(r[0] - (double)(float)r[0]) + std::fabs(r[1] - (double)(float)r[1]));
+    }
+    const char* nc = std::getenv("CBX_NO_FP32_DENSITY");
+    if (ea <= 1e-12 * md && !(nc && std::atoi(nc))) {
+      std::vector<double> dc(3 * (n + 1));
+      for (int i = 0; i <= n; ++i) {
+        const double* r = &fd[4 * i];
+        dc[2 * i] = r[3];
+        dc[2 * i + 1] = r[2];
+        const float ab[2] = {(float)r[0], (float)r[1]};
+        std::memcpy(&dc[2 * (n + 1) + i], ab, 8);
+      }
+      double* ddc = c->alloc<double>(dc.size());
+      cuda_check(cudaMemcpy(ddc, dc.data(), dc.size() * 8, cudaMemcpyHostToDevice), "fast table");
+      P.fdc = ddc;
+    }
+  }
   // embedding F(rho), same normalisation (its own grid)
   {
     const Spline& em = c->pot.embed;

@@ -110,6 +110,9 @@ struct KP {
   // [zB zC zD qB qC (zA,qA as two floats)]; null when a table's cubic terms
   // are too large for the fp32 bound (setup_fast)
   const double* ffc;
+  // compressed density records: [D C] (16 B) then, after the last record,
+  // [A B as fp32] (8 B) per record; null when the fp32 rounding bound fails
+  const double* fdc;
   FastTab fe;      // embedding F(rho): 4 doubles/segment (A B C D), padded
   float band_hi, band_lo;  // fp32 r^2 filter: reject above hi, exact test in [lo, hi]
   double guard_r2;         // below: overlap / short-range guard path

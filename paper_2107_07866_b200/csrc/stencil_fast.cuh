@@ -140,6 +140,11 @@ __device__ __forceinline__ double2 lds2(unsigned a) {
   asm("ld.shared.v2.f64 {%0,%1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a));
   return v;
 }
+__device__ __forceinline__ float2 lds_f2(unsigned a) {
+  float2 v;
+  asm("ld.shared.v2.f32 {%0,%1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(a));
+  return v;
+}
 __device__ __forceinline__ int lds_i(unsigned a) {
   int v;
   asm("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(a));
@@ -177,10 +182,11 @@ __device__ __forceinline__ double skin_density(const KP& P, KP* Pp, int par, int
 // 16-byte slot 2 i + (c ^ ((i >> 2) & 1)) (8 distinct bank quads for random i)
 __device__ __forceinline__ int smem_slot32(int i, int c) { return 2 * i + (c ^ ((i >> 2) & 1)); }
 
-template <bool FULL, int B, bool SMEM = false, bool REV = false>
+template <bool FULL, int B, bool SMEM = false, bool REV = false, bool CMPD = false>
 __device__ __forceinline__ void density_site(const KP& P, KP* Pp, int par, int d, bool live,
                                              unsigned tb = 0, int seg_lo = 0,
-                                             bool rev_here = true, bool deep = false) {
+                                             bool rev_here = true, bool deep = false,
+                                             unsigned tb8 = 0) {
   const double4* __restrict__ pdf = P.pdf;
   const int* __restrict__ tgt = P.tgt;
   double ax = kVacant, ay = 0, az = 0, aw = 0;
@@ -239,7 +245,15 @@ __device__ __forceinline__ void density_site(const KP& P, KP* Pp, int par, int d
     for (int b = 0; b < B; ++b)
       if (in[b]) {
         const int li = seg[b] - seg_lo;
-        if (SMEM) {
+        if (SMEM && CMPD) {  // [D C] and the fp32 pair [A B]
+          const int lc = max(li, 0);
+          const double2 dc = lds2(tb + 16 * lc);
+          const float2 ab = lds_f2(tb8 + 8 * lc);
+          tA[b] = (double)ab.x;
+          tB[b] = (double)ab.y;
+          tC[b] = dc.y;
+          tD[b] = dc.x;
+        } else if (SMEM) {
           const int lc = max(li, 0);
           const double2 c0 = lds2(tb + 16 * smem_slot32(lc, 0)), c1 = lds2(tb + 16 * smem_slot32(lc, 1));
           tA[b] = c0.x;
@@ -694,7 +708,7 @@ __device__ __forceinline__ int next_unit(int* s_ctr, int group, int nsb, int nu,
 // records): NT threads = NT/128 groups of 4 warps, one CTA per SM; B = 1
 // (one candidate per iteration) keeps the thread at 64 registers
 constexpr int kDensTabRecords = 3300;  // x 32 B = 105,600 B
-template <bool FULL, int B, int NT, bool REV = false>
+template <bool FULL, int B, int NT, bool REV = false, bool CMPD = false>
 __global__ void __launch_bounds__(NT, 1) k_density_smem(KP P, int nsb) {
   if (blockIdx.x >= nsb) {
     pdl_wait();
@@ -712,7 +726,19 @@ __global__ void __launch_bounds__(NT, 1) k_density_smem(KP P, int nsb) {
   const int nrec = nseg + 1 - seg_lo;
   const double2* src = reinterpret_cast<const double2*>(P.fd.rec + 4 * (size_t)seg_lo);
   // the constant table is staged while the predecessor drains (PDL)
-  for (int q = threadIdx.x; q < 2 * nrec; q += blockDim.x) T[smem_slot32(q >> 1, q & 1)] = __ldg(src + q);
+  // 24-byte records: [D C] 16-byte slots, then the fp32 [A B] pairs
+  double2* T8 = T + kDensTabRecords;  // byte offset 16 x kDensTabRecords
+  if (CMPD) {
+    const int N1 = nseg + 1;
+    const double2* dc = reinterpret_cast<const double2*>(P.fdc) + seg_lo;
+    const double* ab = P.fdc + 2 * (size_t)N1 + seg_lo;
+    for (int q = threadIdx.x; q < nrec; q += blockDim.x) {
+      T[q] = __ldg(dc + q);
+      reinterpret_cast<double*>(T8)[q] = __ldg(ab + q);
+    }
+  } else {
+    for (int q = threadIdx.x; q < 2 * nrec; q += blockDim.x) T[smem_slot32(q >> 1, q & 1)] = __ldg(src + q);
+  }
   __syncthreads();
   pdl_wait();
   pdl_trigger();
@@ -728,8 +754,9 @@ __global__ void __launch_bounds__(NT, 1) k_density_smem(KP P, int nsb) {
     const bool live = unit_cell(G, u, lane, w, c);
     const bool deep = live && unit_deep(G, u, lane, w, FULL);
     for (int par = 0; par < 2; ++par)
-      density_site<FULL, B, true, REV>(P, P.dself, par, live ? (int)(par * G.NC + c) : 0, live,
-                                       smem_addr(T), seg_lo, near_halo(G, u, w), deep);
+      density_site<FULL, B, true, REV, CMPD>(P, P.dself, par, live ? (int)(par * G.NC + c) : 0,
+                                             live, smem_addr(T), seg_lo, near_halo(G, u, w),
+                                             deep, smem_addr(T8));
   }
 }
 
@@ -865,16 +892,28 @@ bool launch_density_fast(const KP& P, int mode, int grid, cudaStream_t s) {
     return e ? atoi(e) : 1;
   }();
   if (dsm) {
-    const size_t bytes = (size_t)kDensTabRecords * 32;
+    const bool cmp = P.fdc != nullptr;  // 24-byte records (fp32 cubic/quadratic terms)
+    const size_t bytes = (size_t)kDensTabRecords * (cmp ? 24 : 32);
     static bool attr = false;
     if (!attr) {
       for (const void* k : {(const void*)k_density_smem<false, 1, 1024>,
                             (const void*)k_density_smem<true, 1, 1024>,
-                            (const void*)k_density_smem<false, 1, 1024, true>})
-        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+                            (const void*)k_density_smem<false, 1, 1024, true>,
+                            (const void*)k_density_smem<false, 1, 1024, false, true>,
+                            (const void*)k_density_smem<true, 1, 1024, false, true>,
+                            (const void*)k_density_smem<false, 1, 1024, true, true>})
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)((size_t)kDensTabRecords * 32));
       attr = true;
     }
     const int g = max(1, min(sm_count(), unit_count(P.G)));
+    if (cmp) {
+      if (mode) launch_pdl(k_density_smem<true, 1, 1024, false, true>, g, 1024, bytes, s, P, g);
+      else if (P.rev.on)
+        launch_pdl(k_density_smem<false, 1, 1024, true, true>, g + 4, 1024, bytes, s, P, g);
+      else launch_pdl(k_density_smem<false, 1, 1024, false, true>, g + 4, 1024, bytes, s, P, g);
+      return !mode;
+    }
     if (mode) launch_pdl(k_density_smem<true, 1, 1024>, g, 1024, bytes, s, P, g);
     else if (P.rev.on) launch_pdl(k_density_smem<false, 1, 1024, true>, g + 4, 1024, bytes, s, P, g);
     else launch_pdl(k_density_smem<false, 1, 1024>, g + 4, 1024, bytes, s, P, g);
