@@ -35,6 +35,10 @@ struct cbx_ctx {
   // deferred StepState finalize (fixed dt, single box): graphs captured with
   // it; a pending finalize may exist on the device; its pair partial count
   bool graph_defer = false, fin_maybe = false;
+  // the host copy of the status equals the device's and nothing ran since
+  // (set by cbx_step on success, cleared on entry to every C-ABI call):
+  // a following cbx_step skips its opening status round trip
+  bool st_fresh = false, st_was_fresh = false;
   int fin_npp = 0;
   size_t flush_bytes = 0;
   bool use_graph = true;
@@ -139,7 +143,11 @@ void bind_constants(cbx_ctx* c) {
 template <class F>
 cbx_status guarded(cbx_ctx* c, F&& f) {
   try {
-    if (c) bind_constants(c);
+    if (c) {
+      c->st_was_fresh = c->st_fresh;
+      c->st_fresh = false;
+      bind_constants(c);
+    }
     f();
     if (c) c->err.clear();
     return CBX_OK;
@@ -1572,15 +1580,19 @@ CBX_API cbx_status cbx_step(cbx_ctx* c, double dt, long nsteps, cbx_state* out) 
     check_cutoff(c);
     if (nsteps < 0) raise(CBX_INVALID_ARGUMENT, "nsteps must be >= 0");
     require_box_or_comm(c, "cbx_step");
-    sync_status(c);
+    const bool fresh = c->st_was_fresh;
+    if (!fresh) sync_status(c);
     if (dt > 0.0) {
-      c->hst.dt_next = dt;
-      c->hst.adaptive = 0;
+      if (!fresh || c->hst.adaptive || c->hst.dt_next != dt) {
+        c->hst.dt_next = dt;
+        c->hst.adaptive = 0;
+        write_status(c);
+      }
     } else {
       c->hst.adaptive = 1;
       c->hst.dt_next = cbx_adaptive_dt(c->hst.max_speed, c->hst.dt_max, c->hst.max_disp);
+      write_status(c);
     }
-    write_status(c);
     if (c->step_graph && c->graph_defer != want_defer(c)) drop_graph(c);
     if (c->use_graph && !c->timing) build_graph(c);
     for (long i = 0; i < nsteps; ++i) {
@@ -1595,6 +1607,7 @@ CBX_API cbx_status cbx_step(cbx_ctx* c, double dt, long nsteps, cbx_state* out) 
     }
     sync_status(c);
     raise_device_error(c, true);
+    c->st_fresh = true;
     if (out) {
       out->step = (long)c->hst.step;
       out->t = c->hst.t;
