@@ -939,7 +939,7 @@ void setup_fast(cbx_ctx* c) {
     }
     const char* nc = std::getenv("CBX_NO_FP32_DENSITY");
     if (ea <= 1e-12 * md && !(nc && std::atoi(nc))) {
-      std::vector<double> dc(3 * (n + 1));
+      std::vector<double> dc(3 * (n + 1) + 2);  // + 16 bytes: the bulk copy rounds up
       for (int i = 0; i <= n; ++i) {
         const double* r = &fd[4 * i];
         dc[2 * i] = r[3];

@@ -151,6 +151,41 @@ __device__ __forceinline__ int lds_i(unsigned a) {
   return v;
 }
 
+// ---- bulk (TMA engine) staging of a constant table into shared memory:
+// one thread arms an mbarrier with the byte count and issues 1-D bulk
+// copies; every thread waits on the barrier's phase 0.  Spares the per-thread
+// load/store round trips of a copy loop at kernel start.
+__device__ __forceinline__ void mbar_init(unsigned mbar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mbar) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned mbar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(unsigned dst, const void* src, unsigned bytes,
+                                         unsigned mbar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          dst),
+      "l"(src), "r"(bytes), "r"(mbar)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait0(unsigned mbar) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n"
+      " @!p bra WAIT%=;\n}" ::"r"(mbar)
+      : "memory");
+}
+// bytes (multiple of 16, both addresses 16-byte aligned) in chunks of 32 KB;
+// called by one thread after mbar_init
+__device__ __forceinline__ void bulk_stage(unsigned dst, const void* src, unsigned bytes,
+                                           unsigned mbar) {
+  const char* s = static_cast<const char*>(src);
+  for (unsigned o = 0; o < bytes; o += 32768u)
+    bulk_g2s(dst + o, s + o, min(32768u, bytes - o), mbar);
+}
+
 // ------------------------------------------------------------------ density
 // one skin candidate that passed the fp32 filter (rare): full decision
 template <bool FULL, bool REV = true>
@@ -722,24 +757,31 @@ __global__ void __launch_bounds__(NT, 1) k_density_smem(KP P, int nsb) {
   double2* T = reinterpret_cast<double2*>(smem_tab);
   const int nseg = P.fd.nseg;
   if (threadIdx.x == 0) s_ctr = 0;
-  const int seg_lo = max(0, nseg + 1 - kDensTabRecords);
+  // an even first record: the fp32 [A B] pairs (8 bytes each) are then
+  // 16-byte aligned for the bulk copy
+  const int seg_lo = CMPD ? (max(0, nseg + 2 - kDensTabRecords) + 1) & ~1
+                          : max(0, nseg + 1 - kDensTabRecords);
   const int nrec = nseg + 1 - seg_lo;
   const double2* src = reinterpret_cast<const double2*>(P.fd.rec + 4 * (size_t)seg_lo);
   // the constant table is staged while the predecessor drains (PDL)
   // 24-byte records: [D C] 16-byte slots, then the fp32 [A B] pairs
   double2* T8 = T + kDensTabRecords;  // byte offset 16 x kDensTabRecords
-  if (CMPD) {
+  __shared__ __align__(8) unsigned long long s_mbar;
+  if (CMPD) {  // two bulk copies ([A B] rounded up to 16 bytes: the table is padded)
     const int N1 = nseg + 1;
-    const double2* dc = reinterpret_cast<const double2*>(P.fdc) + seg_lo;
-    const double* ab = P.fdc + 2 * (size_t)N1 + seg_lo;
-    for (int q = threadIdx.x; q < nrec; q += blockDim.x) {
-      T[q] = __ldg(dc + q);
-      reinterpret_cast<double*>(T8)[q] = __ldg(ab + q);
+    const unsigned mb = smem_addr(&s_mbar);
+    if (threadIdx.x == 0) {
+      const unsigned b16 = 16u * nrec, b8 = (8u * nrec + 15u) & ~15u;
+      mbar_init(mb);
+      mbar_expect_tx(mb, b16 + b8);
+      bulk_stage(smem_addr(T), P.fdc + 2 * (size_t)seg_lo, b16, mb);
+      bulk_stage(smem_addr(T8), P.fdc + 2 * (size_t)N1 + seg_lo, b8, mb);
     }
   } else {
     for (int q = threadIdx.x; q < 2 * nrec; q += blockDim.x) T[smem_slot32(q >> 1, q & 1)] = __ldg(src + q);
   }
-  __syncthreads();
+  __syncthreads();  // the barrier's initialisation is visible
+  if (CMPD) mbar_wait0(smem_addr(&s_mbar));
   pdl_wait();
   pdl_trigger();
   if (P.st->err) return;
@@ -818,9 +860,14 @@ __global__ void __launch_bounds__(NT, 1) k_force_lean_smem(KP P, int nsb) {
   if (threadIdx.x == 0) s_ctr = 0;
   const int seg_lo = max(0, nseg + 1 - kLeanTabRecords);
   const int nrec = nseg + 1 - seg_lo;
-  if (CMP) {  // 48-byte records, three 16-byte chunks each, in order
-    const double2* src = reinterpret_cast<const double2*>(P.ffc + 6 * (size_t)seg_lo);
-    for (int q = threadIdx.x; q < 3 * nrec; q += blockDim.x) T[q] = __ldg(src + q);
+  __shared__ __align__(8) unsigned long long s_mbar;
+  if (CMP) {  // 48-byte records, three 16-byte chunks each, in order: one bulk copy
+    if (threadIdx.x == 0) {
+      const unsigned mb = smem_addr(&s_mbar);
+      mbar_init(mb);
+      mbar_expect_tx(mb, 48u * nrec);
+      bulk_stage(smem_addr(T), P.ffc + 6 * (size_t)seg_lo, 48u * nrec, mb);
+    }
   } else {
     const double2* src = reinterpret_cast<const double2*>(P.ff.rec + 8 * (size_t)seg_lo);
     for (int q = threadIdx.x; q < 4 * nrec; q += blockDim.x)
@@ -831,7 +878,8 @@ __global__ void __launch_bounds__(NT, 1) k_force_lean_smem(KP P, int nsb) {
     const int n = FULL ? c_full_n[par] : c_half_n[par];
     g_soffs[par][k] = k < n ? (FULL ? c_full[par][k] : c_half[par][k]) : 0;
   }
-  __syncthreads();
+  __syncthreads();  // the barrier's initialisation is visible
+  if (CMP) mbar_wait0(smem_addr(&s_mbar));
   pdl_wait();
   pdl_trigger();
   zero_pair_tail(P, nsb);
