@@ -47,43 +47,43 @@ __device__ void ghost_images(const KP& P, long long d, const double4& p);
 __device__ void ghost_images_at(const KP& P, int par, int cx, int cy, int cz, const double4& p);
 // one site per thread of virtual block vb (128 cells x 2 sublattices)
 __device__ __forceinline__ void kick_drift_site(const KP& P, int move, int zero_acc, int images,
-                                                int vb) {
+                                                int vb, double dt, double hk) {
   int par, cx, cy, cz;
   long long d;
   if (!map_site_xyz(P, vb, par, d, cx, cy, cz)) return;
-  // every load of the site issued before the first use (one round trip)
+  // 32-bit site index into per-component base pointers (a single store fits
+  // 2^31 sites); every load of the site issued before the first use
   const long long S = P.S;
-  double4 p = P.pdf[d];
-  double vx = P.vel[d], vy = P.vel[S + d], vz = P.vel[2 * S + d];
-  const double fx = P.frc[d], fy = P.frc[S + d], fz = P.frc[2 * S + d];
-  const double dt = P.st->dt_next;
+  const int i = (int)d;
+  double* __restrict__ vxp = P.vel;
+  double* __restrict__ vyp = P.vel + S;
+  double* __restrict__ vzp = P.vel + 2 * S;
+  double* __restrict__ fxp = P.frc;
+  double* __restrict__ fyp = P.frc + S;
+  double* __restrict__ fzp = P.frc + 2 * S;
+  double4 p = P.pdf[i];
+  double vx = vxp[i], vy = vyp[i], vz = vzp[i];
+  const double fx = fxp[i], fy = fyp[i], fz = fzp[i];
+  if (zero_acc) {
+    P.rho[i] = 0.0;
+    fxp[i] = 0.0;
+    fyp[i] = 0.0;
+    fzp[i] = 0.0;
+  }
   if (p.x >= kVacantTest) {
-    if (zero_acc) {
-      P.rho[d] = 0.0;
-      P.frc[d] = 0.0;
-      P.frc[S + d] = 0.0;
-      P.frc[2 * S + d] = 0.0;
-    }
     if (images) ghost_images_at(P, par, cx, cy, cz, p);
     return;
   }
   if (move) {
-    const double hk = half_kick(P, dt);
     vx = xadd(vx, xmul(fx, hk));
     vy = xadd(vy, xmul(fy, hk));
     vz = xadd(vz, xmul(fz, hk));
     p.x = xadd(p.x, xmul(vx, dt));
     p.y = xadd(p.y, xmul(vy, dt));
     p.z = xadd(p.z, xmul(vz, dt));
-    P.vel[d] = vx;
-    P.vel[S + d] = vy;
-    P.vel[2 * S + d] = vz;
-  }
-  if (zero_acc) {
-    P.rho[d] = 0.0;
-    P.frc[d] = 0.0;
-    P.frc[S + d] = 0.0;
-    P.frc[2 * S + d] = 0.0;
+    vxp[i] = vx;
+    vyp[i] = vy;
+    vzp[i] = vz;
   }
   const long long own = ref_of_dev(d, P.G.NC);
   // fast hash (canonicalize_positions + nearest_site, store.cpp:88-118 and
@@ -167,7 +167,17 @@ __global__ void __launch_bounds__(256, 4) k_kick_drift(KP P, int move, int nsb, 
     clash_kick_drift_body(P, move, blockIdx.x - nsb, gridDim.x - nsb);
     return;
   }
-  for (int vb = blockIdx.x; vb < nvb; vb += nsb) kick_drift_site(P, move, zero_acc, images, vb);
+  // the step's dt and half kick once per block (sim.cpp:250)
+  __shared__ double s_kick[2];
+  if (threadIdx.x == 0) {
+    const double dt = P.st->dt_next;
+    s_kick[0] = dt;
+    s_kick[1] = half_kick(P, dt);
+  }
+  __syncthreads();
+  const double dt = s_kick[0], hk = s_kick[1];
+  for (int vb = blockIdx.x; vb < nvb; vb += nsb)
+    kick_drift_site(P, move, zero_acc, images, vb, dt, hk);
 }
 
 __device__ void clash_kick_drift_body(const KP& P, int move, int blk, int nblk) {
