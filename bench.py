@@ -224,7 +224,9 @@ def run_ours(args, w, path, ws, rank, local):
                                    "frac": f_dens / t_dens / 1e12 / peak.value},
                 "eam_passes": {"achieved": (f_force + f_dens + FLOP_EMB * n) /
                                ((phases["force"] + phases["density"] + phases["embed"]) * 1e-3)
-                               / 1e12}}
+                               / 1e12},
+                # the resource that binds the stencil passes (ncu, profiles/)
+                "binding_resource": prof.get("binding_resource")}
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
         hbm = peaks.get("hbm_gbs")

@@ -64,6 +64,17 @@ def main():
                                                        else None)
         if key and key not in traffic:
             traffic[key] = tb
+        if key == "force_traffic" and "binding_resource" not in traffic:
+            def metric(m):
+                return float(r[hdr.index(m)].replace(",", "")) if m in hdr else None
+            traffic["binding_resource"] = {
+                "name": "L1/shared data pipe (force pass)",
+                "l1_throughput_pct": metric("l1tex__throughput.avg.pct_of_peak_sustained_active"),
+                "fp64_pipe_pct": metric(
+                    "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
+                "shared_wavefronts": metric("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum"),
+                "shared_bank_conflicts": metric(
+                    "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum")}
     open(os.path.join(HERE, f"{tag}_kernels.md"), "w").write("\n".join(lines) + "\n")
     traffic["source"] = f"profiles/{tag}_kernels.md (dram__bytes_read.sum + dram__bytes_write.sum)"
     json.dump(traffic, open(os.path.join(HERE, "latest_traffic.json"), "w"), indent=1)
