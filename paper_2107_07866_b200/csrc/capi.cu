@@ -30,11 +30,22 @@ struct cbx_ctx {
   unsigned long long* d_defects = nullptr;
   std::vector<void*> allocs;
   cudaGraphExec_t step_graph = nullptr;
+  // single-step calls (cbx_step(dt, 1), the Simulation::step loop) use a
+  // graph that completes the step itself: no pending kick or sums to flush
+  cudaGraphExec_t step_graph1 = nullptr;
+  uint64_t graph1_launches = 0;
+  bool single = false;
+  bool g_defer = false, g_merge = false;  // how step_graph was captured
+  bool t_defer = false, t_merge = false;  // how the timed graphs were captured
+  uint64_t g_launches = 0, t_launches = 0;  // kernels per launch of each
   cudaGraphExec_t timed_graph = nullptr;
   void* flush_buf = nullptr;
   // deferred StepState finalize (fixed dt, single box): graphs captured with
   // it; a pending finalize may exist on the device; its pair partial count
   bool graph_defer = false, fin_maybe = false;
+  // merged kick: the last step's second half kick may be pending on the
+  // device (runs in the next step's k_kick_drift, or before the host reads)
+  bool graph_merge = false, k2_maybe = false, merge_now = false;
   // the host copy of the status equals the device's and nothing ran since
   // (set by cbx_step on success, cleared on entry to every C-ABI call):
   // a following cbx_step skips its opening status round trip
@@ -204,9 +215,14 @@ Tab upload_tab(cbx_ctx* c, const Spline& s) {
 
 void sync_status(cbx_ctx* c) {
   if (c->fin_maybe) {  // the last step's StepState sums before the host reads them
-    launch_finalize_pending(c->P, c->fin_npp, c->stream);
+    launch_finalize_pending(c->P, c->stream);
     c->launches += 1;
     c->fin_maybe = false;
+  }
+  if (c->k2_maybe) {  // the last step's second half kick (+ its StepState sums)
+    launch_kick2(c->P, 1, 1, 1, c->stream, 1, c->fin_npp);
+    c->launches += 1;
+    c->k2_maybe = false;
   }
   cuda_check(cudaMemcpyAsync(&c->hst, c->P.st, sizeof(DevStatus), cudaMemcpyDeviceToHost,
                              c->stream),
@@ -319,6 +335,7 @@ void seq_force(cbx_ctx* c) {
   c->clash_f_zero = false;
   KP q = c->P;
   q.use_mask = c->mask_valid ? 1 : 0;
+  q.mark_k2 = c->merge_now && q.use_mask ? 1 : 0;
   ev_mark(c, 6);  // the force kernel alone (roofline of the dominant kernel)
   const bool fused = launch_force(q, c->mode, c->stream);
   ev_mark(c, 7);
@@ -494,7 +511,18 @@ bool want_defer(const cbx_ctx* c) {
     const char* e = std::getenv("CBX_DEFER_FIN");
     return e ? std::atoi(e) != 0 : true;
   }();
-  return on && !has_transport(c) && !c->hst.adaptive;
+  return on && !has_transport(c) && !c->hst.adaptive && !c->single;
+}
+// merge the second half kick of a step into the next step's kick/drift
+// (one pass over v and f less per step): fixed dt, single box, the Newton-3
+// mask-replay passes (the density pass's clash blocks run the pending sums)
+bool want_merge(const cbx_ctx* c) {
+  static const bool on = [] {
+    const char* e = std::getenv("CBX_MERGE_KICK");
+    static const char* d = std::getenv("CBX_DENSITY_SMEM");
+    return (e ? std::atoi(e) != 0 : true) && !(d && !std::atoi(d));
+  }();
+  return on && want_defer(c) && c->mode == CBX_STENCIL_NEWTON3 && c->P.pmask != nullptr;
 }
 
 void seq_step(cbx_ctx* c) {
@@ -517,11 +545,15 @@ void seq_step(cbx_ctx* c) {
   qf.use_mask = 1;  // the force pass below replays the density pass's mask
   const int npp = force_partials(qf, c->mode);
   const bool defer = want_defer(c);
+  const bool merge = want_merge(c);
   c->graph_defer = defer;
+  c->graph_merge = merge;
   c->fin_npp = npp;
   if (!(skip & 1)) launch_kick_drift(c->P, 1, c->stream, zacc ? 1 : 0, 1, npp);
   c->acc_rho_zero = c->acc_frc_zero = zacc;
-  if (!(skip & 2)) launch_rehash_images(c->P, c->stream);
+  if (!(skip & 2))
+    launch_rehash_images(c->P, c->stream, merge ? 1 : 0, embed_grid(c->P), npp,
+                         kick_drift_grid(c->P));
   c->clash_rho_zero = true;
   c->launches += 2;
   ev_mark(c, 1);
@@ -529,10 +561,16 @@ void seq_step(cbx_ctx* c) {
   ev_mark(c, 2);
   if (!(skip & 8)) seq_embed(c);
   ev_mark(c, 3);
+  c->merge_now = merge;
   if (!(skip & 16)) seq_force(c);
+  c->merge_now = false;
   ev_mark(c, 4);
-  if (!(skip & 32)) launch_kick2(c->P, 1, (skip & 64) ? -2 : 1, 1, c->stream, defer ? 2 : 1, npp);
-  if (defer && !g_capturing) c->fin_maybe = true;
+  if (merge) {
+    if (!g_capturing) c->k2_maybe = true;
+  } else {
+    if (!(skip & 32)) launch_kick2(c->P, 1, (skip & 64) ? -2 : 1, 1, c->stream, defer ? 2 : 1, npp);
+    if (defer && !g_capturing) c->fin_maybe = true;
+  }
   c->launches += 1;
   ev_mark(c, 5);
 }
@@ -578,7 +616,19 @@ cudaGraphExec_t capture_step(cbx_ctx* c, bool with_events) {
 }
 
 void build_graph(cbx_ctx* c) {
-  if (!c->step_graph) c->step_graph = capture_step(c, false);
+  if (c->single) {
+    if (!c->step_graph1) {
+      c->step_graph1 = capture_step(c, false);
+      c->graph1_launches = c->graph_launches;
+    }
+    return;
+  }
+  if (!c->step_graph) {
+    c->step_graph = capture_step(c, false);
+    c->g_defer = c->graph_defer;
+    c->g_merge = c->graph_merge;
+    c->g_launches = c->graph_launches;
+  }
 }
 
 // single-box entry points that a slab rank can only run with its exchanges
@@ -594,6 +644,8 @@ void require_box(cbx_ctx* c, const char* what) {
 
 void drop_graph(cbx_ctx* c) {
   if (c->step_graph) cudaGraphExecDestroy(c->step_graph);
+  if (c->step_graph1) cudaGraphExecDestroy(c->step_graph1);
+  c->step_graph1 = nullptr;
   if (c->timed_graph) cudaGraphExecDestroy(c->timed_graph);
   if (c->timed_lite) cudaGraphExecDestroy(c->timed_lite);
   c->step_graph = nullptr;
@@ -1349,7 +1401,6 @@ static cbx_status create_impl(const cbx_box* box, const cbx_potential* pot,
     P.st = c->alloc<DevStatus>(1);
     P.dself = c->alloc<KP>(1);
     c->d_rem_base = c->alloc<int>(2);
-    P.xp = std::getenv("CBX_XP") ? std::atoi(std::getenv("CBX_XP")) : 0;
     {  // the Wigner-Seitz ball of a BCC site: every other site is >= sqrt(3)/2 a0 away
       const double r = (std::sqrt(3.0) / 4.0 - 1e-6) * G.a0;
       const char* fh = std::getenv("CBX_FAST_HASH");
@@ -1593,13 +1644,28 @@ CBX_API cbx_status cbx_step(cbx_ctx* c, double dt, long nsteps, cbx_state* out) 
       c->hst.dt_next = cbx_adaptive_dt(c->hst.max_speed, c->hst.dt_max, c->hst.max_disp);
       write_status(c);
     }
-    if (c->step_graph && c->graph_defer != want_defer(c)) drop_graph(c);
+    struct Single {  // single-step mode for this call only
+      cbx_ctx* c;
+      ~Single() { c->single = false; }
+    } single_guard{c};
+    c->single = nsteps == 1;
+    if (!c->single && c->step_graph &&
+        (c->g_defer != want_defer(c) || c->g_merge != want_merge(c))) {
+      cudaGraphExecDestroy(c->step_graph);
+      c->step_graph = nullptr;
+    }
     if (c->use_graph && !c->timing) build_graph(c);
     for (long i = 0; i < nsteps; ++i) {
       if (c->use_graph && !c->timing) {
+        if (c->single) {
+          cuda_check(cudaGraphLaunch(c->step_graph1, c->stream), "graph launch");
+          c->launches += c->graph1_launches;
+          continue;
+        }
         cuda_check(cudaGraphLaunch(c->step_graph, c->stream), "graph launch");
-        c->launches += c->graph_launches;
-        if (c->graph_defer) c->fin_maybe = true;
+        c->launches += c->g_launches;
+        if (c->g_merge) c->k2_maybe = true;
+        else if (c->g_defer) c->fin_maybe = true;
       } else {
         seq_step(c);
         accumulate_timing(c, true);
@@ -2123,13 +2189,17 @@ CBX_API cbx_status cbx_bench_steps(cbx_ctx* c, double dt, long nsteps, double fl
     c->hst.adaptive = 0;
     write_status(c);
     const bool phases = c->bench_phases;
-    if ((c->step_graph || c->timed_graph || c->timed_lite) && c->graph_defer != want_defer(c))
+    if ((c->timed_graph || c->timed_lite) &&
+        (c->t_defer != want_defer(c) || c->t_merge != want_merge(c)))
       drop_graph(c);
     cudaGraphExec_t* gp = phases ? &c->timed_graph : &c->timed_lite;
     if (!*gp) {
       c->timing_lite = !phases;
       *gp = capture_step(c, true);
       c->timing_lite = false;
+      c->t_defer = c->graph_defer;
+      c->t_merge = c->graph_merge;
+      c->t_launches = c->graph_launches;
     }
     if (!c->ev_outer[0])
       for (auto& e : c->ev_outer) cuda_check(cudaEventCreate(&e), "event");
@@ -2151,8 +2221,9 @@ CBX_API cbx_status cbx_bench_steps(cbx_ctx* c, double dt, long nsteps, double fl
       cudaEventRecord(c->ev_outer[0], c->stream);
       cuda_check(cudaGraphLaunch(*gp, c->stream), "graph launch");
       cudaEventRecord(c->ev_outer[1], c->stream);
-      c->launches += c->graph_launches;
-      if (c->graph_defer) c->fin_maybe = true;
+      c->launches += c->t_launches;
+      if (c->t_merge) c->k2_maybe = true;
+      else if (c->t_defer) c->fin_maybe = true;
       cuda_check(cudaEventSynchronize(c->ev_outer[1]), "event sync");
       float ms;
       cudaEventElapsedTime(&ms, c->ev_outer[0], c->ev_outer[1]);

@@ -77,7 +77,16 @@ struct DevStatus {
   // an otherwise idle block of the next step's k_kick_drift (fixed dt) or
   // before the host reads the status (k_finalize_pending)
   int fin_pending, fin_stepping, fin_energies;
+  int fin_nemb, fin_npp, fin_nke;  // partial counts of the pending sums
+  int fin_clash;  // > 0: the clash records' sums are in that many reserved slots
+  // merged kick: the step's second half kick is pending and runs in the next
+  // step's k_kick_drift (set by the force pass, consumed by k_rehash_images)
+  int k2_pending;
 };
+
+// clash blocks of k_kick_drift / k_kick2, and the reserved partial slots
+// (the last kClashSlots of each partial array) of the merged kick
+constexpr int kClashSlots = 8;
 
 struct P2PLinks;
 
@@ -120,7 +129,7 @@ struct KP {
   struct KP* dself;        // this parameter block in device memory (guard paths)
   unsigned long long* pmask;  // [S][2] pair masks from the density pass (or null)
   int use_mask;               // force pass replays pmask (set per launch by the host)
-  int xp;                     // timing experiments only (CBX_XP): 1 fixed table row, 2 no RED
+  int mark_k2;                // force pass: mark the second half kick pending (merged kick)
   // fast hash: an atom closer than sqrt(hash_r2) to its own site (the
   // half nearest-neighbour distance sqrt(3)/4 a0 less a margin far above
   // rounding) hashes to that site and needs no periodic wrap (0: off)
@@ -309,7 +318,6 @@ void launch_clash_force(const KP& P, cudaStream_t s);
 void launch_kick_drift(const KP& P, int move, cudaStream_t s, int zero_acc = 0, int images = 0,
                        int n_pairp = 0);
 // update_hash pass 2 + ghost clash images in one single-block launch
-void launch_rehash_images(const KP& P, cudaStream_t s);
 void launch_clash_zero(const KP& P, int what, cudaStream_t s);
 void launch_rehash(const KP& P, cudaStream_t s);
 void launch_ghost_fill(const KP& P, cudaStream_t s);
@@ -320,8 +328,14 @@ void launch_clash_images(const KP& P, cudaStream_t s, int zero_rho = 0);
 // n_pairp: pair-energy partials written by the preceding force pass
 void launch_kick2(const KP& P, int kick, int stepping, int energies, cudaStream_t s, int fin = 1,
                   int n_pairp = -1);
-void launch_finalize_pending(const KP& P, int n_pairp, cudaStream_t s);
+void launch_finalize_pending(const KP& P, cudaStream_t s);
+// merge != 0: a pending second half kick found by k_kick_drift is marked
+// consumed here and the previous step's StepState sums are marked pending
+// (for the density pass's idle block), with these partial counts
+void launch_rehash_images(const KP& P, cudaStream_t s, int merge, int n_emb, int n_pairp,
+                          int n_ke);
 int force_partials(const KP& P, int mode);  // partials the force launch writes
+int kick_drift_grid(const KP& P);           // KE partials of a merged-kick k_kick_drift
 
 void launch_count_defects(const KP& P, unsigned long long* out, cudaStream_t s);
 void upload_offsets(const int* half_dev[2], const int half_n[2], const int* full_dev[2],

@@ -26,6 +26,7 @@
 
 #include "cbx_device.cuh"
 #include "p2p.cuh"
+#include "finalize.cuh"
 
 namespace cbx {
 

@@ -748,6 +748,9 @@ __global__ void __launch_bounds__(NT, 1) k_density_smem(KP P, int nsb) {
   if (blockIdx.x >= nsb) {
     pdl_wait();
     pdl_trigger();
+    // merged kick: the previous step's StepState sums, pending since
+    // k_rehash_images, in the first clash block (it runs in the pass's tail)
+    if (blockIdx.x == nsb) finalize_pending<NT>(P);
     clash_body<0>(P, blockIdx.x - nsb, gridDim.x - nsb);
     return;
   }
@@ -882,6 +885,7 @@ __global__ void __launch_bounds__(NT, 1) k_force_lean_smem(KP P, int nsb) {
   if (CMP) mbar_wait0(smem_addr(&s_mbar));
   pdl_wait();
   pdl_trigger();
+  if (P.mark_k2 && blockIdx.x == 0 && threadIdx.x == 0) P.st->k2_pending = 1;  // merged kick
   zero_pair_tail(P, nsb);
   if (P.st->err || P.st->n_ovl) return;
   const int group = threadIdx.x >> 7;

@@ -21,6 +21,7 @@
 
 #include "cbx_device.cuh"
 #include "p2p.cuh"
+#include "finalize.cuh"
 
 namespace cbx {
 
@@ -45,9 +46,11 @@ __device__ void clash_kick_drift_body(const KP& P, int move, int blk, int nblk);
 // images: also write the site's ghost images (the step path's k_ghost_fill)
 __device__ void ghost_images(const KP& P, long long d, const double4& p);
 __device__ void ghost_images_at(const KP& P, int par, int cx, int cy, int cz, const double4& p);
+__device__ void clash_kick2_sums(const KP& P, int blk);
 // one site per thread of virtual block vb (128 cells x 2 sublattices)
 __device__ __forceinline__ void kick_drift_site(const KP& P, int move, int zero_acc, int images,
-                                                int vb, double dt, double hk) {
+                                                int vb, double dt, double hk, bool k2,
+                                                double& v2s, double& v2m) {
   int par, cx, cy, cz;
   long long d;
   if (!map_site_xyz(P, vb, par, d, cx, cy, cz)) return;
@@ -73,6 +76,14 @@ __device__ __forceinline__ void kick_drift_site(const KP& P, int move, int zero_
   if (p.x >= kVacantTest) {
     if (images) ghost_images_at(P, par, cx, cy, cz, p);
     return;
+  }
+  if (k2) {  // k_kick2 of the previous step (sim.cpp:262-270), same arithmetic
+    vx = xadd(vx, xmul(fx, hk));
+    vy = xadd(vy, xmul(fy, hk));
+    vz = xadd(vz, xmul(fz, hk));
+    const double v2 = exact_r2(vx, vy, vz);
+    v2s += v2;
+    v2m = fmax(v2m, v2);
   }
   if (move) {
     vx = xadd(vx, xmul(fx, hk));
@@ -141,43 +152,82 @@ __device__ __forceinline__ void kick_drift_site(const KP& P, int move, int zero_
 }
 
 // a single wave of blocks (resident on every SM) walks the virtual blocks
-template <int NT>
-__device__ void finalize_body(const KP& P, int stepping, int energies, const double* pe, int n_emb,
-                              const double* pp, int n_pairp, int n_ke);
-// the deferred StepState finalize of the previous k_kick2, if one is pending
-template <int NT>
-__device__ void finalize_pending(const KP& P, int n_emb, int n_pairp, int n_ke) {
-  DevStatus* st = P.st;
-  if (!st->fin_pending) return;
-  finalize_body<NT>(*P.dself, st->fin_stepping, st->fin_energies, P.part_emb, n_emb, P.part_pair,
-                    n_pairp, n_ke);
-  __syncthreads();
-  if (threadIdx.x == 0) st->fin_pending = 0;
-}
 
 __global__ void __launch_bounds__(256, 4) k_kick_drift(KP P, int move, int nsb, int zero_acc,
                                                     int images, int nvb, int n_pairp,
                                                     int n_emb, int n_ke) {
   if (blockIdx.x == nsb) {  // an idle clash block: the previous step's StepState
     // sums (the step's dt is fixed when they are deferred)
-    finalize_pending<256>(P, n_emb, n_pairp, n_ke);
+    finalize_pending<256>(P);
   }
   if (P.st->err) return;
   if (blockIdx.x >= nsb) {  // the clash records (fused k_clash_kick_drift)
+    if (P.st->k2_pending && !P.st->n_ovl) clash_kick2_sums(P, blockIdx.x - nsb);
     clash_kick_drift_body(P, move, blockIdx.x - nsb, gridDim.x - nsb);
     return;
   }
-  // the step's dt and half kick once per block (sim.cpp:250)
+  // the step's dt and half kick once per block (sim.cpp:250); a pending
+  // second half kick of the previous step (same fixed dt) runs first
   __shared__ double s_kick[2];
+  __shared__ int s_k2;
   if (threadIdx.x == 0) {
     const double dt = P.st->dt_next;
     s_kick[0] = dt;
     s_kick[1] = half_kick(P, dt);
+    s_k2 = P.st->k2_pending && !P.st->n_ovl;
   }
   __syncthreads();
   const double dt = s_kick[0], hk = s_kick[1];
+  const bool k2 = s_k2 != 0;
+  double v2s = 0.0, v2m = 0.0;
   for (int vb = blockIdx.x; vb < nvb; vb += nsb)
-    kick_drift_site(P, move, zero_acc, images, vb, dt, hk);
+    kick_drift_site(P, move, zero_acc, images, vb, dt, hk, k2, v2s, v2m);
+  if (k2) {  // the previous step's KE / v_max partials (k_kick2's, per block)
+    __shared__ double sh[8];
+    const double sv = block_sum<256>(v2s, sh);
+    const double mv = block_max<256>(v2m, sh);
+    if (threadIdx.x == 0) {
+      P.part_ke[blockIdx.x] = sv;
+      P.part_vmax[blockIdx.x] = mv;
+    }
+  }
+}
+
+// merged kick: the clash records' part of the previous step's second half
+// kick (clash_kick2_body) and of its StepState sums, before the rehash of
+// this step reorders the records: one partial per clash block in the
+// reserved slots n_part - kClashSlots + blk (finalize_body, clash_slots)
+__device__ void clash_kick2_sums(const KP& P, int blk) {
+  const int n = P.st->n_clash;
+  double ee = 0.0, ep = 0.0, s2 = 0.0, m2 = 0.0;
+  for (int i = blk * blockDim.x + threadIdx.x; i < n; i += kClashSlots * blockDim.x) {
+    ee += P.cl.e_emb[i];
+    ep += P.cl.e_pair[i];
+    double v2 = 0.0;
+    if (!P.cl.gf[i]) {
+      const double hk = half_kick(P, P.st->dt_next);
+      const double vx = xadd(P.cl.vx[i], xmul(P.cl.fx[i], hk));
+      const double vy = xadd(P.cl.vy[i], xmul(P.cl.fy[i], hk));
+      const double vz = xadd(P.cl.vz[i], xmul(P.cl.fz[i], hk));
+      P.cl.vx[i] = vx;
+      P.cl.vy[i] = vy;
+      P.cl.vz[i] = vz;
+      v2 = exact_r2(vx, vy, vz);
+    }
+    P.cl.v2[i] = v2;
+    s2 += v2;
+    m2 = fmax(m2, v2);
+  }
+  __shared__ double sh[8];
+  const double a = block_sum<256>(ee, sh), b = block_sum<256>(ep, sh);
+  const double c = block_sum<256>(s2, sh), d = block_max<256>(m2, sh);
+  if (threadIdx.x == 0) {
+    const int q = P.n_part - kClashSlots + blk;
+    P.part_emb[q] = a;
+    P.part_pair[q] = b;
+    P.part_ke[q] = c;
+    P.part_vmax[q] = d;
+  }
 }
 
 __device__ void clash_kick_drift_body(const KP& P, int move, int blk, int nblk) {
@@ -694,9 +744,23 @@ __global__ void __launch_bounds__(1024) k_clash_images(KP P, int zero_rho) {
 }
 // the store phase's two single-block passes in one launch (the step path,
 // whose slot images k_kick_drift and rehash_body already wrote)
-__global__ void __launch_bounds__(1024) k_rehash_images(KP P) {
+__global__ void __launch_bounds__(1024) k_rehash_images(KP P, int merge, int n_emb, int n_pairp,
+                                                       int n_ke) {
   pdl_wait();
   pdl_trigger();
+  if (merge && threadIdx.x == 0 && P.st->k2_pending) {
+    // k_kick_drift ran the previous step's second half kick: its StepState
+    // sums become pending (for the density pass's idle block)
+    DevStatus* st = P.st;
+    st->k2_pending = 0;
+    st->fin_stepping = 1;
+    st->fin_energies = 1;
+    st->fin_nemb = n_emb;
+    st->fin_npp = n_pairp;
+    st->fin_nke = n_ke;
+    st->fin_clash = kClashSlots;  // the records' sums are in the reserved slots
+    st->fin_pending = 1;
+  }
   rehash_body(P);
   __syncthreads();
   clash_images_body(P, 1);
@@ -758,9 +822,6 @@ __device__ void clash_kick2_body(const KP& P, int kick, int blk, int nblk) {
   }
 }
 
-template <int NT>
-__device__ __noinline__ void finalize_body(const KP& P, int stepping, int energies, const double* pe, int n_emb,
-                              const double* pp, int n_pairp, int n_ke);
 
 // fin: the last block to finish runs finalize_body (the StepState sums) --
 // one launch less per step than a separate k_finalize
@@ -769,6 +830,8 @@ __global__ void __launch_bounds__(256, 6) k_kick2(KP P, int kick, int nsb, int f
   pdl_wait();
   pdl_trigger();
   if (P.rev_wait && !rev_wait(P, P.rev_wait)) return;  // the neighbours' force partials
+  // a standalone second half kick completes a merged-kick step (host flush)
+  if (blockIdx.x == 0 && threadIdx.x == 0) P.st->k2_pending = 0;
   __shared__ double sh[8];
   if (blockIdx.x >= nsb) {  // the clash records (fused k_clash_kick2)
     clash_kick2_body(P, kick, blockIdx.x - nsb, gridDim.x - nsb);
@@ -813,6 +876,10 @@ __global__ void __launch_bounds__(256, 6) k_kick2(KP P, int kick, int nsb, int f
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       P.st->fin_stepping = stepping;
       P.st->fin_energies = energies;
+      P.st->fin_nemb = n_emb;
+      P.st->fin_npp = n_pairp;
+      P.st->fin_nke = nsb;
+      P.st->fin_clash = 0;
       P.st->fin_pending = 1;
     }
     return;
@@ -838,86 +905,7 @@ __global__ void k_clash_kick2(KP P, int kick) {
 }
 
 // ------------------------------------------------------------- finalize
-// deterministic sums of the per-block / per-record partials into StepState
-// (fixed per-thread order, four independent accumulators for load
-// parallelism, then a fixed block tree)
-template <int NT>
-__device__ __noinline__ void finalize_body(const KP& P, int stepping, int energies, const double* pe, int n_emb,
-                              const double* pp, int n_pairp, int n_ke) {
-  __shared__ double sh[4][32];
-  DevStatus* st = P.st;
-  if (st->err || st->n_ovl) return;
-  const int nc = st->n_clash;
-  // one pass over every partial array, all loads of a round independent
-  double ea[4] = {0, 0, 0, 0}, ep[4] = {0, 0, 0, 0}, ek[4] = {0, 0, 0, 0},
-         em[4] = {0, 0, 0, 0};
-  const int ne = energies ? n_emb : 0, np = energies ? n_pairp : 0;
-  const int nk = stepping >= 0 ? n_ke : 0;
-  const int n = max(max(ne, np), nk);
-  for (int i0 = threadIdx.x; i0 < n; i0 += 4 * NT) {
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int i = i0 + u * NT;
-      if (i < ne) ea[u] += pe[i];
-      if (i < np) ep[u] += pp[i];
-      if (i < nk) {  // written by other blocks of a fused k_kick2: L2 loads
-        ek[u] += __ldcg(P.part_ke + i);
-        em[u] = fmax(em[u], __ldcg(P.part_vmax + i));
-      }
-    }
-  }
-  for (int i = threadIdx.x; i < nc; i += NT) {
-    if (energies) {
-      ea[0] += P.cl.e_emb[i];
-      ep[0] += P.cl.e_pair[i];
-    }
-    if (stepping >= 0) {
-      const double v2 = __ldcg(P.cl.v2 + i);
-      ek[0] += v2;
-      em[0] = fmax(em[0], v2);
-    }
-  }
-  double v[4] = {(ea[0] + ea[1]) + (ea[2] + ea[3]), (ep[0] + ep[1]) + (ep[2] + ep[3]),
-                 (ek[0] + ek[1]) + (ek[2] + ek[3]), fmax(fmax(em[0], em[1]), fmax(em[2], em[3]))};
-  for (int o = 16; o > 0; o >>= 1) {
-    v[0] += __shfl_xor_sync(0xffffffffu, v[0], o);
-    v[1] += __shfl_xor_sync(0xffffffffu, v[1], o);
-    v[2] += __shfl_xor_sync(0xffffffffu, v[2], o);
-    v[3] = fmax(v[3], __shfl_xor_sync(0xffffffffu, v[3], o));
-  }
-  const int w = threadIdx.x >> 5;
-  if ((threadIdx.x & 31) == 0)
-    for (int q = 0; q < 4; ++q) sh[q][w] = v[q];
-  __syncthreads();
-  if (threadIdx.x != 0) return;
-  double r[4] = {0, 0, 0, 0};
-  for (int i = 0; i < NT / 32; ++i) {
-    r[0] += sh[0][i];
-    r[1] += sh[1][i];
-    r[2] += sh[2][i];
-    r[3] = fmax(r[3], sh[3][i]);
-  }
-  if (energies) {
-    st->embedding = r[0];
-    st->pair = r[1];
-  }
-  if (stepping >= 0) {  // 1: completed a step, 0: measure only
-    st->kinetic = xmul(xmul(xmul(0.5, P.mass), r[2]), P.mv2);  // sim.cpp:269
-    st->max_speed = sqrt(r[3]);
-    if (stepping == 1) {
-      const double dt = st->dt_next;
-      st->step += 1;
-      st->t = xadd(st->t, dt);
-      st->dt = dt;
-    }
-    if (st->adaptive) {  // adaptive_dt, sim.cpp:94-98
-      double dt = st->dt_max;
-      if (st->max_speed > 0.0) dt = fmin(dt, xdiv(st->max_disp, st->max_speed));
-      st->dt_next = fmax(dt, 1e-7);
-    }
-  }
-}
-
+// (finalize_body / finalize_pending: finalize.cuh)
 // L (device copy, slab ranks on the P2P transport): the cross-rank
 // StepState reduction follows in the same kernel -- also after a device
 // error, so the ranks stay in step
@@ -957,7 +945,7 @@ __global__ void __launch_bounds__(256) k_count_defects(KP P, unsigned long long*
 }
 
 // -------------------------------------------------------------- launchers
-constexpr int kClashBlocks = 8;  // blocks of 256 threads for clash-record sweeps
+constexpr int kClashBlocks = kClashSlots;  // blocks of 256 threads for clash-record sweeps
 // per-site sweeps: one resident wave (blocks per SM x SMs) over eam_blocks
 // virtual blocks
 static int site_wave(const KP& P, int per_sm) {
@@ -980,9 +968,11 @@ void launch_kick_drift(const KP& P, int move, cudaStream_t s, int zero_acc, int 
                                                    n_pairp > 0 ? n_pairp : P.n_pair_part,
                                                    embed_grid(P), kick_grid(P));
 }
-void launch_rehash_images(const KP& P, cudaStream_t s) {
-  launch_pdl(k_rehash_images, 1, 1024, 0, s, P);
+void launch_rehash_images(const KP& P, cudaStream_t s, int merge, int n_emb, int n_pairp,
+                          int n_ke) {
+  launch_pdl(k_rehash_images, 1, 1024, 0, s, P, merge, n_emb, n_pairp, n_ke);
 }
+int kick_drift_grid(const KP& P) { return site_wave(P, 4); }
 void launch_rehash(const KP& P, cudaStream_t s) { launch_pdl(k_rehash, 1, 1024, 0, s, P); }
 void launch_ghost_fill(const KP& P, cudaStream_t s) {
   if (P.n_gh) launch_pdl(k_ghost_fill, (int)((P.n_gh + 255) / 256), 256, 0, s, P);
@@ -1002,12 +992,9 @@ void launch_kick2(const KP& P, int kick, int stepping, int energies, cudaStream_
              stepping, energies, n_pairp > 0 ? n_pairp : P.n_pair_part, embed_grid(P),
              eam_blocks(P));
 }
-__global__ void __launch_bounds__(1024) k_finalize_pending(KP P, int n_emb, int n_pairp, int n_ke) {
-  finalize_pending<1024>(P, n_emb, n_pairp, n_ke);
-}
-void launch_finalize_pending(const KP& P, int n_pairp, cudaStream_t s) {
-  k_finalize_pending<<<1, 1024, 0, s>>>(P, embed_grid(P), n_pairp > 0 ? n_pairp : P.n_pair_part,
-                                        kick_grid(P));
+__global__ void __launch_bounds__(1024) k_finalize_pending(KP P) { finalize_pending<1024>(P); }
+void launch_finalize_pending(const KP& P, cudaStream_t s) {
+  k_finalize_pending<<<1, 1024, 0, s>>>(P);
 }
 void launch_finalize(const KP& P, int stepping, int energies, cudaStream_t s,
                      const P2PLinks* links) {

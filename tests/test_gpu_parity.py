@@ -298,7 +298,13 @@ def test_cascade_clash_and_defects(cuda, tables, stencil):
     saw_clash = False
     for chunk in range(8):
         ref.step(1e-4, 25)
-        dev.step(1e-4, 25)
+        sd = dev.step(1e-4, 25)
+        # StepState of a multi-step call: the sums of the last step (clash
+        # records included) after the merged / deferred kicks are flushed
+        sr = ref.state()
+        assert sd["step"] == sr["step"]
+        for k in ("kinetic", "pair", "embedding", "max_speed"):
+            assert close(sd[k], sr[k], 1e-9), (chunk, k, sd[k], sr[k])
         rs, ds = ref.store(), dev.download()
         saw_clash |= (rs.clash_ghost == 0).sum() > 0
         assert ref.count_defects() == dev.count_defects(), chunk
