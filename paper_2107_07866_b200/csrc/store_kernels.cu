@@ -540,11 +540,35 @@ __device__ void ghost_images(const KP& P, long long d, const double4& p) {
 }
 __device__ void ghost_images_at(const KP& P, int par, int cx, int cy, int cz, const double4& p) {
   const Geo& G = P.G;
-  // one image shift per axis at most (every box at least as wide as the
-  // ghost shell): a site has images only within 2g cells of a face
-  if (G.kmx == 1 && G.kmy == 1 && G.kmz <= 1 && cx < G.bx && cx >= G.tx - G.bx && cy < G.by &&
-      cy >= G.ty - G.by && (G.kmz == 0 || (cz < G.bz && cz >= G.tz - G.bz)))
+  // boxes at least 2g cells wide: at most one image shift per axis, the
+  // images are the non-empty subsets of the shifted axes (the same position
+  // arithmetic as the general enumeration below)
+  if (G.kmx == 1 && G.kmy == 1 && G.kmz <= 1 && G.bx >= 2 * G.g && G.by >= 2 * G.g &&
+      (G.kmz == 0 || G.bz >= 2 * G.g)) {
+    const int sx = cx >= G.bx ? -1 : (cx < G.tx - G.bx ? 1 : 0);
+    const int sy = cy >= G.by ? -1 : (cy < G.ty - G.by ? 1 : 0);
+    const int sz = G.kmz == 0 ? 0 : (cz >= G.bz ? -1 : (cz < G.tz - G.bz ? 1 : 0));
+    if (!(sx | sy | sz)) return;
+    const bool vac = p.x >= kVacantTest;
+    const float w = __int_as_float((int)(par * G.NC + cell_of(cx, cy, cz, G)));
+    for (int m = 1; m < 8; ++m) {
+      const int kx = (m & 1) ? sx : 0, ky = (m & 2) ? sy : 0, kz = (m & 4) ? sz : 0;
+      if (((m & 1) && !sx) || ((m & 2) && !sy) || ((m & 4) && !sz)) continue;
+      const long long di =
+          par * G.NC + cell_of(cx + G.bx * kx, cy + G.by * ky, cz + G.bz * kz, G);
+      if (vac) {
+        P.pdf[di] = make_double4(kVacant, kVacant, kVacant, 0.0);
+        P.uf[di] = make_float4(kVacantF, kVacantF, kVacantF, w);
+        continue;
+      }
+      const double4 q = make_double4(xadd(p.x, xmul((double)kx, G.lx)),
+                                     xadd(p.y, xmul((double)ky, G.ly)),
+                                     xadd(p.z, xmul((double)kz, G.lz)), p.w);
+      P.pdf[di] = q;
+      P.uf[di] = make_float4((float)q.x, (float)q.y, (float)q.z, w);
+    }
     return;
+  }
   const long long d = par * G.NC + cell_of(cx, cy, cz, G);
   int xl = 0, xh = 0, yl = 0, yh = 0, zl = 0, zh = 0;  // valid image shifts per axis
   for (int k = 1; k <= G.kmx; ++k) {
