@@ -570,8 +570,8 @@ void seq_step(cbx_ctx* c) {
   } else {
     if (!(skip & 32)) launch_kick2(c->P, 1, (skip & 64) ? -2 : 1, 1, c->stream, defer ? 2 : 1, npp);
     if (defer && !g_capturing) c->fin_maybe = true;
+    c->launches += 1;
   }
-  c->launches += 1;
   ev_mark(c, 5);
 }
 
