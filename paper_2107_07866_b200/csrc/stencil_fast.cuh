@@ -959,6 +959,23 @@ bool launch_density_fast(const KP& P, int mode, int grid, cudaStream_t s) {
       attr = true;
     }
     const int g = max(1, min(sm_count(), unit_count(P.G)));
+    static const int nt_env = [] {  // CBX_DENSITY_NT overrides the rule below
+      const char* e = getenv("CBX_DENSITY_NT");
+      return e ? atoi(e) : 0;
+    }();
+    // at most 7 units per CTA: 7 groups with 72 registers (as the force pass)
+    const int nt = nt_env ? nt_env : ((unit_count(P.G) + g - 1) / g <= 7 ? 896 : 1024);
+    if (cmp && nt == 896 && !mode && !P.rev.on) {
+      static bool attr896 = false;
+      if (!attr896) {
+        cudaFuncSetAttribute((const void*)k_density_smem<false, 1, 896, false, true>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)((size_t)kDensTabRecords * 32));
+        attr896 = true;
+      }
+      launch_pdl(k_density_smem<false, 1, 896, false, true>, g + 4, 896, bytes, s, P, g);
+      return true;
+    }
     if (cmp) {
       if (mode) launch_pdl(k_density_smem<true, 1, 1024, false, true>, g, 1024, bytes, s, P, g);
       else if (P.rev.on)
@@ -995,6 +1012,24 @@ void launch_force_lean(const KP& P, int mode, cudaStream_t s) {
     attr = true;
   }
   const int g = max(1, min(sm_count(), unit_count(P.G)));
+  // at most 7 units per CTA (one wave, e.g. config 2): 7 groups of 128
+  // threads with 72 registers instead of 8 with 64 (CBX_FORCE_NT overrides)
+  static const int nt_env = [] {
+    const char* e = getenv("CBX_FORCE_NT");
+    return e ? atoi(e) : 0;
+  }();
+  const int g0 = max(1, min(sm_count(), unit_count(P.G)));
+  const int nt = nt_env ? nt_env : ((unit_count(P.G) + g0 - 1) / g0 <= 7 ? 896 : 1024);
+  if (nt == 896 && !mode && !P.rev.on) {
+    static bool attr896 = false;
+    if (!attr896) {
+      cudaFuncSetAttribute((const void*)k_force_lean_smem<false, 896, CMP>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+      attr896 = true;
+    }
+    launch_pdl(k_force_lean_smem<false, 896, CMP>, g + 4, 896, bytes, s, P, g);
+    return;
+  }
   if (mode) launch_pdl(k_force_lean_smem<true, 1024, CMP>, g, 1024, bytes, s, P, g);
   else if (P.rev.on)
     launch_pdl(k_force_lean_smem<false, 1024, CMP, true>, g + 4, 1024, bytes, s, P, g);
