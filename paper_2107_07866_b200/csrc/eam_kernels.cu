@@ -376,7 +376,7 @@ int embed_grid(const KP& P) {
   int sms = 148, dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  return std::max(1, std::min(embed_blocks(P), 8 * sms));
+  return std::max(1, std::min(embed_blocks(P), 6 * sms));  // one resident wave (256, 6)
 }
 
 __global__ void k_clash_embed(KP P) { clash_embed_body(P, blockIdx.x, gridDim.x); }

@@ -16,8 +16,21 @@ __device__ __noinline__ void finalize_body(const KP& P, int stepping, int energi
                               const double* pp, int n_pairp, int n_ke, int clash_slots = 0) {
   __shared__ double sh[4][32];
   DevStatus* st = P.st;
-  if (st->err || st->n_ovl) return;
+  // the status words and thread 0's StepState fields are loaded together
+  // with the partials (one memory round trip); the error test follows them
+  const int bad = st->err | st->n_ovl;
   const int nc = st->n_clash;
+  double s_dt = 0.0, s_t = 0.0, s_dtmax = 0.0, s_disp = 0.0;
+  long long s_step = 0;
+  int s_adapt = 0;
+  if (threadIdx.x == 0) {
+    s_dt = st->dt_next;
+    s_t = st->t;
+    s_step = st->step;
+    s_adapt = st->adaptive;
+    s_dtmax = st->dt_max;
+    s_disp = st->max_disp;
+  }
   // one pass over every partial array, all loads of a round independent
   double ea[4] = {0, 0, 0, 0}, ep[4] = {0, 0, 0, 0}, ek[4] = {0, 0, 0, 0},
          em[4] = {0, 0, 0, 0};
@@ -58,6 +71,7 @@ __device__ __noinline__ void finalize_body(const KP& P, int stepping, int energi
       em[0] = fmax(em[0], v2);
     }
   }
+  if (bad) return;
   double v[4] = {(ea[0] + ea[1]) + (ea[2] + ea[3]), (ep[0] + ep[1]) + (ep[2] + ep[3]),
                  (ek[0] + ek[1]) + (ek[2] + ek[3]), fmax(fmax(em[0], em[1]), fmax(em[2], em[3]))};
   for (int o = 16; o > 0; o >>= 1) {
@@ -85,15 +99,15 @@ __device__ __noinline__ void finalize_body(const KP& P, int stepping, int energi
   if (stepping >= 0) {  // 1: completed a step, 0: measure only
     st->kinetic = xmul(xmul(xmul(0.5, P.mass), r[2]), P.mv2);  // sim.cpp:269
     st->max_speed = sqrt(r[3]);
+    const double vmax = sqrt(r[3]);
     if (stepping == 1) {
-      const double dt = st->dt_next;
-      st->step += 1;
-      st->t = xadd(st->t, dt);
-      st->dt = dt;
+      st->step = s_step + 1;
+      st->t = xadd(s_t, s_dt);
+      st->dt = s_dt;
     }
-    if (st->adaptive) {  // adaptive_dt, sim.cpp:94-98
-      double dt = st->dt_max;
-      if (st->max_speed > 0.0) dt = fmin(dt, xdiv(st->max_disp, st->max_speed));
+    if (s_adapt) {  // adaptive_dt, sim.cpp:94-98
+      double dt = s_dtmax;
+      if (vmax > 0.0) dt = fmin(dt, xdiv(s_disp, vmax));
       st->dt_next = fmax(dt, 1e-7);
     }
   }
