@@ -852,6 +852,11 @@ __global__ void __launch_bounds__(NT, 1) k_force_lean_smem(KP P, int nsb) {
   if (blockIdx.x >= nsb) {
     pdl_wait();
     pdl_trigger();
+    // the unused pair partials (read by k_finalize over the full capacity)
+    // are zeroed by an extra block, not by a unit CTA
+    if (blockIdx.x == nsb) {
+      for (int i = nsb + threadIdx.x; i < P.n_pair_part; i += blockDim.x) P.part_pair[i] = 0.0;
+    }
     clash_body<1>(P, blockIdx.x - nsb, gridDim.x - nsb);
     return;
   }
@@ -886,7 +891,7 @@ __global__ void __launch_bounds__(NT, 1) k_force_lean_smem(KP P, int nsb) {
   pdl_wait();
   pdl_trigger();
   if (P.mark_k2 && blockIdx.x == 0 && threadIdx.x == 0) P.st->k2_pending = 1;  // merged kick
-  zero_pair_tail(P, nsb);
+  if (FULL) zero_pair_tail(P, nsb);  // no extra blocks in this launch
   if (P.st->err || P.st->n_ovl) return;
   const int group = threadIdx.x >> 7;
   const int lt = threadIdx.x & 127, lane = lt & 31, w = lt >> 5;
