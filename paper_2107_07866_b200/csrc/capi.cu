@@ -268,6 +268,7 @@ void raise_device_error(cbx_ctx* c, bool in_step) {
   h.err = 0;
   h.n_ovl = 0;
   h.n_mov = 0;
+  h.halt = 0;
   cudaMemcpyAsync(c->P.st, &h, sizeof(DevStatus), cudaMemcpyHostToDevice, c->stream);
   cudaStreamSynchronize(c->stream);
   raise(code, msg);
@@ -823,6 +824,7 @@ void do_upload(cbx_ctx* c, const cbx_store* s) {
   c->hst.n_mov = 0;
   c->hst.err = 0;
   c->hst.n_ovl = 0;
+  c->hst.halt = 0;
   write_status(c);
   seq_fill_ghosts(c);
   launch_uf_refresh(c->P, c->stream);
@@ -1840,6 +1842,10 @@ CBX_API cbx_status cbx_thermostat_rescale(cbx_ctx* c, double temperature, long b
   const cbx_status rc = guarded(c, [&] {
     cudaSetDevice(c->device);
     require_box(c, "cbx_thermostat_rescale");
+    // a pending merged second half kick / deferred StepState sum first: the
+    // sums below read the velocities and reuse the KE partials as scratch
+    sync_status(c);
+    raise_device_error(c, false);
     const int nsb = eam_blocks(c->P), grid = nsb + 8;
     double* psum = c->P.part_ke;  // scratch: the next measure rewrites them
     double* pcnt = c->P.part_vmax;

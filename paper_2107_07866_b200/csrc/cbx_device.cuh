@@ -79,6 +79,11 @@ struct DevStatus {
   int fin_pending, fin_stepping, fin_energies;
   int fin_nemb, fin_npp, fin_nke;  // partial counts of the pending sums
   int fin_clash;  // > 0: the clash records' sums are in that many reserved slots
+  int fin_bad;    // err | n_ovl when the sums were deferred (their step's outcome)
+  // a step of the current multi-step replay failed (set by k_rehash_images of
+  // the next step from the stable status words): the passes of the remaining
+  // steps are no-ops, so the store stays at the failing step (sim.cpp:303-315)
+  int halt;
   // merged kick: the step's second half kick is pending and runs in the next
   // step's k_kick_drift (set by the force pass, consumed by k_rehash_images)
   int k2_pending;

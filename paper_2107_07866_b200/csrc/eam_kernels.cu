@@ -184,7 +184,7 @@ __device__ __forceinline__ void full_orient(const KP& P, const double4& a, long 
 // ------------------------------------------------------------ density pass
 template <bool FULL>
 __global__ void __launch_bounds__(256) k_density(KP P) {
-  if (P.st->err) return;
+  if (P.st->err || P.st->halt) return;
   int par;
   long long d;
   if (!map_site(P, par, d)) return;
@@ -390,7 +390,7 @@ __global__ void k_clash_embed(KP P) { clash_embed_body(P, blockIdx.x, gridDim.x)
 // (the standalone kernel, or the extra blocks of a fused pass)
 template <int MODE>  // 0 density, 1 force
 __device__ void clash_body(const KP& P, int blk, int nblk) {
-  if (P.st->err) return;
+  if (P.st->err || P.st->halt) return;
   if (MODE == 1 && P.st->n_ovl) return;
   const int n = P.st->n_clash;
   if (n == 0) return;

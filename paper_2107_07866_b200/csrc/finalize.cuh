@@ -11,14 +11,18 @@ namespace cbx {
 // deterministic sums of the per-block / per-record partials into StepState
 // (fixed per-thread order, four independent accumulators for load
 // parallelism, then a fixed block tree)
+// bad_at: the outcome of the step whose sums these are, captured when they
+// were deferred (fin_bad); -1 reads the live status words (the sums of the
+// step that just ended).  Read once by thread 0 and shared, so the whole
+// block takes the same branch.
 template <int NT>
 __device__ __noinline__ void finalize_body(const KP& P, int stepping, int energies, const double* pe, int n_emb,
-                              const double* pp, int n_pairp, int n_ke, int clash_slots = 0) {
+                              const double* pp, int n_pairp, int n_ke, int clash_slots = 0,
+                              int bad_at = -1) {
   __shared__ double sh[4][32];
+  __shared__ int s_bad;
   DevStatus* st = P.st;
-  // the status words and thread 0's StepState fields are loaded together
-  // with the partials (one memory round trip); the error test follows them
-  const int bad = st->err | st->n_ovl;
+  if (threadIdx.x == 0) s_bad = bad_at >= 0 ? bad_at : (st->err | st->n_ovl);
   const int nc = st->n_clash;
   double s_dt = 0.0, s_t = 0.0, s_dtmax = 0.0, s_disp = 0.0;
   long long s_step = 0;
@@ -71,7 +75,8 @@ __device__ __noinline__ void finalize_body(const KP& P, int stepping, int energi
       em[0] = fmax(em[0], v2);
     }
   }
-  if (bad) return;
+  __syncthreads();
+  if (s_bad) return;
   double v[4] = {(ea[0] + ea[1]) + (ea[2] + ea[3]), (ep[0] + ep[1]) + (ep[2] + ep[3]),
                  (ek[0] + ek[1]) + (ek[2] + ek[3]), fmax(fmax(em[0], em[1]), fmax(em[2], em[3]))};
   for (int o = 16; o > 0; o >>= 1) {
@@ -120,7 +125,7 @@ __device__ void finalize_pending(const KP& P) {
   DevStatus* st = P.st;
   if (!st->fin_pending) return;
   finalize_body<NT>(*P.dself, st->fin_stepping, st->fin_energies, P.part_emb, st->fin_nemb,
-                    P.part_pair, st->fin_npp, st->fin_nke, st->fin_clash);
+                    P.part_pair, st->fin_npp, st->fin_nke, st->fin_clash, st->fin_bad);
   __syncthreads();
   if (threadIdx.x == 0) st->fin_pending = 0;
 }

@@ -787,7 +787,7 @@ __global__ void __launch_bounds__(NT, 1) k_density_smem(KP P, int nsb) {
   if (CMPD) mbar_wait0(smem_addr(&s_mbar));
   pdl_wait();
   pdl_trigger();
-  if (P.st->err) return;
+  if (P.st->err || P.st->halt) return;
   const int group = threadIdx.x >> 7;
   const int lt = threadIdx.x & 127, lane = lt & 31, w = lt >> 5;
   const Geo& G = P.G;
@@ -811,7 +811,7 @@ __global__ void __launch_bounds__(128, MINB) k_density_fast(KP P, int nsb) {
     clash_body<0>(P, blockIdx.x - nsb, gridDim.x - nsb);
     return;
   }
-  if (P.st->err) return;
+  if (P.st->err || P.st->halt) return;
   const int nb = brick_count(P.G);
   for (;;) {
     const int b = next_brick(&P.work[0]);

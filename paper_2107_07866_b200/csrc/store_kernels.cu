@@ -160,9 +160,11 @@ __global__ void __launch_bounds__(256, 4) k_kick_drift(KP P, int move, int nsb, 
     // sums (the step's dt is fixed when they are deferred)
     finalize_pending<256>(P);
   }
-  if (P.st->err) return;
+  // a failed step (device error or overlap, stable since the previous
+  // step's passes) ends the replay: no further kick, drift or rehash
+  if (P.st->err || P.st->n_ovl) return;
   if (blockIdx.x >= nsb) {  // the clash records (fused k_clash_kick_drift)
-    if (P.st->k2_pending && !P.st->n_ovl) clash_kick2_sums(P, blockIdx.x - nsb);
+    if (P.st->k2_pending) clash_kick2_sums(P, blockIdx.x - nsb);
     clash_kick_drift_body(P, move, blockIdx.x - nsb, gridDim.x - nsb);
     return;
   }
@@ -174,7 +176,7 @@ __global__ void __launch_bounds__(256, 4) k_kick_drift(KP P, int move, int nsb, 
     const double dt = P.st->dt_next;
     s_kick[0] = dt;
     s_kick[1] = half_kick(P, dt);
-    s_k2 = P.st->k2_pending && !P.st->n_ovl;
+    s_k2 = P.st->k2_pending;
   }
   __syncthreads();
   const double dt = s_kick[0], hk = s_kick[1];
@@ -231,7 +233,7 @@ __device__ void clash_kick2_sums(const KP& P, int blk) {
 }
 
 __device__ void clash_kick_drift_body(const KP& P, int move, int blk, int nblk) {
-  if (P.st->err) return;
+  if (P.st->err || P.st->n_ovl) return;
   const int n = P.st->n_clash;
   for (int i = blk * blockDim.x + threadIdx.x; i < n; i += nblk * blockDim.x) {
     if (P.cl.gf[i]) continue;
@@ -397,8 +399,22 @@ __device__ __forceinline__ void copy_record(const Clash& a, int i, const Clash& 
 // that claims a free slot and the rest the new bucket, in order.
 __device__ void ghost_images(const KP& P, long long d, const double4& p);
 
+// single-block store passes (after kick/drift, before the step's density
+// pass): the status words are stable here, so a failure of an earlier step
+// of the replay raises `halt` and the remaining passes of the call skip
+__device__ bool halt_check(const KP& P) {
+  __shared__ int s_halt;
+  if (threadIdx.x == 0) {
+    DevStatus* st = P.st;
+    s_halt = (st->err | st->n_ovl) != 0;
+    if (s_halt) st->halt = 1;
+  }
+  __syncthreads();
+  return s_halt != 0;
+}
+
 __device__ void rehash_body(const KP& P) {
-  if (P.st->err) return;
+  if (P.st->err || P.st->n_ovl) return;
   const int n_old = P.st->n_clash;
   const int n_mov = min(P.st->n_mov, P.cap_mov);
   if (n_old == 0 && n_mov == 0) return;
@@ -525,6 +541,7 @@ __device__ void rehash_body(const KP& P) {
 __global__ void __launch_bounds__(1024) k_rehash(KP P) {
   pdl_wait();
   pdl_trigger();
+  if (halt_check(P)) return;
   rehash_body(P);
 }
 
@@ -654,7 +671,7 @@ __device__ __forceinline__ int image_count(long long id, const Geo& G) {
 
 __device__ void clash_images_body(const KP& P, int zero_rho) {
   if (zero_rho && threadIdx.x == 0) P.work[0] = 0;  // the density pass's brick queue
-  if (P.st->err) return;
+  if (P.st->err || P.st->n_ovl) return;
   const int n = P.st->n_clash;
   const int n_rem = P.st->n_remote;
   if (n == 0 && n_rem == 0) return;
@@ -772,10 +789,12 @@ __global__ void __launch_bounds__(1024) k_rehash_images(KP P, int merge, int n_e
                                                        int n_ke) {
   pdl_wait();
   pdl_trigger();
+  if (halt_check(P)) return;
   if (merge && threadIdx.x == 0 && P.st->k2_pending) {
     // k_kick_drift ran the previous step's second half kick: its StepState
     // sums become pending (for the density pass's idle block)
     DevStatus* st = P.st;
+    st->fin_bad = 0;  // that step completed (else this step would have halted)
     st->k2_pending = 0;
     st->fin_stepping = 1;
     st->fin_energies = 1;
@@ -904,6 +923,7 @@ __global__ void __launch_bounds__(256, 6) k_kick2(KP P, int kick, int nsb, int f
       P.st->fin_npp = n_pairp;
       P.st->fin_nke = nsb;
       P.st->fin_clash = 0;
+      P.st->fin_bad = P.st->err | P.st->n_ovl;  // this step's outcome, stable here
       P.st->fin_pending = 1;
     }
     return;

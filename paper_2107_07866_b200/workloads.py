@@ -8,6 +8,7 @@ drawn with numpy's PCG64 (seed 12345) in interior-site order.
 """
 from __future__ import annotations
 
+import math
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -62,6 +63,26 @@ def pka_site_id(w: Workload, ghost_width: int) -> int:
     return ((g + cz) * ty + (g + cy)) * 2 * tx + 2 * (g + cx)
 
 
+def pka_velocity(w: Workload, mass: float):
+    """Simulation::inject_pka's velocity (sim.cpp:172-185): pka_speed(E, m)
+    along the direction normalised on the host, as the reference computes it"""
+    from .engine import pka_speed
+    d = [float(x) for x in w.pka_dir]
+    ln = math.sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2])
+    s = pka_speed(w.pka_kev * 1000.0, mass) / ln
+    return (d[0] * s, d[1] * s, d[2] * s)
+
+
+def slab_site_id(info, cx: int, cy: int, cz_global: int) -> int:
+    """local reference id of the corner site of global cell (cx, cy, cz) on a
+    slab rank (cbx_slab_info: zoff, bz, g, tx, ty); -1 if another rank owns it"""
+    zoff, bz, g, tx, ty = info[2], info[3], info[4], info[5], info[6]
+    zl = cz_global - zoff
+    if not 0 <= zl < bz:
+        return -1
+    return ((g + zl) * ty + (g + cy)) * 2 * tx + 2 * (g + cx)
+
+
 def build_device_state(w: Workload, potential, device: int = 0, stencil: str = "newton3"):
     """A DeviceStore in the workload's initial state: lattice + MB velocities,
     displacements, rehash, forces, measure (the Simulation constructor path)."""
@@ -78,35 +99,50 @@ def build_device_state(w: Workload, potential, device: int = 0, stencil: str = "
         dev.upload(s)
         dev.rehash()
     dev.eval_forces()
+    if w.pka_kev > 0.0:  # the configuration's PKA (sim.cpp:163-186; measures)
+        dev.inject_pka(pka_site_id(w, box.ghost_width), pka_velocity(w, potential.mass))
     dev.measure()
     return dev, n
 
 
 def build_slab_state(w: Workload, potential, rank: int, nranks: int, device: int = 0,
-                     stencil: str = "newton3", transport: str = "p2p"):
-    """Rank `rank` of a weak-scaled z-slab run: the global box stacks `nranks`
-    copies of the workload's cells along z (cells[2] planes per rank).  The
-    slab holds exactly its planes of the single-box initial state of that
+                     stencil: str = "newton3", transport: str = "p2p",
+                     scaling: str = "weak"):
+    """Rank `rank` of a z-slab run over `nranks` GPUs.
+
+    weak:   the global box stacks `nranks` copies of the workload's cells
+            along z (cells[2] planes per rank) with one PKA at the centre cell
+            of every rank's subdomain (BASELINE config 5);
+    strong: the workload's box itself is split into `nranks` slabs with the
+            one PKA at the global centre (BASELINE config 4).
+    The slab holds exactly its planes of the single-box initial state of the
     global box (same lattice RNG stream and displacement rows).  The ranks
     connect through torch.distributed (P2P handles or the NCCL id); forces
     and the kinetic energy are evaluated collectively."""
     from .engine import SimConfig, make_box
     from .slab import SlabRank
     bx, by, bz = w.cells
-    cfg = SimConfig(box_x=bx, box_y=by, box_z=bz * nranks, temperature=w.temperature,
-                    seed=w.seed)
+    gz = bz * nranks if scaling == "weak" else bz
+    cfg = SimConfig(box_x=bx, box_y=by, box_z=gz, temperature=w.temperature, seed=w.seed)
     gbox, _ = make_box(cfg, potential)
     r = SlabRank(gbox, potential, rank, nranks, device=device, stencil=stencil)
     n = r.init_bcc(w.temperature, w.seed, potential.atomic_number)
     if w.displacement > 0.0:
         per_plane = 2 * bx * by
         z0 = r.info[2]
-        d = displacements(w, per_plane * bz * nranks)[z0 * per_plane:(z0 + r.info[3]) * per_plane]
+        d = displacements(w, per_plane * gz)[z0 * per_plane:(z0 + r.info[3]) * per_plane]
         s = r.download()
         m = s.valid.astype(bool) & ~s.ghost.astype(bool)
         s.pos[m] += d
         r.upload(s)
     r.connect(transport)
     r.eval_forces()
+    if w.pka_kev > 0.0:
+        centres = ([bz * q + bz // 2 for q in range(nranks)] if scaling == "weak" else [gz // 2])
+        v = pka_velocity(w, potential.mass)
+        for cz in centres:
+            site = slab_site_id(r.info, bx // 2, by // 2, cz)
+            if site >= 0:
+                r.inject_pka(site, v)
     r.measure()
     return r, n

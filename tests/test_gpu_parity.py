@@ -312,6 +312,50 @@ def test_cascade_clash_and_defects(cuda, tables, stencil):
     assert saw_clash
 
 
+def test_overlap_halts_multi_step_call(cuda, tables):
+    """An overlap found in step 2 of a 5-step call (fixed dt: merged kicks and
+    deferred StepState sums) ends the call at step 2 like the reference's
+    throw from refresh_forces (sim.cpp:225-231, forces.cpp:414-447): same
+    message, StepState of the completed step 1 with step = 2, and the store
+    as the failing step left it -- positions and velocities of step 2's
+    drift, rho of its density pass -- not several drifts further.
+
+    Setup: a 10 keV-class interstitial shot at a lattice atom of a cold 6^3
+    box along +x; its offset (0.18497741167859 A) was found by a secant
+    search on the oracle so that the pair passes 2.9e-8 A apart exactly at
+    step 2 (overlap threshold 1e-6 A, forces.cpp:15).  Deviation by design:
+    the device clears the force accumulators in the step's first kernel, so
+    the failing step's forces read 0 where the reference keeps step 1's."""
+    from oracle import oracle
+    from paper_2107_07866_b200._lib import CbxRuntimeError
+    ref = oracle.Sim(tables["baseline"], box=(6, 6, 6), temperature=0.0, seed=1)
+    _, a, g = ref.box
+    site = np.array([(g + 3) * a] * 3)
+    ref.insert(site + [0.18497741167859, 0.0, 0.0], 900001, vel=(-1000.0, 0.0, 0.0))
+    ref.fill_ghosts()
+    ref.refresh_forces()
+    dev = device_for(ref, tables["baseline"])
+    dev.set_state(ref.state())
+    with pytest.raises(RuntimeError) as er:
+        ref.step(1e-4, 5)
+    with pytest.raises(CbxRuntimeError) as ed:
+        dev.step(1e-4, 5)
+    assert str(er.value).startswith("step 2: atoms 900001 and ")
+    assert str(ed.value) == str(er.value)
+    sr, sd = ref.state(), dev.state()
+    assert sd["step"] == sr["step"] == 2
+    assert sd["t"] == sr["t"]
+    assert close(sd["kinetic"], sr["kinetic"], 1e-12)
+    rs, ds = ref.store(), dev.download()
+    assert structure(rs) == structure(ds)
+    a_, b_ = by_tag(rs), by_tag(ds)
+    for t, (pa, va, fa, ra, da) in a_.items():
+        pb, vb, fb, rb, db = b_[t]
+        assert np.abs(pa - pb).max() <= 1e-12, t
+        assert np.abs(va - vb).max() <= 1e-9 * max(1.0, np.abs(va).max()), t
+        assert abs(ra - rb) <= REL * max(abs(ra), 1e-300), t
+
+
 def test_adaptive_dt_matches(cuda, tables):
     from oracle import oracle
     ref = oracle.Sim(tables["baseline"], box=(6, 6, 6), temperature=600.0, seed=3)
