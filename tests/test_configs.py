@@ -113,8 +113,8 @@ def test_config45_thermal_step_identical_inputs(cuda, tables, cfg):
     force pipeline and then one velocity-Verlet step on identical inputs agree
     with the reference core (oracle/_ref, all host cores; the C restatement
     where it was not built) for every atom: rho, dF, forces within 1e-10
-    (forces relative to max(|f|, 1 eV/A)), positions bit-exact after the
-    step, energies within 1e-10 plus the serial-sum bound."""
+    (forces relative to max(|f|, 1 eV/A)), positions within 1e-12 A after
+    the step, energies within 1e-10 plus the serial-sum bound."""
     from oracle import oracle
     from paper_2107_07866_b200.workloads import CONFIGS
     w = CONFIGS[cfg]
@@ -132,7 +132,9 @@ def test_config45_thermal_step_identical_inputs(cuda, tables, cfg):
     sr, sd = ref.state(), dev.state()
     for k in ("kinetic", "pair", "embedding"):
         assert abs(sd[k] - sr[k]) <= tol * abs(sr[k]), (k, sd[k], sr[k])
-    slots_parity(ref.store(), dev.download(), pos_tol=0.0)
+    # positions after the drift carry the forces' rounding-level differences
+    # (dt^2 hk df ~ 1e-13 A), like test_full_size's configs 2 and 3
+    slots_parity(ref.store(), dev.download(), pos_tol=1e-12)
 
 
 # ------------------------------------------------------------------ config 3
