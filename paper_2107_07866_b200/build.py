@@ -9,6 +9,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libcascade_b200.so")
+AB_LIB = os.path.join(HERE, "libcascade_b200_ab.so")
 SOURCES = ["host.cpp", "eam_kernels.cu", "store_kernels.cu", "capi.cu", "peak.cu", "slab.cu", "comm.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr",
@@ -32,10 +33,13 @@ def stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not stale():
+def build(force: bool = False, verbose: bool = False, ab: bool = False) -> str:
+    """ab: the experiment build (-DCBX_AB, the A/B environment switches live)
+    into libcascade_b200_ab.so, loaded with CBX_LIB=<path>"""
+    out = AB_LIB if ab else LIB
+    if not ab and not force and not stale():
         return LIB
-    cmd = [nvcc()] + ARCH + FLAGS + ["-shared", "-o", LIB] + \
+    cmd = [nvcc()] + ARCH + FLAGS + (["-DCBX_AB"] if ab else []) + ["-shared", "-o", out] + \
         [os.path.join(CSRC, s) for s in SOURCES]
     r = subprocess.run(cmd, capture_output=True, text=True)
     log = os.path.join(HERE, "build.log")
@@ -46,8 +50,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         raise RuntimeError(f"nvcc failed (see {log})")
     if verbose:
         sys.stderr.write(r.stderr)
-    return LIB
+    return out
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    print(build(force="--force" in sys.argv, verbose=True, ab="--ab" in sys.argv))

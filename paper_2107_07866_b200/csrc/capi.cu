@@ -29,6 +29,7 @@ struct cbx_ctx {
   DevStatus hst{};
   unsigned long long* d_defects = nullptr;
   std::vector<void*> allocs;
+  std::vector<cudaTextureObject_t> textures;
   cudaGraphExec_t step_graph = nullptr;
   // single-step calls (cbx_step(dt, 1), the Simulation::step loop) use a
   // graph that completes the step itself: no pending kick or sums to flush
@@ -63,6 +64,7 @@ struct cbx_ctx {
   uint64_t launches = 0;
   int n_ghost = 0;
   bool fast_ok = true;
+  bool fp32_density = false;  // compressed density records in use (local fp32 guard held)
   bool mask_valid = false;
   bool clash_rho_zero = false;  // the last clash-image pass zeroed the records' rho
   bool clash_f_zero = false;    // the last embed pass zeroed the records' forces
@@ -355,7 +357,7 @@ bool has_transport(const cbx_ctx* c) { return c->comm != nullptr || c->p2p; }
 // the RHO / FRC exchanges fused into the passes (peer memory, Newton-3,
 // neighbours' accumulators mapped); CBX_P2P_FUSED=0 keeps the staged exchanges
 bool rev_fused(const cbx_ctx* c) {
-  static const bool on = !getenv("CBX_P2P_FUSED") || atoi(getenv("CBX_P2P_FUSED"));
+  static const bool on = ab_flag("CBX_P2P_FUSED", 1) != 0;
   return on && c->p2p && c->rev_mapped && !c->fused_off && c->mode == CBX_STENCIL_NEWTON3;
 }
 
@@ -508,21 +510,14 @@ void seq_slab_eval(cbx_ctx* c) {
 // defer the StepState finalize of a step into the next step's first kernel
 // (fixed dt only: with adaptive dt the next kick needs the reduced max speed)
 bool want_defer(const cbx_ctx* c) {
-  static const bool on = [] {
-    const char* e = std::getenv("CBX_DEFER_FIN");
-    return e ? std::atoi(e) != 0 : true;
-  }();
+  static const bool on = ab_flag("CBX_DEFER_FIN", 1) != 0;
   return on && !has_transport(c) && !c->hst.adaptive && !c->single;
 }
 // merge the second half kick of a step into the next step's kick/drift
 // (one pass over v and f less per step): fixed dt, single box, the Newton-3
 // mask-replay passes (the density pass's clash blocks run the pending sums)
 bool want_merge(const cbx_ctx* c) {
-  static const bool on = [] {
-    const char* e = std::getenv("CBX_MERGE_KICK");
-    static const char* d = std::getenv("CBX_DENSITY_SMEM");
-    return (e ? std::atoi(e) != 0 : true) && !(d && !std::atoi(d));
-  }();
+  static const bool on = ab_flag("CBX_MERGE_KICK", 1) && ab_flag("CBX_DENSITY_SMEM", 1);
   return on && want_defer(c) && c->mode == CBX_STENCIL_NEWTON3 && c->P.pmask != nullptr;
 }
 
@@ -532,12 +527,9 @@ void seq_step(cbx_ctx* c) {
     return;
   }
   c->mask_valid = false;
-  // timing experiment only (CBX_SKIP bit mask, results invalid): leave a
-  // phase out of the step to measure its marginal cost inside the graph
-  static const int skip = [] {
-    const char* e = std::getenv("CBX_SKIP");
-    return e ? std::atoi(e) : 0;
-  }();
+  // timing experiment of the A/B build only (CBX_SKIP bit mask, results
+  // invalid): leave a phase out of the step to measure its marginal cost
+  static const int skip = ab_flag("CBX_SKIP", 0);
   ev_mark(c, 0);
   const bool zacc = c->mode != CBX_STENCIL_FULL;  // single box: no remote halo sites
   // kick, drift, hash pass 1 and the slot images in one launch; hash pass 2
@@ -947,52 +939,66 @@ void setup_fast(cbx_ctx* c) {
   P.fd.nseg = n;
   P.ff = P.fd;
   P.ff.rec = dff;
-  // compressed force records: the cubic coefficient (the t^3 h^3 term, ~1e-6
-  // of the linear one at the BASELINE spacing) rounded to fp32 moves z, z'
-  // and rho' by < 1e-13 of their scale; used only when that bound holds
-  P.ffc = nullptr;
-  if (c->fast_ok) {
-    double mz = 0, mq = 0, ez = 0, eq = 0;
+  // force-table chunks for the shared-memory window (fp64: a rigorous bound
+  // on fp32 cubic terms -- 3 |dA| ih / r per pair with the table's largest
+  // |F'| -- exceeds the 1e-10 force tolerance over the window for the
+  // BASELINE table, so the force records stay fp64) and the texture view of
+  // the full 64-byte records
+  {
+    std::vector<double> fz(4 * (n + 1)), fzc(2 * (n + 1)), fqc(n + 3, 0.0);
     for (int i = 0; i <= n; ++i) {
       const double* r = &ff[8 * i];
-      mz = std::max(mz, std::max(std::fabs(r[2]), std::fabs(r[3])));
-      mq = std::max(mq, std::max(std::fabs(r[6]), std::fabs(r[7])));
-      ez = std::max(ez, std::fabs(r[0] - (double)(float)r[0]));
-      eq = std::max(eq, std::fabs(r[4] - (double)(float)r[4]));
+      for (int k = 0; k < 4; ++k) fz[4 * i + k] = r[k];
+      fzc[2 * i] = r[2];
+      fzc[2 * i + 1] = r[3];
+      fqc[i] = r[6];
     }
-    const char* nc = std::getenv("CBX_NO_FP32A");
-    if (3.0 * ez <= 1e-13 * mz && 3.0 * eq <= 1e-13 * mq && !(nc && std::atoi(nc))) {
-      std::vector<double> fc(6 * (n + 1));
-      for (int i = 0; i <= n; ++i) {
-        const double* r = &ff[8 * i];
-        double* o = &fc[6 * i];
-        o[0] = r[1];
-        o[1] = r[2];
-        o[2] = r[3];
-        o[3] = r[5];
-        o[4] = r[6];
-        const float a2[2] = {(float)r[0], (float)r[4]};
-        std::memcpy(&o[5], a2, 8);
-      }
-      double* dfc = c->alloc<double>(fc.size());
-      cuda_check(cudaMemcpy(dfc, fc.data(), fc.size() * 8, cudaMemcpyHostToDevice), "fast table");
-      P.ffc = dfc;
-    }
+    auto up = [&](const std::vector<double>& v) {
+      double* d = c->alloc<double>(v.size());
+      cuda_check(cudaMemcpy(d, v.data(), v.size() * 8, cudaMemcpyHostToDevice), "fast table");
+      return d;
+    };
+    P.ffz = up(fz);
+    P.ffzc = up(fzc);
+    P.ffqc = up(fqc);
+    cudaResourceDesc rd{};
+    rd.resType = cudaResourceTypeLinear;
+    rd.res.linear.devPtr = const_cast<double*>(P.ff.rec);
+    rd.res.linear.desc = cudaCreateChannelDesc<int4>();
+    rd.res.linear.sizeInBytes = ff.size() * sizeof(double);
+    cudaTextureDesc td{};
+    td.readMode = cudaReadModeElementType;
+    cudaTextureObject_t tex = 0;
+    cuda_check(cudaCreateTextureObject(&tex, &rd, &td, nullptr), "force table texture");
+    P.tex_ff = (unsigned long long)tex;
+    c->textures.push_back(tex);
   }
-  // compressed density records for the density pass: the cubic and quadratic
-  // coefficients (~1e-9 and ~1e-6 of rho at the BASELINE spacing) in fp32
-  // move a pair's rho by < 1e-12 of the table's scale (a per-atom rho-bar by
-  // a few 1e-12 against the 1e-10 tolerance); used only when that holds
+  // compressed density records for the density pass: [D C] in fp64, the
+  // cubic and quadratic coefficients A, B (~1e-9 and ~1e-6 of rho at the
+  // BASELINE spacing) in fp32.  Local guard over the staged window (the only
+  // records the compressed path reads; pairs below it use the fp64 records):
+  // for every segment, the fp32 rounding of A and B moves rho(s) by at most
+  // kRhoRel of the smallest |rho| the segment can take (|D| - |C| - |B| - |A|,
+  // required > 0), so each pair's rho is within kRhoRel relative; rho terms
+  // of one sign add up with the same relative bound on every rho-bar (1e-12
+  // against the 1e-10 tolerance).  A table failing it anywhere in the window
+  // (steep or sign-changing rho) keeps the 32-byte fp64 records.
   P.fdc = nullptr;
+  c->fp32_density = false;
   {
-    double md = 0, ea = 0;
-    for (int i = 0; i <= n; ++i) {
+    constexpr double kRhoRel = 1e-12;
+    const int lo = dens_window_lo_cmp(n);
+    bool ok = true;
+    int sign = 0;
+    for (int i = lo; i <= n && ok; ++i) {
       const double* r = &fd[4 * i];
-      md = std::max(md, std::max(std::fabs(r[2]), std::fabs(r[3])));
-      ea = std::max(ea, std::fabs(r[0] - (double)(float)r[0]) + std::fabs(r[1] - (double)(float)r[1]));
+      const double ea = std::fabs(r[0] - (double)(float)r[0]) + std::fabs(r[1] - (double)(float)r[1]);
+      const double m = std::fabs(r[3]) - std::fabs(r[2]) - std::fabs(r[1]) - std::fabs(r[0]);
+      const int sg = r[3] > 0.0 ? 1 : -1;
+      if (!sign) sign = sg;
+      ok = m > 0.0 && sg == sign && ea <= kRhoRel * m;
     }
-    const char* nc = std::getenv("CBX_NO_FP32_DENSITY");
-    if (ea <= 1e-12 * md && !(nc && std::atoi(nc))) {
+    if (ok && !ab_flag("CBX_NO_FP32_DENSITY", 0)) {
       std::vector<double> dc(3 * (n + 1) + 2);  // + 16 bytes: the bulk copy rounds up
       for (int i = 0; i <= n; ++i) {
         const double* r = &fd[4 * i];
@@ -1004,6 +1010,18 @@ void setup_fast(cbx_ctx* c) {
       double* ddc = c->alloc<double>(dc.size());
       cuda_check(cudaMemcpy(ddc, dc.data(), dc.size() * 8, cudaMemcpyHostToDevice), "fast table");
       P.fdc = ddc;
+      c->fp32_density = true;
+      cudaResourceDesc rd{};
+      rd.resType = cudaResourceTypeLinear;
+      rd.res.linear.devPtr = ddc;
+      rd.res.linear.desc = cudaCreateChannelDesc<int4>();
+      rd.res.linear.sizeInBytes = 16 * (size_t)(n + 1);
+      cudaTextureDesc td{};
+      td.readMode = cudaReadModeElementType;
+      cudaTextureObject_t tex = 0;
+      cuda_check(cudaCreateTextureObject(&tex, &rd, &td, nullptr), "density table texture");
+      P.tex_fd = (unsigned long long)tex;
+      c->textures.push_back(tex);
     }
   }
   // embedding F(rho), same normalisation (its own grid)
@@ -1405,15 +1423,13 @@ static cbx_status create_impl(const cbx_box* box, const cbx_potential* pot,
     c->d_rem_base = c->alloc<int>(2);
     {  // the Wigner-Seitz ball of a BCC site: every other site is >= sqrt(3)/2 a0 away
       const double r = (std::sqrt(3.0) / 4.0 - 1e-6) * G.a0;
-      const char* fh = std::getenv("CBX_FAST_HASH");
-      P.hash_r2 = (fh && !std::atoi(fh)) ? 0.0 : r * r;
+      P.hash_r2 = ab_flag("CBX_FAST_HASH", 1) ? r * r : 0.0;
     }
     {
       const int maxn = std::max(std::max(fd[0].size(), fd[1].size()), std::max(hd[0].size(), hd[1].size()));
-      const char* nm = std::getenv("CBX_NOMASK");
       c->mem_cat = CBX_MEM_SLOTS;
-      P.pmask = maxn <= 126 && !(nm && std::atoi(nm)) ? c->alloc<unsigned long long>(2 * S)
-                                                       : nullptr;
+      P.pmask = maxn <= 126 && !ab_flag("CBX_NOMASK", 0) ? c->alloc<unsigned long long>(2 * S)
+                                                         : nullptr;
     }
 
     c->mem_cat = CBX_MEM_REDUCTION;
@@ -1462,6 +1478,7 @@ CBX_API void cbx_destroy(cbx_ctx* c) {
   for (void* p : c->p2p_opened) cudaIpcCloseMemHandle(p);
   if (c->p2p_region) cudaFree(c->p2p_region);
   if (c->stream) cudaStreamSynchronize(c->stream);
+  for (cudaTextureObject_t t : c->textures) cudaDestroyTextureObject(t);
   for (void* p : c->allocs) cudaFree(p);
   if (c->flush_buf) cudaFree(c->flush_buf);
   for (auto& e : c->ev)
@@ -2258,10 +2275,11 @@ CBX_API cbx_status cbx_bench_phases(cbx_ctx* c, int on) {
 CBX_API cbx_status cbx_describe(cbx_ctx* c, char* buf, long n) {
   return guarded(c, [&] {
     std::snprintf(buf, n,
-                  "{\"stencil\": %d, \"fast_ok\": %d, "
+                  "{\"stencil\": %d, \"fast_ok\": %d, \"fp32_density\": %d, "
+                  "\"force_table\": %d, "
                   "\"pair_mask\": %d, \"slots\": %lld, \"ghost_sites\": %d, "
                   "\"clash_capacity\": %d, \"band_A2\": %.3e, \"sm_count\": %d}",
-                  c->mode, (int)c->fast_ok,
+                  c->mode, (int)c->fast_ok, (int)c->fp32_density, force_table_mode(),
                   (int)(c->P.pmask != nullptr), c->S, c->n_ghost, c->P.cap_clash, c->band,
                   [] {
                     int d = 0, n = 0;

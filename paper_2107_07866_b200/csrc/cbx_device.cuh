@@ -112,6 +112,16 @@ struct RevHalo {
   int on;
 };
 
+// records of the density spline staged in shared memory by the density pass
+// (x 32 B = 105,600 B; x 24 B compressed), and the first staged record of the
+// compressed window: even, so the fp32 [A B] pairs (8 B each) start 16-byte
+// aligned for the bulk copy (host: the fp32 guard covers exactly this window)
+constexpr int kDensTabRecords = 3300;
+__host__ __device__ __forceinline__ int dens_window_lo_cmp(int nseg) {
+  const int lo = nseg + 2 - kDensTabRecords;
+  return ((lo > 0 ? lo : 0) + 1) & ~1;
+}
+
 struct KP {
   Geo G;
   RevHalo rev;
@@ -120,10 +130,13 @@ struct KP {
   float4* uf;      // fp32 shadow (x, y, z, owner-or--1) for the candidate filter
   int* work;       // persistent-kernel work counters (zeroed per launch)
   FastTab fd, ff;  // density / force fast tables
-  // force table with the cubic coefficients in fp32, 48-byte records
-  // [zB zC zD qB qC (zA,qA as two floats)]; null when a table's cubic terms
-  // are too large for the fp32 bound (setup_fast)
-  const double* ffc;
+  // force-table chunks staged in shared memory by the force pass (fp64):
+  // [zA zB zC zD] per record (32 B); [zC zD] (16 B) and qC (8 B) per record
+  // (split-3); the full 64-byte records ff.rec are also bound to the texture
+  // tex_ff (int4 texels, 4 per record) for the chunks fetched through TEX
+  const double *ffz, *ffzc, *ffqc;
+  unsigned long long tex_ff;  // cudaTextureObject_t
+  unsigned long long tex_fd;  // the compressed density records' [D C] (int4 texels)
   // compressed density records: [D C] (16 B) then, after the last record,
   // [A B as fp32] (8 B) per record; null when the fp32 rounding bound fails
   const double* fdc;
@@ -317,6 +330,7 @@ void launch_clash_density(const KP& P, cudaStream_t s);
 // literal: the reference arithmetic of spline_eval (stencil mode 2)
 void launch_embed(const KP& P, cudaStream_t s, bool literal = false);
 bool launch_force(const KP& P, int mode, cudaStream_t s);
+int force_table_mode();  // the force pass's table source (kTabSplit, ...)
 void launch_clash_force(const KP& P, cudaStream_t s);
 // zero_acc: clear the interior sites' rho / force accumulators as well;
 // images: write each site's ghost images too (the step path, no ghost fill)

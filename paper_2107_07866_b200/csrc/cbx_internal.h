@@ -12,6 +12,7 @@
 
 #include <cstdint>
 #include <cmath>
+#include <cstdlib>
 
 #if defined(__CUDACC__)
 #define CBX_HD __host__ __device__ __forceinline__
@@ -20,6 +21,20 @@
 #endif
 
 namespace cbx {
+
+// A/B switches of the experiment build (nvcc -DCBX_AB): read from the
+// environment there (each restores an earlier design for a same-box
+// comparison); the release library compiles every one to its default, so no
+// environment variable can change its physics, layout or timing.
+inline int ab_flag(const char* name, int dflt) {
+#ifdef CBX_AB
+  const char* e = std::getenv(name);
+  return e ? std::atoi(e) : dflt;
+#else
+  (void)name;
+  return dflt;
+#endif
+}
 
 // Invalid (vacant) slots carry this x/y/z so that any distance to them
 // exceeds every cutoff: no separate validity load in the stencil loops.

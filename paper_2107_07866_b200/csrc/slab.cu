@@ -512,10 +512,7 @@ void launch_remote_df(const KP& P, cudaStream_t s) { k_remote_df<<<8, 256, 0, s>
 
 int launch_p2p_exchange(const KP& P, const P2PLinks& L, int kind, long long gs_lo,
                         long long gs_hi, int* rem_base, cudaStream_t s) {
-  static const int fused = [] {
-    const char* e = getenv("CBX_P2P_SPLIT");
-    return e ? !atoi(e) : 1;
-  }();
+  static const int fused = !ab_flag("CBX_P2P_SPLIT", 0);
   if (fused) {
     static int cap = 0;
     if (!cap) {  // co-resident blocks of the fused kernel

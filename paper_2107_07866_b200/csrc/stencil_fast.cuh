@@ -145,10 +145,32 @@ __device__ __forceinline__ float2 lds_f2(unsigned a) {
   asm("ld.shared.v2.f32 {%0,%1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(a));
   return v;
 }
+__device__ __forceinline__ double lds_d(unsigned a) {
+  double v;
+  asm("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+  return v;
+}
 __device__ __forceinline__ int lds_i(unsigned a) {
   int v;
   asm("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(a));
   return v;
+}
+
+// 16 bytes of the 64-byte force record `seg` (chunk c: 0 [zA zB], 1 [zC zD],
+// 2 [qA qB], 3 [qC qD]) through the texture path: the TEX data pipe runs
+// beside the LSU pipe that serves the shared-memory table, the partner
+// gathers and the reductions (tabbench: 2 LDS.128 + 1 TLD per lane cost what
+// 2 LDS.128 alone cost)
+__device__ __forceinline__ double2 tex_chunk(unsigned long long tex, int seg, int c) {
+  const int4 q = tex1Dfetch<int4>((cudaTextureObject_t)tex, 4 * seg + c);
+  return make_double2(__hiloint2double(q.y, q.x), __hiloint2double(q.w, q.z));
+}
+
+// 16-byte record i of a table bound to a texture of int4 texels (the
+// density pass's [D C] records)
+__device__ __forceinline__ double2 tex_rec16(unsigned long long tex, int i) {
+  const int4 q = tex1Dfetch<int4>((cudaTextureObject_t)tex, i);
+  return make_double2(__hiloint2double(q.y, q.x), __hiloint2double(q.w, q.z));
 }
 
 // ---- bulk (TMA engine) staging of a constant table into shared memory:
@@ -217,7 +239,10 @@ __device__ __forceinline__ double skin_density(const KP& P, KP* Pp, int par, int
 // 16-byte slot 2 i + (c ^ ((i >> 2) & 1)) (8 distinct bank quads for random i)
 __device__ __forceinline__ int smem_slot32(int i, int c) { return 2 * i + (c ^ ((i >> 2) & 1)); }
 
-template <bool FULL, int B, bool SMEM = false, bool REV = false, bool CMPD = false>
+// CMPD: 0 the fp64 32-byte records of the window in shared memory; 1 the
+// compressed records ([D C] fp64 + [A B] fp32) in shared memory; 2 compressed,
+// [D C] by texture fetch (TEX pipe) and [A B] in shared memory (LSU pipe)
+template <bool FULL, int B, bool SMEM = false, bool REV = false, int CMPD = 0>
 __device__ __forceinline__ void density_site(const KP& P, KP* Pp, int par, int d, bool live,
                                              unsigned tb = 0, int seg_lo = 0,
                                              bool rev_here = true, bool deep = false,
@@ -236,8 +261,64 @@ __device__ __forceinline__ void density_site(const KP& P, KP* Pp, int par, int d
   const double lo = P.cut2_lo, g2 = P.guard_r2;
   double acc = 0.0;
   unsigned long long m0 = 0, m1 = 0;
-  // inner shells: direct fp64 gather, batched; the common case is decided
-  // by one compare, the near-cutoff / guard cases drop to decide()
+  // inner shells: direct fp64 gather; the common case is decided by one
+  // compare, the near-cutoff / guard cases drop to decide().  B == 1 (the
+  // shared-memory kernels): software-pipelined, the next candidate's gather
+  // is in flight while the current one's table lookup and RED run
+  if constexpr (B == 1) {
+    int jn = d + offs[0];
+    double qx, qy, qz, qw;
+    ld256(pdf + jn, qx, qy, qz, qw);
+    int tn = deep ? jn : __ldg(tgt + jn);
+#pragma unroll 1
+    for (int k = 0; k < nin; ++k) {
+      const int j = jn, t = tn;
+      const double px = qx, py = qy, pz = qz;
+      if (k + 1 < nin) {
+        jn = d + offs[k + 1];
+        ld256(pdf + jn, qx, qy, qz, qw);
+        tn = deep ? jn : __ldg(tgt + jn);
+      }
+      const double dx = xsub(ax, px), dy = xsub(ay, py), dz = xsub(az, pz);
+      const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+      bool in = r2 <= lo && r2 >= g2;
+      if (!in && r2 <= P.cut2_hi) {
+        const int st = decide<FULL>(P, par, k, j, ax, ay, az, px, py, pz, dx, dy, dz, r2);
+        if (st == 1) {
+          in = true;
+        } else if (st == 2) {
+          m1 |= kGuardBit;
+          acc += guard_rho(Pp, d, j, t, dx, dy, dz, FULL);
+        }
+      }
+      if (in) {
+        double sv;
+        const int sg = seg_index(P.fd, r2 * rsqrt_nr(r2), sv);
+        const int li = sg - seg_lo;
+        double tA, tB, tC, tD;
+        if (SMEM && CMPD && li >= 0) {  // [D C] and the fp32 pair [A B]
+          const double2 dc = CMPD == 2 ? tex_rec16(P.tex_fd, sg) : lds2(tb + 16 * li);
+          const float2 ab = lds_f2(tb8 + 8 * li);
+          tA = (double)ab.x;
+          tB = (double)ab.y;
+          tC = dc.y;
+          tD = dc.x;
+        } else if (SMEM && li >= 0) {
+          const double2 c0 = lds2(tb + 16 * smem_slot32(li, 0)), c1 = lds2(tb + 16 * smem_slot32(li, 1));
+          tA = c0.x;
+          tB = c0.y;
+          tC = c1.x;
+          tD = c1.y;
+        } else {
+          ld256(P.fd.rec + 4 * (size_t)sg, tA, tB, tC, tD);
+        }
+        const double rho = fma(fma(fma(tA, sv, tB), sv, tC), sv, tD);
+        acc += rho;
+        if (!FULL) red_add(REV && rev_here ? acc_ptr_up(P, t, -1) : P.rho + t, rho);
+        set_bit(m0, m1, k);
+      }
+    }
+  } else
   for (int k0 = 0; k0 < nin; k0 += B) {
     int j[B], t[B], seg[B];
     bool in[B];
@@ -282,7 +363,7 @@ __device__ __forceinline__ void density_site(const KP& P, KP* Pp, int par, int d
         const int li = seg[b] - seg_lo;
         if (SMEM && CMPD) {  // [D C] and the fp32 pair [A B]
           const int lc = max(li, 0);
-          const double2 dc = lds2(tb + 16 * lc);
+          const double2 dc = CMPD == 2 ? tex_rec16(P.tex_fd, lc + seg_lo) : lds2(tb + 16 * lc);
           const float2 ab = lds_f2(tb8 + 8 * lc);
           tA[b] = (double)ab.x;
           tB[b] = (double)ab.y;
@@ -501,14 +582,25 @@ __device__ __forceinline__ unsigned long long warp_or64(unsigned long long m) {
   return ((unsigned long long)hi << 32) | lo;
 }
 
+// Force-table sources (template TB of the force pass):
+//   kTabSmem64: the 64-byte records of the window in shared memory, 4 LDS.128
+//   kTabSplit:  [zA zB][zC zD] of the window in shared memory (2 LDS.128),
+//               [qA qB][qC qD] by texture fetches (2 TLD) -- the LSU and TEX
+//               pipes share the lookups
+//   kTabSplit3: [zC zD] (LDS.128) + qC (LDS.64) in shared memory, [zA zB]
+//               [qA qB] by texture fetches
+// Pairs below the window (cascade cores) fetch every chunk by texture.
+constexpr int kTabSmem64 = 0, kTabSplit = 2, kTabSplit3 = 3;
+constexpr int kTabSmemBytes[4] = {64, 0, 32, 24};
+
 // force pass, lean variant: one pair per iteration, no batching, so the
 // register footprint allows 6-8 resident CTAs per SM (latency hidden by
 // warps instead of by in-thread batching).  Warp-uniform union sweep.
-template <bool FULL, bool SMEM, bool CMP = false, bool REV = false>
+template <bool FULL, int TB, bool REV = false, bool PIPE = false>
 __device__ __forceinline__ double force_site_lean(const KP& P, KP* Pp, int par, int d,
                                                   bool live, unsigned tb = 0,
                                                   int seg_lo = 0, bool rev_here = false,
-                                                  bool deep = false) {
+                                                  bool deep = false, unsigned tb8 = 0) {
   const double4* __restrict__ pdf = P.pdf;
   const int* __restrict__ tgt = P.tgt;
   const long long S = P.S;
@@ -531,8 +623,11 @@ __device__ __forceinline__ double force_site_lean(const KP& P, KP* Pp, int par, 
   const double ih = P.ff.ih;
   const double r2_idle = P.cut2_lo;
   double fx = 0.0, fy = 0.0, fz = 0.0, e = 0.0;
-  // one 32-bit word of the mask at a time: the warp walks the union of its
-  // lanes' words (warp-uniform offset), lanes without the bit idle
+  // the warp walks the union of its lanes' masks (warp-uniform offset, lanes
+  // without the bit idle), one 32-bit word at a time.  PIPE: software-
+  // pipelined, the partner gather of the next pair is in flight while the
+  // current pair's table lookups and arithmetic run
+  if constexpr (!PIPE) {
 #pragma unroll 1
   for (int wd = 0; wd < 4; ++wd) {
     const unsigned long long mw = wd < 2 ? m0 : m1;
@@ -553,27 +648,41 @@ __device__ __forceinline__ double force_site_lean(const KP& P, KP* Pp, int par, 
       const double ri = rsqrt_nr(r2);
       double sb;
       const int seg = seg_index(P.ff, r2 * ri, sb);
-      double zA, zB, zC, zD, qA, qB, qC, qD;
+      double zA, zB, zC, zD, qA, qB, qC;
       const int li = seg - seg_lo;
       const int lc = max(li, 0);
-      if (SMEM && CMP) {  // 48-byte record, cubic terms in fp32
-        const unsigned a = tb + 48 * lc;
-        const double2 c0 = lds2(a), c1 = lds2(a + 16), c2 = lds2(a + 32);
-        zB = c0.x; zC = c0.y; zD = c1.x; qB = c1.y; qC = c2.x;
-        const unsigned long long ab = (unsigned long long)__double_as_longlong(c2.y);
-        zA = (double)__uint_as_float((unsigned)ab);
-        qA = (double)__uint_as_float((unsigned)(ab >> 32));
-        qD = 0.0;
-      } else if (SMEM) {
+      if (TB == kTabSplit) {
+        const double2 q0 = tex_chunk(P.tex_ff, seg, 2), q1 = tex_chunk(P.tex_ff, seg, 3);
+        qA = q0.x; qB = q0.y; qC = q1.x;
+        if (li >= 0) {
+          const double2 c0 = lds2(tb + 32 * lc), c1 = lds2(tb + 32 * lc + 16);
+          zA = c0.x; zB = c0.y; zC = c1.x; zD = c1.y;
+        } else {
+          const double2 c0 = tex_chunk(P.tex_ff, seg, 0), c1 = tex_chunk(P.tex_ff, seg, 1);
+          zA = c0.x; zB = c0.y; zC = c1.x; zD = c1.y;
+        }
+      } else if (TB == kTabSplit3) {
+        const double2 c0 = tex_chunk(P.tex_ff, seg, 0), q0 = tex_chunk(P.tex_ff, seg, 2);
+        zA = c0.x; zB = c0.y; qA = q0.x; qB = q0.y;
+        if (li >= 0) {
+          const double2 c1 = lds2(tb + 16 * lc);
+          zC = c1.x; zD = c1.y;
+          qC = lds_d(tb8 + 8 * lc);
+        } else {
+          const double2 c1 = tex_chunk(P.tex_ff, seg, 1), q1 = tex_chunk(P.tex_ff, seg, 3);
+          zC = c1.x; zD = c1.y; qC = q1.x;
+        }
+      } else {
         const double2 c0 = lds2(tb + 16 * smem_slot(lc, 0)), c1 = lds2(tb + 16 * smem_slot(lc, 1));
         const double2 c2 = lds2(tb + 16 * smem_slot(lc, 2)), c3 = lds2(tb + 16 * smem_slot(lc, 3));
         zA = c0.x; zB = c0.y; zC = c1.x; zD = c1.y;
-        qA = c2.x; qB = c2.y; qC = c3.x; qD = c3.y;
-      }
-      if (!SMEM || li < 0) {  // below the window (cascade cores): global record
-        const double* rec = P.ff.rec + 8 * (size_t)seg;
-        ld256(rec, zA, zB, zC, zD);
-        ld256(rec + 4, qA, qB, qC, qD);
+        qA = c2.x; qB = c2.y; qC = c3.x;
+        if (li < 0) {  // below the window (cascade cores): global record
+          const double* rec = P.ff.rec + 8 * (size_t)seg;
+          double qD;
+          ld256(rec, zA, zB, zC, zD);
+          ld256(rec + 4, qA, qB, qC, qD);
+        }
       }
       const double s15 = 1.5 * sb, s2 = sb + sb;
       const double z = fma(fma(fma(zA, sb, zB), sb, zC), sb, zD);
@@ -605,7 +714,113 @@ __device__ __forceinline__ double force_site_lean(const KP& P, KP* Pp, int par, 
           }
         }
       }
+  }
+  }
+  } else {
+  unsigned long long u0 = warp_or64(m0), u1 = warp_or64(m1);
+  int bit = -1;
+  auto pop = [&]() {
+    if (u0) {
+      bit = __ffsll(u0) - 1;
+      u0 &= u0 - 1;
+    } else if (u1) {
+      bit = 63 + __ffsll(u1);
+      u1 &= u1 - 1;
+    } else {
+      bit = -1;
     }
+  };
+  bool nv = false;
+  int nj = d, nt = d;
+  double npx = 0, npy = 0, npz = 0, npw = 0;
+  auto fetch = [&]() {
+    nv = ((bit < 64 ? m0 >> bit : m1 >> (bit - 64)) & 1) != 0;
+    nj = nv ? d + lds_i(s_offs + 4 * bit) : d;
+    ld256(pdf + nj, npx, npy, npz, npw);
+    nt = deep ? nj : __ldg(tgt + nj);
+  };
+  pop();
+  if (bit >= 0) fetch();
+#pragma unroll 1
+  while (bit >= 0) {
+    const bool v = nv;
+    const int t = nt;
+    const double px = npx, py = npy, pz = npz, pw = npw;
+    pop();
+    if (bit >= 0) fetch();
+    const double dx = xsub(ax, px), dy = xsub(ay, py), dz = xsub(az, pz);
+    double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+    r2 = v ? r2 : r2_idle;
+    const double ri = rsqrt_nr(r2);
+    double sb;
+    const int seg = seg_index(P.ff, r2 * ri, sb);
+    double zA, zB, zC, zD, qA, qB, qC;
+    const int li = seg - seg_lo;
+    const int lc = max(li, 0);
+    if (TB == kTabSplit) {
+      const double2 q0 = tex_chunk(P.tex_ff, seg, 2), q1 = tex_chunk(P.tex_ff, seg, 3);
+      qA = q0.x; qB = q0.y; qC = q1.x;
+      if (li >= 0) {
+        const double2 c0 = lds2(tb + 32 * lc), c1 = lds2(tb + 32 * lc + 16);
+        zA = c0.x; zB = c0.y; zC = c1.x; zD = c1.y;
+      } else {
+        const double2 c0 = tex_chunk(P.tex_ff, seg, 0), c1 = tex_chunk(P.tex_ff, seg, 1);
+        zA = c0.x; zB = c0.y; zC = c1.x; zD = c1.y;
+      }
+    } else if (TB == kTabSplit3) {
+      const double2 c0 = tex_chunk(P.tex_ff, seg, 0), q0 = tex_chunk(P.tex_ff, seg, 2);
+      zA = c0.x; zB = c0.y; qA = q0.x; qB = q0.y;
+      if (li >= 0) {
+        const double2 c1 = lds2(tb + 16 * lc);
+        zC = c1.x; zD = c1.y;
+        qC = lds_d(tb8 + 8 * lc);
+      } else {
+        const double2 c1 = tex_chunk(P.tex_ff, seg, 1), q1 = tex_chunk(P.tex_ff, seg, 3);
+        zC = c1.x; zD = c1.y; qC = q1.x;
+      }
+    } else {
+      const double2 c0 = lds2(tb + 16 * smem_slot(lc, 0)), c1 = lds2(tb + 16 * smem_slot(lc, 1));
+      const double2 c2 = lds2(tb + 16 * smem_slot(lc, 2)), c3 = lds2(tb + 16 * smem_slot(lc, 3));
+      zA = c0.x; zB = c0.y; zC = c1.x; zD = c1.y;
+      qA = c2.x; qB = c2.y; qC = c3.x;
+      if (li < 0) {  // below the window (cascade cores): global record
+        const double* rec = P.ff.rec + 8 * (size_t)seg;
+        double qD;
+        ld256(rec, zA, zB, zC, zD);
+        ld256(rec + 4, qA, qB, qC, qD);
+      }
+    }
+    const double s15 = 1.5 * sb, s2 = sb + sb;
+    const double z = fma(fma(fma(zA, sb, zB), sb, zC), sb, zD);
+    const double zs = fma(fma(zA, s15, zB), s2, zC);  // dz/ds
+    const double ps = fma(fma(qA, s15, qB), s2, qC);  // drho/ds
+    const double phi = v ? z * ri : 0.0;
+    const double dphi = fma(zs, ih, -phi) * ri;
+    const double mfp = v ? fma((adf + pw) * ps, ih, dphi) * ri : 0.0;
+    const double qx = mfp * dx, qy = mfp * dy, qz = mfp * dz;
+    fx -= qx;
+    fy -= qy;
+    fz -= qz;
+    if (FULL) {
+      e = fma(0.5, phi, e);
+    } else {
+      e += phi;
+      if (v) {
+        if (REV && rev_here) {  // warp-uniform: a plane within reach of the halo
+          double* f = acc_ptr_up(P, t, 0);
+          const long long st = (int)t - ((int)t >= (int)P.G.NC ? (int)P.G.NC : 0) >= (int)P.rev.hi
+                                   ? P.rev.S[1] : S;
+          red_add(f, qx);
+          red_add(f + st, qy);
+          red_add(f + 2 * st, qz);
+        } else {
+          red_add(&P.frc[t], qx);
+          red_add(&P.frc[S + t], qy);
+          red_add(&P.frc[2 * S + t], qz);
+        }
+      }
+    }
+  }
   }
   const int* offs = FULL ? c_full[par] : c_half[par];
   if (guard) {  // the guard pairs skipped by the density pass's mask
@@ -742,8 +957,8 @@ __device__ __forceinline__ int next_unit(int* s_ctr, int group, int nsb, int nu,
 // density pass with the upper rho-spline window in shared memory (32-byte
 // records): NT threads = NT/128 groups of 4 warps, one CTA per SM; B = 1
 // (one candidate per iteration) keeps the thread at 64 registers
-constexpr int kDensTabRecords = 3300;  // x 32 B = 105,600 B
-template <bool FULL, int B, int NT, bool REV = false, bool CMPD = false>
+// kDensTabRecords (cbx_device.cuh): records of the staged window
+template <bool FULL, int B, int NT, bool REV = false, int CMPD = 0>
 __global__ void __launch_bounds__(NT, 1) k_density_smem(KP P, int nsb) {
   if (blockIdx.x >= nsb) {
     pdl_wait();
@@ -762,13 +977,13 @@ __global__ void __launch_bounds__(NT, 1) k_density_smem(KP P, int nsb) {
   if (threadIdx.x == 0) s_ctr = 0;
   // an even first record: the fp32 [A B] pairs (8 bytes each) are then
   // 16-byte aligned for the bulk copy
-  const int seg_lo = CMPD ? (max(0, nseg + 2 - kDensTabRecords) + 1) & ~1
-                          : max(0, nseg + 1 - kDensTabRecords);
+  const int seg_lo = CMPD ? dens_window_lo_cmp(nseg) : max(0, nseg + 1 - kDensTabRecords);
   const int nrec = nseg + 1 - seg_lo;
   const double2* src = reinterpret_cast<const double2*>(P.fd.rec + 4 * (size_t)seg_lo);
   // the constant table is staged while the predecessor drains (PDL)
   // 24-byte records: [D C] 16-byte slots, then the fp32 [A B] pairs
-  double2* T8 = T + kDensTabRecords;  // byte offset 16 x kDensTabRecords
+  // (CMPD 2: only the [A B] pairs are staged, from offset 0)
+  double2* T8 = CMPD == 2 ? T : T + kDensTabRecords;  // byte offset 16 x kDensTabRecords
   __shared__ __align__(8) unsigned long long s_mbar;
   if (CMPD) {  // two bulk copies ([A B] rounded up to 16 bytes: the table is padded)
     const int N1 = nseg + 1;
@@ -776,8 +991,12 @@ __global__ void __launch_bounds__(NT, 1) k_density_smem(KP P, int nsb) {
     if (threadIdx.x == 0) {
       const unsigned b16 = 16u * nrec, b8 = (8u * nrec + 15u) & ~15u;
       mbar_init(mb);
-      mbar_expect_tx(mb, b16 + b8);
-      bulk_stage(smem_addr(T), P.fdc + 2 * (size_t)seg_lo, b16, mb);
+      if (CMPD == 2) {
+        mbar_expect_tx(mb, b8);
+      } else {
+        mbar_expect_tx(mb, b16 + b8);
+        bulk_stage(smem_addr(T), P.fdc + 2 * (size_t)seg_lo, b16, mb);
+      }
       bulk_stage(smem_addr(T8), P.fdc + 2 * (size_t)N1 + seg_lo, b8, mb);
     }
   } else {
@@ -843,11 +1062,20 @@ __global__ void __launch_bounds__(128, 4) k_force_fast(KP P) {
 }
 
 // lean force pass with the upper spline window (records [seg_lo, nseg])
-// in shared memory: 1024 threads, one CTA per SM, 8 groups of 4 warps each
-// on their own brick.  Pairs below the window (cascade cores) read global.
-constexpr int kLeanTabRecords = 3300;  // x 64 B = 211,200 B (x 48 B = 158,400 B compressed)
+// in shared memory (TB: which 16-byte chunks, see kTabSmem64 / kTabSplit /
+// kTabSplit3): 1024 threads, one CTA per SM, 8 groups of 4 warps each on
+// their own unit.  Pairs below the window (cascade cores) read global /
+// texture records.
+constexpr int kLeanTabRecords = 3300;  // x 64 B = 211,200 B; split: x 32 B / x 24 B
 
-template <bool FULL, int NT, bool CMP, bool REV = false>
+__host__ __device__ __forceinline__ int force_window_lo(int nseg, int tb) {
+  const int lo = nseg + 1 - kLeanTabRecords;
+  // the split-3 window starts on an even record: its 8-byte qC array is then
+  // 16-byte aligned for the bulk copy
+  return tb == kTabSplit3 ? ((lo > 0 ? lo : 0) + 1) & ~1 : (lo > 0 ? lo : 0);
+}
+
+template <bool FULL, int NT, int TB, bool REV = false, bool PIPE = false>
 __global__ void __launch_bounds__(NT, 1) k_force_lean_smem(KP P, int nsb) {
   if (blockIdx.x >= nsb) {
     pdl_wait();
@@ -866,15 +1094,23 @@ __global__ void __launch_bounds__(NT, 1) k_force_lean_smem(KP P, int nsb) {
   double2* T = reinterpret_cast<double2*>(smem_tab);
   const int nseg = P.ff.nseg;  // records 0..nseg (padded)
   if (threadIdx.x == 0) s_ctr = 0;
-  const int seg_lo = max(0, nseg + 1 - kLeanTabRecords);
+  const int seg_lo = force_window_lo(nseg, TB);
   const int nrec = nseg + 1 - seg_lo;
+  const unsigned tb8 = smem_addr(T) + 16u * kLeanTabRecords;  // split-3: the qC array
   __shared__ __align__(8) unsigned long long s_mbar;
-  if (CMP) {  // 48-byte records, three 16-byte chunks each, in order: one bulk copy
+  if (TB != kTabSmem64) {  // bulk copies of the window's chunks, one thread
     if (threadIdx.x == 0) {
       const unsigned mb = smem_addr(&s_mbar);
       mbar_init(mb);
-      mbar_expect_tx(mb, 48u * nrec);
-      bulk_stage(smem_addr(T), P.ffc + 6 * (size_t)seg_lo, 48u * nrec, mb);
+      if (TB == kTabSplit) {
+        mbar_expect_tx(mb, 32u * nrec);
+        bulk_stage(smem_addr(T), P.ffz + 4 * (size_t)seg_lo, 32u * nrec, mb);
+      } else {
+        const unsigned b8 = (8u * nrec + 15u) & ~15u;
+        mbar_expect_tx(mb, 16u * nrec + b8);
+        bulk_stage(smem_addr(T), P.ffzc + 2 * (size_t)seg_lo, 16u * nrec, mb);
+        bulk_stage(tb8, P.ffqc + seg_lo, b8, mb);
+      }
     }
   } else {
     const double2* src = reinterpret_cast<const double2*>(P.ff.rec + 8 * (size_t)seg_lo);
@@ -887,7 +1123,7 @@ __global__ void __launch_bounds__(NT, 1) k_force_lean_smem(KP P, int nsb) {
     g_soffs[par][k] = k < n ? (FULL ? c_full[par][k] : c_half[par][k]) : 0;
   }
   __syncthreads();  // the barrier's initialisation is visible
-  if (CMP) mbar_wait0(smem_addr(&s_mbar));
+  if (TB != kTabSmem64) mbar_wait0(smem_addr(&s_mbar));
   pdl_wait();
   pdl_trigger();
   if (P.mark_k2 && blockIdx.x == 0 && threadIdx.x == 0) P.st->k2_pending = 1;  // merged kick
@@ -905,9 +1141,9 @@ __global__ void __launch_bounds__(NT, 1) k_force_lean_smem(KP P, int nsb) {
     const bool live = unit_cell(G, u, lane, w, c);
     const bool deep = live && unit_deep(G, u, lane, w, FULL);
     for (int par = 0; par < 2; ++par)
-      e += force_site_lean<FULL, true, CMP, REV>(P, P.dself, par, live ? (int)(par * G.NC + c) : 0,
-                                                 live, smem_addr(T), seg_lo, near_halo(G, u, w),
-                                                 deep);
+      e += force_site_lean<FULL, TB, REV, PIPE>(P, P.dself, par, live ? (int)(par * G.NC + c) : 0,
+                                          live, smem_addr(T), seg_lo, near_halo(G, u, w), deep,
+                                          tb8);
   }
   block_partial<NT>(e, P.part_pair);
 }
@@ -940,58 +1176,52 @@ static int sm_count() {
   return sms;
 }
 
+// the shared-memory density pass for one table layout (CMPD, see
+// density_site); returns true when the clash-record pass ran in the launch
+template <int CMPD>
+bool launch_density_smem(const KP& P, int mode, cudaStream_t s) {
+  const size_t bytes = (size_t)kDensTabRecords * (CMPD == 2 ? 8 : CMPD == 1 ? 24 : 32);
+  static bool attr = false;
+  if (!attr) {
+    for (const void* k : {(const void*)k_density_smem<false, 1, 1024, false, CMPD>,
+                          (const void*)k_density_smem<true, 1, 1024, false, CMPD>,
+                          (const void*)k_density_smem<false, 1, 1024, true, CMPD>,
+                          (const void*)k_density_smem<false, 1, 896, false, CMPD>})
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    attr = true;
+  }
+  const int g = max(1, min(sm_count(), unit_count(P.G)));
+  static const int nt_env = ab_flag("CBX_DENSITY_NT", 0);  // overrides the rule below
+  // at most 7 units per CTA: 7 groups with 72 registers (as the force pass)
+  const int nt = nt_env ? nt_env : ((unit_count(P.G) + g - 1) / g <= 7 ? 896 : 1024);
+  if (nt == 896 && !mode && !P.rev.on) {
+    launch_pdl(k_density_smem<false, 1, 896, false, CMPD>, g + 4, 896, bytes, s, P, g);
+    return true;
+  }
+  if (mode) launch_pdl(k_density_smem<true, 1, 1024, false, CMPD>, g, 1024, bytes, s, P, g);
+  else if (P.rev.on)
+    launch_pdl(k_density_smem<false, 1, 1024, true, CMPD>, g + 4, 1024, bytes, s, P, g);
+  else launch_pdl(k_density_smem<false, 1, 1024, false, CMPD>, g + 4, 1024, bytes, s, P, g);
+  return !mode;
+}
+int density_table_mode(const KP& P) {
+  // compressed records when the local fp32 guard held (P.fdc), with [D C]
+  // through the texture path by default (CBX_DENSITY_TAB=1: all in smem)
+  static const int tm = ab_flag("CBX_DENSITY_TAB", 2);
+  return P.fdc ? tm : 0;
+}
+
 // density pass: the lean 1024-thread kernel with the rho-spline window in
-// shared memory (default); CBX_DENSITY_SMEM=0 selects the 128-thread batched
-// kernel.  Returns true when the clash-record pass ran in the same launch.
+// shared memory (default); CBX_DENSITY_SMEM=0 (A/B build) selects the
+// 128-thread batched kernel.  Returns true when the clash-record pass ran in
+// the same launch.
 bool launch_density_fast(const KP& P, int mode, int grid, cudaStream_t s) {
-  static const int dsm = [] {
-    const char* e = getenv("CBX_DENSITY_SMEM");
-    return e ? atoi(e) : 1;
-  }();
+  static const int dsm = ab_flag("CBX_DENSITY_SMEM", 1);
   if (dsm) {
-    const bool cmp = P.fdc != nullptr;  // 24-byte records (fp32 cubic/quadratic terms)
-    const size_t bytes = (size_t)kDensTabRecords * (cmp ? 24 : 32);
-    static bool attr = false;
-    if (!attr) {
-      for (const void* k : {(const void*)k_density_smem<false, 1, 1024>,
-                            (const void*)k_density_smem<true, 1, 1024>,
-                            (const void*)k_density_smem<false, 1, 1024, true>,
-                            (const void*)k_density_smem<false, 1, 1024, false, true>,
-                            (const void*)k_density_smem<true, 1, 1024, false, true>,
-                            (const void*)k_density_smem<false, 1, 1024, true, true>})
-        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)((size_t)kDensTabRecords * 32));
-      attr = true;
-    }
-    const int g = max(1, min(sm_count(), unit_count(P.G)));
-    static const int nt_env = [] {  // CBX_DENSITY_NT overrides the rule below
-      const char* e = getenv("CBX_DENSITY_NT");
-      return e ? atoi(e) : 0;
-    }();
-    // at most 7 units per CTA: 7 groups with 72 registers (as the force pass)
-    const int nt = nt_env ? nt_env : ((unit_count(P.G) + g - 1) / g <= 7 ? 896 : 1024);
-    if (cmp && nt == 896 && !mode && !P.rev.on) {
-      static bool attr896 = false;
-      if (!attr896) {
-        cudaFuncSetAttribute((const void*)k_density_smem<false, 1, 896, false, true>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)((size_t)kDensTabRecords * 32));
-        attr896 = true;
-      }
-      launch_pdl(k_density_smem<false, 1, 896, false, true>, g + 4, 896, bytes, s, P, g);
-      return true;
-    }
-    if (cmp) {
-      if (mode) launch_pdl(k_density_smem<true, 1, 1024, false, true>, g, 1024, bytes, s, P, g);
-      else if (P.rev.on)
-        launch_pdl(k_density_smem<false, 1, 1024, true, true>, g + 4, 1024, bytes, s, P, g);
-      else launch_pdl(k_density_smem<false, 1, 1024, false, true>, g + 4, 1024, bytes, s, P, g);
-      return !mode;
-    }
-    if (mode) launch_pdl(k_density_smem<true, 1, 1024>, g, 1024, bytes, s, P, g);
-    else if (P.rev.on) launch_pdl(k_density_smem<false, 1, 1024, true>, g + 4, 1024, bytes, s, P, g);
-    else launch_pdl(k_density_smem<false, 1, 1024>, g + 4, 1024, bytes, s, P, g);
-    return !mode;
+    const int tm = density_table_mode(P);
+    if (tm == 2) return launch_density_smem<2>(P, mode, s);
+    if (tm == 1) return launch_density_smem<1>(P, mode, s);
+    return launch_density_smem<0>(P, mode, s);
   }
   const int ex = mode ? 0 : kClashBlocks128;  // fused clash pass (Newton-3)
   if (mode) k_density_fast<true, 4, 4><<<grid, 128, 0, s>>>(P, grid);
@@ -1000,50 +1230,55 @@ bool launch_density_fast(const KP& P, int mode, int grid, cudaStream_t s) {
 }
 
 // force pass: with a valid pair mask the lean mask-replay kernel with the
-// force spline window in shared memory; otherwise (positions changed since
-// the density pass) the decision path, which re-derives every pair
-template <bool CMP>
+// force spline window in shared memory (+ texture chunks); otherwise
+// (positions changed since the density pass) the decision path, which
+// re-derives every pair
+template <int TB, bool PIPE>
 void launch_force_lean(const KP& P, int mode, cudaStream_t s) {
-  const size_t bytes = (size_t)kLeanTabRecords * (CMP ? 48 : 64);
+  const size_t bytes = (size_t)kLeanTabRecords * kTabSmemBytes[TB] + 16;
   static bool attr = false;
   if (!attr) {
     // default carveout: the driver takes the smallest shared-memory split
     // that fits the table and leaves the rest of the SM's 256 KB as L1 for
-    // the partner gathers (an explicit carveout hint measured 10 % slower)
-    for (const void* k : {(const void*)k_force_lean_smem<false, 1024, CMP>,
-                          (const void*)k_force_lean_smem<true, 1024, CMP>,
-                          (const void*)k_force_lean_smem<false, 1024, CMP, true>})
+    // the partner gathers and the texture fetches
+    for (const void* k : {(const void*)k_force_lean_smem<false, 1024, TB, false, PIPE>,
+                          (const void*)k_force_lean_smem<true, 1024, TB, false, PIPE>,
+                          (const void*)k_force_lean_smem<false, 1024, TB, true, PIPE>,
+                          (const void*)k_force_lean_smem<false, 896, TB, false, PIPE>})
       cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
     attr = true;
   }
   const int g = max(1, min(sm_count(), unit_count(P.G)));
   // at most 7 units per CTA (one wave, e.g. config 2): 7 groups of 128
   // threads with 72 registers instead of 8 with 64 (CBX_FORCE_NT overrides)
-  static const int nt_env = [] {
-    const char* e = getenv("CBX_FORCE_NT");
-    return e ? atoi(e) : 0;
-  }();
-  const int g0 = max(1, min(sm_count(), unit_count(P.G)));
-  const int nt = nt_env ? nt_env : ((unit_count(P.G) + g0 - 1) / g0 <= 7 ? 896 : 1024);
+  static const int nt_env = ab_flag("CBX_FORCE_NT", 0);
+  const int nt = nt_env ? nt_env : ((unit_count(P.G) + g - 1) / g <= 7 ? 896 : 1024);
   if (nt == 896 && !mode && !P.rev.on) {
-    static bool attr896 = false;
-    if (!attr896) {
-      cudaFuncSetAttribute((const void*)k_force_lean_smem<false, 896, CMP>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-      attr896 = true;
-    }
-    launch_pdl(k_force_lean_smem<false, 896, CMP>, g + 4, 896, bytes, s, P, g);
+    launch_pdl(k_force_lean_smem<false, 896, TB, false, PIPE>, g + 4, 896, bytes, s, P, g);
     return;
   }
-  if (mode) launch_pdl(k_force_lean_smem<true, 1024, CMP>, g, 1024, bytes, s, P, g);
+  if (mode) launch_pdl(k_force_lean_smem<true, 1024, TB, false, PIPE>, g, 1024, bytes, s, P, g);
   else if (P.rev.on)
-    launch_pdl(k_force_lean_smem<false, 1024, CMP, true>, g + 4, 1024, bytes, s, P, g);
-  else launch_pdl(k_force_lean_smem<false, 1024, CMP>, g + 4, 1024, bytes, s, P, g);
+    launch_pdl(k_force_lean_smem<false, 1024, TB, true, PIPE>, g + 4, 1024, bytes, s, P, g);
+  else launch_pdl(k_force_lean_smem<false, 1024, TB, false, PIPE>, g + 4, 1024, bytes, s, P, g);
+}
+int force_table_mode() {
+  static const int tb = ab_flag("CBX_FORCE_TAB", kTabSplit3);
+  return tb;
 }
 bool launch_force_fast(const KP& P, int mode, int grid, cudaStream_t s) {
   if (P.use_mask) {
-    if (P.ffc) launch_force_lean<true>(P, mode, s);
-    else launch_force_lean<false>(P, mode, s);
+    const int tb = force_table_mode();
+    static const bool pipe = ab_flag("CBX_FORCE_PIPE", 0) != 0;
+    if (pipe) {
+      if (tb == kTabSplit3) launch_force_lean<kTabSplit3, true>(P, mode, s);
+      else if (tb == kTabSmem64) launch_force_lean<kTabSmem64, true>(P, mode, s);
+      else launch_force_lean<kTabSplit, true>(P, mode, s);
+    } else {
+      if (tb == kTabSplit3) launch_force_lean<kTabSplit3, false>(P, mode, s);
+      else if (tb == kTabSmem64) launch_force_lean<kTabSmem64, false>(P, mode, s);
+      else launch_force_lean<kTabSplit, false>(P, mode, s);
+    }
     return !mode;
   }
   if (mode) k_force_fast<true, 2><<<grid, 128, 0, s>>>(P);

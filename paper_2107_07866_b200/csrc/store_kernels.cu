@@ -999,10 +999,7 @@ static int site_wave(const KP& P, int per_sm) {
     cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
     return n;
   }();
-  static const int wave = [] {  // CBX_SITE_WAVE=0: one block per virtual block
-    const char* e = std::getenv("CBX_SITE_WAVE");
-    return e ? std::atoi(e) : 1;
-  }();
+  static const int wave = ab_flag("CBX_SITE_WAVE", 1);  // 0: one block per virtual block
   return wave ? std::max(1, std::min(eam_blocks(P), per_sm * sms)) : eam_blocks(P);
 }
 void launch_kick_drift(const KP& P, int move, cudaStream_t s, int zero_acc, int images,
@@ -1053,10 +1050,7 @@ void launch_count_defects(const KP& P, unsigned long long* out, cudaStream_t s) 
 
 namespace cbx {
 bool pdl_enabled() {
-  static const bool on = [] {
-    const char* e = getenv("CBX_PDL");
-    return e ? atoi(e) != 0 : true;
-  }();
+  static const bool on = ab_flag("CBX_PDL", 1) != 0;
   return on;
 }
 }  // namespace cbx

@@ -48,13 +48,15 @@ def _block(vals):
 
 def write_baseline_table(path: str, rho_max: float = BASELINE_RHO_MAX, nrho: int = 5000,
                          nr: int = 5000, cutoff: float = 5.6, a0: float = 2.855,
-                         mass: float = 55.845) -> str:
-    phi, rho, emb = baseline_functions()
+                         mass: float = 55.845, rho_k: float = 2.0) -> str:
+    """rho_k: the density decay constant (2.0 = BASELINE; tests use steeper
+    tables to exercise the fp64 fallback of the compressed records)"""
+    phi, rho, emb = baseline_functions(rho_k=rho_k)
     drho = rho_max / (nrho - 1)
     dr = cutoff / nr
     lines = [
-        "BASELINE synthetic EAM: phi=Morse(D=0.4,alpha=1.4,r0=2.85); rho=exp(-2(r-2.48)); "
-        "F=-sqrt(rho); rho_max=%.17g\n" % rho_max,
+        "BASELINE synthetic EAM: phi=Morse(D=0.4,alpha=1.4,r0=2.85); rho=exp(-%g(r-2.48)); "
+        "F=-sqrt(rho); rho_max=%.17g\n" % (rho_k, rho_max),
         "26 %.17g %.17g bcc\n" % (mass, a0),
         "%d %.17g %d %.17g %.17g\n" % (nrho, drho, nr, dr, cutoff),
     ]

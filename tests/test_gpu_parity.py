@@ -312,6 +312,27 @@ def test_cascade_clash_and_defects(cuda, tables, stencil):
     assert saw_clash
 
 
+@pytest.mark.parametrize("rho_k,compressed", [(2.0, 1), (12.0, 0)])
+def test_density_record_guard_local(cuda, tables, tmp_path, rho_k, compressed):
+    """The compressed density records (fp32 A, B) are used only where the
+    local guard of setup_fast holds: for every segment of the staged window
+    the fp32 rounding moves rho(s) by <= 1e-12 of the smallest |rho| the
+    segment takes.  BASELINE (rho = exp(-2(r - 2.48))): 1.5e-13, compressed;
+    a steep rho = exp(-12(r - 2.48)): 5.4e-12, so the fp64 records are kept.
+    Both meet the 1e-10 parity with the oracle."""
+    from oracle import oracle
+    from paper_2107_07866_b200.potential import write_baseline_table
+    path = (tables["baseline"] if rho_k == 2.0 else
+            write_baseline_table(str(tmp_path / "steep.eam"), rho_k=rho_k))
+    ref = oracle.Sim(path, box=(8, 8, 8), temperature=600.0, seed=5)
+    ref.step(1e-3, 3)
+    dev = device_for(ref, path)
+    assert dev.describe()["fp32_density"] == compressed
+    e_ref, e_dev = ref.eval_forces(), dev.eval_forces()
+    assert close(e_ref[0], e_dev[0]) and close(e_ref[1], e_dev[1]), (e_ref, e_dev)
+    assert_store_parity(ref.store(), dev.download(), what=f"rho_k={rho_k}")
+
+
 def test_overlap_halts_multi_step_call(cuda, tables):
     """An overlap found in step 2 of a 5-step call (fixed dt: merged kicks and
     deferred StepState sums) ends the call at step 2 like the reference's
