@@ -247,8 +247,15 @@ CBX_API long cbx_run_series(cbx_ctx* ctx, double* t, long* defects);
 /* thermostat_rescale (sim.cpp:188-221) toward `temperature` in the band of
  * `boundary_cells` cells at the faces (0 = whole box); then measure */
 CBX_API cbx_status cbx_thermostat_rescale(cbx_ctx* ctx, double temperature, long boundary_cells);
-/* write_snapshot / write_timeseries (analysis.cpp:77-116) */
+/* write_snapshot / write_timeseries (analysis.cpp:77-116).  cbx_write_snapshot
+ * returns once the file is written; cbx_write_snapshot_async packs the store on
+ * the device, copies it to page-locked memory on a side stream and writes the
+ * file from a host thread while later calls (steps) proceed -- two in flight,
+ * a third waits for the oldest; cbx_snapshot_wait joins them (the first write
+ * error is returned).  cbx_run uses the asynchronous form. */
 CBX_API cbx_status cbx_write_snapshot(cbx_ctx* ctx, const char* path, double t_ps);
+CBX_API cbx_status cbx_write_snapshot_async(cbx_ctx* ctx, const char* path, double t_ps);
+CBX_API cbx_status cbx_snapshot_wait(cbx_ctx* ctx);
 CBX_API cbx_status cbx_write_timeseries(const char* path, long n, const double* t,
                                         const long* defects);
 

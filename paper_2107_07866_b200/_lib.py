@@ -163,6 +163,8 @@ SIGNATURES = [
     ("cbx_run_series", C.c_long, [_P, C.POINTER(C.c_double), C.POINTER(C.c_long)]),
     ("cbx_thermostat_rescale", C.c_int, [_P, _D, C.c_long]),
     ("cbx_write_snapshot", C.c_int, [_P, C.c_char_p, _D]),
+    ("cbx_write_snapshot_async", C.c_int, [_P, C.c_char_p, _D]),
+    ("cbx_snapshot_wait", C.c_int, [_P]),
     ("cbx_write_timeseries", C.c_int, [C.c_char_p, C.c_long, C.POINTER(C.c_double),
                                        C.POINTER(C.c_long)]),
     ("cbx_nccl_unique_id", C.c_int, [_P, C.c_long]),

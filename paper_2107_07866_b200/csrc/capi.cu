@@ -6,6 +6,7 @@
 #include <cstring>
 #include <memory>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "cbx_comm.h"
@@ -13,6 +14,17 @@
 #include "cbx_host.h"
 
 using namespace cbx;
+
+// one in-flight snapshot: device pack buffer, page-locked host copy, the
+// events of the pack and the D2H, and the thread formatting the file
+struct SnapSlot {
+  double4* dev = nullptr;
+  double4* host = nullptr;
+  size_t bytes = 0;
+  cudaEvent_t packed = nullptr, copied = nullptr;
+  std::thread writer;
+  std::string error;
+};
 
 struct cbx_ctx {
   int device = 0;
@@ -30,6 +42,9 @@ struct cbx_ctx {
   unsigned long long* d_defects = nullptr;
   std::vector<void*> allocs;
   std::vector<cudaTextureObject_t> textures;
+  SnapSlot snap[2];  // asynchronous snapshots (double-buffered)
+  int snap_next = 0;
+  cudaStream_t snap_stream = nullptr;
   cudaGraphExec_t step_graph = nullptr;
   // single-step calls (cbx_step(dt, 1), the Simulation::step loop) use a
   // graph that completes the step itself: no pending kick or sums to flush
@@ -1470,6 +1485,14 @@ CBX_API void cbx_destroy(cbx_ctx* c) {
   if (c->device >= 0 && c->device < 64 && g_const_owner[c->device] == c)
     g_const_owner[c->device] = nullptr;
   drop_graph(c);
+  for (SnapSlot& q : c->snap) {
+    if (q.writer.joinable()) q.writer.join();
+    if (q.dev) cudaFree(q.dev);
+    if (q.host) cudaFreeHost(q.host);
+    if (q.packed) cudaEventDestroy(q.packed);
+    if (q.copied) cudaEventDestroy(q.copied);
+  }
+  if (c->snap_stream) cudaStreamDestroy(c->snap_stream);
   if (c->comm) {
     if (c->stream) cudaStreamSynchronize(c->stream);
     nccl().comm_destroy(c->comm);
@@ -1895,70 +1918,158 @@ CBX_API cbx_status cbx_thermostat_rescale(cbx_ctx* c, double temperature, long b
   return rc == CBX_OK ? cbx_measure(c) : rc;
 }
 
+// ---- write_snapshot (analysis.cpp:90-116) with an asynchronous D2H --------
+// The interior slots in reference-id order (for_each_interior_id,
+// store.h:82-93) and the clash records in (key, bucket) order are packed on
+// the step stream into a device buffer (one 32-byte entry per site / record:
+// x, y, z, tag bits; vacant sites and ghost records flagged by x = 1e30),
+// copied to page-locked host memory on a side stream, and formatted by a host
+// thread -- while the following steps run.  Two slots: a third snapshot waits
+// for the oldest.  The file text equals the reference's byte for byte.
+namespace {
+__global__ void k_snapshot_pack(KP P, double4* out, long long ni, int n_clash) {
+  const Geo& G = P.G;
+  const long long row = 2ll * G.bx;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < ni + n_clash;
+       e += (long long)gridDim.x * blockDim.x) {
+    if (e < ni) {
+      const long long r = e / row, x2 = e - r * row;
+      const int y = (int)(r % G.by), z = (int)(r / G.by);
+      const int par = (int)(x2 & 1);
+      const long long d =
+          par * G.NC + cell_of((int)(x2 >> 1) + G.g, y + G.g, z + G.g, G);
+      const double4 p = P.pdf[d];
+      out[e] = make_double4(p.x, p.y, p.z, __longlong_as_double((long long)P.tag[d]));
+    } else {
+      const int i = (int)(e - ni);
+      out[e] = make_double4(P.cl.gf[i] ? kVacant : P.cl.px[i], P.cl.py[i], P.cl.pz[i],
+                            __longlong_as_double((long long)P.cl.tag[i]));
+    }
+  }
+}
+
+// the reference's text from a packed snapshot (host side, any thread)
+bool format_snapshot(const char* path, const double4* e, long long ni, long nc, double t_ps,
+                     const cbx_box& box, const char* sym) {
+  long n_atoms = 0;
+  for (long long i = 0; i < ni + nc; ++i) n_atoms += e[i].x < kVacantTest;
+  std::FILE* f = std::fopen(path, "w");
+  if (!f) return false;
+  const double a0 = box.a0, shift = box.ghost_width * a0;
+  char tb[48];
+  std::snprintf(tb, sizeof tb, "%.9g", t_ps);  // csv_time (analysis.cpp:66-75)
+  if (!std::strpbrk(tb, ".eE") && std::strspn(tb, "-0123456789") == std::strlen(tb))
+    std::strcat(tb, ".0");
+  std::fprintf(f, "%ld\n", n_atoms);
+  std::fprintf(f,
+               "Lattice=\"%.10g 0 0 0 %.10g 0 0 0 %.10g\" "
+               "Properties=species:S:1:pos:R:3:tag:I:1 Time=%s\n",
+               box.box_x * a0, box.box_y * a0, box.box_z * a0, tb);
+  for (long long i = 0; i < ni + nc; ++i) {
+    if (!(e[i].x < kVacantTest)) continue;
+    unsigned long long tag;
+    std::memcpy(&tag, &e[i].w, sizeof tag);
+    std::fprintf(f, "%s %.10g %.10g %.10g %llu\n", sym, e[i].x - shift, e[i].y - shift,
+                 e[i].z - shift, tag);
+  }
+  const bool bad = std::ferror(f) != 0;
+  std::fclose(f);
+  return !bad;
+}
+
+// wait for snapshot slot k's writer; its error text, if any
+std::string snapshot_join(cbx_ctx* c, int k) {
+  SnapSlot& q = c->snap[k];
+  if (q.writer.joinable()) q.writer.join();
+  std::string e;
+  e.swap(q.error);
+  return e;
+}
+}  // namespace
+
+// pack + async D2H + background formatting of one snapshot
+void snapshot_async(cbx_ctx* c, const std::string& path, double t_ps) {
+  const Geo& G = c->G;
+  const long long ni = 2ll * G.bx * G.by * G.bz;
+  const int k = c->snap_next;
+  const std::string prev = snapshot_join(c, k);
+  if (!prev.empty()) raise(CBX_RUNTIME, prev);
+  SnapSlot& q = c->snap[k];
+  sync_status(c);  // n_clash, pending kicks
+  raise_device_error(c, false);
+  const int nc = c->hst.n_clash;
+  const size_t need = (size_t)(ni + nc) * sizeof(double4);
+  if (need > q.bytes) {
+    if (q.dev) cudaFree(q.dev);
+    if (q.host) cudaFreeHost(q.host);
+    q.dev = nullptr;
+    q.host = nullptr;
+    const size_t cap = (size_t)(ni + c->P.cap_clash) * sizeof(double4);
+    cuda_check(cudaMalloc(&q.dev, cap), "snapshot buffer");
+    cuda_check(cudaHostAlloc(&q.host, cap, cudaHostAllocDefault), "snapshot host buffer");
+    q.bytes = cap;
+  }
+  if (!c->snap_stream)
+    cuda_check(cudaStreamCreateWithFlags(&c->snap_stream, cudaStreamNonBlocking), "stream");
+  if (!q.packed) cuda_check(cudaEventCreateWithFlags(&q.packed, cudaEventDisableTiming), "event");
+  if (!q.copied) cuda_check(cudaEventCreateWithFlags(&q.copied, cudaEventDisableTiming), "event");
+  const long long n = ni + nc;
+  const int grid = (int)std::min<long long>((n + 255) / 256, 8 * 148);
+  k_snapshot_pack<<<grid, 256, 0, c->stream>>>(c->P, q.dev, ni, nc);
+  c->launches += 1;
+  cuda_check(cudaEventRecord(q.packed, c->stream), "event");
+  cuda_check(cudaStreamWaitEvent(c->snap_stream, q.packed, 0), "event");
+  cuda_check(cudaMemcpyAsync(q.host, q.dev, (size_t)n * sizeof(double4), cudaMemcpyDeviceToHost,
+                             c->snap_stream),
+             "snapshot D2H");
+  cuda_check(cudaEventRecord(q.copied, c->snap_stream), "event");
+  const unsigned z = (unsigned)c->pot.atomic_number;
+  const char* sym = z < sizeof(kSymbols) / sizeof(kSymbols[0]) ? kSymbols[z] : "X";
+  const int dev = c->device;
+  const cbx_box box = c->box;
+  q.writer = std::thread([&q, path, t_ps, ni, nc, box, sym, dev] {
+    cudaSetDevice(dev);
+    if (cudaEventSynchronize(q.copied) != cudaSuccess) {
+      q.error = "snapshot copy failed: " + path;
+      return;
+    }
+    if (!format_snapshot(path.c_str(), q.host, ni, nc, t_ps, box, sym))
+      q.error = "cannot write " + path;
+  });
+  c->snap_next ^= 1;
+}
+
+// every pending snapshot written (the first error raised)
+void snapshot_wait(cbx_ctx* c) {
+  std::string err;
+  for (int k = 0; k < 2; ++k) {
+    const std::string e = snapshot_join(c, k);
+    if (err.empty()) err = e;
+  }
+  if (!err.empty()) raise(CBX_RUNTIME, err);
+}
+
+CBX_API cbx_status cbx_write_snapshot_async(cbx_ctx* c, const char* path, double t_ps) {
+  return guarded(c, [&] {
+    cudaSetDevice(c->device);
+    require_box(c, "cbx_write_snapshot");
+    snapshot_async(c, path, t_ps);
+  });
+}
+
+CBX_API cbx_status cbx_snapshot_wait(cbx_ctx* c) {
+  return guarded(c, [&] { snapshot_wait(c); });
+}
+
 // write_snapshot (analysis.cpp:90-116): interior slots in id order, then the
-// interior clash records in (key, bucket) order, at time t_ps
+// interior clash records in (key, bucket) order, at time t_ps; returns once
+// the file is written
 CBX_API cbx_status cbx_write_snapshot(cbx_ctx* c, const char* path, double t_ps) {
   return guarded(c, [&] {
     cudaSetDevice(c->device);
     require_box(c, "cbx_write_snapshot");
-    const Geo& G = c->G;
-    const long long S = c->S;
-    std::vector<double> pos(3 * S);
-    std::vector<uint64_t> tag(S);
-    std::vector<unsigned char> valid(S), ghost(S);
-    cbx_store st{};
-    st.n_slots = S;
-    st.pos = pos.data();
-    st.tag = tag.data();
-    st.valid = valid.data();
-    st.ghost = ghost.data();
-    do_download(c, &st);  // counts the clash records
-    const long nc = st.n_clash;
-    std::vector<int64_t> ck(nc);
-    std::vector<double> cp(3 * nc);
-    std::vector<uint64_t> ct(nc);
-    std::vector<unsigned char> cg(nc);
-    st.clash_key = ck.data();
-    st.clash_pos = cp.data();
-    st.clash_tag = ct.data();
-    st.clash_ghost = cg.data();
-    if (nc) do_download(c, &st);
-    long n_atoms = 0;
-    for (long long id = 0; id < S; ++id) n_atoms += valid[id] && !ghost[id];
-    for (long i = 0; i < nc; ++i) n_atoms += !cg[i];
-    std::FILE* f = std::fopen(path, "w");
-    if (!f) raise(CBX_RUNTIME, std::string("cannot open ") + path + " for writing");
-    const double a0 = c->box.a0, shift = c->box.ghost_width * a0;
-    const unsigned z = (unsigned)c->pot.atomic_number;
-    const char* sym = z < sizeof(kSymbols) / sizeof(kSymbols[0]) ? kSymbols[z] : "X";
-    char tb[48];
-    std::snprintf(tb, sizeof tb, "%.9g", t_ps);  // csv_time (analysis.cpp:66-75)
-    if (!std::strpbrk(tb, ".eE") && std::strspn(tb, "-0123456789") == std::strlen(tb))
-      std::strcat(tb, ".0");
-    std::fprintf(f, "%ld\n", n_atoms);
-    std::fprintf(f,
-                 "Lattice=\"%.10g 0 0 0 %.10g 0 0 0 %.10g\" "
-                 "Properties=species:S:1:pos:R:3:tag:I:1 Time=%s\n",
-                 c->box.box_x * a0, c->box.box_y * a0, c->box.box_z * a0, tb);
-    const long long tx2 = 2ll * G.tx;
-    for (long z_ = G.g; z_ < G.g + G.bz; ++z_)  // for_each_interior_id (store.h:82-93)
-      for (long y = G.g; y < G.g + G.by; ++y) {
-        const long long row = ((long long)z_ * G.ty + y) * tx2;
-        for (long x = 2 * G.g; x < 2 * (G.g + G.bx); ++x) {
-          const long long id = row + x;
-          if (!valid[id] || ghost[id]) continue;
-          std::fprintf(f, "%s %.10g %.10g %.10g %llu\n", sym, pos[3 * id] - shift,
-                       pos[3 * id + 1] - shift, pos[3 * id + 2] - shift,
-                       (unsigned long long)tag[id]);
-        }
-      }
-    for (long i = 0; i < nc; ++i)
-      if (!cg[i])
-        std::fprintf(f, "%s %.10g %.10g %.10g %llu\n", sym, cp[3 * i] - shift,
-                     cp[3 * i + 1] - shift, cp[3 * i + 2] - shift, (unsigned long long)ct[i]);
-    const bool bad = std::ferror(f) != 0;
-    std::fclose(f);
-    if (bad) raise(CBX_RUNTIME, std::string("write failed: ") + path);
+    snapshot_async(c, path, t_ps);
+    snapshot_wait(c);
   });
 }
 
@@ -2022,7 +2133,9 @@ CBX_API cbx_status cbx_run(cbx_ctx* c, const cbx_run_spec* r, const char* log_pa
   auto snapshot = [&](const char* suffix) -> cbx_status {  // sim.cpp:279-282
     if (!nonempty(r->snapshot_prefix)) return CBX_OK;
     cbx_get_state(c, &st);
-    return cbx_write_snapshot(c, (std::string(r->snapshot_prefix) + suffix).c_str(), st.t);
+    // written in the background while the next steps run (cbx_snapshot_wait
+    // before cbx_run returns)
+    return cbx_write_snapshot_async(c, (std::string(r->snapshot_prefix) + suffix).c_str(), st.t);
   };
   auto log_line = [&]() {
     if (!log) return;
@@ -2047,6 +2160,7 @@ CBX_API cbx_status cbx_run(cbx_ctx* c, const cbx_run_spec* r, const char* log_pa
     const cbx_status e = cbx_step(c, -1.0, n, &st);
     if (e) {
       const std::string err = c->err;
+      cbx_snapshot_wait(c);
       if (nonempty(r->snapshot_prefix)) {
         cbx_get_state(c, &st);
         cbx_write_snapshot(c, (std::string(r->snapshot_prefix) + "_postmortem.xyz").c_str(),
@@ -2136,6 +2250,10 @@ CBX_API cbx_status cbx_run(cbx_ctx* c, const cbx_run_spec* r, const char* log_pa
       break;
     rc = snapshot("_final.xyz");
   } while (false);
+  {  // the background snapshot writers finish before the run returns
+    const cbx_status w = cbx_snapshot_wait(c);
+    if (!rc) rc = w;
+  }
   if (log && log != stdout) std::fclose(log);
   if (log == stdout) std::fflush(stdout);
   return rc;

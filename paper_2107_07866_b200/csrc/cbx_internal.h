@@ -80,6 +80,9 @@ struct Geo {
   // sh = 31 + ceil(log2 d), m = ceil(2^sh / d)); device site mapping
   unsigned long long mbx, mby;
   int sbx, sby;
+  // stencil-pass work units walk columns of strips along y when rows hold
+  // whole strips (unit_strip, stencil_fast.cuh); 0 keeps the row order
+  int col_units;
 };
 
 // exact floor(n / d) for 0 <= n < 2^31 from the constants of make_magic

@@ -250,6 +250,7 @@ Geo make_geo(const cbx_box& b) {
   };
   magic((unsigned)G.bx, G.mbx, G.sbx);
   magic((unsigned)G.by, G.mby, G.sby);
+  G.col_units = ab_flag("CBX_COL_UNITS", 1);
   return G;
 }
 

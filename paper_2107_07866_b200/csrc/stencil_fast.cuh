@@ -912,9 +912,25 @@ __host__ __device__ __forceinline__ int strip_count(const Geo& G) {
 __host__ __device__ __forceinline__ int unit_count(const Geo& G) {
   return strip_count(G) * ((G.bz + 3) / 4);
 }
-__device__ __forceinline__ bool unit_cell(const Geo& G, int u, int lane, int w, int& c) {
+// strip of unit u within its z block.  When rows hold whole strips
+// (bx % 32 == 0, e.g. configs 4 and 5) consecutive units walk down a column
+// of strips along y: a CTA's concurrent groups then share the partner rows
+// of a compact (36 x 11 x 6)-cell neighbourhood that fits L1 (row order
+// spans whole rows: a 5-row x 6-plane working set 3x the L1)
+__device__ __forceinline__ int unit_strip(const Geo& G, int u, int& zb) {
   const int ns = strip_count(G);
-  const int zb = u / ns, e = (u - zb * ns) * 32 + lane, cz = zb * 4 + w;
+  zb = u / ns;
+  const int r = u - zb * ns;
+  if (G.bx % 32 == 0 && G.col_units) {
+    const int xs = r / G.by, y = r - xs * G.by;
+    return y * (G.bx / 32) + xs;
+  }
+  return r;
+}
+__device__ __forceinline__ bool unit_cell(const Geo& G, int u, int lane, int w, int& c) {
+  int zb;
+  const int st = unit_strip(G, u, zb);
+  const int e = st * 32 + lane, cz = zb * 4 + w;
   const bool live = e < G.bx * G.by && cz < G.bz;
   const int cy = e / G.bx, cx = e - cy * G.bx;
   c = live ? (int)cell_of(cx + G.g, cy + G.g, cz + G.g, G) : 0;
@@ -926,8 +942,9 @@ __device__ __forceinline__ bool unit_cell(const Geo& G, int u, int lane, int w, 
 // rank the z-halo planes' owner is the site itself too (tgt, capi.cu), so
 // only x and y matter there.
 __device__ __forceinline__ bool unit_deep(const Geo& G, int u, int lane, int w, bool full) {
-  const int ns = strip_count(G);
-  const int zb = u / ns, e = (u - zb * ns) * 32 + lane, cz = zb * 4 + w;
+  int zb;
+  const int st = unit_strip(G, u, zb);
+  const int e = st * 32 + lane, cz = zb * 4 + w;
   const int cy = e / G.bx, cx = e - cy * G.bx;
   return cx >= G.g && cx < G.bx - G.g && cy >= G.g && cy < G.by - G.g &&
          (G.slab || (cz < G.bz - G.g && (!full || cz >= G.g)));
@@ -1205,9 +1222,10 @@ bool launch_density_smem(const KP& P, int mode, cudaStream_t s) {
   return !mode;
 }
 int density_table_mode(const KP& P) {
-  // compressed records when the local fp32 guard held (P.fdc), with [D C]
-  // through the texture path by default (CBX_DENSITY_TAB=1: all in smem)
-  static const int tm = ab_flag("CBX_DENSITY_TAB", 2);
+  // compressed records when the local fp32 guard held (P.fdc), all in
+  // shared memory (CBX_DENSITY_TAB=2: [D C] through the texture path -- the
+  // same time at config 5, its fetch latency sits on the pair's chain)
+  static const int tm = ab_flag("CBX_DENSITY_TAB", 1);
   return P.fdc ? tm : 0;
 }
 
@@ -1244,7 +1262,8 @@ void launch_force_lean(const KP& P, int mode, cudaStream_t s) {
     for (const void* k : {(const void*)k_force_lean_smem<false, 1024, TB, false, PIPE>,
                           (const void*)k_force_lean_smem<true, 1024, TB, false, PIPE>,
                           (const void*)k_force_lean_smem<false, 1024, TB, true, PIPE>,
-                          (const void*)k_force_lean_smem<false, 896, TB, false, PIPE>})
+                          (const void*)k_force_lean_smem<false, 896, TB, false, PIPE>,
+                          (const void*)k_force_lean_smem<false, 896, TB, true, PIPE>})
       cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
     attr = true;
   }
@@ -1252,9 +1271,13 @@ void launch_force_lean(const KP& P, int mode, cudaStream_t s) {
   // at most 7 units per CTA (one wave, e.g. config 2): 7 groups of 128
   // threads with 72 registers instead of 8 with 64 (CBX_FORCE_NT overrides)
   static const int nt_env = ab_flag("CBX_FORCE_NT", 0);
-  const int nt = nt_env ? nt_env : ((unit_count(P.G) + g - 1) / g <= 7 ? 896 : 1024);
-  if (nt == 896 && !mode && !P.rev.on) {
-    launch_pdl(k_force_lean_smem<false, 896, TB, false, PIPE>, g + 4, 896, bytes, s, P, g);
+  // 896 threads (72 registers, 28 warps) measured ahead of 1024 (64
+  // registers, spills) at config 5 too: 7.27 vs 7.38-7.54 ms
+  const int nt = nt_env ? nt_env : 896;
+  if (nt == 896 && !mode) {
+    if (P.rev.on)
+      launch_pdl(k_force_lean_smem<false, 896, TB, true, PIPE>, g + 4, 896, bytes, s, P, g);
+    else launch_pdl(k_force_lean_smem<false, 896, TB, false, PIPE>, g + 4, 896, bytes, s, P, g);
     return;
   }
   if (mode) launch_pdl(k_force_lean_smem<true, 1024, TB, false, PIPE>, g, 1024, bytes, s, P, g);

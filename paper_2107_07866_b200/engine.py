@@ -360,6 +360,14 @@ class DeviceStore:
         t = self.state()["t"] if t_ps is None else t_ps
         self._check(self.lib.cbx_write_snapshot(self.h, path.encode(), t))
 
+    def write_snapshot_async(self, path: str, t_ps: Optional[float] = None):
+        """pack now, copy and write in the background (snapshot_wait joins)"""
+        t = self.state()["t"] if t_ps is None else t_ps
+        self._check(self.lib.cbx_write_snapshot_async(self.h, path.encode(), t))
+
+    def snapshot_wait(self):
+        self._check(self.lib.cbx_snapshot_wait(self.h))
+
     def run(self, spec: "_lib.RunSpec", log_path: str = ""):
         self._spec = spec  # keep the strings alive
         self._check(self.lib.cbx_run(self.h, C.byref(spec), log_path.encode()))

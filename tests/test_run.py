@@ -214,3 +214,43 @@ def test_device_run_time_cap(cuda, tables):
     sim.run()
     assert sim.state["step"] == ref.state()["step"]
     assert np.array_equal(sim.series[1], ref.series()[1])
+
+
+@pytest.mark.gpu
+def test_async_snapshot_overlaps_steps(cuda, tables, tmp_path):
+    """cbx_write_snapshot_async (the run loop's snapshots, analysis.cpp:90-116):
+    the store is packed on the step stream, copied on a side stream and
+    written by a host thread while later steps run; the file holds the state
+    at the call, byte-identical to the synchronous writer's and to the
+    oracle's; two in flight, a third waits for the oldest"""
+    from oracle import oracle
+    from paper_2107_07866_b200 import DeviceStore, EamPotential
+    ref = oracle.Sim(tables["baseline"], box=(7, 6, 5), temperature=600.0, seed=11,
+                     pka_energy_kev=0.3, pka_site=(3, 3, 2))
+    ref.step(1e-3, 3)
+    ref.inject_pka()
+    ref.step(1e-4, 30)  # off-lattice records in the clash list
+    dims, a0, g = ref.box
+    pot = EamPotential.load(tables["baseline"])
+    a = DeviceStore((*dims, a0, g), pot)
+    b = DeviceStore((*dims, a0, g), pot)
+    for d in (a, b):
+        d.upload(ref.store())
+        d.set_state(ref.state())
+    t = ref.state()["t"]
+    ref.write_snapshot(str(tmp_path / "o.xyz"))
+    a.write_snapshot(str(tmp_path / "a.xyz"), t)
+    b.write_snapshot_async(str(tmp_path / "b1.xyz"), t)
+    b.step(1e-4, 5)
+    b.write_snapshot_async(str(tmp_path / "b2.xyz"))
+    b.step(1e-4, 5)
+    b.write_snapshot_async(str(tmp_path / "b3.xyz"))  # waits for b1's writer
+    b.snapshot_wait()
+    assert filecmp.cmp(tmp_path / "a.xyz", tmp_path / "b1.xyz", shallow=False)
+    assert filecmp.cmp(tmp_path / "o.xyz", tmp_path / "b1.xyz", shallow=False)
+    ref.step(1e-4, 5)
+    ref.write_snapshot(str(tmp_path / "o2.xyz"))
+    n0, h0, s0, tg0, p0 = read_xyz(tmp_path / "o2.xyz")
+    n1, h1, s1, tg1, p1 = read_xyz(tmp_path / "b2.xyz")
+    assert n0 == n1 and np.array_equal(tg0, tg1) and np.abs(p0 - p1).max() <= 1e-9
+    assert os.path.getsize(tmp_path / "b3.xyz") > 0
