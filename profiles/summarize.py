@@ -1,11 +1,12 @@
 """Summarise ncu captures into the committed profiles/ files.
 
-    python profiles/summarize.py <report.ncu-rep> <launches.csv> <tag>
+    python profiles/summarize.py <report.ncu-rep> <launches.csv> <tag> [config]
 
 Writes profiles/<tag>_kernels.md (per-kernel key metrics of the --set full
 capture), profiles/<tag>_launches.csv (launch list: kernel, duration) and
-profiles/latest_traffic.json (dram bytes per launch of the dominant kernels,
-read by bench.py for roofline.traffic).
+profiles/traffic_<config>.json (dram bytes per launch of the dominant kernels
+and the counters of the resource binding the force pass, measured on that
+configuration; read by bench.py for roofline.traffic of the same config).
 """
 import csv
 import io
@@ -28,6 +29,10 @@ KEYS = [
     ("smsp__inst_executed.sum", "warp instructions"),
     ("l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum", "L1 ld sectors"),
     ("l1tex__t_sectors_pipe_lsu_mem_global_op_red.sum", "RED sectors"),
+    ("l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed", "LSU data pipe %"),
+    ("l1tex__data_pipe_tex_wavefronts.avg.pct_of_peak_sustained_elapsed", "TEX data pipe %"),
+    ("lts__d_atomic_input_cycles_active.avg.pct_of_peak_sustained_elapsed", "L2 atomic %"),
+    ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "DRAM %"),
     ("launch__registers_per_thread", "registers"),
     ("launch__grid_size", "grid"),
 ]
@@ -40,6 +45,7 @@ def to_bytes(v, unit):
 
 def main():
     rep, launches, tag = sys.argv[1:4]
+    config = sys.argv[4] if len(sys.argv) > 4 else "c5"
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
                          text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
@@ -68,16 +74,24 @@ def main():
             def metric(m):
                 return float(r[hdr.index(m)].replace(",", "")) if m in hdr else None
             traffic["binding_resource"] = {
-                "name": "L1/shared data pipe (force pass)",
+                "name": "L1 LSU data pipe (force pass)",
                 "l1_throughput_pct": metric("l1tex__throughput.avg.pct_of_peak_sustained_active"),
+                "lsu_pipe_pct": metric(
+                    "l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed"),
+                "tex_pipe_pct": metric(
+                    "l1tex__data_pipe_tex_wavefronts.avg.pct_of_peak_sustained_elapsed"),
+                "l2_atomic_pct": metric(
+                    "lts__d_atomic_input_cycles_active.avg.pct_of_peak_sustained_elapsed"),
+                "issue_active_pct": metric("smsp__issue_active.avg.pct_of_peak_sustained_active"),
                 "fp64_pipe_pct": metric(
                     "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
                 "shared_wavefronts": metric("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum"),
                 "shared_bank_conflicts": metric(
                     "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum")}
     open(os.path.join(HERE, f"{tag}_kernels.md"), "w").write("\n".join(lines) + "\n")
-    traffic["source"] = f"profiles/{tag}_kernels.md (dram__bytes_read.sum + dram__bytes_write.sum)"
-    json.dump(traffic, open(os.path.join(HERE, "latest_traffic.json"), "w"), indent=1)
+    traffic["source"] = (f"profiles/{tag}_kernels.md, config {config} "
+                         "(dram__bytes_read.sum + dram__bytes_write.sum per launch)")
+    json.dump(traffic, open(os.path.join(HERE, f"traffic_{config}.json"), "w"), indent=1)
     # launch list: kernel name, duration
     out = []
     with open(launches) as f:
