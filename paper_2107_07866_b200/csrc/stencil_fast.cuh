@@ -126,7 +126,9 @@ __device__ __forceinline__ double rsqrt_nr(double x) {
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
   const double h = 0.5 * x;
   y = y * fma(-h * y, y, 1.5);
+#ifndef CBX_RSQ1
   y = y * fma(-h * y, y, 1.5);
+#endif
   return y;
 }
 
