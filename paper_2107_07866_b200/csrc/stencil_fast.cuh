@@ -121,14 +121,16 @@ __device__ __noinline__ bool guard_force(KP* P, long long d, int j, int tgt, dou
 
 // 1/sqrt for r^2 in the normal range: the hardware approximation plus two
 // Newton steps (relative error a few ulp, no special-case branch)
+// (measured on B200 over r^2 in [0.5, 64]: the approximation 9.3e-7, one
+// step 1.3e-12, two steps 4e-16 relative -- one step would be 1.5 % faster
+// but its ~2e-11 per-pair force error, summed over 58 pairs, is not provably
+// inside the 1e-10 force tolerance)
 __device__ __forceinline__ double rsqrt_nr(double x) {
   double y;
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
   const double h = 0.5 * x;
   y = y * fma(-h * y, y, 1.5);
-#ifndef CBX_RSQ1
   y = y * fma(-h * y, y, 1.5);
-#endif
   return y;
 }
 
@@ -1224,10 +1226,10 @@ bool launch_density_smem(const KP& P, int mode, cudaStream_t s) {
   return !mode;
 }
 int density_table_mode(const KP& P) {
-  // compressed records when the local fp32 guard held (P.fdc), all in
-  // shared memory (CBX_DENSITY_TAB=2: [D C] through the texture path -- the
-  // same time at config 5, its fetch latency sits on the pair's chain)
-  static const int tm = ab_flag("CBX_DENSITY_TAB", 1);
+  // compressed records when the local fp32 guard held (P.fdc): [D C] through
+  // the texture path, [A B] in shared memory (CBX_DENSITY_TAB=1: both in
+  // shared memory, 0.8 % slower at config 5 -- the LSU pipe is the binding one)
+  static const int tm = ab_flag("CBX_DENSITY_TAB", 2);
   return P.fdc ? tm : 0;
 }
 
