@@ -300,11 +300,22 @@ def run_ours(args, w, path, ws, rank, local):
            "clocks": clocks.summary(),
            "kernels_ms_per_step": {k: v / K for k, v in t.items()},
            "phases_ms_per_step": phases,
-           "state_after_timed_steps": {k: st_end[k] for k in ("step", "t", "kinetic", "pair",
-                                                             "embedding", "max_speed")},
+           "state_after_timed_steps": dict(
+               {k: st_end[k] for k in ("step", "t", "kinetic", "pair", "embedding",
+                                       "max_speed")},
+               clash_records=int(dev.lib.cbx_clash_count(dev.h)),
+               defects=_defects(dev)),
            "fp64_peak_probe": {"tflops": peak.value, "sm_mhz_est": mhz.value},
            "engine": dev.describe()}
     return res
+
+
+def _defects(dev):
+    """Wigner-Seitz (vacancies, interstitials, Frenkel pairs) of this rank's store"""
+    try:
+        return list(dev.count_defects())
+    except Exception:  # noqa: BLE001 -- informational only
+        return None
 
 
 def _sum_over_ranks(v, ws, local):

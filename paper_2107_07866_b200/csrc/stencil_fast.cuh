@@ -642,7 +642,11 @@ __device__ __forceinline__ double force_site_lean(const KP& P, KP* Pp, int par, 
       const int bit = __ffs(cu) - 1;
       cu &= cu - 1;
       const bool v = (co >> bit) & 1;
-      const int j = v ? d + lds_i(so + 4 * bit) : d;
+      // the offset: a warp-uniform index, from the constant cache (no LSU
+      // wavefront) or the staged shared-memory copy
+      const int off = P.offs_const ? (FULL ? c_full[par][32 * wd + bit] : c_half[par][32 * wd + bit])
+                                   : lds_i(so + 4 * bit);
+      const int j = v ? d + off : d;
       double px, py, pz, pw;
       ld256(pdf + j, px, py, pz, pw);
       const int t = deep ? j : __ldg(tgt + j);
