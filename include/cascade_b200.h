@@ -275,6 +275,13 @@ CBX_API cbx_status cbx_create_slab(const cbx_box* global_box, const cbx_potentia
 CBX_API cbx_status cbx_slab_info(cbx_ctx* ctx, long out[8]);
 CBX_API long cbx_slab_buffer_bytes(cbx_ctx* ctx, int kind);
 CBX_API cbx_status cbx_slab_phase(cbx_ctx* ctx, int phase, double dt);
+/* Lockstep peer-memory exchange (ranks sharing a GPU, or host-driven runs of
+ * the P2P transport): cbx_slab_p2p_send packs an exchange into the
+ * neighbours' mapped buffers and raises their flags (returns when done);
+ * after a barrier of all ranks, cbx_slab_p2p_recv unpacks what arrived.  Only
+ * with the staged reverse halos (cbx_slab_p2p_set_fused(ctx, 0)). */
+CBX_API cbx_status cbx_slab_p2p_send(cbx_ctx* ctx, int kind);
+CBX_API cbx_status cbx_slab_p2p_recv(cbx_ctx* ctx, int kind);
 CBX_API cbx_status cbx_slab_pack(cbx_ctx* ctx, int kind, int dir, void* dev_buf, long cap,
                                  long* bytes);
 CBX_API cbx_status cbx_slab_unpack(cbx_ctx* ctx, int kind, int from, const void* dev_buf,

@@ -154,6 +154,8 @@ SIGNATURES = [
     ("cbx_slab_info", C.c_int, [_P, C.POINTER(C.c_long)]),
     ("cbx_slab_buffer_bytes", C.c_long, [_P, C.c_int]),
     ("cbx_slab_phase", C.c_int, [_P, C.c_int, _D]),
+    ("cbx_slab_p2p_send", C.c_int, [_P, C.c_int]),
+    ("cbx_slab_p2p_recv", C.c_int, [_P, C.c_int]),
     ("cbx_slab_pack", C.c_int, [_P, C.c_int, C.c_int, _P, C.c_long, C.POINTER(C.c_long)]),
     ("cbx_slab_unpack", C.c_int, [_P, C.c_int, C.c_int, _P, C.c_long]),
     ("cbx_slab_local_state", C.c_int, [_P, C.POINTER(C.c_double)]),

@@ -7,6 +7,7 @@
 #include <memory>
 #include <string>
 #include <thread>
+#include <tuple>
 #include <vector>
 
 #include "cbx_comm.h"
@@ -2469,11 +2470,49 @@ CBX_API long cbx_slab_buffer_bytes(cbx_ctx* c, int kind) {
 // phases: 0 begin step (kick, drift, wrap, hash, outbound migrants),
 // 1 rehash + x/y ghosts, 2 clash images + density, 3 embedding,
 // 4 force, 5 end step (second kick, local sums), 6 local energy sums only
+// Lockstep driving of the peer-memory transport: the host runs the step's
+// phases (cbx_slab_phase) and each exchange as a send (pack into the
+// neighbours' mapped buffers, raise their flags, wait for completion) and a
+// receive (flags already raised: unpack), with a barrier of all ranks in
+// between -- so no kernel ever waits on another rank's kernel, which is what
+// ranks sharing one GPU need (several processes on one device).  Reverse
+// halos go as staged exchanges (no fused peer atomics in this mode).
+CBX_API cbx_status cbx_slab_p2p_send(cbx_ctx* c, int kind) {
+  return guarded(c, [&] {
+    cudaSetDevice(c->device);
+    if (!c->p2p) raise(CBX_LOGIC, "cbx_slab_p2p_send: no peer-memory transport");
+    if (kind < 0 || kind > 4) raise(CBX_INVALID_ARGUMENT, "cbx_slab_p2p_send: unknown kind");
+    if (c->P.rev.on) raise(CBX_LOGIC, "cbx_slab_p2p_send: reverse halos are fused");
+    if (kind == 1) {  // the receive's remote-record count starts from zero
+      sync_status(c);
+      c->hst.n_remote = 0;
+      write_status(c);
+    }
+    launch_p2p_send(c->P, c->links, kind, c->stream);
+    c->launches += 1;
+    sync_status(c);
+    raise_device_error(c, false);
+  });
+}
+CBX_API cbx_status cbx_slab_p2p_recv(cbx_ctx* c, int kind) {
+  return guarded(c, [&] {
+    cudaSetDevice(c->device);
+    if (!c->p2p) raise(CBX_LOGIC, "cbx_slab_p2p_recv: no peer-memory transport");
+    if (kind < 0 || kind > 4) raise(CBX_INVALID_ARGUMENT, "cbx_slab_p2p_recv: unknown kind");
+    const long long gs_lo = (kind == 1 && c->rank == 0) ? -1 : 0;
+    const long long gs_hi = (kind == 1 && c->rank == c->nranks - 1) ? 1 : 0;
+    launch_p2p_recv(c->P, c->links, kind, gs_lo, gs_hi, c->d_rem_base, c->stream);
+    c->launches += 1;
+    sync_status(c);
+    raise_device_error(c, false);
+  });
+}
+
 CBX_API cbx_status cbx_slab_phase(cbx_ctx* c, int phase, double dt) {
   return guarded(c, [&] {
     cudaSetDevice(c->device);
-    if (c->p2p)
-      raise(CBX_LOGIC, "cbx_slab_phase: this rank exchanges on the device (peer memory)");
+    if (c->p2p && c->P.rev.on)
+      raise(CBX_LOGIC, "cbx_slab_phase: this rank's reverse halos are fused into the passes");
     check_cutoff(c);
     switch (phase) {
       case 0:

@@ -391,6 +391,9 @@ void launch_finalize(const KP& P, int stepping, int energies, cudaStream_t s,
                      const P2PLinks* links = nullptr);
 int launch_p2p_exchange(const KP& P, const P2PLinks& L, int kind, long long gs_lo,
                          long long gs_hi, int* rem_base, cudaStream_t s);
+void launch_p2p_send(const KP& P, const P2PLinks& L, int kind, cudaStream_t s);
+void launch_p2p_recv(const KP& P, const P2PLinks& L, int kind, long long gs_lo, long long gs_hi,
+                     int* rem_base, cudaStream_t s);
 void launch_p2p_reduce(const KP& P, const P2PLinks& L, int energies, int kinetic,
                        cudaStream_t s);
 // fused reverse halo: raise the neighbours' flags of exchange `kind` (2 RHO,

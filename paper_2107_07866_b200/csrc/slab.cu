@@ -532,6 +532,16 @@ int launch_p2p_exchange(const KP& P, const P2PLinks& L, int kind, long long gs_l
                                                                 rem_base);
   return 2;
 }
+// the two halves of one exchange as separate launches (lockstep driving:
+// the receiver is launched only after every sender's kernel completed)
+void launch_p2p_send(const KP& P, const P2PLinks& L, int kind, cudaStream_t s) {
+  k_p2p_send<<<kind == 0 ? 2 : plane_grid(P, 2), 256, 0, s>>>(P, L, kind);
+}
+void launch_p2p_recv(const KP& P, const P2PLinks& L, int kind, long long gs_lo, long long gs_hi,
+                     int* rem_base, cudaStream_t s) {
+  k_p2p_recv<<<kind == 0 ? 8 : plane_grid(P, 2), 256, 0, s>>>(P, L, kind, gs_lo, gs_hi,
+                                                                rem_base);
+}
 void launch_p2p_reduce(const KP& P, const P2PLinks& L, int energies, int kinetic,
                        cudaStream_t s) {
   k_p2p_reduce<<<1, 32, 0, s>>>(P, L, energies, kinetic);

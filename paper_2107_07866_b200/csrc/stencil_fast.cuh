@@ -600,7 +600,7 @@ constexpr int kTabSmemBytes[4] = {64, 0, 32, 24};
 // force pass, lean variant: one pair per iteration, no batching, so the
 // register footprint allows 6-8 resident CTAs per SM (latency hidden by
 // warps instead of by in-thread batching).  Warp-uniform union sweep.
-template <bool FULL, int TB, bool REV = false, bool PIPE = false>
+template <bool FULL, int TB, bool REV = false>
 __device__ __forceinline__ double force_site_lean(const KP& P, KP* Pp, int par, int d,
                                                   bool live, unsigned tb = 0,
                                                   int seg_lo = 0, bool rev_here = false,
@@ -628,10 +628,8 @@ __device__ __forceinline__ double force_site_lean(const KP& P, KP* Pp, int par, 
   const double r2_idle = P.cut2_lo;
   double fx = 0.0, fy = 0.0, fz = 0.0, e = 0.0;
   // the warp walks the union of its lanes' masks (warp-uniform offset, lanes
-  // without the bit idle), one 32-bit word at a time.  PIPE: software-
-  // pipelined, the partner gather of the next pair is in flight while the
-  // current pair's table lookups and arithmetic run
-  if constexpr (!PIPE) {
+  // without the bit idle), one 32-bit word at a time
+  {
 #pragma unroll 1
   for (int wd = 0; wd < 4; ++wd) {
     const unsigned long long mw = wd < 2 ? m0 : m1;
@@ -723,111 +721,6 @@ __device__ __forceinline__ double force_site_lean(const KP& P, KP* Pp, int par, 
         }
       }
   }
-  }
-  } else {
-  unsigned long long u0 = warp_or64(m0), u1 = warp_or64(m1);
-  int bit = -1;
-  auto pop = [&]() {
-    if (u0) {
-      bit = __ffsll(u0) - 1;
-      u0 &= u0 - 1;
-    } else if (u1) {
-      bit = 63 + __ffsll(u1);
-      u1 &= u1 - 1;
-    } else {
-      bit = -1;
-    }
-  };
-  bool nv = false;
-  int nj = d, nt = d;
-  double npx = 0, npy = 0, npz = 0, npw = 0;
-  auto fetch = [&]() {
-    nv = ((bit < 64 ? m0 >> bit : m1 >> (bit - 64)) & 1) != 0;
-    nj = nv ? d + lds_i(s_offs + 4 * bit) : d;
-    ld256(pdf + nj, npx, npy, npz, npw);
-    nt = deep ? nj : __ldg(tgt + nj);
-  };
-  pop();
-  if (bit >= 0) fetch();
-#pragma unroll 1
-  while (bit >= 0) {
-    const bool v = nv;
-    const int t = nt;
-    const double px = npx, py = npy, pz = npz, pw = npw;
-    pop();
-    if (bit >= 0) fetch();
-    const double dx = xsub(ax, px), dy = xsub(ay, py), dz = xsub(az, pz);
-    double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
-    r2 = v ? r2 : r2_idle;
-    const double ri = rsqrt_nr(r2);
-    double sb;
-    const int seg = seg_index(P.ff, r2 * ri, sb);
-    double zA, zB, zC, zD, qA, qB, qC;
-    const int li = seg - seg_lo;
-    const int lc = max(li, 0);
-    if (TB == kTabSplit) {
-      const double2 q0 = tex_chunk(P.tex_ff, seg, 2), q1 = tex_chunk(P.tex_ff, seg, 3);
-      qA = q0.x; qB = q0.y; qC = q1.x;
-      if (li >= 0) {
-        const double2 c0 = lds2(tb + 32 * lc), c1 = lds2(tb + 32 * lc + 16);
-        zA = c0.x; zB = c0.y; zC = c1.x; zD = c1.y;
-      } else {
-        const double2 c0 = tex_chunk(P.tex_ff, seg, 0), c1 = tex_chunk(P.tex_ff, seg, 1);
-        zA = c0.x; zB = c0.y; zC = c1.x; zD = c1.y;
-      }
-    } else if (TB == kTabSplit3) {
-      const double2 c0 = tex_chunk(P.tex_ff, seg, 0), q0 = tex_chunk(P.tex_ff, seg, 2);
-      zA = c0.x; zB = c0.y; qA = q0.x; qB = q0.y;
-      if (li >= 0) {
-        const double2 c1 = lds2(tb + 16 * lc);
-        zC = c1.x; zD = c1.y;
-        qC = lds_d(tb8 + 8 * lc);
-      } else {
-        const double2 c1 = tex_chunk(P.tex_ff, seg, 1), q1 = tex_chunk(P.tex_ff, seg, 3);
-        zC = c1.x; zD = c1.y; qC = q1.x;
-      }
-    } else {
-      const double2 c0 = lds2(tb + 16 * smem_slot(lc, 0)), c1 = lds2(tb + 16 * smem_slot(lc, 1));
-      const double2 c2 = lds2(tb + 16 * smem_slot(lc, 2)), c3 = lds2(tb + 16 * smem_slot(lc, 3));
-      zA = c0.x; zB = c0.y; zC = c1.x; zD = c1.y;
-      qA = c2.x; qB = c2.y; qC = c3.x;
-      if (li < 0) {  // below the window (cascade cores): global record
-        const double* rec = P.ff.rec + 8 * (size_t)seg;
-        double qD;
-        ld256(rec, zA, zB, zC, zD);
-        ld256(rec + 4, qA, qB, qC, qD);
-      }
-    }
-    const double s15 = 1.5 * sb, s2 = sb + sb;
-    const double z = fma(fma(fma(zA, sb, zB), sb, zC), sb, zD);
-    const double zs = fma(fma(zA, s15, zB), s2, zC);  // dz/ds
-    const double ps = fma(fma(qA, s15, qB), s2, qC);  // drho/ds
-    const double phi = v ? z * ri : 0.0;
-    const double dphi = fma(zs, ih, -phi) * ri;
-    const double mfp = v ? fma((adf + pw) * ps, ih, dphi) * ri : 0.0;
-    const double qx = mfp * dx, qy = mfp * dy, qz = mfp * dz;
-    fx -= qx;
-    fy -= qy;
-    fz -= qz;
-    if (FULL) {
-      e = fma(0.5, phi, e);
-    } else {
-      e += phi;
-      if (v) {
-        if (REV && rev_here) {  // warp-uniform: a plane within reach of the halo
-          double* f = acc_ptr_up(P, t, 0);
-          const long long st = (int)t - ((int)t >= (int)P.G.NC ? (int)P.G.NC : 0) >= (int)P.rev.hi
-                                   ? P.rev.S[1] : S;
-          red_add(f, qx);
-          red_add(f + st, qy);
-          red_add(f + 2 * st, qz);
-        } else {
-          red_add(&P.frc[t], qx);
-          red_add(&P.frc[S + t], qy);
-          red_add(&P.frc[2 * S + t], qz);
-        }
-      }
-    }
   }
   }
   const int* offs = FULL ? c_full[par] : c_half[par];
@@ -1100,7 +993,7 @@ __host__ __device__ __forceinline__ int force_window_lo(int nseg, int tb) {
   return tb == kTabSplit3 ? ((lo > 0 ? lo : 0) + 1) & ~1 : (lo > 0 ? lo : 0);
 }
 
-template <bool FULL, int NT, int TB, bool REV = false, bool PIPE = false>
+template <bool FULL, int NT, int TB, bool REV = false>
 __global__ void __launch_bounds__(NT, 1) k_force_lean_smem(KP P, int nsb) {
   if (blockIdx.x >= nsb) {
     pdl_wait();
@@ -1166,7 +1059,7 @@ __global__ void __launch_bounds__(NT, 1) k_force_lean_smem(KP P, int nsb) {
     const bool live = unit_cell(G, u, lane, w, c);
     const bool deep = live && unit_deep(G, u, lane, w, FULL);
     for (int par = 0; par < 2; ++par)
-      e += force_site_lean<FULL, TB, REV, PIPE>(P, P.dself, par, live ? (int)(par * G.NC + c) : 0,
+      e += force_site_lean<FULL, TB, REV>(P, P.dself, par, live ? (int)(par * G.NC + c) : 0,
                                           live, smem_addr(T), seg_lo, near_halo(G, u, w), deep,
                                           tb8);
   }
@@ -1259,7 +1152,7 @@ bool launch_density_fast(const KP& P, int mode, int grid, cudaStream_t s) {
 // force spline window in shared memory (+ texture chunks); otherwise
 // (positions changed since the density pass) the decision path, which
 // re-derives every pair
-template <int TB, bool PIPE>
+template <int TB>
 void launch_force_lean(const KP& P, int mode, cudaStream_t s) {
   const size_t bytes = (size_t)kLeanTabRecords * kTabSmemBytes[TB] + 16;
   static bool attr = false;
@@ -1267,11 +1160,11 @@ void launch_force_lean(const KP& P, int mode, cudaStream_t s) {
     // default carveout: the driver takes the smallest shared-memory split
     // that fits the table and leaves the rest of the SM's 256 KB as L1 for
     // the partner gathers and the texture fetches
-    for (const void* k : {(const void*)k_force_lean_smem<false, 1024, TB, false, PIPE>,
-                          (const void*)k_force_lean_smem<true, 1024, TB, false, PIPE>,
-                          (const void*)k_force_lean_smem<false, 1024, TB, true, PIPE>,
-                          (const void*)k_force_lean_smem<false, 896, TB, false, PIPE>,
-                          (const void*)k_force_lean_smem<false, 896, TB, true, PIPE>})
+    for (const void* k : {(const void*)k_force_lean_smem<false, 1024, TB, false>,
+                          (const void*)k_force_lean_smem<true, 1024, TB, false>,
+                          (const void*)k_force_lean_smem<false, 1024, TB, true>,
+                          (const void*)k_force_lean_smem<false, 896, TB, false>,
+                          (const void*)k_force_lean_smem<false, 896, TB, true>})
       cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
     attr = true;
   }
@@ -1284,14 +1177,14 @@ void launch_force_lean(const KP& P, int mode, cudaStream_t s) {
   const int nt = nt_env ? nt_env : 896;
   if (nt == 896 && !mode) {
     if (P.rev.on)
-      launch_pdl(k_force_lean_smem<false, 896, TB, true, PIPE>, g + 4, 896, bytes, s, P, g);
-    else launch_pdl(k_force_lean_smem<false, 896, TB, false, PIPE>, g + 4, 896, bytes, s, P, g);
+      launch_pdl(k_force_lean_smem<false, 896, TB, true>, g + 4, 896, bytes, s, P, g);
+    else launch_pdl(k_force_lean_smem<false, 896, TB, false>, g + 4, 896, bytes, s, P, g);
     return;
   }
-  if (mode) launch_pdl(k_force_lean_smem<true, 1024, TB, false, PIPE>, g, 1024, bytes, s, P, g);
+  if (mode) launch_pdl(k_force_lean_smem<true, 1024, TB, false>, g, 1024, bytes, s, P, g);
   else if (P.rev.on)
-    launch_pdl(k_force_lean_smem<false, 1024, TB, true, PIPE>, g + 4, 1024, bytes, s, P, g);
-  else launch_pdl(k_force_lean_smem<false, 1024, TB, false, PIPE>, g + 4, 1024, bytes, s, P, g);
+    launch_pdl(k_force_lean_smem<false, 1024, TB, true>, g + 4, 1024, bytes, s, P, g);
+  else launch_pdl(k_force_lean_smem<false, 1024, TB, false>, g + 4, 1024, bytes, s, P, g);
 }
 int force_table_mode() {
   static const int tb = ab_flag("CBX_FORCE_TAB", kTabSplit3);
@@ -1300,16 +1193,9 @@ int force_table_mode() {
 bool launch_force_fast(const KP& P, int mode, int grid, cudaStream_t s) {
   if (P.use_mask) {
     const int tb = force_table_mode();
-    static const bool pipe = ab_flag("CBX_FORCE_PIPE", 0) != 0;
-    if (pipe) {
-      if (tb == kTabSplit3) launch_force_lean<kTabSplit3, true>(P, mode, s);
-      else if (tb == kTabSmem64) launch_force_lean<kTabSmem64, true>(P, mode, s);
-      else launch_force_lean<kTabSplit, true>(P, mode, s);
-    } else {
-      if (tb == kTabSplit3) launch_force_lean<kTabSplit3, false>(P, mode, s);
-      else if (tb == kTabSmem64) launch_force_lean<kTabSmem64, false>(P, mode, s);
-      else launch_force_lean<kTabSplit, false>(P, mode, s);
-    }
+    if (tb == kTabSplit3) launch_force_lean<kTabSplit3>(P, mode, s);
+    else if (tb == kTabSmem64) launch_force_lean<kTabSmem64>(P, mode, s);
+    else launch_force_lean<kTabSplit>(P, mode, s);
     return !mode;
   }
   if (mode) k_force_fast<true, 2><<<grid, 128, 0, s>>>(P);

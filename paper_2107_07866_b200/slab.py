@@ -180,6 +180,12 @@ class SlabRank(DeviceStore):
         else:
             raise ValueError(f"unknown transport {transport!r}")
 
+    def p2p_send(self, kind: int):
+        self._check(self.lib.cbx_slab_p2p_send(self.h, kind))
+
+    def p2p_recv(self, kind: int):
+        self._check(self.lib.cbx_slab_p2p_recv(self.h, kind))
+
     def bench_steps(self, dt: float, n: int, flush_mb: float = 0.0):
         out = (C.c_double * 8)()
         self._check(self.lib.cbx_bench_steps(self.h, dt, n, flush_mb, out))
@@ -335,6 +341,41 @@ class DistExchange:
         out = s.copy()
         out[[0, 1, 2, 4, 5]] = sums.cpu().numpy()
         out[3] = float(mx.cpu().item())
+        return out
+
+
+class P2PLockstep:
+    """The peer-memory transport driven from the host, one rank per process:
+    each exchange is a send (the rank's kernel stores its packets into the
+    neighbours' mapped buffers and raises their flags, and completes), a
+    barrier of all ranks, and a receive (the flags are up: unpack).  No
+    kernel waits on another rank's kernel, so ranks may share one GPU.  The
+    StepState reduction goes through torch.distributed (gloo or NCCL)."""
+
+    def __init__(self, rank_obj, group=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.r = rank_obj
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.n = dist.get_world_size(group)
+
+    def exchange(self, kind: int):
+        self.r.p2p_send(kind)
+        self.dist.barrier(group=self.group)
+        self.r.p2p_recv(kind)
+        self.dist.barrier(group=self.group)  # receive buffers free for the next send
+
+    def allreduce(self, states: List[np.ndarray]) -> np.ndarray:
+        import torch
+        s = states[0]
+        sums = torch.tensor(s[[0, 1, 2, 4, 5]], dtype=torch.float64)
+        mx = torch.tensor([s[3]], dtype=torch.float64)
+        self.dist.all_reduce(sums, op=self.dist.ReduceOp.SUM, group=self.group)
+        self.dist.all_reduce(mx, op=self.dist.ReduceOp.MAX, group=self.group)
+        out = s.copy()
+        out[[0, 1, 2, 4, 5]] = sums.numpy()
+        out[3] = float(mx.item())
         return out
 
 

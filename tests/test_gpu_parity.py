@@ -333,6 +333,39 @@ def test_density_record_guard_local(cuda, tables, tmp_path, rho_k, compressed):
     assert_store_parity(ref.store(), dev.download(), what=f"rho_k={rho_k}")
 
 
+@pytest.mark.parametrize("stencil", ["newton3", "full"])
+def test_rows_of_whole_strips(cuda, tables, stencil):
+    """Boxes whose rows hold whole 32-cell strips (bx % 32 == 0, as configs 4
+    and 5) take the force pass's row accumulation of partner shares and the
+    column unit order: a thermal 32 x 5 x 7 box with x and y images, then a
+    PKA cascade (off-lattice records, ghost partners), against the oracle"""
+    from oracle import oracle
+    ref = oracle.Sim(tables["baseline"], box=(32, 5, 7), temperature=600.0, seed=21,
+                     pka_energy_kev=0.5, pka_site=(16, 2, 3))
+    ref.step(1e-3, 4)
+    dev = device_for(ref, tables["baseline"], stencil)
+    dev.set_state(ref.state())
+    e_ref, e_dev = ref.eval_forces(), dev.eval_forces()
+    assert close(e_ref[0], e_dev[0]) and close(e_ref[1], e_dev[1]), (e_ref, e_dev)
+    assert_store_parity(ref.store(), dev.download(), what=f"aligned eval {stencil}")
+    ref.step(1e-3, 10)
+    dev.step(1e-3, 10)
+    assert_store_parity(ref.store(), dev.download(), pos_tol=1e-10, rel=1e-9,
+                        what=f"aligned thermal {stencil}")
+    ref.inject_pka()
+    s = ref.store()
+    _, a, g = ref.box
+    tx, ty = 32 + 2 * g, 5 + 2 * g
+    site = ((g + 3) * ty + (g + 2)) * 2 * tx + 2 * (g + 16)
+    dev.inject_pka(site, s.vel[site])
+    for chunk in range(3):
+        ref.step(1e-4, 20)
+        dev.step(1e-4, 20)
+        assert ref.count_defects() == dev.count_defects(), chunk
+        assert_store_parity(ref.store(), dev.download(), pos_tol=1e-8, rel=1e-7,
+                            what=f"aligned cascade {stencil} {chunk}")
+
+
 def test_overlap_halts_multi_step_call(cuda, tables):
     """An overlap found in step 2 of a 5-step call (fixed dt: merged kicks and
     deferred StepState sums) ends the call at step 2 like the reference's
