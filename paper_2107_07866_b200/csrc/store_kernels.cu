@@ -47,26 +47,57 @@ __device__ void clash_kick_drift_body(const KP& P, int move, int blk, int nblk);
 __device__ void ghost_images(const KP& P, long long d, const double4& p);
 __device__ void ghost_images_at(const KP& P, int par, int cx, int cy, int cz, const double4& p);
 __device__ void clash_kick2_sums(const KP& P, int blk);
+// a site's record as the sweep loads it (every load issued before the
+// first use: one memory round trip per site)
+struct KdSite {
+  long long d;
+  int par, cx, cy, cz;
+  bool live;
+  double4 p;
+  double vx, vy, vz, fx, fy, fz;
+};
+__device__ __forceinline__ void kick_drift_load(const KP& P, int vb, KdSite& a) {
+  a.live = map_site_xyz(P, vb, a.par, a.d, a.cx, a.cy, a.cz);
+  if (!a.live) return;
+  // 32-bit site index into per-component base pointers (a single store fits
+  // 2^31 sites)
+  const long long S = P.S;
+  const int i = (int)a.d;
+  a.p = P.pdf[i];
+  a.vx = P.vel[i];
+  a.vy = P.vel[S + i];
+  a.vz = P.vel[2 * S + i];
+  a.fx = P.frc[i];
+  a.fy = P.frc[S + i];
+  a.fz = P.frc[2 * S + i];
+}
+__device__ __forceinline__ void kick_drift_proc(const KP& P, int move, int zero_acc, int images,
+                                                double dt, double hk, bool k2, double& v2s,
+                                                double& v2m, const KdSite& a);
 // one site per thread of virtual block vb (128 cells x 2 sublattices)
 __device__ __forceinline__ void kick_drift_site(const KP& P, int move, int zero_acc, int images,
                                                 int vb, double dt, double hk, bool k2,
                                                 double& v2s, double& v2m) {
-  int par, cx, cy, cz;
-  long long d;
-  if (!map_site_xyz(P, vb, par, d, cx, cy, cz)) return;
-  // 32-bit site index into per-component base pointers (a single store fits
-  // 2^31 sites); every load of the site issued before the first use
+  KdSite a;
+  kick_drift_load(P, vb, a);
+  if (a.live) kick_drift_proc(P, move, zero_acc, images, dt, hk, k2, v2s, v2m, a);
+}
+__device__ __forceinline__ void kick_drift_proc(const KP& P, int move, int zero_acc, int images,
+                                                double dt, double hk, bool k2, double& v2s,
+                                                double& v2m, const KdSite& a) {
   const long long S = P.S;
+  const long long d = a.d;
   const int i = (int)d;
+  const int par = a.par, cx = a.cx, cy = a.cy, cz = a.cz;
   double* __restrict__ vxp = P.vel;
   double* __restrict__ vyp = P.vel + S;
   double* __restrict__ vzp = P.vel + 2 * S;
   double* __restrict__ fxp = P.frc;
   double* __restrict__ fyp = P.frc + S;
   double* __restrict__ fzp = P.frc + 2 * S;
-  double4 p = P.pdf[i];
-  double vx = vxp[i], vy = vyp[i], vz = vzp[i];
-  const double fx = fxp[i], fy = fyp[i], fz = fzp[i];
+  double4 p = a.p;
+  double vx = a.vx, vy = a.vy, vz = a.vz;
+  const double fx = a.fx, fy = a.fy, fz = a.fz;
   if (zero_acc) {
     P.rho[i] = 0.0;
     fxp[i] = 0.0;
@@ -153,9 +184,11 @@ __device__ __forceinline__ void kick_drift_site(const KP& P, int move, int zero_
 
 // a single wave of blocks (resident on every SM) walks the virtual blocks
 
-__global__ void __launch_bounds__(256, 4) k_kick_drift(KP P, int move, int nsb, int zero_acc,
-                                                    int images, int nvb, int n_pairp,
-                                                    int n_emb, int n_ke) {
+// (two virtual blocks per thread with both sites' loads in flight measured
+// slower at config 5: 1.89 vs 1.79 ms, 80 registers and spills)
+__global__ void __launch_bounds__(256, 4)
+    k_kick_drift(KP P, int move, int nsb, int zero_acc, int images, int nvb, int n_pairp,
+                 int n_emb, int n_ke) {
   if (blockIdx.x == nsb) {  // an idle clash block: the previous step's StepState
     // sums (the step's dt is fixed when they are deferred)
     finalize_pending<256>(P);
