@@ -231,6 +231,9 @@ Tab upload_tab(cbx_ctx* c, const Spline& s) {
   return t;
 }
 
+bool has_transport(const cbx_ctx* c);
+bool want_merge(const cbx_ctx* c);
+
 void sync_status(cbx_ctx* c) {
   if (c->fin_maybe) {  // the last step's StepState sums before the host reads them
     launch_finalize_pending(c->P, c->stream);
@@ -238,8 +241,16 @@ void sync_status(cbx_ctx* c) {
     c->fin_maybe = false;
   }
   if (c->k2_maybe) {  // the last step's second half kick (+ its StepState sums)
-    launch_kick2(c->P, 1, 1, 1, c->stream, 1, c->fin_npp);
-    c->launches += 1;
+    if (has_transport(c)) {  // slab rank: after the neighbours' force partials,
+      KP q = c->P;           // then the sums and the cross-rank reduction
+      q.rev_wait = c->P.rev.on ? 4 : 0;
+      launch_kick2(q, 1, -2, 0, c->stream);
+      launch_finalize(c->P, 1, 1, c->stream, c->d_links);
+      c->launches += 2;
+    } else {
+      launch_kick2(c->P, 1, 1, 1, c->stream, 1, c->fin_npp);
+      c->launches += 1;
+    }
     c->k2_maybe = false;
   }
   cuda_check(cudaMemcpyAsync(&c->hst, c->P.st, sizeof(DevStatus), cudaMemcpyDeviceToHost,
@@ -471,11 +482,23 @@ void seq_slab_step(cbx_ctx* c) {
   c->mask_valid = false;
   ev_mark(c, 0);
   memset_field(c, &c->P.st->n_out);
+  // merged kick (peer memory, fixed dt): the previous step's second half
+  // kick runs in this step's k_kick_drift once the neighbours' force
+  // partials are in; its sums + reduction in the density pass's idle block
+  const bool merge = want_merge(c);
+  c->graph_merge = merge;
+  c->graph_defer = false;
+  KP qf = c->P;
+  qf.use_mask = 1;
+  const int npp = force_partials(qf, c->mode);
+  c->fin_npp = npp;
   // interior accumulators cleared here, the halo sites' by the POS unpack
   const bool zacc = c->mode != CBX_STENCIL_FULL;
-  launch_kick_drift(c->P, 1, c->stream, zacc ? 1 : 0);
+  KP qk = c->P;
+  qk.rev_wait = merge && c->P.rev.on ? 4 : 0;
+  launch_kick_drift(qk, 1, c->stream, zacc ? 1 : 0, 0, npp);
   slab_exchange(c, 0);  // migrants
-  launch_rehash(c->P, c->stream);
+  launch_rehash(c->P, c->stream, merge ? 1 : 0, embed_grid(c->P), npp, kick_drift_grid(c->P));
   launch_ghost_fill(c->P, c->stream);
   c->launches += 3;
   memset_field(c, &c->P.st->n_remote);
@@ -493,10 +516,16 @@ void seq_slab_step(cbx_ctx* c) {
   ev_mark(c, 3);
   launch_remote_df(c->P, c->stream);
   c->launches += 1;
+  c->merge_now = merge;
   seq_force(c);
+  c->merge_now = false;
   slab_reverse(c, 4);  // force partials (reverse)
   ev_mark(c, 4);
-  slab_finish(c, 1, 1, 1);
+  if (merge) {
+    if (!g_capturing) c->k2_maybe = true;
+  } else {
+    slab_finish(c, 1, 1, 1);
+  }
   ev_mark(c, 5);
 }
 
@@ -534,6 +563,14 @@ bool want_defer(const cbx_ctx* c) {
 // mask-replay passes (the density pass's clash blocks run the pending sums)
 bool want_merge(const cbx_ctx* c) {
   static const bool on = ab_flag("CBX_MERGE_KICK", 1) && ab_flag("CBX_DENSITY_SMEM", 1);
+  // slab ranks on the peer-memory transport merge too: the next k_kick_drift
+  // waits for the neighbours' force partials, and the deferred StepState sums
+  // carry the cross-rank reduction (finalize_pending); not with NCCL (its
+  // all-reduce is a stream operation, not a kernel tail)
+  static const bool slab = ab_flag("CBX_SLAB_MERGE", 1) != 0;
+  if (has_transport(c))
+    return on && slab && c->p2p && !c->hst.adaptive && !c->single &&
+           c->mode == CBX_STENCIL_NEWTON3 && c->P.pmask != nullptr;
   return on && want_defer(c) && c->mode == CBX_STENCIL_NEWTON3 && c->P.pmask != nullptr;
 }
 

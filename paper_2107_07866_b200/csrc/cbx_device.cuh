@@ -80,6 +80,7 @@ struct DevStatus {
   int fin_nemb, fin_npp, fin_nke;  // partial counts of the pending sums
   int fin_clash;  // > 0: the clash records' sums are in that many reserved slots
   int fin_bad;    // err | n_ovl when the sums were deferred (their step's outcome)
+  int fin_reduce; // slab ranks (peer memory): the cross-rank reduction follows the sums
   // a step of the current multi-step replay failed (set by k_rehash_images of
   // the next step from the stable status words): the passes of the remaining
   // steps are no-ops, so the store stays at the failing step (sim.cpp:303-315)
@@ -339,7 +340,8 @@ void launch_kick_drift(const KP& P, int move, cudaStream_t s, int zero_acc = 0, 
                        int n_pairp = 0);
 // update_hash pass 2 + ghost clash images in one single-block launch
 void launch_clash_zero(const KP& P, int what, cudaStream_t s);
-void launch_rehash(const KP& P, cudaStream_t s);
+void launch_rehash(const KP& P, cudaStream_t s, int merge = 0, int n_emb = 0, int n_pairp = 0,
+                   int n_ke = 0);
 void launch_ghost_fill(const KP& P, cudaStream_t s);
 // zero_rho: also zero the records' density accumulators (density follows)
 void launch_clash_images(const KP& P, cudaStream_t s, int zero_rho = 0);

@@ -5,6 +5,7 @@
 // density pass (eam_kernels.cu) each instantiate their own copy.
 #pragma once
 #include "cbx_device.cuh"
+#include "p2p.cuh"
 
 namespace cbx {
 
@@ -127,7 +128,16 @@ __device__ void finalize_pending(const KP& P) {
   finalize_body<NT>(*P.dself, st->fin_stepping, st->fin_energies, P.part_emb, st->fin_nemb,
                     P.part_pair, st->fin_npp, st->fin_nke, st->fin_clash, st->fin_bad);
   __syncthreads();
-  if (threadIdx.x == 0) st->fin_pending = 0;
+  if (threadIdx.x == 0) {
+    // slab ranks on the peer-memory transport: the StepState sums over the
+    // ranks (every rank's deferred finalize reaches this point in the same
+    // kernel of the same step; also after an error, so the ranks stay in step)
+    if (st->fin_reduce && P.lk) {
+      __threadfence();
+      p2p_reduce_thread(*P.dself, *P.lk, st->fin_energies, st->fin_stepping >= 0);
+    }
+    st->fin_pending = 0;
+  }
 }
 
 }  // namespace cbx

@@ -196,6 +196,9 @@ __global__ void __launch_bounds__(256, 4)
   // a failed step (device error or overlap, stable since the previous
   // step's passes) ends the replay: no further kick, drift or rehash
   if (P.st->err || P.st->n_ovl) return;
+  // slab ranks with the merged kick: the neighbours' force partials of the
+  // previous step (fused reverse halo) are in before any force is read
+  if (P.rev_wait && !rev_wait(P, P.rev_wait)) return;
   if (blockIdx.x >= nsb) {  // the clash records (fused k_clash_kick_drift)
     if (P.st->k2_pending) clash_kick2_sums(P, blockIdx.x - nsb);
     clash_kick_drift_body(P, move, blockIdx.x - nsb, gridDim.x - nsb);
@@ -571,10 +574,27 @@ __device__ void rehash_body(const KP& P) {
     P.st->n_mov = 0;
   }
 }
-__global__ void __launch_bounds__(1024) k_rehash(KP P) {
+__global__ void __launch_bounds__(1024) k_rehash(KP P, int merge, int n_emb, int n_pairp,
+                                                 int n_ke) {
   pdl_wait();
   pdl_trigger();
   if (halt_check(P)) return;
+  if (merge && threadIdx.x == 0 && P.st->k2_pending) {
+    // slab ranks (peer memory), merged kick: k_kick_drift ran the previous
+    // step's second half kick; its StepState sums and the cross-rank
+    // reduction become pending for the density pass's idle block
+    DevStatus* st = P.st;
+    st->fin_bad = 0;
+    st->k2_pending = 0;
+    st->fin_stepping = 1;
+    st->fin_energies = 1;
+    st->fin_nemb = n_emb;
+    st->fin_npp = n_pairp;
+    st->fin_nke = n_ke;
+    st->fin_clash = kClashSlots;
+    st->fin_reduce = 1;
+    st->fin_pending = 1;
+  }
   rehash_body(P);
 }
 
@@ -828,6 +848,7 @@ __global__ void __launch_bounds__(1024) k_rehash_images(KP P, int merge, int n_e
     // sums become pending (for the density pass's idle block)
     DevStatus* st = P.st;
     st->fin_bad = 0;  // that step completed (else this step would have halted)
+    st->fin_reduce = 0;
     st->k2_pending = 0;
     st->fin_stepping = 1;
     st->fin_energies = 1;
@@ -957,6 +978,7 @@ __global__ void __launch_bounds__(256, 6) k_kick2(KP P, int kick, int nsb, int f
       P.st->fin_nke = nsb;
       P.st->fin_clash = 0;
       P.st->fin_bad = P.st->err | P.st->n_ovl;  // this step's outcome, stable here
+      P.st->fin_reduce = 0;
       P.st->fin_pending = 1;
     }
     return;
@@ -1047,7 +1069,9 @@ void launch_rehash_images(const KP& P, cudaStream_t s, int merge, int n_emb, int
   launch_pdl(k_rehash_images, 1, 1024, 0, s, P, merge, n_emb, n_pairp, n_ke);
 }
 int kick_drift_grid(const KP& P) { return site_wave(P, 4); }
-void launch_rehash(const KP& P, cudaStream_t s) { launch_pdl(k_rehash, 1, 1024, 0, s, P); }
+void launch_rehash(const KP& P, cudaStream_t s, int merge, int n_emb, int n_pairp, int n_ke) {
+  launch_pdl(k_rehash, 1, 1024, 0, s, P, merge, n_emb, n_pairp, n_ke);
+}
 void launch_ghost_fill(const KP& P, cudaStream_t s) {
   if (P.n_gh) launch_pdl(k_ghost_fill, (int)((P.n_gh + 255) / 256), 256, 0, s, P);
 }
