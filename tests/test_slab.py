@@ -276,11 +276,12 @@ def native_rank(ref, path, transport):
     r = S.SlabRank((*dims, a0, g), EamPotential.load(path), 0, 1)
     r.connect("p2p" if transport.startswith("p2p") else transport)
     if transport.startswith("p2p"):
-        # the reverse halos fused into the passes (default) or staged
-        assert r.fused
-        if transport == "p2p-staged":
-            _lib.check(r.lib.cbx_slab_p2p_set_fused(r.h, 0), r.h)
-            assert not r.lib.cbx_slab_p2p_fused(r.h)
+        # the reverse halos as staged exchanges (default) or fused into the
+        # passes (peer atomics into the neighbours' accumulators)
+        assert not r.fused
+        if transport == "p2p-fused":
+            _lib.check(r.lib.cbx_slab_p2p_set_fused(r.h, 1), r.h)
+            assert r.lib.cbx_slab_p2p_fused(r.h)
     r.upload_global(ref.store())
     r.set_state(ref.state())
     return r
@@ -299,7 +300,7 @@ def test_slab_local_exchange_single_rank(cuda, tables):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("transport", ["p2p", "p2p-staged", "nccl"])
+@pytest.mark.parametrize("transport", ["p2p", "p2p-fused", "nccl"])
 def test_slab_graph_eval_and_trajectory(cuda, tables, transport):
     """exchanges captured in the step graph (NCCL self send/recv, or the
     flag-synchronised peer-memory kernels): forces, energies and a 60-step
@@ -329,7 +330,7 @@ def test_slab_graph_eval_and_trajectory(cuda, tables, transport):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("transport", ["p2p", "p2p-staged", "nccl"])
+@pytest.mark.parametrize("transport", ["p2p", "p2p-fused", "nccl"])
 def test_slab_graph_cascade(cuda, tables, transport):
     """cascade with adaptive dt through the NCCL step graph: clash records,
     defect counts and the global-max-speed time step match the oracle"""
