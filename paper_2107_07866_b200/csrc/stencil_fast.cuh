@@ -756,125 +756,6 @@ __device__ __forceinline__ double force_site_lean(const KP& P, KP* Pp, int par, 
   return e;
 }
 
-// Two pairs per iteration (ILP): both partners' gathers, then both table
-// fetches (texture + shared), then both evaluations -- twice the memory
-// operations in flight per warp at ~100 registers (640-thread CTAs).  The
-// Newton-3 single-box / staged-halo form with the kTabSplit3 table.
-__device__ __forceinline__ double force_site_ilp2(const KP& P, KP* Pp, int par, int d, bool live,
-                                                  unsigned tb, int seg_lo, bool deep,
-                                                  unsigned tb8) {
-  const double4* __restrict__ pdf = P.pdf;
-  const int* __restrict__ tgt = P.tgt;
-  const long long S = P.S;
-  double ax = kVacant, ay = 0, az = 0, adf = 0;
-  if (live) ld256(pdf + d, ax, ay, az, adf);
-  const bool occ = ax < kVacantTest;
-  unsigned long long m0 = 0, m1 = 0;
-  if (occ) {
-    m0 = P.pmask[2 * (size_t)d];
-    m1 = P.pmask[2 * (size_t)d + 1];
-  }
-  const bool guard = (m1 & kGuardBit) != 0;
-  m1 &= ~kGuardBit;
-  const double ih = P.ff.ih;
-  const double r2_idle = P.cut2_lo;
-  double fx = 0.0, fy = 0.0, fz = 0.0, e = 0.0;
-#pragma unroll 1
-  for (int wd = 0; wd < 4; ++wd) {
-    const unsigned long long mw = wd < 2 ? m0 : m1;
-    const unsigned co = (wd & 1) ? (unsigned)(mw >> 32) : (unsigned)mw;
-    unsigned cu = __reduce_or_sync(0xffffffffu, co);
-    while (cu) {
-      int bit[2];
-      bool v[2];
-      int j[2], t[2];
-      double px[2], py[2], pz[2], pw[2];
-#pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        bit[q] = cu ? __ffs(cu) - 1 : -1;
-        if (cu) cu &= cu - 1;
-        v[q] = bit[q] >= 0 && ((co >> bit[q]) & 1);
-        const int off = bit[q] >= 0 ? c_half[par][32 * wd + bit[q]] : 0;
-        j[q] = v[q] ? d + off : d;
-        ld256(pdf + j[q], px[q], py[q], pz[q], pw[q]);
-        t[q] = deep ? j[q] : __ldg(tgt + j[q]);
-      }
-      double dx[2], dy[2], dz[2], ri[2], sb[2];
-      int seg[2];
-      double zA[2], zB[2], zC[2], zD[2], qA[2], qB[2], qC[2];
-#pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        dx[q] = xsub(ax, px[q]);
-        dy[q] = xsub(ay, py[q]);
-        dz[q] = xsub(az, pz[q]);
-        double r2 = fma(dz[q], dz[q], fma(dy[q], dy[q], dx[q] * dx[q]));
-        r2 = v[q] ? r2 : r2_idle;
-        ri[q] = rsqrt_nr(r2);
-        seg[q] = seg_index(P.ff, r2 * ri[q], sb[q]);
-      }
-#pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        const double2 c0 = tex_chunk(P.tex_ff, seg[q], 0), q0 = tex_chunk(P.tex_ff, seg[q], 2);
-        zA[q] = c0.x; zB[q] = c0.y; qA[q] = q0.x; qB[q] = q0.y;
-        const int li = seg[q] - seg_lo;
-        if (li >= 0) {
-          const double2 c1 = lds2(tb + 16 * li);
-          zC[q] = c1.x; zD[q] = c1.y;
-          qC[q] = lds_d(tb8 + 8 * li);
-        } else {
-          const double2 c1 = tex_chunk(P.tex_ff, seg[q], 1), q1 = tex_chunk(P.tex_ff, seg[q], 3);
-          zC[q] = c1.x; zD[q] = c1.y; qC[q] = q1.x;
-        }
-      }
-#pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        const double s = sb[q], s15 = 1.5 * s, s2 = s + s;
-        const double z = fma(fma(fma(zA[q], s, zB[q]), s, zC[q]), s, zD[q]);
-        const double zs = fma(fma(zA[q], s15, zB[q]), s2, zC[q]);
-        const double ps = fma(fma(qA[q], s15, qB[q]), s2, qC[q]);
-        const double phi = v[q] ? z * ri[q] : 0.0;
-        const double dphi = fma(zs, ih, -phi) * ri[q];
-        const double mfp = v[q] ? fma((adf + pw[q]) * ps, ih, dphi) * ri[q] : 0.0;
-        const double qx = mfp * dx[q], qy = mfp * dy[q], qz = mfp * dz[q];
-        fx -= qx;
-        fy -= qy;
-        fz -= qz;
-        e += phi;
-        if (v[q]) {
-          red_add(&P.frc[t[q]], qx);
-          red_add(&P.frc[S + t[q]], qy);
-          red_add(&P.frc[2 * S + t[q]], qz);
-        }
-      }
-    }
-  }
-  if (guard) {  // the guard pairs skipped by the density pass's mask
-    const int n = c_half_n[par];
-    const int* offs = c_half[par];
-    for (int kk = 0; kk < n; ++kk) {
-      const int jj = d + offs[kk];
-      double px, py, pz, pw;
-      ld256(pdf + jj, px, py, pz, pw);
-      const double ddx = xsub(ax, px), ddy = xsub(ay, py), ddz = xsub(az, pz);
-      const double r2 = fma(ddz, ddz, fma(ddy, ddy, ddx * ddx));
-      if (decide<false>(P, par, kk, jj, ax, ay, az, px, py, pz, ddx, ddy, ddz, r2) != 2) continue;
-      double q[4];
-      if (guard_force(Pp, d, jj, __ldg(tgt + jj), ddx, ddy, ddz, adf + pw, false, q)) {
-        fx -= q[0];
-        fy -= q[1];
-        fz -= q[2];
-        e += q[3];
-      }
-    }
-  }
-  if (occ) {
-    red_add(&P.frc[d], fx);
-    red_add(&P.frc[S + d], fy);
-    red_add(&P.frc[2 * S + d], fz);
-  }
-  return e;
-}
-
 // one pair-energy partial per CTA: warp sums, then the warps in order
 // (deterministic for a given grid)
 template <int NT>
@@ -1178,10 +1059,6 @@ __global__ void __launch_bounds__(NT, 1) k_force_lean_smem(KP P, int nsb) {
     const bool live = unit_cell(G, u, lane, w, c);
     const bool deep = live && unit_deep(G, u, lane, w, FULL);
     for (int par = 0; par < 2; ++par)
-      if (!FULL && !REV && TB == kTabSplit3 && NT == 640)
-        e += force_site_ilp2(P, P.dself, par, live ? (int)(par * G.NC + c) : 0, live,
-                             smem_addr(T), seg_lo, deep, tb8);
-      else
       e += force_site_lean<FULL, TB, REV>(P, P.dself, par, live ? (int)(par * G.NC + c) : 0,
                                           live, smem_addr(T), seg_lo, near_halo(G, u, w), deep,
                                           tb8);
@@ -1298,16 +1175,6 @@ void launch_force_lean(const KP& P, int mode, cudaStream_t s) {
   // 896 threads (72 registers, 28 warps) measured ahead of 1024 (64
   // registers, spills) at config 5 too: 7.27 vs 7.38-7.54 ms
   const int nt = nt_env ? nt_env : 896;
-  if (nt == 640 && !mode && !P.rev.on && TB == kTabSplit3) {
-    static bool a640 = false;
-    if (!a640) {
-      cudaFuncSetAttribute((const void*)k_force_lean_smem<false, 640, TB, false>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-      a640 = true;
-    }
-    launch_pdl(k_force_lean_smem<false, 640, TB, false>, g + 4, 640, bytes, s, P, g);
-    return;
-  }
   if (nt == 896 && !mode) {
     if (P.rev.on)
       launch_pdl(k_force_lean_smem<false, 896, TB, true>, g + 4, 896, bytes, s, P, g);
