@@ -182,6 +182,11 @@ CBX_API cbx_status cbx_last_timings(cbx_ctx* ctx, double out_ms[8]);
 CBX_API cbx_status cbx_enable_timing(cbx_ctx* ctx, int on);
 CBX_API cbx_status cbx_count_pairs(cbx_ctx* ctx, uint64_t out[2]);
 CBX_API cbx_status cbx_kernel_launches(cbx_ctx* ctx, uint64_t* n); /* cumulative */
+/* skin-candidate counters of the density passes run while counting is on:
+ * enable = 1 zeroes them and starts counting, 0 stops; out = {skin candidates
+ * examined, skin candidates listed} (the regional displacement bound prunes
+ * the difference; site slots of live lanes, vacant ones included) */
+CBX_API cbx_status cbx_skin_stats(cbx_ctx* ctx, int enable, uint64_t out[2]);
 /* JSON description of the context's kernel configuration */
 /* Device bytes by structure (the CLI's bench-mem, tools/src/main.cpp:72-115):
  * out[k] for k < CBX_MEM_CATEGORIES, then slots, clash capacity, ghost

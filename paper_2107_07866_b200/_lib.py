@@ -141,6 +141,7 @@ SIGNATURES = [
     ("cbx_last_timings", C.c_int, [_P, C.POINTER(C.c_double)]),
     ("cbx_enable_timing", C.c_int, [_P, C.c_int]),
     ("cbx_count_pairs", C.c_int, [_P, C.POINTER(C.c_uint64)]),
+    ("cbx_skin_stats", C.c_int, [_P, C.c_int, C.POINTER(C.c_uint64)]),
     ("cbx_kernel_launches", C.c_int, [_P, C.POINTER(C.c_uint64)]),
     ("cbx_describe", C.c_int, [_P, C.c_char_p, C.c_long]),
     ("cbx_slab_p2p_fused", C.c_int, [_P]),

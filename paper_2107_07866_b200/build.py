@@ -39,17 +39,32 @@ def build(force: bool = False, verbose: bool = False, ab: bool = False) -> str:
     out = AB_LIB if ab else LIB
     if not ab and not force and not stale():
         return LIB
-    cmd = [nvcc()] + ARCH + FLAGS + (["-DCBX_AB"] if ab else []) + ["-shared", "-o", out] + \
-        [os.path.join(CSRC, s) for s in SOURCES]
-    r = subprocess.run(cmd, capture_output=True, text=True)
+    # one object per translation unit, compiled in parallel, then linked
+    import concurrent.futures as cf
+    import tempfile
+    tmp = tempfile.mkdtemp(prefix="cbx_build_")
+    extra = ["-DCBX_AB"] if ab else []
+    objs = [os.path.join(tmp, os.path.splitext(s)[0] + ".o") for s in SOURCES]
+    cmds = [[nvcc()] + ARCH + FLAGS + extra + ["-c", "-o", o, os.path.join(CSRC, s)]
+            for s, o in zip(SOURCES, objs)]
+    link = [nvcc()] + ARCH + ["-shared", "-cudart", "static", "-ldl", "-o", out] + objs
+    with cf.ThreadPoolExecutor(max_workers=len(cmds)) as ex:
+        rs = list(ex.map(lambda c: subprocess.run(c, capture_output=True, text=True), cmds))
     log = os.path.join(HERE, "build.log")
+    text = "".join(" ".join(c) + "\n" + r.stdout + r.stderr for c, r in zip(cmds, rs))
+    bad = [r for r in rs if r.returncode != 0]
+    if not bad:
+        r = subprocess.run(link, capture_output=True, text=True)
+        text += " ".join(link) + "\n" + r.stdout + r.stderr
+        if r.returncode != 0:
+            bad = [r]
     with open(log, "w") as f:
-        f.write(" ".join(cmd) + "\n" + r.stdout + r.stderr)
-    if r.returncode != 0:
-        sys.stderr.write(r.stderr[-6000:])
+        f.write(text)
+    if bad:
+        sys.stderr.write(bad[0].stderr[-6000:])
         raise RuntimeError(f"nvcc failed (see {log})")
     if verbose:
-        sys.stderr.write(r.stderr)
+        sys.stderr.write(text)
     return out
 
 

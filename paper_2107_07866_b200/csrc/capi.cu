@@ -810,6 +810,9 @@ void do_upload(cbx_ctx* c, const cbx_store* s) {
       c->P, H, s->vel != nullptr, s->force != nullptr, s->rho != nullptr, s->df != nullptr,
       s->tag != nullptr, s->valid != nullptr, s->ghost != nullptr);
   c->launches += 1;
+  // new positions: no regional displacement bound is valid until the next
+  // k_kick_drift + pass 2 publish one
+  if (c->P.ustamp) cudaMemsetAsync(c->P.ustamp, 0, sizeof(unsigned long long), st);
   auto site_live = [&](long long id) {
     return (s->valid ? s->valid[id] != 0 : true) && !(s->ghost && s->ghost[id]);
   };
@@ -991,6 +994,37 @@ void setup_fast(cbx_ctx* c) {
   cuda_check(cudaMemcpy(dfd, fd.data(), fd.size() * 8, cudaMemcpyHostToDevice), "fast table");
   cuda_check(cudaMemcpy(dff, ff.data(), ff.size() * 8, cudaMemcpyHostToDevice), "fast table");
   P.fd.rec = dfd;
+  {  // fp64 [A B] pairs (shared-memory window) and the [C D] pairs bound to
+     // a texture (int4 texels) for the default density pass
+    std::vector<double> ab(2 * (n + 1)), cd(2 * (n + 1));
+    for (int i = 0; i <= n; ++i) {
+      ab[2 * i] = fd[4 * i];
+      ab[2 * i + 1] = fd[4 * i + 1];
+      cd[2 * i] = fd[4 * i + 2];
+      cd[2 * i + 1] = fd[4 * i + 3];
+    }
+    double* dab = c->alloc<double>(ab.size());
+    cuda_check(cudaMemcpy(dab, ab.data(), ab.size() * 8, cudaMemcpyHostToDevice), "fast table");
+    P.fdab = dab;
+    double* dcd = c->alloc<double>(cd.size());
+    cuda_check(cudaMemcpy(dcd, cd.data(), cd.size() * 8, cudaMemcpyHostToDevice), "fast table");
+    cudaResourceDesc rd{};
+    rd.resType = cudaResourceTypeLinear;
+    rd.res.linear.devPtr = dcd;
+    rd.res.linear.desc = cudaCreateChannelDesc<int4>();
+    rd.res.linear.sizeInBytes = cd.size() * sizeof(double);
+    cudaTextureDesc td{};
+    td.readMode = cudaReadModeElementType;
+    cudaTextureObject_t tex = 0;
+    cuda_check(cudaCreateTextureObject(&tex, &rd, &td, nullptr), "density record texture");
+    P.tex_fd4 = (unsigned long long)tex;
+    c->textures.push_back(tex);
+    rd.res.linear.devPtr = dab;
+    rd.res.linear.sizeInBytes = ab.size() * sizeof(double);
+    cuda_check(cudaCreateTextureObject(&tex, &rd, &td, nullptr), "density record texture");
+    P.tex_fab64 = (unsigned long long)tex;
+    c->textures.push_back(tex);
+  }
   P.fd.ih = 1.0 / de.h;
   P.fd.c0 = -de.x0 / de.h;
   P.fd.nseg = n;
@@ -1078,6 +1112,16 @@ void setup_fast(cbx_ctx* c) {
       cudaTextureObject_t tex = 0;
       cuda_check(cudaCreateTextureObject(&tex, &rd, &td, nullptr), "density table texture");
       P.tex_fd = (unsigned long long)tex;
+      c->textures.push_back(tex);
+      // its own allocation: texture memory starts on the texture alignment
+      double* dabf = c->alloc<double>(n + 1);
+      cuda_check(cudaMemcpy(dabf, &dc[2 * (n + 1)], 8 * (size_t)(n + 1), cudaMemcpyHostToDevice),
+                 "fast table");
+      rd.res.linear.devPtr = dabf;
+      rd.res.linear.desc = cudaCreateChannelDesc<int2>();
+      rd.res.linear.sizeInBytes = 8 * (size_t)(n + 1);
+      cuda_check(cudaCreateTextureObject(&tex, &rd, &td, nullptr), "density table texture");
+      P.tex_fab = (unsigned long long)tex;
       c->textures.push_back(tex);
     }
   }
@@ -1308,6 +1352,7 @@ static cbx_status create_impl(const cbx_box* box, const cbx_potential* pot,
     std::vector<int> hd[2], fd[2];
     std::vector<long long> ff[2];
     int hin[2] = {0, 0}, fin[2] = {0, 0};
+    SkinGroups skh[2], skf[2];
     for (int par = 0; par < 2; ++par) {
       auto delta = [&](const Offset& o) {
         const int q = par ^ o.cross;
@@ -1319,18 +1364,26 @@ static cbx_status create_impl(const cbx_box* box, const cbx_potential* pot,
         const double x = o.dx + h, y = o.dy + h, z = o.dz + h;
         return (x * x + y * y + z * z) * box->a0 * box->a0;
       };
-      auto order = [&](std::vector<Offset> v, int& nin) {
+      auto order = [&](std::vector<Offset> v, int& nin, SkinGroups& sg) {
         std::stable_sort(v.begin(), v.end(),
                          [&](const Offset& a, const Offset& b) { return dist2(a) < dist2(b); });
         nin = 0;
         for (const Offset& o : v)
           if (dist2(o) <= pot->cutoff * pot->cutoff) ++nin;
+        // skin shells (equal lattice distance) beyond nin, at most 4 groups:
+        // the last one takes every remaining shell at its smallest distance
+        sg = SkinGroups{};
+        for (int k = nin; k < (int)v.size(); ++k) {
+          const bool fresh = k == nin || dist2(v[k]) != dist2(v[k - 1]);
+          if (fresh && sg.n < 4) sg.len[sg.n++] = std::sqrt(dist2(v[k]));
+          sg.end[sg.n - 1] = k + 1;
+        }
         return v;
       };
-      for (const Offset& o : order(c->offs.half[par], hin[par])) {
+      for (const Offset& o : order(c->offs.half[par], hin[par], skh[par])) {
         hd[par].push_back(delta(o));
       }
-      for (const Offset& o : order(c->offs.full[par], fin[par])) {
+      for (const Offset& o : order(c->offs.full[par], fin[par], skf[par])) {
         fd[par].push_back(delta(o));
         ff[par].push_back(o.flat);
       }
@@ -1389,6 +1442,11 @@ static cbx_status create_impl(const cbx_box* box, const cbx_potential* pot,
     KP& P = c->P;
     P.G = G;
     P.S = S;
+    for (int par = 0; par < 2; ++par) {
+      P.skh[par] = skh[par];
+      P.skf[par] = skf[par];
+    }
+    P.nin64 = std::max(std::max(hin[0], hin[1]), std::max(fin[0], fin[1])) <= 64;
     P.accel = accel_factor();
     P.mv2 = mv2_to_ev();
     c->mem_cat = CBX_MEM_SLOTS;
@@ -1490,7 +1548,22 @@ static cbx_status create_impl(const cbx_box* box, const cbx_potential* pot,
                                                          : nullptr;
     }
 
+    // regional displacement bounds (density-pass skin pruning): rows of
+    // whole 32-cell chunks only
+    P.ub = nullptr;
+    P.ustamp = nullptr;
+    if (G.bx % 32 == 0 && G.g <= 32 && ab_flag("CBX_SKIN_PRUNE", 1)) {
+      c->mem_cat = CBX_MEM_SLOTS;
+      P.ub = c->alloc<unsigned long long>(G.NI / 32);
+      cudaMemset(P.ub, 0, (G.NI / 32) * sizeof(unsigned long long));
+      c->mem_cat = CBX_MEM_REDUCTION;
+      P.ustamp = c->alloc<unsigned long long>(2);
+      const unsigned long long st0[2] = {0ull, 1ull};
+      cudaMemcpy(P.ustamp, st0, sizeof(st0), cudaMemcpyHostToDevice);
+    }
     c->mem_cat = CBX_MEM_REDUCTION;
+    P.skin_cnt = c->alloc<unsigned long long>(3);
+    cudaMemset(P.skin_cnt, 0, 3 * sizeof(unsigned long long));
     c->d_defects = c->alloc<unsigned long long>(4);
     // empty store: every slot vacant
     std::vector<double4> vac(S, make_double4(kVacant, kVacant, kVacant, 0.0));
@@ -2328,6 +2401,22 @@ CBX_API cbx_status cbx_last_timings(cbx_ctx* c, double out_ms[8]) {
     for (int i = 0; i < 8; ++i) out_ms[i] = c->t_ms[i];
   });
 }
+CBX_API cbx_status cbx_skin_stats(cbx_ctx* c, int enable, uint64_t out[2]) {
+  return guarded(c, [&] {
+    cudaSetDevice(c->device);
+    unsigned long long h[3];
+    cuda_check(cudaMemcpyAsync(h, c->P.skin_cnt, sizeof h, cudaMemcpyDeviceToHost, c->stream),
+               "skin stats");
+    cuda_check(cudaStreamSynchronize(c->stream), "skin stats");
+    out[0] = h[0];
+    out[1] = h[1];
+    const unsigned long long z[3] = {0ull, 0ull, enable ? 1ull : 0ull};
+    if (enable) cudaMemcpyAsync(c->P.skin_cnt, z, sizeof z, cudaMemcpyHostToDevice, c->stream);
+    else cudaMemcpyAsync(c->P.skin_cnt + 2, z + 2, sizeof z[2], cudaMemcpyHostToDevice, c->stream);
+    cuda_check(cudaStreamSynchronize(c->stream), "skin stats");
+  });
+}
+
 CBX_API cbx_status cbx_count_pairs(cbx_ctx* c, uint64_t out[2]) {
   return guarded(c, [&] {
     cudaSetDevice(c->device);

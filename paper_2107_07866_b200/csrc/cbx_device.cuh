@@ -123,8 +123,34 @@ __host__ __device__ __forceinline__ int dens_window_lo_cmp(int nseg) {
   return ((lo > 0 ? lo : 0) + 1) & ~1;
 }
 
+// Regional displacement bound (density-pass skin pruning).  One entry per
+// chunk of 32 interior cells of an x row (both sublattices), written by
+// k_kick_drift: (stamp << kUbShift) | q, q >= |u| * kUbScale for every atom of
+// the chunk, u = its position minus its own site's lattice position.  A chunk
+// whose atom left the fast hash (wrap / new site) or received an atom in
+// update_hash pass 2 carries kUbQMax ("unbounded").  ustamp[0] is the stamp
+// the density pass accepts (0: no valid bounds), ustamp[1] the stamp of the
+// next k_kick_drift; k_rehash(_images) publishes it after pass 2.
+constexpr int kUbShift = 24;
+constexpr unsigned long long kUbQMax = (1ull << kUbShift) - 1;
+constexpr double kUbScale = 65536.0;  // q in units of 2^-16 A
+constexpr double kUbDirty = 1e300;    // per-site marker: no bound
+// skin shells of an offset list: offsets [nin, end[0]) have lattice
+// distance len[0] (A), [end[0], end[1]) at least len[1], ... (ascending)
+struct SkinGroups {
+  double len[4];
+  int end[4];
+  int n;
+};
+
 struct KP {
   Geo G;
+  unsigned long long* ub;      // regional displacement bounds (null: off)
+  unsigned long long* ustamp;  // [2]
+  SkinGroups skh[2], skf[2];   // half / full lists per sublattice
+  // [3]: skin candidates examined / listed by the density pass, counting on
+  // (cbx_skin_stats; a device word, so captured step graphs see it)
+  unsigned long long* skin_cnt;
   RevHalo rev;
   P2PLinks* lk;  // device copy of the peer links (fused reverse halo signals)
   int rev_wait;  // per launch: wait for the neighbours' flags of this exchange first
@@ -141,6 +167,15 @@ struct KP {
   // compressed density records: [D C] (16 B) then, after the last record,
   // [A B as fp32] (8 B) per record; null when the fp32 rounding bound fails
   const double* fdc;
+  // fp64 density records for the density pass: [A B] pairs (16 B per
+  // record, staged in shared memory) and the [C D] pairs bound to a texture
+  // (one int4 texel per record); nin64: every inner list fits one 64-bit
+  // mask word
+  const double* fdab;
+  unsigned long long tex_fd4;
+  unsigned long long tex_fab;    // the compressed records' fp32 [A B] (int2 texels)
+  unsigned long long tex_fab64;  // fdab (int4 texels)
+  int nin64;
   FastTab fe;      // embedding F(rho): 4 doubles/segment (A B C D), padded
   float band_hi, band_lo;  // fp32 r^2 filter: reject above hi, exact test in [lo, hi]
   double guard_r2;         // below: overlap / short-range guard path

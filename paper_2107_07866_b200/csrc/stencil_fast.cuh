@@ -245,12 +245,16 @@ __device__ __forceinline__ int smem_slot32(int i, int c) { return 2 * i + (c ^ (
 
 // CMPD: 0 the fp64 32-byte records of the window in shared memory; 1 the
 // compressed records ([D C] fp64 + [A B] fp32) in shared memory; 2 compressed,
-// [D C] by texture fetch (TEX pipe) and [A B] in shared memory (LSU pipe)
+// [D C] by texture fetch (TEX pipe) and [A B] in shared memory (LSU pipe);
+// 3-6: the inner loop unrolled by two with alternating register sets (no
+// copies) and a one-word pair mask; tables: 3 fp64 [A B] (16 B) in shared
+// memory + [C D] by texture, 4 (default where the fp32 guard holds) those of
+// 2, 5 both halves of 2 by texture, 6 both fp64 halves by texture
 template <bool FULL, int B, bool SMEM = false, bool REV = false, int CMPD = 0>
 __device__ __forceinline__ void density_site(const KP& P, KP* Pp, int par, int d, bool live,
                                              unsigned tb = 0, int seg_lo = 0,
                                              bool rev_here = true, bool deep = false,
-                                             unsigned tb8 = 0) {
+                                             unsigned tb8 = 0, int n_lim = kMaxOffsets) {
   const double4* __restrict__ pdf = P.pdf;
   const int* __restrict__ tgt = P.tgt;
   double ax = kVacant, ay = 0, az = 0, aw = 0;
@@ -259,7 +263,9 @@ __device__ __forceinline__ void density_site(const KP& P, KP* Pp, int par, int d
     if (FULL && live) P.rho[d] = 0.0;
     return;
   }
-  const int n = FULL ? c_full_n[par] : c_half_n[par];
+  // n_lim: skin shells beyond it are out of cutoff for every lane (regional
+  // displacement bound, skin_end)
+  const int n = min(FULL ? c_full_n[par] : c_half_n[par], n_lim);
   const int nin = FULL ? c_full_nin[par] : c_half_nin[par];
   const int* offs = FULL ? c_full[par] : c_half[par];
   const double lo = P.cut2_lo, g2 = P.guard_r2;
@@ -269,7 +275,83 @@ __device__ __forceinline__ void density_site(const KP& P, KP* Pp, int par, int d
   // compare, the near-cutoff / guard cases drop to decide().  B == 1 (the
   // shared-memory kernels): software-pipelined, the next candidate's gather
   // is in flight while the current one's table lookup and RED run
-  if constexpr (B == 1) {
+  if constexpr (B == 1 && CMPD >= 3) {
+    // one inner candidate once its partner is loaded (nin <= 64: host check)
+    auto cand = [&](int k, int j, int t, double px, double py, double pz) {
+      const double dx = xsub(ax, px), dy = xsub(ay, py), dz = xsub(az, pz);
+      const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+      bool in = r2 <= lo && r2 >= g2;
+      if (!in && r2 <= P.cut2_hi) {
+        const int st = decide<FULL>(P, par, k, j, ax, ay, az, px, py, pz, dx, dy, dz, r2);
+        if (st == 1) {
+          in = true;
+        } else if (st == 2) {
+          m1 |= kGuardBit;
+          acc += guard_rho(Pp, d, j, t, dx, dy, dz, FULL);
+        }
+      }
+      if (in) {
+        double sv;
+        const int sg = seg_index(P.fd, r2 * rsqrt_nr(r2), sv);
+        const int li = sg - seg_lo;
+        double tA, tB, tC, tD;
+        if (CMPD == 5) {  // both halves by texture: [D C] fp64, [A B] fp32
+          const double2 dc = tex_rec16(P.tex_fd, sg);
+          const int2 q = tex1Dfetch<int2>((cudaTextureObject_t)P.tex_fab, sg);
+          tA = (double)__int_as_float(q.x);
+          tB = (double)__int_as_float(q.y);
+          tC = dc.y;
+          tD = dc.x;
+        } else if (CMPD == 6) {  // both halves by texture, fp64
+          const double2 ab = tex_rec16(P.tex_fab64, sg);
+          const double2 cd = tex_rec16(P.tex_fd4, sg);
+          tA = ab.x;
+          tB = ab.y;
+          tC = cd.x;
+          tD = cd.y;
+        } else if (li >= 0 && CMPD == 4) {  // the compressed records of CMPD 2
+          const double2 dc = tex_rec16(P.tex_fd, sg);
+          const float2 ab = lds_f2(tb8 + 8 * li);
+          tA = (double)ab.x;
+          tB = (double)ab.y;
+          tC = dc.y;
+          tD = dc.x;
+        } else if (li >= 0) {
+          const double2 ab = lds2(tb + 16 * li);
+          const double2 cd = tex_rec16(P.tex_fd4, sg);
+          tA = ab.x;
+          tB = ab.y;
+          tC = cd.x;
+          tD = cd.y;
+        } else {
+          ld256(P.fd.rec + 4 * (size_t)sg, tA, tB, tC, tD);
+        }
+        const double rho = fma(fma(fma(tA, sv, tB), sv, tC), sv, tD);
+        acc += rho;
+        if (!FULL) red_add(REV && rev_here ? acc_ptr_up(P, t, -1) : P.rho + t, rho);
+      }
+      m0 |= (unsigned long long)in << k;
+    };
+    int ja = d + offs[0], jb;
+    double xa, ya, za, wa, xb, yb, zb, wb;
+    ld256(pdf + ja, xa, ya, za, wa);
+    int ta = deep ? ja : __ldg(tgt + ja), tq;
+    int k = 0;
+#pragma unroll 1
+    for (; k + 1 < nin; k += 2) {
+      jb = d + offs[k + 1];
+      ld256(pdf + jb, xb, yb, zb, wb);
+      tq = deep ? jb : __ldg(tgt + jb);
+      cand(k, ja, ta, xa, ya, za);
+      if (k + 2 < nin) {
+        ja = d + offs[k + 2];
+        ld256(pdf + ja, xa, ya, za, wa);
+        ta = deep ? ja : __ldg(tgt + ja);
+      }
+      cand(k + 1, jb, tq, xb, yb, zb);
+    }
+    if (k < nin) cand(k, ja, ta, xa, ya, za);
+  } else if constexpr (B == 1) {
     int jn = d + offs[0];
     double qx, qy, qz, qw;
     ld256(pdf + jn, qx, qy, qz, qw);
@@ -872,6 +954,61 @@ __device__ __forceinline__ int next_unit(int* s_ctr, int group, int nsb, int nu,
   return u < unit_lo(blockIdx.x + 1, nsb, nu) ? u : nu;
 }
 
+// Skin pruning by the regional displacement bounds (cbx_device.cuh).  For a
+// pair of sites at lattice distance R whose atoms are displaced by u_i and u_j
+// from them, r = |R + u_j - u_i| >= R - |u_i| - |u_j|.  Every atom a warp's
+// lanes pair with (its own site included) lies in the chunks of planes z..z+g
+// (z-g..z+g with full lists), rows y-g..y+g and x chunks xs-1..xs+1; with U the
+// largest bound among them, a skin shell with R > cutoff + 2U + margin is out
+// of cutoff for every lane, whatever the reference's rounding (margin 1e-9 A
+// against rounding errors of ~1e-12 A in r and u).  Returns the largest R
+// still to examine (+inf when a chunk is unbounded, stale or in a z halo of a
+// slab rank).  Rows holding whole chunks (bx % 32 == 0) only: P.ub is null
+// otherwise.
+template <bool FULL>
+__device__ __forceinline__ double skin_threshold(const KP& P, int u, int w,
+                                                 unsigned long long cur) {
+  if (!cur) return 1e300;
+  const Geo& G = P.G;
+  int zb;
+  const int st = unit_strip(G, u, zb);
+  const int nxs = G.bx >> 5;
+  const int y = st / nxs, xs = st - y * nxs, z = zb * 4 + w;
+  const int g = G.g, ny = 2 * g + 1, nz = FULL ? 2 * g + 1 : g + 1;
+  const int total = nz * ny * 3;
+  unsigned long long q = 0;
+  for (int i = threadIdx.x & 31; i < total; i += 32) {
+    const int iz = i / (ny * 3), r = i - iz * ny * 3, iy = r / 3, ix = r - iy * 3;
+    int zz = z + iz - (FULL ? g : 0);
+    int yy = y + iy - g, xx = xs + ix - 1;
+    yy = ((yy % G.by) + G.by) % G.by;
+    xx = ((xx % nxs) + nxs) % nxs;
+    if (zz < 0 || zz >= G.bz) {
+      if (G.slab) {
+        q = kUbQMax;
+        continue;
+      }
+      zz = ((zz % G.bz) + G.bz) % G.bz;
+    }
+    const unsigned long long e = __ldcg(P.ub + ((size_t)zz * G.by + yy) * nxs + xx);
+    q = max(q, (e >> kUbShift) == cur ? (e & kUbQMax) : kUbQMax);
+  }
+  const unsigned qm = __reduce_max_sync(0xffffffffu, (unsigned)q);
+  if (qm >= (unsigned)kUbQMax) return 1e300;
+  return P.cutoff + 1e-9 + 2.0 * (double)qm / kUbScale;
+}
+// end of the offsets a site of sublattice par examines for threshold T
+template <bool FULL>
+__device__ __forceinline__ int skin_end(const KP& P, int par, double T) {
+  const SkinGroups& sg = FULL ? P.skf[par] : P.skh[par];
+  int n = FULL ? c_full_nin[par] : c_half_nin[par];
+  for (int i = 0; i < sg.n; ++i) {
+    if (sg.len[i] > T) return n;
+    n = sg.end[i];
+  }
+  return kMaxOffsets;
+}
+
 // density pass with the upper rho-spline window in shared memory (32-byte
 // records): NT threads = NT/128 groups of 4 warps, one CTA per SM; B = 1
 // (one candidate per iteration) keeps the thread at 64 registers
@@ -895,21 +1032,32 @@ __global__ void __launch_bounds__(NT, 1) k_density_smem(KP P, int nsb) {
   if (threadIdx.x == 0) s_ctr = 0;
   // an even first record: the fp32 [A B] pairs (8 bytes each) are then
   // 16-byte aligned for the bulk copy
-  const int seg_lo = CMPD ? dens_window_lo_cmp(nseg) : max(0, nseg + 1 - kDensTabRecords);
+  // 4: the tables of 2, the loop of 3; 5, 6: no shared-memory window
+  constexpr int CM = CMPD == 4 ? 2 : CMPD;
+  const int seg_lo = CM == 3 ? max(0, nseg + 1 - kDensTabRecords)
+                     : CM ? dens_window_lo_cmp(nseg) : max(0, nseg + 1 - kDensTabRecords);
   const int nrec = nseg + 1 - seg_lo;
   const double2* src = reinterpret_cast<const double2*>(P.fd.rec + 4 * (size_t)seg_lo);
   // the constant table is staged while the predecessor drains (PDL)
   // 24-byte records: [D C] 16-byte slots, then the fp32 [A B] pairs
   // (CMPD 2: only the [A B] pairs are staged, from offset 0)
-  double2* T8 = CMPD == 2 ? T : T + kDensTabRecords;  // byte offset 16 x kDensTabRecords
+  double2* T8 = CM == 2 ? T : T + kDensTabRecords;  // byte offset 16 x kDensTabRecords
   __shared__ __align__(8) unsigned long long s_mbar;
-  if (CMPD) {  // two bulk copies ([A B] rounded up to 16 bytes: the table is padded)
+  if (CM >= 5) {
+  } else if (CM == 3) {  // the window's fp64 [A B] pairs, one bulk copy
+    if (threadIdx.x == 0) {
+      const unsigned mb = smem_addr(&s_mbar);
+      mbar_init(mb);
+      mbar_expect_tx(mb, 16u * nrec);
+      bulk_stage(smem_addr(T), P.fdab + 2 * (size_t)seg_lo, 16u * nrec, mb);
+    }
+  } else if (CMPD) {  // two bulk copies ([A B] rounded up to 16 bytes: the table is padded)
     const int N1 = nseg + 1;
     const unsigned mb = smem_addr(&s_mbar);
     if (threadIdx.x == 0) {
       const unsigned b16 = 16u * nrec, b8 = (8u * nrec + 15u) & ~15u;
       mbar_init(mb);
-      if (CMPD == 2) {
+      if (CM == 2) {
         mbar_expect_tx(mb, b8);
       } else {
         mbar_expect_tx(mb, b16 + b8);
@@ -921,7 +1069,7 @@ __global__ void __launch_bounds__(NT, 1) k_density_smem(KP P, int nsb) {
     for (int q = threadIdx.x; q < 2 * nrec; q += blockDim.x) T[smem_slot32(q >> 1, q & 1)] = __ldg(src + q);
   }
   __syncthreads();  // the barrier's initialisation is visible
-  if (CMPD) mbar_wait0(smem_addr(&s_mbar));
+  if (CMPD && CM < 5) mbar_wait0(smem_addr(&s_mbar));
   pdl_wait();
   pdl_trigger();
   if (P.st->err || P.st->halt) return;
@@ -929,16 +1077,31 @@ __global__ void __launch_bounds__(NT, 1) k_density_smem(KP P, int nsb) {
   const int lt = threadIdx.x & 127, lane = lt & 31, w = lt >> 5;
   const Geo& G = P.G;
   const int nu = unit_count(G);
+  // stamp of the regional displacement bounds this pass may use (0: none)
+  const unsigned long long ub_cur = P.ub ? __ldcg(P.ustamp) : 0ull;
+  const bool cnt_skin = __ldcg(P.skin_cnt + 2) != 0;
   for (;;) {
     const int u = next_unit(&s_ctr, group, nsb, nu, s_slot);
     if (u >= nu) break;
     int c;
     const bool live = unit_cell(G, u, lane, w, c);
     const bool deep = live && unit_deep(G, u, lane, w, FULL);
-    for (int par = 0; par < 2; ++par)
+    const double skT = skin_threshold<FULL>(P, u, w, ub_cur);
+    for (int par = 0; par < 2; ++par) {
+      const int n_lim = skin_end<FULL>(P, par, skT);
       density_site<FULL, B, true, REV, CMPD>(P, P.dself, par, live ? (int)(par * G.NC + c) : 0,
                                              live, smem_addr(T), seg_lo, near_halo(G, u, w),
-                                             deep, smem_addr(T8));
+                                             deep, smem_addr(T8), n_lim);
+      if (cnt_skin) {  // diagnostic (cbx_skin_stats)
+        const unsigned nl = __popc(__ballot_sync(0xffffffffu, live));
+        if (lane == 0) {
+          const int nf = FULL ? c_full_n[par] : c_half_n[par];
+          const int ni = FULL ? c_full_nin[par] : c_half_nin[par];
+          atomicAdd(P.skin_cnt, (unsigned long long)(min(nf, n_lim) - ni) * nl);
+          atomicAdd(P.skin_cnt + 1, (unsigned long long)(nf - ni) * nl);
+        }
+      }
+    }
   }
 }
 
@@ -1098,7 +1261,8 @@ static int sm_count() {
 // density_site); returns true when the clash-record pass ran in the launch
 template <int CMPD>
 bool launch_density_smem(const KP& P, int mode, cudaStream_t s) {
-  const size_t bytes = (size_t)kDensTabRecords * (CMPD == 2 ? 8 : CMPD == 1 ? 24 : 32);
+  const size_t bytes = CMPD >= 5 ? 16 :
+      (size_t)kDensTabRecords * (CMPD == 3 ? 16 : CMPD >= 2 ? 8 : CMPD == 1 ? 24 : 32);
   static bool attr = false;
   if (!attr) {
     for (const void* k : {(const void*)k_density_smem<false, 1, 1024, false, CMPD>,
@@ -1123,11 +1287,18 @@ bool launch_density_smem(const KP& P, int mode, cudaStream_t s) {
   return !mode;
 }
 int density_table_mode(const KP& P) {
-  // compressed records when the local fp32 guard held (P.fdc): [D C] through
-  // the texture path, [A B] in shared memory (CBX_DENSITY_TAB=1: both in
-  // shared memory, 0.8 % slower at config 5 -- the LSU pipe is the binding one)
-  static const int tm = ab_flag("CBX_DENSITY_TAB", 2);
-  return P.fdc ? tm : 0;
+  // default: the unrolled inner loop (needs the inner offsets in one 64-bit
+  // mask word) with the compressed records where the local fp32 guard held
+  // (P.fdc: [D C] by texture, fp32 [A B] in shared memory -- 4), else fp64
+  // [A B] in shared memory and [C D] by texture (3).  Measured at config 5
+  // (A/B, same box): 4: 4.31 ms; 5 (both halves by texture): 4.33; 3: 4.63;
+  // 6 (fp64, both by texture): 4.67; 2 (round-2 loop, tables of 4): 4.54
+  static const int tm = ab_flag("CBX_DENSITY_TAB", -1);
+  if (tm < 0) return P.nin64 ? (P.fdc ? 4 : 3) : (P.fdc ? 2 : 0);
+  if (tm == 3) return P.nin64 ? 3 : 0;
+  if (tm == 4 || tm == 5) return P.nin64 && P.fdc ? tm : 0;
+  if (tm == 6) return P.nin64 ? 6 : 0;
+  return tm && P.fdc ? tm : 0;
 }
 
 // density pass: the lean 1024-thread kernel with the rho-spline window in
@@ -1138,6 +1309,10 @@ bool launch_density_fast(const KP& P, int mode, int grid, cudaStream_t s) {
   static const int dsm = ab_flag("CBX_DENSITY_SMEM", 1);
   if (dsm) {
     const int tm = density_table_mode(P);
+    if (tm == 3) return launch_density_smem<3>(P, mode, s);
+    if (tm == 4) return launch_density_smem<4>(P, mode, s);
+    if (tm == 5) return launch_density_smem<5>(P, mode, s);
+    if (tm == 6) return launch_density_smem<6>(P, mode, s);
     if (tm == 2) return launch_density_smem<2>(P, mode, s);
     if (tm == 1) return launch_density_smem<1>(P, mode, s);
     return launch_density_smem<0>(P, mode, s);

@@ -73,18 +73,20 @@ __device__ __forceinline__ void kick_drift_load(const KP& P, int vb, KdSite& a) 
 }
 __device__ __forceinline__ void kick_drift_proc(const KP& P, int move, int zero_acc, int images,
                                                 double dt, double hk, bool k2, double& v2s,
-                                                double& v2m, const KdSite& a);
+                                                double& v2m, const KdSite& a, double& ub2);
 // one site per thread of virtual block vb (128 cells x 2 sublattices)
 __device__ __forceinline__ void kick_drift_site(const KP& P, int move, int zero_acc, int images,
                                                 int vb, double dt, double hk, bool k2,
-                                                double& v2s, double& v2m) {
+                                                double& v2s, double& v2m, double& ub2) {
   KdSite a;
   kick_drift_load(P, vb, a);
-  if (a.live) kick_drift_proc(P, move, zero_acc, images, dt, hk, k2, v2s, v2m, a);
+  if (a.live) kick_drift_proc(P, move, zero_acc, images, dt, hk, k2, v2s, v2m, a, ub2);
 }
+// ub2: |u|^2 of the site's atom relative to its own lattice site (fast hash),
+// kUbDirty when it took the wrap / nearest_site path, unchanged when vacant
 __device__ __forceinline__ void kick_drift_proc(const KP& P, int move, int zero_acc, int images,
                                                 double dt, double hk, bool k2, double& v2s,
-                                                double& v2m, const KdSite& a) {
+                                                double& v2m, const KdSite& a, double& ub2) {
   const long long S = P.S;
   const long long d = a.d;
   const int i = (int)d;
@@ -133,11 +135,14 @@ __device__ __forceinline__ void kick_drift_proc(const KP& P, int move, int zero_
   // Wigner-Seitz ball of its own interior site: the rounded corner / centre
   // candidates are that site and no wrap applies)
   bool near_own = false;
+  ub2 = kUbDirty;
   if (P.hash_r2 > 0.0) {
     const double h = 0.5 * par;
     const double ux = p.x - ((double)cx + h) * P.G.a0, uy = p.y - ((double)cy + h) * P.G.a0,
                  uz = p.z - ((double)(cz + P.G.zoff) + h) * P.G.a0;
-    near_own = fma(ux, ux, fma(uy, uy, uz * uz)) < P.hash_r2;
+    const double u2 = fma(ux, ux, fma(uy, uy, uz * uz));
+    near_own = u2 < P.hash_r2;
+    if (near_own) ub2 = u2;
   }
   if (!near_own && !wrap_position(p.x, p.y, p.z, P.G)) {
     set_error(P.st, CBX_LOGIC);
@@ -182,6 +187,19 @@ __device__ __forceinline__ void kick_drift_proc(const KP& P, int move, int zero_
   }
 }
 
+// regional displacement bound of the warp's chunk (32 consecutive interior
+// cells of one row when bx % 32 == 0): the largest |u| of its atoms, rounded
+// up to kUbScale units; atomicMax because both sublattices' warps write it
+__device__ __forceinline__ void ub_note(const KP& P, int vb, double v, unsigned long long stamp) {
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  if ((threadIdx.x & 31) == 0 && v >= 0.0) {
+    const unsigned long long q =
+        v >= kUbDirty ? kUbQMax
+                      : min(kUbQMax, (unsigned long long)(sqrt(v) * kUbScale) + 2ull);
+    atomicMax(P.ub + (size_t)vb * 4 + ((threadIdx.x >> 5) & 3), (stamp << kUbShift) | q);
+  }
+}
+
 // a single wave of blocks (resident on every SM) walks the virtual blocks
 
 // (two virtual blocks per thread with both sites' loads in flight measured
@@ -208,18 +226,29 @@ __global__ void __launch_bounds__(256, 4)
   // second half kick of the previous step (same fixed dt) runs first
   __shared__ double s_kick[2];
   __shared__ int s_k2;
+  __shared__ unsigned long long s_stamp;
   if (threadIdx.x == 0) {
     const double dt = P.st->dt_next;
     s_kick[0] = dt;
     s_kick[1] = half_kick(P, dt);
     s_k2 = P.st->k2_pending;
+    if (P.ub) {
+      s_stamp = P.ustamp[1];
+      // the bounds of the previous step no longer describe the store; the
+      // pass-2 kernel after this one publishes this step's stamp
+      if (blockIdx.x == 0) P.ustamp[0] = 0;
+    }
   }
   __syncthreads();
   const double dt = s_kick[0], hk = s_kick[1];
   const bool k2 = s_k2 != 0;
+  const unsigned long long stamp = s_stamp;
   double v2s = 0.0, v2m = 0.0;
-  for (int vb = blockIdx.x; vb < nvb; vb += nsb)
-    kick_drift_site(P, move, zero_acc, images, vb, dt, hk, k2, v2s, v2m);
+  for (int vb = blockIdx.x; vb < nvb; vb += nsb) {
+    double ub2 = -1.0;
+    kick_drift_site(P, move, zero_acc, images, vb, dt, hk, k2, v2s, v2m, ub2);
+    if (P.ub) ub_note(P, vb, ub2, stamp);
+  }
   if (k2) {  // the previous step's KE / v_max partials (k_kick2's, per block)
     __shared__ double sh[8];
     const double sv = block_sum<256>(v2s, sh);
@@ -449,6 +478,24 @@ __device__ bool halt_check(const KP& P) {
   return s_halt != 0;
 }
 
+// regional displacement bounds (cbx_device.cuh): a slot filled by pass 2
+// makes its chunk unbounded for this step; once pass 2 is done the stamp of
+// this step's k_kick_drift becomes the one the density pass accepts
+__device__ __forceinline__ void ub_dirty(const KP& P, long long dr) {
+  if (!P.ub) return;
+  const Geo& G = P.G;
+  int cx, cy, cz;
+  cell_xyz(dr >= G.NC ? dr - G.NC : dr, G, cx, cy, cz);
+  const long long e = ((long long)(cz - G.g) * G.by + (cy - G.g)) * G.bx + (cx - G.g);
+  atomicMax(P.ub + (e >> 5), (P.ustamp[1] << kUbShift) | kUbQMax);
+}
+__device__ __forceinline__ void ub_publish(const KP& P) {
+  if (!P.ub || P.st->err || P.st->n_ovl) return;
+  const unsigned long long s = P.ustamp[1];
+  P.ustamp[0] = s;
+  P.ustamp[1] = s + 1;
+}
+
 __device__ void rehash_body(const KP& P) {
   if (P.st->err || P.st->n_ovl) return;
   const int n_old = P.st->n_clash;
@@ -523,6 +570,7 @@ __device__ void rehash_body(const KP& P) {
         P.frc[S + dr] = 0.0;
         P.frc[2 * S + dr] = 0.0;
         ghost_images(P, dr, P.pdf[dr]);  // the slot's periodic images follow it
+        ub_dirty(P, dr);  // no displacement bound for the slot's chunk this step
       }
     }
     X.flag[p] = !promote;
@@ -596,6 +644,8 @@ __global__ void __launch_bounds__(1024) k_rehash(KP P, int merge, int n_emb, int
     st->fin_pending = 1;
   }
   rehash_body(P);
+  __syncthreads();
+  if (threadIdx.x == 0) ub_publish(P);
 }
 
 // ------------------------------------------------------ ghost slot images
@@ -861,6 +911,8 @@ __global__ void __launch_bounds__(1024) k_rehash_images(KP P, int merge, int n_e
   rehash_body(P);
   __syncthreads();
   clash_images_body(P, 1);
+  __syncthreads();
+  if (threadIdx.x == 0) ub_publish(P);
 }
 
 // fp32 shadow of every site from pdf (after a host upload)

@@ -390,6 +390,13 @@ class DeviceStore:
         return {"density_ms": t[0], "embed_ms": t[1], "force_ms": t[2], "store_ms": t[3],
                 "integrate_ms": t[4], "step_ms": t[5], "steps": t[6]}
 
+    def skin_stats(self, enable: bool):
+        """(skin candidates examined, skin candidates listed) of the density
+        passes since counting was enabled; enable=True restarts the count"""
+        out = (C.c_uint64 * 2)()
+        self._check(self.lib.cbx_skin_stats(self.h, 1 if enable else 0, out))
+        return int(out[0]), int(out[1])
+
     def count_pairs(self):
         out = (C.c_uint64 * 2)()
         self._check(self.lib.cbx_count_pairs(self.h, out))

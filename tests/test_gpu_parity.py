@@ -366,6 +366,61 @@ def test_rows_of_whole_strips(cuda, tables, stencil):
                             what=f"aligned cascade {stencil} {chunk}")
 
 
+@pytest.mark.parametrize("stencil", ["newton3", "full"])
+def test_skin_pruning_regional_bounds(cuda, tables, stencil):
+    """Density-pass skin pruning by regional displacement bounds (bx % 32 ==
+    0): a skin shell farther than cutoff + 2U (U the largest displacement of
+    any atom from its own site in the neighbouring 32-cell chunks) is skipped.
+    The pair sets, rho, dF and forces stay the oracle's: one step from
+    identical inputs within 1e-10, then a PKA cascade whose chunks (atoms off
+    their sites, slots refilled by update_hash pass 2) lose their bound --
+    and the thermal regions still prune most of the skin"""
+    from oracle import oracle
+    ref = oracle.Sim(tables["baseline"], box=(64, 6, 8), temperature=600.0, seed=33,
+                     pka_energy_kev=1.0, pka_site=(20, 3, 4))
+    ref.step(1e-3, 6)
+    dev = device_for(ref, tables["baseline"], stencil)
+    dev.set_state(ref.state())
+    # after an upload no bound is valid: the first density pass prunes nothing
+    dev.skin_stats(True)
+    e_ref, e_dev = ref.eval_forces(), dev.eval_forces()
+    seen, listed = dev.skin_stats(False)
+    assert listed > 0 and seen == listed, (seen, listed)
+    assert close(e_ref[0], e_dev[0]) and close(e_ref[1], e_dev[1]), (e_ref, e_dev)
+    # one step from identical inputs: the step's own kick/drift publishes the
+    # bounds its density pass uses
+    dev.skin_stats(True)
+    ref.step(1e-3, 1)
+    dev.step(1e-3, 1)
+    seen, listed = dev.skin_stats(False)
+    assert seen < 0.5 * listed, (seen, listed)
+    assert_store_parity(ref.store(), dev.download(), pos_tol=1e-12,
+                        what=f"pruned step {stencil}")
+    ref.step(1e-3, 8)
+    dev.step(1e-3, 8)
+    assert_store_parity(ref.store(), dev.download(), pos_tol=1e-10, rel=1e-9,
+                        what=f"pruned thermal {stencil}")
+    ref.inject_pka()
+    s = ref.store()
+    _, a, g = ref.box
+    tx, ty = 64 + 2 * g, 6 + 2 * g
+    site = ((g + 4) * ty + (g + 3)) * 2 * tx + 2 * (g + 20)
+    dev.inject_pka(site, s.vel[site])
+    saw_clash = False
+    for chunk in range(4):
+        dev.skin_stats(True)
+        ref.step(1e-4, 25)
+        dev.step(1e-4, 25)
+        seen, listed = dev.skin_stats(False)
+        assert seen < listed, (chunk, seen, listed)
+        rs = ref.store()
+        saw_clash |= (rs.clash_ghost == 0).sum() > 0
+        assert ref.count_defects() == dev.count_defects(), chunk
+        assert_store_parity(rs, dev.download(), pos_tol=1e-8, rel=1e-7,
+                            what=f"pruned cascade {stencil} {chunk}")
+    assert saw_clash
+
+
 def test_overlap_halts_multi_step_call(cuda, tables):
     """An overlap found in step 2 of a 5-step call (fixed dt: merged kicks and
     deferred StepState sums) ends the call at step 2 like the reference's
