@@ -2528,9 +2528,11 @@ CBX_API cbx_status cbx_describe(cbx_ctx* c, char* buf, long n) {
                   "{\"stencil\": %d, \"fast_ok\": %d, \"fp32_density\": %d, "
                   "\"force_table\": %d, "
                   "\"pair_mask\": %d, \"slots\": %lld, \"ghost_sites\": %d, "
-                  "\"clash_capacity\": %d, \"band_A2\": %.3e, \"sm_count\": %d}",
+                  "\"clash_capacity\": %d, \"band_A2\": %.3e, \"skin_prune\": %d, "
+                  "\"kick_drift_bulk\": %d, \"sm_count\": %d}",
                   c->mode, (int)c->fast_ok, (int)c->fp32_density, force_table_mode(),
                   (int)(c->P.pmask != nullptr), c->S, c->n_ghost, c->P.cap_clash, c->band,
+                  (int)(c->P.ub != nullptr), (int)kd_bulk(c->P),
                   [] {
                     int d = 0, n = 0;
                     cudaGetDevice(&d);

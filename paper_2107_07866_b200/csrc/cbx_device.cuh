@@ -361,6 +361,56 @@ inline void launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, 
 }
 #endif
 
+#if defined(__CUDACC__)
+// shared-memory loads through a 32-bit shared address held in a register
+// (the generic-to-shared conversion is done once per kernel, not per load)
+__device__ __forceinline__ unsigned smem_addr(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+// ---- bulk (TMA engine) staging of a constant table into shared memory:
+// one thread arms an mbarrier with the byte count and issues 1-D bulk
+// copies; every thread waits on the barrier's phase 0.  Spares the per-thread
+// load/store round trips of a copy loop at kernel start.
+__device__ __forceinline__ void mbar_init(unsigned mbar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mbar) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned mbar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(unsigned dst, const void* src, unsigned bytes,
+                                         unsigned mbar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          dst),
+      "l"(src), "r"(bytes), "r"(mbar)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait0(unsigned mbar) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n"
+      " @!p bra WAIT%=;\n}" ::"r"(mbar)
+      : "memory");
+}
+// bytes (multiple of 16, both addresses 16-byte aligned) in chunks of 32 KB;
+// called by one thread after mbar_init
+__device__ __forceinline__ void bulk_stage(unsigned dst, const void* src, unsigned bytes,
+                                           unsigned mbar) {
+  const char* s = static_cast<const char*>(src);
+  for (unsigned o = 0; o < bytes; o += 32768u)
+    bulk_g2s(dst + o, s + o, min(32768u, bytes - o), mbar);
+}
+
+// wait for the phase of parity `ph` of an mbarrier (multi-stage pipelines)
+__device__ __forceinline__ void mbar_wait(unsigned mbar, unsigned ph) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT%=;\n}" ::"r"(mbar), "r"(ph)
+      : "memory");
+}
+#endif
+
 // device entry points (launch wrappers), implemented in the .cu files
 bool launch_density(const KP& P, int mode, cudaStream_t s);  // true: clash pass fused
 void launch_clash_density(const KP& P, cudaStream_t s);
@@ -393,6 +443,7 @@ void launch_rehash_images(const KP& P, cudaStream_t s, int merge, int n_emb, int
                           int n_ke);
 int force_partials(const KP& P, int mode);  // partials the force launch writes
 int kick_drift_grid(const KP& P);           // KE partials of a merged-kick k_kick_drift
+bool kd_bulk(const KP& P);                  // k_kick_drift_bulk (bx % 128 == 0)
 
 void launch_count_defects(const KP& P, unsigned long long* out, cudaStream_t s);
 void upload_offsets(const int* half_dev[2], const int half_n[2], const int* full_dev[2],

@@ -134,11 +134,6 @@ __device__ __forceinline__ double rsqrt_nr(double x) {
   return y;
 }
 
-// shared-memory loads through a 32-bit shared address held in a register
-// (the generic-to-shared conversion is done once per kernel, not per load)
-__device__ __forceinline__ unsigned smem_addr(const void* p) {
-  return (unsigned)__cvta_generic_to_shared(p);
-}
 __device__ __forceinline__ double2 lds2(unsigned a) {
   double2 v;
   asm("ld.shared.v2.f64 {%0,%1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a));
@@ -175,41 +170,6 @@ __device__ __forceinline__ double2 tex_chunk(unsigned long long tex, int seg, in
 __device__ __forceinline__ double2 tex_rec16(unsigned long long tex, int i) {
   const int4 q = tex1Dfetch<int4>((cudaTextureObject_t)tex, i);
   return make_double2(__hiloint2double(q.y, q.x), __hiloint2double(q.w, q.z));
-}
-
-// ---- bulk (TMA engine) staging of a constant table into shared memory:
-// one thread arms an mbarrier with the byte count and issues 1-D bulk
-// copies; every thread waits on the barrier's phase 0.  Spares the per-thread
-// load/store round trips of a copy loop at kernel start.
-__device__ __forceinline__ void mbar_init(unsigned mbar) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mbar) : "memory");
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(unsigned mbar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(unsigned dst, const void* src, unsigned bytes,
-                                         unsigned mbar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          dst),
-      "l"(src), "r"(bytes), "r"(mbar)
-      : "memory");
-}
-__device__ __forceinline__ void mbar_wait0(unsigned mbar) {
-  asm volatile(
-      "{\n .reg .pred p;\n WAIT%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n"
-      " @!p bra WAIT%=;\n}" ::"r"(mbar)
-      : "memory");
-}
-// bytes (multiple of 16, both addresses 16-byte aligned) in chunks of 32 KB;
-// called by one thread after mbar_init
-__device__ __forceinline__ void bulk_stage(unsigned dst, const void* src, unsigned bytes,
-                                           unsigned mbar) {
-  const char* s = static_cast<const char*>(src);
-  for (unsigned o = 0; o < bytes; o += 32768u)
-    bulk_g2s(dst + o, s + o, min(32768u, bytes - o), mbar);
 }
 
 // ------------------------------------------------------------------ density

@@ -260,6 +260,130 @@ __global__ void __launch_bounds__(256, 4)
   }
 }
 
+// ---- kick/drift with TMA bulk staging (rows of whole virtual blocks,
+// bx % 128 == 0): one thread per CTA streams the inputs of the virtual blocks
+// kKdStages ahead into shared memory (cp.async.bulk + mbarrier); the 256
+// threads read their site from there, so no load occupies a register while
+// it is in flight and each SM keeps ~165 KB of reads outstanding (the
+// register-staged sweep above holds at most one site per thread).  A virtual
+// block's 128 cells are consecutive in one row: per sublattice one 4 KB pdf
+// run and, per velocity / force component, one run of 128 doubles copied
+// from the 16-byte boundary below it (kKdChunk doubles).
+constexpr int kKdStages = 4;
+constexpr int kKdChunk = 130;
+struct KdStage {
+  double4 pdf[2][128];
+  double vel[3][2][kKdChunk];
+  double frc[3][2][kKdChunk];
+};
+constexpr unsigned kKdStageBytes = sizeof(KdStage);
+static_assert(kKdStageBytes % 16 == 0, "stage size");
+
+__device__ __forceinline__ long long kd_cell0(const KP& P, int vb, int& cx0, int& cy, int& cz) {
+  const Geo& G = P.G;
+  const long long e0 = (long long)vb * 128;
+  const long long row = e0 / G.bx;
+  cx0 = (int)(e0 - row * G.bx);
+  cy = (int)(row % G.by);
+  cz = (int)(row / G.by);
+  return cell_of(cx0 + G.g, cy + G.g, cz + G.g, G);
+}
+__device__ __forceinline__ void kd_issue(const KP& P, KdStage* st, unsigned mbar, int vb) {
+  int cx0, cy, cz;
+  const long long c0 = kd_cell0(P, vb, cx0, cy, cz);
+  const long long S = P.S, NC = P.G.NC;
+  mbar_expect_tx(mbar, kKdStageBytes);
+  for (int p = 0; p < 2; ++p) {
+    const long long d0 = p * NC + c0, a0 = d0 & ~1ll;
+    bulk_g2s(smem_addr(&st->pdf[p][0]), P.pdf + d0, 128 * 32, mbar);
+    for (int a = 0; a < 3; ++a) {
+      bulk_g2s(smem_addr(&st->vel[a][p][0]), P.vel + a * S + a0, kKdChunk * 8, mbar);
+      bulk_g2s(smem_addr(&st->frc[a][p][0]), P.frc + a * S + a0, kKdChunk * 8, mbar);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256, 2)
+    k_kick_drift_bulk(KP P, int move, int nsb, int zero_acc, int images, int nvb) {
+  if (blockIdx.x == nsb) finalize_pending<256>(P);
+  if (P.st->err || P.st->n_ovl) return;
+  if (P.rev_wait && !rev_wait(P, P.rev_wait)) return;
+  if (blockIdx.x >= nsb) {
+    if (P.st->k2_pending) clash_kick2_sums(P, blockIdx.x - nsb);
+    clash_kick_drift_body(P, move, blockIdx.x - nsb, gridDim.x - nsb);
+    return;
+  }
+  extern __shared__ __align__(128) unsigned char kd_smem[];
+  KdStage* stg = reinterpret_cast<KdStage*>(kd_smem);
+  __shared__ __align__(8) unsigned long long s_full[kKdStages];
+  __shared__ double s_kick[2];
+  __shared__ int s_k2;
+  __shared__ unsigned long long s_stamp;
+  const int t = threadIdx.x;
+  if (t == 0) {
+    const double dt = P.st->dt_next;
+    s_kick[0] = dt;
+    s_kick[1] = half_kick(P, dt);
+    s_k2 = P.st->k2_pending;
+    if (P.ub) {
+      s_stamp = P.ustamp[1];
+      if (blockIdx.x == 0) P.ustamp[0] = 0;
+    }
+    for (int q = 0; q < kKdStages; ++q) mbar_init(smem_addr(&s_full[q]));
+    for (int q = 0; q < kKdStages; ++q) {
+      const int vb = blockIdx.x + q * nsb;
+      if (vb < nvb) kd_issue(P, &stg[q], smem_addr(&s_full[q]), vb);
+    }
+  }
+  __syncthreads();
+  const double dt = s_kick[0], hk = s_kick[1];
+  const bool k2 = s_k2 != 0;
+  const unsigned long long stamp = s_stamp;
+  const int par = t >> 7, i = t & 127;
+  double v2s = 0.0, v2m = 0.0;
+  int it = 0;
+  for (int vb = blockIdx.x; vb < nvb; vb += nsb, ++it) {
+    const int q = it % kKdStages;
+    mbar_wait(smem_addr(&s_full[q]), (unsigned)(it / kKdStages) & 1u);
+    const KdStage& st = stg[q];
+    KdSite a;
+    int cx0;
+    const long long c0 = kd_cell0(P, vb, cx0, a.cy, a.cz);
+    const long long d = par * P.G.NC + c0;
+    const int o = (int)(d & 1) + i;
+    a.d = d + i;
+    a.par = par;
+    a.cx = cx0 + i + P.G.g;
+    a.cy += P.G.g;
+    a.cz += P.G.g;
+    a.live = true;
+    a.p = st.pdf[par][i];
+    a.vx = st.vel[0][par][o];
+    a.vy = st.vel[1][par][o];
+    a.vz = st.vel[2][par][o];
+    a.fx = st.frc[0][par][o];
+    a.fy = st.frc[1][par][o];
+    a.fz = st.frc[2][par][o];
+    double ub2 = -1.0;
+    kick_drift_proc(P, move, zero_acc, images, dt, hk, k2, v2s, v2m, a, ub2);
+    if (P.ub) ub_note(P, vb, ub2, stamp);
+    __syncthreads();  // stage q is read by every thread: refill it
+    if (t == 0) {
+      const int vn = vb + kKdStages * nsb;
+      if (vn < nvb) kd_issue(P, &stg[q], smem_addr(&s_full[q]), vn);
+    }
+  }
+  if (k2) {
+    __shared__ double sh[8];
+    const double sv = block_sum<256>(v2s, sh);
+    const double mv = block_max<256>(v2m, sh);
+    if (t == 0) {
+      P.part_ke[blockIdx.x] = sv;
+      P.part_vmax[blockIdx.x] = mv;
+    }
+  }
+}
+
 // merged kick: the clash records' part of the previous step's second half
 // kick (clash_kick2_body) and of its StepState sums, before the rehash of
 // this step reorders the records: one partial per clash block in the
@@ -1109,9 +1233,27 @@ static int site_wave(const KP& P, int per_sm) {
   static const int wave = ab_flag("CBX_SITE_WAVE", 1);  // 0: one block per virtual block
   return wave ? std::max(1, std::min(eam_blocks(P), per_sm * sms)) : eam_blocks(P);
 }
+// the bulk-staged sweep where a virtual block is one run of 128 cells of a
+// row (bx % 128 == 0); CBX_KD_BULK=0 (A/B build) keeps the register sweep
+bool kd_bulk(const KP& P) {
+  static const int on = ab_flag("CBX_KD_BULK", 1);
+  return on && P.G.bx % 128 == 0;
+}
+int kick_drift_grid(const KP& P) { return kd_bulk(P) ? site_wave(P, 2) : site_wave(P, 4); }
 void launch_kick_drift(const KP& P, int move, cudaStream_t s, int zero_acc, int images,
                        int n_pairp) {
-  const int nsb = site_wave(P, 4);
+  const int nsb = kick_drift_grid(P);
+  if (kd_bulk(P)) {
+    static bool attr = false;
+    const int bytes = kKdStages * (int)kKdStageBytes;
+    if (!attr) {
+      cudaFuncSetAttribute(k_kick_drift_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+      attr = true;
+    }
+    k_kick_drift_bulk<<<nsb + kClashBlocks, 256, bytes, s>>>(P, move, nsb, zero_acc, images,
+                                                             eam_blocks(P));
+    return;
+  }
   k_kick_drift<<<nsb + kClashBlocks, 256, 0, s>>>(P, move, nsb, zero_acc, images, eam_blocks(P),
                                                    n_pairp > 0 ? n_pairp : P.n_pair_part,
                                                    embed_grid(P), kick_grid(P));
@@ -1120,7 +1262,6 @@ void launch_rehash_images(const KP& P, cudaStream_t s, int merge, int n_emb, int
                           int n_ke) {
   launch_pdl(k_rehash_images, 1, 1024, 0, s, P, merge, n_emb, n_pairp, n_ke);
 }
-int kick_drift_grid(const KP& P) { return site_wave(P, 4); }
 void launch_rehash(const KP& P, cudaStream_t s, int merge, int n_emb, int n_pairp, int n_ke) {
   launch_pdl(k_rehash, 1, 1024, 0, s, P, merge, n_emb, n_pairp, n_ke);
 }

@@ -376,11 +376,14 @@ def test_skin_pruning_regional_bounds(cuda, tables, stencil):
     their sites, slots refilled by update_hash pass 2) lose their bound --
     and the thermal regions still prune most of the skin"""
     from oracle import oracle
-    ref = oracle.Sim(tables["baseline"], box=(64, 6, 8), temperature=600.0, seed=33,
-                     pka_energy_kev=1.0, pka_site=(20, 3, 4))
+    ref = oracle.Sim(tables["baseline"], box=(128, 4, 6), temperature=600.0, seed=33,
+                     pka_energy_kev=1.0, pka_site=(40, 2, 3))
     ref.step(1e-3, 6)
     dev = device_for(ref, tables["baseline"], stencil)
     dev.set_state(ref.state())
+    # rows of whole 128-cell virtual blocks: the TMA-staged kick/drift sweep too
+    desc = dev.describe()
+    assert desc["skin_prune"] == 1 and desc["kick_drift_bulk"] == 1, desc
     # after an upload no bound is valid: the first density pass prunes nothing
     dev.skin_stats(True)
     e_ref, e_dev = ref.eval_forces(), dev.eval_forces()
@@ -403,8 +406,8 @@ def test_skin_pruning_regional_bounds(cuda, tables, stencil):
     ref.inject_pka()
     s = ref.store()
     _, a, g = ref.box
-    tx, ty = 64 + 2 * g, 6 + 2 * g
-    site = ((g + 4) * ty + (g + 3)) * 2 * tx + 2 * (g + 20)
+    tx, ty = 128 + 2 * g, 4 + 2 * g
+    site = ((g + 3) * ty + (g + 2)) * 2 * tx + 2 * (g + 40)
     dev.inject_pka(site, s.vel[site])
     saw_clash = False
     for chunk in range(4):
