@@ -269,7 +269,6 @@ __global__ void __launch_bounds__(256, 4)
 // block's 128 cells are consecutive in one row: per sublattice one 4 KB pdf
 // run and, per velocity / force component, one run of 128 doubles copied
 // from the 16-byte boundary below it (kKdChunk doubles).
-constexpr int kKdStages = 4;
 constexpr int kKdChunk = 130;
 struct KdStage {
   double4 pdf[2][128];
@@ -303,7 +302,8 @@ __device__ __forceinline__ void kd_issue(const KP& P, KdStage* st, unsigned mbar
   }
 }
 
-__global__ void __launch_bounds__(256, 2)
+template <int NS, int MINB>
+__global__ void __launch_bounds__(256, MINB)
     k_kick_drift_bulk(KP P, int move, int nsb, int zero_acc, int images, int nvb) {
   if (blockIdx.x == nsb) finalize_pending<256>(P);
   if (P.st->err || P.st->n_ovl) return;
@@ -315,7 +315,7 @@ __global__ void __launch_bounds__(256, 2)
   }
   extern __shared__ __align__(128) unsigned char kd_smem[];
   KdStage* stg = reinterpret_cast<KdStage*>(kd_smem);
-  __shared__ __align__(8) unsigned long long s_full[kKdStages];
+  __shared__ __align__(8) unsigned long long s_full[NS];
   __shared__ double s_kick[2];
   __shared__ int s_k2;
   __shared__ unsigned long long s_stamp;
@@ -329,8 +329,8 @@ __global__ void __launch_bounds__(256, 2)
       s_stamp = P.ustamp[1];
       if (blockIdx.x == 0) P.ustamp[0] = 0;
     }
-    for (int q = 0; q < kKdStages; ++q) mbar_init(smem_addr(&s_full[q]));
-    for (int q = 0; q < kKdStages; ++q) {
+    for (int q = 0; q < NS; ++q) mbar_init(smem_addr(&s_full[q]));
+    for (int q = 0; q < NS; ++q) {
       const int vb = blockIdx.x + q * nsb;
       if (vb < nvb) kd_issue(P, &stg[q], smem_addr(&s_full[q]), vb);
     }
@@ -343,8 +343,8 @@ __global__ void __launch_bounds__(256, 2)
   double v2s = 0.0, v2m = 0.0;
   int it = 0;
   for (int vb = blockIdx.x; vb < nvb; vb += nsb, ++it) {
-    const int q = it % kKdStages;
-    mbar_wait(smem_addr(&s_full[q]), (unsigned)(it / kKdStages) & 1u);
+    const int q = it % NS;
+    mbar_wait(smem_addr(&s_full[q]), (unsigned)(it / NS) & 1u);
     const KdStage& st = stg[q];
     KdSite a;
     int cx0;
@@ -369,7 +369,7 @@ __global__ void __launch_bounds__(256, 2)
     if (P.ub) ub_note(P, vb, ub2, stamp);
     __syncthreads();  // stage q is read by every thread: refill it
     if (t == 0) {
-      const int vn = vb + kKdStages * nsb;
+      const int vn = vb + NS * nsb;
       if (vn < nvb) kd_issue(P, &stg[q], smem_addr(&s_full[q]), vn);
     }
   }
@@ -1239,19 +1239,38 @@ bool kd_bulk(const KP& P) {
   static const int on = ab_flag("CBX_KD_BULK", 1);
   return on && P.G.bx % 128 == 0;
 }
-int kick_drift_grid(const KP& P) { return kd_bulk(P) ? site_wave(P, 2) : site_wave(P, 4); }
+// stages x CTAs per SM of the bulk sweep (CBX_KD_CFG, A/B build: 42 = 4 x 2)
+static int kd_cfg() {
+  static const int c = ab_flag("CBX_KD_CFG", 42);
+  return c;
+}
+int kick_drift_grid(const KP& P) {
+  return kd_bulk(P) ? site_wave(P, kd_cfg() % 10) : site_wave(P, 4);
+}
+template <int NS, int MINB>
+static void launch_kd_bulk(const KP& P, int move, cudaStream_t s, int zero_acc, int images,
+                           int nsb) {
+  static bool attr = false;
+  const int bytes = NS * (int)kKdStageBytes;
+  if (!attr) {
+    cudaFuncSetAttribute(k_kick_drift_bulk<NS, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         bytes);
+    attr = true;
+  }
+  k_kick_drift_bulk<NS, MINB><<<nsb + kClashBlocks, 256, bytes, s>>>(P, move, nsb, zero_acc,
+                                                                     images, eam_blocks(P));
+}
 void launch_kick_drift(const KP& P, int move, cudaStream_t s, int zero_acc, int images,
                        int n_pairp) {
   const int nsb = kick_drift_grid(P);
   if (kd_bulk(P)) {
-    static bool attr = false;
-    const int bytes = kKdStages * (int)kKdStageBytes;
-    if (!attr) {
-      cudaFuncSetAttribute(k_kick_drift_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-      attr = true;
+    switch (kd_cfg()) {
+      case 33: launch_kd_bulk<3, 3>(P, move, s, zero_acc, images, nsb); break;
+      case 23: launch_kd_bulk<2, 3>(P, move, s, zero_acc, images, nsb); break;
+      case 52: launch_kd_bulk<5, 2>(P, move, s, zero_acc, images, nsb); break;
+      case 81: launch_kd_bulk<8, 1>(P, move, s, zero_acc, images, nsb); break;
+      default: launch_kd_bulk<4, 2>(P, move, s, zero_acc, images, nsb);
     }
-    k_kick_drift_bulk<<<nsb + kClashBlocks, 256, bytes, s>>>(P, move, nsb, zero_acc, images,
-                                                             eam_blocks(P));
     return;
   }
   k_kick_drift<<<nsb + kClashBlocks, 256, 0, s>>>(P, move, nsb, zero_acc, images, eam_blocks(P),
