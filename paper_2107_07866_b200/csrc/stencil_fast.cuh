@@ -905,12 +905,22 @@ __device__ __forceinline__ bool near_halo(const Geo& G, int u, int w) {
 __device__ __forceinline__ int unit_lo(int b, int nsb, int nu) {
   return (int)(((long long)b * nu) / nsb);
 }
+// rr > 0 (default 14): batches of rr consecutive units dealt round-robin to
+// the CTAs -- every CTA sweeps the box bottom-up in step with the others, so
+// the concurrent work is a thin slab of planes whose partners stay in L2
+// (config 5, A/B: force 7.52 -> 7.36 ms, density 4.30 -> 4.16 ms against
+// contiguous per-CTA ranges; batches of 10-21 within noise, 42 slower)
 __device__ __forceinline__ int next_unit(int* s_ctr, int group, int nsb, int nu,
-                                         volatile int* slot) {
+                                         volatile int* slot, int rr = 0) {
   asm volatile("bar.sync %0, 128;" ::"r"(group + 1));
-  if ((threadIdx.x & 127) == 0) slot[group] = unit_lo(blockIdx.x, nsb, nu) + atomicAdd(s_ctr, 1);
+  if ((threadIdx.x & 127) == 0) {
+    const int i = atomicAdd(s_ctr, 1);
+    slot[group] = rr ? ((i / rr) * nsb + blockIdx.x) * rr + i % rr
+                     : unit_lo(blockIdx.x, nsb, nu) + i;
+  }
   asm volatile("bar.sync %0, 128;" ::"r"(group + 1));
   const int u = slot[group];
+  if (rr) return u < nu ? u : nu;
   return u < unit_lo(blockIdx.x + 1, nsb, nu) ? u : nu;
 }
 
@@ -1041,7 +1051,7 @@ __global__ void __launch_bounds__(NT, 1) k_density_smem(KP P, int nsb) {
   const unsigned long long ub_cur = P.ub ? __ldcg(P.ustamp) : 0ull;
   const bool cnt_skin = __ldcg(P.skin_cnt + 2) != 0;
   for (;;) {
-    const int u = next_unit(&s_ctr, group, nsb, nu, s_slot);
+    const int u = next_unit(&s_ctr, group, nsb, nu, s_slot, P.unit_rr);
     if (u >= nu) break;
     int c;
     const bool live = unit_cell(G, u, lane, w, c);
@@ -1176,7 +1186,7 @@ __global__ void __launch_bounds__(NT, 1) k_force_lean_smem(KP P, int nsb) {
   const int nu = unit_count(G);
   double e = 0.0;
   for (;;) {
-    const int u = next_unit(&s_ctr, group, nsb, nu, s_slot);
+    const int u = next_unit(&s_ctr, group, nsb, nu, s_slot, P.unit_rr);
     if (u >= nu) break;
     int c;
     const bool live = unit_cell(G, u, lane, w, c);
