@@ -356,6 +356,57 @@ def test_slab_graph_cascade(cuda, tables, transport):
     assert saw_clash
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("n", [2, 3])
+def test_slab_whole_rows_bulk_and_pruning(cuda, tables, n):
+    """slab ranks whose rows hold whole 128-cell virtual blocks (as config 5
+    per GPU): the TMA-staged kick/drift sweep and the density pass's skin
+    pruning run on every rank (z halos from the neighbours keep their chunks
+    unbounded); a PKA cascade crossing the slab faces at fixed dt matches the
+    single-box oracle"""
+    from oracle import oracle
+    ref = oracle.Sim(tables["baseline"], box=(128, 4, 12), temperature=600.0, seed=99,
+                     pka_energy_kev=0.5, pka_site=(64, 2, 6 if n == 2 else 4))
+    ref.step(1e-3, 5)
+    ref.inject_pka()
+    dom = slab_domain(ref, tables["baseline"], n)
+    for r in dom.ranks:
+        d = r.describe()
+        assert d["kick_drift_bulk"] == 1 and d["skin_prune"] == 1, d
+    dom.prime()
+    saw_clash = False
+    for chunk in range(4):
+        ref.step(1e-4, 15)
+        dom.step(1e-4, 15)
+        rs = ref.store()
+        saw_clash |= (rs.clash_ghost == 0).sum() > 0
+        assert ref.count_defects() == dom.count_defects(), chunk
+        assert_store_parity(_interior(rs), gather(dom, ref), pos_tol=1e-8, rel=1e-7,
+                            what=f"slab rows n={n} chunk {chunk}")
+    assert saw_clash
+
+
+@pytest.mark.gpu
+def test_slab_graph_whole_rows_p2p(cuda, tables):
+    """the in-graph peer-memory step (merged kick on a slab rank) with the
+    TMA-staged kick/drift and skin pruning: 40 steps against the oracle"""
+    from oracle import oracle
+    ref = oracle.Sim(tables["baseline"], box=(128, 4, 8), temperature=600.0, seed=7)
+    r = native_rank(ref, tables["baseline"], "p2p")
+    assert r.describe()["kick_drift_bulk"] == 1
+    r.eval_forces()
+    r.measure()
+    dom = S.SlabDomain([r], None)
+    for chunk in range(2):
+        ref.step(1e-3, 20)
+        st = r.step(1e-3, 20)
+        sr = ref.state()
+        for k in ("kinetic", "pair", "embedding"):
+            assert abs(st[k] - sr[k]) <= 1e-9 * abs(sr[k]), (chunk, k, st[k], sr[k])
+        assert_store_parity(_interior(ref.store()), gather(dom, ref), pos_tol=1e-9, rel=1e-8,
+                            what=f"p2p rows chunk {chunk}")
+
+
 # ------------------------------------------ two processes, peer memory
 def _p2p_lockstep_worker(rank, n, port, table, q):
     """one slab rank per process, both on GPU 0: CUDA IPC mappings of the
