@@ -1353,6 +1353,7 @@ static cbx_status create_impl(const cbx_box* box, const cbx_potential* pot,
     std::vector<long long> ff[2];
     int hin[2] = {0, 0}, fin[2] = {0, 0};
     SkinGroups skh[2], skf[2];
+    int sreach[2] = {0, 0};
     for (int par = 0; par < 2; ++par) {
       auto delta = [&](const Offset& o) {
         const int q = par ^ o.cross;
@@ -1364,7 +1365,7 @@ static cbx_status create_impl(const cbx_box* box, const cbx_potential* pot,
         const double x = o.dx + h, y = o.dy + h, z = o.dz + h;
         return (x * x + y * y + z * z) * box->a0 * box->a0;
       };
-      auto order = [&](std::vector<Offset> v, int& nin, SkinGroups& sg) {
+      auto order = [&](std::vector<Offset> v, int& nin, SkinGroups& sg, int& reach) {
         std::stable_sort(v.begin(), v.end(),
                          [&](const Offset& a, const Offset& b) { return dist2(a) < dist2(b); });
         nin = 0;
@@ -1373,6 +1374,9 @@ static cbx_status create_impl(const cbx_box* box, const cbx_potential* pot,
         // skin shells (equal lattice distance) beyond nin, at most 4 groups:
         // the last one takes every remaining shell at its smallest distance
         sg = SkinGroups{};
+        for (int k = nin; k < (int)v.size(); ++k)
+          reach = std::max(reach, std::max(std::abs(v[k].dx), std::max(std::abs(v[k].dy),
+                                                                      std::abs(v[k].dz))));
         for (int k = nin; k < (int)v.size(); ++k) {
           const bool fresh = k == nin || dist2(v[k]) != dist2(v[k - 1]);
           if (fresh && sg.n < 4) sg.len[sg.n++] = std::sqrt(dist2(v[k]));
@@ -1380,10 +1384,10 @@ static cbx_status create_impl(const cbx_box* box, const cbx_potential* pot,
         }
         return v;
       };
-      for (const Offset& o : order(c->offs.half[par], hin[par], skh[par])) {
+      for (const Offset& o : order(c->offs.half[par], hin[par], skh[par], sreach[0])) {
         hd[par].push_back(delta(o));
       }
-      for (const Offset& o : order(c->offs.full[par], fin[par], skf[par])) {
+      for (const Offset& o : order(c->offs.full[par], fin[par], skf[par], sreach[1])) {
         fd[par].push_back(delta(o));
         ff[par].push_back(o.flat);
       }
@@ -1447,6 +1451,8 @@ static cbx_status create_impl(const cbx_box* box, const cbx_potential* pot,
       P.skf[par] = skf[par];
     }
     P.nin64 = std::max(std::max(hin[0], hin[1]), std::max(fin[0], fin[1])) <= 64;
+    P.skin_reach[0] = sreach[0];
+    P.skin_reach[1] = sreach[1];
     P.accel = accel_factor();
     P.mv2 = mv2_to_ev();
     c->mem_cat = CBX_MEM_SLOTS;

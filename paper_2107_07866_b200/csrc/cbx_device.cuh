@@ -148,6 +148,7 @@ struct KP {
   unsigned long long* ub;      // regional displacement bounds (null: off)
   unsigned long long* ustamp;  // [2]
   SkinGroups skh[2], skf[2];   // half / full lists per sublattice
+  int skin_reach[2];           // cells a skin offset reaches per axis (half, full lists)
   // [3]: skin candidates examined / listed by the density pass, counting on
   // (cbx_skin_stats; a device word, so captured step graphs see it)
   unsigned long long* skin_cnt;

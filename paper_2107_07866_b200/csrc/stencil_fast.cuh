@@ -210,18 +210,48 @@ __device__ __forceinline__ int smem_slot32(int i, int c) { return 2 * i + (c ^ (
 // copies) and a one-word pair mask; tables: 3 fp64 [A B] (16 B) in shared
 // memory + [C D] by texture, 4 (default where the fp32 guard holds) those of
 // 2, 5 both halves of 2 by texture, 6 both fp64 halves by texture
+// end of the offsets a site of sublattice par examines for threshold T
+template <bool FULL>
+__device__ __forceinline__ int skin_end(const KP& P, int par, double T) {
+  const SkinGroups& sg = FULL ? P.skf[par] : P.skh[par];
+  int n = FULL ? c_full_nin[par] : c_half_nin[par];
+  for (int i = 0; i < sg.n; ++i) {
+    if (sg.len[i] > T) return n;
+    n = sg.end[i];
+  }
+  return kMaxOffsets;
+}
+
+// skU (skin pruning, skin_region_bound): the largest displacement bound of
+// the chunks the lanes' skin partners lie in, or >= 1e299 for none; cxs, cys,
+// czs: the site's ghost-inclusive cell.  Returns the end of the offsets
+// examined (the diagnostic count of cbx_skin_stats).
 template <bool FULL, int B, bool SMEM = false, bool REV = false, int CMPD = 0>
-__device__ __forceinline__ void density_site(const KP& P, KP* Pp, int par, int d, bool live,
-                                             unsigned tb = 0, int seg_lo = 0,
-                                             bool rev_here = true, bool deep = false,
-                                             unsigned tb8 = 0, int n_lim = kMaxOffsets) {
+__device__ __forceinline__ int density_site(const KP& P, KP* Pp, int par, int d, bool live,
+                                            unsigned tb = 0, int seg_lo = 0,
+                                            bool rev_here = true, bool deep = false,
+                                            unsigned tb8 = 0, double skU = 1e300, int cxs = 0,
+                                            int cys = 0, int czs = 0) {
   const double4* __restrict__ pdf = P.pdf;
   const int* __restrict__ tgt = P.tgt;
   double ax = kVacant, ay = 0, az = 0, aw = 0;
   if (live) ld256(pdf + d, ax, ay, az, aw);
+  int n_lim = kMaxOffsets;
+  if (skU < 1e299) {  // warp-uniform: the lanes' own displacements |u_i|
+    double u2 = 0.0;
+    if (ax < kVacantTest) {
+      const double h = 0.5 * par;
+      const double ux = ax - ((double)cxs + h) * P.G.a0, uy = ay - ((double)cys + h) * P.G.a0,
+                   uz = az - ((double)(czs + P.G.zoff) + h) * P.G.a0;
+      u2 = fma(ux, ux, fma(uy, uy, uz * uz));
+    }
+    // non-negative floats order as their bit patterns; rounded up
+    const unsigned m = __reduce_max_sync(0xffffffffu, __float_as_uint(__double2float_ru(u2)));
+    n_lim = skin_end<FULL>(P, par, P.cutoff + 1e-9 + skU + sqrt((double)__uint_as_float(m)));
+  }
   if (ax >= kVacantTest) {
     if (FULL && live) P.rho[d] = 0.0;
-    return;
+    return n_lim;
   }
   // n_lim: skin shells beyond it are out of cutoff for every lane (regional
   // displacement bound, skin_end)
@@ -467,6 +497,7 @@ __device__ __forceinline__ void density_site(const KP& P, KP* Pp, int par, int d
     P.pmask[2 * (size_t)d] = m0;
     P.pmask[2 * (size_t)d + 1] = m1;
   }
+  return n_lim;
 }
 
 // -------------------------------------------------------------------- force
@@ -870,13 +901,20 @@ __device__ __forceinline__ int unit_strip(const Geo& G, int u, int& zb) {
   }
   return r;
 }
-__device__ __forceinline__ bool unit_cell(const Geo& G, int u, int lane, int w, int& c) {
+__device__ __forceinline__ bool unit_cell(const Geo& G, int u, int lane, int w, int& c,
+                                          int* gx = nullptr, int* gy = nullptr,
+                                          int* gz = nullptr) {
   int zb;
   const int st = unit_strip(G, u, zb);
   const int e = st * 32 + lane, cz = zb * 4 + w;
   const bool live = e < G.bx * G.by && cz < G.bz;
   const int cy = e / G.bx, cx = e - cy * G.bx;
   c = live ? (int)cell_of(cx + G.g, cy + G.g, cz + G.g, G) : 0;
+  if (gx) {  // ghost-inclusive cell coordinates
+    *gx = cx + G.g;
+    *gy = cy + G.g;
+    *gz = cz + G.g;
+  }
   return live;
 }
 // a "deep" site has every stencil partner in an interior cell (the offsets
@@ -926,25 +964,26 @@ __device__ __forceinline__ int next_unit(int* s_ctr, int group, int nsb, int nu,
 
 // Skin pruning by the regional displacement bounds (cbx_device.cuh).  For a
 // pair of sites at lattice distance R whose atoms are displaced by u_i and u_j
-// from them, r = |R + u_j - u_i| >= R - |u_i| - |u_j|.  Every atom a warp's
-// lanes pair with (its own site included) lies in the chunks of planes z..z+g
-// (z-g..z+g with full lists), rows y-g..y+g and x chunks xs-1..xs+1; with U the
-// largest bound among them, a skin shell with R > cutoff + 2U + margin is out
-// of cutoff for every lane, whatever the reference's rounding (margin 1e-9 A
-// against rounding errors of ~1e-12 A in r and u).  Returns the largest R
-// still to examine (+inf when a chunk is unbounded, stale or in a z halo of a
-// slab rank).  Rows holding whole chunks (bx % 32 == 0) only: P.ub is null
-// otherwise.
+// from them, r = |R + u_j - u_i| >= R - |u_i| - |u_j|.  Every skin partner of
+// a warp's lanes lies in the chunks of planes z..z+s (z-s..z+s with full
+// lists), rows y-s..y+s and x chunks xs-1..xs+1, s the cell reach of the skin
+// offsets (P.skin_reach); with U the largest bound among them and |u_i| the
+// lanes' own displacements (density_site), a skin shell with
+// R > cutoff + U + max |u_i| + margin is out of cutoff for every lane,
+// whatever the reference's rounding (margin 1e-9 A against rounding errors of
+// ~1e-12 A in r and u).  Returns U (>= 1e299 when a chunk is unbounded, stale
+// or in a z halo of a slab rank).  Rows holding whole chunks (bx % 32 == 0)
+// only: P.ub is null otherwise.
 template <bool FULL>
-__device__ __forceinline__ double skin_threshold(const KP& P, int u, int w,
-                                                 unsigned long long cur) {
+__device__ __forceinline__ double skin_region_bound(const KP& P, int u, int w,
+                                                    unsigned long long cur) {
   if (!cur) return 1e300;
   const Geo& G = P.G;
   int zb;
   const int st = unit_strip(G, u, zb);
   const int nxs = G.bx >> 5;
   const int y = st / nxs, xs = st - y * nxs, z = zb * 4 + w;
-  const int g = G.g, ny = 2 * g + 1, nz = FULL ? 2 * g + 1 : g + 1;
+  const int g = P.skin_reach[FULL ? 1 : 0], ny = 2 * g + 1, nz = FULL ? 2 * g + 1 : g + 1;
   const int total = nz * ny * 3;
   unsigned long long q = 0;
   for (int i = threadIdx.x & 31; i < total; i += 32) {
@@ -965,18 +1004,7 @@ __device__ __forceinline__ double skin_threshold(const KP& P, int u, int w,
   }
   const unsigned qm = __reduce_max_sync(0xffffffffu, (unsigned)q);
   if (qm >= (unsigned)kUbQMax) return 1e300;
-  return P.cutoff + 1e-9 + 2.0 * (double)qm / kUbScale;
-}
-// end of the offsets a site of sublattice par examines for threshold T
-template <bool FULL>
-__device__ __forceinline__ int skin_end(const KP& P, int par, double T) {
-  const SkinGroups& sg = FULL ? P.skf[par] : P.skh[par];
-  int n = FULL ? c_full_nin[par] : c_half_nin[par];
-  for (int i = 0; i < sg.n; ++i) {
-    if (sg.len[i] > T) return n;
-    n = sg.end[i];
-  }
-  return kMaxOffsets;
+  return (double)qm / kUbScale;
 }
 
 // density pass with the upper rho-spline window in shared memory (32-byte
@@ -1053,15 +1081,14 @@ __global__ void __launch_bounds__(NT, 1) k_density_smem(KP P, int nsb) {
   for (;;) {
     const int u = next_unit(&s_ctr, group, nsb, nu, s_slot, P.unit_rr);
     if (u >= nu) break;
-    int c;
-    const bool live = unit_cell(G, u, lane, w, c);
+    int c, cxs, cys, czs;
+    const bool live = unit_cell(G, u, lane, w, c, &cxs, &cys, &czs);
     const bool deep = live && unit_deep(G, u, lane, w, FULL);
-    const double skT = skin_threshold<FULL>(P, u, w, ub_cur);
+    const double skU = skin_region_bound<FULL>(P, u, w, ub_cur);
     for (int par = 0; par < 2; ++par) {
-      const int n_lim = skin_end<FULL>(P, par, skT);
-      density_site<FULL, B, true, REV, CMPD>(P, P.dself, par, live ? (int)(par * G.NC + c) : 0,
-                                             live, smem_addr(T), seg_lo, near_halo(G, u, w),
-                                             deep, smem_addr(T8), n_lim);
+      const int n_lim = density_site<FULL, B, true, REV, CMPD>(
+          P, P.dself, par, live ? (int)(par * G.NC + c) : 0, live, smem_addr(T), seg_lo,
+          near_halo(G, u, w), deep, smem_addr(T8), skU, cxs, cys, czs);
       if (cnt_skin) {  // diagnostic (cbx_skin_stats)
         const unsigned nl = __popc(__ballot_sync(0xffffffffu, live));
         if (lane == 0) {
