@@ -1535,6 +1535,7 @@ static cbx_status create_impl(const cbx_box* box, const cbx_potential* pot,
     P.uf = c->alloc<float4>(S);
     P.offs_const = ab_flag("CBX_OFFS_CONST", 1);
     P.unit_rr = ab_flag("CBX_UNIT_RR", 14);
+    P.idle_pred = ab_flag("CBX_IDLE_PRED", 1);
     c->mem_cat = CBX_MEM_REDUCTION;
     P.work = c->alloc<int>(4);
     cudaMemset(P.work, 0, 4 * sizeof(int));

@@ -187,6 +187,7 @@ struct KP {
   int mark_k2;                // force pass: mark the second half kick pending (merged kick)
   int offs_const;             // force pass: stencil offsets from the constant cache (else smem)
   int unit_rr;                // stencil passes: round-robin unit batches (0: contiguous ranges)
+  int idle_pred;              // force pass: idle lanes of the union walk issue no gather
   // fast hash: an atom closer than sqrt(hash_r2) to its own site (the
   // half nearest-neighbour distance sqrt(3)/4 a0 less a margin far above
   // rounding) hashes to that site and needs no periodic wrap (0: off)

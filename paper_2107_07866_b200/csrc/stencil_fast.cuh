@@ -36,6 +36,14 @@ __device__ __forceinline__ void ld256(const void* p, double& a, double& b, doubl
   // free to be scheduled early by the compiler
   asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(p));
 }
+// the 32-byte load only where pred holds (the destinations keep their values)
+__device__ __forceinline__ void ld256_pred(bool pred, const void* p, double& a, double& b,
+                                           double& c, double& d) {
+  asm("{\n .reg .pred q;\n setp.ne.b32 q, %5, 0;\n"
+      " @q ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];\n}"
+      : "+d"(a), "+d"(b), "+d"(c), "+d"(d)
+      : "l"(p), "r"((int)pred));
+}
 __device__ __forceinline__ void red_add(double* p, double v) {
   // no "memory" clobber: reductions need no ordering within the pass
   asm volatile("red.global.add.f64 [%0], %1;" ::"l"(p), "d"(v));
@@ -718,9 +726,15 @@ __device__ __forceinline__ double force_site_lean(const KP& P, KP* Pp, int par, 
       const int off = P.offs_const ? (FULL ? c_full[par][32 * wd + bit] : c_half[par][32 * wd + bit])
                                    : lds_i(so + 4 * bit);
       const int j = v ? d + off : d;
-      double px, py, pz, pw;
-      ld256(pdf + j, px, py, pz, pw);
-      const int t = deep ? j : __ldg(tgt + j);
+      double px = ax, py = ay, pz = az, pw = 0.0;
+      int t = j;
+      if (P.idle_pred) {  // idle lanes issue no gather (sparse offsets touch fewer lines)
+        ld256_pred(v, pdf + j, px, py, pz, pw);
+        if (!deep && v) t = __ldg(tgt + j);
+      } else {
+        ld256(pdf + j, px, py, pz, pw);
+        t = deep ? j : __ldg(tgt + j);
+      }
       const double dx = xsub(ax, px), dy = xsub(ay, py), dz = xsub(az, pz);
       double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
       r2 = v ? r2 : r2_idle;
