@@ -1358,9 +1358,11 @@ void launch_force_lean(const KP& P, int mode, cudaStream_t s) {
   // at most 7 units per CTA (one wave, e.g. config 2): 7 groups of 128
   // threads with 72 registers instead of 8 with 64 (CBX_FORCE_NT overrides)
   static const int nt_env = ab_flag("CBX_FORCE_NT", 0);
-  // 896 threads (72 registers, 28 warps) measured ahead of 1024 (64
-  // registers, spills) at config 5 too: 7.27 vs 7.38-7.54 ms
-  const int nt = nt_env ? nt_env : 896;
+  // more than 7 units per CTA: 1024 threads (64 registers, some spills) --
+  // since the round-robin unit batches and the predicated idle gathers,
+  // 7.12 vs 7.44 ms at config 5 (steps 4-13; 7.36 vs 7.72 at steps 51-60);
+  // round 1's order measured 896 ahead (7.27 vs 7.38-7.54)
+  const int nt = nt_env ? nt_env : ((unit_count(P.G) + g - 1) / g <= 7 ? 896 : 1024);
   if (nt == 896 && !mode) {
     if (P.rev.on)
       launch_pdl(k_force_lean_smem<false, 896, TB, true>, g + 4, 896, bytes, s, P, g);
