@@ -366,12 +366,15 @@ def run_e2e(dev, w, steps, ws=1, local=0, per_call_steps=5):
     barrier()
     t0 = time.perf_counter()
     dev.upload(s)
+    t1 = time.perf_counter()
     energies = 0.0
     for _ in range(steps):
         st = dev.step(w.dt, 1)
         energies += st["kinetic"]  # the step's result read on the host
+    t2 = time.perf_counter()
     s = dev.download(out=s)
-    el = _max_over_ranks(time.perf_counter() - t0, ws, local)
+    t3 = time.perf_counter()
+    el = _max_over_ranks(t3 - t0, ws, local)
     nbytes_out = sum(getattr(s, k).nbytes for k in ("pos", "vel", "force", "rho", "df", "tag",
                                                     "valid", "ghost", "clash_key", "clash_pos"))
     # atoms of the whole job: slot atoms + interior clash records of every rank
@@ -382,7 +385,8 @@ def run_e2e(dev, w, steps, ws=1, local=0, per_call_steps=5):
            "d2h_bytes_per_step": int(nbytes_out / steps + state_bytes), "steps": steps,
            "path": "cbx_upload_store -> %d x cbx_step(dt,1) (StepState to the host every step) "
                    "-> cbx_download_store, pinned host buffers, reference-id AoS layout "
-                   "converted on the device" % steps}
+                   "converted on the device" % steps,
+           "seconds": {"upload": t1 - t0, "steps": t2 - t1, "download": t3 - t2}}
 
     barrier()
     t0 = time.perf_counter()
