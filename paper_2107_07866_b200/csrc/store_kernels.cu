@@ -190,14 +190,18 @@ __device__ __forceinline__ void kick_drift_proc(const KP& P, int move, int zero_
 // regional displacement bound of the warp's chunk (32 consecutive interior
 // cells of one row when bx % 32 == 0): the largest |u| of its atoms, rounded
 // up to kUbScale units; atomicMax because both sublattices' warps write it
-__device__ __forceinline__ void ub_note(const KP& P, int vb, double v, unsigned long long stamp) {
+__device__ __forceinline__ void ub_note_chunk(const KP& P, long long chunk, double v,
+                                              unsigned long long stamp) {
   for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
   if ((threadIdx.x & 31) == 0 && v >= 0.0) {
     const unsigned long long q =
         v >= kUbDirty ? kUbQMax
                       : min(kUbQMax, (unsigned long long)(sqrt(v) * kUbScale) + 2ull);
-    atomicMax(P.ub + (size_t)vb * 4 + ((threadIdx.x >> 5) & 3), (stamp << kUbShift) | q);
+    atomicMax(P.ub + chunk, (stamp << kUbShift) | q);
   }
+}
+__device__ __forceinline__ void ub_note(const KP& P, int vb, double v, unsigned long long stamp) {
+  ub_note_chunk(P, (long long)vb * 4 + ((threadIdx.x >> 5) & 3), v, stamp);
 }
 
 // a single wave of blocks (resident on every SM) walks the virtual blocks
@@ -260,8 +264,8 @@ __global__ void __launch_bounds__(256, 4)
   }
 }
 
-// ---- kick/drift with TMA bulk staging (rows of whole virtual blocks,
-// bx % 128 == 0): one thread per CTA streams the inputs of the virtual blocks
+// ---- kick/drift with TMA bulk staging (rows cut into runs of up to 128
+// cells): one thread per CTA streams the inputs of the virtual blocks
 // kKdStages ahead into shared memory (cp.async.bulk + mbarrier); the 256
 // threads read their site from there, so no load occupies a register while
 // it is in flight and each SM keeps ~165 KB of reads outstanding (the
@@ -278,31 +282,43 @@ struct KdStage {
 constexpr unsigned kKdStageBytes = sizeof(KdStage);
 static_assert(kKdStageBytes % 16 == 0, "stage size");
 
-__device__ __forceinline__ long long kd_cell0(const KP& P, int vb, int& cx0, int& cy, int& cz) {
+// virtual block vb of the bulk sweep: segment seg (128 cells, the last one of
+// a row shorter when bx % 128 != 0) of interior row `row` = vb / nsr
+__host__ __device__ __forceinline__ int kd_segs(const Geo& G) { return (G.bx + 127) / 128; }
+template <bool FR>  // FR: bx % 128 == 0, every run 128 cells
+__device__ __forceinline__ long long kd_cell0(const KP& P, int vb, int& cx0, int& cy, int& cz,
+                                              int& len, int& row) {
   const Geo& G = P.G;
-  const long long e0 = (long long)vb * 128;
-  const long long row = e0 / G.bx;
-  cx0 = (int)(e0 - row * G.bx);
-  cy = (int)(row % G.by);
-  cz = (int)(row / G.by);
+  const int nsr = kd_segs(G);
+  row = vb / nsr;
+  cx0 = (vb - row * nsr) * 128;
+  len = FR ? 128 : min(128, G.bx - cx0);
+  cy = row % G.by;
+  cz = row / G.by;
   return cell_of(cx0 + G.g, cy + G.g, cz + G.g, G);
 }
+template <bool FR>
 __device__ __forceinline__ void kd_issue(const KP& P, KdStage* st, unsigned mbar, int vb) {
-  int cx0, cy, cz;
-  const long long c0 = kd_cell0(P, vb, cx0, cy, cz);
+  int cx0, cy, cz, len, row;
+  const long long c0 = kd_cell0<FR>(P, vb, cx0, cy, cz, len, row);
   const long long S = P.S, NC = P.G.NC;
-  mbar_expect_tx(mbar, kKdStageBytes);
+  unsigned bytes = 0;
+  for (int p = 0; p < 2; ++p)
+    bytes += 32u * len + 48u * ((((p * NC + c0) & 1) + len + 1) & ~1);
+  mbar_expect_tx(mbar, bytes);
   for (int p = 0; p < 2; ++p) {
     const long long d0 = p * NC + c0, a0 = d0 & ~1ll;
-    bulk_g2s(smem_addr(&st->pdf[p][0]), P.pdf + d0, 128 * 32, mbar);
+    // the 8-byte runs from the 16-byte boundary below, an even count
+    const unsigned n8 = 8u * (unsigned)((((d0 & 1) + len + 1) & ~1));
+    bulk_g2s(smem_addr(&st->pdf[p][0]), P.pdf + d0, 32u * len, mbar);
     for (int a = 0; a < 3; ++a) {
-      bulk_g2s(smem_addr(&st->vel[a][p][0]), P.vel + a * S + a0, kKdChunk * 8, mbar);
-      bulk_g2s(smem_addr(&st->frc[a][p][0]), P.frc + a * S + a0, kKdChunk * 8, mbar);
+      bulk_g2s(smem_addr(&st->vel[a][p][0]), P.vel + a * S + a0, n8, mbar);
+      bulk_g2s(smem_addr(&st->frc[a][p][0]), P.frc + a * S + a0, n8, mbar);
     }
   }
 }
 
-template <int NS, int MINB>
+template <int NS, int MINB, bool FR>
 __global__ void __launch_bounds__(256, MINB)
     k_kick_drift_bulk(KP P, int move, int nsb, int zero_acc, int images, int nvb) {
   if (blockIdx.x == nsb) finalize_pending<256>(P);
@@ -332,7 +348,7 @@ __global__ void __launch_bounds__(256, MINB)
     for (int q = 0; q < NS; ++q) mbar_init(smem_addr(&s_full[q]));
     for (int q = 0; q < NS; ++q) {
       const int vb = blockIdx.x + q * nsb;
-      if (vb < nvb) kd_issue(P, &stg[q], smem_addr(&s_full[q]), vb);
+      if (vb < nvb) kd_issue<FR>(P, &stg[q], smem_addr(&s_full[q]), vb);
     }
   }
   __syncthreads();
@@ -347,30 +363,34 @@ __global__ void __launch_bounds__(256, MINB)
     mbar_wait(smem_addr(&s_full[q]), (unsigned)(it / NS) & 1u);
     const KdStage& st = stg[q];
     KdSite a;
-    int cx0;
-    const long long c0 = kd_cell0(P, vb, cx0, a.cy, a.cz);
+    int cx0, len, row;
+    const long long c0 = kd_cell0<FR>(P, vb, cx0, a.cy, a.cz, len, row);
     const long long d = par * P.G.NC + c0;
     const int o = (int)(d & 1) + i;
-    a.d = d + i;
-    a.par = par;
-    a.cx = cx0 + i + P.G.g;
-    a.cy += P.G.g;
-    a.cz += P.G.g;
-    a.live = true;
-    a.p = st.pdf[par][i];
-    a.vx = st.vel[0][par][o];
-    a.vy = st.vel[1][par][o];
-    a.vz = st.vel[2][par][o];
-    a.fx = st.frc[0][par][o];
-    a.fy = st.frc[1][par][o];
-    a.fz = st.frc[2][par][o];
     double ub2 = -1.0;
-    kick_drift_proc(P, move, zero_acc, images, dt, hk, k2, v2s, v2m, a, ub2);
-    if (P.ub) ub_note(P, vb, ub2, stamp);
+    if (i < len) {
+      a.d = d + i;
+      a.par = par;
+      a.cx = cx0 + i + P.G.g;
+      a.cy += P.G.g;
+      a.cz += P.G.g;
+      a.live = true;
+      a.p = st.pdf[par][i];
+      a.vx = st.vel[0][par][o];
+      a.vy = st.vel[1][par][o];
+      a.vz = st.vel[2][par][o];
+      a.fx = st.frc[0][par][o];
+      a.fy = st.frc[1][par][o];
+      a.fz = st.frc[2][par][o];
+      kick_drift_proc(P, move, zero_acc, images, dt, hk, k2, v2s, v2m, a, ub2);
+    }
+    // chunk of 32 cells of the row (bx % 32 == 0 wherever P.ub is set)
+    if (P.ub) ub_note_chunk(P, (long long)row * (P.G.bx >> 5) + (cx0 >> 5) + ((t >> 5) & 3),
+                            ub2, stamp);
     __syncthreads();  // stage q is read by every thread: refill it
     if (t == 0) {
       const int vn = vb + NS * nsb;
-      if (vn < nvb) kd_issue(P, &stg[q], smem_addr(&s_full[q]), vn);
+      if (vn < nvb) kd_issue<FR>(P, &stg[q], smem_addr(&s_full[q]), vn);
     }
   }
   if (k2) {
@@ -1233,12 +1253,15 @@ static int site_wave(const KP& P, int per_sm) {
   static const int wave = ab_flag("CBX_SITE_WAVE", 1);  // 0: one block per virtual block
   return wave ? std::max(1, std::min(eam_blocks(P), per_sm * sms)) : eam_blocks(P);
 }
-// the bulk-staged sweep where a virtual block is one run of 128 cells of a
-// row (bx % 128 == 0); CBX_KD_BULK=0 (A/B build) keeps the register sweep
+// the bulk-staged sweep (a virtual block is a run of up to 128 cells of one
+// row); CBX_KD_BULK=0 (A/B build) keeps the register sweep
 bool kd_bulk(const KP& P) {
   static const int on = ab_flag("CBX_KD_BULK", 1);
-  return on && P.G.bx % 128 == 0;
+  // rows of at least 96 cells: segments of 128 (the last of a row shorter)
+  // keep >= 75 % of the lanes busy; narrower boxes take the register sweep
+  return on && (P.G.bx % 128 == 0 || P.G.bx >= 96);
 }
+static int kd_nvb(const KP& P) { return kd_segs(P.G) * P.G.by * P.G.bz; }
 // stages x CTAs per SM of the bulk sweep (CBX_KD_CFG, A/B build: 42 = 4 x 2)
 static int kd_cfg() {
   static const int c = ab_flag("CBX_KD_CFG", 42);
@@ -1253,12 +1276,18 @@ static void launch_kd_bulk(const KP& P, int move, cudaStream_t s, int zero_acc, 
   static bool attr = false;
   const int bytes = NS * (int)kKdStageBytes;
   if (!attr) {
-    cudaFuncSetAttribute(k_kick_drift_bulk<NS, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         bytes);
+    cudaFuncSetAttribute(k_kick_drift_bulk<NS, MINB, true>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    cudaFuncSetAttribute(k_kick_drift_bulk<NS, MINB, false>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
     attr = true;
   }
-  k_kick_drift_bulk<NS, MINB><<<nsb + kClashBlocks, 256, bytes, s>>>(P, move, nsb, zero_acc,
-                                                                     images, eam_blocks(P));
+  if (P.G.bx % 128 == 0)
+    k_kick_drift_bulk<NS, MINB, true><<<nsb + kClashBlocks, 256, bytes, s>>>(
+        P, move, nsb, zero_acc, images, kd_nvb(P));
+  else
+    k_kick_drift_bulk<NS, MINB, false><<<nsb + kClashBlocks, 256, bytes, s>>>(
+        P, move, nsb, zero_acc, images, kd_nvb(P));
 }
 void launch_kick_drift(const KP& P, int move, cudaStream_t s, int zero_acc, int images,
                        int n_pairp) {
