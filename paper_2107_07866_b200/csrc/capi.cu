@@ -1019,11 +1019,6 @@ void setup_fast(cbx_ctx* c) {
     cuda_check(cudaCreateTextureObject(&tex, &rd, &td, nullptr), "density record texture");
     P.tex_fd4 = (unsigned long long)tex;
     c->textures.push_back(tex);
-    rd.res.linear.devPtr = dab;
-    rd.res.linear.sizeInBytes = ab.size() * sizeof(double);
-    cuda_check(cudaCreateTextureObject(&tex, &rd, &td, nullptr), "density record texture");
-    P.tex_fab64 = (unsigned long long)tex;
-    c->textures.push_back(tex);
   }
   P.fd.ih = 1.0 / de.h;
   P.fd.c0 = -de.x0 / de.h;
@@ -1112,16 +1107,6 @@ void setup_fast(cbx_ctx* c) {
       cudaTextureObject_t tex = 0;
       cuda_check(cudaCreateTextureObject(&tex, &rd, &td, nullptr), "density table texture");
       P.tex_fd = (unsigned long long)tex;
-      c->textures.push_back(tex);
-      // its own allocation: texture memory starts on the texture alignment
-      double* dabf = c->alloc<double>(n + 1);
-      cuda_check(cudaMemcpy(dabf, &dc[2 * (n + 1)], 8 * (size_t)(n + 1), cudaMemcpyHostToDevice),
-                 "fast table");
-      rd.res.linear.devPtr = dabf;
-      rd.res.linear.desc = cudaCreateChannelDesc<int2>();
-      rd.res.linear.sizeInBytes = 8 * (size_t)(n + 1);
-      cuda_check(cudaCreateTextureObject(&tex, &rd, &td, nullptr), "density table texture");
-      P.tex_fab = (unsigned long long)tex;
       c->textures.push_back(tex);
     }
   }

@@ -174,8 +174,6 @@ struct KP {
   // mask word
   const double* fdab;
   unsigned long long tex_fd4;
-  unsigned long long tex_fab;    // the compressed records' fp32 [A B] (int2 texels)
-  unsigned long long tex_fab64;  // fdab (int4 texels)
   int nin64;
   FastTab fe;      // embedding F(rho): 4 doubles/segment (A B C D), padded
   float band_hi, band_lo;  // fp32 r^2 filter: reject above hi, exact test in [lo, hi]

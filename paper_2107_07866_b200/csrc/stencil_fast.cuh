@@ -214,10 +214,10 @@ __device__ __forceinline__ int smem_slot32(int i, int c) { return 2 * i + (c ^ (
 // CMPD: 0 the fp64 32-byte records of the window in shared memory; 1 the
 // compressed records ([D C] fp64 + [A B] fp32) in shared memory; 2 compressed,
 // [D C] by texture fetch (TEX pipe) and [A B] in shared memory (LSU pipe);
-// 3-6: the inner loop unrolled by two with alternating register sets (no
+// 3-4: the inner loop unrolled by two with alternating register sets (no
 // copies) and a one-word pair mask; tables: 3 fp64 [A B] (16 B) in shared
 // memory + [C D] by texture, 4 (default where the fp32 guard holds) those of
-// 2, 5 both halves of 2 by texture, 6 both fp64 halves by texture
+// 2 (both halves by texture, fp32 or fp64: measured slower)
 // end of the offsets a site of sublattice par examines for threshold T
 template <bool FULL>
 __device__ __forceinline__ int skin_end(const KP& P, int par, double T) {
@@ -273,7 +273,7 @@ __device__ __forceinline__ int density_site(const KP& P, KP* Pp, int par, int d,
   // compare, the near-cutoff / guard cases drop to decide().  B == 1 (the
   // shared-memory kernels): software-pipelined, the next candidate's gather
   // is in flight while the current one's table lookup and RED run
-  if constexpr (B == 1 && CMPD >= 3) {
+  if constexpr (B == 1 && (CMPD == 3 || CMPD == 4)) {
     // one inner candidate once its partner is loaded (nin <= 64: host check)
     auto cand = [&](int k, int j, int t, double px, double py, double pz) {
       const double dx = xsub(ax, px), dy = xsub(ay, py), dz = xsub(az, pz);
@@ -293,21 +293,7 @@ __device__ __forceinline__ int density_site(const KP& P, KP* Pp, int par, int d,
         const int sg = seg_index(P.fd, r2 * rsqrt_nr(r2), sv);
         const int li = sg - seg_lo;
         double tA, tB, tC, tD;
-        if (CMPD == 5) {  // both halves by texture: [D C] fp64, [A B] fp32
-          const double2 dc = tex_rec16(P.tex_fd, sg);
-          const int2 q = tex1Dfetch<int2>((cudaTextureObject_t)P.tex_fab, sg);
-          tA = (double)__int_as_float(q.x);
-          tB = (double)__int_as_float(q.y);
-          tC = dc.y;
-          tD = dc.x;
-        } else if (CMPD == 6) {  // both halves by texture, fp64
-          const double2 ab = tex_rec16(P.tex_fab64, sg);
-          const double2 cd = tex_rec16(P.tex_fd4, sg);
-          tA = ab.x;
-          tB = ab.y;
-          tC = cd.x;
-          tD = cd.y;
-        } else if (li >= 0 && CMPD == 4) {  // the compressed records of CMPD 2
+        if (li >= 0 && CMPD == 4) {  // the compressed records of CMPD 2
           const double2 dc = tex_rec16(P.tex_fd, sg);
           const float2 ab = lds_f2(tb8 + 8 * li);
           tA = (double)ab.x;
@@ -1044,8 +1030,7 @@ __global__ void __launch_bounds__(NT, 1) k_density_smem(KP P, int nsb) {
   if (threadIdx.x == 0) s_ctr = 0;
   // an even first record: the fp32 [A B] pairs (8 bytes each) are then
   // 16-byte aligned for the bulk copy
-  // 4: the tables of 2, the loop of 3; 5, 6: no shared-memory window
-  constexpr int CM = CMPD == 4 ? 2 : CMPD;
+  constexpr int CM = CMPD == 4 ? 2 : CMPD;  // 4: the tables of 2, the loop of 3
   const int seg_lo = CM == 3 ? max(0, nseg + 1 - kDensTabRecords)
                      : CM ? dens_window_lo_cmp(nseg) : max(0, nseg + 1 - kDensTabRecords);
   const int nrec = nseg + 1 - seg_lo;
@@ -1055,8 +1040,7 @@ __global__ void __launch_bounds__(NT, 1) k_density_smem(KP P, int nsb) {
   // (CMPD 2: only the [A B] pairs are staged, from offset 0)
   double2* T8 = CM == 2 ? T : T + kDensTabRecords;  // byte offset 16 x kDensTabRecords
   __shared__ __align__(8) unsigned long long s_mbar;
-  if (CM >= 5) {
-  } else if (CM == 3) {  // the window's fp64 [A B] pairs, one bulk copy
+  if (CM == 3) {  // the window's fp64 [A B] pairs, one bulk copy
     if (threadIdx.x == 0) {
       const unsigned mb = smem_addr(&s_mbar);
       mbar_init(mb);
@@ -1081,7 +1065,7 @@ __global__ void __launch_bounds__(NT, 1) k_density_smem(KP P, int nsb) {
     for (int q = threadIdx.x; q < 2 * nrec; q += blockDim.x) T[smem_slot32(q >> 1, q & 1)] = __ldg(src + q);
   }
   __syncthreads();  // the barrier's initialisation is visible
-  if (CMPD && CM < 5) mbar_wait0(smem_addr(&s_mbar));
+  if (CMPD) mbar_wait0(smem_addr(&s_mbar));
   pdl_wait();
   pdl_trigger();
   if (P.st->err || P.st->halt) return;
@@ -1272,7 +1256,7 @@ static int sm_count() {
 // density_site); returns true when the clash-record pass ran in the launch
 template <int CMPD>
 bool launch_density_smem(const KP& P, int mode, cudaStream_t s) {
-  const size_t bytes = CMPD >= 5 ? 16 :
+  const size_t bytes =
       (size_t)kDensTabRecords * (CMPD == 3 ? 16 : CMPD >= 2 ? 8 : CMPD == 1 ? 24 : 32);
   static bool attr = false;
   if (!attr) {
@@ -1302,13 +1286,12 @@ int density_table_mode(const KP& P) {
   // mask word) with the compressed records where the local fp32 guard held
   // (P.fdc: [D C] by texture, fp32 [A B] in shared memory -- 4), else fp64
   // [A B] in shared memory and [C D] by texture (3).  Measured at config 5
-  // (A/B, same box): 4: 4.31 ms; 5 (both halves by texture): 4.33; 3: 4.63;
-  // 6 (fp64, both by texture): 4.67; 2 (round-2 loop, tables of 4): 4.54
+  // (A/B, same box): 4: 4.31 ms; both halves by texture: 4.33; 3: 4.63;
+  // fp64 both by texture: 4.67; 2 (round-2 loop, tables of 4): 4.54
   static const int tm = ab_flag("CBX_DENSITY_TAB", -1);
   if (tm < 0) return P.nin64 ? (P.fdc ? 4 : 3) : (P.fdc ? 2 : 0);
   if (tm == 3) return P.nin64 ? 3 : 0;
-  if (tm == 4 || tm == 5) return P.nin64 && P.fdc ? tm : 0;
-  if (tm == 6) return P.nin64 ? 6 : 0;
+  if (tm == 4) return P.nin64 && P.fdc ? 4 : 0;
   return tm && P.fdc ? tm : 0;
 }
 
@@ -1322,8 +1305,6 @@ bool launch_density_fast(const KP& P, int mode, int grid, cudaStream_t s) {
     const int tm = density_table_mode(P);
     if (tm == 3) return launch_density_smem<3>(P, mode, s);
     if (tm == 4) return launch_density_smem<4>(P, mode, s);
-    if (tm == 5) return launch_density_smem<5>(P, mode, s);
-    if (tm == 6) return launch_density_smem<6>(P, mode, s);
     if (tm == 2) return launch_density_smem<2>(P, mode, s);
     if (tm == 1) return launch_density_smem<1>(P, mode, s);
     return launch_density_smem<0>(P, mode, s);
