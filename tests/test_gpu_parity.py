@@ -424,6 +424,37 @@ def test_skin_pruning_regional_bounds(cuda, tables, stencil):
     assert saw_clash
 
 
+@pytest.mark.parametrize("shift", [0.0, 0.2, 0.45])
+def test_skin_pruning_displaced_atom(cuda, tables, shift):
+    """A perfect lattice (every displacement bound ~0, so the skin shells are
+    pruned) with one atom moved by `shift` A toward its shell-6 neighbour at
+    2 a0 = 5.71 A: at 0.2 A the pair (5.51 A) and, at 0.45 A, a shell-7 pair
+    enter the cutoff (5.6 A) and must be found -- the moved atom's own bound
+    and its chunk's bound lift the skin threshold for every warp that can
+    pair with it; the rest of the box keeps pruning"""
+    from oracle import oracle
+    ref = oracle.Sim(tables["baseline"], box=(64, 4, 8), temperature=0.0, seed=3)
+    dims, a0, g = ref.box
+    tx, ty = 64 + 2 * g, 4 + 2 * g
+    site = ((g + 3) * ty + (g + 1)) * 2 * tx + 2 * (g + 30)  # corner atom of cell (30, 1, 3)
+    s = ref.store()
+    ref.set_atom(site, pos=s.pos[site] + np.array([shift, 0.0, 0.0]))
+    ref.rehash()
+    dev = device_for(ref, tables["baseline"])
+    dev.skin_stats(True)
+    ref.step(1e-3, 1)
+    dev.step(1e-3, 1)
+    seen, listed = dev.skin_stats(False)
+    assert seen < 0.5 * listed, (seen, listed)
+    assert_store_parity(ref.store(), dev.download(), pos_tol=1e-12,
+                        what=f"displaced atom {shift}")
+    # the shifted atom's partners: pairs beyond the lattice shells were counted
+    if shift > 0.0:
+        a, b = by_tag(ref.store()), by_tag(dev.download())
+        t = int(ref.store().tag[site])
+        assert np.abs(a[t][2] - b[t][2]).max() <= 1e-10 * max(1.0, np.abs(a[t][2]).max())
+
+
 def test_overlap_halts_multi_step_call(cuda, tables):
     """An overlap found in step 2 of a 5-step call (fixed dt: merged kicks and
     deferred StepState sums) ends the call at step 2 like the reference's
