@@ -1058,6 +1058,26 @@ void setup_fast(cbx_ctx* c) {
     cuda_check(cudaCreateTextureObject(&tex, &rd, &td, nullptr), "force table texture");
     P.tex_ff = (unsigned long long)tex;
     c->textures.push_back(tex);
+    // the two chunks the force pass fetches through TEX, packed: [zA zB qA qB]
+    // is one 32-byte sector per segment (in the 64-byte records they sit in
+    // two sectors whose other halves -- staged in shared memory -- would
+    // occupy L1 beside the partner gathers; thermal displacements spread a
+    // warp's pairs over ~2000 segments)
+    std::vector<double> fab(4 * (n + 1));
+    for (int i = 0; i <= n; ++i) {
+      const double* r = &ff[8 * i];
+      fab[4 * i] = r[0];
+      fab[4 * i + 1] = r[1];
+      fab[4 * i + 2] = r[4];
+      fab[4 * i + 3] = r[5];
+    }
+    P.ffab = up(fab);
+    rd.res.linear.devPtr = const_cast<double*>(P.ffab);
+    rd.res.linear.sizeInBytes = fab.size() * sizeof(double);
+    cudaTextureObject_t tex2 = 0;
+    cuda_check(cudaCreateTextureObject(&tex2, &rd, &td, nullptr), "force [A B] texture");
+    P.tex_fab = (unsigned long long)tex2;
+    c->textures.push_back(tex2);
   }
   // compressed density records for the density pass: [D C] in fp64, the
   // cubic and quadratic coefficients A, B (~1e-9 and ~1e-6 of rho at the
@@ -1521,6 +1541,8 @@ static cbx_status create_impl(const cbx_box* box, const cbx_potential* pot,
     P.offs_const = ab_flag("CBX_OFFS_CONST", 1);
     P.unit_rr = ab_flag("CBX_UNIT_RR", 14);
     P.idle_pred = ab_flag("CBX_IDLE_PRED", 1);
+    P.skin_lane = ab_flag("CBX_SKIN_LANE", 1);
+    P.tab_packed = ab_flag("CBX_TAB_PACKED", 1);
     c->mem_cat = CBX_MEM_REDUCTION;
     P.work = c->alloc<int>(4);
     cudaMemset(P.work, 0, 4 * sizeof(int));

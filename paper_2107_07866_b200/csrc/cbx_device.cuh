@@ -164,6 +164,8 @@ struct KP {
   // tex_ff (int4 texels, 4 per record) for the chunks fetched through TEX
   const double *ffz, *ffzc, *ffqc;
   unsigned long long tex_ff;  // cudaTextureObject_t
+  const double* ffab;         // [zA zB qA qB] per segment (32 B), bound to tex_fab (int4 texels, 2 per segment)
+  unsigned long long tex_fab;
   unsigned long long tex_fd;  // the compressed density records' [D C] (int4 texels)
   // compressed density records: [D C] (16 B) then, after the last record,
   // [A B as fp32] (8 B) per record; null when the fp32 rounding bound fails
@@ -186,6 +188,8 @@ struct KP {
   int offs_const;             // force pass: stencil offsets from the constant cache (else smem)
   int unit_rr;                // stencil passes: round-robin unit batches (0: contiguous ranges)
   int idle_pred;              // force pass: idle lanes of the union walk issue no gather
+  int tab_packed;             // force pass: the TEX-fetched chunks from the packed [zA zB qA qB] array
+  int skin_lane;              // force pass: each lane walks its own skin bits after the inner union
   // fast hash: an atom closer than sqrt(hash_r2) to its own site (the
   // half nearest-neighbour distance sqrt(3)/4 a0 less a margin far above
   // rounding) hashes to that site and needs no periodic wrap (0: off)

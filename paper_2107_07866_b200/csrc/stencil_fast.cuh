@@ -477,12 +477,31 @@ __device__ __forceinline__ int density_site(const KP& P, KP* Pp, int par, int d,
       pass[b] = k0 + b < n && fmaf(fz, fz, fmaf(fy, fy, fx * fx)) <= hi;
       any |= pass[b];
     }
-    if (any) {
+#ifdef CBX_AB
+    if (any && !P.skin_lane) {  // experiment build: one divergent pass per candidate
 #pragma unroll
       for (int b = 0; b < 4; ++b)
         if (pass[b])
           acc += skin_density<FULL, REV>(P, Pp, par, k0 + b, d, jj[b], __float_as_int(pf[b].w), ax,
                                     ay, az, m0, m1);
+      any = false;
+    }
+#endif
+    if (any) {
+      // each lane walks its OWN passing candidates (few lanes pass any one of
+      // them): the warp runs the full decision max-over-lanes times, not once
+      // per candidate some lane passed
+      unsigned pm = (unsigned)pass[0] | (unsigned)pass[1] << 1 | (unsigned)pass[2] << 2 |
+                    (unsigned)pass[3] << 3;
+#pragma unroll 1
+      while (pm) {
+        const int b = __ffs(pm) - 1;
+        pm &= pm - 1;
+        const int jb = b == 0 ? jj[0] : b == 1 ? jj[1] : b == 2 ? jj[2] : jj[3];
+        const float wb = b == 0 ? pf[0].w : b == 1 ? pf[1].w : b == 2 ? pf[2].w : pf[3].w;
+        acc += skin_density<FULL, REV>(P, Pp, par, k0 + b, d, jb, __float_as_int(wb), ax, ay, az,
+                                       m0, m1);
+      }
     }
   }
   if (FULL) P.rho[d] = acc;
@@ -695,22 +714,60 @@ __device__ __forceinline__ double force_site_lean(const KP& P, KP* Pp, int par, 
   const double r2_idle = P.cut2_lo;
   double fx = 0.0, fy = 0.0, fz = 0.0, e = 0.0;
   // the warp walks the union of its lanes' masks (warp-uniform offset, lanes
-  // without the bit idle), one 32-bit word at a time
+  // without the bit idle), one 32-bit word at a time.  Skin offsets (k >= nin,
+  // P.skin_lane): the lattice puts them beyond the cutoff, so few lanes hold
+  // any one of them (shell 6 at 600 K: ~16 % each) -- after the inner offsets
+  // every lane walks its OWN skin bits (lane-varying offset from the staged
+  // shared-memory copy): max over the lanes of their skin-pair counts
+  // iterations instead of the size of the union
+#ifdef CBX_AB  // experiment build: runtime switches back to the earlier variants
+  const bool packed = P.tab_packed != 0, skin_lane = P.skin_lane != 0;
+#else
+  constexpr bool packed = true, skin_lane = true;
+#endif
+  const int nin = skin_lane ? (FULL ? c_full_nin[par] : c_half_nin[par]) : kMaskBits + 1;
   {
+  int wd = 0;
+  unsigned cu = 0, co = 0;
 #pragma unroll 1
-  for (int wd = 0; wd < 4; ++wd) {
-    const unsigned long long mw = wd < 2 ? m0 : m1;
-    const unsigned co = (wd & 1) ? (unsigned)(mw >> 32) : (unsigned)mw;
-    unsigned cu = __reduce_or_sync(0xffffffffu, co);
-    const unsigned so = s_offs + 128 * wd;
-    while (cu) {
-      const int bit = __ffs(cu) - 1;
-      cu &= cu - 1;
-      const bool v = (co >> bit) & 1;
-      // the offset: a warp-uniform index, from the constant cache (no LSU
-      // wavefront) or the staged shared-memory copy
-      const int off = P.offs_const ? (FULL ? c_full[par][32 * wd + bit] : c_half[par][32 * wd + bit])
-                                   : lds_i(so + 4 * bit);
+  for (;;) {
+      bool v;
+      int off;
+      if (wd <= 4) {  // inner offsets: the union walk
+        if (!cu) {
+          if (wd == 4 || 32 * wd >= nin) {  // the lanes' own skin bits from here
+            if (nin > kMaskBits) break;
+            if (nin < 64) { m0 &= ~0ull << nin; } else { m0 = 0; m1 &= ~0ull << (nin - 64); }
+            wd = 5;
+            continue;
+          }
+          const unsigned long long mw = wd < 2 ? m0 : m1;
+          co = (wd & 1) ? (unsigned)(mw >> 32) : (unsigned)mw;
+          if (nin - 32 * wd < 32) co &= (1u << (nin - 32 * wd)) - 1u;
+          cu = __reduce_or_sync(0xffffffffu, co);
+          ++wd;
+          continue;
+        }
+        const int bit = __ffs(cu) - 1;
+        cu &= cu - 1;
+        v = (co >> bit) & 1;
+        // the offset: a warp-uniform index, from the constant cache (no LSU
+        // wavefront) or the staged shared-memory copy
+        const int k = 32 * (wd - 1) + bit;
+        off = P.offs_const ? (FULL ? c_full[par][k] : c_half[par][k]) : lds_i(s_offs + 4 * k);
+      } else {
+        v = (m0 | m1) != 0;
+        if (!__any_sync(0xffffffffu, v)) break;
+        int k = 0;
+        if (m0) {
+          k = __ffsll((long long)m0) - 1;
+          m0 &= m0 - 1;
+        } else if (m1) {
+          k = 63 + __ffsll((long long)m1);
+          m1 &= m1 - 1;
+        }
+        off = lds_i(s_offs + 4 * k);
+      }
       const int j = v ? d + off : d;
       double px = ax, py = ay, pz = az, pw = 0.0;
       int t = j;
@@ -741,7 +798,10 @@ __device__ __forceinline__ double force_site_lean(const KP& P, KP* Pp, int par, 
           zA = c0.x; zB = c0.y; zC = c1.x; zD = c1.y;
         }
       } else if (TB == kTabSplit3) {
-        const double2 c0 = tex_chunk(P.tex_ff, seg, 0), q0 = tex_chunk(P.tex_ff, seg, 2);
+        // [zA zB] and [qA qB]: the two halves of one 32-byte sector of the
+        // packed array (P.tab_packed; else chunks 0 and 2 of the 64-byte record)
+        const double2 c0 = packed ? tex_rec16(P.tex_fab, 2 * seg) : tex_chunk(P.tex_ff, seg, 0);
+        const double2 q0 = packed ? tex_rec16(P.tex_fab, 2 * seg + 1) : tex_chunk(P.tex_ff, seg, 2);
         zA = c0.x; zB = c0.y; qA = q0.x; qB = q0.y;
         if (li >= 0) {
           const double2 c1 = lds2(tb + 16 * lc);
@@ -793,7 +853,6 @@ __device__ __forceinline__ double force_site_lean(const KP& P, KP* Pp, int par, 
           }
         }
       }
-  }
   }
   }
   const int* offs = FULL ? c_full[par] : c_half[par];

@@ -1,6 +1,9 @@
 """Summarise ncu captures into the committed profiles/ files.
 
-    python profiles/summarize.py <report.ncu-rep> <launches.csv> <tag> [config]
+    python profiles/summarize.py <report.ncu-rep | raw.csv> <launches.csv | -> <tag> [config | -]
+
+(a raw.csv is the `--page raw --csv` export of the report; `-` for the launch
+list or the config skips the launch file / the traffic file)
 
 Writes profiles/<tag>_kernels.md (per-kernel key metrics of the --set full
 capture), profiles/<tag>_launches.csv (launch list: kernel, duration) and
@@ -46,8 +49,12 @@ def to_bytes(v, unit):
 def main():
     rep, launches, tag = sys.argv[1:4]
     config = sys.argv[4] if len(sys.argv) > 4 else "c5"
-    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
-                         text=True).stdout
+    if rep.endswith(".csv"):  # `ncu -i X.ncu-rep --page raw --csv` exported on the GPU box
+        raw = open(rep).read()
+        raw = raw[raw.find('"ID"'):]
+    else:
+        raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                             text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, units = rows[0], rows[1]
     lines = [f"# ncu --set full summary ({tag})", "",
@@ -91,7 +98,11 @@ def main():
     open(os.path.join(HERE, f"{tag}_kernels.md"), "w").write("\n".join(lines) + "\n")
     traffic["source"] = (f"profiles/{tag}_kernels.md, config {config} "
                          "(dram__bytes_read.sum + dram__bytes_write.sum per launch)")
-    json.dump(traffic, open(os.path.join(HERE, f"traffic_{config}.json"), "w"), indent=1)
+    if config != "-":
+        json.dump(traffic, open(os.path.join(HERE, f"traffic_{config}.json"), "w"), indent=1)
+    if launches == "-":
+        print("wrote", tag)
+        return
     # launch list: kernel name, duration
     out = []
     with open(launches) as f:
