@@ -28,6 +28,7 @@ struct SnapSlot {
 };
 
 struct cbx_ctx {
+  std::vector<double> shells;  // distinct lattice distances of the stencil sites within the cutoff
   int device = 0;
   cudaStream_t stream = nullptr;
   cbx_box box{};
@@ -961,6 +962,55 @@ void sync_kp(cbx_ctx* c) {
   cuda_check(cudaMemcpy(c->P.dself, &c->P, sizeof(KP), cudaMemcpyHostToDevice), "kp upload");
 }
 
+// Shared-memory window of the force table (split-3 layout, stencil_fast.cuh).
+// shells: the distinct lattice distances of the stencil sites within the
+// cutoff, ascending.  The window must hold every record a pair near a shell
+// can touch: r in [R - margin, R + margin], and everything from the last
+// shell up to the cutoff (the skin shells enter there).  If dropping the
+// records below the first shell's margin and a stretch inside the widest gap
+// between two shells brings the window down to kLeanTabRecordsGap records,
+// the gapped window is used (pairs inside the gap or below the window -- a
+// cascade core -- fetch every chunk by texture, as pairs below the window
+// always did); otherwise the contiguous top kLeanTabRecords records.
+void force_window_setup(cbx_ctx* c, const std::vector<double>& shells) {
+  KP& P = c->P;
+  const int n1 = P.ff.nseg + 1;  // records 0..nseg
+  const int lo0 = n1 - kLeanTabRecords;
+  P.fw_lo = ((lo0 > 0 ? lo0 : 0) + 1) & ~1;
+  P.fw_gap_lo = 0x7fffffff;
+  P.fw_gap_n = 0;
+  P.fw_cap = kLeanTabRecords;
+  if (shells.empty() || !ab_flag("CBX_FORCE_GAP", 1)) return;
+  constexpr double margin = 0.30;  // A: ~3.5 sigma of a bond length at 600 K
+  const double x0 = c->pot.zr.x0, h = c->pot.zr.h;
+  auto seg_of = [&](double r) { return (int)std::floor((r - x0) / h); };
+  int lo = std::max(0, seg_of(shells.front() - margin)) & ~1;
+  if (lo < P.fw_lo) lo = P.fw_lo;  // never below the contiguous window's start
+  const int need = (n1 - lo) - kLeanTabRecordsGap;
+  if (need <= 0) {  // fits without a gap
+    P.fw_lo = lo;
+    P.fw_cap = kLeanTabRecordsGap;
+    return;
+  }
+  // the widest stretch between two shells' margins
+  int best_lo = 0, best_n = 0;
+  for (size_t i = 0; i + 1 < shells.size(); ++i) {
+    const int a = seg_of(shells[i] + margin) + 1, b = seg_of(shells[i + 1] - margin);
+    if (b - a > best_n) {
+      best_n = b - a;
+      best_lo = a;
+    }
+  }
+  const int gn = (need + 1) & ~1;
+  if (best_n < gn + 2) return;  // no stretch wide enough: contiguous window
+  const int glo = (best_lo + (best_n - gn) / 2 + 1) & ~1;  // centred, even
+  if (glo <= lo || glo + gn >= n1) return;
+  P.fw_lo = lo;
+  P.fw_gap_lo = glo;
+  P.fw_gap_n = gn;
+  P.fw_cap = kLeanTabRecordsGap;
+}
+
 // fast-path tables and the fp32 filter band (stencil_fast.cuh)
 void setup_fast(cbx_ctx* c) {
   KP& P = c->P;
@@ -1413,6 +1463,21 @@ static cbx_status create_impl(const cbx_box* box, const cbx_potential* pot,
     c->const_ready = true;
     if (c->device < 64 && g_const_owner[c->device] == c.get()) g_const_owner[c->device] = nullptr;
     bind_constants(c.get());
+    {  // the force table's shared-memory window, around the stencil's shells
+      std::vector<double> shells;
+      for (int par = 0; par < 2; ++par)
+        for (const Offset& o : c->offs.full[par]) {
+          const double hh = o.cross ? (par ? -0.5 : 0.5) : 0.0;
+          const double x = o.dx + hh, y = o.dy + hh, z = o.dz + hh;
+          const double r = std::sqrt(x * x + y * y + z * z) * box->a0;
+          if (r <= pot->cutoff) shells.push_back(r);
+        }
+      std::sort(shells.begin(), shells.end());
+      std::vector<double> uniq;
+      for (double r : shells)
+        if (uniq.empty() || r - uniq.back() > 1e-6) uniq.push_back(r);
+      c->shells = uniq;  // force_window_setup, once the tables exist
+    }
     // ghost list and owner map
     const long long S = c->S;
     std::vector<int> tgt(S), gdst, gsrc;
@@ -1548,6 +1613,7 @@ static cbx_status create_impl(const cbx_box* box, const cbx_potential* pot,
     cudaMemset(P.work, 0, 4 * sizeof(int));
     c->mem_cat = CBX_MEM_TABLES;
     setup_fast(c.get());
+    force_window_setup(c.get(), c->shells);
     c->mem_cat = CBX_MEM_REDUCTION;
     P.st = c->alloc<DevStatus>(1);
     P.dself = c->alloc<KP>(1);
@@ -2544,10 +2610,12 @@ CBX_API cbx_status cbx_describe(cbx_ctx* c, char* buf, long n) {
                   "\"force_table\": %d, "
                   "\"pair_mask\": %d, \"slots\": %lld, \"ghost_sites\": %d, "
                   "\"clash_capacity\": %d, \"band_A2\": %.3e, \"skin_prune\": %d, "
-                  "\"kick_drift_bulk\": %d, \"sm_count\": %d}",
+                  "\"kick_drift_bulk\": %d, \"force_window\": [%d, %d, %d, %d], "
+                  "\"sm_count\": %d}",
                   c->mode, (int)c->fast_ok, (int)c->fp32_density, force_table_mode(),
                   (int)(c->P.pmask != nullptr), c->S, c->n_ghost, c->P.cap_clash, c->band,
-                  (int)(c->P.ub != nullptr), (int)kd_bulk(c->P),
+                  (int)(c->P.ub != nullptr), (int)kd_bulk(c->P), c->P.fw_lo,
+                  c->P.fw_gap_n ? c->P.fw_gap_lo : -1, c->P.fw_gap_n, c->P.fw_cap,
                   [] {
                     int d = 0, n = 0;
                     cudaGetDevice(&d);

@@ -123,6 +123,16 @@ __host__ __device__ __forceinline__ int dens_window_lo_cmp(int nseg) {
   return ((lo > 0 ? lo : 0) + 1) & ~1;
 }
 
+// records of the force spline window staged in shared memory by the force
+// pass (contiguous: the top kLeanTabRecords records).  Split-3 layout (24 B
+// per record): when the lattice leaves a stretch of r between two neighbour
+// shells that no pair visits short of a cascade core, the window skips it and
+// fits kLeanTabRecordsGap records -- 62.4 KB, inside the 64 KB shared-memory
+// carveout instead of the 100 KB one, i.e. 36 KB more L1 for the partner
+// gathers and the texture fetches (capi.cu force_window_setup)
+constexpr int kLeanTabRecords = 3300;
+constexpr int kLeanTabRecordsGap = 2600;
+
 // Regional displacement bound (density-pass skin pruning).  One entry per
 // chunk of 32 interior cells of an x row (both sublattices), written by
 // k_kick_drift: (stamp << kUbShift) | q, q >= |u| * kUbScale for every atom of
@@ -188,6 +198,10 @@ struct KP {
   int offs_const;             // force pass: stencil offsets from the constant cache (else smem)
   int unit_rr;                // stencil passes: round-robin unit batches (0: contiguous ranges)
   int idle_pred;              // force pass: idle lanes of the union walk issue no gather
+  // force pass, split-3 table: the shared-memory window holds records
+  // [fw_lo, nseg] minus [fw_gap_lo, fw_gap_lo + fw_gap_n) (fw_gap_n == 0:
+  // contiguous, fw_gap_lo = INT_MAX); fw_cap records of capacity
+  int fw_lo, fw_gap_lo, fw_gap_n, fw_cap;
   int tab_packed;             // force pass: the TEX-fetched chunks from the packed [zA zB qA qB] array
   int skin_lane;              // force pass: each lane walks its own skin bits after the inner union
   // fast hash: an atom closer than sqrt(hash_r2) to its own site (the

@@ -477,31 +477,15 @@ __device__ __forceinline__ int density_site(const KP& P, KP* Pp, int par, int d,
       pass[b] = k0 + b < n && fmaf(fz, fz, fmaf(fy, fy, fx * fx)) <= hi;
       any |= pass[b];
     }
-#ifdef CBX_AB
-    if (any && !P.skin_lane) {  // experiment build: one divergent pass per candidate
+    if (any) {
+      // (each lane walking its own passing candidates in a loop -- max over
+      // the lanes instead of one divergent pass per candidate -- measured
+      // slower: density 4.93 vs 4.24 ms at config 5, the loop's selects spill)
 #pragma unroll
       for (int b = 0; b < 4; ++b)
         if (pass[b])
           acc += skin_density<FULL, REV>(P, Pp, par, k0 + b, d, jj[b], __float_as_int(pf[b].w), ax,
                                     ay, az, m0, m1);
-      any = false;
-    }
-#endif
-    if (any) {
-      // each lane walks its OWN passing candidates (few lanes pass any one of
-      // them): the warp runs the full decision max-over-lanes times, not once
-      // per candidate some lane passed
-      unsigned pm = (unsigned)pass[0] | (unsigned)pass[1] << 1 | (unsigned)pass[2] << 2 |
-                    (unsigned)pass[3] << 3;
-#pragma unroll 1
-      while (pm) {
-        const int b = __ffs(pm) - 1;
-        pm &= pm - 1;
-        const int jb = b == 0 ? jj[0] : b == 1 ? jj[1] : b == 2 ? jj[2] : jj[3];
-        const float wb = b == 0 ? pf[0].w : b == 1 ? pf[1].w : b == 2 ? pf[2].w : pf[3].w;
-        acc += skin_density<FULL, REV>(P, Pp, par, k0 + b, d, jb, __float_as_int(wb), ax, ay, az,
-                                       m0, m1);
-      }
     }
   }
   if (FULL) P.rho[d] = acc;
@@ -722,8 +706,9 @@ __device__ __forceinline__ double force_site_lean(const KP& P, KP* Pp, int par, 
   // iterations instead of the size of the union
 #ifdef CBX_AB  // experiment build: runtime switches back to the earlier variants
   const bool packed = P.tab_packed != 0, skin_lane = P.skin_lane != 0;
+  const bool offs_const = P.offs_const != 0, idle_pred = P.idle_pred != 0;
 #else
-  constexpr bool packed = true, skin_lane = true;
+  constexpr bool packed = true, skin_lane = true, offs_const = true, idle_pred = true;
 #endif
   const int nin = skin_lane ? (FULL ? c_full_nin[par] : c_half_nin[par]) : kMaskBits + 1;
   {
@@ -754,7 +739,7 @@ __device__ __forceinline__ double force_site_lean(const KP& P, KP* Pp, int par, 
         // the offset: a warp-uniform index, from the constant cache (no LSU
         // wavefront) or the staged shared-memory copy
         const int k = 32 * (wd - 1) + bit;
-        off = P.offs_const ? (FULL ? c_full[par][k] : c_half[par][k]) : lds_i(s_offs + 4 * k);
+        off = offs_const ? (FULL ? c_full[par][k] : c_half[par][k]) : lds_i(s_offs + 4 * k);
       } else {
         v = (m0 | m1) != 0;
         if (!__any_sync(0xffffffffu, v)) break;
@@ -771,7 +756,7 @@ __device__ __forceinline__ double force_site_lean(const KP& P, KP* Pp, int par, 
       const int j = v ? d + off : d;
       double px = ax, py = ay, pz = az, pw = 0.0;
       int t = j;
-      if (P.idle_pred) {  // idle lanes issue no gather (sparse offsets touch fewer lines)
+      if (idle_pred) {  // idle lanes issue no gather (sparse offsets touch fewer lines)
         ld256_pred(v, pdf + j, px, py, pz, pw);
         if (!deep && v) t = __ldg(tgt + j);
       } else {
@@ -785,7 +770,11 @@ __device__ __forceinline__ double force_site_lean(const KP& P, KP* Pp, int par, 
       double sb;
       const int seg = seg_index(P.ff, r2 * ri, sb);
       double zA, zB, zC, zD, qA, qB, qC;
-      const int li = seg - seg_lo;
+      int li = seg - seg_lo;
+      if (TB == kTabSplit3) {  // the window's gap: records above it move down, inside it -> texture
+        const bool up = seg >= P.fw_gap_lo + P.fw_gap_n;
+        li = up ? li - P.fw_gap_n : (seg >= P.fw_gap_lo ? -1 : li);
+      }
       const int lc = max(li, 0);
       if (TB == kTabSplit) {
         const double2 q0 = tex_chunk(P.tex_ff, seg, 2), q1 = tex_chunk(P.tex_ff, seg, 3);
@@ -1201,7 +1190,7 @@ __global__ void __launch_bounds__(128, 4) k_force_fast(KP P) {
 // kTabSplit3): 1024 threads, one CTA per SM, 8 groups of 4 warps each on
 // their own unit.  Pairs below the window (cascade cores) read global /
 // texture records.
-constexpr int kLeanTabRecords = 3300;  // x 64 B = 211,200 B; split: x 32 B / x 24 B
+// kLeanTabRecords (cbx_device.cuh): x 64 B = 211,200 B; split: x 32 B / x 24 B
 
 __host__ __device__ __forceinline__ int force_window_lo(int nseg, int tb) {
   const int lo = nseg + 1 - kLeanTabRecords;
@@ -1229,9 +1218,12 @@ __global__ void __launch_bounds__(NT, 1) k_force_lean_smem(KP P, int nsb) {
   double2* T = reinterpret_cast<double2*>(smem_tab);
   const int nseg = P.ff.nseg;  // records 0..nseg (padded)
   if (threadIdx.x == 0) s_ctr = 0;
-  const int seg_lo = force_window_lo(nseg, TB);
-  const int nrec = nseg + 1 - seg_lo;
-  const unsigned tb8 = smem_addr(T) + 16u * kLeanTabRecords;  // split-3: the qC array
+  // split-3: the window [fw_lo, nseg] minus the gap [fw_gap_lo, fw_gap_lo +
+  // fw_gap_n) between two neighbour shells (capi.cu, force_window_setup)
+  const int seg_lo = TB == kTabSplit3 ? P.fw_lo : force_window_lo(nseg, TB);
+  const int gap_n = TB == kTabSplit3 ? P.fw_gap_n : 0;
+  const int nrec = nseg + 1 - seg_lo - gap_n;
+  const unsigned tb8 = smem_addr(T) + 16u * (TB == kTabSplit3 ? P.fw_cap : kLeanTabRecords);  // split-3: the qC array
   __shared__ __align__(8) unsigned long long s_mbar;
   if (TB != kTabSmem64) {  // bulk copies of the window's chunks, one thread
     if (threadIdx.x == 0) {
@@ -1241,10 +1233,17 @@ __global__ void __launch_bounds__(NT, 1) k_force_lean_smem(KP P, int nsb) {
         mbar_expect_tx(mb, 32u * nrec);
         bulk_stage(smem_addr(T), P.ffz + 4 * (size_t)seg_lo, 32u * nrec, mb);
       } else {
-        const unsigned b8 = (8u * nrec + 15u) & ~15u;
-        mbar_expect_tx(mb, 16u * nrec + b8);
-        bulk_stage(smem_addr(T), P.ffzc + 2 * (size_t)seg_lo, 16u * nrec, mb);
-        bulk_stage(tb8, P.ffqc + seg_lo, b8, mb);
+        // records below the gap (n1, even) and above it (n2)
+        const int n1 = gap_n ? P.fw_gap_lo - seg_lo : nrec, n2 = nrec - n1;
+        const int up = gap_n ? P.fw_gap_lo + gap_n : 0;  // first record above the gap
+        const unsigned b1 = (8u * n1 + 15u) & ~15u, b2 = (8u * n2 + 15u) & ~15u;
+        mbar_expect_tx(mb, 16u * nrec + b1 + (n2 ? b2 : 0u));
+        bulk_stage(smem_addr(T), P.ffzc + 2 * (size_t)seg_lo, 16u * n1, mb);
+        bulk_stage(tb8, P.ffqc + seg_lo, b1, mb);
+        if (n2) {
+          bulk_stage(smem_addr(T) + 16u * n1, P.ffzc + 2 * (size_t)up, 16u * n2, mb);
+          bulk_stage(tb8 + 8u * n1, P.ffqc + up, b2, mb);
+        }
       }
     }
   } else {
@@ -1380,9 +1379,11 @@ bool launch_density_fast(const KP& P, int mode, int grid, cudaStream_t s) {
 // re-derives every pair
 template <int TB>
 void launch_force_lean(const KP& P, int mode, cudaStream_t s) {
-  const size_t bytes = (size_t)kLeanTabRecords * kTabSmemBytes[TB] + 16;
-  static bool attr = false;
-  if (!attr) {
+  const size_t bytes =
+      (size_t)(TB == kTabSplit3 ? P.fw_cap : kLeanTabRecords) * kTabSmemBytes[TB] + 16;
+  static size_t attr_bytes = 0;  // the largest size the kernels were set up for
+  if (attr_bytes < bytes) {
+    attr_bytes = bytes;
     // default carveout: the driver takes the smallest shared-memory split
     // that fits the table and leaves the rest of the SM's 256 KB as L1 for
     // the partner gathers and the texture fetches
@@ -1392,7 +1393,6 @@ void launch_force_lean(const KP& P, int mode, cudaStream_t s) {
                           (const void*)k_force_lean_smem<false, 896, TB, false>,
                           (const void*)k_force_lean_smem<false, 896, TB, true>})
       cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-    attr = true;
   }
   const int g = max(1, min(sm_count(), unit_count(P.G)));
   // at most 7 units per CTA (one wave, e.g. config 2): 7 groups of 128

@@ -334,6 +334,42 @@ def test_density_record_guard_local(cuda, tables, tmp_path, rho_k, compressed):
 
 
 @pytest.mark.parametrize("stencil", ["newton3", "full"])
+def test_force_window_gap(cuda, tables, stencil):
+    """The force table's shared-memory window skips a stretch of r between two
+    neighbour shells (capi.cu force_window_setup; BASELINE lattice: inside
+    2.855..4.04 A) and everything below the first shell's margin; pairs there
+    fetch their records by texture.  Atoms displaced by up to +-0.55 A per
+    component put pairs inside the gap, at both its edges and below the
+    window: rho, dF, forces and energies against the oracle"""
+    from oracle import oracle
+    ref = oracle.Sim(tables["baseline"], box=(8, 7, 6), temperature=0.0, seed=5)
+    n = 2 * 8 * 7 * 6
+    rng = np.random.default_rng(77)
+    ref.displace_interior(rng.uniform(-0.55, 0.55, size=(n, 3)))
+    ref.rehash()
+    dev = device_for(ref, tables["baseline"], stencil)
+    d = dev.describe()
+    lo, gap_lo, gap_n, cap = d["force_window"]
+    assert gap_lo > lo and gap_n > 0 and cap < 3300, d
+    # pairs inside the gap / below the window exist in this configuration
+    pot_h = 5.6 / 5000
+    s = ref.store()
+    m = real_mask(s)
+    x = s.pos[m]
+    _, a0, _g = ref.box
+    L = np.array([8, 7, 6]) * a0
+    dd = x[:, None, :] - x[None, :, :]
+    dd -= L * np.round(dd / L)
+    r = np.sqrt((dd ** 2).sum(-1))[np.triu_indices(len(x), 1)]
+    seg = np.floor((r - pot_h) / pot_h).astype(int)
+    assert ((seg >= gap_lo) & (seg < gap_lo + gap_n)).sum() > 100
+    assert ((seg < lo) & (seg >= 0)).sum() > 10
+    e_ref, e_dev = ref.eval_forces(), dev.eval_forces()
+    assert close(e_ref[0], e_dev[0]) and close(e_ref[1], e_dev[1]), (e_ref, e_dev)
+    assert_store_parity(ref.store(), dev.download(), what=f"window gap {stencil}")
+
+
+@pytest.mark.parametrize("stencil", ["newton3", "full"])
 def test_rows_of_whole_strips(cuda, tables, stencil):
     """Boxes whose rows hold whole 32-cell strips (bx % 32 == 0, as configs 4
     and 5) take the force pass's row accumulation of partner shares and the
