@@ -1605,6 +1605,16 @@ static cbx_status create_impl(const cbx_box* box, const cbx_potential* pot,
     P.uf = c->alloc<float4>(S);
     P.offs_const = ab_flag("CBX_OFFS_CONST", 1);
     P.unit_rr = ab_flag("CBX_UNIT_RR", 14);
+    {
+      // round-robin batches need several per CTA to balance: a small box
+      // (config 2: 1027 units, 7 per CTA) would leave half the CTAs without a
+      // batch, so it keeps one contiguous unit range per CTA
+      int sms = 148, dv = 0;
+      cudaGetDevice(&dv);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dv);
+      const long long nu = (long long)((G.bx * G.by + 31) / 32) * ((G.bz + 3) / 4);
+      if (P.unit_rr > 0 && nu < 2LL * P.unit_rr * sms) P.unit_rr = 0;
+    }
     P.idle_pred = ab_flag("CBX_IDLE_PRED", 1);
     P.skin_lane = ab_flag("CBX_SKIN_LANE", 1);
     P.tab_packed = ab_flag("CBX_TAB_PACKED", 1);
