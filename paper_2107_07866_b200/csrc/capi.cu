@@ -2621,11 +2621,11 @@ CBX_API cbx_status cbx_describe(cbx_ctx* c, char* buf, long n) {
                   "\"pair_mask\": %d, \"slots\": %lld, \"ghost_sites\": %d, "
                   "\"clash_capacity\": %d, \"band_A2\": %.3e, \"skin_prune\": %d, "
                   "\"kick_drift_bulk\": %d, \"force_window\": [%d, %d, %d, %d], "
-                  "\"sm_count\": %d}",
+                  "\"unit_rr\": %d, \"sm_count\": %d}",
                   c->mode, (int)c->fast_ok, (int)c->fp32_density, force_table_mode(),
                   (int)(c->P.pmask != nullptr), c->S, c->n_ghost, c->P.cap_clash, c->band,
                   (int)(c->P.ub != nullptr), (int)kd_bulk(c->P), c->P.fw_lo,
-                  c->P.fw_gap_n ? c->P.fw_gap_lo : -1, c->P.fw_gap_n, c->P.fw_cap,
+                  c->P.fw_gap_n ? c->P.fw_gap_lo : -1, c->P.fw_gap_n, c->P.fw_cap, c->P.unit_rr,
                   [] {
                     int d = 0, n = 0;
                     cudaGetDevice(&d);

@@ -333,6 +333,22 @@ def test_density_record_guard_local(cuda, tables, tmp_path, rho_k, compressed):
     assert_store_parity(ref.store(), dev.download(), what=f"rho_k={rho_k}")
 
 
+def test_unit_schedule_by_box_size(cuda, tables):
+    """Round-robin unit batches (14 units per batch, one batch per CTA and
+    round) need several rounds to balance; a box with fewer than two rounds of
+    units -- config 2's 50^3 has 1027 units for 148 CTAs -- keeps one contiguous
+    unit range per CTA (describe()["unit_rr"] == 0)"""
+    from paper_2107_07866_b200 import DeviceStore, EamPotential
+    pot = EamPotential.load(tables["baseline"])
+    small = DeviceStore((50, 50, 50, 2.855, 3), pot)
+    d = small.describe()
+    assert d["unit_rr"] == 0, d
+    big = DeviceStore((128, 128, 64, 2.855, 3), pot)
+    d = big.describe()
+    units = (128 * 128 // 32) * (64 // 4)
+    assert units >= 2 * 14 * d["sm_count"] and d["unit_rr"] == 14, d
+
+
 @pytest.mark.parametrize("stencil", ["newton3", "full"])
 def test_force_window_gap(cuda, tables, stencil):
     """The force table's shared-memory window skips a stretch of r between two
